@@ -1,0 +1,332 @@
+#!/usr/bin/env python3
+"""Benchmark: block-Toeplitz matvecs/s (+ GMRES time per iteration) on
+BASELINE.json's config 2 (32x32 array, m = 64, complex128, 1 RHS).
+
+One step = one application of the operator (K2 forward FFT passes -> K3
+bin-pair product -> K4 inverse passes -> edge/corner correction) to a
+device-resident vector. L2 is flushed between steps (untimed 256 MiB
+write), each step is bracketed by CUDA events on the launching stream.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference times the reference's CPU algorithm (the oracle
+restatement in oracle/, the reference itself cannot be built here: Eigen3
+is absent) with every host thread, one column per thread as the
+reference's parallelFor does (proj/src/linsolve.cpp:572).
+
+N > 1 (torchrun): every rank runs an independent replica of the workload
+(a frequency-sweep point per GPU), so scaling is "weak"; the timed region
+is bracketed by barriers and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+CONFIG = "C2"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def measured_hbm():
+    p = REPO / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+
+
+def workload_desc(cfg):
+    L0 = 1 << (2 * cfg.nx - 1 - 1).bit_length()
+    L1 = 1 << (2 * cfg.ny - 1 - 1).bit_length()
+    return (f"{cfg.name}: {cfg.nx}x{cfg.ny} array, m={cfg.m}, {cfg.nrhs} RHS, complex128, "
+            f"pow2 circulant embedding {L1}x{L0}, diag+rank-{cfg.rank} edge/corner corrections")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during measurement."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(rep, cfg, seconds=12.0, threads=1):
+    """Oracle port timed on host cores: returns (matvec/s, count, elapsed)."""
+    import numpy as np
+
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)  # spectra: one-time, untimed
+    t_pre = time.perf_counter() - t0
+    from paper_2506_04710_b200 import gen
+    X = np.asfortranarray(gen.rhs_normal(cfg.n, threads, 77))
+    o.apply_cols(X, nthreads=threads)  # warm
+    count, t0 = 0, time.perf_counter()
+    while True:
+        o.apply_cols(X, nthreads=threads)
+        count += threads
+        el = time.perf_counter() - t0
+        if el >= seconds and count >= 3:
+            break
+    return count / el, count, el, t_pre
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host CPU."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2506_04710_b200 import CONFIGS, ToeplitzRep
+    import numpy as np
+
+    import oracle
+    from paper_2506_04710_b200 import gen
+    cfg = CONFIGS[CONFIG]
+    cores = os.cpu_count() or 1
+    rep = ToeplitzRep.synthetic(cfg)
+    o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)
+    X = np.asfortranarray(gen.rhs_normal(cfg.n, cores, 5))
+    for _ in range(max(1, min(args.warmup, 3))):
+        o.apply_cols(X, nthreads=cores)
+    # Each step: one batch of `cores` independent matvecs (one column per thread);
+    # steps are bounded so the whole run stays within a few minutes.
+    steps = max(1, min(args.steps, 40))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.apply_cols(X, nthreads=cores)
+    el = time.perf_counter() - t0
+    value = steps * cores / el
+    sample = (f"{steps} steps x {cores} concurrent {cfg.name} matvecs (oracle/oracle.cpp restatement of "
+              f"applyA + correction, one column per thread as parallelFor, linsolve.cpp:572)")
+    line = {
+        "impl": "reference", "metric": f"block-Toeplitz matvecs/s ({cfg.name}, complex128)", "value": value,
+        "unit": "matvec/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded generator, include/tbt_gen.h)",
+        "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference C++ cannot be built here (Eigen3 absent, SURVEY.md 8(c)); oracle port timed instead",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--gmres-iters", type=int, default=200)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    from paper_2506_04710_b200 import CONFIGS, SolverOptions, ToeplitzMatvec, ToeplitzRep, gen, rhs_for
+    from paper_2506_04710_b200._lib import TBT_DEVICE
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = CONFIGS[CONFIG]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep, max_nrhs=1, device=local)
+    stream = torch.cuda.Stream()
+    op.set_stream(stream.cuda_stream)
+    info = op.info()
+
+    x_host = np.asarray(gen.rhs_normal(cfg.n, 1, 1000 + rank)[:, 0])
+    x = torch.from_numpy(x_host.copy()).to(f"cuda:{local}")
+    y = torch.empty_like(x)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    K, W = args.steps, args.warmup
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            op.apply_device(x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    with clocks:
+        # ---- value: K device-resident applies, L2 flushed (untimed) between steps
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        barrier()
+        with torch.cuda.stream(stream):
+            for k in range(K):
+                flush.fill_(float(k))
+                ev0[k].record(stream)
+                op.apply_device(x.data_ptr(), y.data_ptr())
+                ev1[k].record(stream)
+        stream.synchronize()
+        barrier()
+        step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+        total_ms = sum(step_ms)
+        if dist is not None:
+            t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+        value = world * K / (total_ms / 1e3)
+
+        # ---- roofline: K3 (bin-pair product) duration, events around each launch
+        op.set_timing(True)
+        with torch.cuda.stream(stream):
+            for k in range(K):
+                flush.fill_(float(k))
+                op.apply_device(x.data_ptr(), y.data_ptr())
+        k3_total, k3_count = op.timing_read()
+        op.set_timing(False)
+        k3_ms = k3_total / max(k3_count, 1)
+
+        # ---- e2e: C-ABI call with pinned HOST buffers (H2D + apply + D2H + sync per step)
+        xh = torch.from_numpy(x_host.copy()).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        import ctypes as C
+        from paper_2506_04710_b200._lib import TBT_HOST, lib
+        for _ in range(W):
+            lib().tbt_apply(op._h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()), 1, TBT_HOST)
+        barrier()
+        ke = max(10, K // 2)
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            st = lib().tbt_apply(op._h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()), 1, TBT_HOST)
+            assert st == 0
+        e2e_s = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = world * ke / e2e_s
+
+        # ---- GMRES: fixed budget (C2 stalls under GMRES(50)+Jacobi)
+        gm = None
+        if not args.no_gmres:
+            b = np.asarray(rhs_for(cfg))
+            bd = torch.from_numpy(b.copy()).to(f"cuda:{local}")
+            xd = torch.empty_like(bd)
+            opt = SolverOptions(tol=cfg.tol, maxIter=args.gmres_iters, restart=cfg.restart)
+            op.gmres(None, SolverOptions(tol=cfg.tol, maxIter=10, restart=cfg.restart), raise_on_fail=False,
+                     where=TBT_DEVICE, b_ptr=bd.data_ptr(), x_ptr=xd.data_ptr(), nrhs=1, hist_cap=64)
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            res = op.gmres(None, opt, raise_on_fail=False, where=TBT_DEVICE, b_ptr=bd.data_ptr(),
+                           x_ptr=xd.data_ptr(), nrhs=1, hist_cap=4 * args.gmres_iters)
+            g1.record(stream)
+            g1.synchronize()
+            gms = g0.elapsed_time(g1)
+            gm = {"config": cfg.name, "restart": cfg.restart, "iterations": res.iterations[0],
+                  "matvecs": res.matvecs, "ms_total": gms, "ms_per_iteration": gms / max(res.iterations[0], 1),
+                  "final_true_residual": res.residual[0], "converged": bool(res.converged[0]),
+                  "note": "fixed budget: the BASELINE generator stalls under GMRES(50)+Jacobi (SURVEY.md App. B)"}
+
+    peak, peak_src = measured_hbm()
+    mm = cfg.m * cfg.m * 16
+    k3_bytes = info.pairs * mm + 2 * info.bins * cfg.m * 16  # spectra once + xhat read + yhat write
+    achieved = k3_bytes / (k3_ms * 1e-3) / 1e9
+    step_mean = total_ms / K
+    b_alg_full = 16 * (info.bins * cfg.m * cfg.m + (2 * cfg.m * info.bins + 2 * cfg.n))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cnt, el, t_pre = cpu_sample(rep, cfg, seconds=12.0, threads=1)
+        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
+               "sample": f"{cnt} single-thread {cfg.name} matvecs in {el:.1f} s (oracle/oracle.cpp, reference "
+                         f"flags -O3; applyA is serial in the reference, linsolve.cpp:260-290); one-time spectra "
+                         f"precompute {t_pre:.2f} s excluded"}
+
+    line = {
+        "metric": f"block-Toeplitz matvecs/s ({cfg.name}, complex128)",
+        "value": value, "unit": "matvec/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": step_mean, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded generator, include/tbt_gen.h; paper geometries unavailable)",
+        "config": {"workload": workload_desc(cfg), "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "spectrum_storage": f"half (bin pairs): {info.pairs} blocks of {info.bins} bins"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "binprod (K3, bin-pair product)",
+                     "bytes_per_launch": k3_bytes, "ms_per_launch": k3_ms, "peak_source": peak_src},
+        "equivalent_full_spectrum_gbs": b_alg_full / (step_mean * 1e-3) / 1e9,
+        "e2e": {"value": e2e, "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16, "d2h_bytes_per_step": cfg.n * 16},
+        "gpu_launches": K * info.kernels_per_apply,
+        "clocks": clocks.summary(),
+        "gmres": gm,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

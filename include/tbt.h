@@ -1,0 +1,165 @@
+/*
+ * tbt.h - C ABI of the B200 multilevel block-Toeplitz matvec + GMRES
+ * (hot path of arXiv 2506.04710, reference "arraymom").
+ *
+ * Each entry point replaces a reference interface (paths relative to
+ * /root/reference/proj):
+ *   tbt_create / tbt_set_generators / tbt_precompute
+ *       ToeplitzMatvec::ToeplitzMatvec(rep, model)  include/arraymom/linsolve.hpp:61
+ *       -> Impl ctor + buildASpectra                  src/linsolve.cpp:160-216,239-258
+ *       (generators in the ToeplitzRep Sparse order   include/arraymom/toeplitz.hpp:72-74,
+ *        src/toeplitz.cpp:305-312)
+ *   tbt_set_correction
+ *       the non-Toeplitz edge/corner terms of Z^part (ToeplitzMatvec::apply's
+ *       B/B^T/C part, src/linsolve.cpp:384-386); here the BASELINE.json
+ *       nine-component diag+rank-r perturbation (include/tbt_gen.h)
+ *   tbt_apply        ToeplitzMatvec::apply        linsolve.hpp:64, linsolve.cpp:373-388
+ *   tbt_apply_a      ToeplitzMatvec::applyA       linsolve.hpp:65, linsolve.cpp:260-290
+ *   tbt_diagonal     ToeplitzMatvec::diagonal     linsolve.hpp:69, linsolve.cpp:390-408
+ *   tbt_size_a       ToeplitzMatvec::sizeA        linsolve.hpp:71
+ *   tbt_gmres        iterativeSolve / gmres       linsolve.hpp:88-89, linsolve.cpp:425-515,551-593
+ *                    (use_a_only = the schurSolve inner A-solve, linsolve.cpp:640-657)
+ *   tbt_status codes UserError (exit 1) / NumericError (exit 2),
+ *                    include/arraymom/common.hpp:38-50
+ *
+ * Conventions: complex values are interleaved (re, im) doubles, binary
+ * compatible with std::complex<double> (common.hpp:28). Vectors use the
+ * reference's unknown order, element-major / basis-minor:
+ * index (r*nx + c)*m + k (src/array_model.cpp:219-220,230-235). Several
+ * right-hand sides are stored column-major (n x nrhs), like Eigen's MatrixXc.
+ * One context is bound to one CUDA device and one stream; calls on a context
+ * are serialised by the caller (the reference's apply is const and
+ * re-entrant per thread; the batched nrhs entry points replace its
+ * per-column threads, linsolve.cpp:572).
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point returns TBT_CUDA_ERROR.
+ */
+#ifndef TBT_H
+#define TBT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TBT_OK = 0,
+  TBT_USER_ERROR = 1,    /* UserError: bad sizes, missing inputs, bad order */
+  TBT_NUMERIC_ERROR = 2, /* NumericError: GMRES did not converge */
+  TBT_CUDA_ERROR = 3     /* device failure / no device */
+} tbt_status;
+
+typedef enum { TBT_HOST = 0, TBT_DEVICE = 1 } tbt_where;
+
+typedef struct tbt_ctx tbt_ctx;
+
+typedef struct {
+  int nx, ny;    /* element grid (level 0 = x columns, level 1 = y rows)  */
+  int m;         /* basis functions per element (reference e5)            */
+  int max_nrhs;  /* largest nrhs later passed to apply/gmres (>= 1)        */
+  int device;    /* CUDA device ordinal                                    */
+  int flags;     /* reserved, 0                                            */
+} tbt_desc;
+
+typedef struct {
+  double tol;       /* relative residual target (reference default 1e-8)   */
+  int max_iter;     /* inner iterations per column (default 2000)          */
+  int restart;      /* GMRES(restart) (default 60)                         */
+  int precondition; /* left Jacobi (default 1, linsolve.hpp:51)            */
+  int use_a_only;   /* 1: operator = applyA (schurSolve's inner solves)    */
+  int hist_cap;     /* history entries kept per column (0 = none)          */
+} tbt_gmres_opts;
+
+typedef struct {
+  int* iterations;   /* [nrhs] inner iterations                            */
+  double* residual;  /* [nrhs] final true relative residual                */
+  int* converged;    /* [nrhs] 1 / 0                                       */
+  double* history;   /* [nrhs][hist_cap][2] (kind, value) pairs or NULL:
+                        kind 0 restart true residual, 1 |g_{j+1}|/beta,
+                        2 final true residual after max_iter               */
+  int* history_len;  /* [nrhs] entries produced (may exceed hist_cap)      */
+  int matvecs;       /* batched operator applications issued               */
+} tbt_gmres_stats;
+
+tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out);
+void tbt_destroy(tbt_ctx* ctx);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* tbt_last_error(void);
+
+/* Binds the context to an existing cudaStream_t (NULL = its own stream). */
+tbt_status tbt_set_stream(tbt_ctx* ctx, void* stream);
+void* tbt_get_stream(tbt_ctx* ctx);
+
+/* Canonical A generators, nx*ny + (nx-1)*(ny-1) blocks of m x m
+ * column-major complex, ToeplitzRep Sparse order (see above). Host memory. */
+tbt_status tbt_set_generators(tbt_ctx* ctx, const double* blocks,
+                              long long nblocks);
+
+/* 40 diag + rank-r terms (8 edge/corner components x 5 relations, layout of
+ * tbtgen_correction in tbt_gen.h). rank 0 with d = NULL clears. Host memory. */
+tbt_status tbt_set_correction(tbt_ctx* ctx, int rank, const double* d,
+                              const double* u, const double* v);
+
+/* Fourier-domain blocks in bin-pair-major layout (kernel K1); cached until
+ * destroy or the next set_generators. */
+tbt_status tbt_precompute(tbt_ctx* ctx);
+
+/* y = Z x (full synthetic operator) for nrhs columns. Device-resident
+ * single-column applies are replayed from a CUDA graph cached per
+ * (x, y) pointer pair. */
+tbt_status tbt_apply(tbt_ctx* ctx, const double* x, double* y, int nrhs,
+                     int where);
+/* y = A x (pure two-level block-Toeplitz part). */
+tbt_status tbt_apply_a(tbt_ctx* ctx, const double* x, double* y, int nrhs,
+                       int where);
+/* Diagonal of Z (length n, host memory). */
+tbt_status tbt_diagonal(tbt_ctx* ctx, double* d);
+long long tbt_size_a(const tbt_ctx* ctx);
+
+/* Restarted GMRES with x0 = 0 for nrhs columns in lockstep. b, x are
+ * n x nrhs column-major in `where` memory. Returns TBT_NUMERIC_ERROR when a
+ * column did not converge, with x, stats and the message still filled in. */
+tbt_status tbt_gmres(tbt_ctx* ctx, const double* b, double* x, int nrhs,
+                     const tbt_gmres_opts* opts, tbt_gmres_stats* stats,
+                     int where);
+
+/* Introspection for tests and the bench. */
+typedef struct {
+  long long n;          /* nx*ny*m                                        */
+  long long bins;       /* L = L1*L0                                      */
+  long long pairs;      /* stored Fourier blocks (bin pairs + self bins)  */
+  int L0, L1;
+  long long spectra_bytes;     /* device bytes of the stored blocks       */
+  int binprod_kernel;          /* K3 variant id                           */
+  int kernels_per_apply;       /* launches of one tbt_apply (nrhs = 1)    */
+  int has_antisym;             /* Z(0,0) not symmetric: block-diag fixup  */
+} tbt_info;
+tbt_status tbt_get_info(const tbt_ctx* ctx, tbt_info* info);
+
+/* Copies the stored Fourier block of bin f (m x m row-major: [a][b] =
+ * the reference's ahat[(a*m+b)*L + f], linsolve.cpp:147,256) to host. For a
+ * bin stored as the transposed partner the transpose is returned. */
+tbt_status tbt_get_spectrum_bin(tbt_ctx* ctx, long long f, double* out);
+
+/* Per-launch timing of the bin-product kernel (K3). While enabled, every
+ * apply records CUDA events around K3 on the context stream (and is not
+ * replayed from a CUDA graph); tbt_timing_read synchronises and returns the
+ * summed K3 milliseconds and the number of timed launches since enabling. */
+tbt_status tbt_set_timing(tbt_ctx* ctx, int on);
+tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
+
+/* Times `iters` back-to-back device-resident applies (nrhs columns) with
+ * CUDA events on the context stream; out_ms = mean ms per apply and
+ * out_binprod_ms = mean ms of the bin-product kernel (events around it). */
+tbt_status tbt_bench_apply(tbt_ctx* ctx, const double* x_dev, double* y_dev,
+                           int nrhs, int iters, int use_graph, double* out_ms,
+                           double* out_binprod_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TBT_H */

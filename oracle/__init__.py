@@ -1,0 +1,197 @@
+"""CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+ctypes binding of oracle/liboracle.so, a C++ restatement of the
+reference's matvec / GMRES (see oracle/oracle.h for the file:line map), and
+of oracle/_ref/libref_fft.so, the reference's own fftInPlace compiled from
+/root/reference/proj/src/fft.cpp. Only tests/, __graft_entry__.smoke() and
+bench.py's CPU legs may import this package, as the checker or the timed CPU
+baseline; the product path (paper_2506_04710_b200 / libtbt.so) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_FFT_SO = HERE / "_ref" / "libref_fft.so"
+
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int)
+_lib = None
+_ref = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not ORACLE_SO.exists():
+            raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle`")
+        L = C.CDLL(str(ORACLE_SO))
+        L.orc_next_pow2.restype = C.c_size_t
+        L.orc_next_pow2.argtypes = [C.c_size_t]
+        L.orc_fft.restype = C.c_int
+        L.orc_fft.argtypes = [dp, C.c_size_t, C.c_int]
+        L.orc_create.restype = C.c_void_p
+        L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, dp]
+        L.orc_destroy.restype = None
+        L.orc_destroy.argtypes = [C.c_void_p]
+        L.orc_precompute.argtypes = [C.c_void_p, C.c_int]
+        L.orc_ahat.argtypes = [C.c_void_p, dp]
+        L.orc_bins.restype = C.c_longlong
+        L.orc_bins.argtypes = [C.c_void_p]
+        L.orc_set_correction.argtypes = [C.c_void_p, C.c_int, dp, dp, dp]
+        L.orc_apply_a.argtypes = [C.c_void_p, dp, dp]
+        L.orc_apply.argtypes = [C.c_void_p, dp, dp]
+        L.orc_apply_cols.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_int, C.c_int]
+        L.orc_apply_rows.argtypes = [C.c_void_p, dp, C.POINTER(C.c_longlong), C.c_longlong, dp]
+        L.orc_dense.argtypes = [C.c_void_p, dp]
+        L.orc_diagonal.argtypes = [C.c_void_p, dp]
+        L.orc_gmres.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                C.c_int, C.c_int, ip, dp, ip, dp, C.c_int, ip]
+        _lib = L
+    return _lib
+
+
+def ref_lib() -> C.CDLL | None:
+    """The reference's own fft.cpp (None when oracle/_ref was not built)."""
+    global _ref
+    if _ref is None and REF_FFT_SO.exists():
+        L = C.CDLL(str(REF_FFT_SO))
+        L.ref_next_pow2.restype = C.c_size_t
+        L.ref_next_pow2.argtypes = [C.c_size_t]
+        L.ref_fft.restype = C.c_int
+        L.ref_fft.argtypes = [dp, C.c_size_t, C.c_int]
+        _ref = L
+    return _ref
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(dp)
+
+
+def fft(a: np.ndarray, inverse: bool = False) -> np.ndarray:
+    out = np.array(a, dtype=np.complex128, copy=True)
+    if lib().orc_fft(_p(out), out.size, 1 if inverse else 0):
+        raise ValueError("fftInPlace: length must be a power of two")
+    return out
+
+
+def ref_fft(a: np.ndarray, inverse: bool = False) -> np.ndarray:
+    out = np.array(a, dtype=np.complex128, copy=True)
+    if ref_lib().ref_fft(_p(out), out.size, 1 if inverse else 0):
+        raise ValueError("fftInPlace: length must be a power of two")
+    return out
+
+
+class Oracle:
+    """Restated ToeplitzMatvec + gmres over canonical Sparse generators."""
+
+    def __init__(self, nx, ny, m, generators_raw: np.ndarray, correction=None, precompute=True,
+                 nthreads: int = 0):
+        self.nx, self.ny, self.m = nx, ny, m
+        self.n = nx * ny * m
+        g = np.ascontiguousarray(generators_raw, dtype=np.complex128)
+        self._h = lib().orc_create(nx, ny, m, _p(g))
+        if not self._h:
+            raise ValueError("orc_create failed")
+        if correction is not None:
+            rank, d, u, v = correction
+            d = np.ascontiguousarray(d)
+            u = np.ascontiguousarray(u) if rank > 0 else np.zeros(1, np.complex128)
+            v = np.ascontiguousarray(v) if rank > 0 else np.zeros(1, np.complex128)
+            lib().orc_set_correction(self._h, rank, _p(d), _p(u), _p(v))
+        if precompute:
+            self.precompute(nthreads)
+
+    @classmethod
+    def from_rep(cls, rep, precompute=True, nthreads: int = 0):
+        corr = None
+        if rep.correction is not None:
+            c = rep.correction
+            corr = (c.rank, c.d, c.u, c.v)
+        return cls(rep.nx, rep.ny, rep.m, rep.generators, corr, precompute, nthreads)
+
+    def precompute(self, nthreads: int = 0):
+        lib().orc_precompute(self._h, nthreads)
+
+    def close(self):
+        if self._h:
+            lib().orc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def bins(self) -> int:
+        return int(lib().orc_bins(self._h))
+
+    def ahat(self) -> np.ndarray:
+        """Reference layout [(m*e5+n)*L + f] reshaped to (m, m, L)."""
+        out = np.empty((self.m, self.m, self.bins), dtype=np.complex128)
+        if lib().orc_ahat(self._h, _p(out)):
+            raise RuntimeError("no spectra")
+        return out
+
+    def _vec(self, fn, x):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.empty_like(x)
+        if fn(self._h, _p(x), _p(y)):
+            raise RuntimeError("oracle apply failed")
+        return y
+
+    def apply(self, x):
+        return self._vec(lib().orc_apply, x)
+
+    def applyA(self, x):
+        return self._vec(lib().orc_apply_a, x)
+
+    def apply_cols(self, X, nthreads=0, a_only=False):
+        X = np.asfortranarray(X, dtype=np.complex128)
+        Y = np.empty_like(X, order="F")
+        if lib().orc_apply_cols(self._h, _p(X), _p(Y), X.shape[1], nthreads, 1 if a_only else 0):
+            raise RuntimeError("orc_apply_cols failed")
+        return Y
+
+    def apply_rows(self, x, elems):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        el = np.ascontiguousarray(elems, dtype=np.int64)
+        y = np.empty((len(el), self.m), dtype=np.complex128)
+        if lib().orc_apply_rows(self._h, _p(x), el.ctypes.data_as(C.POINTER(C.c_longlong)), len(el), _p(y)):
+            raise RuntimeError("orc_apply_rows failed")
+        return y
+
+    def dense(self):
+        z = np.empty((self.n, self.n), dtype=np.complex128, order="F")
+        lib().orc_dense(self._h, _p(z))
+        return z
+
+    def diagonal(self):
+        d = np.empty(self.n, dtype=np.complex128)
+        lib().orc_diagonal(self._h, _p(d))
+        return d
+
+    def gmres(self, b, tol=1e-8, max_iter=2000, restart=60, precondition=True, use_a_only=False,
+              nthreads=1, hist_cap=4096):
+        b = np.asarray(b, dtype=np.complex128)
+        vec = b.ndim == 1
+        bc = np.asfortranarray(b[:, None] if vec else b)
+        k = bc.shape[1]
+        x = np.empty_like(bc, order="F")
+        its = np.zeros(k, np.int32)
+        res = np.zeros(k, np.float64)
+        conv = np.zeros(k, np.int32)
+        hist = np.zeros((k, hist_cap, 2), np.float64)
+        hlen = np.zeros(k, np.int32)
+        lib().orc_gmres(self._h, _p(bc), _p(x), k, tol, max_iter, restart, 1 if precondition else 0,
+                        1 if use_a_only else 0, nthreads, its.ctypes.data_as(ip), _p(res),
+                        conv.ctypes.data_as(ip), _p(hist), hist_cap, hlen.ctypes.data_as(ip))
+        hists = [hist[c, :min(int(hlen[c]), hist_cap)].copy() for c in range(k)]
+        return dict(x=x[:, 0] if vec else x, iterations=its.tolist(), residual=res.tolist(),
+                    converged=conv.tolist(), history=hists)

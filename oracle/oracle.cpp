@@ -1,0 +1,585 @@
+// CPU oracle: a restatement of the reference's multilevel block-Toeplitz
+// matvec and restarted GMRES (see oracle.h). TEST INFRASTRUCTURE ONLY.
+//
+// Built with the reference's flags (-std=c++20 -O3 -DNDEBUG, no fast-math;
+// proj/CMakeLists.txt:3,11-13,32) by oracle/Makefile.
+#include "oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <utility>
+#include <vector>
+
+using cplx = std::complex<double>;
+using cvec = std::vector<cplx>;
+
+namespace {
+
+// --- Foundation --------------------------------------------------------
+
+// parallelFor / resolveThreads (proj/src/mesh.cpp:27-59): static contiguous
+// split of [0, count) over std::threads; 0 means hardware concurrency.
+int threadsFor(int requested) {
+  if (requested > 0) return requested;
+  unsigned hc = std::thread::hardware_concurrency();
+  return hc ? static_cast<int>(hc) : 1;
+}
+
+template <typename Fn>
+void forkJoin(long count, int nthreads, Fn&& fn) {
+  nthreads = threadsFor(nthreads);
+  if (nthreads <= 1 || count <= 1) {
+    fn(0L, count);
+    return;
+  }
+  const long workers = std::min<long>(nthreads, count);
+  const long chunk = (count + workers - 1) / workers;
+  std::vector<std::thread> pool;
+  for (long w = 0; w < workers; ++w) {
+    const long lo = w * chunk, hi = std::min(count, lo + chunk);
+    if (lo < hi) pool.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  for (auto& t : pool) t.join();
+}
+
+// --- FFT (proj/src/fft.cpp) ---------------------------------------------
+
+size_t pow2AtLeast(size_t n) {  // fft.cpp:22-26
+  size_t p = 1;
+  while (p < n) p *= 2;
+  return p;
+}
+
+// fft.cpp:28-53: iterative radix-2 decimation in time. Bit-reversal
+// permutation first, then butterflies of growing span whose twiddle is
+// advanced by repeated multiplication with polar(1, sign*2*pi/len).
+// Forward sign is -1; the inverse is unscaled.
+bool radix2(cplx* a, size_t n, bool inverse) {
+  if (n == 0 || (n & (n - 1)) != 0) return false;
+  size_t rev = 0;
+  for (size_t k = 1; k < n; ++k) {
+    size_t mask = n >> 1;
+    while (rev & mask) {
+      rev ^= mask;
+      mask >>= 1;
+    }
+    rev ^= mask;
+    if (k < rev) std::swap(a[k], a[rev]);
+  }
+  const double sgn = inverse ? 1.0 : -1.0;
+  for (size_t span = 2; span <= n; span *= 2) {
+    const cplx step = std::polar(1.0, sgn * 2.0 * M_PI / static_cast<double>(span));
+    const size_t half = span / 2;
+    for (size_t base = 0; base < n; base += span) {
+      cplx tw{1.0, 0.0};
+      for (size_t q = 0; q < half; ++q) {
+        const cplx even = a[base + q];
+        const cplx odd = a[base + q + half] * tw;
+        a[base + q] = even + odd;
+        a[base + q + half] = even - odd;
+        tw *= step;
+      }
+    }
+  }
+  return true;
+}
+
+// Eigen conventions the reference relies on (linsolve.cpp:466, :429 ...):
+// a.dot(b) = sum conj(a_i) b_i, norm = sqrt(sum |v_i|^2).
+cplx cdot(const cvec& a, const cvec& b) {
+  cplx s{0.0, 0.0};
+  for (size_t i = 0; i < a.size(); ++i) s += std::conj(a[i]) * b[i];
+  return s;
+}
+double cnorm(const cvec& a) {
+  double s = 0.0;
+  for (const cplx& v : a) s += std::norm(v);
+  return std::sqrt(s);
+}
+
+const int kSlotOfComp[10] = {-1, 0, 1, 2, 3, -1, 4, 5, 6, 7};
+
+int componentOf(int nx, int ny, int r, int c) {  // include/tbt_gen.h
+  const bool left = c == 0, right = c == nx - 1;
+  const bool bottom = r == 0, top = r == ny - 1;
+  if (left && bottom) return 1;
+  if (left && top) return 3;
+  if (right && bottom) return 7;
+  if (right && top) return 9;
+  if (left) return 2;
+  if (right) return 8;
+  if (bottom) return 4;
+  if (top) return 6;
+  return 5;
+}
+
+}  // namespace
+
+struct orc_op {
+  int nx = 0, ny = 0, e5 = 0;
+  long nA = 0;
+  std::vector<cplx> gen;  // canonical blocks, column-major each
+  long L0 = 1, L1 = 1, L = 1;
+  std::vector<cplx> ahat;  // [(m*e5+n)*L + f], f = s1*L0 + s0
+  bool haveSpectra = false;
+
+  int rank = 0;
+  std::vector<cplx> pDense;  // 40 dense m x m perturbations, column-major
+
+  // Canonical block index of shift (i >= 0, j), reference storage order
+  // aGen[0][j] / aGen[i][j-(1-nx)] (toeplitz.hpp:72-74, toeplitz.cpp:305-312).
+  long blockIndex(int i, int j) const {
+    if (i == 0) return j;
+    return nx + static_cast<long>(i - 1) * (2 * nx - 1) + (j - (1 - nx));
+  }
+
+  // aEntry (linsolve.cpp:218-227), Sparse branch: negative half through the
+  // block symmetry A(-i,-j) = A(i,j)^T.
+  cplx aEntry(int i, int j, int m, int n) const {
+    if (i < 0 || (i == 0 && j < 0)) return aEntry(-i, -j, n, m);
+    const long t = blockIndex(i, j);
+    return gen[static_cast<size_t>(t) * e5 * e5 + static_cast<size_t>(n) * e5 + m];
+  }
+
+  // fft2 (linsolve.cpp:229-237): length-L0 transforms of the L1 rows, then
+  // length-L1 transforms of the L0 columns through a gathered copy.
+  void fft2(cplx* g, bool inverse) const {
+    for (long r = 0; r < L1; ++r) radix2(g + r * L0, static_cast<size_t>(L0), inverse);
+    cvec col(static_cast<size_t>(L1));
+    for (long c = 0; c < L0; ++c) {
+      for (long r = 0; r < L1; ++r) col[r] = g[r * L0 + c];
+      radix2(col.data(), static_cast<size_t>(L1), inverse);
+      for (long r = 0; r < L1; ++r) g[r * L0 + c] = col[r];
+    }
+  }
+
+  // buildASpectra (linsolve.cpp:239-258): each (m, n) entry sequence over
+  // the 2-D shifts is scattered to (i mod L1, j mod L0) and transformed.
+  void buildSpectra(int nthreads) {
+    ahat.assign(static_cast<size_t>(e5) * e5 * L, cplx{0.0, 0.0});
+    forkJoin(static_cast<long>(e5) * e5, nthreads, [&](long lo, long hi) {
+      cvec grid(static_cast<size_t>(L));
+      for (long mn = lo; mn < hi; ++mn) {
+        const int m = static_cast<int>(mn / e5), n = static_cast<int>(mn % e5);
+        std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+        for (int i = 1 - ny; i <= ny - 1; ++i)
+          for (int j = 1 - nx; j <= nx - 1; ++j) {
+            const long s1 = i >= 0 ? i : L1 + i;
+            const long s0 = j >= 0 ? j : L0 + j;
+            grid[s1 * L0 + s0] = aEntry(i, j, m, n);
+          }
+        fft2(grid.data(), false);
+        std::copy(grid.begin(), grid.end(), ahat.begin() + mn * L);
+      }
+    });
+    haveSpectra = true;
+  }
+
+  // applyA (linsolve.cpp:260-290).
+  void applyA(const cplx* x, cplx* y) const {
+    cvec xhat(static_cast<size_t>(e5) * L);
+    cvec grid(static_cast<size_t>(L));
+    for (int n = 0; n < e5; ++n) {
+      std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+      for (int r = 0; r < ny; ++r)
+        for (int c = 0; c < nx; ++c)
+          grid[static_cast<long>(r) * L0 + c] = x[(static_cast<long>(r) * nx + c) * e5 + n];
+      fft2(grid.data(), false);
+      std::copy(grid.begin(), grid.end(), xhat.begin() + static_cast<long>(n) * L);
+    }
+    const double scale = 1.0 / static_cast<double>(L);
+    for (int m = 0; m < e5; ++m) {
+      std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+      for (int n = 0; n < e5; ++n) {
+        const cplx* g = ahat.data() + (static_cast<size_t>(m) * e5 + n) * L;
+        const cplx* xr = xhat.data() + static_cast<size_t>(n) * L;
+        for (long f = 0; f < L; ++f) grid[f] += g[f] * xr[f];
+      }
+      fft2(grid.data(), true);
+      for (int r = 0; r < ny; ++r)
+        for (int c = 0; c < nx; ++c)
+          y[(static_cast<long>(r) * nx + c) * e5 + m] = grid[static_cast<long>(r) * L0 + c] * scale;
+    }
+  }
+
+  // Synthetic nine-component correction (tbt_gen.h): for every element e
+  // of a non-interior component and every relation with an in-array
+  // neighbour e', y_e += P x_e' and y_e' += P^T x_e.
+  template <typename Visit>
+  void forEachCorrection(Visit&& visit) const {
+    if (pDense.empty()) return;
+    static const int dr[5] = {0, 0, 0, 1, -1};
+    static const int dc[5] = {0, 1, -1, 0, 0};
+    for (int r = 0; r < ny; ++r)
+      for (int c = 0; c < nx; ++c) {
+        const int comp = componentOf(nx, ny, r, c);
+        if (comp == 5) continue;
+        for (int rel = 0; rel < 5; ++rel) {
+          const int r2 = r + dr[rel], c2 = c + dc[rel];
+          if (r2 < 0 || r2 >= ny || c2 < 0 || c2 >= nx) continue;
+          const cplx* P = pDense.data() + static_cast<size_t>(kSlotOfComp[comp] * 5 + rel) * e5 * e5;
+          visit(static_cast<long>(r) * nx + c, static_cast<long>(r2) * nx + c2, P);
+        }
+      }
+  }
+
+  void addCorrection(const cplx* x, cplx* y) const {
+    forEachCorrection([&](long e, long e2, const cplx* P) {
+      for (int a = 0; a < e5; ++a) {
+        cplx s1{0.0, 0.0}, s2{0.0, 0.0};
+        for (int b = 0; b < e5; ++b) {
+          s1 += P[static_cast<size_t>(b) * e5 + a] * x[e2 * e5 + b];  // (P x_e')_a
+          s2 += P[static_cast<size_t>(a) * e5 + b] * x[e * e5 + b];   // (P^T x_e)_a
+        }
+        y[e * e5 + a] += s1;
+        y[e2 * e5 + a] += s2;
+      }
+    });
+  }
+
+  void apply(const cplx* x, cplx* y) const {
+    applyA(x, y);
+    addCorrection(x, y);
+  }
+
+  // Z(e, e') block entry (a, b) from the generators (partBlock Sparse
+  // branch, toeplitz.cpp:436-447): shift = target - source.
+  cplx zEntry(long e, long e2, int a, int b) const {
+    const int r = static_cast<int>(e / nx), c = static_cast<int>(e % nx);
+    const int r2 = static_cast<int>(e2 / nx), c2 = static_cast<int>(e2 % nx);
+    return aEntry(r - r2, c - c2, a, b);
+  }
+};
+
+extern "C" {
+
+size_t orc_next_pow2(size_t n) { return pow2AtLeast(n); }
+
+int orc_fft(double* a, size_t n, int inverse) {
+  return radix2(reinterpret_cast<cplx*>(a), n, inverse != 0) ? 0 : 1;
+}
+
+orc_op* orc_create(int nx, int ny, int m, const double* blocks) {
+  if (nx < 1 || ny < 1 || m < 1 || blocks == nullptr) return nullptr;
+  auto* op = new orc_op;
+  op->nx = nx;
+  op->ny = ny;
+  op->e5 = m;
+  op->nA = static_cast<long>(nx) * ny * m;
+  const size_t nb = static_cast<size_t>(nx) * ny + static_cast<size_t>(nx - 1) * (ny - 1);
+  op->gen.resize(nb * m * m);
+  std::memcpy(static_cast<void*>(op->gen.data()), blocks, nb * m * m * sizeof(cplx));
+  op->L1 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * ny - 1)));
+  op->L0 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * nx - 1)));
+  op->L = op->L1 * op->L0;
+  return op;
+}
+
+void orc_destroy(orc_op* op) { delete op; }
+
+int orc_precompute(orc_op* op, int nthreads) {
+  if (!op) return 1;
+  op->buildSpectra(nthreads);
+  return 0;
+}
+
+long long orc_bins(const orc_op* op) { return op ? op->L : 0; }
+
+int orc_ahat(const orc_op* op, double* out) {
+  if (!op || !op->haveSpectra) return 1;
+  std::memcpy(out, op->ahat.data(), op->ahat.size() * sizeof(cplx));
+  return 0;
+}
+
+int orc_set_correction(orc_op* op, int rank, const double* d, const double* u,
+                       const double* v) {
+  if (!op || rank < 0 || !d) return 1;
+  const int m = op->e5;
+  op->rank = rank;
+  op->pDense.assign(static_cast<size_t>(40) * m * m, cplx{0.0, 0.0});
+  const cplx* D = reinterpret_cast<const cplx*>(d);
+  const cplx* U = reinterpret_cast<const cplx*>(u);
+  const cplx* V = reinterpret_cast<const cplx*>(v);
+  for (int s = 0; s < 40; ++s) {
+    cplx* P = op->pDense.data() + static_cast<size_t>(s) * m * m;
+    for (int b = 0; b < m; ++b)
+      for (int a = 0; a < m; ++a) {
+        cplx acc = (a == b) ? D[static_cast<size_t>(s) * m + a] : cplx{0.0, 0.0};
+        for (int q = 0; q < rank; ++q)
+          acc += U[(static_cast<size_t>(s) * rank + q) * m + a] *
+                 V[(static_cast<size_t>(s) * rank + q) * m + b];
+        P[static_cast<size_t>(b) * m + a] = acc;
+      }
+  }
+  return 0;
+}
+
+int orc_apply_a(const orc_op* op, const double* x, double* y) {
+  if (!op || !op->haveSpectra) return 1;
+  op->applyA(reinterpret_cast<const cplx*>(x), reinterpret_cast<cplx*>(y));
+  return 0;
+}
+
+int orc_apply(const orc_op* op, const double* x, double* y) {
+  if (!op || !op->haveSpectra) return 1;
+  op->apply(reinterpret_cast<const cplx*>(x), reinterpret_cast<cplx*>(y));
+  return 0;
+}
+
+int orc_apply_cols(const orc_op* op, const double* x, double* y, int ncols,
+                   int nthreads, int a_only) {
+  if (!op || !op->haveSpectra || ncols < 0) return 1;
+  const cplx* X = reinterpret_cast<const cplx*>(x);
+  cplx* Y = reinterpret_cast<cplx*>(y);
+  forkJoin(ncols, nthreads, [&](long lo, long hi) {
+    for (long c = lo; c < hi; ++c) {
+      if (a_only)
+        op->applyA(X + c * op->nA, Y + c * op->nA);
+      else
+        op->apply(X + c * op->nA, Y + c * op->nA);
+    }
+  });
+  return 0;
+}
+
+int orc_apply_rows(const orc_op* op, const double* xd, const long long* elems,
+                   long long count, double* yd) {
+  if (!op) return 1;
+  const cplx* x = reinterpret_cast<const cplx*>(xd);
+  cplx* y = reinterpret_cast<cplx*>(yd);
+  const int m = op->e5;
+  const long ne = static_cast<long>(op->nx) * op->ny;
+  for (long long k = 0; k < count; ++k) {
+    const long e = static_cast<long>(elems[k]);
+    if (e < 0 || e >= ne) return 1;
+    cplx* out = y + k * m;
+    for (int a = 0; a < m; ++a) out[a] = cplx{0.0, 0.0};
+    for (long e2 = 0; e2 < ne; ++e2)
+      for (int b = 0; b < m; ++b) {
+        const cplx xv = x[e2 * m + b];
+        for (int a = 0; a < m; ++a) out[a] += op->zEntry(e, e2, a, b) * xv;
+      }
+    op->forEachCorrection([&](long ea, long eb, const cplx* P) {
+      if (ea == e)
+        for (int a = 0; a < m; ++a)
+          for (int b = 0; b < m; ++b) out[a] += P[static_cast<size_t>(b) * m + a] * x[eb * m + b];
+      if (eb == e)
+        for (int a = 0; a < m; ++a)
+          for (int b = 0; b < m; ++b) out[a] += P[static_cast<size_t>(a) * m + b] * x[ea * m + b];
+    });
+  }
+  return 0;
+}
+
+int orc_dense(const orc_op* op, double* zd) {
+  if (!op) return 1;
+  const int m = op->e5;
+  const long ne = static_cast<long>(op->nx) * op->ny;
+  const long N = ne * m;
+  cplx* z = reinterpret_cast<cplx*>(zd);
+  for (long e = 0; e < ne; ++e)
+    for (long e2 = 0; e2 < ne; ++e2)
+      for (int b = 0; b < m; ++b)
+        for (int a = 0; a < m; ++a)
+          z[(e2 * m + b) * N + e * m + a] = op->zEntry(e, e2, a, b);
+  op->forEachCorrection([&](long e, long e2, const cplx* P) {
+    for (int b = 0; b < m; ++b)
+      for (int a = 0; a < m; ++a) {
+        z[(e2 * m + b) * N + e * m + a] += P[static_cast<size_t>(b) * m + a];
+        z[(e * m + b) * N + e2 * m + a] += P[static_cast<size_t>(a) * m + b];
+      }
+  });
+  return 0;
+}
+
+int orc_diagonal(const orc_op* op, double* dd) {
+  if (!op) return 1;
+  const int m = op->e5;
+  const long ne = static_cast<long>(op->nx) * op->ny;
+  cplx* d = reinterpret_cast<cplx*>(dd);
+  // ToeplitzMatvec::diagonal (linsolve.cpp:397-399): aEntry(0,0,m,m).
+  for (long p = 0; p < ne; ++p)
+    for (int a = 0; a < m; ++a) d[p * m + a] = op->aEntry(0, 0, a, a);
+  op->forEachCorrection([&](long e, long e2, const cplx* P) {
+    if (e != e2) return;
+    for (int a = 0; a < m; ++a) d[e * m + a] += 2.0 * P[static_cast<size_t>(a) * m + a];
+  });
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Outcome {
+  int iterations = 0;
+  double residual = 0.0;
+  bool converged = false;
+};
+
+struct History {
+  double* buf;
+  int cap;
+  int len = 0;
+  void push(double kind, double v) {
+    if (buf && len < cap) {
+      buf[2 * len] = kind;
+      buf[2 * len + 1] = v;
+    }
+    ++len;
+  }
+};
+
+// gmres (linsolve.cpp:425-515): restarted GMRES(restart), x0 = 0, left
+// Jacobi, modified Gram-Schmidt with the conjugated inner product, complex
+// Givens rotations, inner exit at |g_{j+1}|/beta < 0.1 tol, lucky breakdown,
+// back substitution; maxIter counts inner iterations.
+template <typename Op>
+Outcome gmresColumn(const Op& op, const cvec& b, cvec& x, const cvec* invDiag,
+                    double tol, int maxIter, int restart, History& hist) {
+  const size_t n = b.size();
+  const double bnorm = cnorm(b);
+  Outcome out;
+  x.assign(n, cplx{0.0, 0.0});
+  if (bnorm == 0.0) {
+    out.converged = true;
+    return out;
+  }
+  auto precond = [&](cvec& v) {
+    if (!invDiag) return;
+    for (size_t k = 0; k < n; ++k) v[k] *= (*invDiag)[k];
+  };
+
+  std::vector<cvec> basis;
+  std::vector<cplx> h(static_cast<size_t>(restart + 1) * restart);
+  auto H = [&](int i, int j) -> cplx& { return h[static_cast<size_t>(j) * (restart + 1) + i]; };
+  std::vector<cplx> cs(restart), sn(restart), g(restart + 1);
+  cvec ax(n), w(n);
+
+  while (out.iterations < maxIter) {
+    op(x, ax);
+    cvec r(n);
+    for (size_t k = 0; k < n; ++k) r[k] = b[k] - ax[k];
+    out.residual = cnorm(r) / bnorm;
+    hist.push(0.0, out.residual);
+    if (out.residual < tol) {
+      out.converged = true;
+      return out;
+    }
+    precond(r);
+    const double beta = cnorm(r);
+    if (beta == 0.0) {
+      out.converged = true;
+      return out;
+    }
+    basis.assign(1, r);
+    for (auto& v : basis[0]) v /= beta;
+    std::fill(g.begin(), g.end(), cplx{0.0, 0.0});
+    std::fill(h.begin(), h.end(), cplx{0.0, 0.0});
+    g[0] = beta;
+    int j = 0;
+    for (; j < restart && out.iterations < maxIter; ++j, ++out.iterations) {
+      op(basis[j], w);
+      precond(w);
+      for (int i = 0; i <= j; ++i) {
+        H(i, j) = cdot(basis[i], w);
+        const cplx hij = H(i, j);
+        for (size_t k = 0; k < n; ++k) w[k] -= hij * basis[i][k];
+      }
+      H(j + 1, j) = cnorm(w);
+      if (std::abs(H(j + 1, j)) > 0.0) {
+        const cplx hn = H(j + 1, j);
+        cvec v(n);
+        for (size_t k = 0; k < n; ++k) v[k] = w[k] / hn;
+        basis.push_back(std::move(v));
+      }
+      for (int i = 0; i < j; ++i) {
+        const cplx t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
+        H(i + 1, j) = -std::conj(sn[i]) * H(i, j) + std::conj(cs[i]) * H(i + 1, j);
+        H(i, j) = t;
+      }
+      const double den = std::sqrt(std::norm(H(j, j)) + std::norm(H(j + 1, j)));
+      if (den == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = std::conj(H(j, j)) / den;
+        sn[j] = std::conj(H(j + 1, j)) / den;
+      }
+      H(j, j) = cs[j] * H(j, j) + sn[j] * H(j + 1, j);
+      H(j + 1, j) = 0.0;
+      const cplx gj = g[j];
+      g[j] = cs[j] * gj;
+      g[j + 1] = -std::conj(sn[j]) * gj;
+      hist.push(1.0, std::abs(g[j + 1]) / beta);
+      if (std::abs(g[j + 1]) / beta < 0.1 * tol) {
+        ++j;
+        ++out.iterations;
+        break;
+      }
+      if (basis.size() == static_cast<size_t>(j) + 1) {
+        ++j;
+        ++out.iterations;
+        break;
+      }
+    }
+    std::vector<cplx> yv(j);
+    for (int i = j - 1; i >= 0; --i) {
+      cplx s = g[i];
+      for (int k2 = i + 1; k2 < j; ++k2) s -= H(i, k2) * yv[k2];
+      yv[i] = s / H(i, i);
+    }
+    for (int i = 0; i < j; ++i)
+      for (size_t k = 0; k < n; ++k) x[k] += yv[i] * basis[i][k];
+  }
+  // maxIter exhausted: final true residual (linsolve.cpp:512-513).
+  op(x, ax);
+  cvec r(n);
+  for (size_t k = 0; k < n; ++k) r[k] = b[k] - ax[k];
+  out.residual = cnorm(r) / bnorm;
+  out.converged = out.residual < tol;
+  hist.push(2.0, out.residual);
+  return out;
+}
+
+}  // namespace
+
+extern "C" int orc_gmres(const orc_op* op, const double* b, double* x,
+                         int ncols, double tol, int max_iter, int restart,
+                         int precondition, int use_a_only, int nthreads,
+                         int* iterations, double* residual, int* converged,
+                         double* hist, int hist_cap, int* hist_len) {
+  if (!op || !op->haveSpectra || ncols < 0 || restart < 1) return 1;
+  const long n = op->nA;
+  cvec invDiag;
+  if (precondition) {
+    // iterativeSolve (linsolve.cpp:556-563): 1/d, or 1 where d == 0.
+    invDiag.resize(n);
+    orc_diagonal(op, reinterpret_cast<double*>(invDiag.data()));
+    if (use_a_only)
+      for (long p = 0; p < n; ++p) invDiag[p] = op->aEntry(0, 0, static_cast<int>(p % op->e5), static_cast<int>(p % op->e5));
+    for (auto& d : invDiag) d = (std::abs(d) > 0.0) ? 1.0 / d : cplx{1.0, 0.0};
+  }
+  auto opFull = [op](const cvec& in, cvec& out) { op->apply(in.data(), out.data()); };
+  auto opA = [op](const cvec& in, cvec& out) { op->applyA(in.data(), out.data()); };
+  forkJoin(ncols, nthreads, [&](long lo, long hi) {
+    for (long c = lo; c < hi; ++c) {
+      cvec bc(reinterpret_cast<const cplx*>(b) + c * n, reinterpret_cast<const cplx*>(b) + (c + 1) * n);
+      cvec xc;
+      History h{hist ? hist + 2L * hist_cap * c : nullptr, hist_cap};
+      const Outcome o = use_a_only
+                            ? gmresColumn(opA, bc, xc, precondition ? &invDiag : nullptr, tol, max_iter, restart, h)
+                            : gmresColumn(opFull, bc, xc, precondition ? &invDiag : nullptr, tol, max_iter, restart, h);
+      std::memcpy(x + 2 * c * n, xc.data(), n * sizeof(cplx));
+      if (iterations) iterations[c] = o.iterations;
+      if (residual) residual[c] = o.residual;
+      if (converged) converged[c] = o.converged ? 1 : 0;
+      if (hist_len) hist_len[c] = h.len;
+    }
+  });
+  return 0;
+}

@@ -1,0 +1,622 @@
+// C ABI (include/tbt.h): context lifecycle, input staging, apply / solve
+// entry points. Host-side C++; all arithmetic runs in the kernels of
+// fft.cu / spectra.cu / binprod.cu / correction.cu / gmres.cu.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tbt_internal.cuh"
+
+namespace tbt {
+
+
+namespace {
+thread_local std::string gLastError;
+const int kSlotOfComp[10] = {-1, 0, 1, 2, 3, -1, 4, 5, 6, 7};
+
+int componentOf(int nx, int ny, int r, int c) {  // include/tbt_gen.h
+  const bool left = c == 0, right = c == nx - 1;
+  const bool bottom = r == 0, top = r == ny - 1;
+  if (left && bottom) return 1;
+  if (left && top) return 3;
+  if (right && bottom) return 7;
+  if (right && top) return 9;
+  if (left) return 2;
+  if (right) return 8;
+  if (bottom) return 4;
+  if (top) return 6;
+  return 5;
+}
+
+int pow2AtLeast(int n) {  // nextPow2, proj/src/fft.cpp:22-26
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+template <typename Fn>
+tbt_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return TBT_OK;
+  } catch (const Error& e) {
+    gLastError = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    gLastError = e.what();
+    return TBT_CUDA_ERROR;
+  }
+}
+
+void freePtr(void* p) {
+  if (p) cudaFree(p);
+}
+
+std::vector<double2> twiddles(int n) {
+  std::vector<double2> t(n);
+  for (int k = 0; k < n; ++k) {
+    const long double ang = -2.0L * 3.141592653589793238462643383279502884L * k / n;
+    t[k] = make_double2(static_cast<double>(cosl(ang)), static_cast<double>(sinl(ang)));
+  }
+  return t;
+}
+
+// Inverse diagonal on the host (iterativeSolve, linsolve.cpp:556-563).
+void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
+  const int m = c.m;
+  std::vector<double2> d(static_cast<size_t>(c.n));
+  const double2* z0 = c.genHost.data();  // block (0,0), column-major
+  for (int e = 0; e < c.ne; ++e)
+    for (int a = 0; a < m; ++a) d[static_cast<size_t>(e) * m + a] = z0[static_cast<size_t>(a) * m + a];
+  if (c.haveCorr) {
+    // Self relation contributes P + P^T, diagonal 2 (d_a + sum_q U_aq V_aq).
+    std::vector<double2> hu(static_cast<size_t>(40) * c.rank * m), hv(hu.size());
+    if (c.rank > 0) {
+      TBT_CUDA_CHECK(cudaMemcpy(hu.data(), c.dCorrU, hu.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+      TBT_CUDA_CHECK(cudaMemcpy(hv.data(), c.dCorrV, hv.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    }
+    for (int r = 0; r < c.ny; ++r)
+      for (int col = 0; col < c.nx; ++col) {
+        const int comp = componentOf(c.nx, c.ny, r, col);
+        if (comp == 5) continue;
+        const int slot = kSlotOfComp[comp] * 5;
+        const int e = r * c.nx + col;
+        for (int a = 0; a < m; ++a) {
+          double2 p = c.corrDHost[static_cast<size_t>(slot) * m + a];
+          for (int q = 0; q < c.rank; ++q) {
+            const double2 u = hu[(static_cast<size_t>(slot) * c.rank + q) * m + a];
+            const double2 v = hv[(static_cast<size_t>(slot) * c.rank + q) * m + a];
+            p = cadd(p, cmul(u, v));
+          }
+          double2& dd = d[static_cast<size_t>(e) * m + a];
+          dd = cadd(dd, make_double2(2.0 * p.x, 2.0 * p.y));
+        }
+      }
+  }
+  if (dOut) *dOut = d;
+  std::vector<double2> inv(d.size());
+  for (size_t k = 0; k < d.size(); ++k) {
+    const double2 v = d[k];
+    if (std::hypot(v.x, v.y) > 0.0) {
+      // 1 / (a + bi) with Smith scaling.
+      double2 r;
+      if (std::fabs(v.x) >= std::fabs(v.y)) {
+        const double t = v.y / v.x, den = v.x + v.y * t;
+        r = make_double2(1.0 / den, -t / den);
+      } else {
+        const double t = v.x / v.y, den = v.x * t + v.y;
+        r = make_double2(t / den, -1.0 / den);
+      }
+      inv[k] = r;
+    } else {
+      inv[k] = make_double2(1.0, 0.0);
+    }
+  }
+  if (!c.dDiagInv) TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInv, c.n * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInv, inv.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+void requireReady(const Ctx& c) {
+  TBT_USER_CHECK(c.havePrecompute, "tbt: call tbt_precompute before apply/solve");
+}
+
+// One single-column apply, replayed from the cached CUDA graph unless K3
+// timing is on.
+void runApply1(Ctx& c, const double2* x, double2* y, bool withCorr) {
+  if (c.timeBinprod) {
+    applyInternal(c, x, y, 1, withCorr);
+    return;
+  }
+  if (!c.graphExec || c.graphX != x || c.graphY != y || c.graphCorr != withCorr) {
+    c.dropGraph();
+    cudaGraph_t graph;
+    TBT_CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      applyInternal(c, x, y, 1, withCorr);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &graph);
+      throw;
+    }
+    TBT_CUDA_CHECK(cudaStreamEndCapture(c.stream, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&c.graphExec, graph, 0);
+    cudaGraphDestroy(graph);
+    TBT_CUDA_CHECK(e);
+    c.graphX = x;
+    c.graphY = y;
+    c.graphCorr = withCorr;
+  }
+  TBT_CUDA_CHECK(cudaGraphLaunch(c.graphExec, c.stream));
+}
+
+}  // namespace
+
+int smCount(int device) {
+  static int cached[64] = {0};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  int v = 0;
+  TBT_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  if (device >= 0 && device < 64) cached[device] = v;
+  return v;
+}
+
+void setError(const std::string& msg) { gLastError = msg; }
+
+}  // namespace tbt
+
+using namespace tbt;
+
+struct tbt_ctx {
+  Ctx c;
+};
+
+extern "C" {
+
+const char* tbt_last_error(void) { return gLastError.c_str(); }
+
+tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
+  return guarded([&] {
+    TBT_USER_CHECK(desc && out, "tbt_create: null argument");
+    TBT_USER_CHECK(desc->nx >= 1 && desc->ny >= 1 && desc->m >= 1, "tbt_create: nx, ny, m must be >= 1");
+    TBT_USER_CHECK(desc->max_nrhs >= 1, "tbt_create: max_nrhs must be >= 1");
+    *out = nullptr;
+    int ndev = 0;
+    TBT_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    TBT_USER_CHECK(desc->device >= 0 && desc->device < ndev, "tbt_create: no such CUDA device");
+    cudaDeviceProp prop;
+    TBT_CUDA_CHECK(cudaGetDeviceProperties(&prop, desc->device));
+    if (prop.major != 10) throw Error{TBT_CUDA_ERROR, "tbt_create: built for sm_100a (B200), device is sm_" +
+                                                          std::to_string(prop.major * 10 + prop.minor)};
+    TBT_CUDA_CHECK(cudaSetDevice(desc->device));
+    auto* h = new tbt_ctx;
+    Ctx& c = h->c;
+    c.nx = desc->nx;
+    c.ny = desc->ny;
+    c.m = desc->m;
+    c.ne = c.nx * c.ny;
+    c.n = static_cast<long long>(c.ne) * c.m;
+    c.maxNrhs = desc->max_nrhs;
+    c.device = desc->device;
+    c.L1 = pow2AtLeast(2 * c.ny - 1);  // linsolve.cpp:240-242
+    c.L0 = pow2AtLeast(2 * c.nx - 1);
+    c.L = static_cast<long long>(c.L0) * c.L1;
+    try {
+      TBT_USER_CHECK(c.L0 <= 256 && c.L1 <= 256, "tbt_create: embedding length above 256 (nx, ny <= 128)");
+      TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.ownStream = true;
+      const long long B = static_cast<long long>(c.maxNrhs) * c.m;
+      TBT_CUDA_CHECK(cudaMalloc(&c.dT, static_cast<long long>(c.ny) * c.L0 * B * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dXhat, c.L * B * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dYhat, c.L * B * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dXin, c.ne * B * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dYout, c.ne * B * sizeof(double2)));
+      const auto t0 = twiddles(c.L0), t1 = twiddles(c.L1);
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTw0, c.L0 * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTw1, c.L1 * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dTw0, t0.data(), c.L0 * sizeof(double2), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dTw1, t1.data(), c.L1 * sizeof(double2), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
+      TBT_CUDA_CHECK(cudaEventCreate(&c.evBinB));
+      c.binprodKernel = binprodVariant(c.m);
+    } catch (...) {
+      tbt_destroy(h);
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void tbt_destroy(tbt_ctx* h) {
+  if (!h) return;
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  for (void* p : {static_cast<void*>(c.dSpectra), static_cast<void*>(c.dPairF), static_cast<void*>(c.dPairG),
+                  static_cast<void*>(c.dAntisym), static_cast<void*>(c.dTw0), static_cast<void*>(c.dTw1),
+                  static_cast<void*>(c.dCorrD), static_cast<void*>(c.dCorrU), static_cast<void*>(c.dCorrV),
+                  static_cast<void*>(c.dTermInfo), static_cast<void*>(c.dTargetList),
+                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dT),
+                  static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
+                  static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv)})
+    freePtr(p);
+  c.dropGraph();
+  for (auto e : c.tEvA) cudaEventDestroy(e);
+  for (auto e : c.tEvB) cudaEventDestroy(e);
+  if (c.evBinA) cudaEventDestroy(c.evBinA);
+  if (c.evBinB) cudaEventDestroy(c.evBinB);
+  if (c.ownStream && c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+}
+
+tbt_status tbt_set_stream(tbt_ctx* h, void* stream) {
+  return guarded([&] {
+    TBT_USER_CHECK(h, "tbt_set_stream: null context");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (c.ownStream) {
+      TBT_CUDA_CHECK(cudaStreamDestroy(c.stream));
+      c.ownStream = false;
+      c.stream = nullptr;
+    }
+    if (stream) {
+      c.stream = static_cast<cudaStream_t>(stream);
+    } else {
+      TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.ownStream = true;
+    }
+  });
+}
+
+void* tbt_get_stream(tbt_ctx* h) { return h ? static_cast<void*>(h->c.stream) : nullptr; }
+
+long long tbt_size_a(const tbt_ctx* h) { return h ? h->c.n : 0; }
+
+tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblocks) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && blocks, "tbt_set_generators: null argument");
+    Ctx& c = h->c;
+    const long long want = static_cast<long long>(c.nx) * c.ny + static_cast<long long>(c.nx - 1) * (c.ny - 1);
+    TBT_USER_CHECK(nblocks == want, "tbt_set_generators: expected " + std::to_string(want) +
+                                        " canonical blocks (nx*ny + (nx-1)*(ny-1)), got " +
+                                        std::to_string(nblocks));
+    const size_t cnt = static_cast<size_t>(want) * c.m * c.m;
+    c.genHost.resize(cnt);
+    std::memcpy(static_cast<void*>(c.genHost.data()), blocks, cnt * sizeof(double2));
+    c.haveGenerators = true;
+    c.havePrecompute = false;
+  });
+}
+
+tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const double* u, const double* v) {
+  return guarded([&] {
+    TBT_USER_CHECK(h, "tbt_set_correction: null context");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(rank >= 0, "tbt_set_correction: rank must be >= 0");
+    freePtr(c.dCorrD);
+    freePtr(c.dCorrU);
+    freePtr(c.dCorrV);
+    freePtr(c.dTermInfo);
+    freePtr(c.dTargetList);
+    freePtr(c.dTargetPtr);
+    freePtr(c.dProj);
+    c.dCorrD = c.dCorrU = c.dCorrV = c.dProj = nullptr;
+    c.dTermInfo = c.dTargetList = c.dTargetPtr = nullptr;
+    c.haveCorr = false;
+    c.nTerms = c.nTargets = 0;
+    c.dropGraph();
+    if (d == nullptr) {
+      if (c.havePrecompute) refreshDiagonal(c, nullptr);
+      return;
+    }
+    TBT_USER_CHECK(rank == 0 || (u && v), "tbt_set_correction: rank > 0 needs U and V");
+    const int m = c.m;
+    c.rank = rank;
+    c.corrDHost.assign(reinterpret_cast<const double2*>(d), reinterpret_cast<const double2*>(d) + 40 * m);
+    TBT_CUDA_CHECK(cudaMalloc(&c.dCorrD, 40 * m * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMemcpy(c.dCorrD, d, 40 * m * sizeof(double2), cudaMemcpyHostToDevice));
+    const size_t uvBytes = static_cast<size_t>(40) * std::max(rank, 1) * m * sizeof(double2);
+    TBT_CUDA_CHECK(cudaMalloc(&c.dCorrU, uvBytes));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dCorrV, uvBytes));
+    if (rank > 0) {
+      TBT_CUDA_CHECK(cudaMemcpy(c.dCorrU, u, static_cast<size_t>(40) * rank * m * sizeof(double2),
+                                cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dCorrV, v, static_cast<size_t>(40) * rank * m * sizeof(double2),
+                                cudaMemcpyHostToDevice));
+    }
+    // Term list grouped by target element (CSR).
+    static const int dr[5] = {0, 0, 0, 1, -1};
+    static const int dc[5] = {0, 1, -1, 0, 0};
+    std::vector<std::vector<std::array<int, 4>>> byTarget(c.ne);
+    for (int r = 0; r < c.ny; ++r)
+      for (int col = 0; col < c.nx; ++col) {
+        const int comp = componentOf(c.nx, c.ny, r, col);
+        if (comp == 5) continue;
+        const int e = r * c.nx + col;
+        for (int rel = 0; rel < 5; ++rel) {
+          const int r2 = r + dr[rel], c2 = col + dc[rel];
+          if (r2 < 0 || r2 >= c.ny || c2 < 0 || c2 >= c.nx) continue;
+          const int e2 = r2 * c.nx + c2;
+          const int slot = kSlotOfComp[comp] * 5 + rel;
+          byTarget[e].push_back({e, e2, slot, 0});   // y_e  += P   x_e'
+          byTarget[e2].push_back({e2, e, slot, 1});  // y_e' += P^T x_e
+        }
+      }
+    std::vector<int> info, targets, ptr{0};
+    for (int e = 0; e < c.ne; ++e) {
+      if (byTarget[e].empty()) continue;
+      targets.push_back(e);
+      for (auto& t : byTarget[e]) info.insert(info.end(), t.begin(), t.end());
+      ptr.push_back(static_cast<int>(info.size() / 4));
+    }
+    c.nTerms = static_cast<int>(info.size() / 4);
+    c.nTargets = static_cast<int>(targets.size());
+    if (c.nTerms > 0) {
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTermInfo, info.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTargetList, targets.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTargetPtr, ptr.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dTermInfo, info.data(), info.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dTargetList, targets.data(), targets.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dTargetPtr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dProj, static_cast<size_t>(c.nTerms) * c.maxNrhs * std::max(rank, 1) *
+                                              sizeof(double2)));
+    }
+    c.haveCorr = true;
+    if (c.havePrecompute) refreshDiagonal(c, nullptr);
+  });
+}
+
+tbt_status tbt_precompute(tbt_ctx* h) {
+  return guarded([&] {
+    TBT_USER_CHECK(h, "tbt_precompute: null context");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(c.haveGenerators, "tbt_precompute: call tbt_set_generators first");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    c.dropGraph();
+    buildSpectra(c);
+    refreshDiagonal(c, nullptr);
+    c.havePrecompute = true;
+  });
+}
+
+static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, int where, bool withCorr) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && x && y, "tbt_apply: null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, "tbt_apply: nrhs outside [1, max_nrhs]");
+    TBT_USER_CHECK(where == TBT_HOST || where == TBT_DEVICE, "tbt_apply: bad memory kind");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    const long long total = c.n * nrhs;
+    const size_t bytes = total * sizeof(double2);
+    const double2* xin = reinterpret_cast<const double2*>(x);
+    double2* yout = reinterpret_cast<double2*>(y);
+    if (where == TBT_HOST) {
+      if (nrhs == 1) {
+        TBT_CUDA_CHECK(cudaMemcpyAsync(c.dXin, xin, bytes, cudaMemcpyHostToDevice, c.stream));
+      } else {
+        TBT_CUDA_CHECK(cudaMemcpyAsync(c.dYout, xin, bytes, cudaMemcpyHostToDevice, c.stream));
+        launchLayout(c.dYout, c.dXin, c.n, nrhs, true, c.stream, c.m);
+      }
+      if (nrhs == 1)
+        runApply1(c, c.dXin, c.dYout, withCorr);
+      else
+        applyInternal(c, c.dXin, c.dYout, nrhs, withCorr);
+      if (nrhs == 1) {
+        TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dYout, bytes, cudaMemcpyDeviceToHost, c.stream));
+      } else {
+        launchLayout(c.dYout, c.dXin, c.n, nrhs, false, c.stream, c.m);
+        TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dXin, bytes, cudaMemcpyDeviceToHost, c.stream));
+      }
+      TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    } else {
+      if (nrhs == 1) {
+        runApply1(c, xin, yout, withCorr);
+      } else {
+        launchLayout(xin, c.dXin, c.n, nrhs, true, c.stream, c.m);
+        applyInternal(c, c.dXin, c.dYout, nrhs, withCorr);
+        launchLayout(c.dYout, yout, c.n, nrhs, false, c.stream, c.m);
+      }
+    }
+  });
+}
+
+tbt_status tbt_apply(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
+  return applyCommon(h, x, y, nrhs, where, true);
+}
+
+tbt_status tbt_apply_a(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
+  return applyCommon(h, x, y, nrhs, where, false);
+}
+
+tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && d, "tbt_diagonal: null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    std::vector<double2> dd;
+    refreshDiagonal(c, &dd);
+    std::memcpy(d, dd.data(), dd.size() * sizeof(double2));
+  });
+}
+
+tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt_gmres_opts* opts,
+                     tbt_gmres_stats* stats, int where) {
+  std::string failure;
+  tbt_status st = guarded([&] {
+    TBT_USER_CHECK(h && b && x && opts, "tbt_gmres: null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, "tbt_gmres: nrhs outside [1, max_nrhs]");
+    TBT_USER_CHECK(opts->restart >= 1 && opts->max_iter >= 0 && opts->tol > 0.0, "tbt_gmres: bad options");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    const long long total = c.n * nrhs;
+    const size_t bytes = total * sizeof(double2);
+    double2 *db = nullptr, *dx = nullptr;
+    TBT_CUDA_CHECK(cudaMalloc(&db, bytes));
+    TBT_CUDA_CHECK(cudaMalloc(&dx, bytes));
+    std::vector<GmresState> out;
+    std::vector<double> hist;
+    int matvecs = 0;
+    try {
+      const double2* bsrc = reinterpret_cast<const double2*>(b);
+      if (where == TBT_HOST) {
+        TBT_CUDA_CHECK(cudaMemcpyAsync(dx, bsrc, bytes, cudaMemcpyHostToDevice, c.stream));
+        launchLayout(dx, db, c.n, nrhs, true, c.stream, c.m);
+      } else {
+        launchLayout(bsrc, db, c.n, nrhs, true, c.stream, c.m);
+      }
+      gmresSolve(c, db, dx, nrhs, *opts, opts->use_a_only != 0, out, hist, matvecs);
+      double2* xdst = reinterpret_cast<double2*>(x);
+      if (where == TBT_HOST) {
+        launchLayout(dx, db, c.n, nrhs, false, c.stream, c.m);
+        TBT_CUDA_CHECK(cudaMemcpyAsync(xdst, db, bytes, cudaMemcpyDeviceToHost, c.stream));
+      } else {
+        launchLayout(dx, xdst, c.n, nrhs, false, c.stream, c.m);
+      }
+      TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    } catch (...) {
+      cudaFree(db);
+      cudaFree(dx);
+      throw;
+    }
+    cudaFree(db);
+    cudaFree(dx);
+    if (stats) {
+      const int cap = std::max(0, opts->hist_cap);
+      for (int k = 0; k < nrhs; ++k) {
+        if (stats->iterations) stats->iterations[k] = out[k].iterations;
+        if (stats->residual) stats->residual[k] = out[k].residual;
+        if (stats->converged) stats->converged[k] = out[k].converged;
+        if (stats->history_len) stats->history_len[k] = out[k].histLen;
+        if (stats->history && cap > 0)
+          std::memcpy(stats->history + static_cast<size_t>(2) * cap * k, hist.data() + static_cast<size_t>(2) * cap * k,
+                      sizeof(double) * 2 * cap);
+      }
+      stats->matvecs = matvecs;
+    }
+    for (int k = 0; k < nrhs; ++k)
+      if (!out[k].converged && failure.empty())
+        failure = "gmres did not converge for column " + std::to_string(k) + ": best residual " +
+                  std::to_string(out[k].residual) + " after " + std::to_string(out[k].iterations) + " iterations";
+  });
+  if (st == TBT_OK && !failure.empty()) {
+    gLastError = failure;
+    return TBT_NUMERIC_ERROR;
+  }
+  return st;
+}
+
+tbt_status tbt_get_info(const tbt_ctx* h, tbt_info* info) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && info, "tbt_get_info: null argument");
+    const Ctx& c = h->c;
+    info->n = c.n;
+    info->bins = c.L;
+    info->pairs = c.npairs;
+    info->L0 = c.L0;
+    info->L1 = c.L1;
+    info->spectra_bytes = c.npairs * static_cast<long long>(c.m) * c.m * 16;
+    info->binprod_kernel = c.binprodKernel;
+    info->kernels_per_apply = 5 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? (c.rank > 0 ? 2 : 1) : 0);
+    info->has_antisym = c.hasAntisym ? 1 : 0;
+  });
+}
+
+tbt_status tbt_get_spectrum_bin(tbt_ctx* h, long long f, double* out) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && out, "tbt_get_spectrum_bin: null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(f >= 0 && f < c.L, "tbt_get_spectrum_bin: bin out of range");
+    const long long code = c.pairOfBin[f];
+    const long long p = code >= 0 ? code : -code - 1;
+    const size_t mm = static_cast<size_t>(c.m) * c.m;
+    std::vector<double2> blk(mm);
+    TBT_CUDA_CHECK(cudaMemcpy(blk.data(), c.dSpectra + p * mm, mm * sizeof(double2), cudaMemcpyDeviceToHost));
+    double2* o = reinterpret_cast<double2*>(out);
+    for (int a = 0; a < c.m; ++a)
+      for (int b = 0; b < c.m; ++b)
+        o[static_cast<size_t>(a) * c.m + b] = code >= 0 ? blk[static_cast<size_t>(a) * c.m + b]
+                                                        : blk[static_cast<size_t>(b) * c.m + a];
+  });
+}
+
+tbt_status tbt_set_timing(tbt_ctx* h, int on) {
+  return guarded([&] {
+    TBT_USER_CHECK(h, "tbt_set_timing: null context");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.timeBinprod = on != 0;
+    c.tCount = 0;
+  });
+}
+
+tbt_status tbt_timing_read(tbt_ctx* h, double* total, int* count) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && total && count, "tbt_timing_read: null argument");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    double sum = 0.0;
+    for (int k = 0; k < c.tCount; ++k) {
+      float ms = 0.f;
+      TBT_CUDA_CHECK(cudaEventElapsedTime(&ms, c.tEvA[k], c.tEvB[k]));
+      sum += ms;
+    }
+    *total = sum;
+    *count = c.tCount;
+  });
+}
+
+tbt_status tbt_bench_apply(tbt_ctx* h, const double* x_dev, double* y_dev, int nrhs, int iters, int use_graph,
+                           double* out_ms, double* out_binprod_ms) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && x_dev && y_dev && iters >= 1, "tbt_bench_apply: bad argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(nrhs == 1, "tbt_bench_apply: nrhs must be 1");
+    const double2* x = reinterpret_cast<const double2*>(x_dev);
+    double2* y = reinterpret_cast<double2*>(y_dev);
+    cudaEvent_t e0, e1;
+    TBT_CUDA_CHECK(cudaEventCreate(&e0));
+    TBT_CUDA_CHECK(cudaEventCreate(&e1));
+    cudaGraphExec_t exec = nullptr;
+    if (use_graph) {
+      cudaGraph_t graph;
+      TBT_CUDA_CHECK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      applyInternal(c, x, y, 1, true);
+      TBT_CUDA_CHECK(cudaStreamEndCapture(c.stream, &graph));
+      TBT_CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+    }
+    // Whole applies.
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    TBT_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+    for (int k = 0; k < iters; ++k) {
+      if (exec)
+        TBT_CUDA_CHECK(cudaGraphLaunch(exec, c.stream));
+      else
+        applyInternal(c, x, y, 1, true);
+    }
+    TBT_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+    TBT_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    TBT_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    if (out_ms) *out_ms = ms / iters;
+    // The bin-product kernel alone, back to back on the same data.
+    if (out_binprod_ms) {
+      TBT_CUDA_CHECK(cudaEventRecord(e0, c.stream));
+      for (int k = 0; k < iters; ++k) launchBinProduct(c, 1);
+      TBT_CUDA_CHECK(cudaEventRecord(e1, c.stream));
+      TBT_CUDA_CHECK(cudaEventSynchronize(e1));
+      TBT_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      *out_binprod_ms = ms / iters;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+}  // extern "C"

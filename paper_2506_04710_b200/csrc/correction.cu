@@ -1,0 +1,101 @@
+// Non-Toeplitz terms of the operator, applied in the spatial domain after
+// the inverse transform:
+//  * the synthetic nine-component edge/corner correction (BASELINE.json;
+//    include/tbt_gen.h), the stand-in for ToeplitzMatvec::apply's margin
+//    coupling (proj/src/linsolve.cpp:384-386): per term
+//        y_t += diag(d) x_s + U (V^T x_s)      (P)
+//        y_t += diag(d) x_s + V (U^T x_s)      (P^T)
+//    as a rank-r projection pass plus a per-target accumulation pass;
+//  * the antisymmetric part K of Z(0,0) (see spectra.cu): y_e += K x_e.
+// Internal vector layout is [element][rhs][basis].
+#include "tbt_internal.cuh"
+
+namespace tbt {
+namespace {
+
+// One warp per (term, rhs): proj[t][rhs][q] = sum_a W[s][q][a] x[src][rhs][a].
+__global__ void corrProject(const int* __restrict__ termInfo, int nTerms, const double2* __restrict__ U,
+                            const double2* __restrict__ V, const double2* __restrict__ x, double2* __restrict__ proj,
+                            int m, int rank, int nrhs) {
+  const int warpsPerBlock = blockDim.x / 32;
+  const long long wid = static_cast<long long>(blockIdx.x) * warpsPerBlock + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<long long>(nTerms) * nrhs) return;
+  const int t = static_cast<int>(wid / nrhs), rhs = static_cast<int>(wid % nrhs);
+  const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+  const double2* W = (trans ? U : V) + static_cast<long long>(slot) * rank * m;
+  const double2* xs = x + (static_cast<long long>(src) * nrhs + rhs) * m;
+  for (int q = 0; q < rank; ++q) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int a = lane; a < m; a += 32) cfma(s, W[static_cast<long long>(q) * m + a], xs[a]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+    }
+    if (lane == 0) proj[(static_cast<long long>(t) * nrhs + rhs) * rank + q] = s;
+  }
+}
+
+// One CTA per (target, rhs), threads over the basis index.
+__global__ void corrApply(const int* __restrict__ termInfo, const int* __restrict__ targetList,
+                          const int* __restrict__ targetPtr, const double2* __restrict__ D,
+                          const double2* __restrict__ U, const double2* __restrict__ V,
+                          const double2* __restrict__ x, const double2* __restrict__ proj, double2* __restrict__ y,
+                          int m, int rank, int nrhs) {
+  const int ti = blockIdx.x, rhs = blockIdx.y;
+  const int e = targetList[ti];
+  const int t0 = targetPtr[ti], t1 = targetPtr[ti + 1];
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int t = t0; t < t1; ++t) {
+      const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+      cfma(acc, D[static_cast<long long>(slot) * m + a], x[(static_cast<long long>(src) * nrhs + rhs) * m + a]);
+      const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * rank * m;
+      const double2* pr = proj + (static_cast<long long>(t) * nrhs + rhs) * rank;
+      for (int q = 0; q < rank; ++q) cfma(acc, W2[static_cast<long long>(q) * m + a], pr[q]);
+    }
+    double2* out = y + (static_cast<long long>(e) * nrhs + rhs) * m + a;
+    *out = cadd(*out, acc);
+  }
+}
+
+// y[e][rhs][a] += sum_b K[a][b] x[e][rhs][b].
+__global__ void antisymApply(const double2* __restrict__ K, const double2* __restrict__ x, double2* __restrict__ y,
+                             int m, int nrhs) {
+  extern __shared__ double2 sx[];
+  const long long base = (static_cast<long long>(blockIdx.x) * nrhs + blockIdx.y) * m;
+  for (int b = threadIdx.x; b < m; b += blockDim.x) sx[b] = x[base + b];
+  __syncthreads();
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int b = 0; b < m; ++b) cfma(s, K[static_cast<long long>(a) * m + b], sx[b]);
+    y[base + a] = cadd(y[base + a], s);
+  }
+}
+
+}  // namespace
+
+void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs) {
+  if (!c.haveCorr || c.nTerms == 0) return;
+  if (c.rank > 0) {
+    const long long warps = static_cast<long long>(c.nTerms) * nrhs;
+    const int blocks = static_cast<int>((warps + 7) / 8);
+    corrProject<<<blocks, 256, 0, c.stream>>>(c.dTermInfo, c.nTerms, c.dCorrU, c.dCorrV, x, c.dProj, c.m, c.rank,
+                                              nrhs);
+    TBT_CUDA_CHECK(cudaGetLastError());
+  }
+  dim3 grid(c.nTargets, nrhs);
+  corrApply<<<grid, 64, 0, c.stream>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x,
+                                       c.dProj, y, c.m, c.rank, nrhs);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs) {
+  if (!c.hasAntisym) return;
+  dim3 grid(c.ne, nrhs);
+  antisymApply<<<grid, 64, c.m * sizeof(double2), c.stream>>>(c.dAntisym, x, y, c.m, nrhs);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tbt

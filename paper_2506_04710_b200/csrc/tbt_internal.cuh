@@ -1,0 +1,163 @@
+// Internal declarations of the B200 block-Toeplitz library (libtbt.so).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tbt.h"
+
+namespace tbt {
+
+// ---------------------------------------------------------------- errors
+void setError(const std::string& msg);
+struct Error {
+  tbt_status code;
+  std::string msg;
+};
+#define TBT_CUDA_CHECK(expr)                                                     \
+  do {                                                                           \
+    cudaError_t e_ = (expr);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      throw ::tbt::Error{TBT_CUDA_ERROR, std::string(#expr) + ": " +             \
+                                            cudaGetErrorString(e_)};             \
+  } while (0)
+#define TBT_USER_CHECK(cond, msg)                                                \
+  do {                                                                           \
+    if (!(cond)) throw ::tbt::Error{TBT_USER_ERROR, (msg)};                     \
+  } while (0)
+
+// ---------------------------------------------------------------- complex
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc += a * b
+__host__ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__host__ __device__ __forceinline__ void cfma_conj(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// ---------------------------------------------------------------- FFT plan
+// One batched 1-D pass over "lines" of a [point][batch] layout (batch
+// contiguous). Line l, point p, batch b lives at
+//   base + l*line_stride + p*point_stride + b      (complex units).
+struct FftPass {
+  const double2* in = nullptr;
+  double2* out = nullptr;
+  long long in_line_stride = 0, in_point_stride = 0;
+  long long out_line_stride = 0, out_point_stride = 0;
+  int lines = 0;
+  int n = 1;       // transform length
+  int n_in = 1;    // leading input points that may be non-zero
+  int n_out = 1;   // leading output points written
+  int batch = 0;   // batch entries per point
+  int inverse = 0;
+  double scale = 1.0;
+  const double2* tw = nullptr;  // exp(-2 pi i t / n), t < n
+};
+void launchFftPass(const FftPass& p, cudaStream_t s);
+
+// ---------------------------------------------------------------- context
+struct CorrTerm {  // y[target] += P x[source] (trans 0) or P^T x[source]
+  int target, source, slot, trans;
+};
+
+struct Ctx {
+  int nx = 0, ny = 0, m = 0, ne = 0, maxNrhs = 1, device = 0;
+  long long n = 0;  // nx*ny*m
+  int L0 = 1, L1 = 1;
+  long long L = 1;
+  cudaStream_t stream = nullptr;
+  bool ownStream = false;
+
+  // Generators (host copy kept for diagonal / K) and spectra.
+  std::vector<double2> genHost;
+  bool haveGenerators = false, havePrecompute = false;
+  long long npairs = 0;
+  double2* dSpectra = nullptr;    // [npairs][m][m] row-major
+  int* dPairF = nullptr;          // representative bin of pair p
+  int* dPairG = nullptr;          // partner bin (== F for self-paired)
+  std::vector<int> pairF, pairG;  // host copies
+  std::vector<long long> pairOfBin;  // bin -> pair (negative: -(p+1) transposed)
+  bool hasAntisym = false;
+  double2* dAntisym = nullptr;    // K = (Z0 - Z0^T)/2, [a][b] row-major
+
+  // Twiddles for L0, L1.
+  double2* dTw0 = nullptr;
+  double2* dTw1 = nullptr;
+
+  // Correction.
+  int rank = 0;
+  bool haveCorr = false;
+  double2* dCorrD = nullptr;  // [40][m]
+  double2* dCorrU = nullptr;  // [40][rank][m]
+  double2* dCorrV = nullptr;
+  std::vector<double2> corrDHost;
+  int nTerms = 0, nTargets = 0;
+  int* dTermInfo = nullptr;     // [nTerms][4] {target, source, slot, trans}
+  int* dTargetList = nullptr;   // [nTargets] target elements
+  int* dTargetPtr = nullptr;    // [nTargets+1] CSR over terms
+  double2* dProj = nullptr;     // [nTerms][nrhs][rank]
+
+  // Work buffers sized for maxNrhs.
+  double2* dT = nullptr;      // [ny][L0][B]
+  double2* dXhat = nullptr;   // [L][B]
+  double2* dYhat = nullptr;   // [L][B]
+  double2* dXin = nullptr;    // [ne][B] staging (host/colmajor input)
+  double2* dYout = nullptr;   // [ne][B]
+  double2* dDiagInv = nullptr;
+
+  // Timing hooks: event pairs around K3, one per timed apply.
+  cudaEvent_t evBinA = nullptr, evBinB = nullptr;
+  bool timeBinprod = false;
+  std::vector<cudaEvent_t> tEvA, tEvB;
+  int tCount = 0;
+  int binprodKernel = 0;
+
+  // CUDA graph of one device-resident single-column apply.
+  cudaGraphExec_t graphExec = nullptr;
+  const void* graphX = nullptr;
+  void* graphY = nullptr;
+  bool graphCorr = false;
+  void dropGraph() {
+    if (graphExec) cudaGraphExecDestroy(graphExec);
+    graphExec = nullptr;
+    graphX = graphY = nullptr;
+  }
+};
+
+// Kernels / launchers implemented in the .cu files.
+void buildSpectra(Ctx& c);                                    // spectra.cu
+void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
+void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
+int binprodVariant(int m);                                    // binprod.cu
+void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
+void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs);     // correction.cu
+void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s, int m);  // apply.cu
+
+// GMRES (gmres.cu): per-column state mirrored to the host.
+struct GmresState {
+  double bnorm, beta, residual;
+  int iterations, ncount, stopInner, done, converged, cycleActive, histLen, pad;
+};
+void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres_opts& o, bool useAOnly,
+                std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs);
+
+// Launch configuration helper: SM count of the context's device.
+int smCount(int device);
+
+}  // namespace tbt

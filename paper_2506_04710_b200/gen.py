@@ -1,0 +1,80 @@
+"""Seeded synthetic inputs (include/tbt_gen.h) as numpy arrays.
+
+Complex arrays are numpy complex128 (binary layout of interleaved doubles).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import dp, lib, llp
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags.c_contiguous or a.flags.f_contiguous
+    return a.ctypes.data_as(dp)
+
+
+def num_blocks(nx: int, ny: int) -> int:
+    return int(lib().tbtgen_num_blocks(nx, ny))
+
+
+def block_shift(nx: int, ny: int, t: int) -> tuple[int, int]:
+    i, j = C.c_int(), C.c_int()
+    if lib().tbtgen_block_shift(nx, ny, t, C.byref(i), C.byref(j)):
+        raise IndexError(t)
+    return i.value, j.value
+
+
+def blocks(nx: int, ny: int, m: int, seed: int, nthreads: int = 0) -> np.ndarray:
+    """Canonical generator blocks, shape (nb, m, m) with [t, a, b] = Z_t(a, b)
+    (memory is column-major per block, as the C ABI expects: use
+    `blocks_raw` to pass it on)."""
+    raw = blocks_raw(nx, ny, m, seed, nthreads)
+    return np.transpose(raw, (0, 2, 1))
+
+
+def blocks_raw(nx: int, ny: int, m: int, seed: int, nthreads: int = 0) -> np.ndarray:
+    nb = num_blocks(nx, ny)
+    out = np.empty((nb, m, m), dtype=np.complex128)  # [t][b][a] = column-major blocks
+    if lib().tbtgen_blocks(nx, ny, m, seed, _ptr(out), nthreads):
+        raise ValueError("tbtgen_blocks failed")
+    return out
+
+
+def correction(m: int, rank: int, seed: int, scale: float = 0.1):
+    """(d[40, m], U[40, rank, m], V[40, rank, m]) in the C ABI layout."""
+    d = np.empty((40, m), dtype=np.complex128)
+    u = np.empty((40, max(rank, 1), m), dtype=np.complex128)
+    v = np.empty_like(u)
+    if lib().tbtgen_correction(m, rank, seed, scale, _ptr(d), _ptr(u), _ptr(v)):
+        raise ValueError("tbtgen_correction failed")
+    return d, u[:, :rank].copy(), v[:, :rank].copy()
+
+
+def rhs_normal(n: int, ncols: int, seed: int) -> np.ndarray:
+    out = np.empty((ncols, n), dtype=np.complex128)
+    if lib().tbtgen_rhs_normal(n, ncols, seed, _ptr(out)):
+        raise ValueError("tbtgen_rhs_normal failed")
+    return out.T  # n x ncols, column-major memory
+
+
+def rhs_delta_steered(nx: int, ny: int, m: int, seed: int, steer_deg: float = 30.0) -> np.ndarray:
+    out = np.empty(nx * ny * m, dtype=np.complex128)
+    if lib().tbtgen_rhs_delta_steered(nx, ny, m, seed, steer_deg, _ptr(out)):
+        raise ValueError("tbtgen_rhs_delta_steered failed")
+    return out
+
+
+def rhs_ports(nx: int, ny: int, m: int, seed: int):
+    ne = nx * ny
+    out = np.empty((ne, ne * m), dtype=np.complex128)
+    rows = np.empty(ne, dtype=np.int64)
+    if lib().tbtgen_rhs_ports(nx, ny, m, seed, _ptr(out), rows.ctypes.data_as(llp)):
+        raise ValueError("tbtgen_rhs_ports failed")
+    return out.T, rows
+
+
+def component(nx: int, ny: int, r: int, c: int) -> int:
+    return int(lib().tbtgen_component(nx, ny, r, c))

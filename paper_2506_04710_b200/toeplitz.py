@@ -1,0 +1,249 @@
+"""Host-side mirror of the reference's operator and solver API
+(proj/include/arraymom/linsolve.hpp:26-95) over the C ABI of libtbt.so.
+
+    ToeplitzMatvec(rep)      -> ToeplitzMatvec(rep, model)   linsolve.hpp:61
+      .apply / .applyA / .diagonal / .sizeA / .sizeM          linsolve.hpp:64-72
+    toeplitz_matvec(rep, x)  -> toeplitzMatvec               linsolve.hpp:80-81
+    iterative_solve(rep, V, opt) -> iterativeSolve           linsolve.hpp:88-89
+    SolverOptions / SolveResult / UserError / NumericError   linsolve.hpp:40-53,
+                                                             common.hpp:38-50
+
+`ToeplitzRep` here holds what the hot path consumes from the reference's
+ToeplitzRep (toeplitz.hpp:67-107): nx, ny, e5 = m and the Sparse A
+generators aGen (toeplitz.hpp:72-74), plus the synthetic nine-component
+correction that stands in for the margin blocks of the BASELINE workloads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import TBT_DEVICE, TBT_HOST, TbtDesc, TbtGmresOpts, TbtGmresStats, TbtInfo, dp, lib
+
+
+class UserError(RuntimeError):
+    """Bad input (reference UserError, exit code 1)."""
+
+
+class NumericError(RuntimeError):
+    """Numerical failure, e.g. GMRES non-convergence (reference NumericError, exit code 2)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no usable sm_100 device."""
+
+
+def _check(status: int) -> None:
+    if status == _lib.TBT_OK:
+        return
+    msg = _lib.last_error()
+    if status == _lib.TBT_USER_ERROR:
+        raise UserError(msg)
+    if status == _lib.TBT_NUMERIC_ERROR:
+        raise NumericError(msg)
+    raise DeviceError(msg)
+
+
+@dataclass
+class Correction:
+    rank: int
+    d: np.ndarray  # (40, m)
+    u: np.ndarray  # (40, rank, m)
+    v: np.ndarray  # (40, rank, m)
+
+
+@dataclass
+class ToeplitzRep:
+    nx: int
+    ny: int
+    m: int
+    generators: np.ndarray  # (nb, m, m) column-major blocks, raw layout of gen.blocks_raw
+    correction: Correction | None = None
+
+    @classmethod
+    def synthetic(cls, cfg) -> "ToeplitzRep":
+        from . import gen
+        blk = gen.blocks_raw(cfg.nx, cfg.ny, cfg.m, cfg.seed)
+        corr = None
+        if cfg.rank >= 0 and cfg.scale > 0:
+            d, u, v = gen.correction(cfg.m, cfg.rank, cfg.seed, cfg.scale)
+            corr = Correction(cfg.rank, d, u, v)
+        return cls(cfg.nx, cfg.ny, cfg.m, blk, corr)
+
+    def elementEdges(self) -> int:  # toeplitz.hpp:98
+        return self.nx * self.ny * self.m
+
+
+@dataclass
+class SolverOptions:  # linsolve.hpp:47-53
+    tol: float = 1e-8
+    maxIter: int = 2000
+    restart: int = 60
+    precondition: bool = True
+    threads: int = 1  # accepted for API parity; columns run in lockstep on the GPU
+
+
+@dataclass
+class SolveResult:  # linsolve.hpp:40-45
+    current: np.ndarray
+    residual: list
+    iterations: list
+    solver: str = "gmres"
+    converged: list = field(default_factory=list)
+    history: list = field(default_factory=list)
+    matvecs: int = 0
+
+
+def _as_cols(x: np.ndarray) -> tuple[np.ndarray, int, bool]:
+    x = np.asarray(x, dtype=np.complex128)
+    vec = x.ndim == 1
+    if vec:
+        x = x[:, None]
+    return np.asfortranarray(x), x.shape[1], vec
+
+
+class ToeplitzMatvec:
+    """FFT-accelerated application of Z^part (linsolve.hpp:59-77) on a B200."""
+
+    def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0):
+        self.rep = rep
+        self._h = C.c_void_p()
+        desc = TbtDesc(rep.nx, rep.ny, rep.m, max_nrhs, device, 0)
+        _check(lib().tbt_create(C.byref(desc), C.byref(self._h)))
+        gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
+        _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))
+        if rep.correction is not None:
+            c = rep.correction
+            d = np.ascontiguousarray(c.d)
+            u = np.ascontiguousarray(c.u) if c.rank > 0 else None
+            v = np.ascontiguousarray(c.v) if c.rank > 0 else None
+            _check(lib().tbt_set_correction(self._h, c.rank, d.ctypes.data_as(dp),
+                                            u.ctypes.data_as(dp) if u is not None else None,
+                                            v.ctypes.data_as(dp) if v is not None else None))
+        _check(lib().tbt_precompute(self._h))
+        self.max_nrhs = max_nrhs
+
+    def close(self) -> None:
+        if self._h:
+            lib().tbt_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- reference methods -------------------------------------------------
+    def sizeA(self) -> int:
+        return int(lib().tbt_size_a(self._h))
+
+    def sizeM(self) -> int:
+        return 0  # margin unknowns are folded into the synthetic correction
+
+    def _apply(self, fn, x):
+        xc, k, vec = _as_cols(x)
+        if xc.shape[0] != self.sizeA():
+            raise UserError(f"matvec: vector length {xc.shape[0]} does not match system size {self.sizeA()}")
+        y = np.empty_like(xc, order="F")
+        _check(fn(self._h, xc.ctypes.data, y.ctypes.data, k, TBT_HOST))
+        return y[:, 0] if vec else y
+
+    def apply(self, x):
+        return self._apply(lib().tbt_apply, x)
+
+    def applyA(self, x):
+        return self._apply(lib().tbt_apply_a, x)
+
+    def diagonal(self) -> np.ndarray:
+        d = np.empty(self.sizeA(), dtype=np.complex128)
+        _check(lib().tbt_diagonal(self._h, d.ctypes.data_as(dp)))
+        return d
+
+    # -- device-pointer entry points (bench / torch interop) ----------------
+    def apply_device(self, x_ptr: int, y_ptr: int, nrhs: int = 1, a_only: bool = False) -> None:
+        fn = lib().tbt_apply_a if a_only else lib().tbt_apply
+        _check(fn(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), nrhs, TBT_DEVICE))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        _check(lib().tbt_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def stream(self) -> int:
+        return int(lib().tbt_get_stream(self._h) or 0)
+
+    def info(self) -> TbtInfo:
+        inf = TbtInfo()
+        _check(lib().tbt_get_info(self._h, C.byref(inf)))
+        return inf
+
+    def spectrum_bin(self, f: int) -> np.ndarray:
+        out = np.empty((self.rep.m, self.rep.m), dtype=np.complex128)
+        _check(lib().tbt_get_spectrum_bin(self._h, f, out.ctypes.data_as(dp)))
+        return out
+
+    def set_timing(self, on: bool) -> None:
+        _check(lib().tbt_set_timing(self._h, 1 if on else 0))
+
+    def timing_read(self) -> tuple[float, int]:
+        tot, cnt = C.c_double(), C.c_int()
+        _check(lib().tbt_timing_read(self._h, C.byref(tot), C.byref(cnt)))
+        return tot.value, cnt.value
+
+    def bench_apply(self, x_ptr: int, y_ptr: int, iters: int, use_graph: bool = True):
+        ms, bms = C.c_double(), C.c_double()
+        _check(lib().tbt_bench_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), 1, iters,
+                                     1 if use_graph else 0, C.byref(ms), C.byref(bms)))
+        return ms.value, bms.value
+
+    def gmres(self, b, opt: SolverOptions, use_a_only: bool = False, hist_cap: int = 4096,
+              raise_on_fail: bool = True, where: int = TBT_HOST, b_ptr: int = 0, x_ptr: int = 0,
+              nrhs: int | None = None) -> SolveResult:
+        if where == TBT_HOST:
+            bc, k, vec = _as_cols(b)
+            x = np.empty_like(bc, order="F")
+            bp, xp = bc.ctypes.data, x.ctypes.data
+        else:
+            k, vec, x = int(nrhs), False, None
+            bp, xp = b_ptr, x_ptr
+        its = np.zeros(k, dtype=np.int32)
+        res = np.zeros(k, dtype=np.float64)
+        conv = np.zeros(k, dtype=np.int32)
+        hlen = np.zeros(k, dtype=np.int32)
+        hist = np.zeros((k, max(hist_cap, 1), 2), dtype=np.float64)
+        st = TbtGmresStats(its.ctypes.data_as(C.POINTER(C.c_int)), res.ctypes.data_as(dp),
+                           conv.ctypes.data_as(C.POINTER(C.c_int)), hist.ctypes.data_as(dp),
+                           hlen.ctypes.data_as(C.POINTER(C.c_int)), 0)
+        o = TbtGmresOpts(opt.tol, opt.maxIter, opt.restart, 1 if opt.precondition else 0,
+                         1 if use_a_only else 0, hist_cap)
+        status = lib().tbt_gmres(self._h, C.c_void_p(bp), C.c_void_p(xp), k, C.byref(o), C.byref(st), where)
+        if status not in (_lib.TBT_OK, _lib.TBT_NUMERIC_ERROR) or (status != _lib.TBT_OK and raise_on_fail):
+            _check(status)
+        histories = [hist[c, :min(int(hlen[c]), hist_cap)].copy() for c in range(k)]
+        cur = None if x is None else (x[:, 0] if vec else x)
+        return SolveResult(cur, res.tolist(), its.tolist(), "gmres", conv.tolist(), histories, st.matvecs)
+
+
+def toeplitz_matvec(rep: ToeplitzRep, x) -> np.ndarray:
+    """One-shot wrapper (linsolve.hpp:80-81)."""
+    op = ToeplitzMatvec(rep)
+    try:
+        return op.apply(x)
+    finally:
+        op.close()
+
+
+def iterative_solve(rep: ToeplitzRep, V, opt: SolverOptions | None = None) -> SolveResult:
+    """iterativeSolve (linsolve.cpp:551-593): restarted GMRES per column,
+    Jacobi on by default; raises NumericError if a column does not converge."""
+    opt = opt or SolverOptions()
+    Vc, k, _ = _as_cols(V)
+    op = ToeplitzMatvec(rep, max_nrhs=k)
+    try:
+        if Vc.shape[0] != op.sizeA():
+            raise UserError("iterativeSolve: excitation size mismatch")
+        return op.gmres(V, opt)
+    finally:
+        op.close()

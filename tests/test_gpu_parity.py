@@ -1,0 +1,177 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle on
+identical seeded inputs. Tolerances are the north star's: matvec relative
+error <= 1e-11 (complex128); GMRES solution and residual history within
+1e-8 relative."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2506_04710_b200 import (CONFIGS, Config, SolverOptions, ToeplitzMatvec, ToeplitzRep, UserError,
+                                   gen, rhs_for)
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-11
+GMRES_TOL = 1e-8
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def rep_for(nx, ny, m, seed=1, rank=4, antisym=False, corr=True):
+    cfg = Config("t", nx, ny, m, 1, rank, seed, "normal", 20)
+    rep = ToeplitzRep.synthetic(cfg)
+    if not corr:
+        rep.correction = None
+    if antisym:
+        rng = np.random.default_rng(seed + 99)
+        k = rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))
+        rep.generators[0] += 0.3 * (k - k.T)
+    return rep
+
+
+SHAPES = [(4, 4, 24), (1, 1, 5), (1, 5, 3), (6, 1, 4), (3, 5, 7), (5, 3, 8), (7, 9, 64), (9, 5, 128),
+          (5, 4, 192), (16, 16, 64), (17, 9, 32)]
+
+
+@pytest.mark.parametrize("nx,ny,m", SHAPES)
+@pytest.mark.parametrize("antisym", [False, True])
+def test_apply_matches_oracle(gpu, nx, ny, m, antisym):
+    rep = rep_for(nx, ny, m, seed=nx + 7 * ny, antisym=antisym)
+    op = ToeplitzMatvec(rep)
+    o = oracle.Oracle.from_rep(rep)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        x = rng.standard_normal(o.n) + 1j * rng.standard_normal(o.n)
+        assert rel(op.apply(x), o.apply(x)) < MATVEC_TOL
+        assert rel(op.applyA(x), o.applyA(x)) < MATVEC_TOL
+    assert np.array_equal(op.apply(np.zeros(o.n, complex)), np.zeros(o.n, complex))
+    assert np.allclose(op.diagonal(), o.diagonal(), rtol=1e-14, atol=0)
+
+
+def test_spectra_bins_match_reference_layout(gpu):
+    nx, ny, m = 5, 3, 6
+    rep = rep_for(nx, ny, m, antisym=False)
+    op = ToeplitzMatvec(rep)
+    ah = oracle.Oracle.from_rep(rep).ahat()  # [(m*e5+n)*L + f]
+    inf = op.info()
+    assert inf.bins == 64 and inf.pairs == (64 + 4) // 2
+    for f in range(inf.bins):
+        blk = op.spectrum_bin(f)
+        assert np.abs(blk - ah[:, :, f]).max() < 1e-13 * np.abs(ah).max(), f
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_config_apply(gpu, name):
+    cfg = CONFIGS[name]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep)
+    o = oracle.Oracle.from_rep(rep, nthreads=0)
+    x = gen.rhs_normal(cfg.n, 1, 1234)[:, 0]
+    assert rel(op.apply(x), o.apply(x)) < MATVEC_TOL
+    b = np.asarray(rhs_for(cfg))
+    b = b[:, 0] if b.ndim == 2 else b
+    assert rel(op.apply(b), o.apply(b)) < MATVEC_TOL
+
+
+def test_c4_sampled_rows(gpu):
+    # Full-size C4 through the direct spatial oracle at sampled elements.
+    cfg = CONFIGS["C4"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep)
+    x = gen.rhs_normal(cfg.n, 1, cfg.seed)[:, 0]
+    y = op.apply(x).reshape(cfg.nx * cfg.ny, cfg.m)
+    o = oracle.Oracle.from_rep(rep, precompute=False)
+    el = [0, 63, 64 * 31 + 17, 64 * 64 - 1]
+    yr = o.apply_rows(x, el)
+    assert np.linalg.norm(y[el] - yr) / np.linalg.norm(yr) < MATVEC_TOL
+    # linearity at full size
+    w = gen.rhs_normal(cfg.n, 1, 99)[:, 0]
+    a = 0.7 - 0.2j
+    assert rel(op.apply(x + a * w), op.apply(x) + a * op.apply(w)) < 1e-13
+
+
+def test_multi_rhs_apply(gpu):
+    rep = rep_for(6, 5, 64)
+    op = ToeplitzMatvec(rep, max_nrhs=3)
+    o = oracle.Oracle.from_rep(rep)
+    X = gen.rhs_normal(o.n, 3, 5)
+    Y = op.apply(X)
+    for c in range(3):
+        assert rel(Y[:, c], o.apply(np.ascontiguousarray(X[:, c]))) < MATVEC_TOL
+
+
+def test_user_errors(gpu):
+    op = ToeplitzMatvec(rep_for(3, 3, 4))
+    with pytest.raises(UserError):
+        op.apply(np.zeros(5, complex))
+    with pytest.raises(UserError):
+        ToeplitzMatvec(ToeplitzRep(3, 3, 4, np.zeros((3, 4, 4), complex)))
+
+
+def hist_close(h_gpu, h_ref, tol):
+    assert h_gpu.shape == h_ref.shape, (h_gpu.shape, h_ref.shape)
+    assert np.array_equal(h_gpu[:, 0], h_ref[:, 0])
+    r = np.abs(h_gpu[:, 1] - h_ref[:, 1]) / np.maximum(np.abs(h_ref[:, 1]), 1e-300)
+    assert r.max() < tol, r.max()
+
+
+def test_gmres_c1_parity(gpu):
+    cfg = CONFIGS["C1"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep)
+    o = oracle.Oracle.from_rep(rep)
+    b = gen.rhs_normal(cfg.n, 1, cfg.seed)[:, 0]
+    opt = SolverOptions(tol=cfg.tol, maxIter=cfg.max_iter, restart=cfg.restart)
+    g = op.gmres(b, opt)
+    r = o.gmres(b, tol=cfg.tol, max_iter=cfg.max_iter, restart=cfg.restart)
+    assert g.converged == [1] and r["converged"] == [1]
+    assert g.iterations == r["iterations"]
+    assert rel(g.current, r["x"]) < GMRES_TOL
+    hist_close(g.history[0], r["history"][0], GMRES_TOL)
+
+
+def test_gmres_c2_budget_parity(gpu):
+    # C2 stalls under GMRES(50)+Jacobi: compare a fixed
+    # 100-iteration budget (2 restarts) history and iterate.
+    cfg = CONFIGS["C2"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep)
+    o = oracle.Oracle.from_rep(rep)
+    b = rhs_for(cfg)
+    opt = SolverOptions(tol=cfg.tol, maxIter=100, restart=cfg.restart)
+    g = op.gmres(b, opt, raise_on_fail=False)
+    r = o.gmres(b, tol=cfg.tol, max_iter=100, restart=cfg.restart)
+    assert g.iterations == r["iterations"] == [100]
+    hist_close(g.history[0], r["history"][0], GMRES_TOL)
+    assert rel(g.current, r["x"]) < GMRES_TOL
+
+
+def test_gmres_multi_column_and_a_only(gpu):
+    rep = rep_for(5, 4, 8, seed=3)
+    o = oracle.Oracle.from_rep(rep)
+    B = gen.rhs_normal(o.n, 3, 21)
+    B[:, 1] = 0.0  # zero column converges immediately (bnorm == 0)
+    op = ToeplitzMatvec(rep, max_nrhs=3)
+    for a_only in (False, True):
+        opt = SolverOptions(tol=1e-9, maxIter=500, restart=12)
+        g = op.gmres(B, opt, use_a_only=a_only)
+        r = o.gmres(B, tol=1e-9, max_iter=500, restart=12, use_a_only=a_only)
+        assert g.iterations == r["iterations"]
+        assert g.converged == r["converged"] == [1, 1, 1]
+        for c in range(3):
+            if c == 1:
+                assert not np.any(g.current[:, c])
+                continue
+            assert rel(g.current[:, c], r["x"][:, c]) < GMRES_TOL
+            hist_close(g.history[c], r["history"][c], GMRES_TOL)
+
+
+def test_gmres_nonconvergence_raises(gpu):
+    from paper_2506_04710_b200 import NumericError
+    rep = rep_for(4, 4, 8)
+    op = ToeplitzMatvec(rep)
+    b = gen.rhs_normal(op.sizeA(), 1, 3)[:, 0]
+    with pytest.raises(NumericError):
+        op.gmres(b, SolverOptions(tol=1e-15, maxIter=7, restart=3))
