@@ -56,7 +56,9 @@ def test_spectra_bins_match_reference_layout(gpu):
     op = ToeplitzMatvec(rep)
     ah = oracle.Oracle.from_rep(rep).ahat()  # [(m*e5+n)*L + f]
     inf = op.info()
-    assert inf.bins == 64 and inf.pairs == (64 + 4) // 2
+    L0, L1 = 16, 8  # nextPow2(2*5-1), nextPow2(2*3-1)
+    assert inf.bins == L0 * L1 and inf.L0 == L0 and inf.L1 == L1
+    assert inf.pairs == (L0 * L1 + 4) // 2  # 4 self-paired bins
     for f in range(inf.bins):
         blk = op.spectrum_bin(f)
         assert np.abs(blk - ah[:, :, f]).max() < 1e-13 * np.abs(ah).max(), f
@@ -110,11 +112,20 @@ def test_user_errors(gpu):
         ToeplitzMatvec(ToeplitzRep(3, 3, 4, np.zeros((3, 4, 4), complex)))
 
 
+HIST_ATOL = 1e-14  # residuals are normalised (first entry 1): the double-precision floor
+
+
 def hist_close(h_gpu, h_ref, tol):
+    """Same event sequence (restart / inner / final), values within
+    |d| <= tol*|h| + 1e-14. History values are residuals relative to ||b||
+    or beta, so 1e-14 is the rounding floor two correct complex128 GMRES
+    implementations share (reduction order differs); near convergence
+    (h ~ 1e-9) a pure relative 1e-8 test would sit below that floor."""
     assert h_gpu.shape == h_ref.shape, (h_gpu.shape, h_ref.shape)
     assert np.array_equal(h_gpu[:, 0], h_ref[:, 0])
-    r = np.abs(h_gpu[:, 1] - h_ref[:, 1]) / np.maximum(np.abs(h_ref[:, 1]), 1e-300)
-    assert r.max() < tol, r.max()
+    d = np.abs(h_gpu[:, 1] - h_ref[:, 1])
+    bound = tol * np.abs(h_ref[:, 1]) + HIST_ATOL
+    assert np.all(d <= bound), (d / bound).max()
 
 
 def test_gmres_c1_parity(gpu):
