@@ -77,7 +77,8 @@ typedef struct {
   double* residual;  /* [nrhs] final true relative residual                */
   int* converged;    /* [nrhs] 1 / 0                                       */
   double* history;   /* [nrhs][hist_cap][2] (kind, value) pairs or NULL:
-                        kind 0 restart true residual, 1 |g_{j+1}|/beta,
+                        kind 0 restart true residual, 1 |g_{j+1}|/beta_0
+                        (beta_0: first cycle's preconditioned residual),
                         2 final true residual after max_iter               */
   int* history_len;  /* [nrhs] entries produced (may exceed hist_cap)      */
   int matvecs;       /* batched operator applications issued               */

@@ -460,6 +460,7 @@ Outcome gmresColumn(const Op& op, const cvec& b, cvec& x, const cvec* invDiag,
   std::vector<cplx> cs(restart), sn(restart), g(restart + 1);
   cvec ax(n), w(n);
 
+  double beta0 = 0.0;  // history scale: first cycle's preconditioned residual
   while (out.iterations < maxIter) {
     op(x, ax);
     cvec r(n);
@@ -476,6 +477,7 @@ Outcome gmresColumn(const Op& op, const cvec& b, cvec& x, const cvec* invDiag,
       out.converged = true;
       return out;
     }
+    if (beta0 == 0.0) beta0 = beta;
     basis.assign(1, r);
     for (auto& v : basis[0]) v /= beta;
     std::fill(g.begin(), g.end(), cplx{0.0, 0.0});
@@ -515,7 +517,7 @@ Outcome gmresColumn(const Op& op, const cvec& b, cvec& x, const cvec* invDiag,
       const cplx gj = g[j];
       g[j] = cs[j] * gj;
       g[j + 1] = -std::conj(sn[j]) * gj;
-      hist.push(1.0, std::abs(g[j + 1]) / beta);
+      hist.push(1.0, std::abs(g[j + 1]) / beta0);
       if (std::abs(g[j + 1]) / beta < 0.1 * tol) {
         ++j;
         ++out.iterations;

@@ -70,7 +70,9 @@ int orc_diagonal(const orc_op* op, double* d);
  * without the throw: per column iterations / final relative residual /
  * converged flag, and a history of (kind, value) pairs:
  * kind 0 = true relative residual at a restart (linsolve.cpp:447-448),
- * kind 1 = |g_{j+1}| / beta after inner iteration (linsolve.cpp:492),
+ * kind 1 = |g_{j+1}| / beta_0 after inner iteration (linsolve.cpp:489-492;
+ *          beta_0 = first cycle's preconditioned residual, so late cycles
+ *          are not rescaled by their own small beta),
  * kind 2 = final true residual once maxIter is exhausted (linsolve.cpp:512).
  * hist has hist_cap pairs per column; hist_len gets the count per column.
  * use_a_only selects applyA as the operator (schurSolve's inner solve,

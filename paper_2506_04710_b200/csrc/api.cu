@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -97,26 +98,35 @@ void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
       }
   }
   if (dOut) *dOut = d;
-  std::vector<double2> inv(d.size());
-  for (size_t k = 0; k < d.size(); ++k) {
-    const double2 v = d[k];
-    if (std::hypot(v.x, v.y) > 0.0) {
-      // 1 / (a + bi) with Smith scaling.
-      double2 r;
-      if (std::fabs(v.x) >= std::fabs(v.y)) {
-        const double t = v.y / v.x, den = v.x + v.y * t;
-        r = make_double2(1.0 / den, -t / den);
+  auto invert = [](const std::vector<double2>& dv) {
+    std::vector<double2> inv(dv.size());
+    for (size_t k = 0; k < dv.size(); ++k) {
+      const double2 v = dv[k];
+      if (std::hypot(v.x, v.y) > 0.0) {
+        // 1 / (a + bi) with Smith scaling.
+        if (std::fabs(v.x) >= std::fabs(v.y)) {
+          const double t = v.y / v.x, den = v.x + v.y * t;
+          inv[k] = make_double2(1.0 / den, -t / den);
+        } else {
+          const double t = v.x / v.y, den = v.x * t + v.y;
+          inv[k] = make_double2(t / den, -1.0 / den);
+        }
       } else {
-        const double t = v.x / v.y, den = v.x * t + v.y;
-        r = make_double2(t / den, -1.0 / den);
+        inv[k] = make_double2(1.0, 0.0);
       }
-      inv[k] = r;
-    } else {
-      inv[k] = make_double2(1.0, 0.0);
     }
-  }
+    return inv;
+  };
+  // Full operator (iterativeSolve) and pure A (schurSolve's inner solves,
+  // linsolve.cpp:604-610): A's diagonal is aEntry(0,0,m,m) alone.
+  std::vector<double2> dA(static_cast<size_t>(c.n));
+  for (int e = 0; e < c.ne; ++e)
+    for (int a = 0; a < m; ++a) dA[static_cast<size_t>(e) * m + a] = z0[static_cast<size_t>(a) * m + a];
+  const auto inv = invert(d), invA = invert(dA);
   if (!c.dDiagInv) TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInv, c.n * sizeof(double2)));
+  if (!c.dDiagInvA) TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInvA, c.n * sizeof(double2)));
   TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInv, inv.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
+  TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInvA, invA.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
 }
 
 void requireReady(const Ctx& c) {
@@ -217,9 +227,18 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       TBT_CUDA_CHECK(cudaMalloc(&c.dTw1, c.L1 * sizeof(double2)));
       TBT_CUDA_CHECK(cudaMemcpy(c.dTw0, t0.data(), c.L0 * sizeof(double2), cudaMemcpyHostToDevice));
       TBT_CUDA_CHECK(cudaMemcpy(c.dTw1, t1.data(), c.L1 * sizeof(double2), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+      TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evFork, cudaEventDisableTiming));
+      TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evJoin, cudaEventDisableTiming));
+      c.fused2d = fft2dSupported(c.L0, c.L1);
+      const char* fenv = getenv("TBT_FFT");
+      c.forceMultiPass = fenv && std::string(fenv) == "passes";
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinB));
       c.binprodKernel = binprodVariant(c.m);
+      // K3 v2 (TMA ring) for single-RHS applies unless TBT_BINPROD=1 asks for v1.
+      const char* env = getenv("TBT_BINPROD");
+      if (c.binprodKernel > 0 && !(env && env[0] == '1')) c.binprodKernel += 10;
     } catch (...) {
       tbt_destroy(h);
       throw;
@@ -237,15 +256,19 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dAntisym), static_cast<void*>(c.dTw0), static_cast<void*>(c.dTw1),
                   static_cast<void*>(c.dCorrD), static_cast<void*>(c.dCorrU), static_cast<void*>(c.dCorrV),
                   static_cast<void*>(c.dTermInfo), static_cast<void*>(c.dTargetList),
-                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dT),
+                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dElemPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dYcorr),
+                  static_cast<void*>(c.dT),
                   static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
-                  static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv)})
+                  static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv), static_cast<void*>(c.dDiagInvA)})
     freePtr(p);
   c.dropGraph();
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);
   if (c.evBinA) cudaEventDestroy(c.evBinA);
   if (c.evBinB) cudaEventDestroy(c.evBinB);
+  if (c.evFork) cudaEventDestroy(c.evFork);
+  if (c.evJoin) cudaEventDestroy(c.evJoin);
+  if (c.side) cudaStreamDestroy(c.side);
   if (c.ownStream && c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }
@@ -301,8 +324,11 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     freePtr(c.dTargetList);
     freePtr(c.dTargetPtr);
     freePtr(c.dProj);
+    freePtr(c.dElemPtr);
+    freePtr(c.dYcorr);
+    c.dYcorr = nullptr;
     c.dCorrD = c.dCorrU = c.dCorrV = c.dProj = nullptr;
-    c.dTermInfo = c.dTargetList = c.dTargetPtr = nullptr;
+    c.dTermInfo = c.dTargetList = c.dTargetPtr = c.dElemPtr = nullptr;
     c.haveCorr = false;
     c.nTerms = c.nTargets = 0;
     c.dropGraph();
@@ -343,8 +369,9 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
           byTarget[e2].push_back({e2, e, slot, 1});  // y_e' += P^T x_e
         }
       }
-    std::vector<int> info, targets, ptr{0};
+    std::vector<int> info, targets, ptr{0}, eptr{0};
     for (int e = 0; e < c.ne; ++e) {
+      eptr.push_back(eptr.back() + static_cast<int>(byTarget[e].size()));
       if (byTarget[e].empty()) continue;
       targets.push_back(e);
       for (auto& t : byTarget[e]) info.insert(info.end(), t.begin(), t.end());
@@ -352,6 +379,8 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     }
     c.nTerms = static_cast<int>(info.size() / 4);
     c.nTargets = static_cast<int>(targets.size());
+    c.maxTermsPerTarget = 0;
+    for (size_t k = 0; k + 1 < ptr.size(); ++k) c.maxTermsPerTarget = std::max(c.maxTermsPerTarget, ptr[k + 1] - ptr[k]);
     if (c.nTerms > 0) {
       TBT_CUDA_CHECK(cudaMalloc(&c.dTermInfo, info.size() * sizeof(int)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dTargetList, targets.size() * sizeof(int)));
@@ -359,8 +388,11 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
       TBT_CUDA_CHECK(cudaMemcpy(c.dTermInfo, info.data(), info.size() * sizeof(int), cudaMemcpyHostToDevice));
       TBT_CUDA_CHECK(cudaMemcpy(c.dTargetList, targets.data(), targets.size() * sizeof(int), cudaMemcpyHostToDevice));
       TBT_CUDA_CHECK(cudaMemcpy(c.dTargetPtr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dElemPtr, eptr.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dElemPtr, eptr.data(), eptr.size() * sizeof(int), cudaMemcpyHostToDevice));
       TBT_CUDA_CHECK(cudaMalloc(&c.dProj, static_cast<size_t>(c.nTerms) * c.maxNrhs * std::max(rank, 1) *
                                               sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dYcorr, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
     }
     c.haveCorr = true;
     if (c.havePrecompute) refreshDiagonal(c, nullptr);

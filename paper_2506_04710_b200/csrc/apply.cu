@@ -42,7 +42,76 @@ void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool t
   TBT_CUDA_CHECK(cudaGetLastError());
 }
 
+namespace {
+
+void binProductTimed(Ctx& c, int nrhs) {
+  cudaStream_t s = c.stream;
+  if (c.timeBinprod) {
+    if (c.tCount == static_cast<int>(c.tEvA.size())) {
+      cudaEvent_t a, b;
+      TBT_CUDA_CHECK(cudaEventCreate(&a));
+      TBT_CUDA_CHECK(cudaEventCreate(&b));
+      c.tEvA.push_back(a);
+      c.tEvB.push_back(b);
+    }
+    TBT_CUDA_CHECK(cudaEventRecord(c.tEvA[c.tCount], s));
+    launchBinProduct(c, nrhs);
+    TBT_CUDA_CHECK(cudaEventRecord(c.tEvB[c.tCount], s));
+    ++c.tCount;
+  } else {
+    launchBinProduct(c, nrhs);
+  }
+}
+
+// K2 -> K3 -> K4 with the cluster-fused transforms; the correction's rank-r
+// projections run in a parallel branch (side stream) joined before K4.
+bool applyFused(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
+  const int B = nrhs * c.m;
+  int CL = 1, BC = 16;
+  fft2dPlan(c.L0, c.L1, c.nx, c.ny, B, smCount(c.device), &CL, &BC);
+  const bool corr = withCorr && c.haveCorr && c.nTerms > 0;
+  const bool proj = corr;
+  if (proj) {
+    TBT_CUDA_CHECK(cudaEventRecord(c.evFork, c.stream));
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(c.side, c.evFork, 0));
+    launchCorrVector(c, x, c.dYcorr, nrhs, c.side);
+    TBT_CUDA_CHECK(cudaEventRecord(c.evJoin, c.side));
+  }
+  Fft2dArgs f;
+  f.in = x;
+  f.out = c.dXhat;
+  f.nx = c.nx;
+  f.ny = c.ny;
+  f.L0 = c.L0;
+  f.L1 = c.L1;
+  f.B = B;
+  f.tw0 = c.dTw0;
+  f.tw1 = c.dTw1;
+  if (!launchFft2d(f, CL, BC, false, c.stream)) {
+    if (proj) TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.evJoin, 0));
+    return false;
+  }
+  binProductTimed(c, nrhs);
+  if (proj) TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.evJoin, 0));
+  Fft2dArgs iv = f;
+  iv.in = c.dYhat;
+  iv.out = y;
+  iv.scale = 1.0 / static_cast<double>(c.L);
+  if (corr) {
+    iv.corr = 1;
+    iv.tPtr = c.dElemPtr;
+    iv.ycorr = c.dYcorr;
+  }
+  if (!launchFft2d(iv, CL, BC, true, c.stream)) throw Error{TBT_CUDA_ERROR, "inverse 2-D transform launch"};
+  TBT_CUDA_CHECK(cudaGetLastError());
+  launchAntisym(c, x, y, nrhs);
+  return true;
+}
+
+}  // namespace
+
 void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
+  if (c.fused2d && !c.forceMultiPass && applyFused(c, x, y, nrhs, withCorr)) return;
   const long long B = static_cast<long long>(nrhs) * c.m;
   cudaStream_t s = c.stream;
 
@@ -76,21 +145,7 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
   fb.tw = c.dTw1;
   launchFftPass(fb, s);
 
-  if (c.timeBinprod) {
-    if (c.tCount == static_cast<int>(c.tEvA.size())) {
-      cudaEvent_t a, b;
-      TBT_CUDA_CHECK(cudaEventCreate(&a));
-      TBT_CUDA_CHECK(cudaEventCreate(&b));
-      c.tEvA.push_back(a);
-      c.tEvB.push_back(b);
-    }
-    TBT_CUDA_CHECK(cudaEventRecord(c.tEvA[c.tCount], s));
-    launchBinProduct(c, nrhs);
-    TBT_CUDA_CHECK(cudaEventRecord(c.tEvB[c.tCount], s));
-    ++c.tCount;
-  } else {
-    launchBinProduct(c, nrhs);
-  }
+  binProductTimed(c, nrhs);
 
   FftPass ib;  // inverse, level 1: keep the ny element rows
   ib.in = c.dYhat;

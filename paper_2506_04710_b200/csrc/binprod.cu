@@ -17,6 +17,7 @@
 // (16-byte streaming loads, evict-first) and feeds 2 complex MACs.
 #include <algorithm>
 
+#include "ptx.cuh"
 #include "tbt_internal.cuh"
 
 namespace tbt {
@@ -134,6 +135,154 @@ binprodGeneric(const double2* __restrict__ S, const int* __restrict__ pairF, con
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K3 v2 (single RHS): persistent, warp-specialised, TMA-engine ring.
+// One producer warp streams each (pair, row-chunk) of the spectrum plus the
+// matching xhat segments into a STAGES-deep shared-memory ring with
+// cp.async.bulk (evict-first L2 policy for the spectrum, evict-last for the
+// vectors); eight consumer warps compute from shared memory and release the
+// slot as soon as their operands are in registers. One CTA per SM.
+template <int M, int TC, int RCH, int STAGES>
+struct RingCfg {
+  static constexpr int NT = 256;
+  static constexpr int TRN = NT / TC;
+  static constexpr int CPT = M / TC;
+  static constexpr int RPT = RCH / TRN;
+  static constexpr int NCH = M / RCH;
+  static constexpr uint32_t CHUNK = RCH * M * 16;
+  static constexpr uint32_t XF = M * 16;
+  static constexpr uint32_t XG = RCH * 16;
+  static constexpr uint32_t STAGE = CHUNK + XF + XG;
+  static constexpr uint32_t RED = 2 * (NT / 32) * M * 16;
+  static constexpr uint32_t SMEM = STAGES * STAGE + RED + 2 * STAGES * 8;
+  static_assert(M % TC == 0 && RCH % TRN == 0 && M % RCH == 0 && STAGE % 16 == 0, "ring tile");
+};
+
+template <int M, int TC, int RCH, int STAGES>
+__global__ void __launch_bounds__(288, 1)
+binprodRing(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
+            long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat) {
+  using C = RingCfg<M, TC, RCH, STAGES>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double2* red = reinterpret_cast<double2*>(smem + STAGES * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + C::RED);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbarInit(full + s, 1);
+      mbarInit(empty + s, C::NT / 32);
+    }
+    fenceBarrierInit();
+  }
+  __syncthreads();
+  if (blockIdx.x >= npairs) return;
+  const long long mine = (npairs - 1 - blockIdx.x) / gridDim.x + 1;
+  const long long total = mine * C::NCH;
+
+  if (warp == C::NT / 32) {  // producer warp
+    if (lane == 0) {
+      const uint64_t polS = policyEvictFirst();
+      const uint64_t polX = policyEvictLast();
+      for (long long it = 0; it < total; ++it) {
+        const int s = static_cast<int>(it % STAGES);
+        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+        const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+        const int ch = static_cast<int>(it % C::NCH);
+        const long long f = pairF[p], g = pairG[p];
+        mbarWait(empty + s, ph ^ 1u);
+        unsigned char* st = smem + s * C::STAGE;
+        mbarArriveExpectTx(full + s, C::STAGE);
+        bulkG2S(st, S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + s, polS);
+        bulkG2S(st + C::CHUNK, xhat + f * M, C::XF, full + s, polX);
+        bulkG2S(st + C::CHUNK + C::XF, xhat + g * M + ch * RCH, C::XG, full + s, polX);
+      }
+    }
+    return;
+  }
+
+  const int tc = threadIdx.x % TC, tr = threadIdx.x / TC;
+  double2 yga[C::CPT];
+  for (long long it = 0; it < total; ++it) {
+    const int s = static_cast<int>(it % STAGES);
+    const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+    const long long pi = it / C::NCH;
+    const int ch = static_cast<int>(it % C::NCH);
+    const long long p = blockIdx.x + pi * gridDim.x;
+    if (ch == 0) {
+#pragma unroll
+      for (int j = 0; j < C::CPT; ++j) yga[j] = make_double2(0.0, 0.0);
+    }
+    mbarWait(full + s, ph);
+    const double2* A = reinterpret_cast<const double2*>(smem + s * C::STAGE);
+    const double2* xf = A + RCH * M;
+    const double2* xg = xf + M;
+    double2 a[C::RPT][C::CPT], xfr[C::CPT], xgv[C::RPT];
+#pragma unroll
+    for (int j = 0; j < C::CPT; ++j) xfr[j] = xf[tc + TC * j];
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) {
+      xgv[i] = xg[tr + C::TRN * i];
+#pragma unroll
+      for (int j = 0; j < C::CPT; ++j) a[i][j] = A[(tr + C::TRN * i) * M + tc + TC * j];
+    }
+    __syncwarp();
+    if (lane == 0) mbarArrive(empty + s);  // slot free: operands are in registers
+
+    const long long f = pairF[p], g = pairG[p];
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < C::CPT; ++j) cfma(acc, a[i][j], xfr[j]);
+#pragma unroll
+      for (int off = TC / 2; off >= 1; off >>= 1) acc = cadd(acc, shflXor(acc, off));
+      if (tc == 0) yhat[f * M + ch * RCH + tr + C::TRN * i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < C::RPT; ++i)
+#pragma unroll
+      for (int j = 0; j < C::CPT; ++j) cfma(yga[j], a[i][j], xgv[i]);
+
+    if (ch == C::NCH - 1) {
+      if (TC == 16) {
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) yga[j] = cadd(yga[j], shflXor(yga[j], 16));
+      }
+      double2* rb = red + (pi & 1) * (C::NT / 32) * M;
+      if (lane < TC) {
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) rb[warp * M + tc + TC * j] = yga[j];
+      }
+      namedBarrier(1, C::NT);
+      if (f != g) {
+        for (int q = threadIdx.x; q < M; q += C::NT) {
+          double2 acc = rb[q];
+#pragma unroll
+          for (int w = 1; w < C::NT / 32; ++w) acc = cadd(acc, rb[w * M + q]);
+          yhat[g * M + q] = acc;
+        }
+      }
+    }
+  }
+}
+
+template <int M, int TC, int RCH, int STAGES>
+void launchRing(Ctx& c) {
+  using C = RingCfg<M, TC, RCH, STAGES>;
+  static bool attrSet = false;
+  if (!attrSet) {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodRing<M, TC, RCH, STAGES>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attrSet = true;
+  }
+  const int sms = smCount(c.device);
+  const int grid = static_cast<int>(std::min<long long>(c.npairs, sms));
+  binprodRing<M, TC, RCH, STAGES><<<grid, C::NT + 32, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,
+                                                                          c.dXhat, c.dYhat);
+}
+
 template <int M, int TC, int RCH>
 void launchTile(Ctx& c, int nrhs) {
   const int sms = smCount(c.device);
@@ -154,6 +303,15 @@ int binprodVariant(int m) {
 }
 
 void launchBinProduct(Ctx& c, int nrhs) {
+  if (nrhs == 1 && c.binprodKernel >= 11) {
+    switch (c.binprodKernel) {
+      case 11: launchRing<64, 16, 64, 3>(c); break;
+      case 12: launchRing<128, 32, 16, 4>(c); break;
+      case 13: launchRing<192, 32, 16, 3>(c); break;
+    }
+    TBT_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   switch (binprodVariant(c.m)) {
     case 1: launchTile<64, 16, 64>(c, nrhs); break;
     case 2: launchTile<128, 32, 32>(c, nrhs); break;

@@ -8,6 +8,8 @@
 //    as a rank-r projection pass plus a per-target accumulation pass;
 //  * the antisymmetric part K of Z(0,0) (see spectra.cu): y_e += K x_e.
 // Internal vector layout is [element][rhs][basis].
+#include <algorithm>
+
 #include "tbt_internal.cuh"
 
 namespace tbt {
@@ -60,6 +62,48 @@ __global__ void corrApply(const int* __restrict__ termInfo, const int* __restric
   }
 }
 
+// One CTA per (target element, rhs): the rank-r projections of all the
+// target's terms (one warp per term) into shared memory, then
+// ycorr[e][rhs][a] = sum_t diag(d_t) x_src + W2_t proj_t. Depends on x only,
+// so it runs in a parallel branch beside the transforms and the bin product.
+__global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInfo, const int* __restrict__ targetList,
+                                                 const int* __restrict__ targetPtr, const double2* __restrict__ D,
+                                                 const double2* __restrict__ U, const double2* __restrict__ V,
+                                                 const double2* __restrict__ x, double2* __restrict__ ycorr, int m,
+                                                 int rank, int nrhs) {
+  extern __shared__ double2 sproj[];  // [terms of this target][rank]
+  const int ti = blockIdx.x, rhs = blockIdx.y;
+  const int e = targetList[ti];
+  const int t0 = targetPtr[ti], t1 = targetPtr[ti + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = t0 + warp; t < t1; t += blockDim.x / 32) {
+    const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+    const double2* W = (trans ? U : V) + static_cast<long long>(slot) * rank * m;
+    const double2* xs = x + (static_cast<long long>(src) * nrhs + rhs) * m;
+    for (int q = 0; q < rank; ++q) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int a = lane; a < m; a += 32) cfma(s, __ldg(W + static_cast<long long>(q) * m + a), __ldg(xs + a));
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+      }
+      if (lane == 0) sproj[(t - t0) * rank + q] = s;
+    }
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int t = t0; t < t1; ++t) {
+      const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+      cfma(acc, __ldg(D + static_cast<long long>(slot) * m + a), __ldg(x + (static_cast<long long>(src) * nrhs + rhs) * m + a));
+      const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * rank * m + a;
+      for (int q = 0; q < rank; ++q) cfma(acc, __ldg(W2 + static_cast<long long>(q) * m), sproj[(t - t0) * rank + q]);
+    }
+    ycorr[(static_cast<long long>(e) * nrhs + rhs) * m + a] = acc;
+  }
+}
+
 // y[e][rhs][a] += sum_b K[a][b] x[e][rhs][b].
 __global__ void antisymApply(const double2* __restrict__ K, const double2* __restrict__ x, double2* __restrict__ y,
                              int m, int nrhs) {
@@ -75,6 +119,15 @@ __global__ void antisymApply(const double2* __restrict__ K, const double2* __res
 }
 
 }  // namespace
+
+void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
+  if (!c.haveCorr || c.nTerms == 0) return;
+  dim3 grid(c.nTargets, nrhs);
+  const size_t smem = static_cast<size_t>(c.maxTermsPerTarget) * std::max(c.rank, 1) * sizeof(double2);
+  corrFused<<<grid, 256, smem, s>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr,
+                                    c.m, c.rank, nrhs);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
 
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs) {
   if (!c.haveCorr || c.nTerms == 0) return;

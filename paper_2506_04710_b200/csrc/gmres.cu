@@ -102,6 +102,12 @@ __device__ double2 gridTotal(const double2* part, double2* scratch) {
   return r;
 }
 
+// Per-CTA partials are double-buffered by barrier parity: a CTA may write
+// the next phase's partial while slower CTAs still sum the previous one.
+__device__ __forceinline__ double2* partSlot(const GmresArgs& A, int phase, int col) {
+  return A.partial + (static_cast<long long>(phase & 1) * A.ncols + col) * gridDim.x;
+}
+
 __device__ __forceinline__ long long slotIndex(long long s, int col, int ncols, int m) {
   const long long e = s / m, a = s % m;
   return (e * ncols + col) * m + a;
@@ -140,15 +146,16 @@ __global__ void __launch_bounds__(kThreads) gmresInit(GmresArgs A) {
       acc.x += v.x * v.x + v.y * v.y;
     }
     const double2 t = blockSum(acc, scratch);
-    if (threadIdx.x == 0) A.partial[static_cast<long long>(col) * gridDim.x + blockIdx.x] = t;
+    if (threadIdx.x == 0) partSlot(A, 0, col)[blockIdx.x] = t;
   }
   gridBarrier(A.bar);
   for (int col = 0; col < A.ncols; ++col) {
-    const double2 tot = gridTotal(A.partial + static_cast<long long>(col) * gridDim.x, scratch);
+    const double2 tot = gridTotal(partSlot(A, 0, col), scratch);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       GmresState& st = A.st[col];
       st.bnorm = sqrt(tot.x);
       st.beta = 0.0;
+      st.beta0 = 0.0;
       st.residual = 0.0;
       st.iterations = 0;
       st.ncount = 0;
@@ -180,13 +187,13 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
         acc.x += r.x * r.x + r.y * r.y;
       }
     const double2 t = blockSum(acc, scratch);
-    if (threadIdx.x == 0) A.partial[static_cast<long long>(col) * gridDim.x + blockIdx.x] = t;
+    if (threadIdx.x == 0) partSlot(A, 0, col)[blockIdx.x] = t;
   }
   gridBarrier(A.bar);
   const long long nall = slots * A.ncols;
   for (int col = 0; col < A.ncols; ++col) {
     if (!sFlag[col]) continue;
-    const double2 tot = gridTotal(A.partial + static_cast<long long>(col) * gridDim.x, scratch);
+    const double2 tot = gridTotal(partSlot(A, 0, col), scratch);
     const double bnorm = A.st[col].bnorm;
     const double res = sqrt(tot.x) / bnorm;
     int decision = 0;  // 0 run, 1 converged, 2 out of iterations
@@ -218,12 +225,12 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
         acc.x += z.x * z.x + z.y * z.y;
       }
     const double2 t = blockSum(acc, scratch);
-    if (threadIdx.x == 0) A.partial[static_cast<long long>(col) * gridDim.x + blockIdx.x] = t;
+    if (threadIdx.x == 0) partSlot(A, 1, col)[blockIdx.x] = t;
   }
   gridBarrier(A.bar);
   for (int col = 0; col < A.ncols; ++col) {
     if (!sFlag[col]) continue;
-    const double2 tot = gridTotal(A.partial + static_cast<long long>(col) * gridDim.x, scratch);
+    const double2 tot = gridTotal(partSlot(A, 1, col), scratch);
     const double beta = sqrt(tot.x);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       GmresState& st = A.st[col];
@@ -234,6 +241,7 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
         st.stopInner = 1;
       } else {
         st.beta = beta;
+        if (st.beta0 == 0.0) st.beta0 = beta;
         st.ncount = 0;
         st.stopInner = 0;
         st.cycleActive = 1;
@@ -275,13 +283,13 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
         cfma_conj(acc, A.V[q], wv);
       }
     const double2 t = blockSum(acc, scratch);
-    if (threadIdx.x == 0) A.partial[static_cast<long long>(col) * gridDim.x + blockIdx.x] = t;
+    if (threadIdx.x == 0) partSlot(A, 0, col)[blockIdx.x] = t;
   }
   gridBarrier(A.bar);
   for (int i = 0; i <= j; ++i) {
     for (int col = 0; col < A.ncols; ++col) {
       if (!sFlag[col]) continue;
-      const double2 h = gridTotal(A.partial + static_cast<long long>(col) * gridDim.x, scratch);
+      const double2 h = gridTotal(partSlot(A, i, col), scratch);
       if (blockIdx.x == 0 && threadIdx.x == 0) A.H[static_cast<long long>(col) * ldh * A.restart + i + j * ldh] = h;
       const double2* vi = A.V + static_cast<long long>(i) * nall;
       const double2* vn = A.V + static_cast<long long>(i + 1) * nall;
@@ -297,13 +305,13 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
           acc.x += wv.x * wv.x + wv.y * wv.y;
       }
       const double2 t = blockSum(acc, scratch);
-      if (threadIdx.x == 0) A.partial[static_cast<long long>(col) * gridDim.x + blockIdx.x] = t;
+      if (threadIdx.x == 0) partSlot(A, i + 1, col)[blockIdx.x] = t;
     }
     gridBarrier(A.bar);
   }
   for (int col = 0; col < A.ncols; ++col) {
     if (!sFlag[col]) continue;
-    const double2 tot = gridTotal(A.partial + static_cast<long long>(col) * gridDim.x, scratch);
+    const double2 tot = gridTotal(partSlot(A, j + 1, col), scratch);
     const double hn = sqrt(tot.x);
     if (hn > 0.0) {
       double2* vn = A.V + static_cast<long long>(j + 1) * nall;
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
     st.iterations += 1;
     st.ncount = j + 1;
     const double rel = cabs2(g[j + 1]) / st.beta;
-    pushHist(A, col, 1.0, rel);
+    pushHist(A, col, 1.0, cabs2(g[j + 1]) / st.beta0);
     if (rel < 0.1 * A.tol || !(hn > 0.0) || st.ncount >= A.restart || st.iterations >= A.maxIter) st.stopInner = 1;
   }
 }
@@ -440,7 +448,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     A.sn = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
     A.ycoef = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
     A.hist = static_cast<double*>(dalloc(sizeof(double) * 2 * ncols * std::max(1, A.histCap)));
-    A.partial = static_cast<double2*>(dalloc(sizeof(double2) * ncols * grid));
+    A.partial = static_cast<double2*>(dalloc(sizeof(double2) * 2 * ncols * grid));
     A.bar = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 2));
     A.b = b;
     A.x = x;
@@ -452,7 +460,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     TBT_CUDA_CHECK(cudaMemsetAsync(A.V, 0, sizeof(double2) * nall * (R + 1), s));
     TBT_CUDA_CHECK(cudaMemsetAsync(A.H, 0, sizeof(double2) * ncols * (R + 1) * R, s));
     TBT_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * nall, s));
-    A.dinv = o.precondition ? c.dDiagInv : nullptr;
+    A.dinv = o.precondition ? (useAOnly ? c.dDiagInvA : c.dDiagInv) : nullptr;
     const size_t smem = sizeof(int) * ncols;
 
     matvecs = 0;

@@ -71,6 +71,23 @@ struct FftPass {
 };
 void launchFftPass(const FftPass& p, cudaStream_t s);
 
+// Cluster-fused 2-D transform (fft2d.cu).
+struct Fft2dArgs {
+  const double2* in = nullptr;
+  double2* out = nullptr;
+  int nx = 0, ny = 0, L0 = 1, L1 = 1, B = 0;
+  const double2* tw0 = nullptr;
+  const double2* tw1 = nullptr;
+  double scale = 1.0;
+  // Inverse-transform epilogue: edge/corner correction (correction.cu).
+  int corr = 0;
+  const int* tPtr = nullptr;       // [ne+1] terms of element e (non-empty -> add ycorr)
+  const double2* ycorr = nullptr;  // [e][B] correction vector (launchCorrVector)
+};
+bool fft2dSupported(int L0, int L1);
+void fft2dPlan(int L0, int L1, int nx, int ny, int B, int sms, int* CL, int* BC);
+bool launchFft2d(const Fft2dArgs& a, int CL, int BC, bool inverse, cudaStream_t s);
+
 // ---------------------------------------------------------------- context
 struct CorrTerm {  // y[target] += P x[source] (trans 0) or P^T x[source]
   int target, source, slot, trans;
@@ -83,6 +100,10 @@ struct Ctx {
   long long L = 1;
   cudaStream_t stream = nullptr;
   bool ownStream = false;
+  cudaStream_t side = nullptr;             // parallel branch (correction projection)
+  cudaEvent_t evFork = nullptr, evJoin = nullptr;
+  bool fused2d = false;                    // cluster-fused 2-D transforms available
+  bool forceMultiPass = false;             // TBT_FFT=passes
 
   // Generators (host copy kept for diagonal / K) and spectra.
   std::vector<double2> genHost;
@@ -107,10 +128,12 @@ struct Ctx {
   double2* dCorrU = nullptr;  // [40][rank][m]
   double2* dCorrV = nullptr;
   std::vector<double2> corrDHost;
-  int nTerms = 0, nTargets = 0;
+  int nTerms = 0, nTargets = 0, maxTermsPerTarget = 0;
+  double2* dYcorr = nullptr;    // [ne][maxNrhs*m] correction vector
   int* dTermInfo = nullptr;     // [nTerms][4] {target, source, slot, trans}
   int* dTargetList = nullptr;   // [nTargets] target elements
   int* dTargetPtr = nullptr;    // [nTargets+1] CSR over terms
+  int* dElemPtr = nullptr;      // [ne+1] CSR over terms by element
   double2* dProj = nullptr;     // [nTerms][nrhs][rank]
 
   // Work buffers sized for maxNrhs.
@@ -119,7 +142,8 @@ struct Ctx {
   double2* dYhat = nullptr;   // [L][B]
   double2* dXin = nullptr;    // [ne][B] staging (host/colmajor input)
   double2* dYout = nullptr;   // [ne][B]
-  double2* dDiagInv = nullptr;
+  double2* dDiagInv = nullptr;   // 1/diag(Z), Jacobi of iterativeSolve
+  double2* dDiagInvA = nullptr;  // 1/diag(A), Jacobi of the A-only solves
 
   // Timing hooks: event pairs around K3, one per timed apply.
   cudaEvent_t evBinA = nullptr, evBinB = nullptr;
@@ -146,12 +170,13 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 int binprodVariant(int m);                                    // binprod.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
+void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
 void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs);     // correction.cu
 void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s, int m);  // apply.cu
 
 // GMRES (gmres.cu): per-column state mirrored to the host.
 struct GmresState {
-  double bnorm, beta, residual;
+  double bnorm, beta, residual, beta0;
   int iterations, ncount, stopInner, done, converged, cycleActive, histLen, pad;
 };
 void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres_opts& o, bool useAOnly,

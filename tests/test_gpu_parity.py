@@ -94,14 +94,39 @@ def test_c4_sampled_rows(gpu):
     assert rel(op.apply(x + a * w), op.apply(x) + a * op.apply(w)) < 1e-13
 
 
-def test_multi_rhs_apply(gpu):
-    rep = rep_for(6, 5, 64)
-    op = ToeplitzMatvec(rep, max_nrhs=3)
+@pytest.fixture(params=["fused", "passes"])
+def fft_path(request, monkeypatch):
+    """Both transform paths: cluster-fused 2-D kernels and 1-D line passes."""
+    if request.param == "passes":
+        monkeypatch.setenv("TBT_FFT", "passes")
+    else:
+        monkeypatch.delenv("TBT_FFT", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("nx,ny,m,k", [(6, 5, 64, 3), (5, 4, 8, 3), (4, 4, 24, 2), (9, 5, 128, 2), (3, 5, 7, 4)])
+def test_multi_rhs_apply(gpu, fft_path, nx, ny, m, k):
+    rep = rep_for(nx, ny, m)
+    op = ToeplitzMatvec(rep, max_nrhs=k)
     o = oracle.Oracle.from_rep(rep)
-    X = gen.rhs_normal(o.n, 3, 5)
+    X = gen.rhs_normal(o.n, k, 5)
     Y = op.apply(X)
-    for c in range(3):
-        assert rel(Y[:, c], o.apply(np.ascontiguousarray(X[:, c]))) < MATVEC_TOL
+    Ya = op.applyA(X)
+    for c in range(k):
+        xc = np.ascontiguousarray(X[:, c])
+        assert rel(Y[:, c], o.apply(xc)) < MATVEC_TOL
+        assert rel(Ya[:, c], o.applyA(xc)) < MATVEC_TOL
+
+
+def test_gmres_single_column_small(gpu, fft_path):
+    rep = rep_for(5, 4, 8, seed=3)
+    o = oracle.Oracle.from_rep(rep)
+    b = gen.rhs_normal(o.n, 1, 21)[:, 0]
+    op = ToeplitzMatvec(rep)
+    g = op.gmres(b, SolverOptions(tol=1e-9, maxIter=500, restart=12))
+    r = o.gmres(b, tol=1e-9, max_iter=500, restart=12)
+    assert g.iterations == r["iterations"]
+    hist_close(g.history[0], r["history"][0], GMRES_TOL)
 
 
 def test_user_errors(gpu):
@@ -159,7 +184,7 @@ def test_gmres_c2_budget_parity(gpu):
     assert rel(g.current, r["x"]) < GMRES_TOL
 
 
-def test_gmres_multi_column_and_a_only(gpu):
+def test_gmres_multi_column_and_a_only(gpu, fft_path):
     rep = rep_for(5, 4, 8, seed=3)
     o = oracle.Oracle.from_rep(rep)
     B = gen.rhs_normal(o.n, 3, 21)
