@@ -137,6 +137,8 @@ typedef struct {
   int binprod_kernel;          /* K3 variant id                           */
   int kernels_per_apply;       /* launches of one tbt_apply (nrhs = 1)    */
   int has_antisym;             /* Z(0,0) not symmetric: block-diag fixup  */
+  int apply_path;              /* 2 persistent single kernel, 1 cluster-fused
+                                  transforms, 0 line passes                */
 } tbt_info;
 tbt_status tbt_get_info(const tbt_ctx* ctx, tbt_info* info);
 
@@ -151,6 +153,15 @@ tbt_status tbt_get_spectrum_bin(tbt_ctx* ctx, long long f, double* out);
  * summed K3 milliseconds and the number of timed launches since enabling. */
 tbt_status tbt_set_timing(tbt_ctx* ctx, int on);
 tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
+
+/* Phase timing of the persistent single-kernel apply: `on` arms
+ * %globaltimer stamps (CTA 0) at its phase boundaries for later applies;
+ * out_us (may be NULL) receives the phases of the last armed apply:
+ * [0] row FFTs + correction, [1] column FFTs, [2] bin products,
+ * [3] inverse column FFTs, [4] inverse row FFTs (microseconds);
+ * [5..8] latest and [9..12] earliest CTA arrival at barriers 0..3, relative
+ * to the start of the phase the barrier ends. out_us holds 13 doubles. */
+tbt_status tbt_phase_times(tbt_ctx* ctx, int on, double* out_us);
 
 /* Times `iters` back-to-back device-resident applies (nrhs columns) with
  * CUDA events on the context stream; out_ms = mean ms per apply and

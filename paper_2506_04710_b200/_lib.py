@@ -37,7 +37,7 @@ class TbtInfo(C.Structure):
     _fields_ = [("n", C.c_longlong), ("bins", C.c_longlong), ("pairs", C.c_longlong),
                 ("L0", C.c_int), ("L1", C.c_int), ("spectra_bytes", C.c_longlong),
                 ("binprod_kernel", C.c_int), ("kernels_per_apply", C.c_int),
-                ("has_antisym", C.c_int)]
+                ("has_antisym", C.c_int), ("apply_path", C.c_int)]
 
 
 # name -> (restype, argtypes); the exported C ABI of tbt.h and tbt_gen.h.
@@ -60,6 +60,7 @@ SIGNATURES = {
     "tbt_get_spectrum_bin": (C.c_int, [C.c_void_p, C.c_longlong, dp]),
     "tbt_bench_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, dp, dp]),
     "tbt_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "tbt_phase_times": (C.c_int, [C.c_void_p, C.c_int, dp]),
     "tbt_timing_read": (C.c_int, [C.c_void_p, dp, ip]),
     "tbtgen_num_blocks": (C.c_longlong, [C.c_int, C.c_int]),
     "tbtgen_block_shift": (C.c_int, [C.c_int, C.c_int, C.c_longlong, ip, ip]),

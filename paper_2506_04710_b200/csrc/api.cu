@@ -231,6 +231,19 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evFork, cudaEventDisableTiming));
       TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evJoin, cudaEventDisableTiming));
       c.fused2d = fft2dSupported(c.L0, c.L1);
+      TBT_CUDA_CHECK(cudaMalloc(&c.dGridBar, 2 * sizeof(unsigned)));
+      TBT_CUDA_CHECK(cudaMemset(c.dGridBar, 0, 2 * sizeof(unsigned)));
+      {
+        const size_t nfl = (2 * static_cast<size_t>(smCount(c.device)) + 1) * 16;
+        TBT_CUDA_CHECK(cudaMalloc(&c.dBarFlags, nfl * sizeof(unsigned long long)));
+        TBT_CUDA_CHECK(cudaMemset(c.dBarFlags, 0, nfl * sizeof(unsigned long long)));
+      }
+      TBT_CUDA_CHECK(cudaMalloc(&c.dPhaseNs, 32 * sizeof(unsigned long long)));
+      TBT_CUDA_CHECK(cudaMemset(c.dPhaseNs, 0, 32 * sizeof(unsigned long long)));
+      const char* aenv = getenv("TBT_APPLY");
+      c.persistent = !(aenv && std::string(aenv) == "multi");
+      const char* penv = getenv("TBT_PREFETCH");
+      if (penv) c.prefetchAt = std::max(0, std::min(2, atoi(penv)));
       const char* fenv = getenv("TBT_FFT");
       c.forceMultiPass = fenv && std::string(fenv) == "passes";
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
@@ -256,10 +269,12 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dAntisym), static_cast<void*>(c.dTw0), static_cast<void*>(c.dTw1),
                   static_cast<void*>(c.dCorrD), static_cast<void*>(c.dCorrU), static_cast<void*>(c.dCorrV),
                   static_cast<void*>(c.dTermInfo), static_cast<void*>(c.dTargetList),
-                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dElemPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dYcorr),
+                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dElemPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dYcorr), static_cast<void*>(c.dTermVec),
+                  static_cast<void*>(c.dPairInfo), static_cast<void*>(c.dPairTargetPtr),
                   static_cast<void*>(c.dT),
                   static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
-                  static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv), static_cast<void*>(c.dDiagInvA)})
+                  static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv), static_cast<void*>(c.dDiagInvA),
+                  static_cast<void*>(c.dGridBar), static_cast<void*>(c.dPhaseNs), static_cast<void*>(c.dBarFlags)})
     freePtr(p);
   c.dropGraph();
   for (auto e : c.tEvA) cudaEventDestroy(e);
@@ -326,7 +341,13 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     freePtr(c.dProj);
     freePtr(c.dElemPtr);
     freePtr(c.dYcorr);
+    freePtr(c.dTermVec);
+    freePtr(c.dPairInfo);
+    freePtr(c.dPairTargetPtr);
     c.dYcorr = nullptr;
+    c.dTermVec = nullptr;
+    c.dPairInfo = c.dPairTargetPtr = nullptr;
+    c.nCorrPairs = 0;
     c.dCorrD = c.dCorrU = c.dCorrV = c.dProj = nullptr;
     c.dTermInfo = c.dTargetList = c.dTargetPtr = c.dElemPtr = nullptr;
     c.haveCorr = false;
@@ -393,6 +414,31 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
       TBT_CUDA_CHECK(cudaMalloc(&c.dProj, static_cast<size_t>(c.nTerms) * c.maxNrhs * std::max(rank, 1) *
                                               sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dYcorr, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMemset(c.dYcorr, 0, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
+      // (target, source) pairs: terms of one target grouped by source.
+      std::vector<int> pinfo, pptr{0};
+      for (int e : targets) {
+        std::vector<std::array<int, 4>> mine;
+        for (auto& t : byTarget[e]) {
+          const int code = t[2] * 2 + t[3];
+          bool merged = false;
+          for (auto& q : mine)
+            if (q[1] == t[1] && q[3] < 0) {
+              q[3] = code;
+              merged = true;
+              break;
+            }
+          if (!merged) mine.push_back({e, t[1], code, -1});
+        }
+        for (auto& q : mine) pinfo.insert(pinfo.end(), q.begin(), q.end());
+        pptr.push_back(static_cast<int>(pinfo.size() / 4));
+      }
+      c.nCorrPairs = static_cast<int>(pinfo.size() / 4);
+      TBT_CUDA_CHECK(cudaMalloc(&c.dPairInfo, pinfo.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dPairTargetPtr, pptr.size() * sizeof(int)));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dPairInfo, pinfo.data(), pinfo.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMemcpy(c.dPairTargetPtr, pptr.data(), pptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      TBT_CUDA_CHECK(cudaMalloc(&c.dTermVec, static_cast<size_t>(c.nCorrPairs) * c.m * sizeof(double2)));
     }
     c.haveCorr = true;
     if (c.havePrecompute) refreshDiagonal(c, nullptr);
@@ -551,7 +597,12 @@ tbt_status tbt_get_info(const tbt_ctx* h, tbt_info* info) {
     info->L1 = c.L1;
     info->spectra_bytes = c.npairs * static_cast<long long>(c.m) * c.m * 16;
     info->binprod_kernel = c.binprodKernel;
-    info->kernels_per_apply = 5 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? (c.rank > 0 ? 2 : 1) : 0);
+    const bool pers = c.persistent && persistentSupported(c);
+    const bool fused = !pers && c.fused2d && !c.forceMultiPass;
+    info->kernels_per_apply = pers ? 1
+                              : fused ? 3 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? 1 : 0)
+                                      : 5 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? (c.rank > 0 ? 2 : 1) : 0);
+    info->apply_path = pers ? 2 : (fused ? 1 : 0);
     info->has_antisym = c.hasAntisym ? 1 : 0;
   });
 }
@@ -598,6 +649,31 @@ tbt_status tbt_timing_read(tbt_ctx* h, double* total, int* count) {
     }
     *total = sum;
     *count = c.tCount;
+  });
+}
+
+tbt_status tbt_phase_times(tbt_ctx* h, int on, double* out_us) {
+  return guarded([&] {
+    TBT_USER_CHECK(h, "tbt_phase_times: null context");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.dropGraph();
+    if (out_us) {
+      unsigned long long ns[32];
+      TBT_CUDA_CHECK(cudaMemcpy(ns, c.dPhaseNs, sizeof(ns), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < 5; ++k) out_us[k] = ns[k + 1] >= ns[k] ? 1e-3 * static_cast<double>(ns[k + 1] - ns[k]) : 0.0;
+      // [5..8]: latest CTA arrival at barrier k relative to CTA 0's phase start;
+      // [9..12]: earliest arrival.
+      for (int k = 0; k < 4; ++k) {
+        out_us[5 + k] = ns[8 + k] >= ns[k] ? 1e-3 * static_cast<double>(ns[8 + k] - ns[k]) : -1.0;
+        out_us[9 + k] = ns[16 + k] >= ns[k] ? 1e-3 * static_cast<double>(ns[16 + k] - ns[k]) : -1.0;
+      }
+    }
+    // Reset the arrival extrema for the next armed apply.
+    std::vector<unsigned long long> init(32, 0ULL);
+    for (int k = 16; k < 24; ++k) init[k] = ~0ULL;
+    TBT_CUDA_CHECK(cudaMemcpy(c.dPhaseNs, init.data(), 32 * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    c.phaseTiming = on != 0;
   });
 }
 

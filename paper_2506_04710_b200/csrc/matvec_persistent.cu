@@ -1,0 +1,608 @@
+// The whole single-RHS operator application as ONE persistent cooperative
+// kernel (one CTA per SM), replacing the K2 -> K3 -> K4 launch chain of
+// apply.cu for the sizes it is instantiated for:
+//
+//   phase A1  row FFTs along level 0 of x (nx non-zero points per row)
+//   --- grid barrier ---
+//   phase A2  column FFTs along level 1 (ny non-zero points)  -> xhat
+//   --- grid barrier ---
+//   phase B   bin-pair products (K3): producer warp streams the spectrum
+//             through a cp.async.bulk ring; its first STAGES chunks are
+//             issued at kernel start, i.e. the HBM stream ramps up while
+//             phase A is still transforming x; meanwhile two auxiliary
+//             warps per CTA build the edge/corner correction's term vectors
+//   --- grid barrier ---
+//   phase C1  inverse column FFTs, keep ny rows (aux warps: correction sums)
+//   --- grid barrier ---
+//   phase C2  inverse row FFTs, keep nx points, 1/L, + correction -> y
+//
+// FFT lines are warp-level work items (Stockham in registers, the
+// inter-step exchange through a warp-private shared-memory slab, __syncwarp
+// only), so the transform phases need no CTA-wide synchronisation.
+// Restates applyA + apply (proj/src/linsolve.cpp:260-290,373-388).
+#include <algorithm>
+
+#include "fft_reg.cuh"
+#include "ptx.cuh"
+#include "tbt_internal.cuh"
+
+namespace tbt {
+namespace {
+
+using fftreg::fftReg;
+using fftreg::Split;
+
+constexpr int kConsumers = 256;
+constexpr int kAux = 2;                                   // auxiliary warps
+constexpr int kThreadsP = kConsumers + 32 + 32 * kAux;  // + producer warp + auxiliary warps
+
+struct PArgs {
+  const double2* S;
+  const int* pairF;
+  const int* pairG;
+  long long npairs;
+  const double2* x;
+  double2* y;
+  double2* xhat;
+  double2* yhat;
+  double2* T;  // [ny][L0][m] intermediate
+  const double2* tw0;
+  const double2* tw1;
+  int nx, ny, L0, L1;
+  double scale;
+  unsigned* bar;
+  unsigned long long* barFlags;  // monotonic grid-barrier arrival counter
+  // correction
+  int corr;
+  const int* tInfo;
+  const int* targetList;
+  const int* targetPtr;
+  int nTargets;
+  const int* elemPtr;
+  const double2* D;
+  const double2* U;
+  const double2* V;
+  int rank;
+  int nTerms;
+  int nPairs;
+  const int* pInfo;       // [pair][4] {target, source, code0, code1}, code = slot*2+trans or -1
+  const int* pTargetPtr;  // [nTargets+1] CSR of pairs by target (same order as targetList)
+  double2* tvec;          // [nPairs][M] pair vectors
+  double2* ycorr;
+  int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
+  unsigned long long* phaseNs;  // optional: globaltimer at phase boundaries (CTA 0)
+};
+
+__device__ __forceinline__ void stamp(const PArgs& a, int k) {
+  if (a.phaseNs && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.phaseNs[k] = t;
+  }
+}
+
+// Grid barrier on one monotonic 64-bit arrival counter: each CTA adds 1
+// with release semantics and spins (acquire loads, no sleep) until the
+// counter reaches the next multiple of the grid size. Nothing is ever reset,
+// so consecutive barriers and launches need no generation word. With phase
+// timing armed it also records the earliest / latest CTA arrival of barrier
+// k (ns) at phaseNs[16+k] / phaseNs[8+k].
+__device__ __forceinline__ unsigned long long atomAddRelease(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long ldAcquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void gridSync(unsigned long long* counter, const PArgs& a, int k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (a.phaseNs) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(a.phaseNs + 8 + k, t);
+      atomicMin(a.phaseNs + 16 + k, t);
+    }
+    const unsigned long long g = gridDim.x;
+    const unsigned long long old = atomAddRelease(counter, 1ULL);
+    const unsigned long long target = (old / g + 1) * g;
+    uint32_t spin = 0;
+    while (ldAcquire(counter) < target)
+      if (++spin > (1u << 30)) __trap();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double2 shflXorP(double2 v, int off) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, off);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, off);
+  return v;
+}
+
+// Warp-level batched line FFT: WB batch entries per warp, LANES butterfly
+// lanes per entry (LANES * WB == 32). For N <= 16 each lane owns a line.
+template <int N>
+struct WarpFft {
+  using S = Split<N>;
+  static constexpr int LANES = S::R2 == 1 ? 1 : S::LANES;
+  static constexpr int WB = 32 / LANES;
+  static constexpr int SLAB = S::R2 == 1 ? 0 : N * WB;  // double2 per warp
+};
+
+template <int N, bool INV, class Src, class Snk>
+__device__ __forceinline__ void warpLineFft(double2* slab, const double2* tw, Src src, Snk snk) {
+  using S = Split<N>;
+  using W = WarpFft<N>;
+  const int lane = threadIdx.x & 31;
+  const int b = lane % W::WB, ii = lane / W::WB;
+  if constexpr (S::R2 == 1) {
+    double2 u[S::R1];
+#pragma unroll
+    for (int r = 0; r < S::R1; ++r) u[r] = src(r, b);
+    fftReg<S::R1, INV>(u);
+#pragma unroll
+    for (int r = 0; r < S::R1; ++r) snk(r, b, u[r], r);
+  } else {
+    if (ii < S::R2) {
+      double2 u[S::R1];
+#pragma unroll
+      for (int r = 0; r < S::R1; ++r) u[r] = src(ii + r * S::R2, b);
+      fftReg<S::R1, INV>(u);
+#pragma unroll
+      for (int r = 0; r < S::R1; ++r) slab[(ii * S::R1 + r) * W::WB + b] = u[r];
+    }
+    __syncwarp();
+    if (ii < S::R1) {
+      double2 u[S::R2];
+#pragma unroll
+      for (int r = 0; r < S::R2; ++r) u[r] = slab[(ii + r * S::R1) * W::WB + b];
+#pragma unroll
+      for (int r = 1; r < S::R2; ++r) {
+        double2 w = __ldg(tw + r * ii);
+        if (INV) w.y = -w.y;
+        u[r] = cmul(u[r], w);
+      }
+      fftReg<S::R2, INV>(u);
+#pragma unroll
+      for (int r = 0; r < S::R2; ++r) snk(ii + r * S::R1, b, u[r], r);
+    }
+    __syncwarp();
+  }
+}
+
+// Output point of register r for the calling lane (matches warpLineFft).
+template <int N>
+__device__ __forceinline__ int outPoint(int r) {
+  using S = Split<N>;
+  using W = WarpFft<N>;
+  if constexpr (S::R2 == 1) return r;
+  const int ii = (threadIdx.x & 31) / W::WB;
+  return ii + r * S::R1;
+}
+template <int N>
+__device__ __forceinline__ bool outActive() {
+  using S = Split<N>;
+  using W = WarpFft<N>;
+  if constexpr (S::R2 == 1) return true;
+  return (threadIdx.x & 31) / W::WB < S::R1;
+}
+
+// Correction, one latency round per phase:
+// A1: one warp per term t computes the whole term vector
+//       tvec[t] = diag(d) x_src + W2 (W^T x_src)
+//     (projections reduced across the warp, then expanded in registers);
+// A2: one warp per target element sums its terms' vectors into ycorr[e];
+// C2: the inverse-row pass adds ycorr (prefetched before the transform).
+// One (target, source) pair: up to two terms sharing x_src (P of the
+// target's relation and P^T of the source's relation back, or P and P^T of a
+// self relation), tvec[pair] = sum_terms diag(d) x_src + W2 (W^T x_src).
+// Runs on the auxiliary warp during phase B, off the critical path.
+template <int M>
+__device__ void termItem(const PArgs& a, int p) {
+  constexpr int KPL = (M + 31) / 32;
+  constexpr int QB = 8;  // projections loaded / reduced per batch
+  const int lane = threadIdx.x & 31;
+  const int4 info = *reinterpret_cast<const int4*>(a.pInfo + 4 * p);
+  const double2* xs = a.x + static_cast<long long>(info.y) * M;
+  double2 xv[KPL], acc[KPL];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int kk = lane + 32 * k;
+    xv[k] = kk < M ? __ldg(xs + kk) : make_double2(0.0, 0.0);
+    acc[k] = make_double2(0.0, 0.0);
+  }
+  for (int ent = 0; ent < 2; ++ent) {
+    const int code = ent == 0 ? info.z : info.w;
+    if (code < 0) continue;
+    const int slot = code >> 1, trans = code & 1;
+    const double2* W = (trans ? a.U : a.V) + static_cast<long long>(slot) * a.rank * M;
+    const double2* W2 = (trans ? a.V : a.U) + static_cast<long long>(slot) * a.rank * M;
+#pragma unroll
+    for (int k = 0; k < KPL; ++k)
+      if (lane + 32 * k < M) cfma(acc[k], __ldg(a.D + slot * M + lane + 32 * k), xv[k]);
+    for (int q0 = 0; q0 < a.rank; q0 += QB) {
+      double2 sq[QB];
+#pragma unroll
+      for (int q = 0; q < QB; ++q) {
+        sq[q] = make_double2(0.0, 0.0);
+        if (q0 + q < a.rank) {
+#pragma unroll
+          for (int k = 0; k < KPL; ++k)
+            if (lane + 32 * k < M) cfma(sq[q], __ldg(W + (q0 + q) * M + lane + 32 * k), xv[k]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QB; ++q) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) sq[q] = cadd(sq[q], shflXorP(sq[q], off));
+      }
+#pragma unroll
+      for (int q = 0; q < QB; ++q)
+        if (q0 + q < a.rank) {
+#pragma unroll
+          for (int k = 0; k < KPL; ++k)
+            if (lane + 32 * k < M) cfma(acc[k], __ldg(W2 + (q0 + q) * M + lane + 32 * k), sq[q]);
+        }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KPL; ++k)
+    if (lane + 32 * k < M) a.tvec[static_cast<long long>(p) * M + lane + 32 * k] = acc[k];
+}
+
+template <int M>
+__device__ void sumTermsItem(const PArgs& a, int ti) {
+  constexpr int KPL = (M + 31) / 32;
+  constexpr int TMAX = 6;
+  const int lane = threadIdx.x & 31;
+  const int e = a.targetList[ti];
+  const int t0 = a.pTargetPtr[ti], t1 = a.pTargetPtr[ti + 1];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int kk = lane + 32 * k;
+    if (kk >= M) continue;
+    double2 v[TMAX];
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j)
+      v[j] = (t0 + j < t1) ? __ldcg(a.tvec + static_cast<long long>(t0 + j) * M + kk) : make_double2(0.0, 0.0);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j) acc = cadd(acc, v[j]);
+    for (int t = t0 + TMAX; t < t1; ++t) acc = cadd(acc, __ldcg(a.tvec + static_cast<long long>(t) * M + kk));
+    a.ycorr[static_cast<long long>(e) * M + kk] = acc;
+  }
+}
+
+template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+struct PCfg {
+  static constexpr int TRN = kConsumers / TC;
+  static constexpr int CPT = M / TC;
+  static constexpr int RPT = RCH / TRN;
+  static constexpr int NCH = M / RCH;
+  static constexpr uint32_t CHUNK = RCH * M * 16;
+  static constexpr uint32_t XF = M * 16;
+  static constexpr uint32_t XG = RCH * 16;
+  static constexpr uint32_t STAGE = CHUNK + XF + XG;
+  static constexpr uint32_t RED = 2 * (kConsumers / 32) * M * 16;
+  static constexpr int SLAB0 = WarpFft<N0>::SLAB, SLAB1 = WarpFft<N1>::SLAB;
+  static constexpr int SLAB = (SLAB0 > SLAB1 ? SLAB0 : SLAB1) > 1 ? (SLAB0 > SLAB1 ? SLAB0 : SLAB1) : 1;
+  static constexpr uint32_t FFTB = (kConsumers / 32) * SLAB * 16;
+  static constexpr uint32_t SMEM = STAGES * STAGE + RED + FFTB + 2 * STAGES * 8;
+};
+
+template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+__global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
+  using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double2* red = reinterpret_cast<double2*>(smem + STAGES * C::STAGE);
+  double2* fftb = reinterpret_cast<double2*>(smem + STAGES * C::STAGE + C::RED);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + C::RED + C::FFTB);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == kConsumers / 32;
+  const bool aux = warp > kConsumers / 32;
+  const int auxId = blockIdx.x * kAux + (warp - kConsumers / 32 - 1);  // valid when aux
+  double2* slab = fftb + ((producer || aux) ? 0 : warp) * C::SLAB;
+  const int nwarps = gridDim.x * (kConsumers / 32);
+  const int gw = blockIdx.x * (kConsumers / 32) + warp;  // global consumer warp id
+
+  stamp(a, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbarInit(full + s, 1);
+      mbarInit(empty + s, kConsumers / 32);
+    }
+    fenceBarrierInit();
+  }
+  __syncthreads();
+
+  const long long mine = blockIdx.x < a.npairs ? (a.npairs - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long total = mine * C::NCH;
+  const long long pre = total < STAGES ? total : STAGES;
+  uint64_t polS = 0, polX = 0;
+  auto prefetch = [&]() {
+    // Spectrum chunks of the first STAGES items: independent of x.
+    for (long long it = 0; it < pre; ++it) {
+      const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+      const int ch = static_cast<int>(it % C::NCH);
+      mbarArriveExpectTx(full + it, C::STAGE);
+      bulkG2S(smem + it * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + it,
+              polS);
+    }
+  };
+  if (producer && lane == 0) {
+    polS = policyEvictFirst();
+    polX = policyEvictLast();
+    if (a.prefetchAt == 0) prefetch();
+  }
+
+  using W0 = WarpFft<N0>;
+  using W1 = WarpFft<N1>;
+  const double2 zero = make_double2(0.0, 0.0);
+
+  // ---- phase A1: row FFTs (level 0)
+  if (!producer && !aux) {
+    const int chunks0 = M / W0::WB;
+    const int rowItems = a.ny * chunks0;
+    const int items = rowItems;
+    for (int it = gw; it < items; it += nwarps) {
+      if (it < rowItems) {
+        const int r = it / chunks0, b0 = (it % chunks0) * W0::WB;
+        warpLineFft<N0, false>(
+            slab, a.tw0,
+            [&](int c, int b) { return c < a.nx ? a.x[(static_cast<long long>(r) * a.nx + c) * M + b0 + b] : zero; },
+            [&](int s0, int b, double2 v, int) { a.T[(static_cast<long long>(r) * a.L0 + s0) * M + b0 + b] = v; });
+      }
+    }
+  }
+  gridSync(a.barFlags, a, 0);
+  stamp(a, 1);
+  if (producer && lane == 0 && a.prefetchAt == 1) prefetch();
+  // ---- phase A2: column FFTs (level 1) -> xhat
+  if (!producer && !aux) {
+    const int chunks1 = M / W1::WB;
+    const int colItems = a.L0 * chunks1;
+    const int items = colItems;
+    for (int it = gw; it < items; it += nwarps) {
+      const int s0 = it / chunks1, b0 = (it % chunks1) * W1::WB;
+      warpLineFft<N1, false>(
+          slab, a.tw1,
+          [&](int r, int b) { return r < a.ny ? a.T[(static_cast<long long>(r) * a.L0 + s0) * M + b0 + b] : zero; },
+          [&](int s1, int b, double2 v, int) { a.xhat[(static_cast<long long>(s1) * a.L0 + s0) * M + b0 + b] = v; });
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  gridSync(a.barFlags, a, 1);
+  stamp(a, 2);
+  if (producer && lane == 0 && a.prefetchAt == 2) prefetch();
+
+  // ---- phase B: bin-pair products (+ correction term vectors on the aux warp)
+  if (aux) {
+    if (a.corr)
+      for (int p = auxId; p < a.nPairs; p += gridDim.x * kAux) termItem<M>(a, p);
+  } else if (producer) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (long long it = 0; it < total; ++it) {
+        const int s = static_cast<int>(it % STAGES);
+        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+        const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+        const int ch = static_cast<int>(it % C::NCH);
+        const long long f = a.pairF[p], g = a.pairG[p];
+        unsigned char* st = smem + s * C::STAGE;
+        if (it >= pre) {
+          mbarWait(empty + s, ph ^ 1u);
+          mbarArriveExpectTx(full + s, C::STAGE);
+          bulkG2S(st, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + s, polS);
+        }
+        bulkG2S(st + C::CHUNK, a.xhat + f * M, C::XF, full + s, polX);
+        bulkG2S(st + C::CHUNK + C::XF, a.xhat + g * M + ch * RCH, C::XG, full + s, polX);
+      }
+    }
+  } else {
+    const int tc = threadIdx.x % TC, tr = threadIdx.x / TC;
+    double2 yga[C::CPT];
+    for (long long it = 0; it < total; ++it) {
+      const int s = static_cast<int>(it % STAGES);
+      const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+      const long long pi = it / C::NCH;
+      const int ch = static_cast<int>(it % C::NCH);
+      const long long p = blockIdx.x + pi * gridDim.x;
+      if (ch == 0) {
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) yga[j] = zero;
+      }
+      mbarWait(full + s, ph);
+      const double2* A = reinterpret_cast<const double2*>(smem + s * C::STAGE);
+      const double2* xf = A + RCH * M;
+      const double2* xg = xf + M;
+      double2 av[C::RPT][C::CPT], xfr[C::CPT], xgv[C::RPT];
+#pragma unroll
+      for (int j = 0; j < C::CPT; ++j) xfr[j] = xf[tc + TC * j];
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i) {
+        xgv[i] = xg[tr + C::TRN * i];
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) av[i][j] = A[(tr + C::TRN * i) * M + tc + TC * j];
+      }
+      __syncwarp();
+      if (lane == 0) mbarArrive(empty + s);
+      const long long f = a.pairF[p], g = a.pairG[p];
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i) {
+        double2 acc = zero;
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) cfma(acc, av[i][j], xfr[j]);
+#pragma unroll
+        for (int off = TC / 2; off >= 1; off >>= 1) acc = cadd(acc, shflXorP(acc, off));
+        if (tc == 0) a.yhat[f * M + ch * RCH + tr + C::TRN * i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < C::RPT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) cfma(yga[j], av[i][j], xgv[i]);
+      if (ch == C::NCH - 1) {
+        if (TC == 16) {
+#pragma unroll
+          for (int j = 0; j < C::CPT; ++j) yga[j] = cadd(yga[j], shflXorP(yga[j], 16));
+        }
+        double2* rb = red + (pi & 1) * (kConsumers / 32) * M;
+        if (lane < TC) {
+#pragma unroll
+          for (int j = 0; j < C::CPT; ++j) rb[warp * M + tc + TC * j] = yga[j];
+        }
+        namedBarrier(1, kConsumers);
+        if (f != g) {
+          for (int q = threadIdx.x; q < M; q += kConsumers) {
+            double2 acc = rb[q];
+#pragma unroll
+            for (int w = 1; w < kConsumers / 32; ++w) acc = cadd(acc, rb[w * M + q]);
+            a.yhat[g * M + q] = acc;
+          }
+        }
+      }
+    }
+  }
+  gridSync(a.barFlags, a, 2);
+  stamp(a, 3);
+
+  // ---- phase C1: inverse column FFTs, keep ny rows -> T (+ correction sums on the aux warp)
+  if (aux) {
+    if (a.corr)
+      for (int ti = auxId; ti < a.nTargets; ti += gridDim.x * kAux) sumTermsItem<M>(a, ti);
+  } else if (!producer) {
+    const int chunks1 = M / W1::WB;
+    const int items = a.L0 * chunks1;
+    for (int it = gw; it < items; it += nwarps) {
+      const int s0 = it / chunks1, b0 = (it % chunks1) * W1::WB;
+      warpLineFft<N1, true>(
+          slab, a.tw1, [&](int s1, int b) { return a.yhat[(static_cast<long long>(s1) * a.L0 + s0) * M + b0 + b]; },
+          [&](int r, int b, double2 v, int) {
+            if (r < a.ny) a.T[(static_cast<long long>(r) * a.L0 + s0) * M + b0 + b] = v;
+          });
+    }
+  }
+  gridSync(a.barFlags, a, 3);
+  stamp(a, 4);
+  // ---- phase C2: inverse row FFTs, keep nx points, scale, correction -> y
+  if (!producer && !aux) {
+    constexpr int RO = Split<N0>::R2 == 1 ? Split<N0>::R1 : Split<N0>::R2;  // outputs per lane
+    const int chunks0 = M / W0::WB;
+    const int items = a.ny * chunks0;
+    const int bl = (threadIdx.x & 31) % W0::WB;
+    for (int it = gw; it < items; it += nwarps) {
+      const int r = it / chunks0, b0 = (it % chunks0) * W0::WB;
+      double2 pre[RO];
+#pragma unroll
+      for (int q = 0; q < RO; ++q) {
+        const int c = outPoint<N0>(q);
+        pre[q] = zero;
+        if (a.corr && outActive<N0>() && c < a.nx)  // ycorr is zero off the targets
+          pre[q] = __ldcg(a.ycorr + (static_cast<long long>(r) * a.nx + c) * M + b0 + bl);
+      }
+      warpLineFft<N0, true>(
+          slab, a.tw0, [&](int s0, int b) { return a.T[(static_cast<long long>(r) * a.L0 + s0) * M + b0 + b]; },
+          [&](int c, int b, double2 v, int q) {
+            if (c < a.nx) {
+              const long long e = static_cast<long long>(r) * a.nx + c;
+              a.y[e * M + b0 + b] = cadd(cscale(v, a.scale), pre[q]);
+            }
+          });
+    }
+  }
+  stamp(a, 5);
+}
+
+template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr) {
+  using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
+  static_assert(C::SMEM <= 227 * 1024, "shared memory");
+  auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1>;
+  static bool attr = false;
+  if (!attr) {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  PArgs a{};
+  a.S = c.dSpectra;
+  a.pairF = c.dPairF;
+  a.pairG = c.dPairG;
+  a.npairs = c.npairs;
+  a.x = x;
+  a.y = y;
+  a.xhat = c.dXhat;
+  a.yhat = c.dYhat;
+  a.T = c.dT;
+  a.tw0 = c.dTw0;
+  a.tw1 = c.dTw1;
+  a.nx = c.nx;
+  a.ny = c.ny;
+  a.L0 = c.L0;
+  a.L1 = c.L1;
+  a.scale = 1.0 / static_cast<double>(c.L);
+  a.bar = c.dGridBar;
+  a.barFlags = c.dBarFlags;
+  a.corr = (withCorr && c.haveCorr && c.nTerms > 0) ? 1 : 0;
+  a.tInfo = c.dTermInfo;
+  a.targetList = c.dTargetList;
+  a.targetPtr = c.dTargetPtr;
+  a.nTargets = c.nTargets;
+  a.elemPtr = c.dElemPtr;
+  a.D = c.dCorrD;
+  a.U = c.dCorrU;
+  a.V = c.dCorrV;
+  a.rank = c.rank;
+  a.nTerms = c.nTerms;
+  a.tvec = c.dTermVec;
+  a.nPairs = c.nCorrPairs;
+  a.pInfo = c.dPairInfo;
+  a.pTargetPtr = c.dPairTargetPtr;
+  a.ycorr = c.dYcorr;
+  a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
+  a.prefetchAt = c.prefetchAt;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(smCount(c.device));
+  cfg.blockDim = dim3(kThreadsP);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TBT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+  return true;
+}
+
+}  // namespace
+
+bool persistentSupported(const Ctx& c) {
+  if (c.hasAntisym) return false;
+  const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
+  switch (key) {
+    case 64064064: case 128128128: case 192256256: case 64032032: case 128032016: case 64016032:
+      return true;
+    default:
+      return false;
+  }
+}
+
+bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr) {
+  if (!persistentSupported(c)) return false;
+  const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
+  switch (key) {
+    case 64064064: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr);
+    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr);
+    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr);
+    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr);
+    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr);
+    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr);
+    default: return false;
+  }
+}
+
+}  // namespace tbt

@@ -103,6 +103,12 @@ struct Ctx {
   cudaStream_t side = nullptr;             // parallel branch (correction projection)
   cudaEvent_t evFork = nullptr, evJoin = nullptr;
   bool fused2d = false;                    // cluster-fused 2-D transforms available
+  bool persistent = false;                 // single-kernel apply (matvec_persistent.cu)
+  unsigned* dGridBar = nullptr;            // grid barrier counter / generation
+  unsigned long long* dBarFlags = nullptr; // flag-line grid barrier (matvec_persistent.cu)
+  bool phaseTiming = false;
+  int prefetchAt = 0;                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
+  unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
 
   // Generators (host copy kept for diagonal / K) and spectra.
@@ -130,6 +136,10 @@ struct Ctx {
   std::vector<double2> corrDHost;
   int nTerms = 0, nTargets = 0, maxTermsPerTarget = 0;
   double2* dYcorr = nullptr;    // [ne][maxNrhs*m] correction vector
+  double2* dTermVec = nullptr;  // [nCorrPairs][m] per-(target,source) vectors (persistent apply)
+  int nCorrPairs = 0;
+  int* dPairInfo = nullptr;       // [pair][4] {target, source, code0, code1}
+  int* dPairTargetPtr = nullptr;  // [nTargets+1]
   int* dTermInfo = nullptr;     // [nTerms][4] {target, source, slot, trans}
   int* dTargetList = nullptr;   // [nTargets] target elements
   int* dTargetPtr = nullptr;    // [nTargets+1] CSR over terms
@@ -181,6 +191,10 @@ struct GmresState {
 };
 void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres_opts& o, bool useAOnly,
                 std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs);
+
+// Persistent single-kernel apply (matvec_persistent.cu).
+bool persistentSupported(const Ctx& c);
+bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr);
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);

@@ -192,6 +192,11 @@ class ToeplitzMatvec:
         _check(lib().tbt_timing_read(self._h, C.byref(tot), C.byref(cnt)))
         return tot.value, cnt.value
 
+    def phase_times(self, on: bool = True):
+        out = (C.c_double * 13)()
+        _check(lib().tbt_phase_times(self._h, 1 if on else 0, out))
+        return list(out)
+
     def bench_apply(self, x_ptr: int, y_ptr: int, iters: int, use_graph: bool = True):
         ms, bms = C.c_double(), C.c_double()
         _check(lib().tbt_bench_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), 1, iters,
