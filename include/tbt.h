@@ -70,6 +70,11 @@ typedef struct {
   int precondition; /* left Jacobi (default 1, linsolve.hpp:51)            */
   int use_a_only;   /* 1: operator = applyA (schurSolve's inner solves)    */
   int hist_cap;     /* history entries kept per column (0 = none)          */
+  int orthog;       /* Arnoldi orthogonalisation, both modified Gram-Schmidt
+                       (linsolve.cpp:465-468): 0 = the projection sweep, one
+                       grid barrier per projection; 1 = low-synchronisation
+                       form h = (I+L)^-1 V^H w, 3 barriers per step (single
+                       column, n <= 4096 * SMs; else falls back to 0)     */
 } tbt_gmres_opts;
 
 typedef struct {

@@ -25,7 +25,8 @@ class TbtDesc(C.Structure):
 
 class TbtGmresOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int),
-                ("precondition", C.c_int), ("use_a_only", C.c_int), ("hist_cap", C.c_int)]
+                ("precondition", C.c_int), ("use_a_only", C.c_int), ("hist_cap", C.c_int),
+                ("orthog", C.c_int)]
 
 
 class TbtGmresStats(C.Structure):

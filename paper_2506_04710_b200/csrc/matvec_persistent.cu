@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "fft_reg.cuh"
+#include "grid_sync.cuh"
 #include "ptx.cuh"
 #include "tbt_internal.cuh"
 
@@ -70,6 +71,7 @@ struct PArgs {
   double2* tvec;          // [nPairs][M] pair vectors
   double2* ycorr;
   int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
+  const int* skip;              // optional: the whole launch is a no-op when *skip != 0
   unsigned long long* phaseNs;  // optional: globaltimer at phase boundaries (CTA 0)
 };
 
@@ -81,23 +83,8 @@ __device__ __forceinline__ void stamp(const PArgs& a, int k) {
   }
 }
 
-// Grid barrier on one monotonic 64-bit arrival counter: each CTA adds 1
-// with release semantics and spins (acquire loads, no sleep) until the
-// counter reaches the next multiple of the grid size. Nothing is ever reset,
-// so consecutive barriers and launches need no generation word. With phase
-// timing armed it also records the earliest / latest CTA arrival of barrier
-// k (ns) at phaseNs[16+k] / phaseNs[8+k].
-__device__ __forceinline__ unsigned long long atomAddRelease(unsigned long long* p, unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ unsigned long long ldAcquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
+// Grid barrier (grid_sync.cuh); with phase timing armed it also records the
+// earliest / latest CTA arrival of barrier k (ns) at phaseNs[16+k] / phaseNs[8+k].
 __device__ __forceinline__ void gridSync(unsigned long long* counter, const PArgs& a, int k) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -107,12 +94,7 @@ __device__ __forceinline__ void gridSync(unsigned long long* counter, const PArg
       atomicMax(a.phaseNs + 8 + k, t);
       atomicMin(a.phaseNs + 16 + k, t);
     }
-    const unsigned long long g = gridDim.x;
-    const unsigned long long old = atomAddRelease(counter, 1ULL);
-    const unsigned long long target = (old / g + 1) * g;
-    uint32_t spin = 0;
-    while (ldAcquire(counter) < target)
-      if (++spin > (1u << 30)) __trap();
+    gridArriveWait(counter);
   }
   __syncthreads();
 }
@@ -310,6 +292,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   const int nwarps = gridDim.x * (kConsumers / 32);
   const int gw = blockIdx.x * (kConsumers / 32) + warp;  // global consumer warp id
 
+  if (a.skip && *reinterpret_cast<const volatile int*>(a.skip)) return;  // uniform: set before launch
   stamp(a, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -564,6 +547,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr) {
   a.ycorr = c.dYcorr;
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
   a.prefetchAt = c.prefetchAt;
+  a.skip = c.skipFlag;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(smCount(c.device));
   cfg.blockDim = dim3(kThreadsP);

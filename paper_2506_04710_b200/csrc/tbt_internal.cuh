@@ -107,7 +107,8 @@ struct Ctx {
   unsigned* dGridBar = nullptr;            // grid barrier counter / generation
   unsigned long long* dBarFlags = nullptr; // flag-line grid barrier (matvec_persistent.cu)
   bool phaseTiming = false;
-  int prefetchAt = 0;                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
+  int prefetchAt = 0;
+  const int* skipFlag = nullptr;           // device flag: persistent applies become no-ops when set                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
 

@@ -84,6 +84,7 @@ class SolverOptions:  # linsolve.hpp:47-53
     restart: int = 60
     precondition: bool = True
     threads: int = 1  # accepted for API parity; columns run in lockstep on the GPU
+    orthog: int = 1   # 0: MGS projection sweep; 1: low-synchronisation MGS (same coefficients)
 
 
 @dataclass
@@ -222,7 +223,7 @@ class ToeplitzMatvec:
                            conv.ctypes.data_as(C.POINTER(C.c_int)), hist.ctypes.data_as(dp),
                            hlen.ctypes.data_as(C.POINTER(C.c_int)), 0)
         o = TbtGmresOpts(opt.tol, opt.maxIter, opt.restart, 1 if opt.precondition else 0,
-                         1 if use_a_only else 0, hist_cap)
+                         1 if use_a_only else 0, hist_cap, opt.orthog)
         status = lib().tbt_gmres(self._h, C.c_void_p(bp), C.c_void_p(xp), k, C.byref(o), C.byref(st), where)
         if status not in (_lib.TBT_OK, _lib.TBT_NUMERIC_ERROR) or (status != _lib.TBT_OK and raise_on_fail):
             _check(status)

@@ -118,12 +118,13 @@ def test_multi_rhs_apply(gpu, fft_path, nx, ny, m, k):
         assert rel(Ya[:, c], o.applyA(xc)) < MATVEC_TOL
 
 
-def test_gmres_single_column_small(gpu, fft_path):
+@pytest.mark.parametrize("orthog", [0, 1])
+def test_gmres_single_column_small(gpu, fft_path, orthog):
     rep = rep_for(5, 4, 8, seed=3)
     o = oracle.Oracle.from_rep(rep)
     b = gen.rhs_normal(o.n, 1, 21)[:, 0]
     op = ToeplitzMatvec(rep)
-    g = op.gmres(b, SolverOptions(tol=1e-9, maxIter=500, restart=12))
+    g = op.gmres(b, SolverOptions(tol=1e-9, maxIter=500, restart=12, orthog=orthog))
     r = o.gmres(b, tol=1e-9, max_iter=500, restart=12)
     assert g.iterations == r["iterations"]
     hist_close(g.history[0], r["history"][0], GMRES_TOL)
@@ -153,13 +154,14 @@ def hist_close(h_gpu, h_ref, tol):
     assert np.all(d <= bound), (d / bound).max()
 
 
-def test_gmres_c1_parity(gpu):
+@pytest.mark.parametrize("orthog", [0, 1])
+def test_gmres_c1_parity(gpu, orthog):
     cfg = CONFIGS["C1"]
     rep = ToeplitzRep.synthetic(cfg)
     op = ToeplitzMatvec(rep)
     o = oracle.Oracle.from_rep(rep)
     b = gen.rhs_normal(cfg.n, 1, cfg.seed)[:, 0]
-    opt = SolverOptions(tol=cfg.tol, maxIter=cfg.max_iter, restart=cfg.restart)
+    opt = SolverOptions(tol=cfg.tol, maxIter=cfg.max_iter, restart=cfg.restart, orthog=orthog)
     g = op.gmres(b, opt)
     r = o.gmres(b, tol=cfg.tol, max_iter=cfg.max_iter, restart=cfg.restart)
     assert g.converged == [1] and r["converged"] == [1]
@@ -168,18 +170,19 @@ def test_gmres_c1_parity(gpu):
     hist_close(g.history[0], r["history"][0], GMRES_TOL)
 
 
-def test_gmres_c2_budget_parity(gpu):
+@pytest.mark.parametrize("orthog", [0, 1])
+def test_gmres_c2_budget_parity(gpu, orthog):
     # C2 stalls under GMRES(50)+Jacobi: compare a fixed
-    # 100-iteration budget (2 restarts) history and iterate.
+    # 200-iteration budget (4 restarts, the bench's budget) history and iterate.
     cfg = CONFIGS["C2"]
     rep = ToeplitzRep.synthetic(cfg)
     op = ToeplitzMatvec(rep)
     o = oracle.Oracle.from_rep(rep)
     b = rhs_for(cfg)
-    opt = SolverOptions(tol=cfg.tol, maxIter=100, restart=cfg.restart)
+    opt = SolverOptions(tol=cfg.tol, maxIter=200, restart=cfg.restart, orthog=orthog)
     g = op.gmres(b, opt, raise_on_fail=False)
-    r = o.gmres(b, tol=cfg.tol, max_iter=100, restart=cfg.restart)
-    assert g.iterations == r["iterations"] == [100]
+    r = o.gmres(b, tol=cfg.tol, max_iter=200, restart=cfg.restart)
+    assert g.iterations == r["iterations"] == [200]
     hist_close(g.history[0], r["history"][0], GMRES_TOL)
     assert rel(g.current, r["x"]) < GMRES_TOL
 
