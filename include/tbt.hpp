@@ -1,0 +1,122 @@
+// tbt.hpp - header-only C++ mirror of the reference's operator / solver API
+// (proj/include/arraymom/linsolve.hpp:40-95) over the C ABI of tbt.h.
+// A reference caller swaps `arraymom::ToeplitzMatvec` for `tbt::ToeplitzMatvec`
+// and `arraymom::iterativeSolve` for `tbt::iterativeSolve`.
+#pragma once
+
+#include <complex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tbt.h"
+
+namespace tbt {
+
+using Complex = std::complex<double>;  // common.hpp:28
+using Vector = std::vector<Complex>;
+
+struct UserError : std::runtime_error {  // common.hpp:40-43
+  using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {  // common.hpp:47-50
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(tbt_status s) {
+  if (s == TBT_OK) return;
+  const std::string msg = tbt_last_error();
+  if (s == TBT_USER_ERROR) throw UserError(msg);
+  if (s == TBT_NUMERIC_ERROR) throw NumericError(msg);
+  throw DeviceError(msg);
+}
+
+struct SolverOptions {  // linsolve.hpp:47-53
+  double tol = 1e-8;
+  int maxIter = 2000;
+  int restart = 60;
+  bool precondition = true;
+  int threads = 1;  // columns run in lockstep on the device
+};
+
+struct SolveResult {  // linsolve.hpp:40-45
+  std::vector<Vector> current;  // one vector per column
+  std::vector<double> residual;
+  std::vector<int> iterations;
+  std::string solver = "gmres";
+};
+
+// ToeplitzMatvec (linsolve.hpp:59-77). Generators: ToeplitzRep::aGen in the
+// Sparse order (toeplitz.hpp:72-74), each m x m column-major.
+class ToeplitzMatvec {
+ public:
+  ToeplitzMatvec(int nx, int ny, int m, const std::vector<Complex>& generators, int maxNrhs = 1,
+                 int device = 0) {
+    tbt_desc d{nx, ny, m, maxNrhs, device, 0};
+    check(tbt_create(&d, &ctx_));
+    const long long nb = static_cast<long long>(nx) * ny + static_cast<long long>(nx - 1) * (ny - 1);
+    if (static_cast<long long>(generators.size()) != nb * m * m) {
+      tbt_destroy(ctx_);
+      throw UserError("ToeplitzMatvec: generator count mismatch");
+    }
+    check(tbt_set_generators(ctx_, reinterpret_cast<const double*>(generators.data()), nb));
+  }
+  ~ToeplitzMatvec() { tbt_destroy(ctx_); }
+  ToeplitzMatvec(const ToeplitzMatvec&) = delete;
+  ToeplitzMatvec& operator=(const ToeplitzMatvec&) = delete;
+
+  // Optional edge/corner terms (tbt_gen.h layout), then the spectra.
+  void setCorrection(int rank, const Complex* d, const Complex* u, const Complex* v) {
+    check(tbt_set_correction(ctx_, rank, reinterpret_cast<const double*>(d), reinterpret_cast<const double*>(u),
+                             reinterpret_cast<const double*>(v)));
+  }
+  void precompute() { check(tbt_precompute(ctx_)); }
+
+  Vector apply(const Vector& x) const { return run(tbt_apply, x); }    // linsolve.hpp:64
+  Vector applyA(const Vector& x) const { return run(tbt_apply_a, x); } // linsolve.hpp:65
+  Vector diagonal() const {                                             // linsolve.hpp:69
+    Vector d(static_cast<size_t>(sizeA()));
+    check(tbt_diagonal(ctx_, reinterpret_cast<double*>(d.data())));
+    return d;
+  }
+  long sizeA() const { return static_cast<long>(tbt_size_a(ctx_)); }
+  long sizeM() const { return 0; }
+  tbt_ctx* handle() const { return ctx_; }
+
+ private:
+  using Fn = tbt_status (*)(tbt_ctx*, const double*, double*, int, int);
+  Vector run(Fn fn, const Vector& x) const {
+    if (static_cast<long>(x.size()) != sizeA()) throw UserError("matvec: vector length mismatch");
+    Vector y(x.size());
+    check(fn(ctx_, reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data()), 1, TBT_HOST));
+    return y;
+  }
+  tbt_ctx* ctx_ = nullptr;
+};
+
+// iterativeSolve (linsolve.hpp:88-89): columns of V, throws NumericError if
+// any column did not converge (linsolve.cpp:591).
+inline SolveResult iterativeSolve(ToeplitzMatvec& op, const std::vector<Vector>& V, const SolverOptions& opt) {
+  const int p = static_cast<int>(V.size());
+  const long n = op.sizeA();
+  std::vector<Complex> b(static_cast<size_t>(n) * p), x(b.size());
+  for (int c = 0; c < p; ++c) std::copy(V[c].begin(), V[c].end(), b.begin() + static_cast<long>(c) * n);
+  tbt_gmres_opts o{opt.tol, opt.maxIter, opt.restart, opt.precondition ? 1 : 0, 0, 0, 1};
+  std::vector<int> its(p), conv(p), hlen(p);
+  std::vector<double> res(p);
+  tbt_gmres_stats st{its.data(), res.data(), conv.data(), nullptr, hlen.data(), 0};
+  const tbt_status s = tbt_gmres(op.handle(), reinterpret_cast<const double*>(b.data()),
+                                 reinterpret_cast<double*>(x.data()), p, &o, &st, TBT_HOST);
+  SolveResult out;
+  for (int c = 0; c < p; ++c)
+    out.current.emplace_back(x.begin() + static_cast<long>(c) * n, x.begin() + static_cast<long>(c + 1) * n);
+  out.residual = res;
+  out.iterations = its;
+  check(s);
+  return out;
+}
+
+}  // namespace tbt

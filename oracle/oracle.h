@@ -6,9 +6,13 @@
  * product path.
  *
  * Every function restates the reference file:line named beside it
- * (/root/reference/proj/...). The reference itself cannot be built here
- * (Eigen3 is absent); its fftInPlace is compiled
- * separately into oracle/_ref to pin restated FFT (tests/test_oracle_pin.py).
+ * (/root/reference/proj/...). Pinning status:
+ *  - fftInPlace: PINNED bit-exactly against the reference's own fft.cpp,
+ *    compiled into oracle/_ref (tests/test_oracle.py, tests/golden/).
+ *  - applyA / gmres: PARITY UNPINNED against reference outputs -- the
+ *    reference linsolve.cpp needs Eigen3, which is absent here, and no
+ *    golden vectors exist; checked instead against SPEC.md's known-answer
+ *    properties with an independent dense numpy product / LU solve.
  * The synthetic nine-component correction is not reference code; it is the
  * BASELINE.json perturbation, defined in include/tbt_gen.h.
  */
