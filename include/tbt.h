@@ -60,8 +60,13 @@ typedef struct {
   int m;         /* basis functions per element (reference e5)            */
   int max_nrhs;  /* largest nrhs later passed to apply/gmres (>= 1)        */
   int device;    /* CUDA device ordinal                                    */
-  int flags;     /* reserved, 0                                            */
+  int flags;     /* TBT_EMBED_SMOOTH or 0                                 */
 } tbt_desc;
+
+/* Embedding choice: 0 = the reference's next power of two >= 2n-1 per level
+ * (linsolve.cpp:240-242); TBT_EMBED_SMOOTH = the smallest 2^a 3^b length
+ * >= 2n-1 (mixed-radix transforms), e.g. 36 x 18 bins instead of 64 x 32. */
+#define TBT_EMBED_SMOOTH 1
 
 typedef struct {
   double tol;       /* relative residual target (reference default 1e-8)   */

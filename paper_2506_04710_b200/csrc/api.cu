@@ -38,6 +38,14 @@ int pow2AtLeast(int n) {  // nextPow2, proj/src/fft.cpp:22-26
   return p;
 }
 
+// Smallest transform length with a compiled mixed-radix (2^a 3^b) plan.
+int smoothAtLeast(int n) {
+  static const int kSizes[] = {1, 2, 3, 4, 6, 8, 9, 12, 16, 18, 24, 32, 36, 48, 64, 72, 96, 128, 144, 192, 256};
+  for (int s : kSizes)
+    if (s >= n) return s;
+  return pow2AtLeast(n);
+}
+
 template <typename Fn>
 tbt_status guarded(Fn&& fn) {
   try {
@@ -209,8 +217,13 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
     c.n = static_cast<long long>(c.ne) * c.m;
     c.maxNrhs = desc->max_nrhs;
     c.device = desc->device;
-    c.L1 = pow2AtLeast(2 * c.ny - 1);  // linsolve.cpp:240-242
-    c.L0 = pow2AtLeast(2 * c.nx - 1);
+    // Circulant embedding length per level >= 2n-1: the reference's next
+    // power of two (linsolve.cpp:240-242), or with TBT_EMBED_SMOOTH the
+    // smallest 3-smooth length (e.g. 36 x 18 instead of 64 x 32 for C3);
+    // both embed the same Toeplitz operator exactly.
+    const bool smooth = (desc->flags & TBT_EMBED_SMOOTH) != 0;
+    c.L1 = smooth ? smoothAtLeast(2 * c.ny - 1) : pow2AtLeast(2 * c.ny - 1);
+    c.L0 = smooth ? smoothAtLeast(2 * c.nx - 1) : pow2AtLeast(2 * c.nx - 1);
     c.L = static_cast<long long>(c.L0) * c.L1;
     try {
       TBT_USER_CHECK(c.L0 <= 256 && c.L1 <= 256, "tbt_create: embedding length above 256 (nx, ny <= 128)");

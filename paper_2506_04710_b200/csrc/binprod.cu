@@ -303,6 +303,7 @@ int binprodVariant(int m) {
 }
 
 void launchBinProduct(Ctx& c, int nrhs) {
+  if (nrhs >= kGemmMinRhs && launchBinProductGemm(c, nrhs)) return;
   if (nrhs == 1 && c.binprodKernel >= 11) {
     switch (c.binprodKernel) {
       case 11: launchRing<64, 16, 64, 3>(c); break;

@@ -1,0 +1,190 @@
+// K3 for many right-hand sides (C3: 162 port excitations): the bin-pair
+// product becomes two complex GEMMs per stored block,
+//     Yhat_f = Ahat X_f,      Yhat_g = Ahat^T X_g      (X: m x nrhs),
+// computed on the FP64 tensor path (mma.sync.m8n8k4.f64, "DMMA": on B200 it
+// runs at the FP64 peak with one instruction per 256 FMAs). A complex
+// 8x8x4 block is four real DMMAs (Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br;
+// no 3M trick, so rounding stays that of the plain product). The reference
+// re-streams every block once per column (linsolve.cpp:276-282, 572).
+//
+// CTA tile: all M rows x NTILE right-hand sides of one (pair, transpose)
+// item; 8 warps, warp w owns rows [w*M/8, (w+1)*M/8). K advances in chunks
+// of 32 through a cp.async double buffer: the A chunk (M x 32 for A, or the
+// 32 contiguous rows of A for A^T) and the X chunk (32 x NTILE).
+#include <algorithm>
+
+#include "tbt_internal.cuh"
+
+namespace tbt {
+namespace {
+
+constexpr int NT = 256;
+constexpr int KC = 32;     // K chunk
+constexpr int NTILE = 56;  // right-hand sides per CTA tile (7 n-blocks of 8)
+constexpr int NB = NTILE / 8;
+constexpr int PADC = 4;    // complex padding per smem row (bank spread)
+
+__device__ __forceinline__ void cpAsync16(void* dst, const void* src, bool pred) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cpCommit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpWait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int M>
+struct GemmCfg {
+  static constexpr int MW = M / 8;   // rows per warp
+  static constexpr int MB = MW / 8;  // m-blocks per warp
+  // A chunk: non-transposed [M][KC+PADC]; transposed [KC][M] (rows of A).
+  static constexpr int A_ELEMS = M * (KC + PADC) > KC * M ? M * (KC + PADC) : KC * M;
+  static constexpr int B_ELEMS = NTILE * (KC + PADC);
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;  // double2
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(double2);
+};
+
+// item = ((p * 2 + t) * nTiles + tile); t = 1 is the transposed product.
+template <int M>
+__global__ void __launch_bounds__(NT, 1)
+binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
+            long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int nrhs) {
+  using C = GemmCfg<M>;
+  extern __shared__ __align__(16) double2 gsm[];
+  const int nTiles = (nrhs + NTILE - 1) / NTILE;
+  const long long items = npairs * 2 * nTiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const long long B = static_cast<long long>(nrhs) * M;
+
+  for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+    const int tile = static_cast<int>(item % nTiles);
+    const int t = static_cast<int>((item / nTiles) & 1);
+    const long long p = item / (2 * nTiles);
+    const int f = pairF[p], g = pairG[p];
+    if (t == 1 && f == g) continue;  // self-paired bin: one product only
+    const int bin = t == 0 ? f : g;
+    const double2* A = S + p * M * M;
+    const double2* X = xhat + static_cast<long long>(bin) * B;  // column n at X + n*M
+    double2* Y = yhat + static_cast<long long>(bin) * B;
+    const int n0 = tile * NTILE;
+
+    double acc[C::MB][NB][2][2];  // [mblock][nblock][re/im][c0/c1]
+#pragma unroll
+    for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+
+    auto load = [&](int kc, int stage) {
+      double2* sA = gsm + stage * C::STAGE;
+      double2* sB = sA + C::A_ELEMS;
+      const int k0 = kc * KC;
+      if (t == 0) {  // sA[i][k] = A[i][k0 + k]
+        for (int q = threadIdx.x; q < M * KC; q += NT) {
+          const int i = q / KC, k = q % KC;
+          cpAsync16(sA + i * (KC + PADC) + k, A + static_cast<long long>(i) * M + k0 + k, true);
+        }
+      } else {  // sA[k][i] = A[k0 + k][i]  (contiguous rows)
+        for (int q = threadIdx.x; q < KC * M; q += NT) cpAsync16(sA + q, A + static_cast<long long>(k0) * M + q, true);
+      }
+      for (int q = threadIdx.x; q < NTILE * KC; q += NT) {  // sB[n][k] = X[n0+n][k0+k]
+        const int n = q / KC, k = q % KC;
+        const bool ok = n0 + n < nrhs;
+        cpAsync16(sB + n * (KC + PADC) + k, X + static_cast<long long>(ok ? n0 + n : 0) * M + k0 + k, ok);
+      }
+      cpCommit();
+    };
+
+    constexpr int NKC = M / KC;
+    load(0, 0);
+    for (int kc = 0; kc < NKC; ++kc) {
+      if (kc + 1 < NKC) {
+        load(kc + 1, (kc + 1) & 1);
+        cpWait<1>();
+      } else {
+        cpWait<0>();
+      }
+      __syncthreads();
+      const double2* sA = gsm + (kc & 1) * C::STAGE;
+      const double2* sB = sA + C::A_ELEMS;
+#pragma unroll
+      for (int kk = 0; kk < KC; kk += 4) {
+        double ar[C::MB], ai[C::MB], br[NB], bi[NB];
+#pragma unroll
+        for (int a = 0; a < C::MB; ++a) {
+          const int i = warp * C::MW + a * 8 + gid;
+          const double2 v = t == 0 ? sA[i * (KC + PADC) + kk + tig] : sA[(kk + tig) * M + i];
+          ar[a] = v.x;
+          ai[a] = v.y;
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const double2 v = sB[(b * 8 + gid) * (KC + PADC) + kk + tig];
+          br[b] = v.x;
+          bi[b] = v.y;
+        }
+#pragma unroll
+        for (int a = 0; a < C::MB; ++a) {
+          const double nai = -ai[a];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+            dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // D fragment: row gid, columns 2*tig + {0,1}; Y[n][i] (column n contiguous).
+#pragma unroll
+    for (int a = 0; a < C::MB; ++a) {
+      const int i = warp * C::MW + a * 8 + gid;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = n0 + b * 8 + 2 * tig + h;
+          if (n < nrhs) Y[static_cast<long long>(n) * M + i] = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+        }
+    }
+  }
+}
+
+template <int M>
+void launchGemm(Ctx& c, int nrhs) {
+  using C = GemmCfg<M>;
+  static bool attr = false;
+  if (!attr) {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(C::SMEM)));
+    attr = true;
+  }
+  const int nTiles = (nrhs + NTILE - 1) / NTILE;
+  const long long items = c.npairs * 2 * nTiles;
+  const int grid = static_cast<int>(std::min<long long>(items, 16LL * smCount(c.device)));
+  binprodGemm<M><<<grid, NT, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, nrhs);
+}
+
+}  // namespace
+
+bool launchBinProductGemm(Ctx& c, int nrhs) {
+  switch (c.m) {
+    case 64: launchGemm<64>(c, nrhs); break;
+    case 128: launchGemm<128>(c, nrhs); break;
+    default: return false;
+  }
+  TBT_CUDA_CHECK(cudaGetLastError());
+  return true;
+}
+
+}  // namespace tbt

@@ -17,7 +17,7 @@
 namespace tbt {
 namespace {
 
-using fftreg::fftReg;
+using fftreg::dftReg;
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
@@ -40,7 +40,7 @@ fftPassKernel(FftPass p) {
     double2 u[R1];
 #pragma unroll
     for (int r = 0; r < R1; ++r) u[r] = (bok && r < p.n_in) ? ldg2(in + r * p.in_point_stride) : zero;
-    fftReg<R1, INV>(u);
+    dftReg<R1, INV>(u);
 #pragma unroll
     for (int r = 0; r < R1; ++r)
       if (bok && r < p.n_out) out[r * p.out_point_stride] = cscale(u[r], p.scale);
@@ -54,7 +54,7 @@ fftPassKernel(FftPass p) {
         const int pt = i + r * R2;
         u[r] = (bok && pt < p.n_in) ? ldg2(in + (long long)pt * p.in_point_stride) : zero;
       }
-      fftReg<R1, INV>(u);
+      dftReg<R1, INV>(u);
 #pragma unroll
       for (int r = 0; r < R1; ++r) sbuf[(i * R1 + r) * BC + b] = u[r];
     }
@@ -70,7 +70,7 @@ fftPassKernel(FftPass p) {
         if (INV) w.y = -w.y;
         u[r] = cmul(u[r], w);
       }
-      fftReg<R2, INV>(u);
+      dftReg<R2, INV>(u);
 #pragma unroll
       for (int r = 0; r < R2; ++r) {
         const int pt = i + r * R1;
@@ -95,18 +95,14 @@ void launchT(const FftPass& p, cudaStream_t s) {
 template <int BC>
 void launchN(const FftPass& p, cudaStream_t s) {
   switch (p.n) {
-    case 1: launchT<1, 1, BC>(p, s); break;
-    case 2: launchT<2, 1, BC>(p, s); break;
-    case 4: launchT<4, 1, BC>(p, s); break;
-    case 8: launchT<8, 1, BC>(p, s); break;
-    case 16: launchT<16, 1, BC>(p, s); break;
-    case 32: launchT<4, 8, BC>(p, s); break;
-    case 64: launchT<8, 8, BC>(p, s); break;
-    case 128: launchT<8, 16, BC>(p, s); break;
-    case 256: launchT<16, 16, BC>(p, s); break;
+#define TBT_CASE(N) \
+  case N: launchT<fftreg::Split<N>::R1, fftreg::Split<N>::R2, BC>(p, s); break;
+    TBT_CASE(1) TBT_CASE(2) TBT_CASE(3) TBT_CASE(4) TBT_CASE(6) TBT_CASE(8) TBT_CASE(9) TBT_CASE(12)
+    TBT_CASE(16) TBT_CASE(18) TBT_CASE(24) TBT_CASE(32) TBT_CASE(36) TBT_CASE(48) TBT_CASE(64) TBT_CASE(72)
+    TBT_CASE(96) TBT_CASE(128) TBT_CASE(144) TBT_CASE(192) TBT_CASE(256)
+#undef TBT_CASE
     default:
-      throw Error{TBT_USER_ERROR, "FFT length " + std::to_string(p.n) +
-                                      " not supported (powers of two up to 256)"};
+      throw Error{TBT_USER_ERROR, "FFT length " + std::to_string(p.n) + " not supported"};
   }
 }
 

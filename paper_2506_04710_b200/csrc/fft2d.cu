@@ -29,7 +29,7 @@ namespace cg = cooperative_groups;
 namespace tbt {
 namespace {
 
-using fftreg::fftReg;
+using fftreg::dftReg;
 using fftreg::Split;
 
 // One line of length N for one batch entry per thread (ii = butterfly
@@ -44,7 +44,7 @@ __device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, co
       double2 u[S::R1];
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) u[r] = src(r);
-      fftReg<S::R1, INV>(u);
+      dftReg<S::R1, INV>(u);
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) snk(r, u[r]);
     }
@@ -53,7 +53,7 @@ __device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, co
       double2 u[S::R1];
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) u[r] = src(ii + r * S::R2);
-      fftReg<S::R1, INV>(u);
+      dftReg<S::R1, INV>(u);
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) st[(ii * S::R1 + r) * BC + b] = u[r];
     }
@@ -68,7 +68,7 @@ __device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, co
         if (INV) w.y = -w.y;
         u[r] = cmul(u[r], w);
       }
-      fftReg<S::R2, INV>(u);
+      dftReg<S::R2, INV>(u);
 #pragma unroll
       for (int r = 0; r < S::R2; ++r) snk(ii + r * S::R1, u[r]);
     }
@@ -213,6 +213,7 @@ bool fft2dSupported(int L0, int L1) {
   const int key = L0 * 1000 + L1;
   switch (key) {
     case 8008: case 16016: case 32032: case 64064: case 128128: case 256256: case 64032: case 16008:
+    case 36018:
       return true;
     default:
       return false;
@@ -224,8 +225,8 @@ bool fft2dSupported(int L0, int L1) {
 void fft2dPlan(int L0, int L1, int nx, int ny, int B, int sms, int* CL, int* BC) {
   (void)L1;
   (void)nx;
-  int cl = std::min(8, L0);
-  while (cl > 1 && cl > ny) cl /= 2;  // keep every CTA busy in the row pass
+  int cl = 8;
+  while (cl > 1 && (L0 % cl != 0 || cl > ny)) cl /= 2;  // columns split evenly, rows keep CTAs busy
   if (cl < 1) cl = 1;
   int bc = 16;
   auto xbufBytes = [&](int c) {
@@ -248,6 +249,7 @@ bool launchFft2d(const Fft2dArgs& a, int CL, int BC, bool inverse, cudaStream_t 
     case 256256: return launchBC<256, 256>(a, CL, BC, inverse, s);
     case 64032: return launchBC<64, 32>(a, CL, BC, inverse, s);
     case 16008: return launchBC<16, 8>(a, CL, BC, inverse, s);
+    case 36018: return launchBC<36, 18>(a, CL, BC, inverse, s);
     default: return false;
   }
 }

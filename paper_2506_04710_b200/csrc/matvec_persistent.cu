@@ -30,7 +30,7 @@
 namespace tbt {
 namespace {
 
-using fftreg::fftReg;
+using fftreg::dftReg;
 using fftreg::Split;
 
 constexpr int kConsumers = 256;
@@ -125,7 +125,7 @@ __device__ __forceinline__ void warpLineFft(double2* slab, const double2* tw, Sr
     double2 u[S::R1];
 #pragma unroll
     for (int r = 0; r < S::R1; ++r) u[r] = src(r, b);
-    fftReg<S::R1, INV>(u);
+    dftReg<S::R1, INV>(u);
 #pragma unroll
     for (int r = 0; r < S::R1; ++r) snk(r, b, u[r], r);
   } else {
@@ -133,7 +133,7 @@ __device__ __forceinline__ void warpLineFft(double2* slab, const double2* tw, Sr
       double2 u[S::R1];
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) u[r] = src(ii + r * S::R2, b);
-      fftReg<S::R1, INV>(u);
+      dftReg<S::R1, INV>(u);
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) slab[(ii * S::R1 + r) * W::WB + b] = u[r];
     }
@@ -148,7 +148,7 @@ __device__ __forceinline__ void warpLineFft(double2* slab, const double2* tw, Sr
         if (INV) w.y = -w.y;
         u[r] = cmul(u[r], w);
       }
-      fftReg<S::R2, INV>(u);
+      dftReg<S::R2, INV>(u);
 #pragma unroll
       for (int r = 0; r < S::R2; ++r) snk(ii + r * S::R1, b, u[r], r);
     }

@@ -180,6 +180,8 @@ void buildSpectra(Ctx& c);                                    // spectra.cu
 void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 int binprodVariant(int m);                                    // binprod.cu
+constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEMM
+bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
 void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs);     // correction.cu

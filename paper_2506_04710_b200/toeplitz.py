@@ -109,10 +109,14 @@ def _as_cols(x: np.ndarray) -> tuple[np.ndarray, int, bool]:
 class ToeplitzMatvec:
     """FFT-accelerated application of Z^part (linsolve.hpp:59-77) on a B200."""
 
-    def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0):
+    def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0, embed: str = "pow2"):
+        """embed: "pow2" (the reference's nextPow2 embedding) or "smooth"
+        (smallest 2^a 3^b length per level, mixed-radix transforms)."""
         self.rep = rep
         self._h = C.c_void_p()
-        desc = TbtDesc(rep.nx, rep.ny, rep.m, max_nrhs, device, 0)
+        if embed not in ("pow2", "smooth"):
+            raise UserError(f"embed must be 'pow2' or 'smooth', got {embed!r}")
+        desc = TbtDesc(rep.nx, rep.ny, rep.m, max_nrhs, device, 1 if embed == "smooth" else 0)
         _check(lib().tbt_create(C.byref(desc), C.byref(self._h)))
         gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
         _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))

@@ -50,6 +50,30 @@ def test_apply_matches_oracle(gpu, nx, ny, m, antisym):
     assert np.allclose(op.diagonal(), o.diagonal(), rtol=1e-14, atol=0)
 
 
+SMOOTH_SHAPES = [(18, 9, 8, (36, 18)), (5, 3, 7, (9, 6)), (2, 7, 6, (3, 16)), (10, 12, 12, (24, 24)),
+                 (37, 5, 4, (96, 9)), (70, 3, 2, (144, 6)), (90, 2, 3, (192, 3)), (18, 9, 64, (36, 18))]
+
+
+@pytest.mark.parametrize("nx,ny,m,L", SMOOTH_SHAPES)
+def test_smooth_embedding_apply(gpu, nx, ny, m, L):
+    """Mixed-radix (2^a 3^b) circulant embedding: a different exact embedding
+    of the same operator, so it must agree with the reference's pow2 one."""
+    rep = rep_for(nx, ny, m, seed=nx + ny)
+    op = ToeplitzMatvec(rep, embed="smooth")
+    inf = op.info()
+    assert (inf.L0, inf.L1) == L
+    o = oracle.Oracle.from_rep(rep)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(o.n) + 1j * rng.standard_normal(o.n)
+    assert rel(op.apply(x), o.apply(x)) < MATVEC_TOL
+    assert rel(op.applyA(x), o.applyA(x)) < MATVEC_TOL
+    op3 = ToeplitzMatvec(rep, embed="smooth", max_nrhs=9)
+    X = gen.rhs_normal(o.n, 9, 4)
+    Y = op3.apply(X)
+    for c in (0, 8):
+        assert rel(Y[:, c], o.apply(np.ascontiguousarray(X[:, c]))) < MATVEC_TOL
+
+
 def test_spectra_bins_match_reference_layout(gpu):
     nx, ny, m = 5, 3, 6
     rep = rep_for(nx, ny, m, antisym=False)
@@ -104,7 +128,8 @@ def fft_path(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("nx,ny,m,k", [(6, 5, 64, 3), (5, 4, 8, 3), (4, 4, 24, 2), (9, 5, 128, 2), (3, 5, 7, 4)])
+@pytest.mark.parametrize("nx,ny,m,k", [(6, 5, 64, 3), (5, 4, 8, 3), (4, 4, 24, 2), (9, 5, 128, 2), (3, 5, 7, 4),
+                                       (6, 5, 64, 9), (5, 3, 128, 60), (7, 4, 64, 57)])
 def test_multi_rhs_apply(gpu, fft_path, nx, ny, m, k):
     rep = rep_for(nx, ny, m)
     op = ToeplitzMatvec(rep, max_nrhs=k)
@@ -128,6 +153,25 @@ def test_gmres_single_column_small(gpu, fft_path, orthog):
     r = o.gmres(b, tol=1e-9, max_iter=500, restart=12)
     assert g.iterations == r["iterations"]
     hist_close(g.history[0], r["history"][0], GMRES_TOL)
+
+
+@pytest.mark.parametrize("embed", ["pow2", "smooth"])
+def test_c3_ports_apply(gpu, embed):
+    """C3 (two 9x9 arrays as 18x9, m = 128, 162 unit port columns): the
+    bin product is the DMMA batched GEMM; sampled columns vs the oracle.
+    The smooth embedding is 36 x 18 bins instead of 64 x 32."""
+    cfg = CONFIGS["C3"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep, max_nrhs=cfg.nrhs, embed=embed)
+    V = np.asarray(rhs_for(cfg))
+    assert V.shape == (cfg.n, 162)
+    Y = op.apply(V)
+    o = oracle.Oracle.from_rep(rep, nthreads=0)
+    for c in [0, 17, 80, 161]:
+        assert rel(Y[:, c], o.apply(np.ascontiguousarray(V[:, c]))) < MATVEC_TOL
+    # linearity across columns: Z (V a) = (Z V) a
+    a = gen.rhs_normal(162, 1, 5)[:, 0]
+    assert rel(op.apply(V @ a), Y @ a) < 1e-12
 
 
 def test_user_errors(gpu):

@@ -1,0 +1,67 @@
+// FP64 throughput on the B200: DFMA (vector) vs mma.sync.m8n8k4.f64 (DMMA).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 fp64test.cu -o fp64test
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dfma(double* out, int iters) {
+  double a[8], b = 1.0000001, c = 0.9999999;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void dmma(double* out, int iters) {
+  double acc[4][2];
+  double af = 1.0 + threadIdx.x * 1e-6, bf = 0.5;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(acc[k][0]), "+d"(acc[k][1])
+                   : "d"(af), "d"(bf));
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += acc[k][0] + acc[k][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+  double* out;
+  cudaMalloc(&out, 8);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 20000;
+  for (int bpsm : {1, 2, 4, 8}) {
+    dim3 g(sms * bpsm), t(256);
+    dfma<<<g, t>>>(out, 100);
+    cudaEventRecord(a);
+    dfma<<<g, t>>>(out, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    double flops = 2.0 * 8 * iters * (double)g.x * t.x;
+    printf("DFMA  %d CTA/SM: %.1f TFLOP/s\n", bpsm, flops / (ms * 1e-3) / 1e12);
+    dmma<<<g, t>>>(out, 100);
+    cudaEventRecord(a);
+    dmma<<<g, t>>>(out, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    flops = 2.0 * 256 * 4 * iters * (double)g.x * (t.x / 32);
+    printf("DMMA  %d CTA/SM: %.1f TFLOP/s\n", bpsm, flops / (ms * 1e-3) / 1e12);
+  }
+  printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+}

@@ -18,22 +18,35 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--nocorr", action="store_true")
+ap.add_argument("--embed", default="pow2")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 rep = ToeplitzRep.synthetic(cfg)
 if args.nocorr:
     rep.correction = None
-op = ToeplitzMatvec(rep)
+op = ToeplitzMatvec(rep, max_nrhs=cfg.nrhs, embed=args.embed)
 _st = torch.cuda.Stream()
 op.set_stream(_st.cuda_stream)
 torch.cuda.set_stream(_st)
-x = torch.from_numpy(np.asarray(gen.rhs_normal(cfg.n, 1, 3)[:, 0]).copy()).cuda()
+K = cfg.nrhs
+x = torch.from_numpy(np.asfortranarray(gen.rhs_normal(cfg.n, K, 3)).T.copy()).cuda()  # column-major n x K
 y = torch.empty_like(x)
 for _ in range(args.iters):
-    op.apply_device(x.data_ptr(), y.data_ptr())
+    op.apply_device(x.data_ptr(), y.data_ptr(), K)
 torch.cuda.synchronize()
 print("ok", args.config, float(y.abs().sum()))
 
+if K > 1:
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        op.apply_device(x.data_ptr(), y.data_ptr(), K)
+    e.record(); e.synchronize()
+    ms = s.elapsed_time(e) / 10
+    flops = 8.0 * cfg.m * cfg.m * K * op.info().bins
+    print(f"nrhs={K}: {ms:.3f} ms per batched apply, {K / ms * 1e3:.0f} column-matvecs/s, "
+          f"bin-product {flops / (ms * 1e-3) / 1e12:.1f} TFLOP/s equivalent over the whole apply")
+    sys.exit(0)
 if "--phases" in sys.argv or True:
     import statistics
     op.phase_times(True)
