@@ -147,8 +147,8 @@ typedef struct {
   int binprod_kernel;          /* K3 variant id                           */
   int kernels_per_apply;       /* launches of one tbt_apply (nrhs = 1)    */
   int has_antisym;             /* Z(0,0) not symmetric: block-diag fixup  */
-  int apply_path;              /* 2 persistent single kernel, 1 cluster-fused
-                                  transforms, 0 line passes                */
+  int apply_path;              /* 3 distributed, 2 persistent single kernel,
+                                  1 cluster-fused transforms, 0 line passes */
 } tbt_info;
 tbt_status tbt_get_info(const tbt_ctx* ctx, tbt_info* info);
 
@@ -163,6 +163,21 @@ tbt_status tbt_get_spectrum_bin(tbt_ctx* ctx, long long f, double* out);
  * summed K3 milliseconds and the number of timed launches since enabling. */
 tbt_status tbt_set_timing(tbt_ctx* ctx, int on);
 tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
+
+/* ---- Multi-GPU: one process per GPU, the operator sharded over nranks ----
+ * Element rows are split in contiguous slabs (vectors); level-0 bin columns
+ * in groups closed under s0 -> L0-s0 (Fourier blocks, ~1/nranks each); the
+ * two FFT transposes are grouped ncclSend/ncclRecv all-to-alls. No
+ * reference counterpart. Call sequence on every rank:
+ * tbt_create -> tbt_set_generators (all blocks) -> [tbt_set_correction] ->
+ * tbt_dist_init -> tbt_precompute; tbt_apply/tbt_apply_a/tbt_diagonal then
+ * take and return this rank's row slab (tbt_dist_rows). */
+tbt_status tbt_dist_unique_id(char* id /* NCCL_UNIQUE_ID_BYTES = 128 */);
+tbt_status tbt_dist_init(tbt_ctx* ctx, int nranks, int rank, const char* id);
+tbt_status tbt_dist_rows(const tbt_ctx* ctx, int* row_begin, int* row_end);
+/* The partition itself (host only, no device needed). */
+tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin,
+                         int* row_end, int* ncols, int* cols);
 
 /* Phase timing of the persistent single-kernel apply: `on` arms
  * %globaltimer stamps (CTA 0) at its phase boundaries for later applies;

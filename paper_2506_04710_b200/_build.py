@@ -69,7 +69,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 sys.stderr.write(r.stderr)
     objs = [BUILD / (s.stem + ".o") for s in cus] + [BUILD / (s.stem + ".cpp.o") for s in cpps]
     if force or _needs(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

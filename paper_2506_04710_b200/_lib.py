@@ -61,6 +61,10 @@ SIGNATURES = {
     "tbt_get_spectrum_bin": (C.c_int, [C.c_void_p, C.c_longlong, dp]),
     "tbt_bench_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, dp, dp]),
     "tbt_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "tbt_dist_unique_id": (C.c_int, [C.c_char_p]),
+    "tbt_dist_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
+    "tbt_dist_rows": (C.c_int, [C.c_void_p, ip, ip]),
+    "tbt_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, ip, ip, ip, ip]),
     "tbt_phase_times": (C.c_int, [C.c_void_p, C.c_int, dp]),
     "tbt_timing_read": (C.c_int, [C.c_void_p, dp, ip]),
     "tbtgen_num_blocks": (C.c_longlong, [C.c_int, C.c_int]),

@@ -144,7 +144,7 @@ void requireReady(const Ctx& c) {
 // One single-column apply, replayed from the cached CUDA graph unless K3
 // timing is on.
 void runApply1(Ctx& c, const double2* x, double2* y, bool withCorr) {
-  if (c.timeBinprod) {
+  if (c.timeBinprod || c.dist) {
     applyInternal(c, x, y, 1, withCorr);
     return;
   }
@@ -290,6 +290,7 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dGridBar), static_cast<void*>(c.dPhaseNs), static_cast<void*>(c.dBarFlags)})
     freePtr(p);
   c.dropGraph();
+  distFree(c);
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);
   if (c.evBinA) cudaEventDestroy(c.evBinA);
@@ -479,7 +480,8 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
     TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, "tbt_apply: nrhs outside [1, max_nrhs]");
     TBT_USER_CHECK(where == TBT_HOST || where == TBT_DEVICE, "tbt_apply: bad memory kind");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
-    const long long total = c.n * nrhs;
+    const long long nloc = c.dist ? static_cast<long long>(c.myRows) * c.nx * c.m : c.n;
+    const long long total = nloc * nrhs;
     const size_t bytes = total * sizeof(double2);
     const double2* xin = reinterpret_cast<const double2*>(x);
     double2* yout = reinterpret_cast<double2*>(y);
@@ -488,7 +490,7 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
         TBT_CUDA_CHECK(cudaMemcpyAsync(c.dXin, xin, bytes, cudaMemcpyHostToDevice, c.stream));
       } else {
         TBT_CUDA_CHECK(cudaMemcpyAsync(c.dYout, xin, bytes, cudaMemcpyHostToDevice, c.stream));
-        launchLayout(c.dYout, c.dXin, c.n, nrhs, true, c.stream, c.m);
+        launchLayout(c.dYout, c.dXin, nloc, nrhs, true, c.stream, c.m);
       }
       if (nrhs == 1)
         runApply1(c, c.dXin, c.dYout, withCorr);
@@ -497,7 +499,7 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
       if (nrhs == 1) {
         TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dYout, bytes, cudaMemcpyDeviceToHost, c.stream));
       } else {
-        launchLayout(c.dYout, c.dXin, c.n, nrhs, false, c.stream, c.m);
+        launchLayout(c.dYout, c.dXin, nloc, nrhs, false, c.stream, c.m);
         TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dXin, bytes, cudaMemcpyDeviceToHost, c.stream));
       }
       TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -505,9 +507,9 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
       if (nrhs == 1) {
         runApply1(c, xin, yout, withCorr);
       } else {
-        launchLayout(xin, c.dXin, c.n, nrhs, true, c.stream, c.m);
+        launchLayout(xin, c.dXin, nloc, nrhs, true, c.stream, c.m);
         applyInternal(c, c.dXin, c.dYout, nrhs, withCorr);
-        launchLayout(c.dYout, yout, c.n, nrhs, false, c.stream, c.m);
+        launchLayout(c.dYout, yout, nloc, nrhs, false, c.stream, c.m);
       }
     }
   });
@@ -528,7 +530,9 @@ tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
     requireReady(c);
     std::vector<double2> dd;
     refreshDiagonal(c, &dd);
-    std::memcpy(d, dd.data(), dd.size() * sizeof(double2));
+    const size_t first = c.dist ? static_cast<size_t>(c.myRow0) * c.nx * c.m : 0;
+    const size_t count = c.dist ? static_cast<size_t>(c.myRows) * c.nx * c.m : dd.size();
+    std::memcpy(d, dd.data() + first, count * sizeof(double2));
   });
 }
 
@@ -538,6 +542,7 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
   tbt_status st = guarded([&] {
     TBT_USER_CHECK(h && b && x && opts, "tbt_gmres: null argument");
     Ctx& c = h->c;
+    TBT_USER_CHECK(!c.dist, "tbt_gmres: not available on a distributed context yet (apply is)");
     requireReady(c);
     TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, "tbt_gmres: nrhs outside [1, max_nrhs]");
     TBT_USER_CHECK(opts->restart >= 1 && opts->max_iter >= 0 && opts->tol > 0.0, "tbt_gmres: bad options");
@@ -610,12 +615,12 @@ tbt_status tbt_get_info(const tbt_ctx* h, tbt_info* info) {
     info->L1 = c.L1;
     info->spectra_bytes = c.npairs * static_cast<long long>(c.m) * c.m * 16;
     info->binprod_kernel = c.binprodKernel;
-    const bool pers = c.persistent && persistentSupported(c);
+    const bool pers = !c.dist && c.persistent && persistentSupported(c);
     const bool fused = !pers && c.fused2d && !c.forceMultiPass;
     info->kernels_per_apply = pers ? 1
                               : fused ? 3 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? 1 : 0)
                                       : 5 + (c.hasAntisym ? 1 : 0) + (c.haveCorr ? (c.rank > 0 ? 2 : 1) : 0);
-    info->apply_path = pers ? 2 : (fused ? 1 : 0);
+    info->apply_path = c.dist ? 3 : (pers ? 2 : (fused ? 1 : 0));
     info->has_antisym = c.hasAntisym ? 1 : 0;
   });
 }
@@ -662,6 +667,78 @@ tbt_status tbt_timing_read(tbt_ctx* h, double* total, int* count) {
     }
     *total = sum;
     *count = c.tCount;
+  });
+}
+
+tbt_status tbt_dist_unique_id(char* id) {
+  return guarded([&] {
+    TBT_USER_CHECK(id, "tbt_dist_unique_id: null argument");
+    ncclUniqueId u;
+    const ncclResult_t r = nccl().getUniqueId(&u);
+    if (r != ncclSuccess) throw Error{TBT_CUDA_ERROR, std::string("ncclGetUniqueId: ") + nccl().errorString(r)};
+    std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin, int* row_end, int* ncols,
+                         int* cols) {
+  return guarded([&] {
+    TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks && ny >= 1 && L0 >= 1, "tbt_dist_plan: bad arguments");
+    std::vector<int> rs;
+    std::vector<std::vector<int>> cl;
+    distPlan(ny, L0, nranks, rs, cl);
+    if (row_begin) *row_begin = rs[rank];
+    if (row_end) *row_end = rs[rank + 1];
+    if (ncols) *ncols = static_cast<int>(cl[rank].size());
+    if (cols) std::copy(cl[rank].begin(), cl[rank].end(), cols);
+  });
+}
+
+tbt_status tbt_dist_init(tbt_ctx* h, int nranks, int rank, const char* id) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && id, "tbt_dist_init: null argument");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
+    TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "tbt_dist_init: bad rank");
+    TBT_USER_CHECK(nranks <= c.L0, "tbt_dist_init: more ranks than level-0 bins");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    distFree(c);
+    c.dropGraph();
+    c.nranks = nranks;
+    c.myRank = rank;
+    distPlan(c.ny, c.L0, nranks, c.rowStart, c.colsOfRank);
+    c.myRow0 = c.rowStart[rank];
+    c.myRows = c.rowStart[rank + 1] - c.rowStart[rank];
+    c.myColList = c.colsOfRank[rank];
+    c.colsOffset.assign(nranks + 1, 0);
+    std::vector<int> flat;
+    for (int q = 0; q < nranks; ++q) {
+      flat.insert(flat.end(), c.colsOfRank[q].begin(), c.colsOfRank[q].end());
+      c.colsOffset[q + 1] = static_cast<int>(flat.size());
+    }
+    const long long B = static_cast<long long>(c.maxNrhs) * c.m;
+    const long long myCols = static_cast<long long>(c.myColList.size());
+    TBT_CUDA_CHECK(cudaMalloc(&c.dColsOfRank, flat.size() * sizeof(int)));
+    TBT_CUDA_CHECK(cudaMemcpy(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dTrow, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dSend, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dTcol, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dRecv, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dXfull, c.ne * B * sizeof(double2)));
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    const ncclResult_t r = nccl().commInitRank(&c.comm, nranks, u, rank);
+    if (r != ncclSuccess) throw Error{TBT_CUDA_ERROR, std::string("ncclCommInitRank: ") + nccl().errorString(r)};
+    c.dist = true;
+  });
+}
+
+tbt_status tbt_dist_rows(const tbt_ctx* h, int* row_begin, int* row_end) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && row_begin && row_end, "tbt_dist_rows: null argument");
+    const Ctx& c = h->c;
+    *row_begin = c.dist ? c.myRow0 : 0;
+    *row_end = c.dist ? c.myRow0 + c.myRows : c.ny;
   });
 }
 

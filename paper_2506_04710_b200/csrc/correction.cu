@@ -144,9 +144,11 @@ void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs) {
   TBT_CUDA_CHECK(cudaGetLastError());
 }
 
-void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs) {
+void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs, int nElems) {
   if (!c.hasAntisym) return;
-  dim3 grid(c.ne, nrhs);
+  if (nElems < 0) nElems = c.ne;
+  if (nElems == 0) return;
+  dim3 grid(nElems, nrhs);
   antisymApply<<<grid, 64, c.m * sizeof(double2), c.stream>>>(c.dAntisym, x, y, c.m, nrhs);
   TBT_CUDA_CHECK(cudaGetLastError());
 }

@@ -105,17 +105,33 @@ void buildSpectra(Ctx& c) {
   }
 
   // Bin pairs: f and its partner -f; representatives are f <= partner.
+  // Distributed: only the columns this rank owns (closed under s0 -> -s0,
+  // dist.cu), bins renumbered to the rank's local [s1][j] layout.
+  std::vector<int> colPos(c.L0, -1);
+  int nLocalCols = c.L0;
+  if (c.dist) {
+    nLocalCols = static_cast<int>(c.myColList.size());
+    for (int j = 0; j < nLocalCols; ++j) colPos[c.myColList[j]] = j;
+  } else {
+    for (int j = 0; j < c.L0; ++j) colPos[j] = j;
+  }
+  auto localBin = [&](long long f) {
+    return static_cast<int>((f / c.L0) * nLocalCols + colPos[f % c.L0]);
+  };
   c.pairF.clear();
   c.pairG.clear();
+  std::vector<int> pairFGlobal;
   c.pairOfBin.assign(static_cast<size_t>(c.L), 0);
   for (long long f = 0; f < c.L; ++f) {
     const int s1 = static_cast<int>(f / c.L0), s0i = static_cast<int>(f % c.L0);
+    if (colPos[s0i] < 0) continue;
     const long long g = static_cast<long long>((c.L1 - s1) % c.L1) * c.L0 + (c.L0 - s0i) % c.L0;
     if (f <= g) {
       c.pairOfBin[f] = static_cast<long long>(c.pairF.size());
       if (g != f) c.pairOfBin[g] = -(static_cast<long long>(c.pairF.size()) + 1);
-      c.pairF.push_back(static_cast<int>(f));
-      c.pairG.push_back(static_cast<int>(g));
+      c.pairF.push_back(localBin(f));
+      c.pairG.push_back(localBin(g));
+      pairFGlobal.push_back(static_cast<int>(f));
     }
   }
   c.npairs = static_cast<long long>(c.pairF.size());
@@ -125,11 +141,14 @@ void buildSpectra(Ctx& c) {
   if (c.dPairG) cudaFree(c.dPairG);
   c.dSpectra = nullptr;
   c.dPairF = c.dPairG = nullptr;
-  TBT_CUDA_CHECK(cudaMalloc(&c.dSpectra, c.npairs * mm * sizeof(double2)));
-  TBT_CUDA_CHECK(cudaMalloc(&c.dPairF, c.npairs * sizeof(int)));
-  TBT_CUDA_CHECK(cudaMalloc(&c.dPairG, c.npairs * sizeof(int)));
+  int* dPairFGlobal = nullptr;
+  TBT_CUDA_CHECK(cudaMalloc(&c.dSpectra, std::max<long long>(c.npairs, 1) * mm * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dPairF, std::max<long long>(c.npairs, 1) * sizeof(int)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dPairG, std::max<long long>(c.npairs, 1) * sizeof(int)));
+  TBT_CUDA_CHECK(cudaMalloc(&dPairFGlobal, std::max<long long>(c.npairs, 1) * sizeof(int)));
   TBT_CUDA_CHECK(cudaMemcpyAsync(c.dPairF, c.pairF.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
   TBT_CUDA_CHECK(cudaMemcpyAsync(c.dPairG, c.pairG.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
+  TBT_CUDA_CHECK(cudaMemcpyAsync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
 
   // Generators and S0 on the device for the gather.
   double2 *dGen = nullptr, *dS0 = nullptr, *dG = nullptr;
@@ -169,13 +188,14 @@ void buildSpectra(Ctx& c) {
     pb.batch = static_cast<int>(B);
     pb.tw = c.dTw1;
     launchFftPass(pb, s);
-    scatterPairs<<<sms * 8, 256, 0, s>>>(dG, c.dPairF, c.dSpectra, c.npairs, m, a0, r);
+    if (c.npairs > 0) scatterPairs<<<sms * 8, 256, 0, s>>>(dG, dPairFGlobal, c.dSpectra, c.npairs, m, a0, r);
     TBT_CUDA_CHECK(cudaGetLastError());
   }
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(dG);
   cudaFree(dS0);
   cudaFree(dGen);
+  cudaFree(dPairFGlobal);
 }
 
 }  // namespace tbt

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cstdint>
 #include <string>
@@ -112,6 +113,24 @@ struct Ctx {
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
 
+  // Multi-GPU (dist.cu): this rank owns element rows [myRow0, myRow0 +
+  // myRows) of the vectors and the bin columns myColList (closed under
+  // s0 -> L0 - s0, so both bins of every stored pair are local).
+  bool dist = false;
+  int nranks = 1, myRank = 0;
+  ncclComm_t comm = nullptr;
+  std::vector<int> rowStart;                  // [nranks+1]
+  std::vector<std::vector<int>> colsOfRank;   // [nranks]
+  std::vector<int> myColList;
+  int myRow0 = 0, myRows = 0;
+  int* dColsOfRank = nullptr;                 // concatenated column lists
+  std::vector<int> colsOffset;                // [nranks+1] offsets into dColsOfRank
+  double2* dTrow = nullptr;   // [myRows][L0][B]
+  double2* dTcol = nullptr;   // [ny][myCols][B]
+  double2* dSend = nullptr;
+  double2* dRecv = nullptr;
+  double2* dXfull = nullptr;  // [ne][B] all-gathered x for the correction
+
   // Generators (host copy kept for diagonal / K) and spectra.
   std::vector<double2> genHost;
   bool haveGenerators = false, havePrecompute = false;
@@ -184,7 +203,7 @@ constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
-void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs);     // correction.cu
+void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs, int nElems = -1);  // correction.cu
 void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s, int m);  // apply.cu
 
 // GMRES (gmres.cu): per-column state mirrored to the host.
@@ -194,6 +213,23 @@ struct GmresState {
 };
 void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres_opts& o, bool useAOnly,
                 std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs);
+
+// Multi-GPU (dist.cu). NCCL entry points resolved at run time.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl();
+void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols);
+void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);
+void distFree(Ctx& c);
 
 // Persistent single-kernel apply (matvec_persistent.cu).
 bool persistentSupported(const Ctx& c);

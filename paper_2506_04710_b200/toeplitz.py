@@ -109,9 +109,13 @@ def _as_cols(x: np.ndarray) -> tuple[np.ndarray, int, bool]:
 class ToeplitzMatvec:
     """FFT-accelerated application of Z^part (linsolve.hpp:59-77) on a B200."""
 
-    def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0, embed: str = "pow2"):
+    def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0, embed: str = "pow2",
+                 dist: tuple | None = None):
         """embed: "pow2" (the reference's nextPow2 embedding) or "smooth"
-        (smallest 2^a 3^b length per level, mixed-radix transforms)."""
+        (smallest 2^a 3^b length per level, mixed-radix transforms).
+        dist: (nranks, rank, nccl_unique_id_bytes) to shard the operator over
+        one process per GPU (see dist_unique_id / init_from_torch); apply /
+        applyA / diagonal then work on this rank's element-row slab."""
         self.rep = rep
         self._h = C.c_void_p()
         if embed not in ("pow2", "smooth"):
@@ -128,6 +132,9 @@ class ToeplitzMatvec:
             _check(lib().tbt_set_correction(self._h, c.rank, d.ctypes.data_as(dp),
                                             u.ctypes.data_as(dp) if u is not None else None,
                                             v.ctypes.data_as(dp) if v is not None else None))
+        if dist is not None:
+            nranks, rank, uid = dist
+            _check(lib().tbt_dist_init(self._h, int(nranks), int(rank), bytes(uid)))
         _check(lib().tbt_precompute(self._h))
         self.max_nrhs = max_nrhs
 
@@ -144,7 +151,15 @@ class ToeplitzMatvec:
 
     # -- reference methods -------------------------------------------------
     def sizeA(self) -> int:
-        return int(lib().tbt_size_a(self._h))
+        """Unknowns held by this process (the row slab when distributed)."""
+        r0, r1 = self.rows()
+        return (r1 - r0) * self.rep.nx * self.rep.m
+
+    def rows(self) -> tuple[int, int]:
+        """Element rows [begin, end) this process owns (all rows unless distributed)."""
+        a, b = C.c_int(), C.c_int()
+        _check(lib().tbt_dist_rows(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def sizeM(self) -> int:
         return 0  # margin unknowns are folded into the synthetic correction
@@ -234,6 +249,31 @@ class ToeplitzMatvec:
         histories = [hist[c, :min(int(hlen[c]), hist_cap)].copy() for c in range(k)]
         cur = None if x is None else (x[:, 0] if vec else x)
         return SolveResult(cur, res.tolist(), its.tolist(), "gmres", conv.tolist(), histories, st.matvecs)
+
+
+def dist_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for tbt_dist_init (call on rank 0)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().tbt_dist_unique_id(buf))
+    return buf.raw
+
+
+def dist_plan(ny: int, L0: int, nranks: int, rank: int):
+    """(row_begin, row_end, columns) of `rank` in the multi-GPU partition."""
+    rb, re_, nc = C.c_int(), C.c_int(), C.c_int()
+    cols = (C.c_int * max(L0, 1))()
+    _check(lib().tbt_dist_plan(ny, L0, nranks, rank, C.byref(rb), C.byref(re_), C.byref(nc), cols))
+    return rb.value, re_.value, [cols[k] for k in range(nc.value)]
+
+
+def init_from_torch(group=None) -> tuple:
+    """(nranks, rank, uid) for ToeplitzMatvec(dist=...) from an initialised
+    torch.distributed process group (rank 0 makes the id, all receive it)."""
+    import torch.distributed as tdist
+    rank, world = tdist.get_rank(group), tdist.get_world_size(group)
+    obj = [dist_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0, group=group)
+    return world, rank, obj[0]
 
 
 def toeplitz_matvec(rep: ToeplitzRep, x) -> np.ndarray:
