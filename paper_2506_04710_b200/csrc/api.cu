@@ -287,7 +287,8 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dT),
                   static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
                   static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv), static_cast<void*>(c.dDiagInvA),
-                  static_cast<void*>(c.dGridBar), static_cast<void*>(c.dPhaseNs), static_cast<void*>(c.dBarFlags)})
+                  static_cast<void*>(c.dGridBar), static_cast<void*>(c.dPhaseNs), static_cast<void*>(c.dBarFlags),
+                  static_cast<void*>(c.dGen)})
     freePtr(p);
   c.dropGraph();
   distFree(c);
@@ -333,9 +334,17 @@ tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblock
     TBT_USER_CHECK(nblocks == want, "tbt_set_generators: expected " + std::to_string(want) +
                                         " canonical blocks (nx*ny + (nx-1)*(ny-1)), got " +
                                         std::to_string(nblocks));
-    const size_t cnt = static_cast<size_t>(want) * c.m * c.m;
-    c.genHost.resize(cnt);
-    std::memcpy(static_cast<void*>(c.genHost.data()), blocks, cnt * sizeof(double2));
+    // Blocks go straight to the device (freed after tbt_precompute); the host
+    // keeps only Z(0,0) for the diagonal and the antisymmetric split, so a
+    // 19 GB generator set (C5) is not duplicated in host memory.
+    const size_t mm = static_cast<size_t>(c.m) * c.m;
+    const size_t cnt = static_cast<size_t>(want) * mm;
+    c.genHost.assign(reinterpret_cast<const double2*>(blocks), reinterpret_cast<const double2*>(blocks) + mm);
+    if (c.dGen) cudaFree(c.dGen);
+    c.dGen = nullptr;
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dGen, cnt * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMemcpy(c.dGen, blocks, cnt * sizeof(double2), cudaMemcpyHostToDevice));
     c.haveGenerators = true;
     c.havePrecompute = false;
   });
@@ -463,11 +472,14 @@ tbt_status tbt_precompute(tbt_ctx* h) {
   return guarded([&] {
     TBT_USER_CHECK(h, "tbt_precompute: null context");
     Ctx& c = h->c;
-    TBT_USER_CHECK(c.haveGenerators, "tbt_precompute: call tbt_set_generators first");
+    TBT_USER_CHECK(c.haveGenerators && c.dGen, "tbt_precompute: call tbt_set_generators first");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     c.dropGraph();
     buildSpectra(c);
     refreshDiagonal(c, nullptr);
+    cudaFree(c.dGen);
+    c.dGen = nullptr;
+    c.haveGenerators = false;  // a new precompute needs the blocks again
     c.havePrecompute = true;
   });
 }

@@ -79,7 +79,7 @@ __global__ void scatterPairs(const double2* __restrict__ G, const int* __restric
 void buildSpectra(Ctx& c) {
   const int m = c.m, nx = c.nx, ny = c.ny;
   const long long mm = static_cast<long long>(m) * m;
-  const long long nb = static_cast<long long>(nx) * ny + static_cast<long long>(nx - 1) * (ny - 1);
+  // canonical generator blocks: c.dGen (tbt_set_generators)
   cudaStream_t s = c.stream;
 
   // Split Z(0,0) into symmetric / antisymmetric parts on the host.
@@ -151,10 +151,9 @@ void buildSpectra(Ctx& c) {
   TBT_CUDA_CHECK(cudaMemcpyAsync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
 
   // Generators and S0 on the device for the gather.
-  double2 *dGen = nullptr, *dS0 = nullptr, *dG = nullptr;
-  TBT_CUDA_CHECK(cudaMalloc(&dGen, nb * mm * sizeof(double2)));
+  const double2* dGen = c.dGen;
+  double2 *dS0 = nullptr, *dG = nullptr;
   TBT_CUDA_CHECK(cudaMalloc(&dS0, mm * sizeof(double2)));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(dGen, c.genHost.data(), nb * mm * sizeof(double2), cudaMemcpyHostToDevice, s));
   TBT_CUDA_CHECK(cudaMemcpyAsync(dS0, s0.data(), mm * sizeof(double2), cudaMemcpyHostToDevice, s));
 
   // Row chunks bounded to ~4 GiB of transform workspace.
@@ -194,7 +193,6 @@ void buildSpectra(Ctx& c) {
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(dG);
   cudaFree(dS0);
-  cudaFree(dGen);
   cudaFree(dPairFGlobal);
 }
 

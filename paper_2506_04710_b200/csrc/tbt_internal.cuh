@@ -132,7 +132,8 @@ struct Ctx {
   double2* dXfull = nullptr;  // [ne][B] all-gathered x for the correction
 
   // Generators (host copy kept for diagonal / K) and spectra.
-  std::vector<double2> genHost;
+  std::vector<double2> genHost;   // only the self block Z(0,0) (m*m, column-major)
+  double2* dGen = nullptr;        // all canonical blocks on the device until tbt_precompute
   bool haveGenerators = false, havePrecompute = false;
   long long npairs = 0;
   double2* dSpectra = nullptr;    // [npairs][m][m] row-major
