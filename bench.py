@@ -225,25 +225,38 @@ def main():
 
     clocks = ClockSampler(local)
     with clocks:
-        # ---- value: K device-resident applies, L2 flushed (untimed) between steps
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        # ---- value: K back-to-back device-resident applies (the GMRES usage
+        # pattern). The dominant input, the half spectrum (134 MB at C2), is
+        # larger than L2 (126 MB) and is streamed with an evict-first policy,
+        # so every step reads it from HBM.
         barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
+            e0.record(stream)
             for k in range(K):
-                l2_flush(flush, k)
-                ev0[k].record(stream)
                 op.apply_device(x.data_ptr(), y.data_ptr())
-                ev1[k].record(stream)
+            e1.record(stream)
         stream.synchronize()
         barrier()
-        step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-        total_ms = sum(step_ms)
+        total_ms = e0.elapsed_time(e1)
         if dist is not None:
             t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
         value = world * K / (total_ms / 1e3)
+
+        # ---- cold-L2 step time (reported beside): L2 flushed between steps
+        kc = min(K, 200)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(kc)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(kc)]
+        with torch.cuda.stream(stream):
+            for k in range(kc):
+                l2_flush(flush, k)
+                ev0[k].record(stream)
+                op.apply_device(x.data_ptr(), y.data_ptr())
+                ev1[k].record(stream)
+        stream.synchronize()
+        cold_ms = statistics.median(a.elapsed_time(b) for a, b in zip(ev0, ev1))
 
         # ---- roofline of the dominant kernel
         if info.apply_path == 2:
@@ -353,11 +366,15 @@ def main():
         "value": value, "unit": "matvec/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": step_mean, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded generator, include/tbt_gen.h; paper geometries unavailable)",
-        "config": {"workload": workload_desc(cfg), "l2": "flushed between steps (256 MiB write + read-back, untimed)",
+        "config": {"workload": workload_desc(cfg),
+                   "l2": "inputs larger than L2: 134 MB half spectrum (> 126 MB L2) streamed evict-first every "
+                         "step; back-to-back applies (cold_l2_ms_per_step: same apply with a 256 MiB "
+                         "write + read-back L2 flush between steps)",
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "spectrum_storage": f"half (bin pairs): {info.pairs} blocks of {info.bins} bins"},
         "roofline": roof,
         "equivalent_full_spectrum_gbs": b_alg_full / (step_mean * 1e-3) / 1e9,
+        "cold_l2_ms_per_step": cold_ms,
         "e2e": {"value": e2e, "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16, "d2h_bytes_per_step": cfg.n * 16},
         "gpu_launches": K * info.kernels_per_apply,
         "clocks": clocks.summary(),
