@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "gmres_dev.cuh"
 #include "tbt_internal.cuh"
 
 namespace tbt {
@@ -259,6 +260,8 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       if (penv) c.prefetchAt = std::max(0, std::min(2, atoi(penv)));
       const char* fenv = getenv("TBT_FFT");
       c.forceMultiPass = fenv && std::string(fenv) == "passes";
+      const char* genv = getenv("TBT_GMRES");
+      c.forceUnfused = genv && std::string(genv) == "unfused";
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinB));
       c.binprodKernel = binprodVariant(c.m);
@@ -292,6 +295,7 @@ void tbt_destroy(tbt_ctx* h) {
     freePtr(p);
   c.dropGraph();
   distFree(c);
+  freeGmresWorkspace(c);
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);
   if (c.evBinA) cudaEventDestroy(c.evBinA);
@@ -376,6 +380,7 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     c.haveCorr = false;
     c.nTerms = c.nTargets = 0;
     c.dropGraph();
+    freeGmresWorkspace(c);
     if (d == nullptr) {
       if (c.havePrecompute) refreshDiagonal(c, nullptr);
       return;
@@ -475,6 +480,7 @@ tbt_status tbt_precompute(tbt_ctx* h) {
     TBT_USER_CHECK(c.haveGenerators && c.dGen, "tbt_precompute: call tbt_set_generators first");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     c.dropGraph();
+    freeGmresWorkspace(c);
     buildSpectra(c);
     refreshDiagonal(c, nullptr);
     cudaFree(c.dGen);
@@ -561,36 +567,37 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     const long long total = c.n * nrhs;
     const size_t bytes = total * sizeof(double2);
-    double2 *db = nullptr, *dx = nullptr;
-    TBT_CUDA_CHECK(cudaMalloc(&db, bytes));
-    TBT_CUDA_CHECK(cudaMalloc(&dx, bytes));
+    GmresWs* W = gmresWorkspace(c);
+    if (W->bufLen < total) {
+      if (W->bufB) cudaFree(W->bufB);
+      if (W->bufX) cudaFree(W->bufX);
+      W->bufB = W->bufX = nullptr;
+      W->bufLen = 0;
+      TBT_CUDA_CHECK(cudaMalloc(&W->bufB, bytes));
+      TBT_CUDA_CHECK(cudaMalloc(&W->bufX, bytes));
+      W->bufLen = total;
+    }
+    double2* db = W->bufB;
+    double2* dx = W->bufX;
     std::vector<GmresState> out;
     std::vector<double> hist;
     int matvecs = 0;
-    try {
-      const double2* bsrc = reinterpret_cast<const double2*>(b);
-      if (where == TBT_HOST) {
-        TBT_CUDA_CHECK(cudaMemcpyAsync(dx, bsrc, bytes, cudaMemcpyHostToDevice, c.stream));
-        launchLayout(dx, db, c.n, nrhs, true, c.stream, c.m);
-      } else {
-        launchLayout(bsrc, db, c.n, nrhs, true, c.stream, c.m);
-      }
-      gmresSolve(c, db, dx, nrhs, *opts, opts->use_a_only != 0, out, hist, matvecs);
-      double2* xdst = reinterpret_cast<double2*>(x);
-      if (where == TBT_HOST) {
-        launchLayout(dx, db, c.n, nrhs, false, c.stream, c.m);
-        TBT_CUDA_CHECK(cudaMemcpyAsync(xdst, db, bytes, cudaMemcpyDeviceToHost, c.stream));
-      } else {
-        launchLayout(dx, xdst, c.n, nrhs, false, c.stream, c.m);
-      }
-      TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    } catch (...) {
-      cudaFree(db);
-      cudaFree(dx);
-      throw;
+    const double2* bsrc = reinterpret_cast<const double2*>(b);
+    if (where == TBT_HOST) {
+      TBT_CUDA_CHECK(cudaMemcpyAsync(dx, bsrc, bytes, cudaMemcpyHostToDevice, c.stream));
+      launchLayout(dx, db, c.n, nrhs, true, c.stream, c.m);
+    } else {
+      launchLayout(bsrc, db, c.n, nrhs, true, c.stream, c.m);
     }
-    cudaFree(db);
-    cudaFree(dx);
+    gmresSolve(c, db, dx, nrhs, *opts, opts->use_a_only != 0, out, hist, matvecs);
+    double2* xdst = reinterpret_cast<double2*>(x);
+    if (where == TBT_HOST) {
+      launchLayout(dx, db, c.n, nrhs, false, c.stream, c.m);
+      TBT_CUDA_CHECK(cudaMemcpyAsync(xdst, db, bytes, cudaMemcpyDeviceToHost, c.stream));
+    } else {
+      launchLayout(dx, xdst, c.n, nrhs, false, c.stream, c.m);
+    }
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     if (stats) {
       const int cap = std::max(0, opts->hist_cap);
       for (int k = 0; k < nrhs; ++k) {

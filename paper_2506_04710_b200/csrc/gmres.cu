@@ -19,168 +19,15 @@
 #include <algorithm>
 #include <cmath>
 
-#include "grid_sync.cuh"
-#include "tbt_internal.cuh"
+#include <cstring>
+
+#include "gmres_dev.cuh"
 
 namespace tbt {
 
-struct GmresArgs {
-  int ncols, restart, maxIter, histCap, precondition;
-  double tol;
-  int ne, m;
-  GmresState* st;
-  double2* H;       // [ncols][(restart+1)*restart], H(i,j) at i + j*(restart+1)
-  double2* g;       // [ncols][restart+1]
-  double2* cs;      // [ncols][restart]
-  double2* sn;      // [ncols][restart]
-  double2* ycoef;   // [ncols][restart]
-  double* hist;     // [ncols][histCap][2]
-  double2* partial; // [2][ncols][grid]
-  unsigned long long* bar;  // monotonic grid-barrier counter
-  const double2* b;
-  double2* x;
-  const double2* ax;
-  double2* w;
-  double2* V;       // [restart+1][ne*ncols*m]
-  const double2* dinv;  // [ne*m] or null
-  int j;            // Arnoldi column of this launch
-};
-
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int FAST_K = 8;  // slots per thread in the register-resident Arnoldi
-constexpr int RMAX = 128;  // largest restart the staged Givens / solve support
-
-__device__ __forceinline__ void gridBarrier(unsigned long long* bar) { gridBarrierMono(bar); }
-
-__device__ __forceinline__ double2 shfl2(double2 v, int src) {
-  v.x = __shfl_sync(0xffffffffu, v.x, src);
-  v.y = __shfl_sync(0xffffffffu, v.y, src);
-  return v;
-}
-
-// Butterfly sum: every lane ends with the same bits.
-__device__ __forceinline__ double2 warpSum(double2 v) {
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
-  }
-  return v;
-}
-
-// Per-CTA partial of v written to part[blockIdx.x] (thread 0).
-__device__ __forceinline__ void blockPartial(double2 v, double2* scratch, double2* part) {
-  v = warpSum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) scratch[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double2 s = scratch[0];
-    for (int k = 1; k < kWarps; ++k) s = cadd(s, scratch[k]);
-    part[blockIdx.x] = s;
-  }
-}
-
-// Grid total of the partials, computed by each warp independently in a
-// fixed order (bitwise identical in every warp and CTA).
-__device__ __forceinline__ double2 warpTotal(const double2* part) {
-  const int lane = threadIdx.x & 31;
-  double2 s = make_double2(0.0, 0.0);
-  for (int k = lane; k < static_cast<int>(gridDim.x); k += 32) s = cadd(s, __ldcg(part + k));
-  return warpSum(s);
-}
-
-__device__ __forceinline__ double2* partSlot(const GmresArgs& A, int phase, int col) {
-  return A.partial + (static_cast<long long>(phase & 1) * A.ncols + col) * gridDim.x;
-}
-
-__device__ __forceinline__ long long slotIndex(long long s, int col, int ncols, int m) {
-  const long long e = s / m, a = s % m;
-  return (e * ncols + col) * m + a;
-}
-
-__device__ void pushHist(const GmresArgs& A, int col, double kind, double v) {
-  GmresState& st = A.st[col];
-  if (st.histLen < A.histCap) {
-    A.hist[(static_cast<long long>(col) * A.histCap + st.histLen) * 2] = kind;
-    A.hist[(static_cast<long long>(col) * A.histCap + st.histLen) * 2 + 1] = v;
-  }
-  st.histLen++;
-}
-
-__device__ __forceinline__ double cabs2(double2 a) { return hypot(a.x, a.y); }
-__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
-
-// Smith's complex division a / b.
-__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
-  if (fabs(b.x) >= fabs(b.y)) {
-    const double r = b.y / b.x, d = b.x + b.y * r;
-    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
-  }
-  const double r = b.x / b.y, d = b.x * r + b.y;
-  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
-}
-
-// Givens sweep for Arnoldi column j of one GMRES column (linsolve.cpp:472-501),
-// executed by one CTA: H(0..j, j), cs, sn staged in shared memory by all
-// threads, the sequential rotations by thread 0, results written back.
-// hcolIn (optional) already holds H(0..j, j) in shared memory.
-__device__ void givensStep(const GmresArgs& A, int col, int j, double hn, const double2* hcolIn,
-                           double2* sh /* >= 3*RMAX+4 */) {
-  const int ldh = A.restart + 1;
-  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
-  double2* cs = A.cs + static_cast<long long>(col) * A.restart;
-  double2* sn = A.sn + static_cast<long long>(col) * A.restart;
-  double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
-  double2* hc = sh;               // [j+2]
-  double2* scs = sh + RMAX + 2;   // [j]
-  double2* ssn = scs + RMAX;      // [j]
-  __syncthreads();
-  for (int t = threadIdx.x; t <= j; t += blockDim.x) hc[t] = hcolIn ? hcolIn[t] : H[t + j * ldh];
-  for (int t = threadIdx.x; t < j; t += blockDim.x) {
-    scs[t] = cs[t];
-    ssn[t] = sn[t];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    GmresState& st = A.st[col];
-    hc[j + 1] = make_double2(hn, 0.0);
-    for (int i = 0; i < j; ++i) {
-      const double2 a0 = hc[i], a1 = hc[i + 1];
-      hc[i] = cadd(cmul(scs[i], a0), cmul(ssn[i], a1));
-      hc[i + 1] = cadd(cmul(make_double2(-ssn[i].x, ssn[i].y), a0), cmul(cconj(scs[i]), a1));
-    }
-    const double2 hjj = hc[j], hj1 = hc[j + 1];
-    const double den = sqrt((hjj.x * hjj.x + hjj.y * hjj.y) + (hj1.x * hj1.x + hj1.y * hj1.y));
-    double2 c, s;
-    if (den == 0.0) {
-      c = make_double2(1.0, 0.0);
-      s = make_double2(0.0, 0.0);
-    } else {
-      c = make_double2(hjj.x / den, -hjj.y / den);
-      s = make_double2(hj1.x / den, -hj1.y / den);
-    }
-    cs[j] = c;
-    sn[j] = s;
-    hc[j] = cadd(cmul(c, hjj), cmul(s, hj1));
-    hc[j + 1] = make_double2(0.0, 0.0);
-    const double2 gj = g[j];
-    g[j] = cmul(c, gj);
-    const double2 gj1 = cmul(make_double2(-s.x, s.y), gj);
-    g[j + 1] = gj1;
-    st.iterations += 1;
-    st.ncount = j + 1;
-    const double rel = cabs2(gj1) / st.beta;
-    pushHist(A, col, 1.0, cabs2(gj1) / st.beta0);
-    if (rel < 0.1 * A.tol || !(hn > 0.0) || st.ncount >= A.restart || st.iterations >= A.maxIter) st.stopInner = 1;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t <= j + 1; t += blockDim.x) H[t + j * ldh] = hc[t];
-  __syncthreads();
-}
+using namespace gmresdev;
 
 __global__ void __launch_bounds__(kThreads) gmresInit(GmresArgs A) {
   __shared__ double2 scratch[kWarps];
@@ -369,157 +216,14 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldi1(GmresArgs A) {
   if (blockIdx.x == 0) givensStep(A, 0, j, hn, hcol, sh);
 }
 
-// One Arnoldi step j, single column, low-synchronisation MGS: the MGS
-// coefficients h_i = <v_i, (I - v_{i-1}v_{i-1}^H)...(I - v_0 v_0^H) w> are
-// obtained as h = (I + L)^{-1} c with c = V^H w and L the strictly lower
-// part of the basis Gram matrix V^H V (identical to the MGS sweep in exact
-// arithmetic; L accumulates one row per iteration). Three grid barriers per
-// step instead of j + 2:
-//   pass 1  per-CTA partials of c_k = <v_k, w> and S_jk = <v_j, v_k>
-//           (one warp per k, the CTA's row chunk of w and v_j in smem)
-//   -- barrier --  CTA k reduces dot k over the grid
-//   -- barrier --  every CTA: forward substitution for h (warp 0)
-//   pass 2  w' = w - V h, ||w'||^2
-//   -- barrier --  v_{j+1} = w' / ||w'||, Givens (CTA 0)
+// One Arnoldi step j, single column, low-synchronisation MGS (gmres_dev.cuh).
 __global__ void __launch_bounds__(kThreads) gmresArnoldiLS(GmresArgs A, double2* S, double2* dots,
                                                            double2* dotPart) {
-  extern __shared__ double2 shw[];  // [chunk] w, [chunk] v_j, [RMAX+1] c/h, [(RMAX+1)] S row staging
+  extern __shared__ double2 shw[];
   __shared__ double2 scratch[kWarps];
   __shared__ double2 hcol[RMAX + 2];
   __shared__ double2 sh[3 * RMAX + 4];
-  const int run = A.st[0].cycleActive && !A.st[0].stopInner;
-  if (!run) return;  // uniform over the grid
-  const int j = A.j;
-  const int lds = A.restart + 1;
-  const long long n = static_cast<long long>(A.ne) * A.m;
-  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
-  const long long r0 = blockIdx.x * chunk;
-  const int cnt = static_cast<int>(r0 >= n ? 0 : (n - r0 < chunk ? n - r0 : chunk));
-  double2* ws = shw;
-  double2* vj = shw + chunk;
-  double2* cv = vj + chunk;  // [j+1] totals of c, later h
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double2* Vj = A.V + static_cast<long long>(j) * n;
-  for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-    double2 wv = A.w[r0 + r];
-    if (A.dinv) wv = cmul(wv, A.dinv[r0 + r]);
-    ws[r] = wv;
-    vj[r] = Vj[r0 + r];
-  }
-  __syncthreads();
-  // Pass 1: dot k by warp k % 8; c_k in slot k, S_jk in slot lds + k.
-  for (int k = warp; k <= j; k += kWarps) {
-    const double2* Vk = A.V + static_cast<long long>(k) * n + r0;
-    double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
-    int r = lane;
-    for (; r + 96 < cnt; r += 128) {
-      double2 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = Vk[r + 32 * u];
-      cfma_conj(c0, v[0], ws[r]);
-      cfma_conj(c1, v[1], ws[r + 32]);
-      cfma_conj(c0, v[2], ws[r + 64]);
-      cfma_conj(c1, v[3], ws[r + 96]);
-      if (k < j) {
-        cfma_conj(s0, vj[r], v[0]);
-        cfma_conj(s1, vj[r + 32], v[1]);
-        cfma_conj(s0, vj[r + 64], v[2]);
-        cfma_conj(s1, vj[r + 96], v[3]);
-      }
-    }
-    for (; r < cnt; r += 32) {
-      const double2 v = Vk[r];
-      cfma_conj(c0, v, ws[r]);
-      if (k < j) cfma_conj(s0, vj[r], v);
-    }
-    const double2 c = warpSum(cadd(c0, c1));
-    const double2 sjk = warpSum(cadd(s0, s1));
-    if (lane == 0) {
-      dotPart[static_cast<long long>(k) * gridDim.x + blockIdx.x] = c;
-      if (k < j) dotPart[static_cast<long long>(lds + k) * gridDim.x + blockIdx.x] = sjk;
-    }
-  }
-  gridBarrier(A.bar);
-  // Grid totals: CTA d reduces dot d (c_0..c_j, then S_j0..S_j,j-1).
-  const int ndots = 2 * j + 1;
-  for (int d = blockIdx.x; d < ndots; d += gridDim.x) {
-    const int slot = d <= j ? d : lds + (d - j - 1);
-    if (warp == 0) {
-      const double2 t = warpTotal(dotPart + static_cast<long long>(slot) * gridDim.x);
-      if (lane == 0) {
-        dots[slot] = t;
-        if (d > j) S[static_cast<long long>(j) * lds + (d - j - 1)] = t;
-      }
-    }
-  }
-  gridBarrier(A.bar);
-  // Stage the lower triangle rows 1..j of L (shared memory after cv).
-  double2* sL = cv + RMAX + 1;  // packed rows: row i at i*(i-1)/2
-  for (int q = threadIdx.x; q < j * (j + 1) / 2; q += blockDim.x) {
-    // q -> (i, k) with i >= 1, k < i
-    int i = static_cast<int>((1.0 + sqrt(1.0 + 8.0 * q)) * 0.5);
-    while (i * (i - 1) / 2 > q) --i;
-    while ((i + 1) * i / 2 <= q) ++i;
-    const int k = q - i * (i - 1) / 2;
-    sL[q] = __ldcg(S + static_cast<long long>(i) * lds + k);
-  }
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) cv[i] = __ldcg(dots + i);
-  __syncthreads();
-  // h = (I + L)^{-1} c, column-oriented on warp 0 (rows in registers).
-  if (warp == 0) {
-    constexpr int RPL = (RMAX + 31) / 32 + 1;
-    double2 hv[RPL];
-#pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      const int i = lane + 32 * t;
-      hv[t] = i <= j ? cv[i] : make_double2(0.0, 0.0);
-    }
-    for (int k = 0; k < j; ++k) {
-      double2 hk = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int t = 0; t < RPL; ++t)
-        if (t == (k >> 5)) hk = hv[t];
-      hk = shfl2(hk, k & 31);
-#pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const int i = lane + 32 * t;
-        if (i > k && i <= j) hv[t] = csub(hv[t], cmul(sL[i * (i - 1) / 2 + k], hk));
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      const int i = lane + 32 * t;
-      if (i <= j) cv[i] = hv[t];
-    }
-  }
-  __syncthreads();
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = cv[i];
-  // Pass 2: w' = w - V h and ||w'||^2.
-  double2 acc = make_double2(0.0, 0.0);
-  for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-    double2 wv = ws[r];
-    int k = 0;
-    for (; k + 8 <= j + 1; k += 8) {
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = A.V[static_cast<long long>(k + u) * n + r0 + r];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) wv = csub(wv, cmul(cv[k + u], v[u]));
-    }
-    for (; k <= j; ++k) wv = csub(wv, cmul(cv[k], A.V[static_cast<long long>(k) * n + r0 + r]));
-    ws[r] = wv;
-    acc.x += wv.x * wv.x + wv.y * wv.y;
-  }
-  blockPartial(acc, scratch, partSlot(A, 0, 0));
-  gridBarrier(A.bar);
-  const double hn = sqrt(warpTotal(partSlot(A, 0, 0)).x);
-  if (hn > 0.0) {
-    double2* vout = A.V + static_cast<long long>(j + 1) * n + r0;
-    for (int r = threadIdx.x; r < cnt; r += blockDim.x) vout[r] = make_double2(ws[r].x / hn, ws[r].y / hn);
-  }
-  if (blockIdx.x == 0) givensStep(A, 0, j, hn, hcol, sh);
+  arnoldiLS(A, S, dots, dotPart, shw, scratch, hcol, sh, A.bar);
 }
 
 // One Arnoldi step j for every running column (any column count / size).
@@ -661,6 +365,14 @@ __global__ void __launch_bounds__(kThreads) gmresUpdate(GmresArgs A) {
 }
 
 void coopLaunch(const void* fn, int grid, size_t smem, GmresArgs& args, cudaStream_t s) {
+  // Same (maximal) shared-memory carveout as the persistent apply kernel, so
+  // alternating launches do not reconfigure L1/shared memory on every SM.
+  static std::vector<const void*> configured;
+  if (std::find(configured.begin(), configured.end(), fn) == configured.end()) {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared));
+    configured.push_back(fn);
+  }
   void* params[] = {&args};
   TBT_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), params, smem, s));
 }
@@ -681,7 +393,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   const bool fast = ncols == 1 && c.n <= static_cast<long long>(grid) * kThreads * FAST_K;
   const long long lsChunk = (c.n + grid - 1) / grid;
   const bool lowSync = o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
-  const size_t lsSmem = (2 * lsChunk + RMAX + 1 + static_cast<size_t>(R) * (R + 1) / 2) * sizeof(double2);
+  const size_t lsSmem = static_cast<size_t>(arnoldiLSSmem(lsChunk, R)) * sizeof(double2);
 
   GmresArgs A{};
   A.ncols = ncols;
@@ -692,37 +404,60 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   A.tol = o.tol;
   A.ne = c.ne;
   A.m = c.m;
-  // Device allocations for this solve.
-  std::vector<void*> allocs;
-  auto dalloc = [&](size_t bytes) {
-    void* p = nullptr;
-    TBT_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-    allocs.push_back(p);
-    return p;
-  };
+  // Device workspace, cached in the context across solves of the same shape
+  // (allocation and graph instantiation are per-solve costs otherwise).
+  GmresWs& W = *gmresWorkspace(c);
+  const long long key[5] = {ncols, R, nall, std::max(1, A.histCap), grid};
+  if (std::memcmp(key, W.key, sizeof(key)) != 0) {
+    W.release();
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      TBT_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+      W.allocs.push_back(p);
+      return p;
+    };
+    W.st = static_cast<GmresState*>(dalloc(sizeof(GmresState) * ncols));
+    W.H = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1) * R));
+    W.g = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1)));
+    W.cs = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
+    W.sn = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
+    W.ycoef = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
+    W.hist = static_cast<double*>(dalloc(sizeof(double) * 2 * ncols * std::max(1, A.histCap)));
+    W.partial = static_cast<double2*>(dalloc(sizeof(double2) * 2 * ncols * grid));
+    W.bar = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
+    W.ax = static_cast<double2*>(dalloc(sizeof(double2) * nall));
+    W.w = static_cast<double2*>(dalloc(sizeof(double2) * nall));
+    W.V = static_cast<double2*>(dalloc(sizeof(double2) * nall * (R + 1)));
+    W.lsS = static_cast<double2*>(dalloc(sizeof(double2) * (R + 1) * (R + 1)));
+    W.lsDots = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1)));
+    W.lsPart = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1) * grid));
+    TBT_CUDA_CHECK(cudaMemsetAsync(W.bar, 0, sizeof(unsigned long long), s));
+    std::memcpy(W.key, key, sizeof(key));
+  }
+  A.st = W.st;
+  A.H = W.H;
+  A.g = W.g;
+  A.cs = W.cs;
+  A.sn = W.sn;
+  A.ycoef = W.ycoef;
+  A.hist = W.hist;
+  A.partial = W.partial;
+  A.bar = W.bar;
+  A.ax = W.ax;
+  A.w = W.w;
+  A.V = W.V;
+  A.b = b;
+  A.x = x;
+  double2* lsS = W.lsS;
+  double2* lsDots = W.lsDots;
+  double2* lsPart = W.lsPart;
   try {
-    A.st = static_cast<GmresState*>(dalloc(sizeof(GmresState) * ncols));
-    A.H = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1) * R));
-    A.g = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1)));
-    A.cs = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
-    A.sn = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
-    A.ycoef = static_cast<double2*>(dalloc(sizeof(double2) * ncols * R));
-    A.hist = static_cast<double*>(dalloc(sizeof(double) * 2 * ncols * std::max(1, A.histCap)));
-    A.partial = static_cast<double2*>(dalloc(sizeof(double2) * 2 * ncols * grid));
-    A.bar = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
-    A.b = b;
-    A.x = x;
-    double2* ax = static_cast<double2*>(dalloc(sizeof(double2) * nall));
-    A.ax = ax;
-    A.w = static_cast<double2*>(dalloc(sizeof(double2) * nall));
-    A.V = static_cast<double2*>(dalloc(sizeof(double2) * nall * (R + 1)));
-    double2* lsS = static_cast<double2*>(dalloc(sizeof(double2) * (R + 1) * (R + 1)));
-    double2* lsDots = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1)));
-    double2* lsPart = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1) * grid));
-    if (lowSync)
+    if (lowSync) {
       TBT_CUDA_CHECK(cudaFuncSetAttribute(gmresArnoldiLS, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(lsSmem)));
-    TBT_CUDA_CHECK(cudaMemsetAsync(A.bar, 0, sizeof(unsigned long long), s));
+      TBT_CUDA_CHECK(cudaFuncSetAttribute(gmresArnoldiLS, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+    }
     TBT_CUDA_CHECK(cudaMemsetAsync(A.V, 0, sizeof(double2) * nall * (R + 1), s));
     TBT_CUDA_CHECK(cudaMemsetAsync(A.H, 0, sizeof(double2) * ncols * (R + 1) * R, s));
     TBT_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * nall, s));
@@ -748,21 +483,35 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
         coopLaunch(reinterpret_cast<const void*>(gmresArnoldi), grid, smem, A, s);
       }
     };
+    // One inner iteration: the apply and the Arnoldi step, fused into the
+    // persistent apply kernel when possible (one cooperative launch).
+    const bool fuse = lowSync && !c.timeBinprod && !c.dist && !c.forceUnfused;
+    auto iteration = [&](int j) {
+      A.j = j;
+      if (fuse && launchPersistentApply(c, A.V + static_cast<long long>(j) * nall, A.w, !useAOnly, &A, lsS, lsDots,
+                                        lsPart))
+        return;
+      applyInternal(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
+      arnoldi(j);
+    };
     // Single column: the whole inner loop of a cycle is one CUDA graph
     // (restart x [apply, Arnoldi]); every node turns into a no-op once the
     // column's inner loop stopped (device flag), so the host synchronises
     // once per restart cycle.
-    cudaGraphExec_t inner = nullptr;
     const bool useGraph = ncols == 1 && !c.timeBinprod;
-    if (useGraph) {
+    GmresArgs keyA = A;  // what the captured nodes bake in (b, x unused by them)
+    keyA.b = nullptr;
+    keyA.x = nullptr;
+    keyA.j = 0;
+    const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0);
+    if (useGraph && (!W.inner || std::memcmp(&keyA, &W.graphKey, sizeof(GmresArgs)) != 0 || W.graphFlags != flags)) {
+      if (W.inner) cudaGraphExecDestroy(W.inner);
+      W.inner = nullptr;
       c.skipFlag = &A.st[0].stopInner;
       cudaGraph_t gph;
       TBT_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
-        for (int j = 0; j < R; ++j) {
-          applyInternal(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
-          arnoldi(j);
-        }
+        for (int j = 0; j < R; ++j) iteration(j);
       } catch (...) {
         cudaStreamEndCapture(s, &gph);
         c.skipFlag = nullptr;
@@ -770,16 +519,19 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       }
       TBT_CUDA_CHECK(cudaStreamEndCapture(s, &gph));
       c.skipFlag = nullptr;
-      const cudaError_t e = cudaGraphInstantiate(&inner, gph, 0);
+      const cudaError_t e = cudaGraphInstantiate(&W.inner, gph, 0);
       cudaGraphDestroy(gph);
       TBT_CUDA_CHECK(e);
+      W.graphKey = keyA;
+      W.graphFlags = flags;
     }
+    cudaGraphExec_t inner = useGraph ? W.inner : nullptr;
     try {
       pull();
       bool open = !st[0].done;
       for (size_t k = 1; k < st.size(); ++k) open |= !st[k].done;
       while (open) {
-        applyInternal(c, x, ax, ncols, !useAOnly);
+        applyInternal(c, x, W.ax, ncols, !useAOnly);
         ++matvecs;
         coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
         if (useGraph) {
@@ -789,8 +541,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
           bool anyRun = false;
           for (auto& v : st) anyRun |= (v.cycleActive && !v.stopInner);
           for (int j = 0; anyRun && j < R; ++j) {
-            applyInternal(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
-            arnoldi(j);
+            iteration(j);
             if ((j + 1) % 8 == 0 && j + 1 < R) {
               pull();
               bool more = false;
@@ -805,10 +556,8 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
         for (auto& v : st) open |= !v.done;
       }
     } catch (...) {
-      if (inner) cudaGraphExecDestroy(inner);
       throw;
     }
-    if (inner) cudaGraphExecDestroy(inner);
     // Matvecs issued: one per cycle start plus one per inner iteration.
     {
       int it = 0;
@@ -821,11 +570,33 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       TBT_CUDA_CHECK(cudaMemcpy(hist.data(), A.hist, sizeof(double) * 2 * ncols * A.histCap, cudaMemcpyDeviceToHost));
   } catch (...) {
     cudaStreamSynchronize(s);
-    for (void* p : allocs) cudaFree(p);
+    W.release();  // state unknown after a failure: rebuild next time
     throw;
   }
   cudaStreamSynchronize(s);
+}
+
+void freeGmresWorkspace(Ctx& c) {
+  if (c.gmresWs) {
+    c.gmresWs->release();
+    if (c.gmresWs->bufB) cudaFree(c.gmresWs->bufB);
+    if (c.gmresWs->bufX) cudaFree(c.gmresWs->bufX);
+    delete c.gmresWs;
+    c.gmresWs = nullptr;
+  }
+}
+
+GmresWs* gmresWorkspace(Ctx& c) {
+  if (!c.gmresWs) c.gmresWs = new GmresWs;
+  return c.gmresWs;
+}
+
+void GmresWs::release() {
+  if (inner) cudaGraphExecDestroy(inner);
+  inner = nullptr;
   for (void* p : allocs) cudaFree(p);
+  allocs.clear();
+  std::memset(key, 0, sizeof(key));
 }
 
 }  // namespace tbt

@@ -1,0 +1,350 @@
+// Device-side GMRES pieces shared by gmres.cu and the fused apply+Arnoldi
+// step of matvec_persistent.cu (see gmres.cu for the algorithm notes).
+#pragma once
+
+#include <cmath>
+#include <vector>
+
+#include "grid_sync.cuh"
+#include "tbt_internal.cuh"
+
+namespace tbt {
+
+struct GmresArgs {
+  int ncols, restart, maxIter, histCap, precondition;
+  double tol;
+  int ne, m;
+  GmresState* st;
+  double2* H;       // [ncols][(restart+1)*restart], H(i,j) at i + j*(restart+1)
+  double2* g;       // [ncols][restart+1]
+  double2* cs;      // [ncols][restart]
+  double2* sn;      // [ncols][restart]
+  double2* ycoef;   // [ncols][restart]
+  double* hist;     // [ncols][histCap][2]
+  double2* partial; // [2][ncols][grid]
+  unsigned long long* bar;  // monotonic grid-barrier counter
+  const double2* b;
+  double2* x;
+  const double2* ax;
+  double2* w;
+  double2* V;       // [restart+1][ne*ncols*m]
+  const double2* dinv;  // [ne*m] or null
+  int j;            // Arnoldi column of this launch
+};
+
+// Device workspace of gmresSolve, cached in the context (gmres.cu).
+struct GmresWs {
+  long long key[5] = {0, 0, 0, 0, 0};  // ncols, restart, n*ncols, hist cap, grid
+  std::vector<void*> allocs;
+  GmresState* st = nullptr;
+  double2 *H = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *ycoef = nullptr;
+  double* hist = nullptr;
+  double2* partial = nullptr;
+  unsigned long long* bar = nullptr;
+  double2 *ax = nullptr, *w = nullptr, *V = nullptr;
+  double2 *lsS = nullptr, *lsDots = nullptr, *lsPart = nullptr;
+  double2 *bufB = nullptr, *bufX = nullptr;  // tbt_gmres staging
+  long long bufLen = 0;
+  cudaGraphExec_t inner = nullptr;  // captured inner loop of a restart cycle
+  GmresArgs graphKey{};
+  int graphFlags = 0;
+  void release();
+};
+GmresWs* gmresWorkspace(Ctx& c);
+
+namespace gmresdev {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int FAST_K = 8;  // slots per thread in the register-resident Arnoldi
+constexpr int RMAX = 128;  // largest restart the staged Givens / solve support
+
+__device__ __forceinline__ void gridBarrier(unsigned long long* bar) { gridBarrierMono(bar); }
+
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  v.x = __shfl_sync(0xffffffffu, v.x, src);
+  v.y = __shfl_sync(0xffffffffu, v.y, src);
+  return v;
+}
+
+// Butterfly sum: every lane ends with the same bits.
+__device__ __forceinline__ double2 warpSum(double2 v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+  }
+  return v;
+}
+
+// Per-CTA partial of v written to part[blockIdx.x] (thread 0).
+__device__ __forceinline__ void blockPartial(double2 v, double2* scratch, double2* part) {
+  v = warpSum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s = scratch[0];
+    for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) s = cadd(s, scratch[k]);
+    part[blockIdx.x] = s;
+  }
+}
+
+// Grid total of the partials, computed by each warp independently in a
+// fixed order (bitwise identical in every warp and CTA).
+__device__ __forceinline__ double2 warpTotal(const double2* part) {
+  const int lane = threadIdx.x & 31;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = lane; k < static_cast<int>(gridDim.x); k += 32) s = cadd(s, __ldcg(part + k));
+  return warpSum(s);
+}
+
+__device__ __forceinline__ double2* partSlot(const GmresArgs& A, int phase, int col) {
+  return A.partial + (static_cast<long long>(phase & 1) * A.ncols + col) * gridDim.x;
+}
+
+__device__ __forceinline__ long long slotIndex(long long s, int col, int ncols, int m) {
+  const long long e = s / m, a = s % m;
+  return (e * ncols + col) * m + a;
+}
+
+__device__ inline void pushHist(const GmresArgs& A, int col, double kind, double v) {
+  GmresState& st = A.st[col];
+  if (st.histLen < A.histCap) {
+    A.hist[(static_cast<long long>(col) * A.histCap + st.histLen) * 2] = kind;
+    A.hist[(static_cast<long long>(col) * A.histCap + st.histLen) * 2 + 1] = v;
+  }
+  st.histLen++;
+}
+
+__device__ __forceinline__ double cabs2(double2 a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// Smith's complex division a / b.
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, d = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  }
+  const double r = b.x / b.y, d = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
+
+// Givens sweep for Arnoldi column j of one GMRES column (linsolve.cpp:472-501),
+// executed by one CTA: H(0..j, j), cs, sn staged in shared memory by all
+// threads, the sequential rotations by thread 0, results written back.
+// hcolIn (optional) already holds H(0..j, j) in shared memory.
+__device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn, const double2* hcolIn,
+                           double2* sh /* >= 3*RMAX+4 */) {
+  const int ldh = A.restart + 1;
+  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+  double2* cs = A.cs + static_cast<long long>(col) * A.restart;
+  double2* sn = A.sn + static_cast<long long>(col) * A.restart;
+  double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
+  double2* hc = sh;               // [j+2]
+  double2* scs = sh + RMAX + 2;   // [j]
+  double2* ssn = scs + RMAX;      // [j]
+  __syncthreads();
+  for (int t = threadIdx.x; t <= j; t += blockDim.x) hc[t] = hcolIn ? hcolIn[t] : H[t + j * ldh];
+  for (int t = threadIdx.x; t < j; t += blockDim.x) {
+    scs[t] = cs[t];
+    ssn[t] = sn[t];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    GmresState& st = A.st[col];
+    hc[j + 1] = make_double2(hn, 0.0);
+    for (int i = 0; i < j; ++i) {
+      const double2 a0 = hc[i], a1 = hc[i + 1];
+      hc[i] = cadd(cmul(scs[i], a0), cmul(ssn[i], a1));
+      hc[i + 1] = cadd(cmul(make_double2(-ssn[i].x, ssn[i].y), a0), cmul(cconj(scs[i]), a1));
+    }
+    const double2 hjj = hc[j], hj1 = hc[j + 1];
+    const double den = sqrt((hjj.x * hjj.x + hjj.y * hjj.y) + (hj1.x * hj1.x + hj1.y * hj1.y));
+    double2 c, s;
+    if (den == 0.0) {
+      c = make_double2(1.0, 0.0);
+      s = make_double2(0.0, 0.0);
+    } else {
+      c = make_double2(hjj.x / den, -hjj.y / den);
+      s = make_double2(hj1.x / den, -hj1.y / den);
+    }
+    cs[j] = c;
+    sn[j] = s;
+    hc[j] = cadd(cmul(c, hjj), cmul(s, hj1));
+    hc[j + 1] = make_double2(0.0, 0.0);
+    const double2 gj = g[j];
+    g[j] = cmul(c, gj);
+    const double2 gj1 = cmul(make_double2(-s.x, s.y), gj);
+    g[j + 1] = gj1;
+    st.iterations += 1;
+    st.ncount = j + 1;
+    const double rel = cabs2(gj1) / st.beta;
+    pushHist(A, col, 1.0, cabs2(gj1) / st.beta0);
+    if (rel < 0.1 * A.tol || !(hn > 0.0) || st.ncount >= A.restart || st.iterations >= A.maxIter) st.stopInner = 1;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t <= j + 1; t += blockDim.x) H[t + j * ldh] = hc[t];
+  __syncthreads();
+}
+
+// One Arnoldi step j, single column, low-synchronisation MGS (device
+// function: the gmresArnoldiLS kernel and the fused apply+Arnoldi of
+// matvec_persistent.cu run it): the MGS
+// coefficients h_i = <v_i, (I - v_{i-1}v_{i-1}^H)...(I - v_0 v_0^H) w> are
+// obtained as h = (I + L)^{-1} c with c = V^H w and L the strictly lower
+// part of the basis Gram matrix V^H V (identical to the MGS sweep in exact
+// arithmetic; L accumulates one row per iteration). Three grid barriers per
+// step instead of j + 2:
+//   pass 1  per-CTA partials of c_k = <v_k, w> and S_jk = <v_j, v_k>
+//           (one warp per k, the CTA's row chunk of w and v_j in smem)
+//   -- barrier --  CTA k reduces dot k over the grid
+//   -- barrier --  every CTA: forward substitution for h (warp 0)
+//   pass 2  w' = w - V h, ||w'||^2
+//   -- barrier --  v_{j+1} = w' / ||w'||, Givens (CTA 0)
+// shw: dynamic shared memory of arnoldiLSSmem(chunk) double2; scratch:
+// blockDim/32 entries; hcol: RMAX+2; sh: 3*RMAX+4.
+__device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, double2* dotPart, double2* shw,
+                          double2* scratch, double2* hcol, double2* sh, unsigned long long* bar) {
+  const int run = A.st[0].cycleActive && !A.st[0].stopInner;
+  if (!run) return;  // uniform over the grid
+  const int j = A.j;
+  const int lds = A.restart + 1;
+  const long long n = static_cast<long long>(A.ne) * A.m;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk;
+  const int cnt = static_cast<int>(r0 >= n ? 0 : (n - r0 < chunk ? n - r0 : chunk));
+  double2* ws = shw;
+  double2* vj = shw + chunk;
+  double2* cv = vj + chunk;  // [j+1] totals of c, later h
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double2* Vj = A.V + static_cast<long long>(j) * n;
+  for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+    double2 wv = A.w[r0 + r];
+    if (A.dinv) wv = cmul(wv, A.dinv[r0 + r]);
+    ws[r] = wv;
+    vj[r] = Vj[r0 + r];
+  }
+  __syncthreads();
+  // Pass 1: dot k by warp k % 8; c_k in slot k, S_jk in slot lds + k.
+  for (int k = warp; k <= j; k += static_cast<int>(blockDim.x >> 5)) {
+    const double2* Vk = A.V + static_cast<long long>(k) * n + r0;
+    double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
+    int r = lane;
+    for (; r + 96 < cnt; r += 128) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = Vk[r + 32 * u];
+      cfma_conj(c0, v[0], ws[r]);
+      cfma_conj(c1, v[1], ws[r + 32]);
+      cfma_conj(c0, v[2], ws[r + 64]);
+      cfma_conj(c1, v[3], ws[r + 96]);
+      if (k < j) {
+        cfma_conj(s0, vj[r], v[0]);
+        cfma_conj(s1, vj[r + 32], v[1]);
+        cfma_conj(s0, vj[r + 64], v[2]);
+        cfma_conj(s1, vj[r + 96], v[3]);
+      }
+    }
+    for (; r < cnt; r += 32) {
+      const double2 v = Vk[r];
+      cfma_conj(c0, v, ws[r]);
+      if (k < j) cfma_conj(s0, vj[r], v);
+    }
+    const double2 c = warpSum(cadd(c0, c1));
+    const double2 sjk = warpSum(cadd(s0, s1));
+    if (lane == 0) {
+      dotPart[static_cast<long long>(k) * gridDim.x + blockIdx.x] = c;
+      if (k < j) dotPart[static_cast<long long>(lds + k) * gridDim.x + blockIdx.x] = sjk;
+    }
+  }
+  gridBarrier(bar);
+  // Grid totals: CTA d reduces dot d (c_0..c_j, then S_j0..S_j,j-1).
+  const int ndots = 2 * j + 1;
+  for (int d = blockIdx.x; d < ndots; d += gridDim.x) {
+    const int slot = d <= j ? d : lds + (d - j - 1);
+    if (warp == 0) {
+      const double2 t = warpTotal(dotPart + static_cast<long long>(slot) * gridDim.x);
+      if (lane == 0) {
+        dots[slot] = t;
+        if (d > j) S[static_cast<long long>(j) * lds + (d - j - 1)] = t;
+      }
+    }
+  }
+  gridBarrier(bar);
+  // Stage the lower triangle rows 1..j of L (shared memory after cv).
+  double2* sL = cv + RMAX + 1;  // packed rows: row i at i*(i-1)/2
+  for (int q = threadIdx.x; q < j * (j + 1) / 2; q += blockDim.x) {
+    // q -> (i, k) with i >= 1, k < i
+    int i = static_cast<int>((1.0 + sqrt(1.0 + 8.0 * q)) * 0.5);
+    while (i * (i - 1) / 2 > q) --i;
+    while ((i + 1) * i / 2 <= q) ++i;
+    const int k = q - i * (i - 1) / 2;
+    sL[q] = __ldcg(S + static_cast<long long>(i) * lds + k);
+  }
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) cv[i] = __ldcg(dots + i);
+  __syncthreads();
+  // h = (I + L)^{-1} c, column-oriented on warp 0 (rows in registers).
+  if (warp == 0) {
+    constexpr int RPL = (RMAX + 31) / 32 + 1;
+    double2 hv[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      hv[t] = i <= j ? cv[i] : make_double2(0.0, 0.0);
+    }
+    for (int k = 0; k < j; ++k) {
+      double2 hk = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < RPL; ++t)
+        if (t == (k >> 5)) hk = hv[t];
+      hk = shfl2(hk, k & 31);
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i > k && i <= j) hv[t] = csub(hv[t], cmul(sL[i * (i - 1) / 2 + k], hk));
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i <= j) cv[i] = hv[t];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = cv[i];
+  // Pass 2: w' = w - V h and ||w'||^2.
+  double2 acc = make_double2(0.0, 0.0);
+  for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+    double2 wv = ws[r];
+    int k = 0;
+    for (; k + 8 <= j + 1; k += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = A.V[static_cast<long long>(k + u) * n + r0 + r];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv = csub(wv, cmul(cv[k + u], v[u]));
+    }
+    for (; k <= j; ++k) wv = csub(wv, cmul(cv[k], A.V[static_cast<long long>(k) * n + r0 + r]));
+    ws[r] = wv;
+    acc.x += wv.x * wv.x + wv.y * wv.y;
+  }
+  blockPartial(acc, scratch, partSlot(A, 0, 0));
+  gridBarrier(bar);
+  const double hn = sqrt(warpTotal(partSlot(A, 0, 0)).x);
+  if (hn > 0.0) {
+    double2* vout = A.V + static_cast<long long>(j + 1) * n + r0;
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) vout[r] = make_double2(ws[r].x / hn, ws[r].y / hn);
+  }
+  if (blockIdx.x == 0) givensStep(A, 0, j, hn, hcol, sh);
+}
+
+// Dynamic shared memory (double2 count) the LS step needs for a row chunk.
+__host__ __device__ inline long long arnoldiLSSmem(long long chunk, int restart) {
+  return 2 * chunk + RMAX + 1 + static_cast<long long>(restart) * (restart + 1) / 2;
+}
+
+}  // namespace gmresdev
+}  // namespace tbt

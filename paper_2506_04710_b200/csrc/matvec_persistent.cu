@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "fft_reg.cuh"
+#include "gmres_dev.cuh"
 #include "grid_sync.cuh"
 #include "ptx.cuh"
 #include "tbt_internal.cuh"
@@ -72,6 +73,13 @@ struct PArgs {
   double2* ycorr;
   int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
   const int* skip;              // optional: the whole launch is a no-op when *skip != 0
+  // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
+  // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
+  int arnoldi;
+  GmresArgs gm;
+  double2* lsS;
+  double2* lsDots;
+  double2* lsPart;
   unsigned long long* phaseNs;  // optional: globaltimer at phase boundaries (CTA 0)
 };
 
@@ -498,10 +506,23 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     }
   }
   stamp(a, 5);
+  if (a.arnoldi) {
+    gridSync(a.barFlags, a, 4);  // y (= w) complete grid-wide
+    // Shared memory is free again: LS scratch, then hcol / Givens staging.
+    const long long chunk = (static_cast<long long>(a.gm.ne) * a.gm.m + gridDim.x - 1) / gridDim.x;
+    double2* shw = reinterpret_cast<double2*>(smem);
+    double2* tail = shw + gmresdev::arnoldiLSSmem(chunk, a.gm.restart);
+    double2* hcol = tail;
+    double2* sh = hcol + gmresdev::RMAX + 2;
+    double2* scratch = sh + 3 * gmresdev::RMAX + 4;
+    __syncthreads();
+    gmresdev::arnoldiLS(a.gm, a.lsS, a.lsDots, a.lsPart, shw, scratch, hcol, sh, a.barFlags);
+  }
 }
 
 template <int M, int TC, int RCH, int STAGES, int N0, int N1>
-bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr) {
+bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
+             double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr) {
   using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
   auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1>;
@@ -548,6 +569,19 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr) {
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
   a.prefetchAt = c.prefetchAt;
   a.skip = c.skipFlag;
+  a.arnoldi = 0;
+  if (gm) {
+    const long long chunk = (static_cast<long long>(gm->ne) * gm->m + smCount(c.device) - 1) / smCount(c.device);
+    const long long need =
+        (gmresdev::arnoldiLSSmem(chunk, gm->restart) + gmresdev::RMAX + 2 + 3 * gmresdev::RMAX + 4 + 32) *
+        static_cast<long long>(sizeof(double2));
+    if (need > static_cast<long long>(C::SMEM)) return false;
+    a.arnoldi = 1;
+    a.gm = *gm;
+    a.lsS = lsS;
+    a.lsDots = lsDots;
+    a.lsPart = lsPart;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(smCount(c.device));
   cfg.blockDim = dim3(kThreadsP);
@@ -575,16 +609,17 @@ bool persistentSupported(const Ctx& c) {
   }
 }
 
-bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr) {
-  if (!persistentSupported(c)) return false;
+bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm,
+                           double2* lsS, double2* lsDots, double2* lsPart) {
+  if (!persistentSupported(c) || c.dist) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
-    case 64064064: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr);
-    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr);
-    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr);
-    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr);
-    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr);
-    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr);
+    case 64064064: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     default: return false;
   }
 }

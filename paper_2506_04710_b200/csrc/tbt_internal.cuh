@@ -112,6 +112,7 @@ struct Ctx {
   const int* skipFlag = nullptr;           // device flag: persistent applies become no-ops when set                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
+  bool forceUnfused = false;               // TBT_GMRES=unfused: separate apply / Arnoldi launches
 
   // Multi-GPU (dist.cu): this rank owns element rows [myRow0, myRow0 +
   // myRows) of the vectors and the bin columns myColList (closed under
@@ -176,6 +177,8 @@ struct Ctx {
   double2* dDiagInv = nullptr;   // 1/diag(Z), Jacobi of iterativeSolve
   double2* dDiagInvA = nullptr;  // 1/diag(A), Jacobi of the A-only solves
 
+  struct GmresWs* gmresWs = nullptr;  // cached GMRES workspace + inner-loop graph (gmres.cu)
+
   // Timing hooks: event pairs around K3, one per timed apply.
   cudaEvent_t evBinA = nullptr, evBinB = nullptr;
   bool timeBinprod = false;
@@ -234,7 +237,11 @@ void distFree(Ctx& c);
 
 // Persistent single-kernel apply (matvec_persistent.cu).
 bool persistentSupported(const Ctx& c);
-bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr);
+struct GmresArgs;
+struct GmresWs;
+void freeGmresWorkspace(Ctx& c);  // gmres.cu
+bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
+                           double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr);
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);
