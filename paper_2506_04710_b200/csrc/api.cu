@@ -138,6 +138,16 @@ void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
   TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInvA, invA.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
 }
 
+// Page-locked host memory is device-addressable through UVA.
+bool isPinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 void requireReady(const Ctx& c) {
   TBT_USER_CHECK(c.havePrecompute, "tbt: call tbt_precompute before apply/solve");
 }
@@ -503,7 +513,14 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
     const size_t bytes = total * sizeof(double2);
     const double2* xin = reinterpret_cast<const double2*>(x);
     double2* yout = reinterpret_cast<double2*>(y);
-    if (where == TBT_HOST) {
+    if (where == TBT_HOST && nrhs == 1 && !c.dist && c.persistent && persistentSupported(c) && !c.timeBinprod &&
+        isPinned(xin) && isPinned(yout)) {
+      // Zero-copy: the persistent kernel reads x and writes y in pinned host
+      // memory over PCIe/C2C itself, overlapping both transfers with the
+      // HBM spectrum stream instead of serialising two memcpys around it.
+      runApply1(c, xin, yout, withCorr);
+      TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    } else if (where == TBT_HOST) {
       if (nrhs == 1) {
         TBT_CUDA_CHECK(cudaMemcpyAsync(c.dXin, xin, bytes, cudaMemcpyHostToDevice, c.stream));
       } else {
