@@ -104,6 +104,93 @@ __global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInf
   }
 }
 
+// Many right-hand sides: one CTA per (target, chunk of 32 columns). Each
+// term's d, U, V (rank RANK, m = 32*KPL) are staged once in shared memory and
+// reused by all 32 columns of the chunk (instead of once per column); every
+// warp owns 4 columns whose sums stay in registers across the term list.
+template <int KPL, int RANK>
+__global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInfo, const int* __restrict__ targetList,
+                                                 const int* __restrict__ targetPtr, const double2* __restrict__ D,
+                                                 const double2* __restrict__ U, const double2* __restrict__ V,
+                                                 const double2* __restrict__ x, double2* __restrict__ ycorr,
+                                                 int nrhs) {
+  constexpr int M = 32 * KPL;
+  constexpr int RPW = 4;  // columns per warp
+  constexpr int RC = 8 * RPW;
+  __shared__ double2 sW[RANK][M], sW2[RANK][M], sD[M];
+  const int ti = blockIdx.x;
+  const int r0 = blockIdx.y * RC;
+  const int e = targetList[ti];
+  const int t0 = targetPtr[ti], t1 = targetPtr[ti + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 acc[RPW][KPL];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j)
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) acc[j][k] = make_double2(0.0, 0.0);
+  for (int t = t0; t < t1; ++t) {
+    const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+    const double2* W = (trans ? U : V) + static_cast<long long>(slot) * RANK * M;
+    const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * RANK * M;
+    __syncthreads();
+    for (int q = threadIdx.x; q < RANK * M; q += blockDim.x) {
+      (&sW[0][0])[q] = __ldg(W + q);
+      (&sW2[0][0])[q] = __ldg(W2 + q);
+    }
+    for (int q = threadIdx.x; q < M; q += blockDim.x) sD[q] = __ldg(D + static_cast<long long>(slot) * M + q);
+    __syncthreads();
+    // All RPW columns advance together through the rank loop: one shared
+    // memory read of U/V row q serves RPW columns, and the RPW butterfly
+    // reductions interleave.
+    double2 xv[RPW][KPL];
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int r = r0 + warp * RPW + j;
+      const double2* xs = x + (static_cast<long long>(src) * nrhs + r) * M;
+#pragma unroll
+      for (int k = 0; k < KPL; ++k) xv[j][k] = r < nrhs ? __ldg(xs + lane + 32 * k) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      const double2 d = sD[lane + 32 * k];
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) cfma(acc[j][k], d, xv[j][k]);
+    }
+#pragma unroll 1
+    for (int q = 0; q < RANK; ++q) {
+      double2 p[RPW];
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) p[j] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < KPL; ++k) {
+        const double2 w = sW[q][lane + 32 * k];
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) cfma(p[j], w, xv[j][k]);
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          p[j].x += __shfl_xor_sync(0xffffffffu, p[j].x, off);
+          p[j].y += __shfl_xor_sync(0xffffffffu, p[j].y, off);
+        }
+#pragma unroll
+      for (int k = 0; k < KPL; ++k) {
+        const double2 w2 = sW2[q][lane + 32 * k];
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) cfma(acc[j][k], w2, p[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int r = r0 + warp * RPW + j;
+    if (r >= nrhs) break;
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) ycorr[(static_cast<long long>(e) * nrhs + r) * M + lane + 32 * k] = acc[j][k];
+  }
+}
+
 // y[e][rhs][a] += sum_b K[a][b] x[e][rhs][b].
 __global__ void antisymApply(const double2* __restrict__ K, const double2* __restrict__ x, double2* __restrict__ y,
                              int m, int nrhs) {
@@ -122,6 +209,14 @@ __global__ void antisymApply(const double2* __restrict__ K, const double2* __res
 
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
   if (!c.haveCorr || c.nTerms == 0) return;
+  if (nrhs >= 8 && (c.rank == 4 || c.rank == 8) && (c.m == 64 || c.m == 128)) {
+    dim3 grid(c.nTargets, (nrhs + 31) / 32);
+    auto k = c.m == 64 ? (c.rank == 4 ? corrMulti<2, 4> : corrMulti<2, 8>)
+                       : (c.rank == 4 ? corrMulti<4, 4> : corrMulti<4, 8>);
+    k<<<grid, 256, 0, s>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs);
+    TBT_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   dim3 grid(c.nTargets, nrhs);
   const size_t smem = static_cast<size_t>(c.maxTermsPerTarget) * std::max(c.rank, 1) * sizeof(double2);
   corrFused<<<grid, 256, smem, s>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr,

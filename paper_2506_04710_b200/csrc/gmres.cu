@@ -226,6 +226,108 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiLS(GmresArgs A, double2*
   arnoldiLS(A, S, dots, dotPart, shw, scratch, hcol, sh, A.bar);
 }
 
+// One Arnoldi step j for many columns: one CTA per column runs the
+// reference's MGS sweep (linsolve.cpp:465-468) with CTA-level reductions
+// only, so columns proceed independently without grid barriers; w lives in
+// global memory (L2), each projection is one fused sweep
+// "w -= h_i v_i; partial <v_{i+1}, w>".
+__global__ void __launch_bounds__(kThreads) gmresArnoldiCols(GmresArgs A) {
+  __shared__ double2 scratch[kWarps];
+  __shared__ double2 hcol[RMAX + 2];
+  __shared__ double2 sh[3 * RMAX + 4];
+  __shared__ double2 bcast;
+  const int col = blockIdx.x;
+  if (col >= A.ncols) return;
+  const GmresState st = A.st[col];
+  if (!(st.cycleActive && !st.stopInner)) return;
+  const int j = A.j;
+  const long long slots = static_cast<long long>(A.ne) * A.m;
+  const long long nall = slots * A.ncols;
+  // Column col's entries: element e's m values at (e*ncols + col)*m. Each
+  // thread walks a fixed basis index over a strided set of elements (no
+  // index division in the sweeps).
+  const int m = A.m;
+  const int tpe = static_cast<int>(blockDim.x) >= m ? static_cast<int>(blockDim.x) / m : 1;  // threads per element slot
+  const int a = static_cast<int>(threadIdx.x) % m;
+  const int e0 = static_cast<int>(threadIdx.x) / m;
+  const bool activeT = static_cast<int>(threadIdx.x) < tpe * m;
+  const long long qStep = static_cast<long long>(tpe) * A.ncols * m;
+  const long long q0 = (static_cast<long long>(e0) * A.ncols + col) * m + a;
+  const long long sStep = static_cast<long long>(tpe) * m;
+  const long long s0 = static_cast<long long>(e0) * m + a;
+  const int nIter = activeT ? (A.ne - e0 + tpe - 1) / tpe : 0;
+  auto total = [&](double2 v) {  // CTA sum, broadcast to every thread
+    v = warpSum(v);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = scratch[0];
+      for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) t = cadd(t, scratch[k]);
+      bcast = t;
+    }
+    __syncthreads();
+    const double2 r = bcast;
+    __syncthreads();
+    return r;
+  };
+  constexpr int U = 4;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int it = 0; it < nIter; ++it) {
+    const long long qq = q0 + it * qStep;
+    double2 wv = A.w[qq];
+    if (A.dinv) wv = cmul(wv, A.dinv[s0 + it * sStep]);
+    A.w[qq] = wv;
+    cfma_conj(acc, A.V[qq], wv);
+  }
+  double2 h = total(acc);
+  for (int i = 0; i <= j; ++i) {
+    if (threadIdx.x == 0) hcol[i] = h;
+    const double2* vi = A.V + static_cast<long long>(i) * nall;
+    const double2* vn = A.V + static_cast<long long>(i + 1) * nall;
+    acc = make_double2(0.0, 0.0);
+    int it = 0;
+    for (; it + U <= nIter; it += U) {
+      double2 wv[U], v0[U], v1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long qq = q0 + (it + u) * qStep;
+        wv[u] = A.w[qq];
+        v0[u] = vi[qq];
+        v1[u] = i < j ? vn[qq] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        wv[u] = csub(wv[u], cmul(h, v0[u]));
+        A.w[q0 + (it + u) * qStep] = wv[u];
+        if (i < j)
+          cfma_conj(acc, v1[u], wv[u]);
+        else
+          acc.x += wv[u].x * wv[u].x + wv[u].y * wv[u].y;
+      }
+    }
+    for (; it < nIter; ++it) {
+      const long long qq = q0 + it * qStep;
+      const double2 wv = csub(A.w[qq], cmul(h, vi[qq]));
+      A.w[qq] = wv;
+      if (i < j)
+        cfma_conj(acc, vn[qq], wv);
+      else
+        acc.x += wv.x * wv.x + wv.y * wv.y;
+    }
+    h = total(acc);
+  }
+  const double hn = sqrt(h.x);
+  if (hn > 0.0) {
+    double2* vout = A.V + static_cast<long long>(j + 1) * nall;
+    for (int it = 0; it < nIter; ++it) {
+      const long long qq = q0 + it * qStep;
+      const double2 wv = A.w[qq];
+      vout[qq] = make_double2(wv.x / hn, wv.y / hn);
+    }
+  }
+  givensStep(A, col, j, hn, hcol, sh);
+}
+
 // One Arnoldi step j for every running column (any column count / size).
 __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
   __shared__ double2 scratch[kWarps];
@@ -479,6 +581,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
                                                    dim3(kThreads), params, lsSmem, s));
       } else if (fast) {
         coopLaunch(reinterpret_cast<const void*>(gmresArnoldi1), grid, 0, A, s);
+      } else if (ncols > 1 && c.m <= kThreads) {
+        gmresArnoldiCols<<<ncols, kThreads, 0, s>>>(A);
+        TBT_CUDA_CHECK(cudaGetLastError());
       } else {
         coopLaunch(reinterpret_cast<const void*>(gmresArnoldi), grid, smem, A, s);
       }

@@ -128,10 +128,13 @@ def fft_path(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("nx,ny,m,k", [(6, 5, 64, 3), (5, 4, 8, 3), (4, 4, 24, 2), (9, 5, 128, 2), (3, 5, 7, 4),
-                                       (6, 5, 64, 9), (5, 3, 128, 60), (7, 4, 64, 57)])
-def test_multi_rhs_apply(gpu, fft_path, nx, ny, m, k):
-    rep = rep_for(nx, ny, m)
+@pytest.mark.parametrize("nx,ny,m,k,rank", [(6, 5, 64, 3, 4), (5, 4, 8, 3, 4), (4, 4, 24, 2, 4), (9, 5, 128, 2, 4),
+                                            (3, 5, 7, 4, 4), (6, 5, 64, 9, 4), (5, 3, 128, 60, 4), (7, 4, 64, 57, 4),
+                                            (6, 5, 64, 33, 8), (5, 3, 128, 40, 8), (4, 6, 128, 8, 8)])
+def test_multi_rhs_apply(gpu, fft_path, nx, ny, m, k, rank):
+    """k >= 8 with m in {64, 128} and rank 4/8 runs the many-column
+    correction kernel (corrMulti), including ragged last 32-column chunks."""
+    rep = rep_for(nx, ny, m, rank=rank)
     op = ToeplitzMatvec(rep, max_nrhs=k)
     o = oracle.Oracle.from_rep(rep)
     X = gen.rhs_normal(o.n, k, 5)
