@@ -328,6 +328,260 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiCols(GmresArgs A) {
   givensStep(A, col, j, hn, hcol, sh);
 }
 
+// ---------------------------------------------------------------------------
+// Many columns, low-synchronisation MGS (orthog = 1): the same
+// h = (I + L)^{-1} V^H w recurrence as arnoldiLS (gmres_dev.cuh), batched
+// over the columns, in four launches instead of one grid barrier per
+// projection:
+//   lsColsDots    c_k = <v_k, w>, S_jk = <v_j, v_k>: one warp per element,
+//                 lane-strided basis values in registers; per-CTA partials
+//   lsColsSolve   CTA per column: fixed-order totals, forward substitution
+//   lsColsUpdate  w' = M w - V h, ||w'||^2 partials
+//   lsColsFinish  v_{j+1} = w' / ||w'||, Givens (first CTA of each column)
+// Two passes over the basis per step (the sweep reads it j+1 times and
+// rewrites w each time). Every total is a fixed-order sum: reproducible.
+struct ColsLS {
+  double2* part;  // [ncols][2*(restart+1)][nblk]: c_k in slot k, S_jk in slot restart+1+k
+  double2* S;     // [ncols][restart+1][restart+1], S(i,k) = <v_i, v_k>, k < i
+  double2* h;     // [ncols][restart+1]
+  double2* nrm;   // [ncols][nblk]
+  int* run;       // [ncols] column ran this step (snapshot taken by lsColsSolve)
+  int nblk;
+};
+constexpr int kColsElems = kWarps;  // elements per CTA, one per warp
+
+template <int KPL>
+__global__ void __launch_bounds__(kThreads) lsColsDots(GmresArgs A, ColsLS L) {
+  __shared__ double2 red[kWarps][2 * (RMAX + 1)];
+  const int col = blockIdx.y;
+  const GmresState st = A.st[col];
+  if (!(st.cycleActive && !st.stopInner)) return;
+  const int j = A.j, m = A.m, lds = A.restart + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * kColsElems + warp;
+  const bool ev = e < A.ne;
+  const long long nall = static_cast<long long>(A.ne) * m * A.ncols;
+  const long long base = (static_cast<long long>(e) * A.ncols + col) * m;
+  double2 w[KPL], vj[KPL];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int a = lane + 32 * k;
+    w[k] = vj[k] = make_double2(0.0, 0.0);
+    if (ev && a < m) {
+      double2 wv = A.w[base + a];
+      if (A.dinv) wv = cmul(wv, A.dinv[static_cast<long long>(e) * m + a]);
+      w[k] = wv;
+      vj[k] = A.V[static_cast<long long>(j) * nall + base + a];
+    }
+  }
+  for (int kk = 0; kk <= j; kk += 2) {
+    const bool two = kk + 1 <= j;
+    double2 v0[KPL], v1[KPL];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      const int a = lane + 32 * k;
+      const bool ok = ev && a < m;
+      v0[k] = ok ? A.V[static_cast<long long>(kk) * nall + base + a] : make_double2(0.0, 0.0);
+      v1[k] = ok && two ? A.V[static_cast<long long>(kk + 1) * nall + base + a] : make_double2(0.0, 0.0);
+    }
+    double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      cfma_conj(c0, v0[k], w[k]);
+      cfma_conj(c1, v1[k], w[k]);
+      cfma_conj(s0, vj[k], v0[k]);
+      cfma_conj(s1, vj[k], v1[k]);
+    }
+    c0 = warpSum(c0);
+    c1 = warpSum(c1);
+    s0 = warpSum(s0);
+    s1 = warpSum(s1);
+    if (lane == 0) {
+      red[warp][kk] = c0;
+      if (kk < j) red[warp][lds + kk] = s0;
+      if (two) {
+        red[warp][kk + 1] = c1;
+        if (kk + 1 < j) red[warp][lds + kk + 1] = s1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 2 * j + 1; d += blockDim.x) {
+    const int slot = d <= j ? d : lds + (d - j - 1);
+    double2 t = red[0][slot];
+    for (int q = 1; q < kWarps; ++q) t = cadd(t, red[q][slot]);
+    L.part[(static_cast<long long>(col) * 2 * lds + slot) * L.nblk + blockIdx.x] = t;
+  }
+}
+
+// Dynamic shared memory: cv[RMAX+1] + packed strictly-lower rows of L.
+__global__ void __launch_bounds__(kThreads) lsColsSolve(GmresArgs A, ColsLS L) {
+  extern __shared__ double2 shs[];
+  const int col = blockIdx.x;
+  const GmresState st = A.st[col];
+  const int running = st.cycleActive && !st.stopInner;
+  if (threadIdx.x == 0) L.run[col] = running;
+  if (!running) return;
+  const int j = A.j, lds = A.restart + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* cv = shs;
+  double2* sL = shs + RMAX + 1;  // row i (1..j) at i*(i-1)/2
+  double2* S = L.S + static_cast<long long>(col) * lds * lds;
+  const double2* part = L.part + static_cast<long long>(col) * 2 * lds * L.nblk;
+  for (int d = threadIdx.x; d < 2 * j + 1; d += blockDim.x) {
+    const int slot = d <= j ? d : lds + (d - j - 1);
+    double2 t = make_double2(0.0, 0.0);
+    for (int b = 0; b < L.nblk; ++b) t = cadd(t, part[static_cast<long long>(slot) * L.nblk + b]);
+    if (d <= j) {
+      cv[d] = t;
+    } else {
+      const int k = d - j - 1;
+      S[static_cast<long long>(j) * lds + k] = t;
+      sL[j * (j - 1) / 2 + k] = t;
+    }
+  }
+  for (int i = 1 + warp; i < j; i += kWarps)
+    for (int k = lane; k < i; k += 32) sL[i * (i - 1) / 2 + k] = S[static_cast<long long>(i) * lds + k];
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int RPL = (RMAX + 31) / 32 + 1;
+    double2 hv[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      hv[t] = i <= j ? cv[i] : make_double2(0.0, 0.0);
+    }
+    for (int k = 0; k < j; ++k) {
+      double2 hk = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < RPL; ++t)
+        if (t == (k >> 5)) hk = hv[t];
+      hk = shfl2(hk, k & 31);
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i > k && i <= j) hv[t] = csub(hv[t], cmul(sL[i * (i - 1) / 2 + k], hk));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i <= j) L.h[static_cast<long long>(col) * lds + i] = hv[t];
+    }
+  }
+}
+
+template <int KPL>
+__global__ void __launch_bounds__(kThreads) lsColsUpdate(GmresArgs A, ColsLS L) {
+  __shared__ double2 hs[RMAX + 1];
+  __shared__ double2 scratch[kWarps];
+  const int col = blockIdx.y;
+  if (!L.run[col]) return;
+  const int j = A.j, m = A.m, lds = A.restart + 1;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) hs[i] = L.h[static_cast<long long>(col) * lds + i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * kColsElems + warp;
+  const bool ev = e < A.ne;
+  const long long nall = static_cast<long long>(A.ne) * m * A.ncols;
+  const long long base = (static_cast<long long>(e) * A.ncols + col) * m;
+  double2 w[KPL];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int a = lane + 32 * k;
+    w[k] = make_double2(0.0, 0.0);
+    if (ev && a < m) {
+      double2 wv = A.w[base + a];
+      if (A.dinv) wv = cmul(wv, A.dinv[static_cast<long long>(e) * m + a]);
+      w[k] = wv;
+    }
+  }
+  int kk = 0;
+  for (; kk + 2 <= j + 1; kk += 2) {
+    double2 v0[KPL], v1[KPL];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      const int a = lane + 32 * k;
+      const bool ok = ev && a < m;
+      v0[k] = ok ? A.V[static_cast<long long>(kk) * nall + base + a] : make_double2(0.0, 0.0);
+      v1[k] = ok ? A.V[static_cast<long long>(kk + 1) * nall + base + a] : make_double2(0.0, 0.0);
+    }
+    const double2 h0 = hs[kk], h1 = hs[kk + 1];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) w[k] = csub(csub(w[k], cmul(h0, v0[k])), cmul(h1, v1[k]));
+  }
+  if (kk <= j) {
+    const double2 h0 = hs[kk];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      const int a = lane + 32 * k;
+      if (ev && a < m) w[k] = csub(w[k], cmul(h0, A.V[static_cast<long long>(kk) * nall + base + a]));
+    }
+  }
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int a = lane + 32 * k;
+    if (ev && a < m) {
+      A.w[base + a] = w[k];
+      acc.x += w[k].x * w[k].x + w[k].y * w[k].y;
+    }
+  }
+  acc = warpSum(acc);
+  if (lane == 0) scratch[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = scratch[0];
+    for (int q = 1; q < kWarps; ++q) t = cadd(t, scratch[q]);
+    L.nrm[static_cast<long long>(col) * L.nblk + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lsColsFinish(GmresArgs A, ColsLS L) {
+  __shared__ double2 hcol[RMAX + 2];
+  __shared__ double2 sh[3 * RMAX + 4];
+  __shared__ double sHn;
+  const int col = blockIdx.y;
+  if (!L.run[col]) return;
+  const int j = A.j, m = A.m, lds = A.restart + 1;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < L.nblk; ++b) t += L.nrm[static_cast<long long>(col) * L.nblk + b].x;
+    sHn = sqrt(t);
+  }
+  __syncthreads();
+  const double hn = sHn;
+  if (hn > 0.0) {
+    const long long nall = static_cast<long long>(A.ne) * m * A.ncols;
+    const int e0 = blockIdx.x * kColsElems;
+    const int e1 = min(A.ne, e0 + kColsElems);
+    for (int q = threadIdx.x; q < (e1 - e0) * m; q += blockDim.x) {
+      const int e = e0 + q / m, a = q % m;
+      const long long idx = (static_cast<long long>(e) * A.ncols + col) * m + a;
+      const double2 wv = A.w[idx];
+      A.V[static_cast<long long>(j + 1) * nall + idx] = make_double2(wv.x / hn, wv.y / hn);
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = L.h[static_cast<long long>(col) * lds + i];
+    givensStep(A, col, j, hn, hcol, sh);
+  }
+}
+
+size_t lsColsSolveSmem(int restart) {
+  return sizeof(double2) * (RMAX + 1 + static_cast<size_t>(restart) * (restart + 1) / 2);
+}
+
+template <int KPL>
+void lsColsLaunch(const GmresArgs& A, const ColsLS& L, size_t solveSmem, cudaStream_t s) {
+  const dim3 grid(L.nblk, A.ncols);
+  lsColsDots<KPL><<<grid, kThreads, 0, s>>>(A, L);
+  lsColsSolve<<<A.ncols, kThreads, solveSmem, s>>>(A, L);
+  lsColsUpdate<KPL><<<grid, kThreads, 0, s>>>(A, L);
+  lsColsFinish<<<grid, kThreads, 0, s>>>(A, L);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
 // One Arnoldi step j for every running column (any column count / size).
 __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
   __shared__ double2 scratch[kWarps];
@@ -495,6 +749,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   const bool fast = ncols == 1 && c.n <= static_cast<long long>(grid) * kThreads * FAST_K;
   const long long lsChunk = (c.n + grid - 1) / grid;
   const bool lowSync = o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
+  const bool colsLS = o.orthog == 1 && ncols > 1 && c.m <= 256;
+  const int colsKpl = c.m <= 32 ? 1 : c.m <= 64 ? 2 : c.m <= 128 ? 4 : 8;
+  const size_t colsSolveSmem = lsColsSolveSmem(R);
   const size_t lsSmem = static_cast<size_t>(arnoldiLSSmem(lsChunk, R)) * sizeof(double2);
 
   GmresArgs A{};
@@ -533,6 +790,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     W.lsS = static_cast<double2*>(dalloc(sizeof(double2) * (R + 1) * (R + 1)));
     W.lsDots = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1)));
     W.lsPart = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1) * grid));
+    if (ncols > 1) {
+      const long long nblk = (c.ne + kColsElems - 1) / kColsElems;
+      W.clPart = static_cast<double2*>(dalloc(sizeof(double2) * ncols * 2 * (R + 1) * nblk));
+      W.clS = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1) * (R + 1)));
+      W.clH = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1)));
+      W.clNrm = static_cast<double2*>(dalloc(sizeof(double2) * ncols * nblk));
+      W.clRun = static_cast<int*>(dalloc(sizeof(int) * ncols));
+    }
     TBT_CUDA_CHECK(cudaMemsetAsync(W.bar, 0, sizeof(unsigned long long), s));
     std::memcpy(W.key, key, sizeof(key));
   }
@@ -553,7 +818,11 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   double2* lsS = W.lsS;
   double2* lsDots = W.lsDots;
   double2* lsPart = W.lsPart;
+  ColsLS CL{W.clPart, W.clS, W.clH, W.clNrm, W.clRun, static_cast<int>((c.ne + kColsElems - 1) / kColsElems)};
   try {
+    if (colsLS && colsSolveSmem > 48 * 1024)
+      TBT_CUDA_CHECK(cudaFuncSetAttribute(lsColsSolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(colsSolveSmem)));
     if (lowSync) {
       TBT_CUDA_CHECK(cudaFuncSetAttribute(gmresArnoldiLS, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(lsSmem)));
@@ -581,6 +850,13 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
                                                    dim3(kThreads), params, lsSmem, s));
       } else if (fast) {
         coopLaunch(reinterpret_cast<const void*>(gmresArnoldi1), grid, 0, A, s);
+      } else if (colsLS) {
+        switch (colsKpl) {
+          case 1: lsColsLaunch<1>(A, CL, colsSolveSmem, s); break;
+          case 2: lsColsLaunch<2>(A, CL, colsSolveSmem, s); break;
+          case 4: lsColsLaunch<4>(A, CL, colsSolveSmem, s); break;
+          default: lsColsLaunch<8>(A, CL, colsSolveSmem, s); break;
+        }
       } else if (ncols > 1 && c.m <= kThreads) {
         gmresArnoldiCols<<<ncols, kThreads, 0, s>>>(A);
         TBT_CUDA_CHECK(cudaGetLastError());

@@ -43,6 +43,8 @@ struct GmresWs {
   unsigned long long* bar = nullptr;
   double2 *ax = nullptr, *w = nullptr, *V = nullptr;
   double2 *lsS = nullptr, *lsDots = nullptr, *lsPart = nullptr;
+  double2 *clPart = nullptr, *clS = nullptr, *clH = nullptr, *clNrm = nullptr;  // many-column LS
+  int* clRun = nullptr;
   double2 *bufB = nullptr, *bufX = nullptr;  // tbt_gmres staging
   long long bufLen = 0;
   cudaGraphExec_t inner = nullptr;  // captured inner loop of a restart cycle

@@ -256,14 +256,17 @@ def test_gmres_c2_budget_parity(gpu, orthog):
     assert rel(g.current, r["x"]) < GMRES_TOL
 
 
-def test_gmres_multi_column_and_a_only(gpu, fft_path):
+@pytest.mark.parametrize("orthog", [0, 1])
+def test_gmres_multi_column_and_a_only(gpu, fft_path, orthog):
+    """Columns in lockstep; orthog=1 runs the batched low-sync Arnoldi
+    (lsCols* kernels), orthog=0 the per-column MGS sweep."""
     rep = rep_for(5, 4, 8, seed=3)
     o = oracle.Oracle.from_rep(rep)
     B = gen.rhs_normal(o.n, 3, 21)
     B[:, 1] = 0.0  # zero column converges immediately (bnorm == 0)
     op = ToeplitzMatvec(rep, max_nrhs=3)
     for a_only in (False, True):
-        opt = SolverOptions(tol=1e-9, maxIter=500, restart=12)
+        opt = SolverOptions(tol=1e-9, maxIter=500, restart=12, orthog=orthog)
         g = op.gmres(B, opt, use_a_only=a_only)
         r = o.gmres(B, tol=1e-9, max_iter=500, restart=12, use_a_only=a_only)
         assert g.iterations == r["iterations"]
@@ -274,6 +277,26 @@ def test_gmres_multi_column_and_a_only(gpu, fft_path):
                 continue
             assert rel(g.current[:, c], r["x"][:, c]) < GMRES_TOL
             hist_close(g.history[c], r["history"][c], GMRES_TOL)
+
+
+@pytest.mark.parametrize("nx,ny,m,k,orthog", [(4, 3, 128, 10, 1), (6, 5, 64, 20, 1), (4, 3, 128, 10, 0),
+                                              (3, 3, 200, 5, 1)])
+def test_gmres_many_columns(gpu, nx, ny, m, k, orthog):
+    """Many columns at C3-like basis sizes (one warp per element, m/32 values
+    per lane); columns stop at different iterations and restarts."""
+    rep = rep_for(nx, ny, m, seed=5, rank=8)
+    o = oracle.Oracle.from_rep(rep)
+    B = gen.rhs_normal(o.n, k, 33)
+    B[:, 1] *= 1e-3
+    op = ToeplitzMatvec(rep, max_nrhs=k)
+    opt = SolverOptions(tol=1e-8, maxIter=300, restart=15, orthog=orthog)
+    g = op.gmres(B, opt, raise_on_fail=False)
+    r = o.gmres(B, tol=1e-8, max_iter=300, restart=15)
+    assert g.iterations == r["iterations"]
+    assert g.converged == r["converged"]
+    for c in range(k):
+        assert rel(g.current[:, c], r["x"][:, c]) < GMRES_TOL
+        hist_close(g.history[c], r["history"][c], GMRES_TOL)
 
 
 def test_gmres_nonconvergence_raises(gpu):
