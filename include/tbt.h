@@ -170,8 +170,11 @@ tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
  * two FFT transposes are grouped ncclSend/ncclRecv all-to-alls. No
  * reference counterpart. Call sequence on every rank:
  * tbt_create -> tbt_set_generators (all blocks) -> [tbt_set_correction] ->
- * tbt_dist_init -> tbt_precompute; tbt_apply/tbt_apply_a/tbt_diagonal then
- * take and return this rank's row slab (tbt_dist_rows). */
+ * tbt_dist_init -> tbt_precompute; tbt_apply/tbt_apply_a/tbt_diagonal/
+ * tbt_gmres then take and return this rank's row slab (tbt_dist_rows). The
+ * distributed tbt_gmres runs the low-synchronisation Arnoldi (orthog = 1
+ * whatever opts->orthog says) with two ncclAllReduce calls per iteration;
+ * every rank returns the same stats. */
 tbt_status tbt_dist_unique_id(char* id /* NCCL_UNIQUE_ID_BYTES = 128 */);
 tbt_status tbt_dist_init(tbt_ctx* ctx, int nranks, int rank, const char* id);
 tbt_status tbt_dist_rows(const tbt_ctx* ctx, int* row_begin, int* row_end);

@@ -577,12 +577,13 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
   tbt_status st = guarded([&] {
     TBT_USER_CHECK(h && b && x && opts, "tbt_gmres: null argument");
     Ctx& c = h->c;
-    TBT_USER_CHECK(!c.dist, "tbt_gmres: not available on a distributed context yet (apply is)");
     requireReady(c);
     TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, "tbt_gmres: nrhs outside [1, max_nrhs]");
     TBT_USER_CHECK(opts->restart >= 1 && opts->max_iter >= 0 && opts->tol > 0.0, "tbt_gmres: bad options");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
-    const long long total = c.n * nrhs;
+    // Multi-GPU: b and x are this rank's element-row slab (tbt_dist_rows).
+    const long long nloc = c.dist ? static_cast<long long>(c.myRows) * c.nx * c.m : c.n;
+    const long long total = nloc * nrhs;
     const size_t bytes = total * sizeof(double2);
     GmresWs* W = gmresWorkspace(c);
     if (W->bufLen < total) {
@@ -602,17 +603,17 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
     const double2* bsrc = reinterpret_cast<const double2*>(b);
     if (where == TBT_HOST) {
       TBT_CUDA_CHECK(cudaMemcpyAsync(dx, bsrc, bytes, cudaMemcpyHostToDevice, c.stream));
-      launchLayout(dx, db, c.n, nrhs, true, c.stream, c.m);
+      launchLayout(dx, db, nloc, nrhs, true, c.stream, c.m);
     } else {
-      launchLayout(bsrc, db, c.n, nrhs, true, c.stream, c.m);
+      launchLayout(bsrc, db, nloc, nrhs, true, c.stream, c.m);
     }
     gmresSolve(c, db, dx, nrhs, *opts, opts->use_a_only != 0, out, hist, matvecs);
     double2* xdst = reinterpret_cast<double2*>(x);
     if (where == TBT_HOST) {
-      launchLayout(dx, db, c.n, nrhs, false, c.stream, c.m);
+      launchLayout(dx, db, nloc, nrhs, false, c.stream, c.m);
       TBT_CUDA_CHECK(cudaMemcpyAsync(xdst, db, bytes, cudaMemcpyDeviceToHost, c.stream));
     } else {
-      launchLayout(dx, xdst, c.n, nrhs, false, c.stream, c.m);
+      launchLayout(dx, xdst, nloc, nrhs, false, c.stream, c.m);
     }
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     if (stats) {

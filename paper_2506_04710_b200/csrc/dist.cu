@@ -45,20 +45,14 @@ const NcclApi& nccl() {
     TBT_SYM(ncclSend, send);
     TBT_SYM(ncclRecv, recv);
     TBT_SYM(ncclGetErrorString, errorString);
+    TBT_SYM(ncclAllReduce, allReduce);
 #undef TBT_SYM
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart && api.groupEnd &&
-             api.send && api.recv && api.errorString;
+             api.send && api.recv && api.errorString && api.allReduce;
   });
   if (!api.ok) throw Error{TBT_CUDA_ERROR, "NCCL (libnccl.so.2) could not be loaded"};
   return api;
 }
-
-#define TBT_NCCL_CHECK(expr)                                                                  \
-  do {                                                                                        \
-    ncclResult_t r_ = (expr);                                                                 \
-    if (r_ != ncclSuccess)                                                                    \
-      throw ::tbt::Error{TBT_CUDA_ERROR, std::string(#expr) + ": " + nccl().errorString(r_)}; \
-  } while (0)
 
 // Row slabs and column groups (pure host logic; tested on the CPU).
 void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols) {

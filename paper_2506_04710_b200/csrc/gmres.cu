@@ -329,34 +329,183 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiCols(GmresArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// Many columns, low-synchronisation MGS (orthog = 1): the same
-// h = (I + L)^{-1} V^H w recurrence as arnoldiLS (gmres_dev.cuh), batched
-// over the columns, in four launches instead of one grid barrier per
-// projection:
-//   lsColsDots    c_k = <v_k, w>, S_jk = <v_j, v_k>: one warp per element,
-//                 lane-strided basis values in registers; per-CTA partials
-//   lsColsSolve   CTA per column: fixed-order totals, forward substitution
+// Column-blocked GMRES kernels: many columns (C3) and the multi-GPU solve.
+// Grids are (element blocks) x (columns), one warp per element with the m
+// basis values lane-strided in registers (KPL = ceil(m/32) <= 8). Every
+// reduction is two-stage and fixed-order: per-CTA partials
+// part[col][slot][blk], then colReduce sums them per (slot, col) into
+// tot[slot][col] -- the contiguous array a multi-GPU solve all-reduces
+// (ncclAllReduce, the only collective of the solve) before the consumers
+// read it. Low-synchronisation MGS (the arnoldiLS recurrence,
+// gmres_dev.cuh) batched over the columns:
+//   lsColsDots    c_k = <v_k, M w> (slot k), S_jk = <v_j, v_k> (slot j+1+k)
+//   lsColsSolve   CTA per column: h = (I + L)^{-1} c (forward substitution)
 //   lsColsUpdate  w' = M w - V h, ||w'||^2 partials
 //   lsColsFinish  v_{j+1} = w' / ||w'||, Givens (first CTA of each column)
-// Two passes over the basis per step (the sweep reads it j+1 times and
-// rewrites w each time). Every total is a fixed-order sum: reproducible.
+// Two passes over the basis per step; the per-projection sweep reads it j+1
+// times and rewrites w each time.
 struct ColsLS {
-  double2* part;  // [ncols][2*(restart+1)][nblk]: c_k in slot k, S_jk in slot restart+1+k
+  double2* part;  // [ncols][2*(restart+1)][nblk]
+  double2* tot;   // [2*(restart+1)][ncols]
   double2* S;     // [ncols][restart+1][restart+1], S(i,k) = <v_i, v_k>, k < i
   double2* h;     // [ncols][restart+1]
-  double2* nrm;   // [ncols][nblk]
-  int* run;       // [ncols] column ran this step (snapshot taken by lsColsSolve)
+  int* run;       // [ncols] column runs this step / cycle
   int nblk;
 };
 constexpr int kColsElems = kWarps;  // elements per CTA, one per warp
+
+__device__ __forceinline__ long long colsPart(const GmresArgs& A, const ColsLS& L, int col, int slot) {
+  return (static_cast<long long>(col) * 2 * (A.restart + 1) + slot) * L.nblk + blockIdx.x;
+}
+
+// CTA sum of a per-warp value in fixed order, written as partial `slot`.
+__device__ __forceinline__ void colsBlockPartial(const GmresArgs& A, const ColsLS& L, int col, int slot, double2 v,
+                                                 double2* scratch) {
+  v = warpSum(v);
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = scratch[0];
+    for (int q = 1; q < kWarps; ++q) t = cadd(t, scratch[q]);
+    L.part[colsPart(A, L, col, slot)] = t;
+  }
+}
+
+// tot[slot][col] = sum_blk part[col][slot][blk], slots [0, nslots).
+__global__ void colReduce(GmresArgs A, ColsLS L, int nslots) {
+  const int col = blockIdx.x;
+  const int lds2 = 2 * (A.restart + 1);
+  for (int slot = threadIdx.x; slot < nslots; slot += blockDim.x) {
+    const double2* p = L.part + (static_cast<long long>(col) * lds2 + slot) * L.nblk;
+    double2 t = make_double2(0.0, 0.0);
+    for (int b = 0; b < L.nblk; ++b) t = cadd(t, p[b]);
+    L.tot[static_cast<long long>(slot) * A.ncols + col] = t;
+  }
+}
+
+// Element-wise passes of init / cycle start, partial |.|^2 in slot 0:
+//   0  |b|^2                         (gmresInit)
+//   1  w = r = b - A x, |r|^2         (columns not done)
+//   2  v_0 = z = M r, |z|^2           (columns with run = 1)
+//   3  v_0 /= beta                    (run = 1, beta = sqrt(tot[0][col]) > 0)
+template <int KPL>
+__global__ void __launch_bounds__(kThreads) colsVecPass(GmresArgs A, ColsLS L, int mode) {
+  __shared__ double2 scratch[kWarps];
+  const int col = blockIdx.y;
+  if (mode == 1 && A.st[col].done) return;
+  if ((mode == 2 || mode == 3) && !L.run[col]) return;
+  double beta = 1.0;
+  if (mode == 3) {
+    beta = sqrt(L.tot[col].x);
+    if (beta == 0.0) return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, m = A.m;
+  const int e = blockIdx.x * kColsElems + warp;
+  const long long base = (static_cast<long long>(e) * A.ncols + col) * m;
+  double2 acc = make_double2(0.0, 0.0);
+  if (e < A.ne) {
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      const int a = lane + 32 * k;
+      if (a >= m) continue;
+      const long long q = base + a;
+      double2 v;
+      if (mode == 0) {
+        v = A.b[q];
+      } else if (mode == 1) {
+        v = csub(A.b[q], A.ax[q]);
+        A.w[q] = v;
+      } else if (mode == 2) {
+        v = A.w[q];
+        if (A.dinv) v = cmul(v, A.dinv[static_cast<long long>(e) * m + a]);
+        A.V[q] = v;
+      } else {
+        const double2 z = A.V[q];
+        A.V[q] = make_double2(z.x / beta, z.y / beta);
+        continue;
+      }
+      acc.x += v.x * v.x + v.y * v.y;
+    }
+  }
+  if (mode != 3) colsBlockPartial(A, L, col, 0, acc, scratch);
+}
+
+// Per-column state transitions (one thread per column) on the totals:
+//   0  after |b|^2: gmresInit's state
+//   1  after |r|^2: restart residual test (linsolve.cpp:446-452), run flag
+//   2  after |z|^2: beta, g (linsolve.cpp:453-461); run = beta > 0
+__global__ void colsState(GmresArgs A, ColsLS L, int phase) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= A.ncols) return;
+  GmresState& st = A.st[col];
+  const double t = L.tot[col].x;
+  if (phase == 0) {
+    st.bnorm = sqrt(t);
+    st.beta = st.beta0 = st.residual = 0.0;
+    st.iterations = st.ncount = st.histLen = 0;
+    st.stopInner = 1;
+    st.cycleActive = 0;
+    st.done = st.bnorm == 0.0 ? 1 : 0;
+    st.converged = st.done;
+    return;
+  }
+  if (phase == 1) {
+    if (st.done) {
+      L.run[col] = 0;
+      return;
+    }
+    const double res = sqrt(t) / st.bnorm;
+    int decision = 0;
+    if (res < A.tol)
+      decision = 1;
+    else if (st.iterations >= A.maxIter)
+      decision = 2;
+    st.residual = res;
+    pushHist(A, col, decision == 2 ? 2.0 : 0.0, res);
+    if (decision != 0) {
+      st.done = 1;
+      st.converged = decision == 1 ? 1 : 0;
+      st.cycleActive = 0;
+      st.stopInner = 1;
+    }
+    L.run[col] = decision == 0 ? 1 : 0;
+    return;
+  }
+  if (!L.run[col]) return;
+  const double beta = sqrt(t);
+  if (beta == 0.0) {
+    st.done = 1;
+    st.converged = 1;
+    st.cycleActive = 0;
+    st.stopInner = 1;
+    L.run[col] = 0;
+    return;
+  }
+  st.beta = beta;
+  if (st.beta0 == 0.0) st.beta0 = beta;
+  st.ncount = 0;
+  st.stopInner = 0;
+  st.cycleActive = 1;
+  double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
+  for (int k = 0; k <= A.restart; ++k) g[k] = make_double2(0.0, 0.0);
+  g[0] = make_double2(beta, 0.0);
+}
+
+// Snapshot of "column runs this Arnoldi step" (the Givens step of
+// lsColsFinish may stop a column while other CTAs of it still work).
+__global__ void colsRunFlags(GmresArgs A, ColsLS L) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= A.ncols) return;
+  const GmresState st = A.st[col];
+  L.run[col] = st.cycleActive && !st.stopInner;
+}
 
 template <int KPL>
 __global__ void __launch_bounds__(kThreads) lsColsDots(GmresArgs A, ColsLS L) {
   __shared__ double2 red[kWarps][2 * (RMAX + 1)];
   const int col = blockIdx.y;
-  const GmresState st = A.st[col];
-  if (!(st.cycleActive && !st.stopInner)) return;
-  const int j = A.j, m = A.m, lds = A.restart + 1;
+  if (!L.run[col]) return;
+  const int j = A.j, m = A.m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = blockIdx.x * kColsElems + warp;
   const bool ev = e < A.ne;
@@ -398,19 +547,18 @@ __global__ void __launch_bounds__(kThreads) lsColsDots(GmresArgs A, ColsLS L) {
     s1 = warpSum(s1);
     if (lane == 0) {
       red[warp][kk] = c0;
-      if (kk < j) red[warp][lds + kk] = s0;
+      if (kk < j) red[warp][j + 1 + kk] = s0;
       if (two) {
         red[warp][kk + 1] = c1;
-        if (kk + 1 < j) red[warp][lds + kk + 1] = s1;
+        if (kk + 1 < j) red[warp][j + 2 + kk] = s1;
       }
     }
   }
   __syncthreads();
   for (int d = threadIdx.x; d < 2 * j + 1; d += blockDim.x) {
-    const int slot = d <= j ? d : lds + (d - j - 1);
-    double2 t = red[0][slot];
-    for (int q = 1; q < kWarps; ++q) t = cadd(t, red[q][slot]);
-    L.part[(static_cast<long long>(col) * 2 * lds + slot) * L.nblk + blockIdx.x] = t;
+    double2 t = red[0][d];
+    for (int q = 1; q < kWarps; ++q) t = cadd(t, red[q][d]);
+    L.part[colsPart(A, L, col, d)] = t;
   }
 }
 
@@ -418,20 +566,14 @@ __global__ void __launch_bounds__(kThreads) lsColsDots(GmresArgs A, ColsLS L) {
 __global__ void __launch_bounds__(kThreads) lsColsSolve(GmresArgs A, ColsLS L) {
   extern __shared__ double2 shs[];
   const int col = blockIdx.x;
-  const GmresState st = A.st[col];
-  const int running = st.cycleActive && !st.stopInner;
-  if (threadIdx.x == 0) L.run[col] = running;
-  if (!running) return;
+  if (!L.run[col]) return;
   const int j = A.j, lds = A.restart + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* cv = shs;
   double2* sL = shs + RMAX + 1;  // row i (1..j) at i*(i-1)/2
   double2* S = L.S + static_cast<long long>(col) * lds * lds;
-  const double2* part = L.part + static_cast<long long>(col) * 2 * lds * L.nblk;
   for (int d = threadIdx.x; d < 2 * j + 1; d += blockDim.x) {
-    const int slot = d <= j ? d : lds + (d - j - 1);
-    double2 t = make_double2(0.0, 0.0);
-    for (int b = 0; b < L.nblk; ++b) t = cadd(t, part[static_cast<long long>(slot) * L.nblk + b]);
+    const double2 t = L.tot[static_cast<long long>(d) * A.ncols + col];
     if (d <= j) {
       cv[d] = t;
     } else {
@@ -527,30 +669,16 @@ __global__ void __launch_bounds__(kThreads) lsColsUpdate(GmresArgs A, ColsLS L) 
       acc.x += w[k].x * w[k].x + w[k].y * w[k].y;
     }
   }
-  acc = warpSum(acc);
-  if (lane == 0) scratch[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double2 t = scratch[0];
-    for (int q = 1; q < kWarps; ++q) t = cadd(t, scratch[q]);
-    L.nrm[static_cast<long long>(col) * L.nblk + blockIdx.x] = t;
-  }
+  colsBlockPartial(A, L, col, 0, acc, scratch);
 }
 
 __global__ void __launch_bounds__(kThreads) lsColsFinish(GmresArgs A, ColsLS L) {
   __shared__ double2 hcol[RMAX + 2];
   __shared__ double2 sh[3 * RMAX + 4];
-  __shared__ double sHn;
   const int col = blockIdx.y;
   if (!L.run[col]) return;
   const int j = A.j, m = A.m, lds = A.restart + 1;
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < L.nblk; ++b) t += L.nrm[static_cast<long long>(col) * L.nblk + b].x;
-    sHn = sqrt(t);
-  }
-  __syncthreads();
-  const double hn = sHn;
+  const double hn = sqrt(L.tot[col].x);
   if (hn > 0.0) {
     const long long nall = static_cast<long long>(A.ne) * m * A.ncols;
     const int e0 = blockIdx.x * kColsElems;
@@ -572,15 +700,75 @@ size_t lsColsSolveSmem(int restart) {
   return sizeof(double2) * (RMAX + 1 + static_cast<size_t>(restart) * (restart + 1) / 2);
 }
 
-template <int KPL>
-void lsColsLaunch(const GmresArgs& A, const ColsLS& L, size_t solveSmem, cudaStream_t s) {
-  const dim3 grid(L.nblk, A.ncols);
-  lsColsDots<KPL><<<grid, kThreads, 0, s>>>(A, L);
-  lsColsSolve<<<A.ncols, kThreads, solveSmem, s>>>(A, L);
-  lsColsUpdate<KPL><<<grid, kThreads, 0, s>>>(A, L);
-  lsColsFinish<<<grid, kThreads, 0, s>>>(A, L);
-  TBT_CUDA_CHECK(cudaGetLastError());
-}
+// Host side of the column-blocked solve: `reduce(nslots)` = colReduce, then
+// (multi-GPU) the all-reduce of tot[0 .. nslots*ncols).
+struct ColsRunner {
+  GmresArgs* A;
+  ColsLS L;
+  int kpl;
+  size_t solveSmem;
+  Ctx* c;
+  cudaStream_t s;
+
+  void reduce(int nslots) {
+    colReduce<<<A->ncols, 128, 0, s>>>(*A, L, nslots);
+    TBT_CUDA_CHECK(cudaGetLastError());
+    if (c->dist)
+      TBT_NCCL_CHECK(nccl().allReduce(L.tot, L.tot, static_cast<size_t>(nslots) * A->ncols * 2, ncclDouble, ncclSum,
+                                      c->comm, s));
+  }
+  template <int K>
+  void vecPass(int mode) {
+    colsVecPass<K><<<dim3(L.nblk, A->ncols), kThreads, 0, s>>>(*A, L, mode);
+  }
+  void vec(int mode) {
+    switch (kpl) {
+      case 1: vecPass<1>(mode); break;
+      case 2: vecPass<2>(mode); break;
+      case 4: vecPass<4>(mode); break;
+      default: vecPass<8>(mode); break;
+    }
+    TBT_CUDA_CHECK(cudaGetLastError());
+  }
+  void state(int phase) {
+    colsState<<<(A->ncols + 127) / 128, 128, 0, s>>>(*A, L, phase);
+    TBT_CUDA_CHECK(cudaGetLastError());
+  }
+  void init() {
+    vec(0);
+    reduce(1);
+    state(0);
+  }
+  void cycleStart() {
+    vec(1);
+    reduce(1);
+    state(1);
+    vec(2);
+    reduce(1);
+    state(2);
+    vec(3);
+  }
+  template <int K>
+  void arnoldiK() {
+    const dim3 grid(L.nblk, A->ncols);
+    colsRunFlags<<<(A->ncols + 127) / 128, 128, 0, s>>>(*A, L);
+    lsColsDots<K><<<grid, kThreads, 0, s>>>(*A, L);
+    reduce(2 * A->j + 1);
+    lsColsSolve<<<A->ncols, kThreads, solveSmem, s>>>(*A, L);
+    lsColsUpdate<K><<<grid, kThreads, 0, s>>>(*A, L);
+    reduce(1);
+    lsColsFinish<<<grid, kThreads, 0, s>>>(*A, L);
+    TBT_CUDA_CHECK(cudaGetLastError());
+  }
+  void arnoldi() {
+    switch (kpl) {
+      case 1: arnoldiK<1>(); break;
+      case 2: arnoldiK<2>(); break;
+      case 4: arnoldiK<4>(); break;
+      default: arnoldiK<8>(); break;
+    }
+  }
+};
 
 // One Arnoldi step j for every running column (any column count / size).
 __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
@@ -740,16 +928,23 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
                 std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs) {
   const int R = o.restart;
   TBT_USER_CHECK(R <= RMAX, "tbt_gmres: restart above " + std::to_string(RMAX));
-  const long long nall = c.n * ncols;
+  // Multi-GPU: this rank's element-row slab (dist.cu); every reduction of
+  // the solve is all-reduced, so all ranks take identical decisions.
+  const int neLoc = c.dist ? c.myRows * c.nx : c.ne;
+  const long long nloc = static_cast<long long>(neLoc) * c.m;
+  const long long nall = nloc * ncols;
   cudaStream_t s = c.stream;
   const int sms = smCount(c.device);
   // One CTA per SM: always co-resident, as the grid barrier requires
   // (cudaLaunchCooperativeKernel rejects a grid that is not).
   const int grid = sms;
-  const bool fast = ncols == 1 && c.n <= static_cast<long long>(grid) * kThreads * FAST_K;
-  const long long lsChunk = (c.n + grid - 1) / grid;
-  const bool lowSync = o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
-  const bool colsLS = o.orthog == 1 && ncols > 1 && c.m <= 256;
+  // Column-blocked kernels + all-reduces for the multi-GPU solve (always
+  // low-synchronisation MGS there) and for many columns.
+  const bool colsLS = c.dist || (o.orthog == 1 && ncols > 1 && c.m <= 256);
+  TBT_USER_CHECK(!c.dist || c.m <= 256, "tbt_gmres: distributed solve supports m <= 256");
+  const bool fast = !colsLS && ncols == 1 && nloc <= static_cast<long long>(grid) * kThreads * FAST_K;
+  const long long lsChunk = (nloc + grid - 1) / grid;
+  const bool lowSync = !colsLS && o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
   const int colsKpl = c.m <= 32 ? 1 : c.m <= 64 ? 2 : c.m <= 128 ? 4 : 8;
   const size_t colsSolveSmem = lsColsSolveSmem(R);
   const size_t lsSmem = static_cast<size_t>(arnoldiLSSmem(lsChunk, R)) * sizeof(double2);
@@ -761,12 +956,12 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   A.histCap = std::max(0, o.hist_cap);
   A.precondition = o.precondition;
   A.tol = o.tol;
-  A.ne = c.ne;
+  A.ne = neLoc;
   A.m = c.m;
   // Device workspace, cached in the context across solves of the same shape
   // (allocation and graph instantiation are per-solve costs otherwise).
   GmresWs& W = *gmresWorkspace(c);
-  const long long key[5] = {ncols, R, nall, std::max(1, A.histCap), grid};
+  const long long key[6] = {ncols, R, nall, std::max(1, A.histCap), grid, colsLS ? 1 : 0};
   if (std::memcmp(key, W.key, sizeof(key)) != 0) {
     W.release();
     auto dalloc = [&](size_t bytes) {
@@ -790,12 +985,12 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     W.lsS = static_cast<double2*>(dalloc(sizeof(double2) * (R + 1) * (R + 1)));
     W.lsDots = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1)));
     W.lsPart = static_cast<double2*>(dalloc(sizeof(double2) * 2 * (R + 1) * grid));
-    if (ncols > 1) {
-      const long long nblk = (c.ne + kColsElems - 1) / kColsElems;
+    if (colsLS) {
+      const long long nblk = (neLoc + kColsElems - 1) / kColsElems;
       W.clPart = static_cast<double2*>(dalloc(sizeof(double2) * ncols * 2 * (R + 1) * nblk));
+      W.clTot = static_cast<double2*>(dalloc(sizeof(double2) * ncols * 2 * (R + 1)));
       W.clS = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1) * (R + 1)));
       W.clH = static_cast<double2*>(dalloc(sizeof(double2) * ncols * (R + 1)));
-      W.clNrm = static_cast<double2*>(dalloc(sizeof(double2) * ncols * nblk));
       W.clRun = static_cast<int*>(dalloc(sizeof(int) * ncols));
     }
     TBT_CUDA_CHECK(cudaMemsetAsync(W.bar, 0, sizeof(unsigned long long), s));
@@ -818,7 +1013,8 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   double2* lsS = W.lsS;
   double2* lsDots = W.lsDots;
   double2* lsPart = W.lsPart;
-  ColsLS CL{W.clPart, W.clS, W.clH, W.clNrm, W.clRun, static_cast<int>((c.ne + kColsElems - 1) / kColsElems)};
+  ColsRunner cols{&A, ColsLS{W.clPart, W.clTot, W.clS, W.clH, W.clRun, (neLoc + kColsElems - 1) / kColsElems},
+                  colsKpl, colsSolveSmem, &c, s};
   try {
     if (colsLS && colsSolveSmem > 48 * 1024)
       TBT_CUDA_CHECK(cudaFuncSetAttribute(lsColsSolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -833,10 +1029,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     TBT_CUDA_CHECK(cudaMemsetAsync(A.H, 0, sizeof(double2) * ncols * (R + 1) * R, s));
     TBT_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * nall, s));
     A.dinv = o.precondition ? (useAOnly ? c.dDiagInvA : c.dDiagInv) : nullptr;
+    if (A.dinv && c.dist) A.dinv += static_cast<long long>(c.myRow0) * c.nx * c.m;
     const size_t smem = sizeof(int) * ncols;
 
     matvecs = 0;
-    coopLaunch(reinterpret_cast<const void*>(gmresInit), grid, smem, A, s);
+    if (colsLS)
+      cols.init();
+    else
+      coopLaunch(reinterpret_cast<const void*>(gmresInit), grid, smem, A, s);
     std::vector<GmresState> st(ncols);
     auto pull = [&]() {
       TBT_CUDA_CHECK(cudaMemcpyAsync(st.data(), A.st, sizeof(GmresState) * ncols, cudaMemcpyDeviceToHost, s));
@@ -851,12 +1051,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       } else if (fast) {
         coopLaunch(reinterpret_cast<const void*>(gmresArnoldi1), grid, 0, A, s);
       } else if (colsLS) {
-        switch (colsKpl) {
-          case 1: lsColsLaunch<1>(A, CL, colsSolveSmem, s); break;
-          case 2: lsColsLaunch<2>(A, CL, colsSolveSmem, s); break;
-          case 4: lsColsLaunch<4>(A, CL, colsSolveSmem, s); break;
-          default: lsColsLaunch<8>(A, CL, colsSolveSmem, s); break;
-        }
+        cols.arnoldi();
       } else if (ncols > 1 && c.m <= kThreads) {
         gmresArnoldiCols<<<ncols, kThreads, 0, s>>>(A);
         TBT_CUDA_CHECK(cudaGetLastError());
@@ -879,7 +1074,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     // (restart x [apply, Arnoldi]); every node turns into a no-op once the
     // column's inner loop stopped (device flag), so the host synchronises
     // once per restart cycle.
-    const bool useGraph = ncols == 1 && !c.timeBinprod;
+    const bool useGraph = ncols == 1 && !c.timeBinprod && !c.dist;
     GmresArgs keyA = A;  // what the captured nodes bake in (b, x unused by them)
     keyA.b = nullptr;
     keyA.x = nullptr;
@@ -914,7 +1109,10 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       while (open) {
         applyInternal(c, x, W.ax, ncols, !useAOnly);
         ++matvecs;
-        coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
+        if (colsLS)
+          cols.cycleStart();
+        else
+          coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
         if (useGraph) {
           TBT_CUDA_CHECK(cudaGraphLaunch(inner, s));
         } else {

@@ -34,7 +34,7 @@ struct GmresArgs {
 
 // Device workspace of gmresSolve, cached in the context (gmres.cu).
 struct GmresWs {
-  long long key[5] = {0, 0, 0, 0, 0};  // ncols, restart, n*ncols, hist cap, grid
+  long long key[6] = {0, 0, 0, 0, 0, 0};  // ncols, restart, n*ncols, hist cap, grid, column-blocked
   std::vector<void*> allocs;
   GmresState* st = nullptr;
   double2 *H = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *ycoef = nullptr;
@@ -43,7 +43,7 @@ struct GmresWs {
   unsigned long long* bar = nullptr;
   double2 *ax = nullptr, *w = nullptr, *V = nullptr;
   double2 *lsS = nullptr, *lsDots = nullptr, *lsPart = nullptr;
-  double2 *clPart = nullptr, *clS = nullptr, *clH = nullptr, *clNrm = nullptr;  // many-column LS
+  double2 *clPart = nullptr, *clTot = nullptr, *clS = nullptr, *clH = nullptr;  // column-blocked solve
   int* clRun = nullptr;
   double2 *bufB = nullptr, *bufX = nullptr;  // tbt_gmres staging
   long long bufLen = 0;

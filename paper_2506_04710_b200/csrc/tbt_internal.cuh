@@ -228,9 +228,18 @@ struct NcclApi {
   ncclResult_t (*groupEnd)() = nullptr;
   ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
 };
 const NcclApi& nccl();
+
+#define TBT_NCCL_CHECK(expr)                                                                  \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      throw ::tbt::Error{TBT_CUDA_ERROR, std::string(#expr) + ": " + nccl().errorString(r_)}; \
+  } while (0)
 void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols);
 void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);
 void distFree(Ctx& c);

@@ -141,3 +141,150 @@ def test_dist_one_rank_nccl(gpu, shape, embed, k):
         ref = o.apply(np.ascontiguousarray(X[:, c]))
         assert np.linalg.norm(Y[:, c] - ref) / np.linalg.norm(ref) < 1e-11
     assert np.allclose(op.diagonal(), o.diagonal(), rtol=1e-14, atol=0)
+
+
+def _ls_gmres_worker(rank, world, port, q, tol, max_iter, restart):
+    """Distributed GMRES as the column-blocked CUDA path runs it
+    (csrc/gmres.cu, ColsRunner): element-row slabs, every reduction a local
+    partial + all_reduce, low-synchronisation MGS h = (I + L)^{-1} V^H M w,
+    Givens / restart / history rules of linsolve.cpp:425-515."""
+    import torch
+    import torch.distributed as tdist
+
+    import oracle
+    from paper_2506_04710_b200 import gen
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = Config("g", 5, 6, 4, 1, 4, 9, "normal", 20)
+        rep = ToeplitzRep.synthetic(cfg)
+        o = oracle.Oracle.from_rep(rep)
+        L0 = 1 << (2 * cfg.nx - 2).bit_length()
+        r0, r1, _ = dist_plan(cfg.ny, L0, world, rank)
+        sl = slice(r0 * cfg.nx * cfg.m, r1 * cfg.nx * cfg.m)
+        b = gen.rhs_normal(o.n, 1, 13)[:, 0]
+        d = o.diagonal()
+        dinv = np.where(np.abs(d) > 0, 1.0 / np.where(d == 0, 1, d), 1.0)[sl]
+        bl = b[sl]
+
+        def allsum(a):
+            t = torch.from_numpy(np.ascontiguousarray(np.atleast_1d(a)))
+            tdist.all_reduce(t)
+            return t.numpy()
+
+        def matvec(xl):
+            parts = [torch.zeros(0, dtype=torch.complex128) for _ in range(world)]
+            tdist.all_gather_object(parts, xl)
+            return o.apply(np.concatenate(parts))[sl]
+
+        def nrm(v):
+            return float(np.sqrt(allsum(np.array([np.vdot(v, v).real]))[0]))
+
+        bnorm = nrm(bl)
+        x = np.zeros_like(bl)
+        hist, its, beta0 = [], 0, 0.0
+        while True:
+            r = bl - matvec(x)
+            res = nrm(r) / bnorm
+            if res < tol:
+                hist.append((0.0, res))
+                break
+            if its >= max_iter:
+                hist.append((2.0, res))
+                break
+            hist.append((0.0, res))
+            z = dinv * r
+            beta = nrm(z)
+            beta0 = beta0 or beta
+            V = [z / beta]
+            H = np.zeros((restart + 1, restart), complex)
+            S = np.zeros((restart + 1, restart + 1), complex)
+            cs, sn = np.zeros(restart, complex), np.zeros(restart, complex)
+            g = np.zeros(restart + 1, complex)
+            g[0] = beta
+            nc = 0
+            for j in range(restart):
+                wz = dinv * matvec(V[j])
+                loc = np.array([np.vdot(V[k], wz) for k in range(j + 1)] + [np.vdot(V[j], V[k]) for k in range(j)])
+                tot = allsum(loc)
+                c, S[j, :j] = tot[:j + 1], tot[j + 1:]
+                h = c.copy()
+                for k in range(j):
+                    h[k + 1:] -= S[k + 1:j + 1, k] * h[k]
+                w = wz - sum(h[k] * V[k] for k in range(j + 1))
+                hn = nrm(w)
+                if hn > 0:
+                    V.append(w / hn)
+                col = np.zeros(restart + 1, complex)
+                col[:j + 1], col[j + 1] = h, hn
+                for i in range(j):
+                    a0, a1 = col[i], col[i + 1]
+                    col[i] = cs[i] * a0 + sn[i] * a1
+                    col[i + 1] = -np.conj(sn[i]) * a0 + np.conj(cs[i]) * a1
+                den = np.sqrt(abs(col[j]) ** 2 + abs(col[j + 1]) ** 2)
+                cs[j], sn[j] = (1, 0) if den == 0 else (np.conj(col[j]) / den, np.conj(col[j + 1]) / den)
+                col[j] = cs[j] * col[j] + sn[j] * col[j + 1]
+                col[j + 1] = 0
+                H[:, j] = col
+                g[j + 1] = -np.conj(sn[j]) * g[j]
+                g[j] = cs[j] * g[j]
+                its += 1
+                nc = j + 1
+                hist.append((1.0, abs(g[j + 1]) / beta0))
+                if abs(g[j + 1]) / beta < 0.1 * tol or not hn > 0 or its >= max_iter:
+                    break
+            y = np.zeros(nc, complex)
+            for i in range(nc - 1, -1, -1):
+                y[i] = (g[i] - H[i, i + 1:nc] @ y[i + 1:nc]) / H[i, i]
+            x = x + sum(y[i] * V[i] for i in range(nc))
+        ref = o.gmres(b, tol=tol, max_iter=max_iter, restart=restart)
+        herr = max(abs(a[1] - bb[1]) / max(abs(bb[1]), 1e-300) for a, bb in zip(hist, ref["history"][0]))
+        kinds_ok = [a[0] for a in hist] == [float(v) for v in ref["history"][0][:, 0]]
+        xerr = np.linalg.norm(x - ref["x"][sl]) / np.linalg.norm(ref["x"][sl])
+        q.put((rank, its == ref["iterations"][0], kinds_ok, float(herr), float(xerr)))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tol,max_iter,restart", [(1e-9, 400, 10), (1e-12, 23, 7)])
+def test_distributed_ls_gmres_gloo_two_ranks(tol, max_iter, restart):
+    """The multi-GPU solve's algorithm on 2 gloo ranks equals the oracle's
+    (MGS) GMRES: iteration count, history kinds and values, solution."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ls_gmres_worker, args=(r, 2, port, q, tol, max_iter, restart)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    out = [q.get(timeout=10) for _ in range(2)]
+    for rank, its_ok, kinds_ok, herr, xerr in out:
+        assert its_ok and kinds_ok, out
+        assert herr < 1e-8 and xerr < 1e-8, out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,k", [((4, 4, 24), 1), ((6, 5, 64), 3), ((4, 3, 128), 12)])
+def test_dist_gmres_one_rank_nccl(gpu, shape, k):
+    """tbt_gmres on a distributed context (column-blocked kernels, NCCL
+    all-reduces on a one-rank communicator) against the oracle."""
+    import oracle
+    from paper_2506_04710_b200 import SolverOptions, ToeplitzMatvec, dist_unique_id, gen
+    nx, ny, m = shape
+    rep = ToeplitzRep.synthetic(Config("d", nx, ny, m, 1, 4, 3, "normal", 20))
+    op = ToeplitzMatvec(rep, max_nrhs=k, dist=(1, 0, dist_unique_id()))
+    o = oracle.Oracle.from_rep(rep)
+    B = gen.rhs_normal(o.n, k, 9)
+    g = op.gmres(B, SolverOptions(tol=1e-8, maxIter=120, restart=15), raise_on_fail=False)
+    r = o.gmres(B, tol=1e-8, max_iter=120, restart=15)
+    assert g.iterations == r["iterations"] and g.converged == r["converged"]
+    for c in range(k):
+        assert np.linalg.norm(g.current[:, c] - r["x"][:, c]) / np.linalg.norm(r["x"][:, c]) < 1e-8
+        h, hr = g.history[c], r["history"][c]
+        assert h.shape == hr.shape and np.array_equal(h[:, 0], hr[:, 0])
+        assert np.all(np.abs(h[:, 1] - hr[:, 1]) <= 1e-8 * np.abs(hr[:, 1]) + 1e-14)
