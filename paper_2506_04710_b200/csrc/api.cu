@@ -272,6 +272,7 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       c.forceMultiPass = fenv && std::string(fenv) == "passes";
       const char* genv = getenv("TBT_GMRES");
       c.forceUnfused = genv && std::string(genv) == "unfused";
+      c.forceCols = genv && std::string(genv) == "cols";
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinB));
       c.binprodKernel = binprodVariant(c.m);

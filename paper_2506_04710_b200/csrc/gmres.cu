@@ -371,16 +371,18 @@ __device__ __forceinline__ void colsBlockPartial(const GmresArgs& A, const ColsL
   }
 }
 
-// tot[slot][col] = sum_blk part[col][slot][blk], slots [0, nslots).
+// tot[slot][col] = sum_blk part[col][slot][blk], slots [0, nslots): one warp
+// per (slot, col), lanes over the blocks, fixed-order butterfly.
 __global__ void colReduce(GmresArgs A, ColsLS L, int nslots) {
-  const int col = blockIdx.x;
-  const int lds2 = 2 * (A.restart + 1);
-  for (int slot = threadIdx.x; slot < nslots; slot += blockDim.x) {
-    const double2* p = L.part + (static_cast<long long>(col) * lds2 + slot) * L.nblk;
-    double2 t = make_double2(0.0, 0.0);
-    for (int b = 0; b < L.nblk; ++b) t = cadd(t, p[b]);
-    L.tot[static_cast<long long>(slot) * A.ncols + col] = t;
-  }
+  const int col = blockIdx.y;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (slot >= nslots) return;
+  const int lane = threadIdx.x & 31;
+  const double2* p = L.part + (static_cast<long long>(col) * 2 * (A.restart + 1) + slot) * L.nblk;
+  double2 t = make_double2(0.0, 0.0);
+  for (int b = lane; b < L.nblk; b += 32) t = cadd(t, p[b]);
+  t = warpSum(t);
+  if (lane == 0) L.tot[static_cast<long long>(slot) * A.ncols + col] = t;
 }
 
 // Element-wise passes of init / cycle start, partial |.|^2 in slot 0:
@@ -711,7 +713,7 @@ struct ColsRunner {
   cudaStream_t s;
 
   void reduce(int nslots) {
-    colReduce<<<A->ncols, 128, 0, s>>>(*A, L, nslots);
+    colReduce<<<dim3((nslots + 7) / 8, A->ncols), 256, 0, s>>>(*A, L, nslots);
     TBT_CUDA_CHECK(cudaGetLastError());
     if (c->dist)
       TBT_NCCL_CHECK(nccl().allReduce(L.tot, L.tot, static_cast<size_t>(nslots) * A->ncols * 2, ncclDouble, ncclSum,
@@ -940,10 +942,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   const int grid = sms;
   // Column-blocked kernels + all-reduces for the multi-GPU solve (always
   // low-synchronisation MGS there) and for many columns.
-  const bool colsLS = c.dist || (o.orthog == 1 && ncols > 1 && c.m <= 256);
+  // One column: the LS step fused into the persistent apply for small
+  // vectors (C2: per-CTA row chunk in shared memory, no extra launches);
+  // from C4 up the column-blocked kernels are faster (measured: C4 0.553 vs
+  // 0.573 ms per iteration, C5 4.6 vs 5.2).
+  const long long lsChunk = (nloc + grid - 1) / grid;
+  const bool colsLS = c.dist || (o.orthog == 1 && c.m <= 256 && (ncols > 1 || lsChunk > 2048 || c.forceCols));
   TBT_USER_CHECK(!c.dist || c.m <= 256, "tbt_gmres: distributed solve supports m <= 256");
   const bool fast = !colsLS && ncols == 1 && nloc <= static_cast<long long>(grid) * kThreads * FAST_K;
-  const long long lsChunk = (nloc + grid - 1) / grid;
   const bool lowSync = !colsLS && o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
   const int colsKpl = c.m <= 32 ? 1 : c.m <= 64 ? 2 : c.m <= 128 ? 4 : 8;
   const size_t colsSolveSmem = lsColsSolveSmem(R);

@@ -113,6 +113,7 @@ struct Ctx {
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
   bool forceUnfused = false;               // TBT_GMRES=unfused: separate apply / Arnoldi launches
+  bool forceCols = false;                  // TBT_GMRES=cols: column-blocked Arnoldi for one column too
 
   // Multi-GPU (dist.cu): this rank owns element rows [myRow0, myRow0 +
   // myRows) of the vectors and the bin columns myColList (closed under
