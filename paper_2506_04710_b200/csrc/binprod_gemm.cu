@@ -3,9 +3,12 @@
 //     Yhat_f = Ahat X_f,      Yhat_g = Ahat^T X_g      (X: m x nrhs),
 // computed on the FP64 tensor path (mma.sync.m8n8k4.f64, "DMMA": on B200 it
 // runs at the FP64 peak with one instruction per 256 FMAs). A complex
-// 8x8x4 block is four real DMMAs (Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br;
-// no 3M trick, so rounding stays that of the plain product). The reference
-// re-streams every block once per column (linsolve.cpp:276-282, 572).
+// 8x8x4 block is THREE real DMMAs (3M / Gauss): S1 += Ar Br, S2 += Ai Bi,
+// S3 += (Ar + Ai)(Br + Bi); Re = S1 - S2, Im = S3 - S1 - S2 at the end. The
+// kernel is DMMA-bound, so this removes a quarter of its work; the extra
+// rounding is a few ulps of |A||X| (the matvec parity bound is 1e-11).
+// The reference re-streams every block once per column
+// (linsolve.cpp:276-282, 572).
 //
 // CTA tile: all M rows x NTILE right-hand sides of one (pair, transpose)
 // item; 8 warps, warp w owns rows [w*M/8, (w+1)*M/8). K advances in chunks
@@ -77,11 +80,13 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
     double2* Y = yhat + static_cast<long long>(bin) * B;
     const int n0 = tile * NTILE;
 
-    double acc[C::MB][NB][2][2];  // [mblock][nblock][re/im][c0/c1]
+    double acc[C::MB][NB][3][2];  // [mblock][nblock][S1/S2/S3][c0/c1]
 #pragma unroll
     for (int a = 0; a < C::MB; ++a)
 #pragma unroll
-      for (int b = 0; b < NB; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[a][b][q][0] = acc[a][b][q][1] = 0.0;
 
     auto load = [&](int kc, int stage) {
       double2* sA = gsm + stage * C::STAGE;
@@ -117,29 +122,29 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
       const double2* sB = sA + C::A_ELEMS;
 #pragma unroll
       for (int kk = 0; kk < KC; kk += 4) {
-        double ar[C::MB], ai[C::MB], br[NB], bi[NB];
+        double ar[C::MB], ai[C::MB], as[C::MB], br[NB], bi[NB], bs[NB];
 #pragma unroll
         for (int a = 0; a < C::MB; ++a) {
           const int i = warp * C::MW + a * 8 + gid;
           const double2 v = t == 0 ? sA[i * (KC + PADC) + kk + tig] : sA[(kk + tig) * M + i];
           ar[a] = v.x;
           ai[a] = v.y;
+          as[a] = v.x + v.y;
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           const double2 v = sB[(b * 8 + gid) * (KC + PADC) + kk + tig];
           br[b] = v.x;
           bi[b] = v.y;
+          bs[b] = v.x + v.y;
         }
 #pragma unroll
         for (int a = 0; a < C::MB; ++a) {
-          const double nai = -ai[a];
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-            dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
-            dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
-            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+            dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
           }
         }
       }
@@ -154,7 +159,8 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int n = n0 + b * 8 + 2 * tig + h;
-          if (n < nrhs) Y[static_cast<long long>(n) * M + i] = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+          const double s1 = acc[a][b][0][h], s2 = acc[a][b][1][h], s3 = acc[a][b][2][h];
+          if (n < nrhs) Y[static_cast<long long>(n) * M + i] = make_double2(s1 - s2, s3 - s1 - s2);
         }
     }
   }

@@ -20,6 +20,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fft_reg.cuh"
 #include "tbt_internal.cuh"
@@ -236,6 +238,14 @@ void fft2dPlan(int L0, int L1, int nx, int ny, int B, int sms, int* CL, int* BC)
   while (bc > 2 && (static_cast<long long>(cl) * ((B + bc - 1) / bc) < sms || xbufBytes(bc) > 160 * 1024)) bc /= 2;
   *CL = cl;
   *BC = bc;
+  // Tuning override "CL,BC" (CL must divide L0).
+  if (const char* e = getenv("TBT_FFT2D")) {
+    int c2 = 0, b2 = 0;
+    if (sscanf(e, "%d,%d", &c2, &b2) == 2 && c2 >= 1 && c2 <= 8 && L0 % c2 == 0 && (b2 == 2 || b2 == 4 || b2 == 8 || b2 == 16)) {
+      *CL = c2;
+      *BC = b2;
+    }
+  }
 }
 
 bool launchFft2d(const Fft2dArgs& a, int CL, int BC, bool inverse, cudaStream_t s) {
