@@ -54,6 +54,15 @@ def measured_hbm():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
 
 
+def ncu_traffic(key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/r1_traffic.json), or None."""
+    try:
+        return json.loads((REPO / "profiles" / "r1_traffic.json").read_text())[key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def workload_desc(cfg):
     L0 = 1 << (2 * cfg.nx - 1 - 1).bit_length()
     L1 = 1 << (2 * cfg.ny - 1 - 1).bit_length()
@@ -351,8 +360,10 @@ def main():
         kname = "binprod (K3, bin-pair product)"
     achieved = kbytes / (kms * 1e-3) / 1e9
     b_alg_full = 16 * (info.bins * cfg.m * cfg.m + (2 * cfg.m * info.bins + 2 * cfg.n))
+    traffic = ncu_traffic(f"{cfg.name}_matvec_persistent") if info.apply_path == 2 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": kname, "bytes_per_launch": kbytes, "ms_per_launch": kms,
+            "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
+            "kernel": kname, "bytes_per_launch": kbytes, "ms_per_launch": kms,
             "peak_source": peak_src}
     if phase_us is not None:
         roof["phase_us"] = dict(zip(["rows+corr", "cols", "binprod", "inv_cols", "inv_rows"], phase_us))
