@@ -126,9 +126,26 @@ tbt_status tbt_apply(tbt_ctx* ctx, const double* x, double* y, int nrhs,
 /* y = A x (pure two-level block-Toeplitz part). */
 tbt_status tbt_apply_a(tbt_ctx* ctx, const double* x, double* y, int nrhs,
                        int where);
-/* Diagonal of Z (length n, host memory). */
+/* Diagonal of Z (length n + n_m, host memory). */
 tbt_status tbt_diagonal(tbt_ctx* ctx, double* d);
 long long tbt_size_a(const tbt_ctx* ctx);
+/* Margin unknowns n_m (0 until tbt_set_margin). */
+long long tbt_size_m(const tbt_ctx* ctx);
+
+/* Margin coupling B / B^T / C, replacing the margin half
+ * of ToeplitzMatvec (linsolve.cpp:179-216 build, :292-349 applyB / applyBT /
+ * applyC, :373-388 composition). e[9]: edges per part of components 1..9
+ * (e[4] must equal m). Layouts (include/tbt_gen.h, tbtgen_margin):
+ *   bside   ToeplitzRep::bSideGen[2][2ny-1], each e_c x (nx*m) column-major
+ *   brow    ToeplitzRep::bRowGen[2][ny][2nx-1], each e_c x m column-major
+ *   bcorner ToeplitzRep::bCorner[4] (corners 3, 9, 1, 7), e_c x (nx*ny*m)
+ *   cmat    the n_m x n_m margin block C (the reference's cBlocks assembled,
+ *           partBlock of every margin part pair), column-major
+ * Afterwards tbt_apply / tbt_diagonal / tbt_gmres act on n + n_m unknowns in
+ * the reference order [elements; margin parts 2, 8, 6, 4, 3, 9, 1, 7]
+ * (array_model.cpp:218-228); tbt_apply_a and use_a_only solves keep n. */
+tbt_status tbt_set_margin(tbt_ctx* ctx, const int* e, const double* bside, const double* brow,
+                          const double* bcorner, const double* cmat);
 
 /* Restarted GMRES with x0 = 0 for nrhs columns in lockstep. b, x are
  * n x nrhs column-major in `where` memory. Returns TBT_NUMERIC_ERROR when a

@@ -68,6 +68,31 @@ int tbtgen_rhs_delta_steered(int nx, int ny, int m, uint64_t seed,
 int tbtgen_rhs_ports(int nx, int ny, int m, uint64_t seed, double* out,
                      long long* port_rows);
 
+/* Margin coupling: synthetic stand-ins for the
+ * reference's margin generators (ToeplitzRep::bSideGen / bRowGen / bCorner,
+ * proj/include/arraymom/toeplitz.hpp:76-84) and the margin-against-margin
+ * blocks ToeplitzMatvec caches as cBlocks (proj/src/linsolve.cpp:210-215).
+ * e[9] = edges per part of components 1..9 (e[4] = m). Margin unknowns follow
+ * the part order of proj/src/array_model.cpp:218-228: ny parts of component
+ * 2, ny of 8, nx of 6, nx of 4, then the corners 3, 9, 1, 7.
+ *   bside  : regions (comp 2, comp 8) x (2ny-1) shifts s = idx + 1 - ny,
+ *            each e_c x (nx*m) column-major: B block (margin row a, element
+ *            row b) = G(a - b)                      (linsolve.cpp:179-185)
+ *   brow   : regions (comp 6, comp 4) x ny element rows j x (2nx-1) shifts
+ *            k = idx + 1 - nx, each e_c x m column-major: block (margin
+ *            column a, element (j, b)) = G_j(a - b)  (linsolve.cpp:187-194)
+ *   bcorner: corners (3, 9, 1, 7), each e_c x (nx*ny*m) column-major
+ *   c      : nM x nM column-major, symmetric (reciprocity)
+ * Regions are concatenated in the order above. Entries are
+ * scale*exp(-j*pi*R)/(1+R)*CN(0,1)/sqrt(m) with R the distance between the
+ * two parts on the (ny+2) x (nx+2) part grid; C adds (2+2j) on its diagonal
+ * (the self-term of a margin part). Returns 0 on success. */
+long long tbtgen_margin_size(int nx, int ny, const int* e);
+long long tbtgen_margin_lengths(int nx, int ny, const int* e, long long* n_bside, long long* n_brow,
+                                long long* n_bcorner);
+int tbtgen_margin(int nx, int ny, const int* e, uint64_t seed, double scale, double* bside, double* brow,
+                  double* bcorner, double* c);
+
 /* Component (1..9) of element (r, c), r = row (y), c = column (x). Corners
  * win over edges; for 1-wide arrays left/bottom win over right/top. */
 int tbtgen_component(int nx, int ny, int r, int c);

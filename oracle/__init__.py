@@ -43,6 +43,9 @@ def lib() -> C.CDLL:
         L.orc_bins.restype = C.c_longlong
         L.orc_bins.argtypes = [C.c_void_p]
         L.orc_set_correction.argtypes = [C.c_void_p, C.c_int, dp, dp, dp]
+        L.orc_set_margin.argtypes = [C.c_void_p, ip, dp, dp, dp, dp]
+        L.orc_size.restype = C.c_longlong
+        L.orc_size.argtypes = [C.c_void_p]
         L.orc_apply_a.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply_cols.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_int, C.c_int]
@@ -90,9 +93,9 @@ class Oracle:
     """Restated ToeplitzMatvec + gmres over canonical Sparse generators."""
 
     def __init__(self, nx, ny, m, generators_raw: np.ndarray, correction=None, precompute=True,
-                 nthreads: int = 0):
+                 nthreads: int = 0, margin=None):
         self.nx, self.ny, self.m = nx, ny, m
-        self.n = nx * ny * m
+        self.nA = self.n = nx * ny * m
         g = np.ascontiguousarray(generators_raw, dtype=np.complex128)
         self._h = lib().orc_create(nx, ny, m, _p(g))
         if not self._h:
@@ -103,6 +106,15 @@ class Oracle:
             u = np.ascontiguousarray(u) if rank > 0 else np.zeros(1, np.complex128)
             v = np.ascontiguousarray(v) if rank > 0 else np.zeros(1, np.complex128)
             lib().orc_set_correction(self._h, rank, _p(d), _p(u), _p(v))
+        if margin is not None:
+            e = np.ascontiguousarray(margin.e, dtype=np.int32)
+            arrs = [np.ascontiguousarray(a, dtype=np.complex128) for a in
+                    (margin.bside, margin.brow, margin.bcorner, margin.c)]
+            arrs = [a if a.size else np.zeros(1, np.complex128) for a in arrs]
+            if lib().orc_set_margin(self._h, e.ctypes.data_as(ip), *[_p(a) for a in arrs]):
+                raise ValueError("orc_set_margin failed")
+            self._margin_keep = arrs
+            self.n = int(lib().orc_size(self._h))
         if precompute:
             self.precompute(nthreads)
 
@@ -112,7 +124,8 @@ class Oracle:
         if rep.correction is not None:
             c = rep.correction
             corr = (c.rank, c.d, c.u, c.v)
-        return cls(rep.nx, rep.ny, rep.m, rep.generators, corr, precompute, nthreads)
+        return cls(rep.nx, rep.ny, rep.m, rep.generators, corr, precompute, nthreads,
+                   getattr(rep, "margin", None))
 
     def precompute(self, nthreads: int = 0):
         lib().orc_precompute(self._h, nthreads)
@@ -168,7 +181,8 @@ class Oracle:
         return y
 
     def dense(self):
-        z = np.empty((self.n, self.n), dtype=np.complex128, order="F")
+        """Dense A (+ correction), nA x nA (margin excluded)."""
+        z = np.empty((self.nA, self.nA), dtype=np.complex128, order="F")
         lib().orc_dense(self._h, _p(z))
         return z
 

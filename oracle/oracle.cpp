@@ -117,6 +117,88 @@ int componentOf(int nx, int ny, int r, int c) {  // include/tbt_gen.h
   return 5;
 }
 
+// Toe1D (linsolve.cpp:54-134): a one-level block-Toeplitz operator with
+// nr x nc blocks of size p x q, block (a, b) = gen(a - b), applied through a
+// circulant embedding of length nextPow2(nr + nc - 1): entry sequences
+// transformed once (build), x transformed per source column j, per-bin
+// products summed over j, inverse transform, crop to nr, 1/L. applyT uses
+// the frequency-reversed spectrum (the transposed circulant).
+struct Toe1D {
+  long p = 0, q = 0;
+  int nr = 0, nc = 0;
+  long L = 0;
+  cvec ghat;  // [(i*q + j)*L + f]
+
+  bool emptyOp() const { return p == 0 || q == 0 || nr == 0 || nc == 0; }
+
+  // gen(s) -> column-major p x q block for s in [1-nc, nr-1].
+  template <typename Gen>
+  void build(long pIn, long qIn, int nrIn, int ncIn, Gen&& gen) {
+    p = pIn;
+    q = qIn;
+    nr = nrIn;
+    nc = ncIn;
+    if (emptyOp()) return;
+    L = static_cast<long>(pow2AtLeast(static_cast<size_t>(nr + nc - 1)));
+    ghat.assign(static_cast<size_t>(p) * q * L, cplx{0.0, 0.0});
+    cvec seq(static_cast<size_t>(L));
+    for (long i = 0; i < p; ++i)
+      for (long j = 0; j < q; ++j) {
+        std::fill(seq.begin(), seq.end(), cplx{0.0, 0.0});
+        for (int s = 0; s < nr; ++s) seq[s] = gen(s)[j * p + i];
+        for (int s = 1; s < nc; ++s) seq[L - s] = gen(-s)[j * p + i];
+        radix2(seq.data(), static_cast<size_t>(L), false);
+        std::copy(seq.begin(), seq.end(), ghat.begin() + (i * q + j) * L);
+      }
+  }
+
+  // y += T x (x: nc*q, y: nr*p).
+  void apply(const cplx* x, cplx* y) const {
+    if (emptyOp()) return;
+    cvec xhat(static_cast<size_t>(q) * L, cplx{0.0, 0.0});
+    for (long j = 0; j < q; ++j) {
+      cplx* row = xhat.data() + j * L;
+      for (int b = 0; b < nc; ++b) row[b] = x[static_cast<long>(b) * q + j];
+      radix2(row, static_cast<size_t>(L), false);
+    }
+    cvec acc(static_cast<size_t>(L));
+    const double scale = 1.0 / static_cast<double>(L);
+    for (long i = 0; i < p; ++i) {
+      std::fill(acc.begin(), acc.end(), cplx{0.0, 0.0});
+      for (long j = 0; j < q; ++j) {
+        const cplx* g = ghat.data() + (i * q + j) * L;
+        const cplx* xr = xhat.data() + j * L;
+        for (long f = 0; f < L; ++f) acc[f] += g[f] * xr[f];
+      }
+      radix2(acc.data(), static_cast<size_t>(L), true);
+      for (int a = 0; a < nr; ++a) y[static_cast<long>(a) * p + i] += acc[a] * scale;
+    }
+  }
+
+  // y += T^T x (x: nr*p, y: nc*q).
+  void applyT(const cplx* x, cplx* y) const {
+    if (emptyOp()) return;
+    cvec xhat(static_cast<size_t>(p) * L, cplx{0.0, 0.0});
+    for (long i = 0; i < p; ++i) {
+      cplx* row = xhat.data() + i * L;
+      for (int a = 0; a < nr; ++a) row[a] = x[static_cast<long>(a) * p + i];
+      radix2(row, static_cast<size_t>(L), false);
+    }
+    cvec acc(static_cast<size_t>(L));
+    const double scale = 1.0 / static_cast<double>(L);
+    for (long j = 0; j < q; ++j) {
+      std::fill(acc.begin(), acc.end(), cplx{0.0, 0.0});
+      for (long i = 0; i < p; ++i) {
+        const cplx* g = ghat.data() + (i * q + j) * L;
+        const cplx* xr = xhat.data() + i * L;
+        for (long f = 0; f < L; ++f) acc[f] += g[(L - f) % L] * xr[f];
+      }
+      radix2(acc.data(), static_cast<size_t>(L), true);
+      for (int b = 0; b < nc; ++b) y[static_cast<long>(b) * q + j] += acc[b] * scale;
+    }
+  }
+};
+
 }  // namespace
 
 struct orc_op {
@@ -129,6 +211,67 @@ struct orc_op {
 
   int rank = 0;
   std::vector<cplx> pDense;  // 40 dense m x m perturbations, column-major
+
+  // Margin coupling (row f1; ToeplitzMatvec::Impl, linsolve.cpp:160-216):
+  // B1/B2 Toeplitz over y (components 2, 8), B3/B4 per element row
+  // Toeplitz over x (components 6, 4), dense corners B5..B8 (3, 9, 1, 7),
+  // C dense margin x margin. Margin order: array_model.cpp:218-228.
+  bool haveMargin = false;
+  int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long nM = 0;
+  cvec bSideRaw, bRowRaw, bCornerRaw, cDense;  // tbt_gen.h layouts
+  Toe1D bSide[2];
+  std::vector<Toe1D> bRow[2];
+  long sideStart[2] = {0, 0}, rowStart[2] = {0, 0}, cornerStart[4] = {0, 0, 0, 0};
+  long cornerOff[4] = {0, 0, 0, 0};  // offsets into bCornerRaw
+
+  long nTot() const { return nA + (haveMargin ? nM : 0); }
+
+  // applyB (linsolve.cpp:292-314): yM = B xA.
+  void applyB(const cplx* xA, cplx* yM) const {
+    for (long k = 0; k < nM; ++k) yM[k] = 0.0;
+    for (int r = 0; r < 2; ++r) bSide[r].apply(xA, yM + sideStart[r]);
+    for (int r = 0; r < 2; ++r)
+      for (int j = 0; j < ny && !bRow[r].empty(); ++j)
+        bRow[r][j].apply(xA + static_cast<long>(j) * nx * e5, yM + rowStart[r]);
+    static const int cc[4] = {3, 9, 1, 7};
+    for (int c = 0; c < 4; ++c) {
+      const long em = e[cc[c] - 1];
+      const cplx* bc = bCornerRaw.data() + cornerOff[c];  // em x nA column-major
+      for (long i = 0; i < em; ++i) {
+        cplx acc{0.0, 0.0};
+        for (long q = 0; q < nA; ++q) acc += bc[q * em + i] * xA[q];
+        yM[cornerStart[c] + i] += acc;
+      }
+    }
+  }
+
+  // applyBT (linsolve.cpp:316-334): yA += B^T xM.
+  void applyBT(const cplx* xM, cplx* yA) const {
+    for (int r = 0; r < 2; ++r) bSide[r].applyT(xM + sideStart[r], yA);
+    for (int r = 0; r < 2; ++r)
+      for (int j = 0; j < ny && !bRow[r].empty(); ++j)
+        bRow[r][j].applyT(xM + rowStart[r], yA + static_cast<long>(j) * nx * e5);
+    static const int cc[4] = {3, 9, 1, 7};
+    for (int c = 0; c < 4; ++c) {
+      const long em = e[cc[c] - 1];
+      const cplx* bc = bCornerRaw.data() + cornerOff[c];
+      for (long q = 0; q < nA; ++q) {
+        cplx acc{0.0, 0.0};
+        for (long i = 0; i < em; ++i) acc += bc[q * em + i] * xM[cornerStart[c] + i];
+        yA[q] += acc;
+      }
+    }
+  }
+
+  // applyC (linsolve.cpp:336-349) with the blocks assembled: yM += C xM.
+  void applyC(const cplx* xM, cplx* yM) const {
+    for (long k = 0; k < nM; ++k) {
+      cplx acc{0.0, 0.0};
+      for (long l = 0; l < nM; ++l) acc += cDense[l * nM + k] * xM[l];
+      yM[k] += acc;
+    }
+  }
 
   // Canonical block index of shift (i >= 0, j), reference storage order
   // aGen[0][j] / aGen[i][j-(1-nx)] (toeplitz.hpp:72-74, toeplitz.cpp:305-312).
@@ -241,9 +384,14 @@ struct orc_op {
     });
   }
 
+  // ToeplitzMatvec::apply (linsolve.cpp:373-388): [A xA + B^T xM; B xA + C xM].
   void apply(const cplx* x, cplx* y) const {
     applyA(x, y);
     addCorrection(x, y);
+    if (!haveMargin || nM == 0) return;
+    applyBT(x + nA, y);
+    applyB(x, y + nA);
+    applyC(x + nA, y + nA);
   }
 
   // Z(e, e') block entry (a, b) from the generators (partBlock Sparse
@@ -318,6 +466,67 @@ int orc_set_correction(orc_op* op, int rank, const double* d, const double* u,
   return 0;
 }
 
+int orc_set_margin(orc_op* op, const int* e, const double* bside, const double* brow, const double* bcorner,
+                   const double* c) {
+  if (!op || !e || e[4] != op->e5) return 1;
+  const int nx = op->nx, ny = op->ny, m = op->e5;
+  for (int q = 0; q < 9; ++q) op->e[q] = e[q];
+  op->nM = static_cast<long>(ny) * (e[1] + e[7]) + static_cast<long>(nx) * (e[5] + e[3]) + e[2] + e[8] + e[0] + e[6];
+  const long nA = op->nA, nM = op->nM;
+  const long nSide = (2L * ny - 1) * (e[1] + e[7]) * nx * m;
+  const long nRow = static_cast<long>(ny) * (2 * nx - 1) * (e[5] + e[3]) * m;
+  const long nCorner = (static_cast<long>(e[2]) + e[8] + e[0] + e[6]) * nA;
+  const cplx* bs = reinterpret_cast<const cplx*>(bside);
+  const cplx* br = reinterpret_cast<const cplx*>(brow);
+  const cplx* bc = reinterpret_cast<const cplx*>(bcorner);
+  const cplx* cc = reinterpret_cast<const cplx*>(c);
+  op->bSideRaw.assign(bs, bs + nSide);
+  op->bRowRaw.assign(br, br + nRow);
+  op->bCornerRaw.assign(bc, bc + nCorner);
+  op->cDense.assign(cc, cc + nM * nM);
+  // Group offsets (linsolve.cpp:196-205).
+  op->sideStart[0] = 0;
+  op->sideStart[1] = static_cast<long>(ny) * e[1];
+  op->rowStart[0] = static_cast<long>(ny) * (e[1] + e[7]);
+  op->rowStart[1] = op->rowStart[0] + static_cast<long>(nx) * e[5];
+  long cs = op->rowStart[1] + static_cast<long>(nx) * e[3];
+  static const int cornerComps[4] = {3, 9, 1, 7};
+  long co = 0;
+  for (int q = 0; q < 4; ++q) {
+    op->cornerStart[q] = cs;
+    op->cornerOff[q] = co;
+    cs += e[cornerComps[q] - 1];
+    co += static_cast<long>(e[cornerComps[q] - 1]) * nA;
+  }
+  // B1/B2 (linsolve.cpp:179-186) and B3/B4 (:187-195).
+  static const int sideComp[2] = {2, 8}, rowComp[2] = {6, 4};
+  long off = 0;
+  for (int r = 0; r < 2; ++r) {
+    const long em = e[sideComp[r] - 1];
+    const cplx* base = op->bSideRaw.data() + off;
+    const long bsz = em * nx * m;
+    op->bSide[r] = Toe1D{};
+    op->bSide[r].build(em, static_cast<long>(nx) * m, ny, ny,
+                       [&](int sft) { return base + static_cast<long>(sft - (1 - ny)) * bsz; });
+    off += (2L * ny - 1) * bsz;
+  }
+  off = 0;
+  for (int r = 0; r < 2; ++r) {
+    const long em = e[rowComp[r] - 1];
+    const long bsz = em * m;
+    op->bRow[r].assign(ny, Toe1D{});
+    for (int j = 0; j < ny; ++j) {
+      const cplx* base = op->bRowRaw.data() + off + static_cast<long>(j) * (2 * nx - 1) * bsz;
+      op->bRow[r][j].build(em, m, nx, nx, [&](int sft) { return base + static_cast<long>(sft - (1 - nx)) * bsz; });
+    }
+    off += static_cast<long>(ny) * (2 * nx - 1) * bsz;
+  }
+  op->haveMargin = true;
+  return 0;
+}
+
+long long orc_size(const orc_op* op) { return op ? op->nTot() : 0; }
+
 int orc_apply_a(const orc_op* op, const double* x, double* y) {
   if (!op || !op->haveSpectra) return 1;
   op->applyA(reinterpret_cast<const cplx*>(x), reinterpret_cast<cplx*>(y));
@@ -340,7 +549,7 @@ int orc_apply_cols(const orc_op* op, const double* x, double* y, int ncols,
       if (a_only)
         op->applyA(X + c * op->nA, Y + c * op->nA);
       else
-        op->apply(X + c * op->nA, Y + c * op->nA);
+        op->apply(X + c * op->nTot(), Y + c * op->nTot());
     }
   });
   return 0;
@@ -408,6 +617,9 @@ int orc_diagonal(const orc_op* op, double* dd) {
     if (e != e2) return;
     for (int a = 0; a < m; ++a) d[e * m + a] += 2.0 * P[static_cast<size_t>(a) * m + a];
   });
+  // Margin diagonal: the C blocks' diagonal (linsolve.cpp:400-406).
+  if (op->haveMargin)
+    for (long k = 0; k < op->nM; ++k) d[op->nA + k] = op->cDense[k * op->nM + k];
   return 0;
 }
 
@@ -556,12 +768,13 @@ extern "C" int orc_gmres(const orc_op* op, const double* b, double* x,
                          int* iterations, double* residual, int* converged,
                          double* hist, int hist_cap, int* hist_len) {
   if (!op || !op->haveSpectra || ncols < 0 || restart < 1) return 1;
-  const long n = op->nA;
+  const long n = use_a_only ? op->nA : op->nTot();
   cvec invDiag;
   if (precondition) {
     // iterativeSolve (linsolve.cpp:556-563): 1/d, or 1 where d == 0.
-    invDiag.resize(n);
+    invDiag.resize(op->nTot());
     orc_diagonal(op, reinterpret_cast<double*>(invDiag.data()));
+    invDiag.resize(n);
     if (use_a_only)
       for (long p = 0; p < n; ++p) invDiag[p] = op->aEntry(0, 0, static_cast<int>(p % op->e5), static_cast<int>(p % op->e5));
     for (auto& d : invDiag) d = (std::abs(d) > 0.0) ? 1.0 / d : cplx{1.0, 0.0};

@@ -50,6 +50,12 @@ int orc_set_correction(orc_op* op, int rank, const double* d, const double* u,
                        const double* v);
 
 /* applyA (linsolve.cpp:260-290): pure two-level Toeplitz product. */
+/* Margin coupling B/B^T/C (row f1), tbt_gen.h layouts; apply, diagonal and
+ * gmres then act on nA + nM unknowns (orc_size). */
+int orc_set_margin(orc_op* op, const int* e, const double* bside, const double* brow, const double* bcorner,
+                   const double* c);
+long long orc_size(const orc_op* op);
+
 int orc_apply_a(const orc_op* op, const double* x, double* y);
 /* Full synthetic operator y = A x + correction (the role of
  * ToeplitzMatvec::apply, linsolve.cpp:373-388). */

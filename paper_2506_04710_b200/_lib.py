@@ -55,6 +55,8 @@ SIGNATURES = {
     "tbt_apply_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "tbt_diagonal": (C.c_int, [C.c_void_p, dp]),
     "tbt_size_a": (C.c_longlong, [C.c_void_p]),
+    "tbt_size_m": (C.c_longlong, [C.c_void_p]),
+    "tbt_set_margin": (C.c_int, [C.c_void_p, ip, dp, dp, dp, dp]),
     "tbt_gmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),
                             C.POINTER(TbtGmresStats), C.c_int]),
     "tbt_get_info": (C.c_int, [C.c_void_p, C.POINTER(TbtInfo)]),
@@ -75,6 +77,9 @@ SIGNATURES = {
     "tbtgen_rhs_delta_steered": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]),
     "tbtgen_rhs_ports": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, dp, llp]),
     "tbtgen_component": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "tbtgen_margin_size": (C.c_longlong, [C.c_int, C.c_int, ip]),
+    "tbtgen_margin_lengths": (C.c_longlong, [C.c_int, C.c_int, ip, llp, llp, llp]),
+    "tbtgen_margin": (C.c_int, [C.c_int, C.c_int, ip, C.c_uint64, C.c_double, dp, dp, dp, dp]),
 }
 
 _lib = None

@@ -106,6 +106,7 @@ void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
         }
       }
   }
+  marginDiagonal(c, d);  // C's diagonal after the element part (linsolve.cpp:400-406)
   if (dOut) *dOut = d;
   auto invert = [](const std::vector<double2>& dv) {
     std::vector<double2> inv(dv.size());
@@ -131,11 +132,17 @@ void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
   std::vector<double2> dA(static_cast<size_t>(c.n));
   for (int e = 0; e < c.ne; ++e)
     for (int a = 0; a < m; ++a) dA[static_cast<size_t>(e) * m + a] = z0[static_cast<size_t>(a) * m + a];
-  const auto inv = invert(d), invA = invert(dA);
-  if (!c.dDiagInv) TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInv, c.n * sizeof(double2)));
+  auto inv = invert(d);
+  const auto invA = invert(dA);
+  // Internal length: the margin pseudo-elements' padding gets 1.
+  const size_t nInt = static_cast<size_t>(c.ne + c.neM) * m;
+  inv.resize(nInt, make_double2(1.0, 0.0));
+  if (c.dDiagInv) cudaFree(c.dDiagInv);
+  c.dDiagInv = nullptr;
+  TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInv, nInt * sizeof(double2)));
   if (!c.dDiagInvA) TBT_CUDA_CHECK(cudaMalloc(&c.dDiagInvA, c.n * sizeof(double2)));
-  TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInv, inv.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
-  TBT_CUDA_CHECK(cudaMemcpy(c.dDiagInvA, invA.data(), c.n * sizeof(double2), cudaMemcpyHostToDevice));
+  uploadSync(c.dDiagInv, inv.data(), nInt * sizeof(double2), c.stream);
+  uploadSync(c.dDiagInvA, invA.data(), c.n * sizeof(double2), c.stream);
 }
 
 // Page-locked host memory is device-addressable through UVA.
@@ -181,6 +188,32 @@ void runApply1(Ctx& c, const double2* x, double2* y, bool withCorr) {
 }
 
 }  // namespace
+
+std::vector<double2> twiddleTable(int n) { return twiddles(n); }
+
+// Host -> device uploads and fills ordered on the context's (non-blocking)
+// stream and completed before returning: a plain cudaMemcpy from pageable
+// memory may return before its DMA lands, and the legacy stream does not
+// order against non-blocking streams.
+void uploadSync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  TBT_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void memsetSync(void* dst, int value, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  TBT_CUDA_CHECK(cudaMemsetAsync(dst, value, bytes, s));
+  TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+bool poisonBuffers() {
+  static const bool on = [] {
+    const char* e = getenv("TBT_POISON");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 int smCount(int device) {
   static int cached[64] = {0};
@@ -246,24 +279,31 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       TBT_CUDA_CHECK(cudaMalloc(&c.dYhat, c.L * B * sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dXin, c.ne * B * sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dYout, c.ne * B * sizeof(double2)));
+      if (poisonBuffers()) {  // TBT_POISON=1: NaN-fill scratch so a read-before-write shows up
+        memsetSync(c.dT, 0xFF, static_cast<long long>(c.ny) * c.L0 * B * sizeof(double2), c.stream);
+        memsetSync(c.dXhat, 0xFF, c.L * B * sizeof(double2), c.stream);
+        memsetSync(c.dYhat, 0xFF, c.L * B * sizeof(double2), c.stream);
+        memsetSync(c.dXin, 0xFF, c.ne * B * sizeof(double2), c.stream);
+        memsetSync(c.dYout, 0xFF, c.ne * B * sizeof(double2), c.stream);
+      }
       const auto t0 = twiddles(c.L0), t1 = twiddles(c.L1);
       TBT_CUDA_CHECK(cudaMalloc(&c.dTw0, c.L0 * sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dTw1, c.L1 * sizeof(double2)));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dTw0, t0.data(), c.L0 * sizeof(double2), cudaMemcpyHostToDevice));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dTw1, t1.data(), c.L1 * sizeof(double2), cudaMemcpyHostToDevice));
+      uploadSync(c.dTw0, t0.data(), c.L0 * sizeof(double2), c.stream);
+      uploadSync(c.dTw1, t1.data(), c.L1 * sizeof(double2), c.stream);
       TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
       TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evFork, cudaEventDisableTiming));
       TBT_CUDA_CHECK(cudaEventCreateWithFlags(&c.evJoin, cudaEventDisableTiming));
       c.fused2d = fft2dSupported(c.L0, c.L1);
       TBT_CUDA_CHECK(cudaMalloc(&c.dGridBar, 2 * sizeof(unsigned)));
-      TBT_CUDA_CHECK(cudaMemset(c.dGridBar, 0, 2 * sizeof(unsigned)));
+      memsetSync(c.dGridBar, 0, 2 * sizeof(unsigned), c.stream);
       {
         const size_t nfl = (2 * static_cast<size_t>(smCount(c.device)) + 1) * 16;
         TBT_CUDA_CHECK(cudaMalloc(&c.dBarFlags, nfl * sizeof(unsigned long long)));
-        TBT_CUDA_CHECK(cudaMemset(c.dBarFlags, 0, nfl * sizeof(unsigned long long)));
+        memsetSync(c.dBarFlags, 0, nfl * sizeof(unsigned long long), c.stream);
       }
       TBT_CUDA_CHECK(cudaMalloc(&c.dPhaseNs, 32 * sizeof(unsigned long long)));
-      TBT_CUDA_CHECK(cudaMemset(c.dPhaseNs, 0, 32 * sizeof(unsigned long long)));
+      memsetSync(c.dPhaseNs, 0, 32 * sizeof(unsigned long long), c.stream);
       const char* aenv = getenv("TBT_APPLY");
       c.persistent = !(aenv && std::string(aenv) == "multi");
       const char* penv = getenv("TBT_PREFETCH");
@@ -306,6 +346,7 @@ void tbt_destroy(tbt_ctx* h) {
     freePtr(p);
   c.dropGraph();
   distFree(c);
+  marginFree(c);
   freeGmresWorkspace(c);
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);
@@ -340,6 +381,39 @@ tbt_status tbt_set_stream(tbt_ctx* h, void* stream) {
 void* tbt_get_stream(tbt_ctx* h) { return h ? static_cast<void*>(h->c.stream) : nullptr; }
 
 long long tbt_size_a(const tbt_ctx* h) { return h ? h->c.n : 0; }
+long long tbt_size_m(const tbt_ctx* h) { return h ? h->c.nM : 0; }
+
+tbt_status tbt_set_margin(tbt_ctx* h, const int* e, const double* bside, const double* brow, const double* bcorner,
+                          const double* cmat) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && e, "tbt_set_margin: null argument");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.dropGraph();
+    freeGmresWorkspace(c);
+    const long long nM = static_cast<long long>(c.ny) * (e[1] + e[7]) + static_cast<long long>(c.nx) * (e[5] + e[3]) +
+                         e[2] + e[8] + e[0] + e[6];
+    TBT_USER_CHECK(nM == 0 || cmat, "tbt_set_margin: C is required when there are margin unknowns");
+    TBT_USER_CHECK((e[1] + e[7] == 0 || bside) && (e[5] + e[3] == 0 || brow) &&
+                       (e[2] + e[8] + e[0] + e[6] == 0 || bcorner),
+                   "tbt_set_margin: missing generator array");
+    marginSet(c, e, reinterpret_cast<const double2*>(bside), reinterpret_cast<const double2*>(brow),
+              reinterpret_cast<const double2*>(bcorner), reinterpret_cast<const double2*>(cmat));
+    // Staging vectors hold the padded pseudo-elements too.
+    const size_t len = static_cast<size_t>(c.ne + c.neM) * c.maxNrhs * c.m;
+    freePtr(c.dXin);
+    freePtr(c.dYout);
+    c.dXin = c.dYout = nullptr;
+    TBT_CUDA_CHECK(cudaMalloc(&c.dXin, len * sizeof(double2)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dYout, len * sizeof(double2)));
+    if (poisonBuffers()) {
+      memsetSync(c.dXin, 0xFF, len * sizeof(double2), c.stream);
+      memsetSync(c.dYout, 0xFF, len * sizeof(double2), c.stream);
+    }
+    if (c.havePrecompute) refreshDiagonal(c, nullptr);
+  });
+}
 
 tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblocks) {
   return guarded([&] {
@@ -359,7 +433,7 @@ tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblock
     c.dGen = nullptr;
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     TBT_CUDA_CHECK(cudaMalloc(&c.dGen, cnt * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMemcpy(c.dGen, blocks, cnt * sizeof(double2), cudaMemcpyHostToDevice));
+    uploadSync(c.dGen, blocks, cnt * sizeof(double2), c.stream);
     c.haveGenerators = true;
     c.havePrecompute = false;
   });
@@ -401,15 +475,13 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     c.rank = rank;
     c.corrDHost.assign(reinterpret_cast<const double2*>(d), reinterpret_cast<const double2*>(d) + 40 * m);
     TBT_CUDA_CHECK(cudaMalloc(&c.dCorrD, 40 * m * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMemcpy(c.dCorrD, d, 40 * m * sizeof(double2), cudaMemcpyHostToDevice));
+    uploadSync(c.dCorrD, d, 40 * m * sizeof(double2), c.stream);
     const size_t uvBytes = static_cast<size_t>(40) * std::max(rank, 1) * m * sizeof(double2);
     TBT_CUDA_CHECK(cudaMalloc(&c.dCorrU, uvBytes));
     TBT_CUDA_CHECK(cudaMalloc(&c.dCorrV, uvBytes));
     if (rank > 0) {
-      TBT_CUDA_CHECK(cudaMemcpy(c.dCorrU, u, static_cast<size_t>(40) * rank * m * sizeof(double2),
-                                cudaMemcpyHostToDevice));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dCorrV, v, static_cast<size_t>(40) * rank * m * sizeof(double2),
-                                cudaMemcpyHostToDevice));
+      uploadSync(c.dCorrU, u, static_cast<size_t>(40) * rank * m * sizeof(double2), c.stream);
+      uploadSync(c.dCorrV, v, static_cast<size_t>(40) * rank * m * sizeof(double2), c.stream);
     }
     // Term list grouped by target element (CSR).
     static const int dr[5] = {0, 0, 0, 1, -1};
@@ -445,15 +517,15 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
       TBT_CUDA_CHECK(cudaMalloc(&c.dTermInfo, info.size() * sizeof(int)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dTargetList, targets.size() * sizeof(int)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dTargetPtr, ptr.size() * sizeof(int)));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dTermInfo, info.data(), info.size() * sizeof(int), cudaMemcpyHostToDevice));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dTargetList, targets.data(), targets.size() * sizeof(int), cudaMemcpyHostToDevice));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dTargetPtr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      uploadSync(c.dTermInfo, info.data(), info.size() * sizeof(int), c.stream);
+      uploadSync(c.dTargetList, targets.data(), targets.size() * sizeof(int), c.stream);
+      uploadSync(c.dTargetPtr, ptr.data(), ptr.size() * sizeof(int), c.stream);
       TBT_CUDA_CHECK(cudaMalloc(&c.dElemPtr, eptr.size() * sizeof(int)));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dElemPtr, eptr.data(), eptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      uploadSync(c.dElemPtr, eptr.data(), eptr.size() * sizeof(int), c.stream);
       TBT_CUDA_CHECK(cudaMalloc(&c.dProj, static_cast<size_t>(c.nTerms) * c.maxNrhs * std::max(rank, 1) *
                                               sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dYcorr, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
-      TBT_CUDA_CHECK(cudaMemset(c.dYcorr, 0, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
+      memsetSync(c.dYcorr, 0, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2), c.stream);
       // (target, source) pairs: terms of one target grouped by source.
       std::vector<int> pinfo, pptr{0};
       for (int e : targets) {
@@ -475,8 +547,8 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
       c.nCorrPairs = static_cast<int>(pinfo.size() / 4);
       TBT_CUDA_CHECK(cudaMalloc(&c.dPairInfo, pinfo.size() * sizeof(int)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dPairTargetPtr, pptr.size() * sizeof(int)));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dPairInfo, pinfo.data(), pinfo.size() * sizeof(int), cudaMemcpyHostToDevice));
-      TBT_CUDA_CHECK(cudaMemcpy(c.dPairTargetPtr, pptr.data(), pptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+      uploadSync(c.dPairInfo, pinfo.data(), pinfo.size() * sizeof(int), c.stream);
+      uploadSync(c.dPairTargetPtr, pptr.data(), pptr.size() * sizeof(int), c.stream);
       TBT_CUDA_CHECK(cudaMalloc(&c.dTermVec, static_cast<size_t>(c.nCorrPairs) * c.m * sizeof(double2)));
     }
     c.haveCorr = true;
@@ -514,6 +586,27 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
     const size_t bytes = total * sizeof(double2);
     const double2* xin = reinterpret_cast<const double2*>(x);
     double2* yout = reinterpret_cast<double2*>(y);
+    if (withCorr && c.margin) {
+      // Full operator with margin parts: vectors of nA + nM rows, internally
+      // padded pseudo-elements after the elements (margin.cu).
+      const long long nU = c.n + c.nM, nInt = static_cast<long long>(c.ne + c.neM) * c.m;
+      const size_t ubytes = static_cast<size_t>(nU) * nrhs * sizeof(double2);
+      if (where == TBT_HOST) {
+        TBT_CUDA_CHECK(cudaMemcpyAsync(c.dYout, xin, ubytes, cudaMemcpyHostToDevice, c.stream));
+        launchLayoutU(c.dYout, c.dXin, nU, nInt, nrhs, true, c.stream, c.m);
+      } else {
+        launchLayoutU(xin, c.dXin, nU, nInt, nrhs, true, c.stream, c.m);
+      }
+      applyOperator(c, c.dXin, c.dYout, nrhs, true);
+      if (where == TBT_HOST) {
+        launchLayoutU(c.dYout, c.dXin, nU, nInt, nrhs, false, c.stream, c.m);
+        TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dXin, ubytes, cudaMemcpyDeviceToHost, c.stream));
+        TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      } else {
+        launchLayoutU(c.dYout, yout, nU, nInt, nrhs, false, c.stream, c.m);
+      }
+      return;
+    }
     if (where == TBT_HOST && nrhs == 1 && !c.dist && c.persistent && persistentSupported(c) && !c.timeBinprod &&
         isPinned(xin) && isPinned(yout)) {
       // Zero-copy: the persistent kernel reads x and writes y in pinned host
@@ -583,17 +676,20 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
     TBT_USER_CHECK(opts->restart >= 1 && opts->max_iter >= 0 && opts->tol > 0.0, "tbt_gmres: bad options");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     // Multi-GPU: b and x are this rank's element-row slab (tbt_dist_rows).
-    const long long nloc = c.dist ? static_cast<long long>(c.myRows) * c.nx * c.m : c.n;
+    // Margin parts (full operator): nA + nM user rows, padded internally.
+    const bool withMargin = c.margin && !opts->use_a_only;
+    const long long nUser = c.dist ? static_cast<long long>(c.myRows) * c.nx * c.m : c.n + (withMargin ? c.nM : 0);
+    const long long nloc = withMargin ? static_cast<long long>(c.ne + c.neM) * c.m : nUser;
     const long long total = nloc * nrhs;
-    const size_t bytes = total * sizeof(double2);
+    const size_t bytes = static_cast<size_t>(nUser) * nrhs * sizeof(double2);
     GmresWs* W = gmresWorkspace(c);
     if (W->bufLen < total) {
       if (W->bufB) cudaFree(W->bufB);
       if (W->bufX) cudaFree(W->bufX);
       W->bufB = W->bufX = nullptr;
       W->bufLen = 0;
-      TBT_CUDA_CHECK(cudaMalloc(&W->bufB, bytes));
-      TBT_CUDA_CHECK(cudaMalloc(&W->bufX, bytes));
+      TBT_CUDA_CHECK(cudaMalloc(&W->bufB, total * sizeof(double2)));
+      TBT_CUDA_CHECK(cudaMalloc(&W->bufX, total * sizeof(double2)));
       W->bufLen = total;
     }
     double2* db = W->bufB;
@@ -604,17 +700,17 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
     const double2* bsrc = reinterpret_cast<const double2*>(b);
     if (where == TBT_HOST) {
       TBT_CUDA_CHECK(cudaMemcpyAsync(dx, bsrc, bytes, cudaMemcpyHostToDevice, c.stream));
-      launchLayout(dx, db, nloc, nrhs, true, c.stream, c.m);
+      launchLayoutU(dx, db, nUser, nloc, nrhs, true, c.stream, c.m);
     } else {
-      launchLayout(bsrc, db, nloc, nrhs, true, c.stream, c.m);
+      launchLayoutU(bsrc, db, nUser, nloc, nrhs, true, c.stream, c.m);
     }
     gmresSolve(c, db, dx, nrhs, *opts, opts->use_a_only != 0, out, hist, matvecs);
     double2* xdst = reinterpret_cast<double2*>(x);
     if (where == TBT_HOST) {
-      launchLayout(dx, db, nloc, nrhs, false, c.stream, c.m);
+      launchLayoutU(dx, db, nUser, nloc, nrhs, false, c.stream, c.m);
       TBT_CUDA_CHECK(cudaMemcpyAsync(xdst, db, bytes, cudaMemcpyDeviceToHost, c.stream));
     } else {
-      launchLayout(dx, xdst, nloc, nrhs, false, c.stream, c.m);
+      launchLayoutU(dx, xdst, nUser, nloc, nrhs, false, c.stream, c.m);
     }
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     if (stats) {
@@ -737,6 +833,7 @@ tbt_status tbt_dist_init(tbt_ctx* h, int nranks, int rank, const char* id) {
     TBT_USER_CHECK(h && id, "tbt_dist_init: null argument");
     Ctx& c = h->c;
     TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
+    TBT_USER_CHECK(!c.margin, "tbt_dist_init: margin parts are not supported on a distributed context");
     TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "tbt_dist_init: bad rank");
     TBT_USER_CHECK(nranks <= c.L0, "tbt_dist_init: more ranks than level-0 bins");
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
@@ -757,7 +854,7 @@ tbt_status tbt_dist_init(tbt_ctx* h, int nranks, int rank, const char* id) {
     const long long B = static_cast<long long>(c.maxNrhs) * c.m;
     const long long myCols = static_cast<long long>(c.myColList.size());
     TBT_CUDA_CHECK(cudaMalloc(&c.dColsOfRank, flat.size() * sizeof(int)));
-    TBT_CUDA_CHECK(cudaMemcpy(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice));
+    uploadSync(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), c.stream);
     TBT_CUDA_CHECK(cudaMalloc(&c.dTrow, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
     TBT_CUDA_CHECK(cudaMalloc(&c.dSend, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
     TBT_CUDA_CHECK(cudaMalloc(&c.dTcol, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
@@ -800,7 +897,7 @@ tbt_status tbt_phase_times(tbt_ctx* h, int on, double* out_us) {
     // Reset the arrival extrema for the next armed apply.
     std::vector<unsigned long long> init(32, 0ULL);
     for (int k = 16; k < 24; ++k) init[k] = ~0ULL;
-    TBT_CUDA_CHECK(cudaMemcpy(c.dPhaseNs, init.data(), 32 * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    uploadSync(c.dPhaseNs, init.data(), 32 * sizeof(unsigned long long), c.stream);
     c.phaseTiming = on != 0;
   });
 }

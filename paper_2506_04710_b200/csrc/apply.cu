@@ -15,16 +15,22 @@ namespace tbt {
 namespace {
 
 // Column-major n x nrhs  <->  internal [e][rhs][a].
-__global__ void layoutKernel(const double2* __restrict__ in, double2* __restrict__ out, long long n, int m,
-                             int nrhs, int toInternal) {
-  const long long total = n * nrhs;
+__global__ void layoutKernel(const double2* __restrict__ in, double2* __restrict__ out, long long nUser,
+                             long long nInt, int m, int nrhs, int toInternal) {
+  const long long total = nInt * nrhs;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
-    // q indexes the internal layout.
+    // q indexes the internal layout [e][rhs][a]; rows past nUser are the
+    // zero padding of the margin pseudo-elements.
     const long long a = q % m;
     const long long rest = q / m;
     const long long rhs = rest % nrhs, e = rest / nrhs;
-    const long long ext = rhs * n + e * m + a;
+    const long long row = e * m + a;
+    if (row >= nUser) {
+      if (toInternal) out[q] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const long long ext = rhs * nUser + row;
     if (toInternal)
       out[q] = in[ext];
     else
@@ -34,12 +40,17 @@ __global__ void layoutKernel(const double2* __restrict__ in, double2* __restrict
 
 }  // namespace
 
+void launchLayoutU(const double2* in, double2* out, long long nUser, long long nInt, int nrhs, bool toInternal,
+                   cudaStream_t s, int m) {
+  const long long total = nInt * nrhs;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
+  layoutKernel<<<blocks, 256, 0, s>>>(in, out, nUser, nInt, m, nrhs, toInternal ? 1 : 0);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
 void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s,
                   int m) {
-  const long long total = n * nrhs;
-  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
-  layoutKernel<<<blocks, 256, 0, s>>>(in, out, n, m, nrhs, toInternal ? 1 : 0);
-  TBT_CUDA_CHECK(cudaGetLastError());
+  launchLayoutU(in, out, n, n, nrhs, toInternal, s, m);
 }
 
 namespace {
@@ -187,6 +198,15 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
 
   launchAntisym(c, x, y, nrhs);
   if (withCorr) launchCorrection(c, x, y, nrhs);
+}
+
+}  // namespace tbt
+
+namespace tbt {
+
+void applyOperator(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
+  applyInternal(c, x, y, nrhs, withCorr);
+  if (withCorr && c.margin) marginApply(c, x, y, nrhs);
 }
 
 }  // namespace tbt

@@ -12,6 +12,7 @@ constexpr uint64_t kStreamBlock = 1ULL << 40;
 constexpr uint64_t kStreamCorr = 2ULL << 40;
 constexpr uint64_t kStreamRhs = 3ULL << 40;
 constexpr uint64_t kStreamPort = 4ULL << 40;
+constexpr uint64_t kStreamMargin = 5ULL << 40;
 
 inline uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ULL;
@@ -213,6 +214,154 @@ int tbtgen_rhs_ports(int nx, int ny, int m, uint64_t seed, double* out,
     const long long row = e * m + portIndex(seed, e, m);
     out[2 * (e * n + row)] = 1.0;
     if (port_rows) port_rows[e] = row;
+  }
+  return 0;
+}
+
+long long tbtgen_margin_size(int nx, int ny, const int* e) {
+  if (nx < 1 || ny < 1 || e == nullptr) return 0;
+  return static_cast<long long>(ny) * (e[1] + e[7]) + static_cast<long long>(nx) * (e[5] + e[3]) + e[2] + e[8] +
+         e[0] + e[6];
+}
+
+long long tbtgen_margin_lengths(int nx, int ny, const int* e, long long* n_bside, long long* n_brow,
+                                long long* n_bcorner) {
+  if (nx < 1 || ny < 1 || e == nullptr) return -1;
+  const long long m = e[4], nA = static_cast<long long>(nx) * ny * m;
+  const long long sside = (2LL * ny - 1) * (e[1] + e[7]) * nx * m;
+  const long long srow = static_cast<long long>(ny) * (2LL * nx - 1) * (e[5] + e[3]) * m;
+  const long long scorner = (static_cast<long long>(e[2]) + e[8] + e[0] + e[6]) * nA;
+  if (n_bside) *n_bside = sside;
+  if (n_brow) *n_brow = srow;
+  if (n_bcorner) *n_bcorner = scorner;
+  return tbtgen_margin_size(nx, ny, e);
+}
+
+namespace {
+
+// Part-grid position (row, col) of margin unknown k (array_model.cpp:218-228:
+// component 2 at column -1, 8 at column nx, 6 at row ny, 4 at row -1;
+// corners 3 (ny,-1), 9 (ny,nx), 1 (-1,-1), 7 (-1,nx)).
+void marginPart(int nx, int ny, const int* e, long long k, int* row, int* col) {
+  const long long g2 = static_cast<long long>(ny) * e[1], g8 = static_cast<long long>(ny) * e[7];
+  const long long g6 = static_cast<long long>(nx) * e[5], g4 = static_cast<long long>(nx) * e[3];
+  if (k < g2) { *row = static_cast<int>(k / e[1]); *col = -1; return; }
+  k -= g2;
+  if (k < g8) { *row = static_cast<int>(k / e[7]); *col = nx; return; }
+  k -= g8;
+  if (k < g6) { *row = ny; *col = static_cast<int>(k / e[5]); return; }
+  k -= g6;
+  if (k < g4) { *row = -1; *col = static_cast<int>(k / e[3]); return; }
+  k -= g4;
+  const int cc[4] = {3, 9, 1, 7};
+  const int cr[4] = {ny, ny, -1, -1}, ccol[4] = {-1, nx, -1, nx};
+  for (int q = 0; q < 4; ++q) {
+    if (k < e[cc[q] - 1]) { *row = cr[q]; *col = ccol[q]; return; }
+    k -= e[cc[q] - 1];
+  }
+  *row = *col = 0;
+}
+
+// One entry: scale * exp(-j pi R)/(1+R) * CN(0,1)/sqrt(m).
+void marginEntry(uint64_t key, uint64_t k, double R, double scale, double ism, double* re, double* im) {
+  double u, v;
+  normalPair(key, k, &u, &v);
+  const double amp = scale * ism / (1.0 + R) / std::sqrt(2.0);
+  const double wr = std::cos(M_PI * R) * amp, wi = -std::sin(M_PI * R) * amp;
+  *re = wr * u - wi * v;
+  *im = wr * v + wi * u;
+}
+
+}  // namespace
+
+int tbtgen_margin(int nx, int ny, const int* e, uint64_t seed, double scale, double* bside, double* brow,
+                  double* bcorner, double* c) {
+  if (nx < 1 || ny < 1 || e == nullptr || e[4] < 1) return 1;
+  for (int q = 0; q < 9; ++q)
+    if (e[q] < 0) return 1;
+  const int m = e[4];
+  const long long nA = static_cast<long long>(nx) * ny * m;
+  const double ism = 1.0 / std::sqrt(static_cast<double>(m));
+  // B sides: region r (comp 2 at column -1, comp 8 at column nx), shift s:
+  // distance between margin part (a, col) and element (a - s, c).
+  const int sideComp[2] = {2, 8};
+  double* out = bside;
+  for (int r = 0; r < 2; ++r) {
+    const int em = e[sideComp[r] - 1];
+    const int colM = r == 0 ? -1 : nx;
+    for (int idx = 0; idx < 2 * ny - 1; ++idx) {
+      const int s = idx + 1 - ny;
+      const uint64_t key = streamKey(seed, kStreamMargin + static_cast<uint64_t>(r) * 4096 + idx);
+      for (long long q = 0; q < static_cast<long long>(nx) * m; ++q) {
+        const int cEl = static_cast<int>(q / m);
+        const double R = std::hypot(static_cast<double>(s), static_cast<double>(colM - cEl));
+        for (int i = 0; i < em; ++i) {
+          const long long o = q * em + i;  // column-major em x (nx*m)
+          if (out) marginEntry(key, static_cast<uint64_t>(o), R, scale, ism, out + 2 * o, out + 2 * o + 1);
+        }
+      }
+      if (out) out += 2LL * em * nx * m;
+    }
+  }
+  // B rows: region r (comp 6 at row ny, comp 4 at row -1), element row j,
+  // shift k: margin part (rowM, a) vs element (j, a - k).
+  const int rowComp[2] = {6, 4};
+  out = brow;
+  for (int r = 0; r < 2; ++r) {
+    const int em = e[rowComp[r] - 1];
+    const int rowM = r == 0 ? ny : -1;
+    for (int j = 0; j < ny; ++j)
+      for (int idx = 0; idx < 2 * nx - 1; ++idx) {
+        const int k = idx + 1 - nx;
+        const double R = std::hypot(static_cast<double>(rowM - j), static_cast<double>(k));
+        const uint64_t key = streamKey(seed, kStreamMargin + (2 + static_cast<uint64_t>(r)) * 4096 * 4096 +
+                                                 static_cast<uint64_t>(j) * 4096 + idx);
+        for (long long o = 0; o < static_cast<long long>(em) * m; ++o)
+          if (out) marginEntry(key, static_cast<uint64_t>(o), R, scale, ism, out + 2 * o, out + 2 * o + 1);
+        if (out) out += 2LL * em * m;
+      }
+  }
+  // Corners 3, 9, 1, 7 against every element.
+  const int cc[4] = {3, 9, 1, 7};
+  const int cr[4] = {ny, ny, -1, -1}, ccol[4] = {-1, nx, -1, nx};
+  out = bcorner;
+  for (int q = 0; q < 4; ++q) {
+    const int em = e[cc[q] - 1];
+    const uint64_t key = streamKey(seed, kStreamMargin + 7ULL * 4096 * 4096 + q);
+    for (long long col = 0; col < nA; ++col) {
+      const long long el = col / m;
+      const int er = static_cast<int>(el / nx), ec = static_cast<int>(el % nx);
+      const double R = std::hypot(static_cast<double>(cr[q] - er), static_cast<double>(ccol[q] - ec));
+      for (int i = 0; i < em; ++i) {
+        const long long o = col * em + i;
+        if (out) marginEntry(key, static_cast<uint64_t>(o), R, scale, ism, out + 2 * o, out + 2 * o + 1);
+      }
+    }
+    if (out) out += 2LL * em * nA;
+  }
+  // C: symmetric, drawn on the upper triangle, (2+2j) on the diagonal.
+  if (c) {
+    const long long nM = tbtgen_margin_size(nx, ny, e);
+    const uint64_t key = streamKey(seed, kStreamMargin + 8ULL * 4096 * 4096);
+    for (long long l = 0; l < nM; ++l) {
+      int rl, cl;
+      marginPart(nx, ny, e, l, &rl, &cl);
+      for (long long k = 0; k <= l; ++k) {
+        int rk, ck;
+        marginPart(nx, ny, e, k, &rk, &ck);
+        const double R = std::hypot(static_cast<double>(rl - rk), static_cast<double>(cl - ck));
+        double re, im;
+        marginEntry(key, static_cast<uint64_t>(l * nM + k), R, scale, ism, &re, &im);
+        if (k == l) {
+          re += 2.0;
+          im += 2.0;
+        }
+        c[2 * (l * nM + k)] = re;  // column l, row k
+        c[2 * (l * nM + k) + 1] = im;
+        c[2 * (k * nM + l)] = re;
+        c[2 * (k * nM + l) + 1] = im;
+      }
+    }
   }
   return 0;
 }

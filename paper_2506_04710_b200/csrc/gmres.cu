@@ -932,7 +932,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   TBT_USER_CHECK(R <= RMAX, "tbt_gmres: restart above " + std::to_string(RMAX));
   // Multi-GPU: this rank's element-row slab (dist.cu); every reduction of
   // the solve is all-reduced, so all ranks take identical decisions.
-  const int neLoc = c.dist ? c.myRows * c.nx : c.ne;
+  // Margin parts (full operator): the neM pseudo-elements join the vector.
+  const bool withMargin = c.margin && !useAOnly;
+  const int neLoc = c.dist ? c.myRows * c.nx : c.ne + (withMargin ? c.neM : 0);
   const long long nloc = static_cast<long long>(neLoc) * c.m;
   const long long nall = nloc * ncols;
   cudaStream_t s = c.stream;
@@ -947,7 +949,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   // from C4 up the column-blocked kernels are faster (measured: C4 0.553 vs
   // 0.573 ms per iteration, C5 4.6 vs 5.2).
   const long long lsChunk = (nloc + grid - 1) / grid;
-  const bool colsLS = c.dist || (o.orthog == 1 && c.m <= 256 && (ncols > 1 || lsChunk > 2048 || c.forceCols));
+  const bool colsLS =
+      c.dist || withMargin || (o.orthog == 1 && c.m <= 256 && (ncols > 1 || lsChunk > 2048 || c.forceCols));
+  TBT_USER_CHECK(!withMargin || c.m <= 256, "tbt_gmres: margin solves support m <= 256");
   TBT_USER_CHECK(!c.dist || c.m <= 256, "tbt_gmres: distributed solve supports m <= 256");
   const bool fast = !colsLS && ncols == 1 && nloc <= static_cast<long long>(grid) * kThreads * FAST_K;
   const bool lowSync = !colsLS && o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
@@ -1073,14 +1077,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       if (fuse && launchPersistentApply(c, A.V + static_cast<long long>(j) * nall, A.w, !useAOnly, &A, lsS, lsDots,
                                         lsPart))
         return;
-      applyInternal(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
+      applyOperator(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
       arnoldi(j);
     };
     // Single column: the whole inner loop of a cycle is one CUDA graph
     // (restart x [apply, Arnoldi]); every node turns into a no-op once the
     // column's inner loop stopped (device flag), so the host synchronises
     // once per restart cycle.
-    const bool useGraph = ncols == 1 && !c.timeBinprod && !c.dist;
+    const bool useGraph = ncols == 1 && !c.timeBinprod && !c.dist && !withMargin;
     GmresArgs keyA = A;  // what the captured nodes bake in (b, x unused by them)
     keyA.b = nullptr;
     keyA.x = nullptr;
@@ -1113,7 +1117,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       bool open = !st[0].done;
       for (size_t k = 1; k < st.size(); ++k) open |= !st[k].done;
       while (open) {
-        applyInternal(c, x, W.ax, ncols, !useAOnly);
+        applyOperator(c, x, W.ax, ncols, !useAOnly);
         ++matvecs;
         if (colsLS)
           cols.cycleStart();

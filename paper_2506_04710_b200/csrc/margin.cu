@@ -1,0 +1,628 @@
+// Margin coupling: the B / B^T / C part of the reference
+// operator, ToeplitzMatvec::apply = [A xA + B^T xM ; B xA + C xM]
+// (proj/src/linsolve.cpp:373-388), for representations with margin parts.
+//
+//   B1/B2  components 2 and 8 (one part per element row): one-level block
+//          Toeplitz over the element rows, block (margin row a, element row
+//          b) = G(a - b) of size e_c x (nx*m)           (linsolve.cpp:179-186)
+//   B3/B4  components 6 and 4 (one part per element column): for every
+//          element row j a one-level block Toeplitz over x, block (margin
+//          column a, element (j, b)) = G_j(a - b), e_c x m; the ny rows sum
+//          into the same margin segment                   (:187-195, :305-307)
+//   B5-B8  corners 3, 9, 1, 7: dense e_c x nA                    (:308-312)
+//   C      margin x margin, dense (the reference caches it block-wise as
+//          cBlocks, :210-215, :336-349)
+//
+// As in the reference, the Toeplitz parts go through circulant embeddings of
+// length nextPow2(2n-1) (Toe1D, linsolve.cpp:54-134), here bin-major on the
+// device: the spectra Ghat[f][i][q] are built once (gather + batched FFT
+// pass), every apply transforms x along the element rows / columns once
+// (shared by both regions), forms the per-bin products for B and, reading
+// the same spectra at the reversed bin, for B^T (the transposed circulant,
+// :316-334), and transforms back with the 1/L crop. Corners and C are
+// warp-per-row dense products.
+//
+// Layouts. Internal vectors are [element][rhs][basis] over ne + neM
+// elements: the margin unknowns k < nM follow the element part as
+// pseudo-elements (element ne + k/m, basis k%m), padded with zeros, so the
+// GMRES kernels see one uniform vector. Margin work vectors use the staging
+// layout [k][rhs] (k in the reference margin order, array_model.cpp:218-228).
+#include <algorithm>
+#include <climits>
+
+#include "tbt_internal.cuh"
+
+namespace tbt {
+
+struct MarginOp {
+  int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long nM = 0;
+  int Ly = 1, Lx = 1;
+  int emSide[2] = {0, 0}, emRow[2] = {0, 0}, emCorner[4] = {0, 0, 0, 0};
+  long long sideStart[2] = {0, 0}, rowStart[2] = {0, 0}, cornerStart[4] = {0, 0, 0, 0};
+  double2* gSide[2] = {nullptr, nullptr};  // [Ly][em][nx*m]
+  double2* gRow[2] = {nullptr, nullptr};   // [ny][Lx][em][m]
+  double2* corner[4] = {nullptr, nullptr, nullptr, nullptr};  // [em][nA] row-major
+  double2* C = nullptr;                    // [nM][nM] row-major
+  double2* twY = nullptr;
+  double2* twX = nullptr;
+  std::vector<double2> diag;               // C's diagonal (host)
+  // Work buffers for max_nrhs columns.
+  double2 *xs = nullptr, *ys = nullptr;        // [nM][K]
+  double2 *hatY = nullptr, *hatZy = nullptr;   // [Ly][nx][K][m]
+  double2 *hatX = nullptr, *hatZx = nullptr;   // [Lx][ny][K][m]
+  double2* hatMs[2] = {nullptr, nullptr};       // [Ly][em][K]
+  double2* hatMr[2] = {nullptr, nullptr};       // [Lx][em][K]
+  double2 *zA = nullptr, *zA2 = nullptr;       // [ne][K][m]
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+
+  double2* alloc(size_t count) {
+    void* p = nullptr;
+    TBT_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double2)));
+    if (poisonBuffers()) memsetSync(p, 0xFF, std::max<size_t>(count, 1) * sizeof(double2), stream);
+    allocs.push_back(p);
+    return static_cast<double2*>(p);
+  }
+  ~MarginOp() {
+    for (void* p : allocs) cudaFree(p);
+  }
+  bool anySide() const { return emSide[0] + emSide[1] > 0; }
+  bool anyRow() const { return emRow[0] + emRow[1] > 0; }
+};
+
+namespace {
+
+int gridFor(long long n) { return static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 4096))); }
+
+// Circulant sequence of a one-level Toeplitz generator set, bin-major:
+// seq[line][s][t] (t = i*q + j over the p x q block, row-major) from raw
+// column-major blocks raw[line][idx][j*p + i], idx = shift + (n - 1); shift
+// s >= 0 at s < n, negative shift -s' at L - s' (Toe1D::build, :66-81).
+__global__ void toeSeq(const double2* __restrict__ raw, double2* __restrict__ seq, int lines, int L, int n, int p,
+                       long long q) {
+  const long long P = static_cast<long long>(p) * q;
+  const long long total = static_cast<long long>(lines) * L * P;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = o % P;
+    const long long ls = o / P;
+    const int s = static_cast<int>(ls % L), line = static_cast<int>(ls / L);
+    int shift;
+    if (s < n)
+      shift = s;
+    else if (s > L - n)
+      shift = s - L;
+    else
+      shift = INT_MIN;
+    double2 v = make_double2(0.0, 0.0);
+    if (shift != INT_MIN) {
+      const long long i = t / q, j = t % q;
+      const long long blk = static_cast<long long>(line) * (2 * n - 1) + shift + (n - 1);
+      v = raw[blk * P + j * p + i];
+    }
+    seq[o] = v;
+  }
+}
+
+// out[r][c] = in[c][r] for a rows x cols column-major input (row-major out).
+__global__ void transposeCM(const double2* __restrict__ in, double2* __restrict__ out, long long rows,
+                            long long cols) {
+  const long long total = rows * cols;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = o / cols, c = o % cols;
+    out[o] = in[c * rows + r];
+  }
+}
+
+// xs[k][rhs] = x[((ne + k/m)*K + rhs)*m + k%m]
+__global__ void marginGather(const double2* __restrict__ x, double2* __restrict__ xs, long long nM, int ne, int m,
+                             int K) {
+  const long long total = nM * K;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = o / K;
+    const int rhs = static_cast<int>(o % K);
+    xs[o] = x[((ne + k / m) * K + rhs) * m + k % m];
+  }
+}
+
+// y pseudo-elements (zero padding past nM) from ys[k][rhs].
+__global__ void marginScatter(const double2* __restrict__ ys, double2* __restrict__ y, long long nM, int ne, int neM,
+                              int m, int K) {
+  const long long total = static_cast<long long>(neM) * m * K;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    // o enumerates the internal pseudo-element region [e'][rhs][b].
+    const int b = static_cast<int>(o % m);
+    const long long rest = o / m;
+    const int rhs = static_cast<int>(rest % K);
+    const long long ep = rest / K;
+    const long long k = ep * m + b;
+    y[static_cast<long long>(ne) * K * m + o] = k < nM ? ys[k * K + rhs] : make_double2(0.0, 0.0);
+  }
+}
+
+// B1/B2 per-bin product: hatMs[r][f][i][rhs] = sum_{c,k} G_r[f][i][c*m+k] hatY[f][c][rhs][k].
+// One warp per (r, f, i, rhs), lanes over the nx*m sources.
+__global__ void sideProd(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+                         const double2* __restrict__ hatY, double2* __restrict__ out0, double2* __restrict__ out1,
+                         int Ly, int nx, int m, int K) {
+  const long long q = static_cast<long long>(nx) * m;
+  const long long items = static_cast<long long>(em0 + em1) * Ly * K;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
+       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int rhs = static_cast<int>(w % K);
+    long long rest = w / K;
+    const int f = static_cast<int>(rest % Ly);
+    int i = static_cast<int>(rest / Ly);
+    const int r = i < em0 ? 0 : 1;
+    if (r == 1) i -= em0;
+    const int em = r == 0 ? em0 : em1;
+    const double2* G = (r == 0 ? g0 : g1) + (static_cast<long long>(f) * em + i) * q;
+    const double2* X = hatY + static_cast<long long>(f) * nx * K * m;
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long t = lane; t < q; t += 32) {
+      const long long c = t / m, k = t % m;
+      cfma(acc, G[t], X[(c * K + rhs) * m + k]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
+  }
+}
+
+// B3/B4 per-bin product: hatMr[r][f][i][rhs] = sum_j sum_k G_r[j][f][i][k] hatX[f][j][rhs][k].
+__global__ void rowProd(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+                        const double2* __restrict__ hatX, double2* __restrict__ out0, double2* __restrict__ out1,
+                        int Lx, int ny, int m, int K) {
+  const long long q = static_cast<long long>(ny) * m;
+  const long long items = static_cast<long long>(em0 + em1) * Lx * K;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
+       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int rhs = static_cast<int>(w % K);
+    long long rest = w / K;
+    const int f = static_cast<int>(rest % Lx);
+    int i = static_cast<int>(rest / Lx);
+    const int r = i < em0 ? 0 : 1;
+    if (r == 1) i -= em0;
+    const int em = r == 0 ? em0 : em1;
+    const double2* G = r == 0 ? g0 : g1;
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long t = lane; t < q; t += 32) {
+      const long long j = t / m, k = t % m;
+      const double2 gv = G[((j * Lx + f) * em + i) * m + k];
+      const double2 xv = hatX[((static_cast<long long>(f) * ny + j) * K + rhs) * m + k];
+      cfma(acc, gv, xv);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
+  }
+}
+
+// B^T over the side regions: hatZy[f][c][rhs][k] = sum_r sum_i G_r[-f][i][c*m+k] hatMs[r][f][i][rhs]
+// (Toe1D::applyT's reversed bin, linsolve.cpp:327-329).
+__global__ void sideProdT(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+                          const double2* __restrict__ hm0, const double2* __restrict__ hm1,
+                          double2* __restrict__ hatZy, int Ly, int nx, int m, int K) {
+  const long long q = static_cast<long long>(nx) * m;
+  const long long total = static_cast<long long>(Ly) * nx * K * m;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(o % m);
+    long long rest = o / m;
+    const int rhs = static_cast<int>(rest % K);
+    rest /= K;
+    const long long c = rest % nx;
+    const int f = static_cast<int>(rest / nx);
+    const int fr = (Ly - f) % Ly;
+    const long long col = c * m + k;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < em0; ++i)
+      cfma(acc, g0[(static_cast<long long>(fr) * em0 + i) * q + col], hm0[(static_cast<long long>(f) * em0 + i) * K + rhs]);
+    for (int i = 0; i < em1; ++i)
+      cfma(acc, g1[(static_cast<long long>(fr) * em1 + i) * q + col], hm1[(static_cast<long long>(f) * em1 + i) * K + rhs]);
+    hatZy[o] = acc;
+  }
+}
+
+// B^T over the row regions: hatZx[f][j][rhs][k] = sum_r sum_i G_r[j][-f][i][k] hatMr[r][f][i][rhs].
+__global__ void rowProdT(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+                         const double2* __restrict__ hm0, const double2* __restrict__ hm1, double2* __restrict__ hatZx,
+                         int Lx, int ny, int m, int K) {
+  const long long total = static_cast<long long>(Lx) * ny * K * m;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(o % m);
+    long long rest = o / m;
+    const int rhs = static_cast<int>(rest % K);
+    rest /= K;
+    const long long j = rest % ny;
+    const int f = static_cast<int>(rest / ny);
+    const int fr = (Lx - f) % Lx;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < em0; ++i)
+      cfma(acc, g0[((j * Lx + fr) * em0 + i) * m + k], hm0[(static_cast<long long>(f) * em0 + i) * K + rhs]);
+    for (int i = 0; i < em1; ++i)
+      cfma(acc, g1[((j * Lx + fr) * em1 + i) * m + k], hm1[(static_cast<long long>(f) * em1 + i) * K + rhs]);
+    hatZx[o] = acc;
+  }
+}
+
+struct CornerArgs {
+  const double2* bc[4];  // [em][nA] row-major
+  int em[4];
+  long long start[4];    // margin offsets
+};
+
+// ys[start_c + i][rhs] = sum_q bc[i][q] xA[q] (B5..B8, linsolve.cpp:308-312).
+__global__ void cornerProd(CornerArgs ca, const double2* __restrict__ x, double2* __restrict__ ys, long long nA,
+                           int m, int K) {
+  const int tot = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
+  const long long items = static_cast<long long>(tot) * K;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
+       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int rhs = static_cast<int>(w % K);
+    int i = static_cast<int>(w / K), c = 0;
+    while (i >= ca.em[c]) i -= ca.em[c++];
+    const double2* row = ca.bc[c] + static_cast<long long>(i) * nA;
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long q = lane; q < nA; q += 32) cfma(acc, row[q], x[((q / m) * K + rhs) * m + q % m]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) ys[(ca.start[c] + i) * K + rhs] = acc;
+  }
+}
+
+// ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349).
+__global__ void cProd(const double2* __restrict__ C, const double2* __restrict__ xs, double2* __restrict__ ys,
+                      long long nM, int K) {
+  const long long items = nM * K;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
+       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const long long k = w / K;
+    const int rhs = static_cast<int>(w % K);
+    const double2* row = C + k * nM;
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long l = lane; l < nM; l += 32) cfma(acc, row[l], xs[l * K + rhs]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) ys[k * K + rhs] = cadd(ys[k * K + rhs], acc);
+  }
+}
+
+// yA += zA + zA2 + sum_c bc^T xM_c (B^T's corner part, linsolve.cpp:328-332).
+__global__ void addBT(double2* __restrict__ y, const double2* __restrict__ zA, const double2* __restrict__ zA2,
+                      CornerArgs ca, const double2* __restrict__ xs, long long nA, int m, int K) {
+  const long long total = nA * K;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    // o enumerates the internal element region [e][rhs][b].
+    const int b = static_cast<int>(o % m);
+    const long long rest = o / m;
+    const int rhs = static_cast<int>(rest % K);
+    const long long e = rest / K;
+    const long long q = e * m + b;
+    double2 acc = y[o];
+    if (zA) acc = cadd(acc, zA[o]);
+    if (zA2) acc = cadd(acc, zA2[o]);
+    for (int c = 0; c < 4; ++c)
+      for (int i = 0; i < ca.em[c]; ++i)
+        cfma(acc, ca.bc[c][static_cast<long long>(i) * nA + q], xs[(ca.start[c] + i) * K + rhs]);
+    y[o] = acc;
+  }
+}
+
+}  // namespace
+
+void marginFree(Ctx& c) {
+  delete c.margin;
+  c.margin = nullptr;
+  c.nM = 0;
+  c.neM = 0;
+}
+
+void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, const double2* bcorner,
+               const double2* Cm) {
+  TBT_USER_CHECK(e[4] == c.m, "tbt_set_margin: e[4] must equal the element basis size m");
+  for (int q = 0; q < 9; ++q) TBT_USER_CHECK(e[q] >= 0, "tbt_set_margin: negative edge count");
+  TBT_USER_CHECK(!c.dist, "tbt_set_margin: not supported on a distributed context");
+  marginFree(c);
+  auto* M = new MarginOp;
+  c.margin = M;
+  M->stream = c.stream;
+  const int nx = c.nx, ny = c.ny, m = c.m, K = c.maxNrhs;
+  const long long nA = c.n;
+  for (int q = 0; q < 9; ++q) M->e[q] = e[q];
+  M->nM = static_cast<long long>(ny) * (e[1] + e[7]) + static_cast<long long>(nx) * (e[5] + e[3]) + e[2] + e[8] +
+          e[0] + e[6];
+  c.nM = M->nM;
+  c.neM = static_cast<int>((M->nM + m - 1) / m);
+  auto p2 = [](int n) {
+    int L = 1;
+    while (L < n) L <<= 1;
+    return L;
+  };
+  M->Ly = p2(2 * ny - 1);  // nextPow2(nr + nc - 1), Toe1D::build (linsolve.cpp:70)
+  M->Lx = p2(2 * nx - 1);
+  M->emSide[0] = e[1];
+  M->emSide[1] = e[7];
+  M->emRow[0] = e[5];
+  M->emRow[1] = e[3];
+  const int cc[4] = {3, 9, 1, 7};
+  for (int q = 0; q < 4; ++q) M->emCorner[q] = e[cc[q] - 1];
+  M->sideStart[0] = 0;
+  M->sideStart[1] = static_cast<long long>(ny) * e[1];
+  M->rowStart[0] = static_cast<long long>(ny) * (e[1] + e[7]);
+  M->rowStart[1] = M->rowStart[0] + static_cast<long long>(nx) * e[5];
+  long long cs = M->rowStart[1] + static_cast<long long>(nx) * e[3];
+  for (int q = 0; q < 4; ++q) {
+    M->cornerStart[q] = cs;
+    cs += M->emCorner[q];
+  }
+  const auto twy = twiddleTable(M->Ly), twx = twiddleTable(M->Lx);
+  M->twY = M->alloc(M->Ly);
+  M->twX = M->alloc(M->Lx);
+  uploadSync(M->twY, twy.data(), twy.size() * sizeof(double2), c.stream);
+  uploadSync(M->twX, twx.data(), twx.size() * sizeof(double2), c.stream);
+  cudaStream_t s = c.stream;
+  // Spectra of B1/B2: seq[s][i][q] then one FFT pass along s.
+  const long long qs = static_cast<long long>(nx) * m;
+  long long off = 0;
+  for (int r = 0; r < 2; ++r) {
+    const int em = M->emSide[r];
+    const long long P = em * qs, rawCount = (2LL * ny - 1) * P;
+    if (em == 0) continue;
+    double2* raw = M->alloc(rawCount);
+    uploadSync(raw, bside + off, rawCount * sizeof(double2), c.stream);
+    double2* seq = M->alloc(static_cast<size_t>(M->Ly) * P);
+    toeSeq<<<gridFor(M->Ly * P), 256, 0, s>>>(raw, seq, 1, M->Ly, ny, em, qs);
+    M->gSide[r] = M->alloc(static_cast<size_t>(M->Ly) * P);
+    FftPass fp;
+    fp.in = seq;
+    fp.out = M->gSide[r];
+    fp.lines = 1;
+    fp.in_point_stride = fp.out_point_stride = P;
+    fp.n = fp.n_in = fp.n_out = M->Ly;
+    fp.batch = static_cast<int>(P);
+    fp.tw = M->twY;
+    launchFftPass(fp, s);
+    off += rawCount;
+  }
+  // Spectra of B3/B4: per element row j, seq[j][s][i][k].
+  off = 0;
+  for (int r = 0; r < 2; ++r) {
+    const int em = M->emRow[r];
+    const long long P = static_cast<long long>(em) * m, rawCount = static_cast<long long>(ny) * (2 * nx - 1) * P;
+    if (em == 0) continue;
+    double2* raw = M->alloc(rawCount);
+    uploadSync(raw, brow + off, rawCount * sizeof(double2), c.stream);
+    double2* seq = M->alloc(static_cast<size_t>(ny) * M->Lx * P);
+    toeSeq<<<gridFor(static_cast<long long>(ny) * M->Lx * P), 256, 0, s>>>(raw, seq, ny, M->Lx, nx, em, m);
+    M->gRow[r] = M->alloc(static_cast<size_t>(ny) * M->Lx * P);
+    FftPass fp;
+    fp.in = seq;
+    fp.out = M->gRow[r];
+    fp.lines = ny;
+    fp.in_line_stride = fp.out_line_stride = M->Lx * P;
+    fp.in_point_stride = fp.out_point_stride = P;
+    fp.n = fp.n_in = fp.n_out = M->Lx;
+    fp.batch = static_cast<int>(P);
+    fp.tw = M->twX;
+    launchFftPass(fp, s);
+    off += rawCount;
+  }
+  // Corners (column-major e_c x nA -> row-major) and C.
+  off = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int em = M->emCorner[q];
+    if (em == 0) continue;
+    double2* raw = M->alloc(static_cast<size_t>(em) * nA);
+    uploadSync(raw, bcorner + off, static_cast<size_t>(em) * nA * sizeof(double2), c.stream);
+    M->corner[q] = M->alloc(static_cast<size_t>(em) * nA);
+    transposeCM<<<gridFor(em * nA), 256, 0, s>>>(raw, M->corner[q], em, nA);
+    off += static_cast<long long>(em) * nA;
+  }
+  if (M->nM > 0) {
+    double2* raw = M->alloc(static_cast<size_t>(M->nM) * M->nM);
+    uploadSync(raw, Cm, static_cast<size_t>(M->nM) * M->nM * sizeof(double2), c.stream);
+    M->C = M->alloc(static_cast<size_t>(M->nM) * M->nM);
+    transposeCM<<<gridFor(M->nM * M->nM), 256, 0, s>>>(raw, M->C, M->nM, M->nM);
+    M->diag.resize(M->nM);
+    for (long long k = 0; k < M->nM; ++k) M->diag[k] = Cm[k * M->nM + k];
+  }
+  TBT_CUDA_CHECK(cudaGetLastError());
+  // Work buffers.
+  M->xs = M->alloc(static_cast<size_t>(M->nM) * K);
+  M->ys = M->alloc(static_cast<size_t>(M->nM) * K);
+  M->hatY = M->alloc(static_cast<size_t>(M->Ly) * nx * K * m);
+  M->hatZy = M->alloc(static_cast<size_t>(M->Ly) * nx * K * m);
+  M->hatX = M->alloc(static_cast<size_t>(M->Lx) * ny * K * m);
+  M->hatZx = M->alloc(static_cast<size_t>(M->Lx) * ny * K * m);
+  for (int r = 0; r < 2; ++r) {
+    M->hatMs[r] = M->alloc(static_cast<size_t>(M->Ly) * std::max(M->emSide[r], 1) * K);
+    M->hatMr[r] = M->alloc(static_cast<size_t>(M->Lx) * std::max(M->emRow[r], 1) * K);
+  }
+  M->zA = M->alloc(static_cast<size_t>(c.ne) * K * m);
+  M->zA2 = M->alloc(static_cast<size_t>(c.ne) * K * m);
+  TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+  // The raw uploads and sequences are no longer needed once the spectra exist.
+}
+
+void marginDiagonal(const Ctx& c, std::vector<double2>& d) {
+  if (!c.margin) return;
+  d.insert(d.end(), c.margin->diag.begin(), c.margin->diag.end());
+}
+
+void marginApply(Ctx& c, const double2* x, double2* y, int K) {
+  MarginOp* M = c.margin;
+  if (!M || M->nM == 0) return;
+  cudaStream_t s = c.stream;
+  const int nx = c.nx, ny = c.ny, m = c.m, ne = c.ne;
+  const long long nA = c.n, B = static_cast<long long>(K) * m;
+  marginGather<<<gridFor(M->nM * K), 256, 0, s>>>(x, M->xs, M->nM, ne, m, K);
+  CornerArgs ca{};
+  for (int q = 0; q < 4; ++q) {
+    ca.bc[q] = M->corner[q];
+    ca.em[q] = M->emCorner[q];
+    ca.start[q] = M->cornerStart[q];
+  }
+  const bool side = M->anySide(), row = M->anyRow();
+  if (side) {
+    // x along the element rows (level 1): hatY[f][c][rhs][k].
+    FftPass fy;
+    fy.in = x;
+    fy.out = M->hatY;
+    fy.lines = 1;
+    fy.in_point_stride = fy.out_point_stride = nx * B;
+    fy.n = fy.n_out = M->Ly;
+    fy.n_in = ny;
+    fy.batch = static_cast<int>(nx * B);
+    fy.tw = M->twY;
+    launchFftPass(fy, s);
+    // Margin side segments along their ny parts.
+    for (int r = 0; r < 2; ++r) {
+      if (M->emSide[r] == 0) continue;
+      FftPass fm;
+      fm.in = M->xs + M->sideStart[r] * K;
+      fm.out = M->hatMs[r];
+      fm.lines = 1;
+      fm.in_point_stride = fm.out_point_stride = static_cast<long long>(M->emSide[r]) * K;
+      fm.n = fm.n_out = M->Ly;
+      fm.n_in = ny;
+      fm.batch = M->emSide[r] * K;
+      fm.tw = M->twY;
+      launchFftPass(fm, s);
+    }
+  }
+  if (row) {
+    // x along the element columns (level 0) per row: hatX[f][j][rhs][k].
+    FftPass fx;
+    fx.in = x;
+    fx.out = M->hatX;
+    fx.lines = ny;
+    fx.in_line_stride = nx * B;
+    fx.in_point_stride = B;
+    fx.out_line_stride = B;
+    fx.out_point_stride = ny * B;
+    fx.n = fx.n_out = M->Lx;
+    fx.n_in = nx;
+    fx.batch = static_cast<int>(B);
+    fx.tw = M->twX;
+    launchFftPass(fx, s);
+    for (int r = 0; r < 2; ++r) {
+      if (M->emRow[r] == 0) continue;
+      FftPass fm;
+      fm.in = M->xs + M->rowStart[r] * K;
+      fm.out = M->hatMr[r];
+      fm.lines = 1;
+      fm.in_point_stride = fm.out_point_stride = static_cast<long long>(M->emRow[r]) * K;
+      fm.n = fm.n_out = M->Lx;
+      fm.n_in = nx;
+      fm.batch = M->emRow[r] * K;
+      fm.tw = M->twX;
+      launchFftPass(fm, s);
+    }
+  }
+  // B^T parts first (they read hatMs / hatMr before the B products reuse them).
+  if (side) {
+    sideProdT<<<gridFor(static_cast<long long>(M->Ly) * nx * B), 256, 0, s>>>(
+        M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1], M->hatMs[0], M->hatMs[1], M->hatZy, M->Ly, nx, m, K);
+    FftPass iz;
+    iz.in = M->hatZy;
+    iz.out = M->zA;
+    iz.lines = 1;
+    iz.in_point_stride = iz.out_point_stride = nx * B;
+    iz.n = iz.n_in = M->Ly;
+    iz.n_out = ny;
+    iz.batch = static_cast<int>(nx * B);
+    iz.inverse = 1;
+    iz.scale = 1.0 / M->Ly;
+    iz.tw = M->twY;
+    launchFftPass(iz, s);
+  }
+  if (row) {
+    rowProdT<<<gridFor(static_cast<long long>(M->Lx) * ny * B), 256, 0, s>>>(
+        M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatMr[0], M->hatMr[1], M->hatZx, M->Lx, ny, m, K);
+    FftPass iz;
+    iz.in = M->hatZx;
+    iz.out = M->zA2;
+    iz.lines = ny;
+    iz.in_line_stride = B;
+    iz.in_point_stride = ny * B;
+    iz.out_line_stride = nx * B;
+    iz.out_point_stride = B;
+    iz.n = iz.n_in = M->Lx;
+    iz.n_out = nx;
+    iz.batch = static_cast<int>(B);
+    iz.inverse = 1;
+    iz.scale = 1.0 / M->Lx;
+    iz.tw = M->twX;
+    launchFftPass(iz, s);
+  }
+  addBT<<<gridFor(nA * K), 256, 0, s>>>(y, side ? M->zA : nullptr, row ? M->zA2 : nullptr, ca, M->xs, nA, m, K);
+  // B xA into the margin staging vector.
+  if (side) {
+    sideProd<<<gridFor(static_cast<long long>(M->emSide[0] + M->emSide[1]) * M->Ly * K * 32), 256, 0, s>>>(
+        M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1], M->hatY, M->hatMs[0], M->hatMs[1], M->Ly, nx, m, K);
+    for (int r = 0; r < 2; ++r) {
+      if (M->emSide[r] == 0) continue;
+      FftPass im;
+      im.in = M->hatMs[r];
+      im.out = M->ys + M->sideStart[r] * K;
+      im.lines = 1;
+      im.in_point_stride = im.out_point_stride = static_cast<long long>(M->emSide[r]) * K;
+      im.n = im.n_in = M->Ly;
+      im.n_out = ny;
+      im.batch = M->emSide[r] * K;
+      im.inverse = 1;
+      im.scale = 1.0 / M->Ly;
+      im.tw = M->twY;
+      launchFftPass(im, s);
+    }
+  }
+  if (row) {
+    rowProd<<<gridFor(static_cast<long long>(M->emRow[0] + M->emRow[1]) * M->Lx * K * 32), 256, 0, s>>>(
+        M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatX, M->hatMr[0], M->hatMr[1], M->Lx, ny, m, K);
+    for (int r = 0; r < 2; ++r) {
+      if (M->emRow[r] == 0) continue;
+      FftPass im;
+      im.in = M->hatMr[r];
+      im.out = M->ys + M->rowStart[r] * K;
+      im.lines = 1;
+      im.in_point_stride = im.out_point_stride = static_cast<long long>(M->emRow[r]) * K;
+      im.n = im.n_in = M->Lx;
+      im.n_out = nx;
+      im.batch = M->emRow[r] * K;
+      im.inverse = 1;
+      im.scale = 1.0 / M->Lx;
+      im.tw = M->twX;
+      launchFftPass(im, s);
+    }
+  }
+  const int cornerRows = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
+  if (cornerRows > 0) cornerProd<<<gridFor(static_cast<long long>(cornerRows) * K * 32), 256, 0, s>>>(ca, x, M->ys, nA, m, K);
+  cProd<<<gridFor(M->nM * K * 32), 256, 0, s>>>(M->C, M->xs, M->ys, M->nM, K);
+  marginScatter<<<gridFor(static_cast<long long>(c.neM) * m * K), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, K);
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tbt

@@ -178,7 +178,13 @@ struct Ctx {
   double2* dDiagInv = nullptr;   // 1/diag(Z), Jacobi of iterativeSolve
   double2* dDiagInvA = nullptr;  // 1/diag(A), Jacobi of the A-only solves
 
-  struct GmresWs* gmresWs = nullptr;  // cached GMRES workspace + inner-loop graph (gmres.cu)
+  struct GmresWs* gmresWs = nullptr;
+
+  // Margin coupling B / B^T / C (margin.cu): nM margin unknowns stored as
+  // neM = ceil(nM/m) zero-padded pseudo-elements after the ne elements.
+  struct MarginOp* margin = nullptr;
+  long long nM = 0;
+  int neM = 0;  // cached GMRES workspace + inner-loop graph (gmres.cu)
 
   // Timing hooks: event pairs around K3, one per timed apply.
   cudaEvent_t evBinA = nullptr, evBinB = nullptr;
@@ -210,6 +216,11 @@ void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // corre
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
 void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs, int nElems = -1);  // correction.cu
 void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s, int m);  // apply.cu
+// External n_user x nrhs column-major <-> internal [e][rhs][m] of n_int rows per column (zero padding).
+void launchLayoutU(const double2* in, double2* out, long long nUser, long long nInt, int nrhs, bool toInternal,
+                   cudaStream_t s, int m);
+// The full operator on internal vectors: applyInternal (+ margin B/B^T/C when present and withCorr).
+void applyOperator(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);
 
 // GMRES (gmres.cu): per-column state mirrored to the host.
 struct GmresState {
@@ -241,6 +252,17 @@ const NcclApi& nccl();
     if (r_ != ncclSuccess)                                                                    \
       throw ::tbt::Error{TBT_CUDA_ERROR, std::string(#expr) + ": " + nccl().errorString(r_)}; \
   } while (0)
+// margin.cu
+void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, const double2* bcorner,
+               const double2* C);
+void marginFree(Ctx& c);
+void marginApply(Ctx& c, const double2* x, double2* y, int nrhs);  // y's element part already holds A x
+void marginDiagonal(const Ctx& c, std::vector<double2>& d);          // appends C's diagonal
+std::vector<double2> twiddleTable(int n);                           // api.cu
+bool poisonBuffers();                                               // api.cu: TBT_POISON=1
+void uploadSync(void* dst, const void* src, size_t bytes, cudaStream_t s);  // api.cu
+void memsetSync(void* dst, int value, size_t bytes, cudaStream_t s);        // api.cu
+
 void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols);
 void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);
 void distFree(Ctx& c);

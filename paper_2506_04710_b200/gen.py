@@ -78,3 +78,24 @@ def rhs_ports(nx: int, ny: int, m: int, seed: int):
 
 def component(nx: int, ny: int, r: int, c: int) -> int:
     return int(lib().tbtgen_component(nx, ny, r, c))
+
+
+def margin(nx: int, ny: int, e, seed: int, scale: float = 0.1):
+    """Synthetic margin coupling (tbt_gen.h tbtgen_margin): a Margin with the
+    reference-shaped generators bSideGen / bRowGen / bCorner and dense C."""
+    from .toeplitz import Margin
+    ea = np.ascontiguousarray(e, dtype=np.int32)
+    assert ea.size == 9
+    ip = C.POINTER(C.c_int)
+    ns, nr, nc = C.c_longlong(), C.c_longlong(), C.c_longlong()
+    nM = int(lib().tbtgen_margin_lengths(nx, ny, ea.ctypes.data_as(ip), C.byref(ns), C.byref(nr), C.byref(nc)))
+    if nM < 0:
+        raise ValueError("bad margin sizes")
+    bside = np.empty(max(ns.value, 1), np.complex128)
+    brow = np.empty(max(nr.value, 1), np.complex128)
+    bcorner = np.empty(max(nc.value, 1), np.complex128)
+    c = np.empty(max(nM * nM, 1), np.complex128)
+    if lib().tbtgen_margin(nx, ny, ea.ctypes.data_as(ip), seed, scale, _ptr(bside), _ptr(brow), _ptr(bcorner),
+                           _ptr(c)):
+        raise ValueError("tbtgen_margin failed")
+    return Margin([int(v) for v in ea], bside[:ns.value], brow[:nr.value], bcorner[:nc.value], c[:nM * nM])

@@ -62,6 +62,7 @@ class ToeplitzRep:
     m: int
     generators: np.ndarray  # (nb, m, m) column-major blocks, raw layout of gen.blocks_raw
     correction: Correction | None = None
+    margin: "Margin | None" = None
 
     @classmethod
     def synthetic(cls, cfg) -> "ToeplitzRep":
@@ -75,6 +76,22 @@ class ToeplitzRep:
 
     def elementEdges(self) -> int:  # toeplitz.hpp:98
         return self.nx * self.ny * self.m
+
+
+@dataclass
+class Margin:
+    """Margin coupling B / B^T / C (ToeplitzRep::bSideGen, bRowGen, bCorner
+    and the margin x margin blocks, toeplitz.hpp:76-95; layouts in
+    include/tbt_gen.h). e: edges per part of components 1..9 (e[4] = m)."""
+    e: list
+    bside: np.ndarray
+    brow: np.ndarray
+    bcorner: np.ndarray
+    c: np.ndarray
+
+    def size(self, nx: int, ny: int) -> int:  # ToeplitzRep::marginEdges, toeplitz.hpp:99-102
+        e = self.e
+        return ny * (e[1] + e[7]) + nx * (e[5] + e[3]) + e[2] + e[8] + e[0] + e[6]
 
 
 @dataclass
@@ -132,6 +149,13 @@ class ToeplitzMatvec:
             _check(lib().tbt_set_correction(self._h, c.rank, d.ctypes.data_as(dp),
                                             u.ctypes.data_as(dp) if u is not None else None,
                                             v.ctypes.data_as(dp) if v is not None else None))
+        if rep.margin is not None:
+            mg = rep.margin
+            e = np.ascontiguousarray(mg.e, dtype=np.int32)
+            arrs = [np.ascontiguousarray(a, dtype=np.complex128) for a in (mg.bside, mg.brow, mg.bcorner, mg.c)]
+            arrs = [a if a.size else np.zeros(1, np.complex128) for a in arrs]
+            _check(lib().tbt_set_margin(self._h, e.ctypes.data_as(C.POINTER(C.c_int)),
+                                        *[a.ctypes.data_as(dp) for a in arrs]))
         if dist is not None:
             nranks, rank, uid = dist
             _check(lib().tbt_dist_init(self._h, int(nranks), int(rank), bytes(uid)))
@@ -162,24 +186,30 @@ class ToeplitzMatvec:
         return a.value, b.value
 
     def sizeM(self) -> int:
-        return 0  # margin unknowns are folded into the synthetic correction
+        """Margin unknowns (ToeplitzMatvec::sizeM, linsolve.hpp:72); 0 without margin data."""
+        return int(lib().tbt_size_m(self._h))
 
-    def _apply(self, fn, x):
+    def size(self) -> int:
+        """Unknowns of apply / diagonal / gmres: sizeA() + sizeM()."""
+        return self.sizeA() + self.sizeM()
+
+    def _apply(self, fn, x, full: bool):
         xc, k, vec = _as_cols(x)
-        if xc.shape[0] != self.sizeA():
-            raise UserError(f"matvec: vector length {xc.shape[0]} does not match system size {self.sizeA()}")
+        n = self.size() if full else self.sizeA()
+        if xc.shape[0] != n:
+            raise UserError(f"matvec: vector length {xc.shape[0]} does not match system size {n}")
         y = np.empty_like(xc, order="F")
         _check(fn(self._h, xc.ctypes.data, y.ctypes.data, k, TBT_HOST))
         return y[:, 0] if vec else y
 
     def apply(self, x):
-        return self._apply(lib().tbt_apply, x)
+        return self._apply(lib().tbt_apply, x, True)
 
     def applyA(self, x):
-        return self._apply(lib().tbt_apply_a, x)
+        return self._apply(lib().tbt_apply_a, x, False)
 
     def diagonal(self) -> np.ndarray:
-        d = np.empty(self.sizeA(), dtype=np.complex128)
+        d = np.empty(self.size(), dtype=np.complex128)
         _check(lib().tbt_diagonal(self._h, d.ctypes.data_as(dp)))
         return d
 
