@@ -54,6 +54,7 @@ struct MarginOp {
   double2* hatMs[2] = {nullptr, nullptr};       // [Ly][em][K]
   double2* hatMr[2] = {nullptr, nullptr};       // [Lx][em][K]
   double2 *zA = nullptr, *zA2 = nullptr;       // [ne][K][m]
+  double2* cornerPart = nullptr;               // [corner rows][K][element blocks]
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
 
@@ -151,6 +152,7 @@ __global__ void sideProd(const double2* __restrict__ g0, const double2* __restri
                          int Ly, int nx, int m, int K) {
   const long long q = static_cast<long long>(nx) * m;
   const long long items = static_cast<long long>(em0 + em1) * Ly * K;
+  (void)q;
   const int lane = threadIdx.x & 31;
   for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
        w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
@@ -163,11 +165,15 @@ __global__ void sideProd(const double2* __restrict__ g0, const double2* __restri
     const int em = r == 0 ? em0 : em1;
     const double2* G = (r == 0 ? g0 : g1) + (static_cast<long long>(f) * em + i) * q;
     const double2* X = hatY + static_cast<long long>(f) * nx * K * m;
-    double2 acc = make_double2(0.0, 0.0);
-    for (long long t = lane; t < q; t += 32) {
-      const long long c = t / m, k = t % m;
-      cfma(acc, G[t], X[(c * K + rhs) * m + k]);
+    // Four independent accumulators over the source elements (loads in flight).
+    double2 a4[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                     make_double2(0.0, 0.0)};
+    for (int c = 0; c < nx; ++c) {
+      const double2* Gc = G + static_cast<long long>(c) * m;
+      const double2* Xc = X + (static_cast<long long>(c) * K + rhs) * m;
+      for (int k = lane; k < m; k += 32) cfma(a4[c & 3], Gc[k], Xc[k]);
     }
+    double2 acc = cadd(cadd(a4[0], a4[1]), cadd(a4[2], a4[3]));
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
@@ -181,7 +187,6 @@ __global__ void sideProd(const double2* __restrict__ g0, const double2* __restri
 __global__ void rowProd(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
                         const double2* __restrict__ hatX, double2* __restrict__ out0, double2* __restrict__ out1,
                         int Lx, int ny, int m, int K) {
-  const long long q = static_cast<long long>(ny) * m;
   const long long items = static_cast<long long>(em0 + em1) * Lx * K;
   const int lane = threadIdx.x & 31;
   for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
@@ -194,13 +199,14 @@ __global__ void rowProd(const double2* __restrict__ g0, const double2* __restric
     if (r == 1) i -= em0;
     const int em = r == 0 ? em0 : em1;
     const double2* G = r == 0 ? g0 : g1;
-    double2 acc = make_double2(0.0, 0.0);
-    for (long long t = lane; t < q; t += 32) {
-      const long long j = t / m, k = t % m;
-      const double2 gv = G[((j * Lx + f) * em + i) * m + k];
-      const double2 xv = hatX[((static_cast<long long>(f) * ny + j) * K + rhs) * m + k];
-      cfma(acc, gv, xv);
+    double2 a4[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                     make_double2(0.0, 0.0)};
+    for (int j = 0; j < ny; ++j) {
+      const double2* Gj = G + ((static_cast<long long>(j) * Lx + f) * em + i) * m;
+      const double2* Xj = hatX + ((static_cast<long long>(f) * ny + j) * K + rhs) * m;
+      for (int k = lane; k < m; k += 32) cfma(a4[j & 3], Gj[k], Xj[k]);
     }
+    double2 acc = cadd(cadd(a4[0], a4[1]), cadd(a4[2], a4[3]));
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
@@ -265,27 +271,61 @@ struct CornerArgs {
   long long start[4];    // margin offsets
 };
 
-// ys[start_c + i][rhs] = sum_q bc[i][q] xA[q] (B5..B8, linsolve.cpp:308-312).
-__global__ void cornerProd(CornerArgs ca, const double2* __restrict__ x, double2* __restrict__ ys, long long nA,
-                           int m, int K) {
-  const int tot = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
-  const long long items = static_cast<long long>(tot) * K;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
-       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const int rhs = static_cast<int>(w % K);
-    int i = static_cast<int>(w / K), c = 0;
-    while (i >= ca.em[c]) i -= ca.em[c++];
-    const double2* row = ca.bc[c] + static_cast<long long>(i) * nA;
+// B5..B8 (linsolve.cpp:308-312), ys[start_c + i][rhs] = sum_q bc[i][q] xA[q],
+// two fixed-order stages: CTA (element block, corner row) partial sums over
+// kCornerElems elements, then cornerReduce over the blocks.
+constexpr int kCornerElems = 16;
+
+__global__ void __launch_bounds__(256) cornerPart(CornerArgs ca, const double2* __restrict__ x,
+                                                  double2* __restrict__ part, int ne, int m, int K, int nblk) {
+  __shared__ double2 red[8];
+  int i = blockIdx.y, c = 0;
+  while (i >= ca.em[c]) i -= ca.em[c++];
+  const long long nA = static_cast<long long>(ne) * m;
+  const double2* row = ca.bc[c] + static_cast<long long>(i) * nA;
+  const int e0 = blockIdx.x * kCornerElems, e1 = min(ne, e0 + kCornerElems);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int rhs = 0; rhs < K; ++rhs) {
     double2 acc = make_double2(0.0, 0.0);
-    for (long long q = lane; q < nA; q += 32) cfma(acc, row[q], x[((q / m) * K + rhs) * m + q % m]);
+    for (int e = e0 + warp; e < e1; e += 8) {
+      const double2* r = row + static_cast<long long>(e) * m;
+      const double2* xe = x + (static_cast<long long>(e) * K + rhs) * m;
+      for (int k = lane; k < m; k += 32) cfma(acc, r[k], xe[k]);
+    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
-    if (lane == 0) ys[(ca.start[c] + i) * K + rhs] = acc;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = red[0];
+      for (int w = 1; w < 8; ++w) t = cadd(t, red[w]);
+      part[(static_cast<long long>(blockIdx.y) * K + rhs) * nblk + blockIdx.x] = t;
+    }
+    __syncthreads();
   }
+}
+
+__global__ void cornerReduce(CornerArgs ca, const double2* __restrict__ part, double2* __restrict__ ys, int K,
+                             int nblk) {
+  const int rowsTot = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rowsTot * K) return;
+  const int rhs = w % K;
+  int i = w / K, c = 0;
+  const int gRow = i;
+  while (i >= ca.em[c]) i -= ca.em[c++];
+  const double2* p = part + (static_cast<long long>(gRow) * K + rhs) * nblk;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int b = lane; b < nblk; b += 32) acc = cadd(acc, p[b]);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+  }
+  if (lane == 0) ys[(ca.start[c] + i) * K + rhs] = acc;
 }
 
 // ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349).
@@ -462,6 +502,8 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
     M->hatMr[r] = M->alloc(static_cast<size_t>(M->Lx) * std::max(M->emRow[r], 1) * K);
   }
   M->zA = M->alloc(static_cast<size_t>(c.ne) * K * m);
+  M->cornerPart = M->alloc(static_cast<size_t>(M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3]) *
+                           K * ((c.ne + kCornerElems - 1) / kCornerElems));
   M->zA2 = M->alloc(static_cast<size_t>(c.ne) * K * m);
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
   // The raw uploads and sequences are no longer needed once the spectra exist.
@@ -619,7 +661,11 @@ void marginApply(Ctx& c, const double2* x, double2* y, int K) {
     }
   }
   const int cornerRows = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
-  if (cornerRows > 0) cornerProd<<<gridFor(static_cast<long long>(cornerRows) * K * 32), 256, 0, s>>>(ca, x, M->ys, nA, m, K);
+  if (cornerRows > 0) {
+    const int nblk = (ne + kCornerElems - 1) / kCornerElems;
+    cornerPart<<<dim3(nblk, cornerRows), 256, 0, s>>>(ca, x, M->cornerPart, ne, m, K, nblk);
+    cornerReduce<<<(cornerRows * K * 32 + 255) / 256, 256, 0, s>>>(ca, M->cornerPart, M->ys, K, nblk);
+  }
   cProd<<<gridFor(M->nM * K * 32), 256, 0, s>>>(M->C, M->xs, M->ys, M->nM, K);
   marginScatter<<<gridFor(static_cast<long long>(c.neM) * m * K), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, K);
   TBT_CUDA_CHECK(cudaGetLastError());
