@@ -73,23 +73,32 @@ class ToeplitzMatvec {
     check(tbt_set_correction(ctx_, rank, reinterpret_cast<const double*>(d), reinterpret_cast<const double*>(u),
                              reinterpret_cast<const double*>(v)));
   }
+  // Margin coupling B / B^T / C (ToeplitzRep::bSideGen, bRowGen, bCorner
+  // and the margin blocks; layouts in tbt_gen.h). apply / diagonal /
+  // iterativeSolve then act on sizeA() + sizeM() unknowns.
+  void setMargin(const int e[9], const Complex* bSide, const Complex* bRow, const Complex* bCorner,
+                 const Complex* c) {
+    check(tbt_set_margin(ctx_, e, reinterpret_cast<const double*>(bSide), reinterpret_cast<const double*>(bRow),
+                         reinterpret_cast<const double*>(bCorner), reinterpret_cast<const double*>(c)));
+  }
   void precompute() { check(tbt_precompute(ctx_)); }
 
-  Vector apply(const Vector& x) const { return run(tbt_apply, x); }    // linsolve.hpp:64
-  Vector applyA(const Vector& x) const { return run(tbt_apply_a, x); } // linsolve.hpp:65
-  Vector diagonal() const {                                             // linsolve.hpp:69
-    Vector d(static_cast<size_t>(sizeA()));
+  Vector apply(const Vector& x) const { return run(tbt_apply, x, size()); }     // linsolve.hpp:64
+  Vector applyA(const Vector& x) const { return run(tbt_apply_a, x, sizeA()); } // linsolve.hpp:65
+  Vector diagonal() const {                                                      // linsolve.hpp:69
+    Vector d(static_cast<size_t>(size()));
     check(tbt_diagonal(ctx_, reinterpret_cast<double*>(d.data())));
     return d;
   }
   long sizeA() const { return static_cast<long>(tbt_size_a(ctx_)); }
-  long sizeM() const { return 0; }
+  long sizeM() const { return static_cast<long>(tbt_size_m(ctx_)); }
+  long size() const { return sizeA() + sizeM(); }
   tbt_ctx* handle() const { return ctx_; }
 
  private:
   using Fn = tbt_status (*)(tbt_ctx*, const double*, double*, int, int);
-  Vector run(Fn fn, const Vector& x) const {
-    if (static_cast<long>(x.size()) != sizeA()) throw UserError("matvec: vector length mismatch");
+  Vector run(Fn fn, const Vector& x, long n) const {
+    if (static_cast<long>(x.size()) != n) throw UserError("matvec: vector length mismatch");
     Vector y(x.size());
     check(fn(ctx_, reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data()), 1, TBT_HOST));
     return y;
@@ -101,7 +110,7 @@ class ToeplitzMatvec {
 // any column did not converge (linsolve.cpp:591).
 inline SolveResult iterativeSolve(ToeplitzMatvec& op, const std::vector<Vector>& V, const SolverOptions& opt) {
   const int p = static_cast<int>(V.size());
-  const long n = op.sizeA();
+  const long n = op.size();
   std::vector<Complex> b(static_cast<size_t>(n) * p), x(b.size());
   for (int c = 0; c < p; ++c) std::copy(V[c].begin(), V[c].end(), b.begin() + static_cast<long>(c) * n);
   tbt_gmres_opts o{opt.tol, opt.maxIter, opt.restart, opt.precondition ? 1 : 0, 0, 0, 1};

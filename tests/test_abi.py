@@ -48,3 +48,26 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(DeviceError):
         ToeplitzMatvec(rep)
     assert _lib.last_error()
+
+
+def test_cpp_mirror_compiles(tmp_path):
+    """include/tbt.hpp (the C++ mirror a reference maintainer would include)
+    compiles against the C ABI header."""
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    src = tmp_path / "use_hpp.cpp"
+    src.write_text('#include "tbt.hpp"\n'
+                   'int main() {\n'
+                   '  std::vector<tbt::Complex> gen(1);\n'
+                   '  try { tbt::ToeplitzMatvec op(1, 1, 1, gen); int e[9] = {0};\n'
+                   '        e[4] = 1; op.setMargin(e, nullptr, nullptr, nullptr, nullptr);\n'
+                   '        op.precompute(); (void)op.apply(tbt::Vector(op.size())); }\n'
+                   '  catch (const std::exception&) {}\n'
+                   '  return 0;\n'
+                   '}\n')
+    r = subprocess.run([gxx, "-std=c++17", "-fsyntax-only", "-I", str(REPO / "include"), str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
