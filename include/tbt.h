@@ -154,6 +154,18 @@ tbt_status tbt_gmres(tbt_ctx* ctx, const double* b, double* x, int nrhs,
                      const tbt_gmres_opts* opts, tbt_gmres_stats* stats,
                      int where);
 
+/* schurSolve (linsolve.cpp:595-682), the reference's
+ * default solver: A [U F] = [V1 B^T] by A-only GMRES (opts, batches of
+ * max_nrhs columns), S = C - B F, LU with partial pivoting and the
+ * pivot-ratio check (:517-528), I2 = -S^-1 B U, I1 = U - F I2. b, x are
+ * (n + n_m) x nrhs column-major; b must vanish on the margin rows
+ * (TBT_USER_ERROR otherwise). TBT_NUMERIC_ERROR on an unconverged inner
+ * solve or a singular S. stats: iterations of the inner solve of each
+ * column, residual = |Z x - b| / |b| for Z = [A B^T; B C]. */
+tbt_status tbt_schur_solve(tbt_ctx* ctx, const double* b, double* x, int nrhs,
+                           const tbt_gmres_opts* opts, tbt_gmres_stats* stats,
+                           int where);
+
 /* Introspection for tests and the bench. */
 typedef struct {
   long long n;          /* nx*ny*m                                        */

@@ -46,6 +46,8 @@ def lib() -> C.CDLL:
         L.orc_set_margin.argtypes = [C.c_void_p, ip, dp, dp, dp, dp]
         L.orc_size.restype = C.c_longlong
         L.orc_size.argtypes = [C.c_void_p]
+        L.orc_schur.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                ip, dp, C.c_char_p, C.c_int]
         L.orc_apply_a.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply_cols.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_int, C.c_int]
@@ -190,6 +192,25 @@ class Oracle:
         d = np.empty(self.n, dtype=np.complex128)
         lib().orc_diagonal(self._h, _p(d))
         return d
+
+    def schur(self, b, tol=1e-8, max_iter=2000, restart=60, precondition=True, nthreads=1):
+        """schurSolve restated: dict(x, iterations, residual) or raises
+        ValueError (user error) / ArithmeticError (numeric)."""
+        b = np.asarray(b, dtype=np.complex128)
+        vec = b.ndim == 1
+        bc = np.asfortranarray(b[:, None] if vec else b)
+        k = bc.shape[1]
+        x = np.empty_like(bc, order="F")
+        its = np.zeros(k, np.int32)
+        res = np.zeros(k, np.float64)
+        err = C.create_string_buffer(512)
+        st = lib().orc_schur(self._h, _p(bc), _p(x), k, tol, max_iter, restart, 1 if precondition else 0, nthreads,
+                             its.ctypes.data_as(ip), _p(res), err, 512)
+        if st == 1:
+            raise ValueError(err.value.decode())
+        if st == 2:
+            raise ArithmeticError(err.value.decode())
+        return dict(x=x[:, 0] if vec else x, iterations=its.tolist(), residual=res.tolist())
 
     def gmres(self, b, tol=1e-8, max_iter=2000, restart=60, precondition=True, use_a_only=False,
               nthreads=1, hist_cap=4096):

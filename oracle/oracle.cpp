@@ -8,7 +8,10 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
+#include <limits>
+#include <string>
 #include <mutex>
 #include <thread>
 #include <utility>
@@ -796,5 +799,165 @@ extern "C" int orc_gmres(const orc_op* op, const double* b, double* x,
       if (hist_len) hist_len[c] = h.len;
     }
   });
+  return 0;
+}
+
+namespace {
+
+// Eigen::PartialPivLU restated (row interchanges on the largest |a| of the
+// column, unit lower L, U in place); perm[k] = original row of row k.
+void luPartialPivot(std::vector<cplx>& a, long n, std::vector<long>& perm) {
+  perm.resize(n);
+  for (long i = 0; i < n; ++i) perm[i] = i;
+  auto A = [&](long i, long j) -> cplx& { return a[j * n + i]; };  // column-major
+  for (long k = 0; k < n; ++k) {
+    long p = k;
+    double best = std::abs(A(k, k));
+    for (long i = k + 1; i < n; ++i)
+      if (std::abs(A(i, k)) > best) {
+        best = std::abs(A(i, k));
+        p = i;
+      }
+    if (p != k) {
+      for (long j = 0; j < n; ++j) std::swap(A(k, j), A(p, j));
+      std::swap(perm[k], perm[p]);
+    }
+    if (A(k, k) == cplx{0.0, 0.0}) continue;
+    for (long i = k + 1; i < n; ++i) A(i, k) /= A(k, k);
+    for (long j = k + 1; j < n; ++j) {
+      const cplx akj = A(k, j);
+      for (long i = k + 1; i < n; ++i) A(i, j) -= A(i, k) * akj;
+    }
+  }
+}
+
+void luSolve(const std::vector<cplx>& lu, const std::vector<long>& perm, long n, cvec& rhs) {
+  cvec y(n);
+  for (long i = 0; i < n; ++i) y[i] = rhs[perm[i]];
+  for (long i = 0; i < n; ++i)
+    for (long k = 0; k < i; ++k) y[i] -= lu[k * n + i] * y[k];
+  for (long i = n - 1; i >= 0; --i) {
+    for (long k = i + 1; k < n; ++k) y[i] -= lu[k * n + i] * y[k];
+    y[i] /= lu[i * n + i];
+  }
+  rhs = y;
+}
+
+}  // namespace
+
+// schurSolve (linsolve.cpp:595-682): A [U F] = [V1 B^T] by A-only GMRES
+// columns (Jacobi of A's diagonal), S = C - B F, PartialPivLU of S with the
+// pivot-ratio check (:517-528), I2 = -S^{-1} B U, I1 = U - F I2, residual of
+// the full operator per column. Returns 0, 1 (user error) or 2 (numeric).
+extern "C" int orc_schur(const orc_op* op, const double* b, double* x, int ncols, double tol, int max_iter,
+                         int restart, int precondition, int nthreads, int* iterations, double* residual, char* err,
+                         int errcap) {
+  auto fail = [&](int code, const std::string& msg) {
+    if (err && errcap > 0) std::snprintf(err, static_cast<size_t>(errcap), "%s", msg.c_str());
+    return code;
+  };
+  if (!op || !op->haveSpectra || ncols < 1) return fail(1, "schurSolve: bad arguments");
+  const long nA = op->nA, nM = op->haveMargin ? op->nM : 0, n = nA + nM;
+  const cplx* B = reinterpret_cast<const cplx*>(b);
+  for (int c = 0; c < ncols; ++c)
+    for (long k = nA; k < n; ++k)
+      if (B[c * n + k] != cplx{0.0, 0.0}) return fail(1, "schurSolve: excitation must vanish on margin rows");
+  cvec invDiagA;
+  if (precondition) {
+    invDiagA.resize(nA);
+    for (long i = 0; i < nA; ++i) {
+      const cplx d = op->aEntry(0, 0, static_cast<int>(i % op->e5), static_cast<int>(i % op->e5));
+      invDiagA[i] = std::abs(d) > 0.0 ? 1.0 / d : cplx{1.0, 0.0};
+    }
+  }
+  // Dense B^T (nA x nM) column by column: B^T e_k.
+  std::vector<cplx> bt(static_cast<size_t>(nA) * nM, cplx{0.0, 0.0});
+  for (long k = 0; k < nM; ++k) {
+    cvec e(nM, cplx{0.0, 0.0});
+    e[k] = 1.0;
+    op->applyBT(e.data(), bt.data() + k * nA);
+  }
+  const long p = ncols, cols = p + nM;
+  std::vector<cplx> uf(static_cast<size_t>(nA) * cols);
+  std::vector<int> its(cols, 0);
+  std::vector<double> res(cols, 0.0);
+  std::vector<int> conv(cols, 0);
+  auto opA = [op](const cvec& in, cvec& out) { op->applyA(in.data(), out.data()); };
+  forkJoin(cols, nthreads, [&](long lo, long hi) {
+    for (long c = lo; c < hi; ++c) {
+      cvec rhs(nA);
+      if (c < p)
+        for (long i = 0; i < nA; ++i) rhs[i] = B[c * n + i];
+      else
+        std::copy(bt.begin() + (c - p) * nA, bt.begin() + (c - p + 1) * nA, rhs.begin());
+      cvec xc;
+      History h{nullptr, 0};
+      const Outcome o = gmresColumn(opA, rhs, xc, precondition ? &invDiagA : nullptr, tol, max_iter, restart, h);
+      std::copy(xc.begin(), xc.end(), uf.begin() + c * nA);
+      its[c] = o.iterations;
+      res[c] = o.residual;
+      conv[c] = o.converged ? 1 : 0;
+    }
+  });
+  for (long c = 0; c < cols; ++c)
+    if (!conv[c])
+      return fail(2, "schur inner solve did not converge (column " + std::to_string(c) + ", best residual " +
+                         std::to_string(res[c]) + ")");
+  cplx* X = reinterpret_cast<cplx*>(x);
+  for (long c = 0; c < p; ++c) {
+    for (long i = 0; i < nA; ++i) X[c * n + i] = uf[c * nA + i];
+    for (long k = 0; k < nM; ++k) X[c * n + nA + k] = 0.0;
+  }
+  if (nM > 0) {
+    // S = C - B F with B = (B^T)^T (plain transpose).
+    std::vector<cplx> S(static_cast<size_t>(nM) * nM);
+    forkJoin(nM, nthreads, [&](long lo, long hi) {
+      for (long l = lo; l < hi; ++l)
+        for (long k = 0; k < nM; ++k) {
+          cplx acc{0.0, 0.0};
+          const cplx* bk = bt.data() + k * nA;
+          const cplx* fl = uf.data() + (p + l) * nA;
+          for (long q = 0; q < nA; ++q) acc += bk[q] * fl[q];
+          S[l * nM + k] = op->cDense[l * nM + k] - acc;
+        }
+    });
+    std::vector<long> perm;
+    luPartialPivot(S, nM, perm);
+    double maxAbs = 0.0, minAbs = std::numeric_limits<double>::infinity();
+    for (long i = 0; i < nM; ++i) {
+      maxAbs = std::max(maxAbs, std::abs(S[i * nM + i]));
+      minAbs = std::min(minAbs, std::abs(S[i * nM + i]));
+    }
+    if (!(minAbs > 1e-14 * maxAbs))
+      return fail(2, "singular matrix in schur complement (pivot ratio " +
+                         std::to_string(minAbs / (maxAbs > 0 ? maxAbs : 1.0)) + ")");
+    for (long c = 0; c < p; ++c) {
+      cvec r(nM);
+      for (long k = 0; k < nM; ++k) {
+        cplx acc{0.0, 0.0};
+        for (long q = 0; q < nA; ++q) acc += bt[k * nA + q] * uf[c * nA + q];
+        r[k] = acc;
+      }
+      luSolve(S, perm, nM, r);
+      for (long k = 0; k < nM; ++k) r[k] = -r[k];  // I2
+      for (long i = 0; i < nA; ++i) {
+        cplx acc{0.0, 0.0};
+        for (long k = 0; k < nM; ++k) acc += uf[(p + k) * nA + i] * r[k];
+        X[c * n + i] = uf[c * nA + i] - acc;
+      }
+      for (long k = 0; k < nM; ++k) X[c * n + nA + k] = r[k];
+    }
+  }
+  for (long c = 0; c < p; ++c) {
+    cvec xc(X + c * n, X + (c + 1) * n), yc(n);
+    op->apply(xc.data(), yc.data());
+    double num = 0.0, bn = 0.0;
+    for (long i = 0; i < n; ++i) {
+      num += std::norm(yc[i] - B[c * n + i]);
+      bn += std::norm(B[c * n + i]);
+    }
+    if (residual) residual[c] = std::sqrt(num) / (bn > 0 ? std::sqrt(bn) : 1.0);
+    if (iterations) iterations[c] = its[c];
+  }
   return 0;
 }

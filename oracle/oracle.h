@@ -92,6 +92,13 @@ int orc_gmres(const orc_op* op, const double* b, double* x, int ncols,
               int use_a_only, int nthreads, int* iterations, double* residual,
               int* converged, double* hist, int hist_cap, int* hist_len);
 
+/* schurSolve (linsolve.cpp:595-682) on the margin representation: A-only
+ * GMRES for [V1, B^T], S = C - B F, partial-pivot LU with the pivot-ratio
+ * check, I2 = -S^-1 B U, I1 = U - F I2. b, x: (nA+nM) x ncols column-major.
+ * Returns 0, 1 (user error) or 2 (numeric error), message in err. */
+int orc_schur(const orc_op* op, const double* b, double* x, int ncols, double tol, int max_iter, int restart,
+              int precondition, int nthreads, int* iterations, double* residual, char* err, int errcap);
+
 #ifdef __cplusplus
 }
 #endif

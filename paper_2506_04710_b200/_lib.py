@@ -59,6 +59,8 @@ SIGNATURES = {
     "tbt_set_margin": (C.c_int, [C.c_void_p, ip, dp, dp, dp, dp]),
     "tbt_gmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),
                             C.POINTER(TbtGmresStats), C.c_int]),
+    "tbt_schur_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),
+                                  C.POINTER(TbtGmresStats), C.c_int]),
     "tbt_get_info": (C.c_int, [C.c_void_p, C.POINTER(TbtInfo)]),
     "tbt_get_spectrum_bin": (C.c_int, [C.c_void_p, C.c_longlong, dp]),
     "tbt_bench_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, dp, dp]),

@@ -738,6 +738,50 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
   return st;
 }
 
+tbt_status tbt_schur_solve(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt_gmres_opts* opts,
+                           tbt_gmres_stats* stats, int where) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && b && x && opts, "tbt_schur_solve: null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(!c.dist, "tbt_schur_solve: not available on a distributed context");
+    TBT_USER_CHECK(nrhs >= 1, "tbt_schur_solve: nrhs must be >= 1");
+    TBT_USER_CHECK(opts->restart >= 1 && opts->max_iter >= 0 && opts->tol > 0.0, "tbt_schur_solve: bad options");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    const long long ntot = c.n + c.nM;
+    const size_t bytes = static_cast<size_t>(ntot) * nrhs * sizeof(double2);
+    double2* db = nullptr;
+    double2* dx = nullptr;
+    struct Free {
+      double2** a;
+      double2** b;
+      ~Free() {
+        if (*a) cudaFree(*a);
+        if (*b) cudaFree(*b);
+      }
+    } fr{&db, &dx};
+    TBT_CUDA_CHECK(cudaMalloc(&db, bytes));
+    TBT_CUDA_CHECK(cudaMalloc(&dx, bytes));
+    TBT_CUDA_CHECK(cudaMemcpyAsync(db, b, bytes, where == TBT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                   c.stream));
+    std::vector<int> its;
+    std::vector<double> res;
+    schurSolve(c, db, dx, nrhs, *opts, its, res);
+    TBT_CUDA_CHECK(cudaMemcpyAsync(x, dx, bytes, where == TBT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                   c.stream));
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (stats) {
+      for (int k = 0; k < nrhs; ++k) {
+        if (stats->iterations) stats->iterations[k] = its[k];
+        if (stats->residual) stats->residual[k] = res[k];
+        if (stats->converged) stats->converged[k] = 1;
+        if (stats->history_len) stats->history_len[k] = 0;
+      }
+      stats->matvecs = 0;
+    }
+  });
+}
+
 tbt_status tbt_get_info(const tbt_ctx* h, tbt_info* info) {
   return guarded([&] {
     TBT_USER_CHECK(h && info, "tbt_get_info: null argument");

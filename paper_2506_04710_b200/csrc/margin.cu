@@ -30,47 +30,9 @@
 #include <algorithm>
 #include <climits>
 
-#include "tbt_internal.cuh"
+#include "margin.cuh"
 
 namespace tbt {
-
-struct MarginOp {
-  int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long nM = 0;
-  int Ly = 1, Lx = 1;
-  int emSide[2] = {0, 0}, emRow[2] = {0, 0}, emCorner[4] = {0, 0, 0, 0};
-  long long sideStart[2] = {0, 0}, rowStart[2] = {0, 0}, cornerStart[4] = {0, 0, 0, 0};
-  double2* gSide[2] = {nullptr, nullptr};  // [Ly][em][nx*m]
-  double2* gRow[2] = {nullptr, nullptr};   // [ny][Lx][em][m]
-  double2* corner[4] = {nullptr, nullptr, nullptr, nullptr};  // [em][nA] row-major
-  double2* C = nullptr;                    // [nM][nM] row-major
-  double2* twY = nullptr;
-  double2* twX = nullptr;
-  std::vector<double2> diag;               // C's diagonal (host)
-  // Work buffers for max_nrhs columns.
-  double2 *xs = nullptr, *ys = nullptr;        // [nM][K]
-  double2 *hatY = nullptr, *hatZy = nullptr;   // [Ly][nx][K][m]
-  double2 *hatX = nullptr, *hatZx = nullptr;   // [Lx][ny][K][m]
-  double2* hatMs[2] = {nullptr, nullptr};       // [Ly][em][K]
-  double2* hatMr[2] = {nullptr, nullptr};       // [Lx][em][K]
-  double2 *zA = nullptr, *zA2 = nullptr;       // [ne][K][m]
-  double2* cornerPart = nullptr;               // [corner rows][K][element blocks]
-  std::vector<void*> allocs;
-  cudaStream_t stream = nullptr;
-
-  double2* alloc(size_t count) {
-    void* p = nullptr;
-    TBT_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double2)));
-    if (poisonBuffers()) memsetSync(p, 0xFF, std::max<size_t>(count, 1) * sizeof(double2), stream);
-    allocs.push_back(p);
-    return static_cast<double2*>(p);
-  }
-  ~MarginOp() {
-    for (void* p : allocs) cudaFree(p);
-  }
-  bool anySide() const { return emSide[0] + emSide[1] > 0; }
-  bool anyRow() const { return emRow[0] + emRow[1] > 0; }
-};
 
 namespace {
 
@@ -432,6 +394,7 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
     const long long P = em * qs, rawCount = (2LL * ny - 1) * P;
     if (em == 0) continue;
     double2* raw = M->alloc(rawCount);
+    M->rawSide[r] = raw;
     uploadSync(raw, bside + off, rawCount * sizeof(double2), c.stream);
     double2* seq = M->alloc(static_cast<size_t>(M->Ly) * P);
     toeSeq<<<gridFor(M->Ly * P), 256, 0, s>>>(raw, seq, 1, M->Ly, ny, em, qs);
@@ -454,6 +417,7 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
     const long long P = static_cast<long long>(em) * m, rawCount = static_cast<long long>(ny) * (2 * nx - 1) * P;
     if (em == 0) continue;
     double2* raw = M->alloc(rawCount);
+    M->rawRow[r] = raw;
     uploadSync(raw, brow + off, rawCount * sizeof(double2), c.stream);
     double2* seq = M->alloc(static_cast<size_t>(ny) * M->Lx * P);
     toeSeq<<<gridFor(static_cast<long long>(ny) * M->Lx * P), 256, 0, s>>>(raw, seq, ny, M->Lx, nx, em, m);

@@ -258,6 +258,9 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
 void marginFree(Ctx& c);
 void marginApply(Ctx& c, const double2* x, double2* y, int nrhs);  // y's element part already holds A x
 void marginDiagonal(const Ctx& c, std::vector<double2>& d);          // appends C's diagonal
+// schur.cu: b, x device (nA + nM) x p column-major (user layout).
+void schurSolve(Ctx& c, const double2* b, double2* x, int p, const tbt_gmres_opts& o, std::vector<int>& iterations,
+                std::vector<double>& residual);
 std::vector<double2> twiddleTable(int n);                           // api.cu
 bool poisonBuffers();                                               // api.cu: TBT_POISON=1
 void uploadSync(void* dst, const void* src, size_t bytes, cudaStream_t s);  // api.cu

@@ -280,6 +280,25 @@ class ToeplitzMatvec:
         cur = None if x is None else (x[:, 0] if vec else x)
         return SolveResult(cur, res.tolist(), its.tolist(), "gmres", conv.tolist(), histories, st.matvecs)
 
+    def schur_solve(self, b, opt: SolverOptions) -> SolveResult:
+        """schurSolve (linsolve.cpp:595-682) on the device: b is (sizeA + sizeM)
+        x p with zero margin rows. Raises UserError / NumericError like the
+        reference (inner solve not converged, singular Schur complement)."""
+        bc, k, vec = _as_cols(b)
+        if bc.shape[0] != self.size():
+            raise UserError(f"schurSolve: excitation size mismatch ({bc.shape[0]} vs {self.size()})")
+        x = np.empty_like(bc, order="F")
+        its = np.zeros(k, dtype=np.int32)
+        res = np.zeros(k, dtype=np.float64)
+        conv = np.zeros(k, dtype=np.int32)
+        hlen = np.zeros(k, dtype=np.int32)
+        st = TbtGmresStats(its.ctypes.data_as(C.POINTER(C.c_int)), res.ctypes.data_as(dp),
+                           conv.ctypes.data_as(C.POINTER(C.c_int)), None, hlen.ctypes.data_as(C.POINTER(C.c_int)), 0)
+        o = TbtGmresOpts(opt.tol, opt.maxIter, opt.restart, 1 if opt.precondition else 0, 1, 0, opt.orthog)
+        _check(lib().tbt_schur_solve(self._h, C.c_void_p(bc.ctypes.data), C.c_void_p(x.ctypes.data), k, C.byref(o),
+                                     C.byref(st), TBT_HOST))
+        return SolveResult(x[:, 0] if vec else x, res.tolist(), its.tolist(), "schur", conv.tolist(), [], 0)
+
 
 def dist_unique_id() -> bytes:
     """A fresh NCCL unique id (128 bytes) for tbt_dist_init (call on rank 0)."""
@@ -311,6 +330,17 @@ def toeplitz_matvec(rep: ToeplitzRep, x) -> np.ndarray:
     op = ToeplitzMatvec(rep)
     try:
         return op.apply(x)
+    finally:
+        op.close()
+
+
+def schur_solve(rep: ToeplitzRep, V, opt: SolverOptions | None = None) -> SolveResult:
+    """schurSolve (linsolve.hpp:93-95) through the device operator."""
+    opt = opt or SolverOptions()
+    k = 1 if np.ndim(V) == 1 else np.shape(V)[1]
+    op = ToeplitzMatvec(rep, max_nrhs=max(1, min(k + (rep.margin.size(rep.nx, rep.ny) if rep.margin else 0), 64)))
+    try:
+        return op.schur_solve(V, opt)
     finally:
         op.close()
 

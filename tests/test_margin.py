@@ -157,3 +157,59 @@ def test_gpu_margin_gmres(gpu, k, orthog):
     ra = o.gmres(np.ascontiguousarray(B[:o.nA, 0]), tol=1e-9, max_iter=400, restart=20, use_a_only=True)
     assert ga.iterations == ra["iterations"]
     assert np.linalg.norm(ga.current - ra["x"]) / np.linalg.norm(ra["x"]) < 1e-8
+
+
+def test_oracle_schur_vs_dense():
+    """schurSolve restated (linsolve.cpp:595-682) equals the dense solve of
+    Z x = [v; 0], and rejects excitations on margin rows."""
+    rep = rep_with_margin(4, 3, 6, [2, 3, 1, 4, 6, 2, 3, 5, 1], corr=False)
+    o = oracle.Oracle.from_rep(rep)
+    Z = dense_full(rep)
+    V = np.zeros((o.n, 2), complex)
+    V[:o.nA] = gen.rhs_normal(o.nA, 2, 4)
+    r = o.schur(V, tol=1e-12, max_iter=3000, restart=40)
+    xs = np.linalg.solve(Z, V)
+    assert np.linalg.norm(r["x"] - xs) / np.linalg.norm(xs) < 1e-9
+    assert max(r["residual"]) < 1e-9
+    bad = V.copy()
+    bad[-1, 0] = 1.0
+    with pytest.raises(ValueError):
+        o.schur(bad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,m,e,p,maxrhs", [(4, 3, 6, [2, 3, 1, 4, 6, 2, 3, 5, 1], 2, 8),
+                                                 (5, 4, 8, [0, 2, 0, 3, 8, 1, 0, 2, 1], 1, 16),
+                                                 (3, 3, 4, [1, 1, 1, 1, 4, 1, 1, 1, 1], 3, 4)])
+def test_gpu_schur_solve(gpu, nx, ny, m, e, p, maxrhs):
+    """schurSolve on the device (row f2) against the oracle's restatement
+    and the dense solve: inner iterations, solution, residual."""
+    from paper_2506_04710_b200 import ToeplitzMatvec
+    rep = rep_with_margin(nx, ny, m, e, corr=False)
+    o = oracle.Oracle.from_rep(rep)
+    op = ToeplitzMatvec(rep, max_nrhs=maxrhs)
+    V = np.zeros((o.n, p), complex)
+    V[:o.nA] = gen.rhs_normal(o.nA, p, 4)
+    opt = SolverOptions(tol=1e-11, maxIter=3000, restart=30)
+    g = op.schur_solve(V, opt)
+    r = o.schur(V, tol=1e-11, max_iter=3000, restart=30)
+    assert g.iterations == r["iterations"]
+    assert np.linalg.norm(g.current - r["x"]) / np.linalg.norm(r["x"]) < 1e-8
+    xs = np.linalg.solve(dense_full(rep), V)
+    assert np.linalg.norm(g.current - xs) / np.linalg.norm(xs) < 1e-8
+    assert max(g.residual) < 1e-8
+
+
+@pytest.mark.gpu
+def test_gpu_schur_errors(gpu):
+    from paper_2506_04710_b200 import NumericError, ToeplitzMatvec, UserError
+    rep = rep_with_margin(4, 3, 6, [2, 3, 1, 4, 6, 2, 3, 5, 1], corr=False)
+    op = ToeplitzMatvec(rep, max_nrhs=4)
+    V = np.zeros((op.size(), 1), complex)
+    V[:op.sizeA(), 0] = gen.rhs_normal(op.sizeA(), 1, 4)[:, 0]
+    bad = V.copy()
+    bad[-1, 0] = 1.0
+    with pytest.raises(UserError):
+        op.schur_solve(bad, SolverOptions())
+    with pytest.raises(NumericError):  # inner solves cannot converge in 2 iterations
+        op.schur_solve(V, SolverOptions(tol=1e-14, maxIter=2, restart=2))
