@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--edges", type=int, default=8)
 ap.add_argument("--no-cpu", action="store_true")
+ap.add_argument("--schur", action="store_true", help="also time schurSolve (needs a config whose A-solves converge, e.g. C1)")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 e = [args.edges] * 9
@@ -78,4 +79,23 @@ if not args.no_cpu:
     yd = y.cpu().numpy()
     ref = o.apply(x.cpu().numpy())
     out["parity_rel_err"] = float(np.linalg.norm(yd - ref) / np.linalg.norm(ref))
+if args.schur:
+    rep.correction = None  # schurSolve's A block is applyA (linsolve.cpp:644)
+    ops = ToeplitzMatvec(rep, max_nrhs=64)
+    V = np.zeros((ops.size(), cfg.nrhs), complex)
+    V[:cfg.n] = gen.rhs_normal(cfg.n, cfg.nrhs, 4)
+    sopt = SolverOptions(tol=cfg.tol, maxIter=cfg.max_iter, restart=cfg.restart)
+    ops.schur_solve(V, sopt)
+    t0 = time.perf_counter()
+    g = ops.schur_solve(V, sopt)
+    out["schur_ms"] = 1e3 * (time.perf_counter() - t0)
+    out["schur_inner_columns"] = cfg.nrhs + ops.sizeM()
+    out["schur_residual"] = max(g.residual)
+    if not args.no_cpu:
+        import oracle
+        o = oracle.Oracle.from_rep(rep)
+        t0 = time.perf_counter()
+        r = o.schur(V, tol=cfg.tol, max_iter=cfg.max_iter, restart=cfg.restart, nthreads=0)
+        out["cpu_oracle_schur_ms_all_cores"] = 1e3 * (time.perf_counter() - t0)
+        out["schur_parity_rel_err"] = float(np.linalg.norm(g.current - r["x"]) / np.linalg.norm(r["x"]))
 print(json.dumps(out))
