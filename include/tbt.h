@@ -166,6 +166,25 @@ tbt_status tbt_schur_solve(tbt_ctx* ctx, const double* b, double* x, int nrhs,
                            const tbt_gmres_opts* opts, tbt_gmres_stats* stats,
                            int where);
 
+/* Row f3: a reference ZTOE1 block cache (saveBlockCache,
+ * proj/src/toeplitz.cpp:700-743; Sparse mode) straight into a precomputed
+ * context: AGen -> generators, BSide/BRow/BCorner -> margin B, the C records
+ * assembled into the margin block by partBlock's rules (:506-573).
+ * tbt_ztoe1_dims reads only the header (e: 9 ints). */
+tbt_status tbt_load_ztoe1(const char* path, int max_nrhs, int device,
+                          int flags, tbt_ctx** ctx);
+tbt_status tbt_ztoe1_dims(const char* path, int* nx, int* ny, int* e);
+/* Host-only parse of a ZTOE1 cache into the tbt_set_generators /
+ * tbt_set_margin layouts (any pointer may be NULL; sizes from
+ * tbt_ztoe1_dims and tbtgen_margin_lengths). */
+tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside,
+                          double* brow, double* bcorner, double* c);
+/* Persisted bin-major half spectrum (+ the self block): tbt_load_spectra
+ * replaces tbt_set_generators + tbt_precompute on a context of the same
+ * nx, ny, m and embedding (K1 skipped across runs). */
+tbt_status tbt_save_spectra(tbt_ctx* ctx, const char* path);
+tbt_status tbt_load_spectra(tbt_ctx* ctx, const char* path);
+
 /* Introspection for tests and the bench. */
 typedef struct {
   long long n;          /* nx*ny*m                                        */

@@ -61,6 +61,11 @@ SIGNATURES = {
                             C.POINTER(TbtGmresStats), C.c_int]),
     "tbt_schur_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),
                                   C.POINTER(TbtGmresStats), C.c_int]),
+    "tbt_load_ztoe1": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "tbt_ztoe1_dims": (C.c_int, [C.c_char_p, ip, ip, ip]),
+    "tbt_ztoe1_read": (C.c_int, [C.c_char_p, dp, dp, dp, dp, dp]),
+    "tbt_save_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "tbt_load_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
     "tbt_get_info": (C.c_int, [C.c_void_p, C.POINTER(TbtInfo)]),
     "tbt_get_spectrum_bin": (C.c_int, [C.c_void_p, C.c_longlong, dp]),
     "tbt_bench_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, dp, dp]),

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -779,6 +780,92 @@ tbt_status tbt_schur_solve(tbt_ctx* h, const double* b, double* x, int nrhs, con
       }
       stats->matvecs = 0;
     }
+  });
+}
+
+tbt_status tbt_load_ztoe1(const char* path, int max_nrhs, int device, int flags, tbt_ctx** out) {
+  return guarded([&] {
+    TBT_USER_CHECK(path && out, "tbt_load_ztoe1: null argument");
+    *out = nullptr;
+    Ztoe1Data z;
+    readZtoe1(path, z);
+    tbt_desc d{z.nx, z.ny, z.e[4], max_nrhs, device, flags};
+    tbt_ctx* h = nullptr;
+    const tbt_status st = tbt_create(&d, &h);
+    if (st != TBT_OK) throw Error{st, gLastError};
+    try {
+      auto chk = [](tbt_status s2) {
+        if (s2 != TBT_OK) throw Error{s2, gLastError};
+      };
+      chk(tbt_set_generators(h, reinterpret_cast<const double*>(z.gen.data()),
+                             static_cast<long long>(z.gen.size() / (static_cast<size_t>(z.e[4]) * z.e[4]))));
+      if (z.nM > 0)
+        chk(tbt_set_margin(h, z.e, reinterpret_cast<const double*>(z.bside.data()),
+                           reinterpret_cast<const double*>(z.brow.data()),
+                           reinterpret_cast<const double*>(z.bcorner.data()),
+                           reinterpret_cast<const double*>(z.c.data())));
+      chk(tbt_precompute(h));
+    } catch (...) {
+      tbt_destroy(h);
+      throw;
+    }
+    *out = h;
+  });
+}
+
+tbt_status tbt_ztoe1_dims(const char* path, int* nx, int* ny, int* e) {
+  return guarded([&] {
+    TBT_USER_CHECK(path && nx && ny && e, "tbt_ztoe1_dims: null argument");
+    std::ifstream in(path, std::ios::binary);
+    TBT_USER_CHECK(static_cast<bool>(in), std::string("cannot open block cache: ") + path);
+    char head[5 + 1 + 4 * 11];
+    in.read(head, sizeof head);
+    TBT_USER_CHECK(in && std::string(head, 5) == "ZTOE1", std::string("not a ZTOE1 block cache: ") + path);
+    std::memcpy(nx, head + 6, 4);
+    std::memcpy(ny, head + 10, 4);
+    std::memcpy(e, head + 14, 36);
+  });
+}
+
+tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside, double* brow, double* bcorner, double* cm) {
+  return guarded([&] {
+    TBT_USER_CHECK(path, "tbt_ztoe1_read: null path");
+    Ztoe1Data z;
+    readZtoe1(path, z);
+    auto put = [](double* dst, const std::vector<double2>& src) {
+      if (dst && !src.empty()) std::memcpy(dst, src.data(), src.size() * sizeof(double2));
+    };
+    put(gen, z.gen);
+    put(bside, z.bside);
+    put(brow, z.brow);
+    put(bcorner, z.bcorner);
+    put(cm, z.c);
+  });
+}
+
+tbt_status tbt_save_spectra(tbt_ctx* h, const char* path) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && path, "tbt_save_spectra: null argument");
+    TBT_CUDA_CHECK(cudaSetDevice(h->c.device));
+    saveSpectra(h->c, path);
+  });
+}
+
+tbt_status tbt_load_spectra(tbt_ctx* h, const char* path) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && path, "tbt_load_spectra: null argument");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    c.dropGraph();
+    freeGmresWorkspace(c);
+    loadSpectra(c, path);
+    if (c.dGen) {
+      cudaFree(c.dGen);
+      c.dGen = nullptr;
+    }
+    c.haveGenerators = false;
+    c.havePrecompute = true;
+    refreshDiagonal(c, nullptr);
   });
 }
 

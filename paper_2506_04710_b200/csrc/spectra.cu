@@ -76,13 +76,11 @@ __global__ void scatterPairs(const double2* __restrict__ G, const int* __restric
 
 }  // namespace
 
-void buildSpectra(Ctx& c) {
-  const int m = c.m, nx = c.nx, ny = c.ny;
+// The self block's antisymmetric part K = (Z0 - Z0^T)/2 (applied in space);
+// returns the symmetric part S0 (column-major) for the gather.
+std::vector<double2> splitSelfBlock(Ctx& c) {
+  const int m = c.m;
   const long long mm = static_cast<long long>(m) * m;
-  // canonical generator blocks: c.dGen (tbt_set_generators)
-  cudaStream_t s = c.stream;
-
-  // Split Z(0,0) into symmetric / antisymmetric parts on the host.
   std::vector<double2> s0(mm), kk(mm);
   c.hasAntisym = false;
   for (int a = 0; a < m; ++a)
@@ -101,12 +99,18 @@ void buildSpectra(Ctx& c) {
   }
   if (c.hasAntisym) {
     TBT_CUDA_CHECK(cudaMalloc(&c.dAntisym, mm * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMemcpyAsync(c.dAntisym, kk.data(), mm * sizeof(double2), cudaMemcpyHostToDevice, s));
+    uploadSync(c.dAntisym, kk.data(), mm * sizeof(double2), c.stream);
   }
+  return s0;
+}
 
-  // Bin pairs: f and its partner -f; representatives are f <= partner.
-  // Distributed: only the columns this rank owns (closed under s0 -> -s0,
-  // dist.cu), bins renumbered to the rank's local [s1][j] layout.
+// Bin pairs f and its partner -f (representatives f <= partner), the
+// device pair tables and the spectrum allocation. Distributed: only the
+// columns this rank owns (closed under s0 -> -s0, dist.cu), bins
+// renumbered to the rank's local [s1][j] layout. pairFGlobal gets the
+// global representative bins.
+void planPairs(Ctx& c, std::vector<int>& pairFGlobal) {
+  const long long mm = static_cast<long long>(c.m) * c.m;
   std::vector<int> colPos(c.L0, -1);
   int nLocalCols = c.L0;
   if (c.dist) {
@@ -120,7 +124,7 @@ void buildSpectra(Ctx& c) {
   };
   c.pairF.clear();
   c.pairG.clear();
-  std::vector<int> pairFGlobal;
+  pairFGlobal.clear();
   c.pairOfBin.assign(static_cast<size_t>(c.L), 0);
   for (long long f = 0; f < c.L; ++f) {
     const int s1 = static_cast<int>(f / c.L0), s0i = static_cast<int>(f % c.L0);
@@ -135,26 +139,35 @@ void buildSpectra(Ctx& c) {
     }
   }
   c.npairs = static_cast<long long>(c.pairF.size());
-
   if (c.dSpectra) cudaFree(c.dSpectra);
   if (c.dPairF) cudaFree(c.dPairF);
   if (c.dPairG) cudaFree(c.dPairG);
   c.dSpectra = nullptr;
   c.dPairF = c.dPairG = nullptr;
-  int* dPairFGlobal = nullptr;
   TBT_CUDA_CHECK(cudaMalloc(&c.dSpectra, std::max<long long>(c.npairs, 1) * mm * sizeof(double2)));
   TBT_CUDA_CHECK(cudaMalloc(&c.dPairF, std::max<long long>(c.npairs, 1) * sizeof(int)));
   TBT_CUDA_CHECK(cudaMalloc(&c.dPairG, std::max<long long>(c.npairs, 1) * sizeof(int)));
+  uploadSync(c.dPairF, c.pairF.data(), c.npairs * sizeof(int), c.stream);
+  uploadSync(c.dPairG, c.pairG.data(), c.npairs * sizeof(int), c.stream);
+}
+
+void buildSpectra(Ctx& c) {
+  const int m = c.m, nx = c.nx, ny = c.ny;
+  const long long mm = static_cast<long long>(m) * m;
+  // canonical generator blocks: c.dGen (tbt_set_generators)
+  cudaStream_t s = c.stream;
+  const std::vector<double2> s0 = splitSelfBlock(c);
+  std::vector<int> pairFGlobal;
+  planPairs(c, pairFGlobal);
+  int* dPairFGlobal = nullptr;
   TBT_CUDA_CHECK(cudaMalloc(&dPairFGlobal, std::max<long long>(c.npairs, 1) * sizeof(int)));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(c.dPairF, c.pairF.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(c.dPairG, c.pairG.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), cudaMemcpyHostToDevice, s));
+  uploadSync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), s);
 
   // Generators and S0 on the device for the gather.
   const double2* dGen = c.dGen;
   double2 *dS0 = nullptr, *dG = nullptr;
   TBT_CUDA_CHECK(cudaMalloc(&dS0, mm * sizeof(double2)));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(dS0, s0.data(), mm * sizeof(double2), cudaMemcpyHostToDevice, s));
+  uploadSync(dS0, s0.data(), mm * sizeof(double2), s);
 
   // Row chunks bounded to ~4 GiB of transform workspace.
   const long long budget = 4LL << 30;

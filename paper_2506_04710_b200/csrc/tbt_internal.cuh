@@ -207,6 +207,8 @@ struct Ctx {
 
 // Kernels / launchers implemented in the .cu files.
 void buildSpectra(Ctx& c);                                    // spectra.cu
+std::vector<double2> splitSelfBlock(Ctx& c);                   // spectra.cu: K on device, returns S0
+void planPairs(Ctx& c, std::vector<int>& pairFGlobal);         // spectra.cu: pair tables + spectrum allocation
 void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 int binprodVariant(int m);                                    // binprod.cu
@@ -252,6 +254,17 @@ const NcclApi& nccl();
     if (r_ != ncclSuccess)                                                                    \
       throw ::tbt::Error{TBT_CUDA_ERROR, std::string(#expr) + ": " + nccl().errorString(r_)}; \
   } while (0)
+// io.cu (row f3): reference ZTOE1 block caches, persisted spectra.
+struct Ztoe1Data {
+  int nx = 0, ny = 0;
+  int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long nM = 0;
+  std::vector<double2> gen, bside, brow, bcorner, c;  // tbt_gen.h layouts; c: nM x nM column-major
+};
+void readZtoe1(const std::string& path, Ztoe1Data& out);
+void saveSpectra(Ctx& c, const std::string& path);
+void loadSpectra(Ctx& c, const std::string& path);
+
 // margin.cu
 void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, const double2* bcorner,
                const double2* C);

@@ -127,20 +127,25 @@ class ToeplitzMatvec:
     """FFT-accelerated application of Z^part (linsolve.hpp:59-77) on a B200."""
 
     def __init__(self, rep: ToeplitzRep, max_nrhs: int = 1, device: int = 0, embed: str = "pow2",
-                 dist: tuple | None = None):
+                 dist: tuple | None = None, spectra_cache: str | None = None):
         """embed: "pow2" (the reference's nextPow2 embedding) or "smooth"
         (smallest 2^a 3^b length per level, mixed-radix transforms).
         dist: (nranks, rank, nccl_unique_id_bytes) to shard the operator over
         one process per GPU (see dist_unique_id / init_from_torch); apply /
-        applyA / diagonal then work on this rank's element-row slab."""
+        applyA / diagonal then work on this rank's element-row slab.
+        spectra_cache: a TBTS1 file; loaded instead of K1 when it exists,
+        written after K1 otherwise (row f3)."""
         self.rep = rep
         self._h = C.c_void_p()
         if embed not in ("pow2", "smooth"):
             raise UserError(f"embed must be 'pow2' or 'smooth', got {embed!r}")
         desc = TbtDesc(rep.nx, rep.ny, rep.m, max_nrhs, device, 1 if embed == "smooth" else 0)
         _check(lib().tbt_create(C.byref(desc), C.byref(self._h)))
-        gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
-        _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))
+        import os
+        cached = spectra_cache is not None and os.path.exists(spectra_cache)
+        if not cached:
+            gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
+            _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))
         if rep.correction is not None:
             c = rep.correction
             d = np.ascontiguousarray(c.d)
@@ -159,8 +164,28 @@ class ToeplitzMatvec:
         if dist is not None:
             nranks, rank, uid = dist
             _check(lib().tbt_dist_init(self._h, int(nranks), int(rank), bytes(uid)))
-        _check(lib().tbt_precompute(self._h))
+        if cached:
+            _check(lib().tbt_load_spectra(self._h, spectra_cache.encode()))
+        else:
+            _check(lib().tbt_precompute(self._h))
+            if spectra_cache is not None:
+                _check(lib().tbt_save_spectra(self._h, spectra_cache.encode()))
         self.max_nrhs = max_nrhs
+
+    @classmethod
+    def from_ztoe1(cls, path: str, max_nrhs: int = 1, device: int = 0, embed: str = "pow2") -> "ToeplitzMatvec":
+        """Operator from a reference ZTOE1 block cache (saveBlockCache,
+        toeplitz.cpp:700-743; Sparse mode), precomputed (row f3)."""
+        nx, ny = C.c_int(), C.c_int()
+        e = (C.c_int * 9)()
+        _check(lib().tbt_ztoe1_dims(path.encode(), C.byref(nx), C.byref(ny), e))
+        self = cls.__new__(cls)
+        self.rep = ToeplitzRep(nx.value, ny.value, e[4], np.empty((0, e[4], e[4]), np.complex128))
+        self._h = C.c_void_p()
+        _check(lib().tbt_load_ztoe1(path.encode(), max_nrhs, device, 1 if embed == "smooth" else 0,
+                                    C.byref(self._h)))
+        self.max_nrhs = max_nrhs
+        return self
 
     def close(self) -> None:
         if self._h:
@@ -298,6 +323,29 @@ class ToeplitzMatvec:
         _check(lib().tbt_schur_solve(self._h, C.c_void_p(bc.ctypes.data), C.c_void_p(x.ctypes.data), k, C.byref(o),
                                      C.byref(st), TBT_HOST))
         return SolveResult(x[:, 0] if vec else x, res.tolist(), its.tolist(), "schur", conv.tolist(), [], 0)
+
+
+def read_ztoe1(path: str) -> ToeplitzRep:
+    """A reference ZTOE1 block cache (Sparse mode) as a ToeplitzRep with its
+    margin data (host-side parse, csrc/io.cu; row f3)."""
+    from . import gen as _gen
+    nx, ny = C.c_int(), C.c_int()
+    e = (C.c_int * 9)()
+    _check(lib().tbt_ztoe1_dims(path.encode(), C.byref(nx), C.byref(ny), e))
+    nx, ny, ev = nx.value, ny.value, [int(v) for v in e]
+    m = ev[4]
+    nb = _gen.num_blocks(nx, ny)
+    g = np.empty((nb, m, m), np.complex128)
+    ea = np.ascontiguousarray(ev, dtype=np.int32)
+    ns, nr, nc = C.c_longlong(), C.c_longlong(), C.c_longlong()
+    nM = int(lib().tbtgen_margin_lengths(nx, ny, ea.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ns), C.byref(nr),
+                                         C.byref(nc)))
+    arrs = [np.empty(max(n, 1), np.complex128) for n in (ns.value, nr.value, nc.value, nM * nM)]
+    _check(lib().tbt_ztoe1_read(path.encode(), g.ctypes.data_as(dp), *[a.ctypes.data_as(dp) for a in arrs]))
+    margin = None
+    if nM > 0:
+        margin = Margin(ev, arrs[0][:ns.value], arrs[1][:nr.value], arrs[2][:nc.value], arrs[3][:nM * nM])
+    return ToeplitzRep(nx, ny, m, g, None, margin)
 
 
 def dist_unique_id() -> bytes:
