@@ -208,6 +208,14 @@ void memsetSync(void* dst, int value, size_t bytes, cudaStream_t s) {
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+bool stagedE2E() {  // TBT_E2E=staged: pinned host buffers through explicit copies, not zero-copy
+  static const bool on = [] {
+    const char* e = getenv("TBT_E2E");
+    return e && std::string(e) == "staged";
+  }();
+  return on;
+}
+
 bool poisonBuffers() {
   static const bool on = [] {
     const char* e = getenv("TBT_POISON");
@@ -609,7 +617,7 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
       return;
     }
     if (where == TBT_HOST && nrhs == 1 && !c.dist && c.persistent && persistentSupported(c) && !c.timeBinprod &&
-        isPinned(xin) && isPinned(yout)) {
+        isPinned(xin) && isPinned(yout) && !stagedE2E()) {
       // Zero-copy: the persistent kernel reads x and writes y in pinned host
       // memory over PCIe/C2C itself, overlapping both transfers with the
       // HBM spectrum stream instead of serialising two memcpys around it.

@@ -275,7 +275,8 @@ void marginDiagonal(const Ctx& c, std::vector<double2>& d);          // appends 
 void schurSolve(Ctx& c, const double2* b, double2* x, int p, const tbt_gmres_opts& o, std::vector<int>& iterations,
                 std::vector<double>& residual);
 std::vector<double2> twiddleTable(int n);                           // api.cu
-bool poisonBuffers();                                               // api.cu: TBT_POISON=1
+bool poisonBuffers();
+bool stagedE2E();                                               // api.cu: TBT_POISON=1
 void uploadSync(void* dst, const void* src, size_t bytes, cudaStream_t s);  // api.cu
 void memsetSync(void* dst, int value, size_t bytes, cudaStream_t s);        // api.cu
 

@@ -24,3 +24,21 @@ for label, xh, yh in [("pinned", torch.from_numpy(x.copy()).pin_memory(), torch.
     dt = (time.perf_counter() - t0) / n
     err = np.linalg.norm(yh.numpy() - ref) / np.linalg.norm(ref)
     print(f"{label}: {dt*1e6:.1f} us per e2e apply ({1/dt:.0f}/s), rel diff vs staged {err:.1e}")
+
+# Pure transfer cost of one step's vectors (pinned, CUDA events).
+xd = torch.empty(cfg.n, dtype=torch.complex128, device="cuda")
+xp = torch.from_numpy(x.copy()).pin_memory()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    for _ in range(5):
+        xd.copy_(xp, non_blocking=True)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(s)
+    for _ in range(100):
+        xd.copy_(xp, non_blocking=True)
+    e1.record(s)
+    for _ in range(100):
+        xp.copy_(xd, non_blocking=True)
+    e2.record(s)
+    e2.synchronize()
+print(f"pinned H2D {cfg.n * 16 / 1e6:.2f} MB: {e0.elapsed_time(e1) * 10:.1f} us, D2H: {e1.elapsed_time(e2) * 10:.1f} us")
