@@ -185,6 +185,30 @@ tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside,
 tbt_status tbt_save_spectra(tbt_ctx* ctx, const char* path);
 tbt_status tbt_load_spectra(tbt_ctx* ctx, const char* path);
 
+/* Row f4, contractions on solved currents (proj/src/postproc.cpp).
+ * portNetwork (:186-230): current is ld x p column-major (ld = n or
+ * n + n_m), feed_rows the port rows (ExcitationSet::feedRows), edge_len the
+ * feed edge length; y, z, s are p x p column-major: Y = I/len^2, Z = Y^-1
+ * (TBT_NUMERIC_ERROR when singular), S = (Z - Z0)(Z + Z0)^-1 with the
+ * sqrt(z0_j / z0_i) power-wave scaling. */
+tbt_status tbt_port_network(tbt_ctx* ctx, const double* current, long long ld,
+                            int p, const long long* feed_rows, double edge_len,
+                            const double* z0, double* y, double* z, double* s,
+                            int where);
+/* arrayFarfield / embeddedElementPatterns (:134-184): tensors_co/cx[c] are
+ * the component far-field tensors (ndir x e[c], column-major; NULL for
+ * empty components), dirs ndir x 3 (row-major unit vectors), parts placed
+ * as in array_model.cpp:218-228 with pitch dx, dy; current (n + n_m) x p,
+ * weights p x q (q = 1: one excitation; the identity: embedded element
+ * patterns); co, cx: ndir x q column-major, already scaled by -j k eta. */
+tbt_status tbt_array_farfield(tbt_ctx* ctx, const double* const* tensors_co,
+                              const double* const* tensors_cx, const int* e,
+                              int ndir, const double* dirs, double dx,
+                              double dy, double k, double eta,
+                              const double* current, int p,
+                              const double* weights, int q, double* co,
+                              double* cx, int where);
+
 /* Introspection for tests and the bench. */
 typedef struct {
   long long n;          /* nx*ny*m                                        */

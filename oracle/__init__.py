@@ -48,6 +48,10 @@ def lib() -> C.CDLL:
         L.orc_size.argtypes = [C.c_void_p]
         L.orc_schur.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                 ip, dp, C.c_char_p, C.c_int]
+        L.orc_port_network.argtypes = [dp, C.c_longlong, C.c_int, C.POINTER(C.c_longlong), C.c_double, dp, dp, dp,
+                                       dp]
+        L.orc_array_farfield.argtypes = [C.c_int, C.c_int, ip, C.POINTER(dp), C.POINTER(dp), C.c_int, dp, C.c_double,
+                                         C.c_double, C.c_double, C.c_double, dp, C.c_int, dp, C.c_int, dp, dp]
         L.orc_apply_a.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply.argtypes = [C.c_void_p, dp, dp]
         L.orc_apply_cols.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_int, C.c_int]
@@ -230,3 +234,45 @@ class Oracle:
         hists = [hist[c, :min(int(hlen[c]), hist_cap)].copy() for c in range(k)]
         return dict(x=x[:, 0] if vec else x, iterations=its.tolist(), residual=res.tolist(),
                     converged=conv.tolist(), history=hists)
+
+
+def port_network(current, feed_rows, edge_len, z0):
+    """portNetwork restated (postproc.cpp:186-230): dict(y, z, s)."""
+    cur = np.asfortranarray(current, dtype=np.complex128)
+    p = cur.shape[1]
+    feed = np.ascontiguousarray(feed_rows, dtype=np.int64)
+    z0 = np.ascontiguousarray(z0, dtype=np.float64)
+    out = [np.empty((p, p), np.complex128, order="F") for _ in range(3)]
+    st = lib().orc_port_network(_p(cur), cur.shape[0], p, feed.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                float(edge_len), z0.ctypes.data_as(dp), *[_p(o) for o in out])
+    if st == 1:
+        raise ValueError("portNetwork: bad arguments")
+    if st == 2:
+        raise ArithmeticError("portNetwork: singular admittance matrix")
+    return dict(y=out[0], z=out[1], s=out[2])
+
+
+def array_farfield(nx, ny, e, tensors, dirs, dx, dy, k, eta, current, weights):
+    """arrayFarfield restated for the columns of current @ weights: (co, cx)."""
+    e = np.ascontiguousarray(e, dtype=np.int32)
+    keep = []
+    pco, pcx = (dp * 9)(), (dp * 9)()
+    for c in range(9):
+        if e[c] == 0 or tensors[c] is None:
+            pco[c] = pcx[c] = None
+            continue
+        a = np.asfortranarray(tensors[c][0], dtype=np.complex128)
+        b = np.asfortranarray(tensors[c][1], dtype=np.complex128)
+        keep += [a, b]
+        pco[c], pcx[c] = _p(a), _p(b)
+    d = np.ascontiguousarray(dirs, dtype=np.float64)
+    cur = np.asfortranarray(current, dtype=np.complex128)
+    W = np.asfortranarray(weights, dtype=np.complex128)
+    if W.ndim == 1:
+        W = W[:, None]
+    ndir, q = d.shape[0], W.shape[1]
+    co = np.empty((ndir, q), np.complex128, order="F")
+    cx = np.empty_like(co)
+    lib().orc_array_farfield(nx, ny, e.ctypes.data_as(ip), pco, pcx, ndir, _p(d), dx, dy, k, eta, _p(cur),
+                             cur.shape[1], _p(W), q, _p(co), _p(cx))
+    return co, cx

@@ -961,3 +961,122 @@ extern "C" int orc_schur(const orc_op* op, const double* b, double* x, int ncols
   }
   return 0;
 }
+
+namespace {
+
+// Eigen PartialPivLU(...).inverse() restated: LU with partial pivoting,
+// then solve against the identity; returns the pivot ratio.
+double luInverse(const std::vector<cplx>& a, long n, std::vector<cplx>& inv) {
+  std::vector<cplx> lu = a;
+  std::vector<long> perm;
+  luPartialPivot(lu, n, perm);
+  double maxAbs = 0.0, minAbs = std::numeric_limits<double>::infinity();
+  for (long i = 0; i < n; ++i) {
+    maxAbs = std::max(maxAbs, std::abs(lu[i * n + i]));
+    minAbs = std::min(minAbs, std::abs(lu[i * n + i]));
+  }
+  inv.assign(static_cast<size_t>(n) * n, cplx{0.0, 0.0});
+  for (long c = 0; c < n; ++c) {
+    cvec e(n, cplx{0.0, 0.0});
+    e[c] = 1.0;
+    luSolve(lu, perm, n, e);
+    std::copy(e.begin(), e.end(), inv.begin() + c * n);
+  }
+  return minAbs / (maxAbs > 0 ? maxAbs : 1.0);
+}
+
+}  // namespace
+
+// portNetwork (postproc.cpp:186-230). Returns 0, 1 (user) or 2 (singular Y).
+extern "C" int orc_port_network(const double* current, long long ld, int p, const long long* feed, double len,
+                                const double* z0, double* y, double* z, double* s) {
+  if (!(len > 0.0) || p < 1) return 1;
+  for (int i = 0; i < p; ++i)
+    if (!(z0[i] > 0.0) || feed[i] < 0 || feed[i] >= ld) return 1;
+  const cplx* cur = reinterpret_cast<const cplx*>(current);
+  std::vector<cplx> Y(static_cast<size_t>(p) * p);
+  const double inv = 1.0 / len;
+  for (int c = 0; c < p; ++c)
+    for (int i = 0; i < p; ++i) Y[c * p + i] = inv * cur[feed[i] + c * ld] * inv;
+  std::vector<cplx> Z;
+  if (!(luInverse(Y, p, Z) > 1e-14)) return 2;
+  std::vector<cplx> zm = Z, zp = Z, zpi;
+  for (int i = 0; i < p; ++i) {
+    zm[i * p + i] -= z0[i];
+    zp[i * p + i] += z0[i];
+  }
+  luInverse(zp, p, zpi);
+  std::vector<cplx> S(static_cast<size_t>(p) * p);
+  for (int j = 0; j < p; ++j)
+    for (int i = 0; i < p; ++i) {
+      cplx acc{0.0, 0.0};
+      for (int k = 0; k < p; ++k) acc += zm[k * p + i] * zpi[j * p + k];
+      S[j * p + i] = acc * std::sqrt(z0[j] / z0[i]);
+    }
+  std::memcpy(y, Y.data(), Y.size() * sizeof(cplx));
+  std::memcpy(z, Z.data(), Z.size() * sizeof(cplx));
+  std::memcpy(s, S.data(), S.size() * sizeof(cplx));
+  return 0;
+}
+
+// arrayFarfield (postproc.cpp:134-170) for the q columns of current * W
+// (q = 1: one excitation; W = I: embeddedElementPatterns, :172-184). Parts
+// in the order and at the offsets of array_model.cpp:218-228.
+extern "C" int orc_array_farfield(int nx, int ny, const int* e, const double* const* tco, const double* const* tcx,
+                                  int ndir, const double* dirs, double dx, double dy, double k, double eta,
+                                  const double* current, int p, const double* weights, int q, double* co,
+                                  double* cx) {
+  struct Part {
+    int comp;
+    long start;
+    double ox, oy;
+  };
+  std::vector<Part> parts;
+  long row = 0;
+  auto place = [&](int cmp, double ox, double oy) {
+    parts.push_back({cmp, row, ox, oy});
+    row += e[cmp - 1];
+  };
+  for (int r = 1; r <= ny; ++r)
+    for (int c = 1; c <= nx; ++c) place(5, (c - 1) * dx, (r - 1) * dy);
+  for (int r = 1; r <= ny; ++r) place(2, 0.0, (r - 1) * dy);
+  for (int r = 1; r <= ny; ++r) place(8, (nx - 1) * dx, (r - 1) * dy);
+  for (int c = 1; c <= nx; ++c) place(6, (c - 1) * dx, (ny - 1) * dy);
+  for (int c = 1; c <= nx; ++c) place(4, (c - 1) * dx, 0.0);
+  place(3, 0.0, (ny - 1) * dy);
+  place(9, (nx - 1) * dx, (ny - 1) * dy);
+  place(1, 0.0, 0.0);
+  place(7, (nx - 1) * dx, 0.0);
+  const long ntot = row;
+  const cplx* cur = reinterpret_cast<const cplx*>(current);
+  const cplx* W = reinterpret_cast<const cplx*>(weights);
+  cplx* CO = reinterpret_cast<cplx*>(co);
+  cplx* CX = reinterpret_cast<cplx*>(cx);
+  const cplx front(0.0, -k * eta);
+  for (int j = 0; j < q; ++j) {
+    cvec comb(ntot, cplx{0.0, 0.0});  // current * excitation (:145)
+    for (int c = 0; c < p; ++c)
+      for (long r = 0; r < ntot; ++r) comb[r] += cur[r + c * ntot] * W[c + static_cast<long>(j) * p];
+    for (int i = 0; i < ndir; ++i) {
+      cplx fco{0.0, 0.0}, fcx{0.0, 0.0};
+      const double* d = dirs + 3 * i;
+      for (const Part& pt : parts) {
+        const int n = e[pt.comp - 1];
+        if (n == 0) continue;
+        const cplx* Tco = reinterpret_cast<const cplx*>(tco[pt.comp - 1]);
+        const cplx* Tcx = reinterpret_cast<const cplx*>(tcx[pt.comp - 1]);
+        cplx sco{0.0, 0.0}, scx{0.0, 0.0};
+        for (int t = 0; t < n; ++t) {
+          sco += Tco[i + static_cast<long>(t) * ndir] * comb[pt.start + t];
+          scx += Tcx[i + static_cast<long>(t) * ndir] * comb[pt.start + t];
+        }
+        const cplx phase = std::polar(1.0, k * (d[0] * pt.ox + d[1] * pt.oy));
+        fco += phase * sco;
+        fcx += phase * scx;
+      }
+      CO[i + static_cast<long>(j) * ndir] = front * fco;
+      CX[i + static_cast<long>(j) * ndir] = front * fcx;
+    }
+  }
+  return 0;
+}

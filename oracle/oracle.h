@@ -99,6 +99,14 @@ int orc_gmres(const orc_op* op, const double* b, double* x, int ncols,
 int orc_schur(const orc_op* op, const double* b, double* x, int ncols, double tol, int max_iter, int restart,
               int precondition, int nthreads, int* iterations, double* residual, char* err, int errcap);
 
+/* portNetwork (postproc.cpp:186-230) and arrayFarfield /
+ * embeddedElementPatterns (:134-184), restated for row f4. */
+int orc_port_network(const double* current, long long ld, int p, const long long* feed, double len,
+                     const double* z0, double* y, double* z, double* s);
+int orc_array_farfield(int nx, int ny, const int* e, const double* const* tco, const double* const* tcx, int ndir,
+                       const double* dirs, double dx, double dy, double k, double eta, const double* current, int p,
+                       const double* weights, int q, double* co, double* cx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,9 @@ SIGNATURES = {
     "tbt_ztoe1_read": (C.c_int, [C.c_char_p, dp, dp, dp, dp, dp]),
     "tbt_save_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
     "tbt_load_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "tbt_port_network": (C.c_int, [C.c_void_p, dp, C.c_longlong, C.c_int, llp, C.c_double, dp, dp, dp, dp, C.c_int]),
+    "tbt_array_farfield": (C.c_int, [C.c_void_p, C.POINTER(dp), C.POINTER(dp), ip, C.c_int, dp, C.c_double,
+                                     C.c_double, C.c_double, C.c_double, dp, C.c_int, dp, C.c_int, dp, dp, C.c_int]),
     "tbt_get_info": (C.c_int, [C.c_void_p, C.POINTER(TbtInfo)]),
     "tbt_get_spectrum_bin": (C.c_int, [C.c_void_p, C.c_longlong, dp]),
     "tbt_bench_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, dp, dp]),

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -874,6 +875,126 @@ tbt_status tbt_load_spectra(tbt_ctx* h, const char* path) {
     c.haveGenerators = false;
     c.havePrecompute = true;
     refreshDiagonal(c, nullptr);
+  });
+}
+
+namespace {
+// Device copy of a host (or device) input; owns the allocation when copied.
+struct In {
+  const void* dev = nullptr;
+  void* own = nullptr;
+  In(const void* src, size_t bytes, int where, cudaStream_t s) {
+    if (!src || bytes == 0) return;
+    if (where == TBT_DEVICE) {
+      dev = src;
+      return;
+    }
+    TBT_CUDA_CHECK(cudaMalloc(&own, bytes));
+    uploadSync(own, src, bytes, s);
+    dev = own;
+  }
+  ~In() {
+    if (own) cudaFree(own);
+  }
+};
+struct Out {
+  void* dev = nullptr;
+  void* own = nullptr;
+  void* host = nullptr;
+  size_t bytes = 0;
+  Out(void* dst, size_t b, int where) : bytes(b) {
+    if (!dst) return;
+    if (where == TBT_DEVICE) {
+      dev = dst;
+      return;
+    }
+    TBT_CUDA_CHECK(cudaMalloc(&own, std::max<size_t>(b, 16)));
+    dev = own;
+    host = dst;
+  }
+  void fetch(cudaStream_t s) {
+    if (host) TBT_CUDA_CHECK(cudaMemcpyAsync(host, own, bytes, cudaMemcpyDeviceToHost, s));
+  }
+  ~Out() {
+    if (own) cudaFree(own);
+  }
+};
+}  // namespace
+
+tbt_status tbt_port_network(tbt_ctx* h, const double* current, long long ld, int p, const long long* feed_rows,
+                            double edge_len, const double* z0, double* y, double* z, double* s, int where) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && current && feed_rows && z0 && y && z && s, "tbt_port_network: null argument");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(p >= 1 && ld >= 1, "tbt_port_network: bad sizes");
+    TBT_USER_CHECK(edge_len > 0.0, "portNetwork: feed edge length must be positive");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    std::vector<double> z0h(p);
+    std::vector<long long> fh(p);
+    if (where == TBT_HOST) {
+      std::memcpy(z0h.data(), z0, p * sizeof(double));
+      std::memcpy(fh.data(), feed_rows, p * sizeof(long long));
+    } else {
+      TBT_CUDA_CHECK(cudaMemcpy(z0h.data(), z0, p * sizeof(double), cudaMemcpyDeviceToHost));
+      TBT_CUDA_CHECK(cudaMemcpy(fh.data(), feed_rows, p * sizeof(long long), cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < p; ++i) {  // postproc.cpp:191-193
+      TBT_USER_CHECK(z0h[i] > 0.0, "portNetwork: reference impedances must be positive");
+      TBT_USER_CHECK(fh[i] >= 0 && fh[i] < ld, "portNetwork: feed row outside the current vector");
+    }
+    cudaStream_t st = c.stream;
+    In dCur(current, static_cast<size_t>(ld) * p * sizeof(double2), where, st);
+    In dFeed(fh.data(), p * sizeof(long long), TBT_HOST, st);
+    In dZ0(z0h.data(), p * sizeof(double), TBT_HOST, st);
+    const size_t pp = static_cast<size_t>(p) * p * sizeof(double2);
+    Out oy(y, pp, where), oz(z, pp, where), os(s, pp, where);
+    portNetwork(c, static_cast<const double2*>(dCur.dev), ld, p, static_cast<const long long*>(dFeed.dev), edge_len,
+                static_cast<const double*>(dZ0.dev), static_cast<double2*>(oy.dev), static_cast<double2*>(oz.dev),
+                static_cast<double2*>(os.dev));
+    oy.fetch(st);
+    oz.fetch(st);
+    os.fetch(st);
+    TBT_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+tbt_status tbt_array_farfield(tbt_ctx* h, const double* const* tensors_co, const double* const* tensors_cx,
+                              const int* e, int ndir, const double* dirs, double dx, double dy, double k, double eta,
+                              const double* current, int p, const double* weights, int q, double* co, double* cx,
+                              int where) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && tensors_co && tensors_cx && e && dirs && current && weights && co && cx,
+                   "tbt_array_farfield: null argument");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(ndir >= 1 && p >= 1 && q >= 1, "tbt_array_farfield: bad sizes");
+    TBT_USER_CHECK(e[4] == c.m, "arrayFarfield: e[4] must equal the element basis size");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    const long long ntot = static_cast<long long>(c.nx) * c.ny * e[4] +
+                           static_cast<long long>(c.ny) * (e[1] + e[7]) + static_cast<long long>(c.nx) * (e[5] + e[3]) +
+                           e[2] + e[8] + e[0] + e[6];
+    std::vector<std::unique_ptr<In>> keep;
+    const double2* tco[9];
+    const double2* tcx[9];
+    for (int i = 0; i < 9; ++i) {
+      TBT_USER_CHECK(e[i] == 0 || (tensors_co[i] && tensors_cx[i]), "arrayFarfield: missing component tensor");
+      const size_t b = static_cast<size_t>(ndir) * e[i] * sizeof(double2);
+      keep.emplace_back(new In(tensors_co[i], b, where, st));
+      tco[i] = static_cast<const double2*>(keep.back()->dev);
+      keep.emplace_back(new In(tensors_cx[i], b, where, st));
+      tcx[i] = static_cast<const double2*>(keep.back()->dev);
+    }
+    In dDirs(dirs, static_cast<size_t>(ndir) * 3 * sizeof(double), where, st);
+    In dCur(current, static_cast<size_t>(ntot) * p * sizeof(double2), where, st);
+    In dW(weights, static_cast<size_t>(p) * q * sizeof(double2), where, st);
+    const size_t ob = static_cast<size_t>(ndir) * q * sizeof(double2);
+    Out oco(co, ob, where), ocx(cx, ob, where);
+    arrayFarfield(c, tco, tcx, e, ndir, static_cast<const double*>(dDirs.dev), dx, dy, k, eta,
+                  static_cast<const double2*>(dCur.dev), ntot, p, static_cast<const double2*>(dW.dev), q,
+                  static_cast<double2*>(oco.dev), static_cast<double2*>(ocx.dev));
+    oco.fetch(st);
+    ocx.fetch(st);
+    TBT_CUDA_CHECK(cudaStreamSynchronize(st));
   });
 }
 

@@ -265,6 +265,13 @@ void readZtoe1(const std::string& path, Ztoe1Data& out);
 void saveSpectra(Ctx& c, const std::string& path);
 void loadSpectra(Ctx& c, const std::string& path);
 
+// postproc.cu (row f4), device pointers.
+void portNetwork(Ctx& c, const double2* current, long long ldc, int p, const long long* feedDev, double len,
+                 const double* z0Dev, double2* y, double2* z, double2* s);
+void arrayFarfield(Ctx& c, const double2* const* tco, const double2* const* tcx, const int* e, int ndir,
+                   const double* dirsDev, double dx, double dy, double k, double eta, const double2* current,
+                   long long ntot, int p, const double2* W, int q, double2* co, double2* cx);
+
 // margin.cu
 void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, const double2* bcorner,
                const double2* C);

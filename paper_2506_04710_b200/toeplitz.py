@@ -325,6 +325,63 @@ class ToeplitzMatvec:
         return SolveResult(x[:, 0] if vec else x, res.tolist(), its.tolist(), "schur", conv.tolist(), [], 0)
 
 
+
+# -- row f4: contractions on solved currents (postproc.cpp) ----------------
+def port_network(op: "ToeplitzMatvec", current, feed_rows, edge_len: float, z0) -> dict:
+    """portNetwork (postproc.cpp:186-230) on the device: Y = I/len^2 from the
+    port rows of the solution, Z = Y^-1, power-wave S. dict(y, z, s)."""
+    cur = np.asfortranarray(current, dtype=np.complex128)
+    p = cur.shape[1]
+    feed = np.ascontiguousarray(feed_rows, dtype=np.int64)
+    z0 = np.ascontiguousarray(z0, dtype=np.float64)
+    if feed.size != p or z0.size != p:
+        raise UserError("portNetwork: need one feed row and one Z0 per port")
+    out = [np.empty((p, p), np.complex128, order="F") for _ in range(3)]
+    _check(lib().tbt_port_network(op._h, cur.ctypes.data_as(dp), cur.shape[0], p,
+                                  feed.ctypes.data_as(C.POINTER(C.c_longlong)), float(edge_len), z0.ctypes.data_as(dp),
+                                  *[o.ctypes.data_as(dp) for o in out], TBT_HOST))
+    return dict(y=out[0], z=out[1], s=out[2])
+
+
+def tarc(s, a) -> float:
+    """Total active reflection coefficient |S a| / |a| (postproc.cpp:232-236)."""
+    a = np.asarray(a, dtype=np.complex128)
+    an = np.linalg.norm(a)
+    if an == 0.0:
+        raise UserError("tarc: zero excitation")
+    return float(np.linalg.norm(np.asarray(s) @ a) / an)
+
+
+def array_farfield(op: "ToeplitzMatvec", tensors, e, dirs, dx: float, dy: float, k: float, eta: float, current,
+                   weights):
+    """arrayFarfield (postproc.cpp:134-170) for the columns of current @ weights
+    on the device; weights = identity gives embeddedElementPatterns
+    (:172-184). tensors[c] = (co, cx), each ndir x e[c], or None. Returns
+    (co, cx), ndir x q."""
+    ea = np.ascontiguousarray(e, dtype=np.int32)
+    keep = []
+    pco, pcx = (dp * 9)(), (dp * 9)()
+    for c in range(9):
+        if ea[c] == 0 or tensors[c] is None:
+            pco[c] = pcx[c] = None
+            continue
+        a = np.asfortranarray(tensors[c][0], dtype=np.complex128)
+        b = np.asfortranarray(tensors[c][1], dtype=np.complex128)
+        keep += [a, b]
+        pco[c], pcx[c] = a.ctypes.data_as(dp), b.ctypes.data_as(dp)
+    d = np.ascontiguousarray(dirs, dtype=np.float64)
+    cur = np.asfortranarray(current, dtype=np.complex128)
+    W = np.asarray(weights, dtype=np.complex128)
+    W = np.asfortranarray(W[:, None] if W.ndim == 1 else W)
+    ndir, q = d.shape[0], W.shape[1]
+    co = np.empty((ndir, q), np.complex128, order="F")
+    cx = np.empty_like(co)
+    _check(lib().tbt_array_farfield(op._h, pco, pcx, ea.ctypes.data_as(C.POINTER(C.c_int)), ndir, d.ctypes.data_as(dp),
+                                    dx, dy, k, eta, cur.ctypes.data_as(dp), cur.shape[1], W.ctypes.data_as(dp), q,
+                                    co.ctypes.data_as(dp), cx.ctypes.data_as(dp), TBT_HOST))
+    return co, cx
+
+
 def read_ztoe1(path: str) -> ToeplitzRep:
     """A reference ZTOE1 block cache (Sparse mode) as a ToeplitzRep with its
     margin data (host-side parse, csrc/io.cu; row f3)."""
