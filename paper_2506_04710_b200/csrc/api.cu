@@ -943,12 +943,24 @@ tbt_status tbt_port_network(tbt_ctx* h, const double* current, long long ld, int
       TBT_USER_CHECK(fh[i] >= 0 && fh[i] < ld, "portNetwork: feed row outside the current vector");
     }
     cudaStream_t st = c.stream;
-    In dCur(current, static_cast<size_t>(ld) * p * sizeof(double2), where, st);
+    // Host input: only the p port rows travel (ExcitationSet::feedRows).
+    std::vector<double2> rows;
+    long long ldUse = ld;
+    if (where == TBT_HOST) {
+      rows.resize(static_cast<size_t>(p) * p);
+      const double2* cur = reinterpret_cast<const double2*>(current);
+      for (int col = 0; col < p; ++col)
+        for (int i = 0; i < p; ++i) rows[static_cast<size_t>(col) * p + i] = cur[fh[i] + col * ld];
+      for (int i = 0; i < p; ++i) fh[i] = i;
+      ldUse = p;
+    }
+    In dCur(where == TBT_HOST ? static_cast<const void*>(rows.data()) : current,
+            static_cast<size_t>(ldUse) * p * sizeof(double2), TBT_HOST == where ? TBT_HOST : where, st);
     In dFeed(fh.data(), p * sizeof(long long), TBT_HOST, st);
     In dZ0(z0h.data(), p * sizeof(double), TBT_HOST, st);
     const size_t pp = static_cast<size_t>(p) * p * sizeof(double2);
     Out oy(y, pp, where), oz(z, pp, where), os(s, pp, where);
-    portNetwork(c, static_cast<const double2*>(dCur.dev), ld, p, static_cast<const long long*>(dFeed.dev), edge_len,
+    portNetwork(c, static_cast<const double2*>(dCur.dev), ldUse, p, static_cast<const long long*>(dFeed.dev), edge_len,
                 static_cast<const double*>(dZ0.dev), static_cast<double2*>(oy.dev), static_cast<double2*>(oz.dev),
                 static_cast<double2*>(os.dev));
     oy.fetch(st);

@@ -106,6 +106,74 @@ __global__ void luSolveCols(const double2* __restrict__ LU, const int* __restric
 }
 
 
+// The whole factorisation in one CTA (small n): the same pivot rule and
+// update order as luPivot / luUpdate, barriers instead of launches.
+__global__ void __launch_bounds__(1024) luFactorSmall(double2* __restrict__ S, int n, int* __restrict__ perm) {
+  __shared__ double bestV[1024];
+  __shared__ int bestI[1024];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      const double2 v = S[i + static_cast<long long>(k) * n];
+      const double a = hypot(v.x, v.y);
+      if (a > bv) {
+        bv = a;
+        bi = i;
+      }
+    }
+    bestV[threadIdx.x] = bv;
+    bestI[threadIdx.x] = bi;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+      if (threadIdx.x < off) {
+        const double ov = bestV[threadIdx.x + off];
+        const int oi = bestI[threadIdx.x + off];
+        if (ov > bestV[threadIdx.x] || (ov == bestV[threadIdx.x] && oi < bestI[threadIdx.x])) {
+          bestV[threadIdx.x] = ov;
+          bestI[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const int p = bestI[0];
+    if (p != k && p < n) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const long long a = k + static_cast<long long>(j) * n, b = p + static_cast<long long>(j) * n;
+        const double2 t = S[a];
+        S[a] = S[b];
+        S[b] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    const double2 piv = S[k + static_cast<long long>(k) * n];
+    if (!(piv.x == 0.0 && piv.y == 0.0)) {
+      const double d = piv.x * piv.x + piv.y * piv.y;
+      const double2 inv = make_double2(piv.x / d, -piv.y / d);
+      for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+        const long long a = i + static_cast<long long>(k) * n;
+        S[a] = cmul(S[a], inv);
+      }
+    }
+    __syncthreads();
+    const int m = n - k - 1;
+    for (int o = threadIdx.x; o < m * m; o += blockDim.x) {
+      const int i = k + 1 + o % m, j = k + 1 + o / m;
+      const double2 l = S[i + static_cast<long long>(k) * n], u = S[k + static_cast<long long>(j) * n];
+      double2& sv = S[i + static_cast<long long>(j) * n];
+      sv = csub(sv, cmul(l, u));
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 }  // namespace dense
 }  // namespace tbt

@@ -153,9 +153,13 @@ double luInvert(double2* M, double2* dst, int p, cudaStream_t s) {
   std::vector<int> id(p);
   for (int i = 0; i < p; ++i) id[i] = i;
   uploadSync(perm.p, id.data(), p * sizeof(int), s);
-  for (int k = 0; k < p; ++k) {
-    dense::luPivot<<<1, 256, 0, s>>>(M, p, k, perm.as<int>());
-    if (k + 1 < p) dense::luUpdate<<<gridFor(static_cast<long long>(p - k - 1) * (p - k - 1)), 256, 0, s>>>(M, p, k);
+  if (p <= 512) {  // one CTA, barriers between steps
+    dense::luFactorSmall<<<1, 1024, 0, s>>>(M, p, perm.as<int>());
+  } else {
+    for (int k = 0; k < p; ++k) {
+      dense::luPivot<<<1, 256, 0, s>>>(M, p, k, perm.as<int>());
+      if (k + 1 < p) dense::luUpdate<<<gridFor(static_cast<long long>(p - k - 1) * (p - k - 1)), 256, 0, s>>>(M, p, k);
+    }
   }
   std::vector<double2> diag(p);
   TBT_CUDA_CHECK(cudaMemcpy2DAsync(diag.data(), sizeof(double2), M, (p + 1) * sizeof(double2), sizeof(double2), p,

@@ -292,11 +292,15 @@ void schurSolve(Ctx& c, const double2* b, double2* x, int p, const tbt_gmres_opt
       for (long long i = 0; i < nM; ++i) id[i] = static_cast<int>(i);
       uploadSync(perm.p, id.data(), nM * sizeof(int), s);
     }
-    for (int k = 0; k < nM; ++k) {
-      dense::luPivot<<<1, 256, 0, s>>>(S.as<double2>(), static_cast<int>(nM), k, perm.as<int>());
-      if (k + 1 < nM) {
-        const long long rest = (nM - k - 1) * (nM - k - 1);
-        dense::luUpdate<<<gridFor(rest), 256, 0, s>>>(S.as<double2>(), static_cast<int>(nM), k);
+    if (nM <= 512) {  // one CTA, barriers between steps
+      dense::luFactorSmall<<<1, 1024, 0, s>>>(S.as<double2>(), static_cast<int>(nM), perm.as<int>());
+    } else {
+      for (int k = 0; k < nM; ++k) {
+        dense::luPivot<<<1, 256, 0, s>>>(S.as<double2>(), static_cast<int>(nM), k, perm.as<int>());
+        if (k + 1 < nM) {
+          const long long rest = (nM - k - 1) * (nM - k - 1);
+          dense::luUpdate<<<gridFor(rest), 256, 0, s>>>(S.as<double2>(), static_cast<int>(nM), k);
+        }
       }
     }
     TBT_CUDA_CHECK(cudaGetLastError());
