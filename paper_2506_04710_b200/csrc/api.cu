@@ -622,7 +622,23 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
       // Zero-copy: the persistent kernel reads x and writes y in pinned host
       // memory over PCIe/C2C itself, overlapping both transfers with the
       // HBM spectrum stream instead of serialising two memcpys around it.
-      runApply1(c, xin, yout, withCorr);
+      // Phase A1 is PCIe-bound here: L2-prefetch up to ~3/4 of L2 worth of
+      // the spectrum meanwhile (TBT_ZC_L2_MB overrides, 0 disables).
+      static const long long zcBytes = [] {
+        const char* e = getenv("TBT_ZC_L2_MB");
+        return static_cast<long long>(e ? std::max(0, atoi(e)) : 96) << 20;
+      }();
+      c.zeroCopyL2Bytes = zcBytes;
+      c.zeroCopyStage = true;
+      try {
+        runApply1(c, xin, yout, withCorr);
+      } catch (...) {
+        c.zeroCopyL2Bytes = 0;
+        c.zeroCopyStage = false;
+        throw;
+      }
+      c.zeroCopyL2Bytes = 0;
+      c.zeroCopyStage = false;
       TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     } else if (where == TBT_HOST) {
       if (nrhs == 1) {

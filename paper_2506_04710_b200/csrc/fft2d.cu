@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "fft_reg.cuh"
+#include "ptx.cuh"
 #include "tbt_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -35,11 +36,12 @@ using fftreg::dftReg;
 using fftreg::Split;
 
 // One line of length N for one batch entry per thread (ii = butterfly
-// lane). All threads of the CTA call it (it contains __syncthreads);
-// `act` masks the work of lanes without a line.
+// lane). All threads of the line group call it: the group synchronises on
+// its own named barrier (bar, nthr threads), so line groups of a CTA do not
+// wait for each other; `act` masks the work of lanes without a line.
 template <int N, int BC, bool INV, class Src, class Snk>
-__device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, const double2* tw, Src src,
-                                        Snk snk) {
+__device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, const double2* tw, int bar, int nthr,
+                                        Src src, Snk snk) {
   using S = Split<N>;
   if constexpr (S::R2 == 1) {
     if (act && ii == 0) {
@@ -59,7 +61,10 @@ __device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, co
 #pragma unroll
       for (int r = 0; r < S::R1; ++r) st[(ii * S::R1 + r) * BC + b] = u[r];
     }
-    __syncthreads();
+    if (nthr > 0)
+      namedBarrier(bar, nthr);
+    else
+      __syncthreads();
     if (act && ii < S::R1) {
       double2 u[S::R2];
 #pragma unroll
@@ -74,7 +79,10 @@ __device__ __forceinline__ void lineFft(double2* st, int ii, int b, bool act, co
 #pragma unroll
       for (int r = 0; r < S::R2; ++r) snk(ii + r * S::R1, u[r]);
     }
-    __syncthreads();
+    if (nthr > 0)
+      namedBarrier(bar, nthr);
+    else
+      __syncthreads();
   }
 }
 
@@ -113,7 +121,7 @@ __global__ void __launch_bounds__(Fft2dCfg<N0, N1, BC>::NT) fft2dKernel(Fft2dArg
       const int i = base + g, r = k + CL * i;
       const bool act = bok && i < rowsLocal && r < a.ny;
       lineFft<N0, BC, false>(
-          st, ii, b, act, a.tw0,
+          st, ii, b, act, a.tw0, 1 + g, C::TPL % 32 == 0 ? C::TPL : 0,
           [&](int c) { return c < a.nx ? a.in[(static_cast<long long>(r) * a.nx + c) * B + bg] : zero; },
           [&](int s0, double2 v) {
             double2* dst = cl.map_shared_rank(xbuf, s0 % CL);
@@ -126,7 +134,7 @@ __global__ void __launch_bounds__(Fft2dCfg<N0, N1, BC>::NT) fft2dKernel(Fft2dArg
       const int j = base + g, s0 = k + CL * j;
       const bool act = bok && j < colsLocal;
       lineFft<N1, BC, false>(
-          st, ii, b, act, a.tw1,
+          st, ii, b, act, a.tw1, 1 + g, C::TPL % 32 == 0 ? C::TPL : 0,
           [&](int r) { return r < a.ny ? xbuf[(static_cast<long long>(j) * a.ny + r) * BC + b] : zero; },
           [&](int s1, double2 v) { a.out[(static_cast<long long>(s1) * a.L0 + s0) * B + bg] = v; });
     }
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(Fft2dCfg<N0, N1, BC>::NT) fft2dKernel(Fft2dArg
       const int j = base + g, s0 = k + CL * j;
       const bool act = bok && j < colsLocal;
       lineFft<N1, BC, true>(
-          st, ii, b, act, a.tw1,
+          st, ii, b, act, a.tw1, 1 + g, C::TPL % 32 == 0 ? C::TPL : 0,
           [&](int s1) { return a.in[(static_cast<long long>(s1) * a.L0 + s0) * B + bg]; },
           [&](int r, double2 v) {
             if (r < a.ny) {
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(Fft2dCfg<N0, N1, BC>::NT) fft2dKernel(Fft2dArg
       const int i = base + g, r = k + CL * i;
       const bool act = bok && i < rowsLocal && r < a.ny;
       lineFft<N0, BC, true>(
-          st, ii, b, act, a.tw0,
+          st, ii, b, act, a.tw0, 1 + g, C::TPL % 32 == 0 ? C::TPL : 0,
           [&](int s0) { return xbuf[(static_cast<long long>(i) * a.L0 + s0) * BC + b]; },
           [&](int c, double2 v) {
             if (c < a.nx) {

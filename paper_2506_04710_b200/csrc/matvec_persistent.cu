@@ -45,6 +45,8 @@ struct PArgs {
   long long npairs;
   const double2* x;
   double2* y;
+  double2* xStage;   // zero-copy x (host memory): A1 also writes it here
+  const double2* xc; // x as the correction terms read it (xStage or x)
   double2* xhat;
   double2* yhat;
   double2* T;  // [ny][L0][m] intermediate
@@ -72,6 +74,7 @@ struct PArgs {
   double2* tvec;          // [nPairs][M] pair vectors
   double2* ycorr;
   int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
+  long long l2Chunks;           // spectrum chunks per CTA bulk-prefetched into L2 at kernel start
   const int* skip;              // optional: the whole launch is a no-op when *skip != 0
   // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
   // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
@@ -197,7 +200,7 @@ __device__ void termItem(const PArgs& a, int p) {
   constexpr int QB = 8;  // projections loaded / reduced per batch
   const int lane = threadIdx.x & 31;
   const int4 info = *reinterpret_cast<const int4*>(a.pInfo + 4 * p);
-  const double2* xs = a.x + static_cast<long long>(info.y) * M;
+  const double2* xs = a.xc + static_cast<long long>(info.y) * M;
   double2 xv[KPL], acc[KPL];
 #pragma unroll
   for (int k = 0; k < KPL; ++k) {
@@ -329,6 +332,15 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     polS = policyEvictFirst();
     polX = policyEvictLast();
     if (a.prefetchAt == 0) prefetch();
+    // Zero-copy applies read x from host memory over PCIe in phase A1 while
+    // HBM idles: stream the chunks after the ring's into L2 meanwhile, so
+    // phase B starts on L2 hits (l2Chunks is 0 for device-resident x).
+    const long long pfEnd = pre + a.l2Chunks < total ? pre + a.l2Chunks : total;
+    for (long long it = pre; it < pfEnd; ++it) {
+      const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+      const int ch = static_cast<int>(it % C::NCH);
+      bulkPrefetchL2(a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK);
+    }
   }
 
   using W0 = WarpFft<N0>;
@@ -345,7 +357,13 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
         const int r = it / chunks0, b0 = (it % chunks0) * W0::WB;
         warpLineFft<N0, false>(
             slab, a.tw0,
-            [&](int c, int b) { return c < a.nx ? a.x[(static_cast<long long>(r) * a.nx + c) * M + b0 + b] : zero; },
+            [&](int c, int b) {
+              if (c >= a.nx) return zero;
+              const long long q = (static_cast<long long>(r) * a.nx + c) * M + b0 + b;
+              const double2 v = a.x[q];
+              if (a.xStage) a.xStage[q] = v;  // zero-copy: later readers use the HBM copy
+              return v;
+            },
             [&](int s0, int b, double2 v, int) { a.T[(static_cast<long long>(r) * a.L0 + s0) * M + b0 + b] = v; });
       }
     }
@@ -538,6 +556,8 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.npairs = c.npairs;
   a.x = x;
   a.y = y;
+  a.xStage = c.zeroCopyStage ? c.dXin : nullptr;
+  a.xc = a.xStage ? a.xStage : x;
   a.xhat = c.dXhat;
   a.yhat = c.dYhat;
   a.T = c.dT;
@@ -568,6 +588,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.ycorr = c.dYcorr;
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
   a.prefetchAt = c.prefetchAt;
+  a.l2Chunks = c.zeroCopyL2Bytes / (static_cast<long long>(smCount(c.device)) * C::CHUNK);
   a.skip = c.skipFlag;
   a.arnoldi = 0;
   if (gm) {

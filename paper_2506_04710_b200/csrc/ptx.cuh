@@ -66,6 +66,11 @@ __device__ __forceinline__ void bulkG2S(void* dst, const void* src, uint32_t byt
       : "memory");
 }
 
+// Bulk prefetch of global memory into L2 (bytes % 16 == 0, 16-byte aligned).
+__device__ __forceinline__ void bulkPrefetchL2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void namedBarrier(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
