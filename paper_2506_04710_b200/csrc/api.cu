@@ -168,6 +168,10 @@ void runApply1(Ctx& c, const double2* x, double2* y, bool withCorr) {
     applyInternal(c, x, y, 1, withCorr);
     return;
   }
+  if (c.usePdl && !c.zeroCopyStage) {  // direct launch: consecutive applies overlap launch and tail (PDL)
+    applyInternal(c, x, y, 1, withCorr);
+    return;
+  }
   if (!c.graphExec || c.graphX != x || c.graphY != y || c.graphCorr != withCorr) {
     c.dropGraph();
     cudaGraph_t graph;
@@ -323,6 +327,8 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       const char* genv = getenv("TBT_GMRES");
       c.forceUnfused = genv && std::string(genv) == "unfused";
       c.forceCols = genv && std::string(genv) == "cols";
+      const char* pdlEnv = getenv("TBT_PDL");
+      c.usePdl = !(pdlEnv && pdlEnv[0] == '0');  // default on; TBT_PDL=0 restores the cached graph
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinA));
       TBT_CUDA_CHECK(cudaEventCreate(&c.evBinB));
       c.binprodKernel = binprodVariant(c.m);

@@ -76,6 +76,7 @@ struct PArgs {
   int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
   long long l2Chunks;           // spectrum chunks per CTA bulk-prefetched into L2 at kernel start
   const int* skip;              // optional: the whole launch is a no-op when *skip != 0
+  int pdl;                      // launched with programmatic stream serialization
   // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
   // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
   int arnoldi;
@@ -342,6 +343,10 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
       bulkPrefetchL2(a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK);
     }
   }
+  // Programmatic dependent launch: the CTA started while the previous apply
+  // was finishing (its set-up and the spectrum prime above touch nothing the
+  // previous grid writes); wait for it before x / T / xhat / y are used.
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   using W0 = WarpFft<N0>;
   using W1 = WarpFft<N1>;
@@ -497,6 +502,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   }
   gridSync(a.barFlags, a, 3);
   stamp(a, 4);
+  // Past the last grid barrier: the next apply may launch its CTAs now.
+  if (a.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- phase C2: inverse row FFTs, keep nx points, scale, correction -> y
   if (!producer && !aux) {
     constexpr int RO = Split<N0>::R2 == 1 ? Split<N0>::R1 : Split<N0>::R2;  // outputs per lane
@@ -590,6 +597,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.prefetchAt = c.prefetchAt;
   a.l2Chunks = c.zeroCopyL2Bytes / (static_cast<long long>(smCount(c.device)) * C::CHUNK);
   a.skip = c.skipFlag;
+  a.pdl = (c.usePdl && !gm && !c.skipFlag) ? 1 : 0;
   a.arnoldi = 0;
   if (gm) {
     const long long chunk = (static_cast<long long>(gm->ne) * gm->m + smCount(c.device) - 1) / smCount(c.device);
@@ -608,11 +616,13 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   cfg.blockDim = dim3(kThreadsP);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = c.stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   TBT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   return true;
 }

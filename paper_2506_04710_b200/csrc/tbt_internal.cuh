@@ -110,7 +110,8 @@ struct Ctx {
   bool phaseTiming = false;
   int prefetchAt = 0;
   long long zeroCopyL2Bytes = 0;  // set around zero-copy launches: spectrum bytes to prefetch into L2
-  bool zeroCopyStage = false;     // set around zero-copy launches: stage x in dXin for the correction reads
+  bool zeroCopyStage = false;
+  bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)     // set around zero-copy launches: stage x in dXin for the correction reads
   const int* skipFlag = nullptr;           // device flag: persistent applies become no-ops when set                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
