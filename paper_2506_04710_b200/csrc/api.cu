@@ -363,6 +363,7 @@ void tbt_destroy(tbt_ctx* h) {
   c.dropGraph();
   distFree(c);
   marginFree(c);
+  clusterSmallFree(c);
   freeGmresWorkspace(c);
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);

@@ -126,6 +126,10 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
     applyDist(c, x, y, nrhs, withCorr);
     return;
   }
+  if (nrhs == 1 && clusterSmallSupported(c, 1)) {  // tiny operators: one cluster, one launch
+    launchClusterApply(c, x, y, withCorr);
+    return;
+  }
   if (nrhs == 1 && c.persistent && !c.timeBinprod && launchPersistentApply(c, x, y, withCorr)) return;
   if (c.fused2d && !c.forceMultiPass && applyFused(c, x, y, nrhs, withCorr)) return;
   const long long B = static_cast<long long>(nrhs) * c.m;

@@ -1043,6 +1043,21 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     const size_t smem = sizeof(int) * ncols;
 
     matvecs = 0;
+    if (ncols == 1 && !withMargin && clusterSmallSupported(c, R)) {
+      // Tiny operator: the whole solve in one cluster launch (cluster_small.cu).
+      launchClusterGmres(c, A, !useAOnly);
+      std::vector<GmresState> st(1);
+      TBT_CUDA_CHECK(cudaMemcpyAsync(st.data(), A.st, sizeof(GmresState), cudaMemcpyDeviceToHost, s));
+      hist.assign(static_cast<size_t>(2) * std::max(1, A.histCap), 0.0);
+      if (A.histCap > 0)
+        TBT_CUDA_CHECK(cudaMemcpyAsync(hist.data(), A.hist, sizeof(double) * 2 * A.histCap, cudaMemcpyDeviceToHost, s));
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+      int restarts = 0;  // matvecs: one per restart (history kinds 0 / 2) + one per inner iteration
+      for (int k = 0; k < std::min(st[0].histLen, A.histCap); ++k) restarts += hist[2 * k] != 1.0;
+      matvecs = restarts + st[0].iterations;
+      out = st;
+      return;
+    }
     if (colsLS)
       cols.init();
     else

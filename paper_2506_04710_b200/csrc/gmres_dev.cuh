@@ -53,6 +53,7 @@ struct GmresWs {
   void release();
 };
 GmresWs* gmresWorkspace(Ctx& c);
+void launchClusterGmres(Ctx& c, const GmresArgs& A, bool withCorr);  // cluster_small.cu
 
 namespace gmresdev {
 

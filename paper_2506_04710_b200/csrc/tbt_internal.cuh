@@ -182,6 +182,7 @@ struct Ctx {
   double2* dDiagInvA = nullptr;  // 1/diag(A), Jacobi of the A-only solves
 
   struct GmresWs* gmresWs = nullptr;
+  struct ClusterSmall* clusterSmall = nullptr;  // one-cluster apply / GMRES for tiny operators (cluster_small.cu)
 
   // Margin coupling B / B^T / C (margin.cu): nM margin unknowns stored as
   // neM = ceil(nM/m) zero-padded pseudo-elements after the ne elements.
@@ -267,6 +268,11 @@ struct Ztoe1Data {
 void readZtoe1(const std::string& path, Ztoe1Data& out);
 void saveSpectra(Ctx& c, const std::string& path);
 void loadSpectra(Ctx& c, const std::string& path);
+
+// cluster_small.cu: tiny operators (C1) on one 8-CTA cluster.
+bool clusterSmallSupported(const Ctx& c, int restart);
+void launchClusterApply(Ctx& c, const double2* x, double2* y, bool withCorr);
+void clusterSmallFree(Ctx& c);
 
 // postproc.cu (row f4), device pointers.
 void portNetwork(Ctx& c, const double2* current, long long ldc, int p, const long long* feedDev, double len,
