@@ -24,6 +24,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "gmres_dev.cuh"
 
@@ -58,8 +60,16 @@ struct CsArgs {
   // shared-memory carve (double2 offsets)
   int oSpec, oX, oXh, oYh, oYall, oV, oW, oXs, oB, oDinv, oS, oH, oG, oCs, oSn, oPart, oTot, oY;
   int oTw0, oTw1, oScr;  // twiddles, per-warp scratch (corrections / inverse partials)
+  int oBin;              // bin map copy (int4 per bin, 16 bytes like a double2)
+  unsigned long long* prof;  // optional: accumulated ns per section (CTA 0)
   int smemD2;
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct CsCtx {
   const CsArgs& a;
@@ -153,7 +163,7 @@ __device__ void clusterApply(CsCtx& c, const double2* vloc, bool withCorr) {
   c.cl.sync();
   for (int t = threadIdx.x; t < a.L * m; t += blockDim.x) {
     const int f = t / m, i = t % m;
-    const int4 bm = a.binMap[f];
+    const int4 bm = reinterpret_cast<const int4*>(c.at(a.oBin))[f];
     yall[t] = c.cl.map_shared_rank(yh, bm.x)[bm.y * m + i];
   }
   __syncthreads();
@@ -209,13 +219,37 @@ __device__ void clusterApply(CsCtx& c, const double2* vloc, bool withCorr) {
       const double2* W2 = (trans ? a.V : a.U) + static_cast<long long>(slot) * a.rank * m;
       const double2* xs = X + src * m;
       double2* o = wsum + (tgt - e0) * m;
-      for (int i = lane; i < m; i += 32) cfma(o[i], __ldg(a.D + slot * m + i), xs[i]);
-      for (int q = 0; q < a.rank; ++q) {
-        double2 pr = make_double2(0.0, 0.0);
-        for (int j = lane; j < m; j += 32) cfma(pr, __ldg(W + q * m + j), xs[j]);
-        pr = gmresdev::warpSum(pr);
-        for (int i = lane; i < m; i += 32) cfma(o[i], __ldg(W2 + q * m + i), pr);
+      // All of the term's U / V / d values a lane needs are loaded up front
+      // (one latency instead of one per projection); m <= 64, rank <= 8.
+      constexpr int QM = 8;
+      double2 wv[QM][2], w2v[QM][2], dv[2], xv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        const bool ok = i < m;
+        dv[h] = ok ? __ldg(a.D + slot * m + i) : make_double2(0.0, 0.0);
+        xv[h] = ok ? xs[i] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+          const bool oq = ok && q < a.rank;
+          wv[q][h] = oq ? __ldg(W + q * m + i) : make_double2(0.0, 0.0);
+          w2v[q][h] = oq ? __ldg(W2 + q * m + i) : make_double2(0.0, 0.0);
+        }
       }
+      double2 acc[2] = {cmul(dv[0], xv[0]), cmul(dv[1], xv[1])};
+#pragma unroll
+      for (int q = 0; q < QM; ++q) {
+        if (q >= a.rank) break;
+        double2 pr = make_double2(0.0, 0.0);
+        cfma(pr, wv[q][0], xv[0]);
+        cfma(pr, wv[q][1], xv[1]);
+        pr = gmresdev::warpSum(pr);
+        cfma(acc[0], w2v[q][0], pr);
+        cfma(acc[1], w2v[q][1], pr);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < m) o[lane + 32 * h] = cadd(o[lane + 32 * h], acc[h]);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < a.nloc; t += blockDim.x) {
@@ -229,14 +263,26 @@ __device__ void clusterApply(CsCtx& c, const double2* vloc, bool withCorr) {
 
 __device__ void loadSpectrum(CsCtx& c) {
   const CsArgs& a = c.a;
+  for (int t = threadIdx.x; t < a.L; t += blockDim.x) reinterpret_cast<int4*>(c.at(a.oBin))[t] = a.binMap[t];
   for (int t = threadIdx.x; t < a.L0; t += blockDim.x) c.at(a.oTw0)[t] = a.tw0[t];
   for (int t = threadIdx.x; t < a.L1; t += blockDim.x) c.at(a.oTw1)[t] = a.tw1[t];
   double2* spec = c.at(a.oSpec);
   const int mm = a.m * a.m;
-  for (int t = threadIdx.x; t < a.kp * mm; t += blockDim.x) {
-    const int lp = t / mm;
-    const int p = c.rank + CL * lp;
-    spec[t] = p < a.npairs ? a.S[static_cast<long long>(p) * mm + t % mm] : make_double2(0.0, 0.0);
+  // Batches of 8 independent loads per thread (one latency per batch).
+  const int total = a.kp * mm;
+  for (int t0 = threadIdx.x; t0 < total; t0 += 8 * blockDim.x) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * blockDim.x;
+      const int p = c.rank + CL * (t / mm);
+      v[u] = (t < total && p < a.npairs) ? __ldg(a.S + static_cast<long long>(p) * mm + t % mm) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t < total) spec[t] = v[u];
+    }
   }
   __syncthreads();
 }
@@ -344,7 +390,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
     int ncount = 0;
     for (int j = 0; j < R && !sStop; ++j) {
       const double2* vj = Vl + static_cast<size_t>(j) * nloc;
+      unsigned long long tp0 = gtime();
       clusterApply(c, vj, withCorr != 0);
+      unsigned long long tp1 = gtime();
       for (int t = threadIdx.x; t < nloc; t += blockDim.x) w[t] = cmul(y[t], dl[t]);
       __syncthreads();
       // Low-sync MGS: c_k = <v_k, w> (slot k), S_jk = <v_j, v_k> (slot j+1+k).
@@ -363,13 +411,34 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
         }
       }
       clusterSum(c, 2 * j + 1);
+      unsigned long long tp2 = gtime();
       for (int k = threadIdx.x; k < j; k += blockDim.x) Sm[j * lds + k] = tot[j + 1 + k];
       __syncthreads();
-      if (threadIdx.x == 0) {  // h = (I + L)^-1 c (forward substitution)
-        for (int i = 0; i <= j; ++i) {
-          double2 h = tot[i];
-          for (int k = 0; k < i; ++k) h = csub(h, cmul(Sm[i * lds + k], hcol[k]));
-          hcol[i] = h;
+      if (threadIdx.x < 32) {  // h = (I + L)^-1 c: column-oriented forward substitution on warp 0
+        constexpr int RPL = (gmresdev::RMAX + 31) / 32 + 1;
+        const int lane = threadIdx.x;
+        double2 hv[RPL];
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane + 32 * t;
+          hv[t] = i <= j ? tot[i] : make_double2(0.0, 0.0);
+        }
+        for (int k = 0; k < j; ++k) {
+          double2 hk = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int t = 0; t < RPL; ++t)
+            if (t == (k >> 5)) hk = hv[t];
+          hk = gmresdev::shfl2(hk, k & 31);
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int i = lane + 32 * t;
+            if (i > k && i <= j) hv[t] = csub(hv[t], cmul(Sm[i * lds + k], hk));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i <= j) hcol[i] = hv[t];
         }
       }
       __syncthreads();
@@ -380,6 +449,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
         w[t] = wv;
         nacc.x += wv.x * wv.x + wv.y * wv.y;
       }
+      unsigned long long tp3 = gtime();
       ctaPartial(c, nacc, 0, red);
       clusterSum(c, 1);
       const double hn = sqrt(tot[0].x);
@@ -424,6 +494,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
       ++histLen;
       ++iterations;
       ncount = j + 1;
+      if (a.prof && lead) {
+        const unsigned long long tp4 = gtime();
+        a.prof[0] += tp1 - tp0;
+        a.prof[1] += tp2 - tp1;
+        a.prof[2] += tp3 - tp2;
+        a.prof[3] += tp4 - tp3;
+        a.prof[4] += 1;
+      }
       __syncthreads();
     }
     // Back substitution and x += V y (:504-510); y coefficients in hcol.
@@ -524,6 +602,7 @@ bool buildArgs(Ctx& c, CsArgs& a, size_t& smemBytes) {
   a.oG = take(R + 1);
   a.oCs = take(R);
   a.oSn = take(R);
+  a.oBin = take(c.L);
   a.oTw0 = take(c.L0);
   a.oTw1 = take(c.L1);
   a.oScr = take(std::max<long long>(static_cast<long long>(CW) * 2 * a.nloc, static_cast<long long>(c.L1) * a.nloc));
@@ -538,7 +617,7 @@ bool buildArgs(Ctx& c, CsArgs& a, size_t& smemBytes) {
 // Whether the one-cluster path serves this context (tiny operators only).
 bool clusterSmallSupported(const Ctx& c, int restart) {
   if (c.dist || c.margin || c.forceMultiPass || c.timeBinprod) return false;
-  if (c.L > 256 || c.m > 64 || c.ne > 256 || c.npairs < 1) return false;
+  if (c.L > 256 || c.m > 64 || c.ne > 256 || c.npairs < 1 || c.rank > 8) return false;
   CsArgs a{};
   size_t base = 0;
   buildArgs(const_cast<Ctx&>(c), a, base);
@@ -600,6 +679,9 @@ void launchClusterGmres(Ctx& c, const GmresArgs& A, bool withCorr) {
   CsArgs a{};
   size_t smem = 0;
   buildArgs(c, a, smem);
+  static const bool prof = getenv("TBT_CLPROF") != nullptr;  // debug: per-section ns in dPhaseNs[24..28]
+  a.prof = prof ? c.dPhaseNs + 24 : nullptr;
+  if (prof) memsetSync(c.dPhaseNs + 24, 0, 5 * sizeof(unsigned long long), c.stream);
   a.binMap = cs.dBinMap;
   const int R = A.restart;
   a.oS = a.oV + (R + 1) * a.nloc;
@@ -613,6 +695,14 @@ void launchClusterGmres(Ctx& c, const GmresArgs& A, bool withCorr) {
   }
   clusterGmresKernel<<<CL, CT, smem, c.stream>>>(a, A, withCorr ? 1 : 0);
   TBT_CUDA_CHECK(cudaGetLastError());
+  if (prof) {
+    unsigned long long ns[5];
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    TBT_CUDA_CHECK(cudaMemcpy(ns, c.dPhaseNs + 24, sizeof(ns), cudaMemcpyDeviceToHost));
+    const double it = ns[4] > 0 ? static_cast<double>(ns[4]) : 1.0;
+    fprintf(stderr, "cluster gmres per iteration (us): apply %.2f dots %.2f subst+update %.2f norm+givens %.2f (%llu its)\n",
+            1e-3 * ns[0] / it, 1e-3 * ns[1] / it, 1e-3 * ns[2] / it, 1e-3 * ns[3] / it, ns[4]);
+  }
 }
 
 }  // namespace tbt
