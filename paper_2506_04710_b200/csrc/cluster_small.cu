@@ -76,21 +76,31 @@ struct CsCtx {
   double2* sm;
   cg::cluster_group cl;
   int rank;
+  int epoch = 0;  // which half of the double-buffered partials the next reduction uses
   __device__ double2* at(int off) const { return sm + off; }
+  __device__ double2* part() const { return sm + a.oPart + (epoch & 1) * 2 * (gmresdev::RMAX + 1); }
 };
 
-// Fixed-order cluster all-reduce of cnt partials (part[0..cnt) in every
-// CTA) into tot[0..cnt) in every CTA.
+// Fixed-order cluster all-reduce of cnt partials (part()[0..cnt) in every
+// CTA) into tot[0..cnt) in every CTA. The partials are double-buffered by
+// epoch, so one cluster barrier per reduction suffices: a CTA can only
+// overwrite this half again after the NEXT reduction's barrier, which every
+// CTA reaches after finishing its reads here.
 __device__ void clusterSum(CsCtx& c, int cnt) {
-  double2* part = c.at(c.a.oPart);
+  double2* part = c.part();
   double2* tot = c.at(c.a.oTot);
   c.cl.sync();
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    double2 t = make_double2(0.0, 0.0);
-    for (int r = 0; r < CL; ++r) t = cadd(t, c.cl.map_shared_rank(part, r)[i]);
+    double2 v[CL];  // all remote loads in flight, then the fixed-order sum
+#pragma unroll
+    for (int r = 0; r < CL; ++r) v[r] = c.cl.map_shared_rank(part, r)[i];
+    double2 t = v[0];
+#pragma unroll
+    for (int r = 1; r < CL; ++r) t = cadd(t, v[r]);
     tot[i] = t;
   }
-  c.cl.sync();
+  __syncthreads();
+  ++c.epoch;
 }
 
 // CTA-level partial sum of v into part[slot] (fixed order).
@@ -102,7 +112,7 @@ __device__ void ctaPartial(CsCtx& c, double2 v, int slot, double2* red) {
   if (threadIdx.x == 0) {
     double2 t = red[0];
     for (int w = 1; w < CW; ++w) t = cadd(t, red[w]);
-    c.at(c.a.oPart)[slot] = t;
+    c.part()[slot] = t;
   }
 }
 
@@ -119,10 +129,17 @@ __device__ void clusterApply(CsCtx& c, const double2* vloc, bool withCorr) {
   const double2* tw1 = c.at(a.oTw1);
   // 1. All-gather the input slices (each CTA published vloc before).
   c.cl.sync();
-  for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
-    const int r = i / a.nloc;
-    const double2* src = c.cl.map_shared_rank(const_cast<double2*>(vloc), r);
-    X[i] = src[i - r * a.nloc];
+  for (int i0 = threadIdx.x; i0 < a.n; i0 += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      const int r = i / a.nloc;
+      v[u] = i < a.n ? c.cl.map_shared_rank(const_cast<double2*>(vloc), r)[i - r * a.nloc] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * blockDim.x < a.n) X[i0 + u * blockDim.x] = v[u];
   }
   __syncthreads();
   // 2. x^ for the own bins: slot s -> pair rank + CL*(s/2), bin f or g.
@@ -161,10 +178,20 @@ __device__ void clusterApply(CsCtx& c, const double2* vloc, bool withCorr) {
   }
   // 4. Every CTA gathers all bins' y^ (DSMEM).
   c.cl.sync();
-  for (int t = threadIdx.x; t < a.L * m; t += blockDim.x) {
-    const int f = t / m, i = t % m;
-    const int4 bm = reinterpret_cast<const int4*>(c.at(a.oBin))[f];
-    yall[t] = c.cl.map_shared_rank(yh, bm.x)[bm.y * m + i];
+  for (int t0 = threadIdx.x; t0 < a.L * m; t0 += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x;
+      v[u] = make_double2(0.0, 0.0);
+      if (t < a.L * m) {
+        const int4 bm = reinterpret_cast<const int4*>(c.at(a.oBin))[t / m];
+        v[u] = c.cl.map_shared_rank(yh, bm.x)[bm.y * m + t % m];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t0 + u * blockDim.x < a.L * m) yall[t0 + u * blockDim.x] = v[u];
   }
   __syncthreads();
   // 5. Inverse DFT for the own elements: partial rows per (output, s1) in
@@ -407,7 +434,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
           else
             for (int t = lane; t < nloc; t += 32) cfma_conj(acc, vj[t], vk[t]);
           acc = gmresdev::warpSum(acc);
-          if (lane == 0) c.at(a.oPart)[d] = acc;
+          if (lane == 0) c.part()[d] = acc;
         }
       }
       clusterSum(c, 2 * j + 1);
@@ -597,7 +624,7 @@ bool buildArgs(Ctx& c, CsArgs& a, size_t& smemBytes) {
   a.oW = take(a.nloc);
   a.oB = take(a.nloc);
   a.oDinv = take(a.nloc);
-  a.oPart = take(2 * (R + 1));
+  a.oPart = take(4 * (R + 1));  // two halves
   a.oTot = take(2 * (R + 1));
   a.oG = take(R + 1);
   a.oCs = take(R);
