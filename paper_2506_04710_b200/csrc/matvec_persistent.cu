@@ -119,12 +119,19 @@ __device__ __forceinline__ double2 shflXorP(double2 v, int off) {
 
 // Warp-level batched line FFT: WB batch entries per warp, LANES butterfly
 // lanes per entry (LANES * WB == 32). For N <= 16 each lane owns a line.
+// The slab between the two radix steps is padded: row ii1 of the first step
+// starts at ii1 * STR with STR = WB (mod 8), so a warp's first-step stores
+// (lanes over ii1 and b) fall into distinct 16-byte bank groups instead of
+// one group per ii1 (16-way conflicts at N = 128, 256 unpadded); the second
+// step's loads stay contiguous.
 template <int N>
 struct WarpFft {
   using S = Split<N>;
   static constexpr int LANES = S::R2 == 1 ? 1 : S::LANES;
   static constexpr int WB = 32 / LANES;
-  static constexpr int SLAB = S::R2 == 1 ? 0 : N * WB;  // double2 per warp
+  static constexpr int STR =
+      WB >= 8 ? S::R1 * WB : S::R1 * WB + ((WB - (S::R1 * WB) % 8) % 8 + 8) % 8;  // padded row stride
+  static constexpr int SLAB = S::R2 == 1 ? 0 : S::R2 * STR;  // double2 per warp
 };
 
 template <int N, bool INV, class Src, class Snk>
@@ -147,13 +154,13 @@ __device__ __forceinline__ void warpLineFft(double2* slab, const double2* tw, Sr
       for (int r = 0; r < S::R1; ++r) u[r] = src(ii + r * S::R2, b);
       dftReg<S::R1, INV>(u);
 #pragma unroll
-      for (int r = 0; r < S::R1; ++r) slab[(ii * S::R1 + r) * W::WB + b] = u[r];
+      for (int r = 0; r < S::R1; ++r) slab[ii * W::STR + r * W::WB + b] = u[r];
     }
     __syncwarp();
     if (ii < S::R1) {
       double2 u[S::R2];
 #pragma unroll
-      for (int r = 0; r < S::R2; ++r) u[r] = slab[(ii + r * S::R1) * W::WB + b];
+      for (int r = 0; r < S::R2; ++r) u[r] = slab[r * W::STR + ii * W::WB + b];
 #pragma unroll
       for (int r = 1; r < S::R2; ++r) {
         double2 w = __ldg(tw + r * ii);
