@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdio>
 #include <cstring>
 
 #include "gmres_dev.cuh"
@@ -1039,6 +1040,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     TBT_CUDA_CHECK(cudaMemsetAsync(A.H, 0, sizeof(double2) * ncols * (R + 1) * R, s));
     TBT_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * nall, s));
     A.dinv = o.precondition ? (useAOnly ? c.dDiagInvA : c.dDiagInv) : nullptr;
+    static const bool lsProf = getenv("TBT_LSPROF") != nullptr;  // debug: LS section timing (CTA 0)
+    A.prof = lsProf ? c.dPhaseNs + 24 : nullptr;
+    if (lsProf) memsetSync(c.dPhaseNs + 24, 0, 5 * sizeof(unsigned long long), s);
     if (A.dinv && c.dist) A.dinv += static_cast<long long>(c.myRow0) * c.nx * c.m;
     const size_t smem = sizeof(int) * ncols;
 
@@ -1169,6 +1173,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       matvecs += it;
     }
     out = st;
+    if (lsProf) {
+      unsigned long long ns[5];
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+      TBT_CUDA_CHECK(cudaMemcpy(ns, c.dPhaseNs + 24, sizeof(ns), cudaMemcpyDeviceToHost));
+      const double it = ns[4] > 0 ? static_cast<double>(ns[4]) : 1.0;
+      fprintf(stderr, "LS step per iteration (us): dots %.2f reduce %.2f subst+update %.2f normalize+givens %.2f (%llu)\n",
+              1e-3 * ns[0] / it, 1e-3 * ns[1] / it, 1e-3 * ns[2] / it, 1e-3 * ns[3] / it, ns[4]);
+    }
     hist.assign(static_cast<size_t>(2) * ncols * std::max(1, A.histCap), 0.0);
     if (A.histCap > 0)
       TBT_CUDA_CHECK(cudaMemcpy(hist.data(), A.hist, sizeof(double) * 2 * ncols * A.histCap, cudaMemcpyDeviceToHost));

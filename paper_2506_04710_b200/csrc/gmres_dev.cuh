@@ -30,6 +30,7 @@ struct GmresArgs {
   double2* V;       // [restart+1][ne*ncols*m]
   const double2* dinv;  // [ne*m] or null
   int j;            // Arnoldi column of this launch
+  unsigned long long* prof;  // optional (TBT_LSPROF): accumulated ns per LS section, CTA 0
 };
 
 // Device workspace of gmresSolve, cached in the context (gmres.cu).
@@ -211,6 +212,11 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
                           double2* scratch, double2* hcol, double2* sh, unsigned long long* bar) {
   const int run = A.st[0].cycleActive && !A.st[0].stopInner;
   if (!run) return;  // uniform over the grid
+  unsigned long long pt[5] = {0, 0, 0, 0, 0};
+  auto mark = [&](int k) {
+    if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt[k]));
+  };
+  mark(0);
   const int j = A.j;
   const int lds = A.restart + 1;
   const long long n = static_cast<long long>(A.ne) * A.m;
@@ -262,6 +268,7 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     }
   }
   gridBarrier(bar);
+  mark(1);
   // Grid totals: CTA d reduces dot d (c_0..c_j, then S_j0..S_j,j-1).
   const int ndots = 2 * j + 1;
   for (int d = blockIdx.x; d < ndots; d += gridDim.x) {
@@ -275,6 +282,7 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     }
   }
   gridBarrier(bar);
+  mark(2);
   // Stage the lower triangle rows 1..j of L (shared memory after cv).
   double2* sL = cv + RMAX + 1;  // packed rows: row i at i*(i-1)/2
   for (int q = threadIdx.x; q < j * (j + 1) / 2; q += blockDim.x) {
@@ -336,12 +344,22 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   }
   blockPartial(acc, scratch, partSlot(A, 0, 0));
   gridBarrier(bar);
+  mark(3);
   const double hn = sqrt(warpTotal(partSlot(A, 0, 0)).x);
   if (hn > 0.0) {
     double2* vout = A.V + static_cast<long long>(j + 1) * n + r0;
     for (int r = threadIdx.x; r < cnt; r += blockDim.x) vout[r] = make_double2(ws[r].x / hn, ws[r].y / hn);
   }
   if (blockIdx.x == 0) givensStep(A, 0, j, hn, hcol, sh);
+  if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t4;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t4));
+    A.prof[0] += pt[1] - pt[0];
+    A.prof[1] += pt[2] - pt[1];
+    A.prof[2] += pt[3] - pt[2];
+    A.prof[3] += t4 - pt[3];
+    A.prof[4] += 1;
+  }
 }
 
 // Dynamic shared memory (double2 count) the LS step needs for a row chunk.
