@@ -109,73 +109,72 @@ __global__ void marginScatter(const double2* __restrict__ ys, double2* __restric
 
 // B1/B2 per-bin product: hatMs[r][f][i][rhs] = sum_{c,k} G_r[f][i][c*m+k] hatY[f][c][rhs][k].
 // One warp per (r, f, i, rhs), lanes over the nx*m sources.
-__global__ void sideProd(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
-                         const double2* __restrict__ hatY, double2* __restrict__ out0, double2* __restrict__ out1,
-                         int Ly, int nx, int m, int K) {
-  const long long q = static_cast<long long>(nx) * m;
-  const long long items = static_cast<long long>(em0 + em1) * Ly * K;
-  (void)q;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
-       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const int rhs = static_cast<int>(w % K);
-    long long rest = w / K;
-    const int f = static_cast<int>(rest % Ly);
-    int i = static_cast<int>(rest / Ly);
-    const int r = i < em0 ? 0 : 1;
-    if (r == 1) i -= em0;
-    const int em = r == 0 ? em0 : em1;
-    const double2* G = (r == 0 ? g0 : g1) + (static_cast<long long>(f) * em + i) * q;
-    const double2* X = hatY + static_cast<long long>(f) * nx * K * m;
-    // Four independent accumulators over the source elements (loads in flight).
-    double2 a4[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                     make_double2(0.0, 0.0)};
-    for (int c = 0; c < nx; ++c) {
-      const double2* Gc = G + static_cast<long long>(c) * m;
-      const double2* Xc = X + (static_cast<long long>(c) * K + rhs) * m;
-      for (int k = lane; k < m; k += 32) cfma(a4[c & 3], Gc[k], Xc[k]);
-    }
-    double2 acc = cadd(cadd(a4[0], a4[1]), cadd(a4[2], a4[3]));
+// CTA-wide fixed-order sum (warp butterflies, then warps in order).
+__device__ __forceinline__ double2 ctaSum128(double2 v, double2* red) {
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-    }
-    if (lane == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
+  for (int off = 16; off >= 1; off >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
   }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double2 t = red[0];
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = cadd(t, red[w]);
+  return t;
+}
+
+// B1/B2 per-bin product: hatMs[r][f][i][rhs] = sum_{c,k} G_r[f][i][c*m+k] hatY[f][c][rhs][k].
+// One CTA per (r, f, i, rhs), threads over the nx*m sources.
+__global__ void __launch_bounds__(128) sideProd(const double2* __restrict__ g0, const double2* __restrict__ g1,
+                                                int em0, int em1, const double2* __restrict__ hatY,
+                                                double2* __restrict__ out0, double2* __restrict__ out1, int Ly,
+                                                int nx, int m, int K) {
+  __shared__ double2 red[4];
+  const int q = nx * m;
+  const long long w = blockIdx.x;
+  const int rhs = static_cast<int>(w % K);
+  const long long rest = w / K;
+  const int f = static_cast<int>(rest % Ly);
+  int i = static_cast<int>(rest / Ly);
+  const int r = i < em0 ? 0 : 1;
+  if (r == 1) i -= em0;
+  const int em = r == 0 ? em0 : em1;
+  const double2* G = (r == 0 ? g0 : g1) + (static_cast<long long>(f) * em + i) * q;
+  const double2* X = hatY + static_cast<long long>(f) * nx * K * m;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < q; t += blockDim.x) {
+    const int c = t / m, k = t - c * m;
+    cfma(acc, __ldg(G + t), X[(static_cast<long long>(c) * K + rhs) * m + k]);
+  }
+  acc = ctaSum128(acc, red);
+  if (threadIdx.x == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
 }
 
 // B3/B4 per-bin product: hatMr[r][f][i][rhs] = sum_j sum_k G_r[j][f][i][k] hatX[f][j][rhs][k].
-__global__ void rowProd(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
-                        const double2* __restrict__ hatX, double2* __restrict__ out0, double2* __restrict__ out1,
-                        int Lx, int ny, int m, int K) {
-  const long long items = static_cast<long long>(em0 + em1) * Lx * K;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
-       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const int rhs = static_cast<int>(w % K);
-    long long rest = w / K;
-    const int f = static_cast<int>(rest % Lx);
-    int i = static_cast<int>(rest / Lx);
-    const int r = i < em0 ? 0 : 1;
-    if (r == 1) i -= em0;
-    const int em = r == 0 ? em0 : em1;
-    const double2* G = r == 0 ? g0 : g1;
-    double2 a4[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                     make_double2(0.0, 0.0)};
-    for (int j = 0; j < ny; ++j) {
-      const double2* Gj = G + ((static_cast<long long>(j) * Lx + f) * em + i) * m;
-      const double2* Xj = hatX + ((static_cast<long long>(f) * ny + j) * K + rhs) * m;
-      for (int k = lane; k < m; k += 32) cfma(a4[j & 3], Gj[k], Xj[k]);
-    }
-    double2 acc = cadd(cadd(a4[0], a4[1]), cadd(a4[2], a4[3]));
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-    }
-    if (lane == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
+// B3/B4 per-bin product: hatMr[r][f][i][rhs] = sum_j sum_k G_r[j][f][i][k] hatX[f][j][rhs][k].
+// One CTA per (r, f, i, rhs), threads over the ny*m sources.
+__global__ void __launch_bounds__(128) rowProd(const double2* __restrict__ g0, const double2* __restrict__ g1,
+                                               int em0, int em1, const double2* __restrict__ hatX,
+                                               double2* __restrict__ out0, double2* __restrict__ out1, int Lx,
+                                               int ny, int m, int K) {
+  __shared__ double2 red[4];
+  const long long w = blockIdx.x;
+  const int rhs = static_cast<int>(w % K);
+  const long long rest = w / K;
+  const int f = static_cast<int>(rest % Lx);
+  int i = static_cast<int>(rest / Lx);
+  const int r = i < em0 ? 0 : 1;
+  if (r == 1) i -= em0;
+  const int em = r == 0 ? em0 : em1;
+  const double2* G = r == 0 ? g0 : g1;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < ny * m; t += blockDim.x) {
+    const int j = t / m, k = t - j * m;
+    cfma(acc, __ldg(G + ((static_cast<long long>(j) * Lx + f) * em + i) * m + k),
+         hatX[((static_cast<long long>(f) * ny + j) * K + rhs) * m + k]);
   }
+  acc = ctaSum128(acc, red);
+  if (threadIdx.x == 0) (r == 0 ? out0 : out1)[(static_cast<long long>(f) * em + i) * K + rhs] = acc;
 }
 
 // B^T over the side regions: hatZy[f][c][rhs][k] = sum_r sum_i G_r[-f][i][c*m+k] hatMs[r][f][i][rhs]
@@ -291,24 +290,17 @@ __global__ void cornerReduce(CornerArgs ca, const double2* __restrict__ part, do
 }
 
 // ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349).
-__global__ void cProd(const double2* __restrict__ C, const double2* __restrict__ xs, double2* __restrict__ ys,
-                      long long nM, int K) {
-  const long long items = nM * K;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < items;
-       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const long long k = w / K;
-    const int rhs = static_cast<int>(w % K);
-    const double2* row = C + k * nM;
-    double2 acc = make_double2(0.0, 0.0);
-    for (long long l = lane; l < nM; l += 32) cfma(acc, row[l], xs[l * K + rhs]);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-    }
-    if (lane == 0) ys[k * K + rhs] = cadd(ys[k * K + rhs], acc);
-  }
+// ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349); CTA per (k, rhs).
+__global__ void __launch_bounds__(128) cProd(const double2* __restrict__ C, const double2* __restrict__ xs,
+                                             double2* __restrict__ ys, long long nM, int K) {
+  __shared__ double2 red[4];
+  const long long k = blockIdx.x / K;
+  const int rhs = static_cast<int>(blockIdx.x % K);
+  const double2* row = C + k * nM;
+  double2 acc = make_double2(0.0, 0.0);
+  for (long long l = threadIdx.x; l < nM; l += blockDim.x) cfma(acc, __ldg(row + l), xs[l * K + rhs]);
+  acc = ctaSum128(acc, red);
+  if (threadIdx.x == 0) ys[k * K + rhs] = cadd(ys[k * K + rhs], acc);
 }
 
 // yA += zA + zA2 + sum_c bc^T xM_c (B^T's corner part, linsolve.cpp:328-332).
@@ -587,7 +579,7 @@ void marginApply(Ctx& c, const double2* x, double2* y, int K) {
   addBT<<<gridFor(nA * K), 256, 0, s>>>(y, side ? M->zA : nullptr, row ? M->zA2 : nullptr, ca, M->xs, nA, m, K);
   // B xA into the margin staging vector.
   if (side) {
-    sideProd<<<gridFor(static_cast<long long>(M->emSide[0] + M->emSide[1]) * M->Ly * K * 32), 256, 0, s>>>(
+    sideProd<<<static_cast<unsigned>(static_cast<long long>(M->emSide[0] + M->emSide[1]) * M->Ly * K), 128, 0, s>>>(
         M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1], M->hatY, M->hatMs[0], M->hatMs[1], M->Ly, nx, m, K);
     for (int r = 0; r < 2; ++r) {
       if (M->emSide[r] == 0) continue;
@@ -606,7 +598,7 @@ void marginApply(Ctx& c, const double2* x, double2* y, int K) {
     }
   }
   if (row) {
-    rowProd<<<gridFor(static_cast<long long>(M->emRow[0] + M->emRow[1]) * M->Lx * K * 32), 256, 0, s>>>(
+    rowProd<<<static_cast<unsigned>(static_cast<long long>(M->emRow[0] + M->emRow[1]) * M->Lx * K), 128, 0, s>>>(
         M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatX, M->hatMr[0], M->hatMr[1], M->Lx, ny, m, K);
     for (int r = 0; r < 2; ++r) {
       if (M->emRow[r] == 0) continue;
@@ -630,7 +622,7 @@ void marginApply(Ctx& c, const double2* x, double2* y, int K) {
     cornerPart<<<dim3(nblk, cornerRows), 256, 0, s>>>(ca, x, M->cornerPart, ne, m, K, nblk);
     cornerReduce<<<(cornerRows * K * 32 + 255) / 256, 256, 0, s>>>(ca, M->cornerPart, M->ys, K, nblk);
   }
-  cProd<<<gridFor(M->nM * K * 32), 256, 0, s>>>(M->C, M->xs, M->ys, M->nM, K);
+  cProd<<<static_cast<unsigned>(M->nM * K), 128, 0, s>>>(M->C, M->xs, M->ys, M->nM, K);
   marginScatter<<<gridFor(static_cast<long long>(c.neM) * m * K), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, K);
   TBT_CUDA_CHECK(cudaGetLastError());
 }
