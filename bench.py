@@ -118,6 +118,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def host_cpu():
+    """Host CPU model and logical core count (record them)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def cpu_sample(rep, cfg, seconds=12.0, threads=1):
     """Oracle port timed on host cores: returns (matvec/s, count, elapsed)."""
     import numpy as np
@@ -172,7 +185,8 @@ def run_reference(args):
         "ms_per_step": 1e3 * el / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded generator, include/tbt_gen.h)",
         "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "port", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference C++ cannot be built here (Eigen3 absent, SURVEY.md 8(c)); oracle port timed instead",
     }
@@ -372,7 +386,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cnt, el, t_pre = cpu_sample(rep, cfg, seconds=12.0, threads=1)
-        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
+        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port", "host": host_cpu(),
                "sample": f"{cnt} single-thread {cfg.name} matvecs in {el:.1f} s (oracle/oracle.cpp, reference "
                          f"flags -O3; applyA is serial in the reference, linsolve.cpp:260-290); one-time spectra "
                          f"precompute {t_pre:.2f} s excluded"}
