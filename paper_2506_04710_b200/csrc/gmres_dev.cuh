@@ -192,6 +192,38 @@ __device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn,
   __syncthreads();
 }
 
+// cv[0..j] <- (I + L)^{-1} cv on one warp, L packed by rows (row i at
+// i(i-1)/2); RPL rows per lane (RPL * 32 > j).
+template <int RPL>
+__device__ __forceinline__ void forwardSubstWarp(double2* cv, const double2* sL, int j, int lane) {
+  double2 hv[RPL];
+  int rowBase[RPL];
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const int i = lane + 32 * t;
+    hv[t] = i <= j ? cv[i] : make_double2(0.0, 0.0);
+    rowBase[t] = i * (i - 1) / 2;
+  }
+  for (int k = 0; k < j; ++k) {
+    double2 hk = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+      if (t == (k >> 5)) hk = hv[t];
+    hk = shfl2(hk, k & 31);
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i > k && i <= j) hv[t] = csub(hv[t], cmul(sL[rowBase[t] + k], hk));
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i <= j) cv[i] = hv[t];
+  }
+}
+
 // One Arnoldi step j, single column, low-synchronisation MGS (device
 // function: the gmresArnoldiLS kernel and the fused apply+Arnoldi of
 // matvec_persistent.cu run it): the MGS
@@ -285,43 +317,17 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   mark(2);
   // Stage the lower triangle rows 1..j of L (shared memory after cv).
   double2* sL = cv + RMAX + 1;  // packed rows: row i at i*(i-1)/2
-  for (int q = threadIdx.x; q < j * (j + 1) / 2; q += blockDim.x) {
-    // q -> (i, k) with i >= 1, k < i
-    int i = static_cast<int>((1.0 + sqrt(1.0 + 8.0 * q)) * 0.5);
-    while (i * (i - 1) / 2 > q) --i;
-    while ((i + 1) * i / 2 <= q) ++i;
-    const int k = q - i * (i - 1) / 2;
-    sL[q] = __ldcg(S + static_cast<long long>(i) * lds + k);
-  }
+  for (int i = 1 + warp; i <= j; i += static_cast<int>(blockDim.x >> 5))  // row i: warp, lanes over k < i
+    for (int k = lane; k < i; k += 32) sL[i * (i - 1) / 2 + k] = __ldcg(S + static_cast<long long>(i) * lds + k);
   for (int i = threadIdx.x; i <= j; i += blockDim.x) cv[i] = __ldcg(dots + i);
   __syncthreads();
-  // h = (I + L)^{-1} c, column-oriented on warp 0 (rows in registers).
+  // h = (I + L)^{-1} c, column-oriented on warp 0 (rows in registers; the
+  // register count follows the restart length).
   if (warp == 0) {
-    constexpr int RPL = (RMAX + 31) / 32 + 1;
-    double2 hv[RPL];
-#pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      const int i = lane + 32 * t;
-      hv[t] = i <= j ? cv[i] : make_double2(0.0, 0.0);
-    }
-    for (int k = 0; k < j; ++k) {
-      double2 hk = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int t = 0; t < RPL; ++t)
-        if (t == (k >> 5)) hk = hv[t];
-      hk = shfl2(hk, k & 31);
-#pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const int i = lane + 32 * t;
-        if (i > k && i <= j) hv[t] = csub(hv[t], cmul(sL[i * (i - 1) / 2 + k], hk));
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      const int i = lane + 32 * t;
-      if (i <= j) cv[i] = hv[t];
-    }
+    if (A.restart < 64)
+      forwardSubstWarp<2>(cv, sL, j, lane);
+    else
+      forwardSubstWarp<(RMAX + 31) / 32 + 1>(cv, sL, j, lane);
   }
   __syncthreads();
   if (blockIdx.x == 0)
