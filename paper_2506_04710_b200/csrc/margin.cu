@@ -29,6 +29,7 @@
 // layout [k][rhs] (k in the reference margin order, array_model.cpp:218-228).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "margin.cuh"
 
@@ -325,6 +326,218 @@ __global__ void addBT(double2* __restrict__ y, const double2* __restrict__ zA, c
   }
 }
 
+
+// ---- single-column fused margin products: every generator spectrum and
+// corner block is read ONCE per apply and feeds both B (row dots) and B^T
+// (column sums at the reversed bin / transposed block). EM bounds the rows
+// per region (registers).
+constexpr int kFuseThreads = 256;
+constexpr int kFuseChunk = 512;  // generator columns per CTA (2 per thread)
+constexpr int kCornerQ = 1024;   // corner columns per CTA (256 when that leaves < 4 CTAs per SM)
+constexpr int kLoadGroup = 16;   // generator loads issued back to back
+
+__device__ __forceinline__ double2 warpSumM(double2 v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+  }
+  return v;
+}
+
+// Fixed-order CTA reduction of nv per-thread values pv[0..nv) into
+// out[v * stride] (thread 0 writes), red: [warps][nv] shared.
+template <int NV>
+__device__ __forceinline__ void ctaReduceMany(double2 (&pv)[NV], int nv, double2* red, double2* out, long long stride) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (v >= nv) break;
+    const double2 t = warpSumM(pv[v]);
+    if (lane == 0) red[warp * NV + v] = t;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double2 t = red[v];
+    for (int w = 1; w < nw; ++w) t = cadd(t, red[w * NV + v]);
+    out[v * stride] = t;
+  }
+}
+
+// B1/B2 + their transposes, one column. CTA per (bin h, q-chunk), q = nx*m.
+//   bpart[(h*(em0+em1) + r*em0 + i)*nch + ch] = sum_q G_r[h][i][q] xhat_y[h][q]
+//   zy[hr][q] = sum_r sum_i G_r[h][i][q] mIn_r[hr][i],  hr = -h mod Ly
+template <int EM>
+__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) sideFused(const double2* __restrict__ g0, const double2* __restrict__ g1,
+                                                          int em0, int em1, const double2* __restrict__ hatY,
+                                                          const double2* __restrict__ in0,
+                                                          const double2* __restrict__ in1, double2* __restrict__ zy,
+                                                          double2* __restrict__ bpart, int Ly, int q, int nch) {
+  __shared__ double2 red[(kFuseThreads / 32) * 2 * EM];
+  __shared__ double2 mIn[2 * EM];
+  __shared__ const double2* rowPtr[2 * EM];
+  const int h = blockIdx.x / nch, ch = blockIdx.x % nch;
+  const int hr = (Ly - h) % Ly;
+  const int qlen = (q + nch - 1) / nch, q0 = ch * qlen, q1 = min(q, q0 + qlen);
+  // Rows past em_r read a valid row (hatY) with weight 0 so every load is
+  // unconditional and the loads of one t issue back to back.
+  if (threadIdx.x < 2 * EM) {
+    const int r = threadIdx.x / EM, i = threadIdx.x % EM, em = r ? em1 : em0;
+    const double2* g = r ? g1 : g0;
+    const bool live = i < em && g != nullptr;
+    rowPtr[threadIdx.x] = live ? g + (static_cast<long long>(h) * em + i) * q : hatY + static_cast<long long>(h) * q;
+    mIn[threadIdx.x] = live ? (r ? in1 : in0)[static_cast<long long>(hr) * em + i] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 pb[2 * EM];
+#pragma unroll
+  for (int v = 0; v < 2 * EM; ++v) pb[v] = make_double2(0.0, 0.0);
+  for (int t = q0 + threadIdx.x; t < q1; t += blockDim.x) {
+    const double2 xv = hatY[static_cast<long long>(h) * q + t];
+    double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int v0 = 0; v0 < 2 * EM; v0 += kLoadGroup) {
+      double2 g[kLoadGroup];
+#pragma unroll
+      for (int v = 0; v < kLoadGroup; ++v) g[v] = __ldg(rowPtr[v0 + v] + t);
+#pragma unroll
+      for (int v = 0; v < kLoadGroup; ++v) {
+        cfma(pb[v0 + v], g[v], xv);
+        cfma(z, g[v], mIn[v0 + v]);
+      }
+    }
+    zy[static_cast<long long>(hr) * q + t] = z;
+  }
+  ctaReduceMany<2 * EM>(pb, 2 * EM, red, bpart + static_cast<long long>(h) * 2 * EM * nch + ch, nch);
+}
+
+// B3/B4 + transposes, one column. CTA per (bin h, chunk of t = j*m + k < ny*m).
+template <int EM>
+__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) rowFused(const double2* __restrict__ g0, const double2* __restrict__ g1,
+                                                         int em0, int em1, const double2* __restrict__ hatX,
+                                                         const double2* __restrict__ in0,
+                                                         const double2* __restrict__ in1, double2* __restrict__ zx,
+                                                         double2* __restrict__ bpart, int Lx, int ny, int m, int nch) {
+  __shared__ double2 red[(kFuseThreads / 32) * 2 * EM];
+  __shared__ double2 mIn[2 * EM];
+  __shared__ const double2* rowPtr[2 * EM];  // row base at j = 0; rows step by jStride[r]
+  __shared__ long long jStride[2 * EM];
+  const int q = ny * m;
+  const int h = blockIdx.x / nch, ch = blockIdx.x % nch;
+  const int hr = (Lx - h) % Lx;
+  const int qlen = (q + nch - 1) / nch, q0 = ch * qlen, q1 = min(q, q0 + qlen);
+  if (threadIdx.x < 2 * EM) {  // dead rows: weight 0 on a valid row of hatX
+    const int r = threadIdx.x / EM, i = threadIdx.x % EM, em = r ? em1 : em0;
+    const double2* g = r ? g1 : g0;
+    const bool live = i < em && g != nullptr;
+    rowPtr[threadIdx.x] = live ? g + (static_cast<long long>(h) * em + i) * m : hatX + static_cast<long long>(h) * ny * m;
+    jStride[threadIdx.x] = live ? static_cast<long long>(Lx) * em * m : m;
+    mIn[threadIdx.x] = live ? (r ? in1 : in0)[static_cast<long long>(hr) * em + i] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 pb[2 * EM];
+#pragma unroll
+  for (int v = 0; v < 2 * EM; ++v) pb[v] = make_double2(0.0, 0.0);
+  for (int t = q0 + threadIdx.x; t < q1; t += blockDim.x) {
+    const int j = t / m, k = t - j * m;
+    const double2 xv = hatX[(static_cast<long long>(h) * ny + j) * m + k];
+    double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int v0 = 0; v0 < 2 * EM; v0 += kLoadGroup) {
+      double2 g[kLoadGroup];
+#pragma unroll
+      for (int v = 0; v < kLoadGroup; ++v) g[v] = __ldg(rowPtr[v0 + v] + j * jStride[v0 + v] + k);
+#pragma unroll
+      for (int v = 0; v < kLoadGroup; ++v) {
+        cfma(pb[v0 + v], g[v], xv);
+        cfma(z, g[v], mIn[v0 + v]);
+      }
+    }
+    zx[(static_cast<long long>(hr) * ny + j) * m + k] = z;
+  }
+  ctaReduceMany<2 * EM>(pb, 2 * EM, red, bpart + static_cast<long long>(h) * 2 * EM * nch + ch, nch);
+}
+
+// out_r[h][i] = sum_ch bpart[(h*2EM + r*EM + i)*nch + ch] (fixed order).
+__global__ void reduceParts(const double2* __restrict__ bpart, double2* __restrict__ out0, double2* __restrict__ out1,
+                            int em0, int em1, int EM, int L, int nch) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < L * 2 * EM; o += gridDim.x * blockDim.x) {
+    const int h = o / (2 * EM), v = o % (2 * EM), r = v / EM, i = v % EM;
+    if (i >= (r == 0 ? em0 : em1)) continue;
+    const double2* p = bpart + static_cast<long long>(o) * nch;
+    double2 t = make_double2(0.0, 0.0);
+    for (int c = 0; c < nch; ++c) t = cadd(t, p[c]);
+    (r == 0 ? out0 : out1)[static_cast<long long>(h) * (r == 0 ? em0 : em1) + i] = t;
+  }
+}
+
+// Corners, one column: B rows (partials per element block) and the B^T
+// corner vector cT[q] = sum_c sum_i bc[i][q] xM_c[i], one read of bc.
+// Handles flattened corner rows [row0, row0 + CR); accum adds into cT.
+template <int CR>
+__global__ void __launch_bounds__(kFuseThreads, 2) cornerFused(CornerArgs ca, const double2* __restrict__ x,
+                                                            const double2* __restrict__ xs,
+                                                            double2* __restrict__ part, double2* __restrict__ cT,
+                                                            long long nA, int qBlock, int nblk, int row0,
+                                                            int accum) {
+  __shared__ double2 red[(kFuseThreads / 32) * CR];
+  __shared__ const double2* rowPtr[CR];
+  __shared__ double2 mcs[CR];
+  __shared__ int sRows;
+  const long long q0 = static_cast<long long>(blockIdx.x) * qBlock;
+  const long long q1 = min(nA, q0 + qBlock);
+  if (threadIdx.x == 0) {  // flatten (corner, row) into u < rows
+    int v = 0, f = 0;
+    for (int c = 0; c < 4; ++c)
+      for (int i = 0; i < ca.em[c]; ++i, ++f)
+        if (f >= row0 && v < CR) {
+          rowPtr[v] = ca.bc[c] + static_cast<long long>(i) * nA;
+          mcs[v] = xs[ca.start[c] + i];
+          ++v;
+        }
+    sRows = v;
+    for (; v < CR; ++v) {  // dead rows: weight 0 on row 0 (cached)
+      rowPtr[v] = rowPtr[0];
+      mcs[v] = make_double2(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+  const int rows = sRows;
+  double2 pb[CR];
+#pragma unroll
+  for (int u = 0; u < CR; ++u) pb[u] = make_double2(0.0, 0.0);
+  for (long long qq = q0 + threadIdx.x; qq < q1; qq += blockDim.x) {
+    const double2 xv = x[qq];
+    double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u0 = 0; u0 < CR; u0 += 16) {  // all 16 rows' loads in flight at once
+      double2 g[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) g[u] = __ldg(rowPtr[u0 + u] + qq);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        cfma(pb[u0 + u], g[u], xv);
+        cfma(z, g[u], mcs[u0 + u]);
+      }
+    }
+    cT[qq] = accum ? cadd(cT[qq], z) : z;
+  }
+  ctaReduceMany<CR>(pb, rows, red, part + static_cast<long long>(row0) * nblk + blockIdx.x, nblk);
+}
+
+// y[q] += zA[q] + zA2[q] + cT[q] (one column).
+__global__ void addBT1(double2* __restrict__ y, const double2* __restrict__ zA, const double2* __restrict__ zA2,
+                       const double2* __restrict__ cT, long long nA) {
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nA;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double2 acc = y[o];
+    if (zA) acc = cadd(acc, zA[o]);
+    if (zA2) acc = cadd(acc, zA2[o]);
+    if (cT) acc = cadd(acc, cT[o]);
+    y[o] = acc;
+  }
+}
+
 }  // namespace
 
 void marginFree(Ctx& c) {
@@ -343,6 +556,11 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
   auto* M = new MarginOp;
   c.margin = M;
   M->stream = c.stream;
+  for (int b = 0; b < 2; ++b) {
+    TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&M->branch[b], cudaStreamNonBlocking));
+    TBT_CUDA_CHECK(cudaEventCreateWithFlags(&M->evJoin[b], cudaEventDisableTiming));
+  }
+  TBT_CUDA_CHECK(cudaEventCreateWithFlags(&M->evFork, cudaEventDisableTiming));
   const int nx = c.nx, ny = c.ny, m = c.m, K = c.maxNrhs;
   const long long nA = c.n;
   for (int q = 0; q < 9; ++q) M->e[q] = e[q];
@@ -458,8 +676,18 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
     M->hatMr[r] = M->alloc(static_cast<size_t>(M->Lx) * std::max(M->emRow[r], 1) * K);
   }
   M->zA = M->alloc(static_cast<size_t>(c.ne) * K * m);
+  // Fused single-column path buffers.
+  M->chunkS = std::max(1, (nx * m + kFuseChunk - 1) / kFuseChunk);
+  M->chunkR = std::max(1, (ny * m + kFuseChunk - 1) / kFuseChunk);
+  for (int r = 0; r < 2; ++r) {
+    M->hatMsOut[r] = M->alloc(static_cast<size_t>(M->Ly) * std::max(M->emSide[r], 1));
+    M->hatMrOut[r] = M->alloc(static_cast<size_t>(M->Lx) * std::max(M->emRow[r], 1));
+  }
+  M->bpartS = M->alloc(static_cast<size_t>(M->Ly) * 2 * 16 * M->chunkS);  // slots r*EM + i, EM <= 16
+  M->bpartR = M->alloc(static_cast<size_t>(M->Lx) * 2 * 16 * M->chunkR);
+  M->cornerT = M->alloc(static_cast<size_t>(nA));
   M->cornerPart = M->alloc(static_cast<size_t>(M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3]) *
-                           K * ((c.ne + kCornerElems - 1) / kCornerElems));
+                           std::max<long long>(K * ((c.ne + kCornerElems - 1) / kCornerElems), (nA + 255) / 256));
   M->zA2 = M->alloc(static_cast<size_t>(c.ne) * K * m);
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
   // The raw uploads and sequences are no longer needed once the spectra exist.
@@ -470,9 +698,174 @@ void marginDiagonal(const Ctx& c, std::vector<double2>& d) {
   d.insert(d.end(), c.margin->diag.begin(), c.margin->diag.end());
 }
 
+namespace {
+
+template <int EM>
+void launchSideFused(MarginOp* M, int nx, int m, cudaStream_t s) {
+  const int q = nx * m;
+  sideFused<EM><<<M->Ly * M->chunkS, kFuseThreads, 0, s>>>(M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1],
+                                                             M->hatY, M->hatMs[0], M->hatMs[1], M->hatZy, M->bpartS,
+                                                             M->Ly, q, M->chunkS);
+}
+template <int EM>
+void launchRowFused(MarginOp* M, int ny, int m, cudaStream_t s) {
+  rowFused<EM><<<M->Lx * M->chunkR, kFuseThreads, 0, s>>>(M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatX,
+                                                           M->hatMr[0], M->hatMr[1], M->hatZx, M->bpartR, M->Lx, ny,
+                                                           m, M->chunkR);
+}
+
+int fuseBound(int a, int b) {
+  const int e = std::max(a, b);
+  return e <= 8 ? 8 : e <= 16 ? 16 : 0;
+}
+
+// One column: B and B^T from a single read of every generator spectrum and
+// corner block (hatMs / hatMr hold the transformed margin inputs, the B
+// results go to hatMsOut / hatMrOut).
+bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
+  MarginOp* M = c.margin;
+  const int nx = c.nx, ny = c.ny, m = c.m, ne = c.ne;
+  const long long nA = c.n;
+  const int emS = fuseBound(M->emSide[0], M->emSide[1]), emR = fuseBound(M->emRow[0], M->emRow[1]);
+  const int cornerRows = M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3];
+  if ((M->anySide() && !emS) || (M->anyRow() && !emR) || !M->hatMsOut[0]) return false;
+  marginGather<<<gridFor(M->nM), 256, 0, c.stream>>>(x, M->xs, M->nM, ne, m, 1);
+  CornerArgs ca{};
+  for (int q = 0; q < 4; ++q) {
+    ca.bc[q] = M->corner[q];
+    ca.em[q] = M->emCorner[q];
+    ca.start[q] = M->cornerStart[q];
+  }
+  const bool side = M->anySide(), row = M->anyRow();
+  // Fork: side products on branch[0], row products on branch[1], corners on
+  // the ctx stream; all three read x / xs only and write disjoint outputs.
+  TBT_CUDA_CHECK(cudaEventRecord(M->evFork, c.stream));
+  for (int b = 0; b < 2; ++b) TBT_CUDA_CHECK(cudaStreamWaitEvent(M->branch[b], M->evFork, 0));
+  cudaStream_t s = M->branch[0];
+  auto fftSeg = [&](const double2* in, double2* out, int em, int L, int nIn, const double2* tw, bool inv,
+                    int nOut, double scale) {
+    FftPass f;
+    f.in = in;
+    f.out = out;
+    f.lines = 1;
+    f.in_point_stride = f.out_point_stride = em;
+    f.n = L;
+    f.n_in = nIn;
+    f.n_out = nOut;
+    f.batch = em;
+    f.inverse = inv ? 1 : 0;
+    f.scale = scale;
+    f.tw = tw;
+    launchFftPass(f, s);
+  };
+  if (side) {
+    FftPass fy;
+    fy.in = x;
+    fy.out = M->hatY;
+    fy.lines = 1;
+    fy.in_point_stride = fy.out_point_stride = static_cast<long long>(nx) * m;
+    fy.n = fy.n_out = M->Ly;
+    fy.n_in = ny;
+    fy.batch = nx * m;
+    fy.tw = M->twY;
+    launchFftPass(fy, s);
+    for (int r = 0; r < 2; ++r)
+      if (M->emSide[r]) fftSeg(M->xs + M->sideStart[r], M->hatMs[r], M->emSide[r], M->Ly, ny, M->twY, false, M->Ly, 1.0);
+    if (emS == 8)
+      launchSideFused<8>(M, nx, m, s);
+    else
+      launchSideFused<16>(M, nx, m, s);
+    reduceParts<<<gridFor(static_cast<long long>(M->Ly) * 2 * emS), 256, 0, s>>>(
+        M->bpartS, M->hatMsOut[0], M->hatMsOut[1], M->emSide[0], M->emSide[1], emS, M->Ly, M->chunkS);
+    FftPass iz;  // B^T side part back to the elements
+    iz.in = M->hatZy;
+    iz.out = M->zA;
+    iz.lines = 1;
+    iz.in_point_stride = iz.out_point_stride = static_cast<long long>(nx) * m;
+    iz.n = iz.n_in = M->Ly;
+    iz.n_out = ny;
+    iz.batch = nx * m;
+    iz.inverse = 1;
+    iz.scale = 1.0 / M->Ly;
+    iz.tw = M->twY;
+    launchFftPass(iz, s);
+    for (int r = 0; r < 2; ++r)
+      if (M->emSide[r])
+        fftSeg(M->hatMsOut[r], M->ys + M->sideStart[r], M->emSide[r], M->Ly, M->Ly, M->twY, true, ny, 1.0 / M->Ly);
+  }
+  s = M->branch[1];
+  if (row) {
+    FftPass fx;
+    fx.in = x;
+    fx.out = M->hatX;
+    fx.lines = ny;
+    fx.in_line_stride = static_cast<long long>(nx) * m;
+    fx.in_point_stride = m;
+    fx.out_line_stride = m;
+    fx.out_point_stride = static_cast<long long>(ny) * m;
+    fx.n = fx.n_out = M->Lx;
+    fx.n_in = nx;
+    fx.batch = m;
+    fx.tw = M->twX;
+    launchFftPass(fx, s);
+    for (int r = 0; r < 2; ++r)
+      if (M->emRow[r]) fftSeg(M->xs + M->rowStart[r], M->hatMr[r], M->emRow[r], M->Lx, nx, M->twX, false, M->Lx, 1.0);
+    if (emR == 8)
+      launchRowFused<8>(M, ny, m, s);
+    else
+      launchRowFused<16>(M, ny, m, s);
+    reduceParts<<<gridFor(static_cast<long long>(M->Lx) * 2 * emR), 256, 0, s>>>(
+        M->bpartR, M->hatMrOut[0], M->hatMrOut[1], M->emRow[0], M->emRow[1], emR, M->Lx, M->chunkR);
+    FftPass iz;
+    iz.in = M->hatZx;
+    iz.out = M->zA2;
+    iz.lines = ny;
+    iz.in_line_stride = m;
+    iz.in_point_stride = static_cast<long long>(ny) * m;
+    iz.out_line_stride = static_cast<long long>(nx) * m;
+    iz.out_point_stride = m;
+    iz.n = iz.n_in = M->Lx;
+    iz.n_out = nx;
+    iz.batch = m;
+    iz.inverse = 1;
+    iz.scale = 1.0 / M->Lx;
+    iz.tw = M->twX;
+    launchFftPass(iz, s);
+    for (int r = 0; r < 2; ++r)
+      if (M->emRow[r])
+        fftSeg(M->hatMrOut[r], M->ys + M->rowStart[r], M->emRow[r], M->Lx, M->Lx, M->twX, true, nx, 1.0 / M->Lx);
+  }
+  s = c.stream;
+  const double2* cT = nullptr;
+  if (cornerRows > 0) {
+    const int qBlock = (nA + kCornerQ - 1) / kCornerQ >= 4LL * smCount(c.device) ? kCornerQ : 256;
+    const int nblk = static_cast<int>((nA + qBlock - 1) / qBlock);
+    // 16 rows per pass keeps the kernel at 2 CTAs/SM; passes after the
+    // first accumulate into cT (stream order).
+    for (int r0 = 0; r0 < cornerRows; r0 += 16)
+      cornerFused<16><<<nblk, kFuseThreads, 0, s>>>(ca, x, M->xs, M->cornerPart, M->cornerT, nA, qBlock, nblk, r0,
+                                                    r0 > 0 ? 1 : 0);
+    cornerReduce<<<(cornerRows * 32 + 255) / 256, 256, 0, s>>>(ca, M->cornerPart, M->ys, 1, nblk);
+    cT = M->cornerT;
+  }
+  for (int b = 0; b < 2; ++b) {  // join
+    TBT_CUDA_CHECK(cudaEventRecord(M->evJoin[b], M->branch[b]));
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, M->evJoin[b], 0));
+  }
+  cProd<<<static_cast<unsigned>(M->nM), 128, 0, s>>>(M->C, M->xs, M->ys, M->nM, 1);
+  addBT1<<<gridFor(nA), 256, 0, s>>>(y, side ? M->zA : nullptr, row ? M->zA2 : nullptr, cT, nA);
+  marginScatter<<<gridFor(static_cast<long long>(c.neM) * m), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, 1);
+  TBT_CUDA_CHECK(cudaGetLastError());
+  return true;
+}
+
+}  // namespace
+
 void marginApply(Ctx& c, const double2* x, double2* y, int K) {
   MarginOp* M = c.margin;
   if (!M || M->nM == 0) return;
+  static const bool noFuse = getenv("TBT_MARGIN_UNFUSED") != nullptr;
+  if (K == 1 && !noFuse && marginApplyFused1(c, x, y)) return;
   cudaStream_t s = c.stream;
   const int nx = c.nx, ny = c.ny, m = c.m, ne = c.ne;
   const long long nA = c.n, B = static_cast<long long>(K) * m;

@@ -31,8 +31,18 @@ struct MarginOp {
   double2* hatMr[2] = {nullptr, nullptr};       // [Lx][em][K]
   double2 *zA = nullptr, *zA2 = nullptr;       // [ne][K][m]
   double2* cornerPart = nullptr;               // [corner rows][K][element blocks]
+  // Single-column fused path (B and B^T from one read of every array).
+  double2* hatMsOut[2] = {nullptr, nullptr};    // [Ly][em]
+  double2* hatMrOut[2] = {nullptr, nullptr};    // [Lx][em]
+  double2 *bpartS = nullptr, *bpartR = nullptr; // B partials per (bin, row, chunk)
+  double2* cornerT = nullptr;                   // [nA] B^T corner contribution
+  int chunkS = 1, chunkR = 1;                   // q-chunks per bin
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
+  // Side / row branches of the single-column apply run beside the corner
+  // branch on the ctx stream (forked and joined with events).
+  cudaStream_t branch[2] = {nullptr, nullptr};
+  cudaEvent_t evFork = nullptr, evJoin[2] = {nullptr, nullptr};
 
   double2* alloc(size_t count) {
     void* p = nullptr;
@@ -43,6 +53,11 @@ struct MarginOp {
   }
   ~MarginOp() {
     for (void* p : allocs) cudaFree(p);
+    for (int b = 0; b < 2; ++b) {
+      if (branch[b]) cudaStreamDestroy(branch[b]);
+      if (evJoin[b]) cudaEventDestroy(evJoin[b]);
+    }
+    if (evFork) cudaEventDestroy(evFork);
   }
   bool anySide() const { return emSide[0] + emSide[1] > 0; }
   bool anyRow() const { return emRow[0] + emRow[1] > 0; }
