@@ -293,7 +293,7 @@ __global__ void cornerReduce(CornerArgs ca, const double2* __restrict__ part, do
 // ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349).
 // ys[k][rhs] += sum_l C[k][l] xs[l][rhs] (applyC, linsolve.cpp:336-349); CTA per (k, rhs).
 __global__ void __launch_bounds__(128) cProd(const double2* __restrict__ C, const double2* __restrict__ xs,
-                                             double2* __restrict__ ys, long long nM, int K) {
+                                             double2* __restrict__ ys, long long nM, int K, int set = 0) {
   __shared__ double2 red[4];
   const long long k = blockIdx.x / K;
   const int rhs = static_cast<int>(blockIdx.x % K);
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(128) cProd(const double2* __restrict__ C, cons
   double2 acc = make_double2(0.0, 0.0);
   for (long long l = threadIdx.x; l < nM; l += blockDim.x) cfma(acc, __ldg(row + l), xs[l * K + rhs]);
   acc = ctaSum128(acc, red);
-  if (threadIdx.x == 0) ys[k * K + rhs] = cadd(ys[k * K + rhs], acc);
+  if (threadIdx.x == 0) ys[k * K + rhs] = set ? acc : cadd(ys[k * K + rhs], acc);
 }
 
 // yA += zA + zA2 + sum_c bc^T xM_c (B^T's corner part, linsolve.cpp:328-332).
@@ -364,21 +364,78 @@ __device__ __forceinline__ void ctaReduceMany(double2 (&pv)[NV], int nv, double2
   }
 }
 
+// Prologue of the side/row kernels: the two margin-part spectra at bin hr,
+// by direct DFT of the nIn margin unknowns (1-D Toeplitz embedding of
+// linsolve.cpp:300-306, zero-padded to L; forward sign as twiddles()):
+//   mIn[r*EM + i] = sum_{j<nIn} xs[start_r + j*em_r + i] tw[(hr*j) mod L].
+// Dead slots (i >= em_r) get 0. Fixed-order reduction over 8 thread groups.
+template <int EM>
+__device__ __forceinline__ void marginDft(const double2* __restrict__ xs0, const double2* __restrict__ xs1, int em0,
+                                          int em1, int nIn, int hr, int L, const double2* __restrict__ tw,
+                                          double2* mIn, double2* scratch /* [8][32] */) {
+  static_assert(2 * EM <= 32, "one warp-wide slot per margin row");
+  const int v = threadIdx.x & 31, grp = threadIdx.x >> 5, ngrp = blockDim.x >> 5;
+  double2 acc = make_double2(0.0, 0.0);
+  if (v < 2 * EM) {
+    const int r = v / EM, i = v % EM, em = r ? em1 : em0;
+    const double2* src = r ? xs1 : xs0;
+    if (i < em && src)
+      for (int j = grp; j < nIn; j += ngrp)
+        cfma(acc, src[static_cast<long long>(j) * em + i], tw[(static_cast<long long>(hr) * j) % L]);
+  }
+  scratch[grp * 32 + v] = acc;
+  __syncthreads();
+  if (threadIdx.x < 2 * EM) {
+    double2 t = scratch[threadIdx.x];
+    for (int g = 1; g < ngrp; ++g) t = cadd(t, scratch[g * 32 + threadIdx.x]);
+    mIn[threadIdx.x] = t;
+  }
+}
+
+// ys[start_r + j*em_r + i] = (1/L) sum_h conj(tw[(h*j) mod L]) sum_ch bpart[(h*2EM + r*EM + i)*nch + ch],
+// j < nOut: the chunk reduction and the inverse 1-D transform of the B
+// rows in one kernel, CTA per (r, i).
+__global__ void __launch_bounds__(256) marginBToYs(const double2* __restrict__ bpart, int EM, int em0, int em1,
+                                                  int L, int nch, int nOut, const double2* __restrict__ tw,
+                                                  double2* __restrict__ ys0, double2* __restrict__ ys1) {
+  extern __shared__ double2 col[];  // [L]
+  const int r = blockIdx.x / EM, i = blockIdx.x % EM, em = r ? em1 : em0;
+  if (i >= em) return;
+  for (int h = threadIdx.x; h < L; h += blockDim.x) {
+    const double2* p = bpart + (static_cast<long long>(h) * 2 * EM + r * EM + i) * nch;
+    double2 t = make_double2(0.0, 0.0);
+    for (int c = 0; c < nch; ++c) t = cadd(t, p[c]);
+    col[h] = t;
+  }
+  __syncthreads();
+  const double sc = 1.0 / L;
+  double2* out = r ? ys1 : ys0;
+  for (int j = threadIdx.x; j < nOut; j += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int h = 0; h < L; ++h) {
+      const double2 w = tw[(static_cast<long long>(h) * j) % L];
+      cfma(acc, col[h], make_double2(w.x, -w.y));
+    }
+    out[static_cast<long long>(j) * em + i] = make_double2(acc.x * sc, acc.y * sc);
+  }
+}
+
 // B1/B2 + their transposes, one column. CTA per (bin h, q-chunk), q = nx*m.
 //   bpart[(h*(em0+em1) + r*em0 + i)*nch + ch] = sum_q G_r[h][i][q] xhat_y[h][q]
 //   zy[hr][q] = sum_r sum_i G_r[h][i][q] mIn_r[hr][i],  hr = -h mod Ly
 template <int EM>
-__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) sideFused(const double2* __restrict__ g0, const double2* __restrict__ g1,
-                                                          int em0, int em1, const double2* __restrict__ hatY,
-                                                          const double2* __restrict__ in0,
-                                                          const double2* __restrict__ in1, double2* __restrict__ zy,
-                                                          double2* __restrict__ bpart, int Ly, int q, int nch) {
-  __shared__ double2 red[(kFuseThreads / 32) * 2 * EM];
+__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1)
+    sideFused(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+              const double2* __restrict__ hatY, const double2* __restrict__ xs0, const double2* __restrict__ xs1,
+              int nIn, const double2* __restrict__ tw, double2* __restrict__ zy, double2* __restrict__ bpart, int Ly,
+              int q, int nch) {
+  __shared__ double2 red[(kFuseThreads / 32) * 32];
   __shared__ double2 mIn[2 * EM];
   __shared__ const double2* rowPtr[2 * EM];
   const int h = blockIdx.x / nch, ch = blockIdx.x % nch;
   const int hr = (Ly - h) % Ly;
   const int qlen = (q + nch - 1) / nch, q0 = ch * qlen, q1 = min(q, q0 + qlen);
+  marginDft<EM>(xs0, xs1, em0, em1, nIn, hr, Ly, tw, mIn, red);
   // Rows past em_r read a valid row (hatY) with weight 0 so every load is
   // unconditional and the loads of one t issue back to back.
   if (threadIdx.x < 2 * EM) {
@@ -386,7 +443,7 @@ __global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) sideFused(const
     const double2* g = r ? g1 : g0;
     const bool live = i < em && g != nullptr;
     rowPtr[threadIdx.x] = live ? g + (static_cast<long long>(h) * em + i) * q : hatY + static_cast<long long>(h) * q;
-    mIn[threadIdx.x] = live ? (r ? in1 : in0)[static_cast<long long>(hr) * em + i] : make_double2(0.0, 0.0);
+    if (!live) mIn[threadIdx.x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   double2 pb[2 * EM];
@@ -413,12 +470,12 @@ __global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) sideFused(const
 
 // B3/B4 + transposes, one column. CTA per (bin h, chunk of t = j*m + k < ny*m).
 template <int EM>
-__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) rowFused(const double2* __restrict__ g0, const double2* __restrict__ g1,
-                                                         int em0, int em1, const double2* __restrict__ hatX,
-                                                         const double2* __restrict__ in0,
-                                                         const double2* __restrict__ in1, double2* __restrict__ zx,
-                                                         double2* __restrict__ bpart, int Lx, int ny, int m, int nch) {
-  __shared__ double2 red[(kFuseThreads / 32) * 2 * EM];
+__global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1)
+    rowFused(const double2* __restrict__ g0, const double2* __restrict__ g1, int em0, int em1,
+             const double2* __restrict__ hatX, const double2* __restrict__ xs0, const double2* __restrict__ xs1,
+             int nIn, const double2* __restrict__ tw, double2* __restrict__ zx, double2* __restrict__ bpart, int Lx,
+             int ny, int m, int nch) {
+  __shared__ double2 red[(kFuseThreads / 32) * 32];
   __shared__ double2 mIn[2 * EM];
   __shared__ const double2* rowPtr[2 * EM];  // row base at j = 0; rows step by jStride[r]
   __shared__ long long jStride[2 * EM];
@@ -426,13 +483,14 @@ __global__ void __launch_bounds__(kFuseThreads, EM <= 8 ? 2 : 1) rowFused(const 
   const int h = blockIdx.x / nch, ch = blockIdx.x % nch;
   const int hr = (Lx - h) % Lx;
   const int qlen = (q + nch - 1) / nch, q0 = ch * qlen, q1 = min(q, q0 + qlen);
+  marginDft<EM>(xs0, xs1, em0, em1, nIn, hr, Lx, tw, mIn, red);
   if (threadIdx.x < 2 * EM) {  // dead rows: weight 0 on a valid row of hatX
     const int r = threadIdx.x / EM, i = threadIdx.x % EM, em = r ? em1 : em0;
     const double2* g = r ? g1 : g0;
     const bool live = i < em && g != nullptr;
     rowPtr[threadIdx.x] = live ? g + (static_cast<long long>(h) * em + i) * m : hatX + static_cast<long long>(h) * ny * m;
     jStride[threadIdx.x] = live ? static_cast<long long>(Lx) * em * m : m;
-    mIn[threadIdx.x] = live ? (r ? in1 : in0)[static_cast<long long>(hr) * em + i] : make_double2(0.0, 0.0);
+    if (!live) mIn[threadIdx.x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   double2 pb[2 * EM];
@@ -473,13 +531,15 @@ __global__ void reduceParts(const double2* __restrict__ bpart, double2* __restri
 
 // Corners, one column: B rows (partials per element block) and the B^T
 // corner vector cT[q] = sum_c sum_i bc[i][q] xM_c[i], one read of bc.
-// Handles flattened corner rows [row0, row0 + CR); accum adds into cT.
+// blockIdx.y handles flattened corner rows [16y, 16y + CR) into its own
+// cT slice cT + y*nA (summed by marginFinish1).
 template <int CR>
 __global__ void __launch_bounds__(kFuseThreads, 2) cornerFused(CornerArgs ca, const double2* __restrict__ x,
                                                             const double2* __restrict__ xs,
                                                             double2* __restrict__ part, double2* __restrict__ cT,
-                                                            long long nA, int qBlock, int nblk, int row0,
-                                                            int accum) {
+                                                            long long nA, int qBlock, int nblk) {
+  const int row0 = blockIdx.y * CR;
+  cT += blockIdx.y * nA;
   __shared__ double2 red[(kFuseThreads / 32) * CR];
   __shared__ const double2* rowPtr[CR];
   __shared__ double2 mcs[CR];
@@ -520,21 +580,30 @@ __global__ void __launch_bounds__(kFuseThreads, 2) cornerFused(CornerArgs ca, co
         cfma(z, g[u], mcs[u0 + u]);
       }
     }
-    cT[qq] = accum ? cadd(cT[qq], z) : z;
+    cT[qq] = z;
   }
   ctaReduceMany<CR>(pb, rows, red, part + static_cast<long long>(row0) * nblk + blockIdx.x, nblk);
 }
 
 // y[q] += zA[q] + zA2[q] + cT[q] (one column).
-__global__ void addBT1(double2* __restrict__ y, const double2* __restrict__ zA, const double2* __restrict__ zA2,
-                       const double2* __restrict__ cT, long long nA) {
-  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nA;
+// One column: yA += zA + zA2 + sum_p cT[p] (B^T parts), and the margin
+// pseudo-elements y[nA + k] = ys[k] + ysC[k] (B rows + C xM), zero past nM.
+__global__ void marginFinish1(double2* __restrict__ y, const double2* __restrict__ zA,
+                              const double2* __restrict__ zA2, const double2* __restrict__ cT, int nT,
+                              const double2* __restrict__ ys, const double2* __restrict__ ysC, long long nA,
+                              long long nM, long long nPad) {
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nA + nPad;
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
-    double2 acc = y[o];
-    if (zA) acc = cadd(acc, zA[o]);
-    if (zA2) acc = cadd(acc, zA2[o]);
-    if (cT) acc = cadd(acc, cT[o]);
-    y[o] = acc;
+    if (o < nA) {
+      double2 acc = y[o];
+      if (zA) acc = cadd(acc, zA[o]);
+      if (zA2) acc = cadd(acc, zA2[o]);
+      for (int p = 0; p < nT; ++p) acc = cadd(acc, cT[p * nA + o]);
+      y[o] = acc;
+    } else {
+      const long long k = o - nA;
+      y[o] = k < nM ? cadd(ys[k], ysC[k]) : make_double2(0.0, 0.0);
+    }
   }
 }
 
@@ -685,7 +754,9 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
   }
   M->bpartS = M->alloc(static_cast<size_t>(M->Ly) * 2 * 16 * M->chunkS);  // slots r*EM + i, EM <= 16
   M->bpartR = M->alloc(static_cast<size_t>(M->Lx) * 2 * 16 * M->chunkR);
-  M->cornerT = M->alloc(static_cast<size_t>(nA));
+  M->cornerT = M->alloc(static_cast<size_t>(nA) *
+                        std::max(1, (M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3] + 15) / 16));
+  M->ysC = M->alloc(static_cast<size_t>(M->nM));
   M->cornerPart = M->alloc(static_cast<size_t>(M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3]) *
                            std::max<long long>(K * ((c.ne + kCornerElems - 1) / kCornerElems), (nA + 255) / 256));
   M->zA2 = M->alloc(static_cast<size_t>(c.ne) * K * m);
@@ -701,17 +772,17 @@ void marginDiagonal(const Ctx& c, std::vector<double2>& d) {
 namespace {
 
 template <int EM>
-void launchSideFused(MarginOp* M, int nx, int m, cudaStream_t s) {
+void launchSideFused(MarginOp* M, const double2* xs, int nx, int ny, int m, cudaStream_t s) {
   const int q = nx * m;
-  sideFused<EM><<<M->Ly * M->chunkS, kFuseThreads, 0, s>>>(M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1],
-                                                             M->hatY, M->hatMs[0], M->hatMs[1], M->hatZy, M->bpartS,
-                                                             M->Ly, q, M->chunkS);
+  sideFused<EM><<<M->Ly * M->chunkS, kFuseThreads, 0, s>>>(
+      M->gSide[0], M->gSide[1], M->emSide[0], M->emSide[1], M->hatY, xs + M->sideStart[0], xs + M->sideStart[1], ny,
+      M->twY, M->hatZy, M->bpartS, M->Ly, q, M->chunkS);
 }
 template <int EM>
-void launchRowFused(MarginOp* M, int ny, int m, cudaStream_t s) {
-  rowFused<EM><<<M->Lx * M->chunkR, kFuseThreads, 0, s>>>(M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatX,
-                                                           M->hatMr[0], M->hatMr[1], M->hatZx, M->bpartR, M->Lx, ny,
-                                                           m, M->chunkR);
+void launchRowFused(MarginOp* M, const double2* xs, int nx, int ny, int m, cudaStream_t s) {
+  rowFused<EM><<<M->Lx * M->chunkR, kFuseThreads, 0, s>>>(
+      M->gRow[0], M->gRow[1], M->emRow[0], M->emRow[1], M->hatX, xs + M->rowStart[0], xs + M->rowStart[1], nx,
+      M->twX, M->hatZx, M->bpartR, M->Lx, ny, m, M->chunkR);
 }
 
 int fuseBound(int a, int b) {
@@ -729,7 +800,8 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
   const int emS = fuseBound(M->emSide[0], M->emSide[1]), emR = fuseBound(M->emRow[0], M->emRow[1]);
   const int cornerRows = M->emCorner[0] + M->emCorner[1] + M->emCorner[2] + M->emCorner[3];
   if ((M->anySide() && !emS) || (M->anyRow() && !emR) || !M->hatMsOut[0]) return false;
-  marginGather<<<gridFor(M->nM), 256, 0, c.stream>>>(x, M->xs, M->nM, ne, m, 1);
+  // One column: the margin unknowns are contiguous right after the elements.
+  const double2* xs = x + nA;
   CornerArgs ca{};
   for (int q = 0; q < 4; ++q) {
     ca.bc[q] = M->corner[q];
@@ -737,28 +809,12 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
     ca.start[q] = M->cornerStart[q];
   }
   const bool side = M->anySide(), row = M->anyRow();
-  // Fork: side products on branch[0], row products on branch[1], corners on
-  // the ctx stream; all three read x / xs only and write disjoint outputs.
+  // Fork: side products on branch[0], row products on branch[1], C and the
+  // corners on the ctx stream; all read x only and write disjoint outputs.
   TBT_CUDA_CHECK(cudaEventRecord(M->evFork, c.stream));
   for (int b = 0; b < 2; ++b) TBT_CUDA_CHECK(cudaStreamWaitEvent(M->branch[b], M->evFork, 0));
-  cudaStream_t s = M->branch[0];
-  auto fftSeg = [&](const double2* in, double2* out, int em, int L, int nIn, const double2* tw, bool inv,
-                    int nOut, double scale) {
-    FftPass f;
-    f.in = in;
-    f.out = out;
-    f.lines = 1;
-    f.in_point_stride = f.out_point_stride = em;
-    f.n = L;
-    f.n_in = nIn;
-    f.n_out = nOut;
-    f.batch = em;
-    f.inverse = inv ? 1 : 0;
-    f.scale = scale;
-    f.tw = tw;
-    launchFftPass(f, s);
-  };
   if (side) {
+    cudaStream_t s = M->branch[0];
     FftPass fy;
     fy.in = x;
     fy.out = M->hatY;
@@ -769,14 +825,13 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
     fy.batch = nx * m;
     fy.tw = M->twY;
     launchFftPass(fy, s);
-    for (int r = 0; r < 2; ++r)
-      if (M->emSide[r]) fftSeg(M->xs + M->sideStart[r], M->hatMs[r], M->emSide[r], M->Ly, ny, M->twY, false, M->Ly, 1.0);
     if (emS == 8)
-      launchSideFused<8>(M, nx, m, s);
+      launchSideFused<8>(M, xs, nx, ny, m, s);
     else
-      launchSideFused<16>(M, nx, m, s);
-    reduceParts<<<gridFor(static_cast<long long>(M->Ly) * 2 * emS), 256, 0, s>>>(
-        M->bpartS, M->hatMsOut[0], M->hatMsOut[1], M->emSide[0], M->emSide[1], emS, M->Ly, M->chunkS);
+      launchSideFused<16>(M, xs, nx, ny, m, s);
+    marginBToYs<<<2 * emS, 256, M->Ly * sizeof(double2), s>>>(M->bpartS, emS, M->emSide[0], M->emSide[1], M->Ly,
+                                                               M->chunkS, ny, M->twY, M->ys + M->sideStart[0],
+                                                               M->ys + M->sideStart[1]);
     FftPass iz;  // B^T side part back to the elements
     iz.in = M->hatZy;
     iz.out = M->zA;
@@ -789,12 +844,9 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
     iz.scale = 1.0 / M->Ly;
     iz.tw = M->twY;
     launchFftPass(iz, s);
-    for (int r = 0; r < 2; ++r)
-      if (M->emSide[r])
-        fftSeg(M->hatMsOut[r], M->ys + M->sideStart[r], M->emSide[r], M->Ly, M->Ly, M->twY, true, ny, 1.0 / M->Ly);
   }
-  s = M->branch[1];
   if (row) {
+    cudaStream_t s = M->branch[1];
     FftPass fx;
     fx.in = x;
     fx.out = M->hatX;
@@ -808,14 +860,13 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
     fx.batch = m;
     fx.tw = M->twX;
     launchFftPass(fx, s);
-    for (int r = 0; r < 2; ++r)
-      if (M->emRow[r]) fftSeg(M->xs + M->rowStart[r], M->hatMr[r], M->emRow[r], M->Lx, nx, M->twX, false, M->Lx, 1.0);
     if (emR == 8)
-      launchRowFused<8>(M, ny, m, s);
+      launchRowFused<8>(M, xs, nx, ny, m, s);
     else
-      launchRowFused<16>(M, ny, m, s);
-    reduceParts<<<gridFor(static_cast<long long>(M->Lx) * 2 * emR), 256, 0, s>>>(
-        M->bpartR, M->hatMrOut[0], M->hatMrOut[1], M->emRow[0], M->emRow[1], emR, M->Lx, M->chunkR);
+      launchRowFused<16>(M, xs, nx, ny, m, s);
+    marginBToYs<<<2 * emR, 256, M->Lx * sizeof(double2), s>>>(M->bpartR, emR, M->emRow[0], M->emRow[1], M->Lx,
+                                                               M->chunkR, nx, M->twX, M->ys + M->rowStart[0],
+                                                               M->ys + M->rowStart[1]);
     FftPass iz;
     iz.in = M->hatZx;
     iz.out = M->zA2;
@@ -831,30 +882,25 @@ bool marginApplyFused1(Ctx& c, const double2* x, double2* y) {
     iz.scale = 1.0 / M->Lx;
     iz.tw = M->twX;
     launchFftPass(iz, s);
-    for (int r = 0; r < 2; ++r)
-      if (M->emRow[r])
-        fftSeg(M->hatMrOut[r], M->ys + M->rowStart[r], M->emRow[r], M->Lx, M->Lx, M->twX, true, nx, 1.0 / M->Lx);
   }
-  s = c.stream;
-  const double2* cT = nullptr;
+  cudaStream_t s = c.stream;
+  cProd<<<static_cast<unsigned>(M->nM), 128, 0, s>>>(M->C, xs, M->ysC, M->nM, 1, 1);
+  const int passes = (cornerRows + 15) / 16;
   if (cornerRows > 0) {
     const int qBlock = (nA + kCornerQ - 1) / kCornerQ >= 4LL * smCount(c.device) ? kCornerQ : 256;
     const int nblk = static_cast<int>((nA + qBlock - 1) / qBlock);
-    // 16 rows per pass keeps the kernel at 2 CTAs/SM; passes after the
-    // first accumulate into cT (stream order).
-    for (int r0 = 0; r0 < cornerRows; r0 += 16)
-      cornerFused<16><<<nblk, kFuseThreads, 0, s>>>(ca, x, M->xs, M->cornerPart, M->cornerT, nA, qBlock, nblk, r0,
-                                                    r0 > 0 ? 1 : 0);
+    // 16 rows per pass (blockIdx.y) keeps the kernel at 2 CTAs/SM.
+    cornerFused<16><<<dim3(nblk, passes), kFuseThreads, 0, s>>>(ca, x, xs, M->cornerPart, M->cornerT, nA, qBlock,
+                                                                nblk);
     cornerReduce<<<(cornerRows * 32 + 255) / 256, 256, 0, s>>>(ca, M->cornerPart, M->ys, 1, nblk);
-    cT = M->cornerT;
   }
   for (int b = 0; b < 2; ++b) {  // join
     TBT_CUDA_CHECK(cudaEventRecord(M->evJoin[b], M->branch[b]));
     TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, M->evJoin[b], 0));
   }
-  cProd<<<static_cast<unsigned>(M->nM), 128, 0, s>>>(M->C, M->xs, M->ys, M->nM, 1);
-  addBT1<<<gridFor(nA), 256, 0, s>>>(y, side ? M->zA : nullptr, row ? M->zA2 : nullptr, cT, nA);
-  marginScatter<<<gridFor(static_cast<long long>(c.neM) * m), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, 1);
+  const long long nPad = static_cast<long long>(c.neM) * m;
+  marginFinish1<<<gridFor(nA + nPad), 256, 0, s>>>(y, side ? M->zA : nullptr, row ? M->zA2 : nullptr, M->cornerT,
+                                                   cornerRows > 0 ? passes : 0, M->ys, M->ysC, nA, M->nM, nPad);
   TBT_CUDA_CHECK(cudaGetLastError());
   return true;
 }

@@ -35,7 +35,8 @@ struct MarginOp {
   double2* hatMsOut[2] = {nullptr, nullptr};    // [Ly][em]
   double2* hatMrOut[2] = {nullptr, nullptr};    // [Lx][em]
   double2 *bpartS = nullptr, *bpartR = nullptr; // B partials per (bin, row, chunk)
-  double2* cornerT = nullptr;                   // [nA] B^T corner contribution
+  double2* cornerT = nullptr;                   // [passes][nA] B^T corner contribution
+  double2* ysC = nullptr;                       // [nM] C xM (one column)
   int chunkS = 1, chunkR = 1;                   // q-chunks per bin
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;

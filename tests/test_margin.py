@@ -113,7 +113,11 @@ def test_margin_generator_layout():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nx,ny,m,e", SHAPES + [(8, 6, 64, [3, 5, 2, 4, 64, 6, 1, 7, 2])])
+# The last two shapes take the wide single-column kernels (9..16 rows per
+# margin part) and two corner passes (> 16 corner rows).
+@pytest.mark.parametrize("nx,ny,m,e", SHAPES + [(8, 6, 64, [3, 5, 2, 4, 64, 6, 1, 7, 2]),
+                                               (4, 3, 6, [5, 12, 6, 10, 6, 9, 5, 11, 4]),
+                                               (3, 7, 5, [9, 16, 1, 3, 5, 14, 8, 2, 0])])
 @pytest.mark.parametrize("k", [1, 3])
 def test_gpu_margin_apply(gpu, nx, ny, m, e, k):
     from paper_2506_04710_b200 import ToeplitzMatvec
