@@ -108,11 +108,11 @@ struct Ctx {
   unsigned* dGridBar = nullptr;            // grid barrier counter / generation
   unsigned long long* dBarFlags = nullptr; // flag-line grid barrier (matvec_persistent.cu)
   bool phaseTiming = false;
-  int prefetchAt = 0;
+  int prefetchAt = 0;                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 after columns
   long long zeroCopyL2Bytes = 0;  // set around zero-copy launches: spectrum bytes to prefetch into L2
-  bool zeroCopyStage = false;
-  bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)     // set around zero-copy launches: stage x in dXin for the correction reads
-  const int* skipFlag = nullptr;           // device flag: persistent applies become no-ops when set                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 none-early
+  bool zeroCopyStage = false;     // set around zero-copy launches: stage x in dXin for the correction reads
+  bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)
+  const int* skipFlag = nullptr;  // device flag: persistent applies become no-ops when set
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
   bool forceUnfused = false;               // TBT_GMRES=unfused: separate apply / Arnoldi launches
