@@ -138,31 +138,49 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // executed by one CTA: H(0..j, j), cs, sn staged in shared memory by all
 // threads, the sequential rotations by thread 0, results written back.
 // hcolIn (optional) already holds H(0..j, j) in shared memory.
-__device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn, const double2* hcolIn,
-                           double2* sh /* >= 3*RMAX+4 */) {
+// Split in two so callers can stage the inputs (givensStage, independent
+// of hn) before a grid barrier and finish after it.
+__device__ inline void givensStage(const GmresArgs& A, int col, int j, const double2* hcolIn, double2* sh) {
   const int ldh = A.restart + 1;
-  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
-  double2* cs = A.cs + static_cast<long long>(col) * A.restart;
-  double2* sn = A.sn + static_cast<long long>(col) * A.restart;
-  double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
+  const double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+  const double2* cs = A.cs + static_cast<long long>(col) * A.restart;
+  const double2* sn = A.sn + static_cast<long long>(col) * A.restart;
   double2* hc = sh;               // [j+2]
   double2* scs = sh + RMAX + 2;   // [j]
   double2* ssn = scs + RMAX;      // [j]
-  __syncthreads();
   for (int t = threadIdx.x; t <= j; t += blockDim.x) hc[t] = hcolIn ? hcolIn[t] : H[t + j * ldh];
   for (int t = threadIdx.x; t < j; t += blockDim.x) {
     scs[t] = cs[t];
     ssn[t] = sn[t];
   }
-  __syncthreads();
+}
+
+// Needs givensStage's shared-memory staging visible (a __syncthreads after it).
+__device__ inline void givensFinish(const GmresArgs& A, int col, int j, double hn, double2* sh) {
+  const int ldh = A.restart + 1;
+  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+  double2* cs = A.cs + static_cast<long long>(col) * A.restart;
+  double2* sn = A.sn + static_cast<long long>(col) * A.restart;
+  double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
+  double2* hc = sh;
+  double2* scs = sh + RMAX + 2;
+  double2* ssn = scs + RMAX;
   if (threadIdx.x == 0) {
     GmresState& st = A.st[col];
+    // Global state the tail needs, loaded before the sequential sweep so
+    // the loads overlap it.
+    const double beta = st.beta, beta0 = st.beta0;
+    const int iters = st.iterations;
+    const double2 gj = g[j];
     hc[j + 1] = make_double2(hn, 0.0);
+    // Rotations 0..j-1 with the running entry carried in registers.
+    double2 carry = hc[0];
     for (int i = 0; i < j; ++i) {
-      const double2 a0 = hc[i], a1 = hc[i + 1];
+      const double2 a0 = carry, a1 = hc[i + 1];
       hc[i] = cadd(cmul(scs[i], a0), cmul(ssn[i], a1));
-      hc[i + 1] = cadd(cmul(make_double2(-ssn[i].x, ssn[i].y), a0), cmul(cconj(scs[i]), a1));
+      carry = cadd(cmul(make_double2(-ssn[i].x, ssn[i].y), a0), cmul(cconj(scs[i]), a1));
     }
+    hc[j] = carry;
     const double2 hjj = hc[j], hj1 = hc[j + 1];
     const double den = sqrt((hjj.x * hjj.x + hjj.y * hjj.y) + (hj1.x * hj1.x + hj1.y * hj1.y));
     double2 c, s;
@@ -177,19 +195,26 @@ __device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn,
     sn[j] = s;
     hc[j] = cadd(cmul(c, hjj), cmul(s, hj1));
     hc[j + 1] = make_double2(0.0, 0.0);
-    const double2 gj = g[j];
     g[j] = cmul(c, gj);
     const double2 gj1 = cmul(make_double2(-s.x, s.y), gj);
     g[j + 1] = gj1;
-    st.iterations += 1;
+    st.iterations = iters + 1;
     st.ncount = j + 1;
-    const double rel = cabs2(gj1) / st.beta;
-    pushHist(A, col, 1.0, cabs2(gj1) / st.beta0);
-    if (rel < 0.1 * A.tol || !(hn > 0.0) || st.ncount >= A.restart || st.iterations >= A.maxIter) st.stopInner = 1;
+    const double rel = cabs2(gj1) / beta;
+    pushHist(A, col, 1.0, cabs2(gj1) / beta0);
+    if (rel < 0.1 * A.tol || !(hn > 0.0) || j + 1 >= A.restart || iters + 1 >= A.maxIter) st.stopInner = 1;
   }
   __syncthreads();
   for (int t = threadIdx.x; t <= j + 1; t += blockDim.x) H[t + j * ldh] = hc[t];
   __syncthreads();
+}
+
+__device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn, const double2* hcolIn,
+                                  double2* sh /* >= 3*RMAX+4 */) {
+  __syncthreads();
+  givensStage(A, col, j, hcolIn, sh);
+  __syncthreads();
+  givensFinish(A, col, j, hn, sh);
 }
 
 // cv[0..j] <- (I + L)^{-1} cv on one warp, L packed by rows (row i at
@@ -267,36 +292,47 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     vj[r] = Vj[r0 + r];
   }
   __syncthreads();
-  // Pass 1: dot k by warp k % 8; c_k in slot k, S_jk in slot lds + k.
-  for (int k = warp; k <= j; k += static_cast<int>(blockDim.x >> 5)) {
-    const double2* Vk = A.V + static_cast<long long>(k) * n + r0;
-    double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
-    int r = lane;
-    for (; r + 96 < cnt; r += 128) {
-      double2 v[4];
+  // Pass 1: warp w owns dots k = w, w + nw, ...; it takes them two at a
+  // time with 8 rows per lane per vector in flight (16 loads), c_k in slot
+  // k, S_jk in slot lds + k.
+  {
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    for (int k0 = warp; k0 <= j; k0 += 2 * nw) {
+      const int k1 = k0 + nw;
+      const bool two = k1 <= j;
+      const double2* V0 = A.V + static_cast<long long>(k0) * n + r0;
+      const double2* V1 = A.V + static_cast<long long>(two ? k1 : k0) * n + r0;
+      double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
+      for (int r = lane; r < cnt; r += 256) {
+        double2 v0[8], v1[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = Vk[r + 32 * u];
-      cfma_conj(c0, v[0], ws[r]);
-      cfma_conj(c1, v[1], ws[r + 32]);
-      cfma_conj(c0, v[2], ws[r + 64]);
-      cfma_conj(c1, v[3], ws[r + 96]);
-      if (k < j) {
-        cfma_conj(s0, vj[r], v[0]);
-        cfma_conj(s1, vj[r + 32], v[1]);
-        cfma_conj(s0, vj[r + 64], v[2]);
-        cfma_conj(s1, vj[r + 96], v[3]);
+        for (int u = 0; u < 8; ++u) {
+          const int rr = r + 32 * u;
+          v0[u] = rr < cnt ? V0[rr] : make_double2(0.0, 0.0);
+          v1[u] = rr < cnt && two ? V1[rr] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int rr = r + 32 * u;
+          if (rr < cnt) {
+            const double2 wv = ws[rr], vv = vj[rr];
+            cfma_conj(c0, v0[u], wv);
+            cfma_conj(s0, vv, v0[u]);
+            cfma_conj(c1, v1[u], wv);
+            cfma_conj(s1, vv, v1[u]);
+          }
+        }
       }
-    }
-    for (; r < cnt; r += 32) {
-      const double2 v = Vk[r];
-      cfma_conj(c0, v, ws[r]);
-      if (k < j) cfma_conj(s0, vj[r], v);
-    }
-    const double2 c = warpSum(cadd(c0, c1));
-    const double2 sjk = warpSum(cadd(s0, s1));
-    if (lane == 0) {
-      dotPart[static_cast<long long>(k) * gridDim.x + blockIdx.x] = c;
-      if (k < j) dotPart[static_cast<long long>(lds + k) * gridDim.x + blockIdx.x] = sjk;
+      const double2 t0 = warpSum(c0), u0 = warpSum(s0);
+      const double2 t1 = warpSum(c1), u1 = warpSum(s1);
+      if (lane == 0) {
+        dotPart[static_cast<long long>(k0) * gridDim.x + blockIdx.x] = t0;
+        if (k0 < j) dotPart[static_cast<long long>(lds + k0) * gridDim.x + blockIdx.x] = u0;
+        if (two) {
+          dotPart[static_cast<long long>(k1) * gridDim.x + blockIdx.x] = t1;
+          if (k1 < j) dotPart[static_cast<long long>(lds + k1) * gridDim.x + blockIdx.x] = u1;
+        }
+      }
     }
   }
   gridBarrier(bar);
@@ -349,6 +385,7 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     acc.x += wv.x * wv.x + wv.y * wv.y;
   }
   blockPartial(acc, scratch, partSlot(A, 0, 0));
+  if (blockIdx.x == 0) givensStage(A, 0, j, hcol, sh);  // made visible by the barrier
   gridBarrier(bar);
   mark(3);
   const double hn = sqrt(warpTotal(partSlot(A, 0, 0)).x);
@@ -356,7 +393,7 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     double2* vout = A.V + static_cast<long long>(j + 1) * n + r0;
     for (int r = threadIdx.x; r < cnt; r += blockDim.x) vout[r] = make_double2(ws[r].x / hn, ws[r].y / hn);
   }
-  if (blockIdx.x == 0) givensStep(A, 0, j, hn, hcol, sh);
+  if (blockIdx.x == 0) givensFinish(A, 0, j, hn, sh);
   if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t4;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t4));
