@@ -543,26 +543,18 @@ __global__ void __launch_bounds__(kFuseThreads, 2) cornerFused(CornerArgs ca, co
   __shared__ double2 red[(kFuseThreads / 32) * CR];
   __shared__ const double2* rowPtr[CR];
   __shared__ double2 mcs[CR];
-  __shared__ int sRows;
   const long long q0 = static_cast<long long>(blockIdx.x) * qBlock;
   const long long q1 = min(nA, q0 + qBlock);
-  if (threadIdx.x == 0) {  // flatten (corner, row) into u < rows
-    int v = 0, f = 0;
-    for (int c = 0; c < 4; ++c)
-      for (int i = 0; i < ca.em[c]; ++i, ++f)
-        if (f >= row0 && v < CR) {
-          rowPtr[v] = ca.bc[c] + static_cast<long long>(i) * nA;
-          mcs[v] = xs[ca.start[c] + i];
-          ++v;
-        }
-    sRows = v;
-    for (; v < CR; ++v) {  // dead rows: weight 0 on row 0 (cached)
-      rowPtr[v] = rowPtr[0];
-      mcs[v] = make_double2(0.0, 0.0);
-    }
+  const int rowsTot = ca.em[0] + ca.em[1] + ca.em[2] + ca.em[3];
+  const int rows = min(CR, rowsTot - row0);
+  if (threadIdx.x < CR) {  // slot u: flattened corner row row0 + u (dead slots re-read the first row, weight 0)
+    const int u = threadIdx.x;
+    int f = row0 + (u < rows ? u : 0), c = 0;
+    while (f >= ca.em[c]) f -= ca.em[c++];
+    rowPtr[u] = ca.bc[c] + static_cast<long long>(f) * nA;
+    mcs[u] = u < rows ? xs[ca.start[c] + f] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int rows = sRows;
   double2 pb[CR];
 #pragma unroll
   for (int u = 0; u < CR; ++u) pb[u] = make_double2(0.0, 0.0);
