@@ -1,7 +1,7 @@
 // C entry points into the reference's own FFT, compiled from
 // /root/reference/proj/src/fft.cpp by oracle/Makefile into
 // oracle/_ref/libref_fft.so. Test infrastructure: pins oracle.cpp's
-// restated radix2() (tests/test_oracle_pin.py).
+// restated radix2() (tests/test_oracle.py, tests/golden/ref_fft.npz).
 #include <complex>
 #include <cstddef>
 #include <stdexcept>
