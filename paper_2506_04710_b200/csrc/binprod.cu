@@ -135,6 +135,48 @@ binprodGeneric(const double2* __restrict__ S, const int* __restrict__ pairF, con
   }
 }
 
+// Any m <= 64, any nrhs: CTA per (pair, chunk of kMultiRc right-hand sides).
+// The m x m block (row stride ld = m | 1, odd, so a warp's row-owner reads
+// and column-owner reads both spread over the bank groups) and the chunk's
+// xhat_f / xhat_g columns are staged in shared memory; thread per output.
+constexpr int kMultiRc = 8;
+__global__ void __launch_bounds__(256)
+binprodMulti(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
+             long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int m, int nrhs) {
+  extern __shared__ double2 smb[];
+  const int ld = m | 1;
+  double2* sA = smb;                      // [m][ld]
+  double2* sxf = sA + m * ld;             // [RC][m]
+  double2* sxg = sxf + kMultiRc * m;      // [RC][m]
+  const int nch = (nrhs + kMultiRc - 1) / kMultiRc;
+  const long long B = static_cast<long long>(nrhs) * m;
+  for (long long item = blockIdx.x; item < npairs * nch; item += gridDim.x) {
+    const long long p = item / nch;
+    const int r0 = static_cast<int>(item % nch) * kMultiRc, rc = min(kMultiRc, nrhs - r0);
+    const long long f = pairF[p], g = pairG[p];
+    const double2* A = S + p * m * m;
+    __syncthreads();  // previous item's readers are done
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) sA[(q / m) * ld + q % m] = A[q];
+    for (int q = threadIdx.x; q < rc * m; q += blockDim.x) {
+      sxf[q] = xhat[f * B + static_cast<long long>(r0) * m + q];
+      sxg[q] = xhat[g * B + static_cast<long long>(r0) * m + q];
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < rc * m; o += blockDim.x) {  // yhat_f = A xhat_f
+      const int rhs = o / m, a = o % m;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int b = 0; b < m; ++b) cfma(acc, sA[a * ld + b], sxf[rhs * m + b]);
+      yhat[f * B + static_cast<long long>(r0) * m + o] = acc;
+    }
+    if (f != g)
+      for (int o = threadIdx.x; o < rc * m; o += blockDim.x) {  // yhat_g = A^T xhat_g
+        const int rhs = o / m, b = o % m;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int a = 0; a < m; ++a) cfma(acc, sA[a * ld + b], sxg[rhs * m + a]);
+        yhat[g * B + static_cast<long long>(r0) * m + o] = acc;
+      }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // K3 v2 (single RHS): persistent, warp-specialised, TMA-engine ring.
@@ -319,6 +361,20 @@ void launchBinProduct(Ctx& c, int nrhs) {
     case 3: launchTile<192, 32, 16>(c, nrhs); break;
     default: {
       const int sms = smCount(c.device);
+      if (c.m <= 64) {
+        const int ld = c.m | 1;
+        const size_t smem = (static_cast<size_t>(c.m) * ld + 2 * kMultiRc * c.m) * sizeof(double2);
+        static bool attr = false;
+        if (!attr) {
+          TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodMulti, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+          attr = true;
+        }
+        const long long items = c.npairs * ((nrhs + kMultiRc - 1) / kMultiRc);
+        const long long grid = std::min<long long>(items, 16LL * sms);
+        binprodMulti<<<static_cast<int>(grid), 256, smem, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,
+                                                                      c.dXhat, c.dYhat, c.m, nrhs);
+        break;
+      }
       const long long grid = std::min<long long>(c.npairs, 4LL * sms);
       binprodGeneric<<<static_cast<int>(grid), 128, 0, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,
                                                                   c.dXhat, c.dYhat, c.m, nrhs);

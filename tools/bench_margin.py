@@ -22,6 +22,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--edges", type=int, default=8)
 ap.add_argument("--no-cpu", action="store_true")
 ap.add_argument("--schur", action="store_true", help="also time schurSolve (needs a config whose A-solves converge, e.g. C1)")
+ap.add_argument("--schur-batch", type=int, default=0, help="max_nrhs of the Schur context (default: all inner columns)")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 e = [args.edges] * 9
@@ -81,7 +82,10 @@ if not args.no_cpu:
     out["parity_rel_err"] = float(np.linalg.norm(yd - ref) / np.linalg.norm(ref))
 if args.schur:
     rep.correction = None  # schurSolve's A block is applyA (linsolve.cpp:644)
-    ops = ToeplitzMatvec(rep, max_nrhs=64)
+    # One lockstep batch for all p + nM inner columns (schurSolve batches by
+    # the context's max_nrhs).
+    nm = ToeplitzMatvec(rep, max_nrhs=1).sizeM()
+    ops = ToeplitzMatvec(rep, max_nrhs=args.schur_batch or (cfg.nrhs + nm))
     V = np.zeros((ops.size(), cfg.nrhs), complex)
     V[:cfg.n] = gen.rhs_normal(cfg.n, cfg.nrhs, 4)
     sopt = SolverOptions(tol=cfg.tol, maxIter=cfg.max_iter, restart=cfg.restart)
