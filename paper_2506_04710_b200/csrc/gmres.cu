@@ -843,8 +843,7 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldi(GmresArgs A) {
 // per column stages the triangle of H in shared memory; warp 0 then solves
 // with its rows in registers.
 __global__ void __launch_bounds__(kThreads) gmresUpdate(GmresArgs A) {
-  extern __shared__ double2 shH[];  // [(restart+1)*restart] + [restart] y
-  __shared__ int sFlagU[1];
+  extern __shared__ double2 shH[];  // [(restart+1)*restart]
   const int ldh = A.restart + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int RPL = RMAX / 32;  // rows per lane
@@ -883,31 +882,27 @@ __global__ void __launch_bounds__(kThreads) gmresUpdate(GmresArgs A) {
     }
   }
   gridBarrier(A.bar);
+  // x += V y over all (slot, column) entries at once (internal layout
+  // [e][col][a]); y and the column state come through L1.
   const long long slots = static_cast<long long>(A.ne) * A.m;
   const long long nall = slots * A.ncols;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  double2* sy = shH;  // reuse: y of the current column
-  for (int col = 0; col < A.ncols; ++col) {
-    __syncthreads();
-    if (threadIdx.x == 0) sFlagU[0] = A.st[col].cycleActive;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < nall; q += stride) {
+    const int col = static_cast<int>((q / A.m) % A.ncols);
+    if (!A.st[col].cycleActive) continue;
     const int nc = A.st[col].ncount;
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) sy[i] = __ldcg(A.ycoef + static_cast<long long>(col) * A.restart + i);
-    __syncthreads();
-    if (!sFlagU[0]) continue;
-    for (long long s = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; s < slots; s += stride) {
-      const long long q = slotIndex(s, col, A.ncols, A.m);
-      double2 xv = A.x[q];
-      int i = 0;
-      for (; i + 8 <= nc; i += 8) {
-        double2 v[8];
+    const double2* sy = A.ycoef + static_cast<long long>(col) * A.restart;
+    double2 xv = A.x[q];
+    int i = 0;
+    for (; i + 8 <= nc; i += 8) {
+      double2 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = A.V[static_cast<long long>(i + u) * nall + q];
+      for (int u = 0; u < 8; ++u) v[u] = A.V[static_cast<long long>(i + u) * nall + q];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv = cadd(xv, cmul(sy[i + u], v[u]));
-      }
-      for (; i < nc; ++i) xv = cadd(xv, cmul(sy[i], A.V[static_cast<long long>(i) * nall + q]));
-      A.x[q] = xv;
+      for (int u = 0; u < 8; ++u) xv = cadd(xv, cmul(__ldcg(sy + i + u), v[u]));
     }
+    for (; i < nc; ++i) xv = cadd(xv, cmul(__ldcg(sy + i), A.V[static_cast<long long>(i) * nall + q]));
+    A.x[q] = xv;
   }
 }
 
