@@ -109,8 +109,8 @@ __global__ void luSolveCols(const double2* __restrict__ LU, const int* __restric
 // The whole factorisation in one CTA (small n): the same pivot rule and
 // update order as luPivot / luUpdate, barriers instead of launches.
 __global__ void __launch_bounds__(1024) luFactorSmall(double2* __restrict__ S, int n, int* __restrict__ perm) {
-  __shared__ double bestV[1024];
-  __shared__ int bestI[1024];
+  __shared__ double bestV[32];
+  __shared__ int bestI[33];
   for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
@@ -124,21 +124,37 @@ __global__ void __launch_bounds__(1024) luFactorSmall(double2* __restrict__ S, i
         bi = i;
       }
     }
-    bestV[threadIdx.x] = bv;
-    bestI[threadIdx.x] = bi;
+    // Largest |v|, ties to the lowest row: warp shuffles, then warp 0 over
+    // the per-warp winners.
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      bestV[threadIdx.x >> 5] = bv;
+      bestI[threadIdx.x >> 5] = bi;
+    }
     __syncthreads();
-    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-      if (threadIdx.x < off) {
-        const double ov = bestV[threadIdx.x + off];
-        const int oi = bestI[threadIdx.x + off];
-        if (ov > bestV[threadIdx.x] || (ov == bestV[threadIdx.x] && oi < bestI[threadIdx.x])) {
-          bestV[threadIdx.x] = ov;
-          bestI[threadIdx.x] = oi;
+    if (threadIdx.x < 32) {
+      const int nw = static_cast<int>(blockDim.x >> 5);
+      bv = threadIdx.x < nw ? bestV[threadIdx.x] : -1.0;
+      bi = threadIdx.x < nw ? bestI[threadIdx.x] : n;
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
         }
       }
-      __syncthreads();
+      if (threadIdx.x == 0) bestI[32] = bi;
     }
-    const int p = bestI[0];
+    __syncthreads();
+    const int p = bestI[32];
     if (p != k && p < n) {
       for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const long long a = k + static_cast<long long>(j) * n, b = p + static_cast<long long>(j) * n;
