@@ -146,6 +146,15 @@ long long tbt_size_m(const tbt_ctx* ctx);
  * (array_model.cpp:218-228); tbt_apply_a and use_a_only solves keep n. */
 tbt_status tbt_set_margin(tbt_ctx* ctx, const int* e, const double* bside, const double* brow,
                           const double* bcorner, const double* cmat);
+/* The margin blocks alone (ToeplitzMatvec::applyB / applyBT / applyC,
+ * linsolve.hpp:66-68; linsolve.cpp:292-314, 316-334, 336-349):
+ *   tbt_apply_b   yM = B xA      x: n   x nrhs, y: n_m x nrhs
+ *   tbt_apply_bt  yA = B^T xM    x: n_m x nrhs, y: n   x nrhs
+ *   tbt_apply_c   yM = C xM      x: n_m x nrhs, y: n_m x nrhs
+ * column-major in `where` memory; user error without margin parts. */
+tbt_status tbt_apply_b(tbt_ctx* ctx, const double* x, double* y, int nrhs, int where);
+tbt_status tbt_apply_bt(tbt_ctx* ctx, const double* x, double* y, int nrhs, int where);
+tbt_status tbt_apply_c(tbt_ctx* ctx, const double* x, double* y, int nrhs, int where);
 
 /* Restarted GMRES with x0 = 0 for nrhs columns in lockstep. b, x are
  * n x nrhs column-major in `where` memory. Returns TBT_NUMERIC_ERROR when a

@@ -85,6 +85,9 @@ class ToeplitzMatvec {
 
   Vector apply(const Vector& x) const { return run(tbt_apply, x, size()); }     // linsolve.hpp:64
   Vector applyA(const Vector& x) const { return run(tbt_apply_a, x, sizeA()); } // linsolve.hpp:65
+  Vector applyB(const Vector& xA) const { return run(tbt_apply_b, xA, sizeA(), sizeM()); }   // linsolve.hpp:66
+  Vector applyBT(const Vector& xM) const { return run(tbt_apply_bt, xM, sizeM(), sizeA()); } // linsolve.hpp:67
+  Vector applyC(const Vector& xM) const { return run(tbt_apply_c, xM, sizeM(), sizeM()); }   // linsolve.hpp:68
   Vector diagonal() const {                                                      // linsolve.hpp:69
     Vector d(static_cast<size_t>(size()));
     check(tbt_diagonal(ctx_, reinterpret_cast<double*>(d.data())));
@@ -97,9 +100,9 @@ class ToeplitzMatvec {
 
  private:
   using Fn = tbt_status (*)(tbt_ctx*, const double*, double*, int, int);
-  Vector run(Fn fn, const Vector& x, long n) const {
+  Vector run(Fn fn, const Vector& x, long n, long nOut = -1) const {
     if (static_cast<long>(x.size()) != n) throw UserError("matvec: vector length mismatch");
-    Vector y(x.size());
+    Vector y(static_cast<size_t>(nOut < 0 ? n : nOut));
     check(fn(ctx_, reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data()), 1, TBT_HOST));
     return y;
   }

@@ -53,6 +53,9 @@ SIGNATURES = {
     "tbt_precompute": (C.c_int, [C.c_void_p]),
     "tbt_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "tbt_apply_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "tbt_apply_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "tbt_apply_bt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "tbt_apply_c": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "tbt_diagonal": (C.c_int, [C.c_void_p, dp]),
     "tbt_size_a": (C.c_longlong, [C.c_void_p]),
     "tbt_size_m": (C.c_longlong, [C.c_void_p]),

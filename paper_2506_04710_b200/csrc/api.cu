@@ -685,6 +685,50 @@ tbt_status tbt_apply_a(tbt_ctx* h, const double* x, double* y, int nrhs, int whe
   return applyCommon(h, x, y, nrhs, where, false);
 }
 
+// One margin block: the input is embedded in a full [xA; xM] vector with the
+// other part zero and only the margin products run (marginApply on a zero
+// y): y = [B^T xM ; B xA + C xM], from which the requested part is read.
+//   part 0: B (xA -> yM), 1: B^T (xM -> yA), 2: C (xM -> yM)
+static tbt_status applyMarginPart(tbt_ctx* h, const double* x, double* y, int nrhs, int where, int part) {
+  static const char* names[3] = {"tbt_apply_b", "tbt_apply_bt", "tbt_apply_c"};
+  return guarded([&] {
+    TBT_USER_CHECK(h && x && y, std::string(names[part]) + ": null argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(c.margin && c.nM > 0, std::string(names[part]) + ": no margin parts (tbt_set_margin)");
+    TBT_USER_CHECK(nrhs >= 1 && nrhs <= c.maxNrhs, std::string(names[part]) + ": nrhs outside [1, max_nrhs]");
+    TBT_USER_CHECK(where == TBT_HOST || where == TBT_DEVICE, std::string(names[part]) + ": bad memory kind");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    const long long nA = c.n, nM = c.nM, nU = nA + nM, nInt = static_cast<long long>(c.ne + c.neM) * c.m;
+    const long long inOff = part == 0 ? 0 : nA, inRows = part == 0 ? nA : nM;
+    const long long outOff = part == 1 ? 0 : nA, outRows = part == 1 ? nA : nM;
+    const cudaMemcpyKind in = where == TBT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind out = where == TBT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    cudaStream_t s = c.stream;
+    // [xA; xM] user layout (nU rows per column) in dYout, then internal in dXin.
+    TBT_CUDA_CHECK(cudaMemsetAsync(c.dYout, 0, static_cast<size_t>(nU) * nrhs * sizeof(double2), s));
+    TBT_CUDA_CHECK(cudaMemcpy2DAsync(c.dYout + inOff, nU * sizeof(double2), x, inRows * sizeof(double2),
+                                     inRows * sizeof(double2), nrhs, in, s));
+    launchLayoutU(c.dYout, c.dXin, nU, nInt, nrhs, true, s, c.m);
+    TBT_CUDA_CHECK(cudaMemsetAsync(c.dYout, 0, static_cast<size_t>(nInt) * nrhs * sizeof(double2), s));
+    marginApply(c, c.dXin, c.dYout, nrhs);
+    launchLayoutU(c.dYout, c.dXin, nU, nInt, nrhs, false, s, c.m);
+    TBT_CUDA_CHECK(cudaMemcpy2DAsync(y, outRows * sizeof(double2), c.dXin + outOff, nU * sizeof(double2),
+                                     outRows * sizeof(double2), nrhs, out, s));
+    if (where == TBT_HOST) TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+tbt_status tbt_apply_b(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
+  return applyMarginPart(h, x, y, nrhs, where, 0);
+}
+tbt_status tbt_apply_bt(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
+  return applyMarginPart(h, x, y, nrhs, where, 1);
+}
+tbt_status tbt_apply_c(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
+  return applyMarginPart(h, x, y, nrhs, where, 2);
+}
+
 tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
   return guarded([&] {
     TBT_USER_CHECK(h && d, "tbt_diagonal: null argument");

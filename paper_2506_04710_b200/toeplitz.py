@@ -218,20 +218,31 @@ class ToeplitzMatvec:
         """Unknowns of apply / diagonal / gmres: sizeA() + sizeM()."""
         return self.sizeA() + self.sizeM()
 
-    def _apply(self, fn, x, full: bool):
+    def _apply(self, fn, x, n: int, n_out: int | None = None):
         xc, k, vec = _as_cols(x)
-        n = self.size() if full else self.sizeA()
         if xc.shape[0] != n:
             raise UserError(f"matvec: vector length {xc.shape[0]} does not match system size {n}")
-        y = np.empty_like(xc, order="F")
+        y = np.empty((n if n_out is None else n_out, k), dtype=np.complex128, order="F")
         _check(fn(self._h, xc.ctypes.data, y.ctypes.data, k, TBT_HOST))
         return y[:, 0] if vec else y
 
     def apply(self, x):
-        return self._apply(lib().tbt_apply, x, True)
+        return self._apply(lib().tbt_apply, x, self.size())
 
     def applyA(self, x):
-        return self._apply(lib().tbt_apply_a, x, False)
+        return self._apply(lib().tbt_apply_a, x, self.sizeA())
+
+    def applyB(self, xA):
+        """yM = B xA (linsolve.hpp:66, linsolve.cpp:292-314)."""
+        return self._apply(lib().tbt_apply_b, xA, self.sizeA(), self.sizeM())
+
+    def applyBT(self, xM):
+        """yA = B^T xM (linsolve.hpp:67, linsolve.cpp:316-334)."""
+        return self._apply(lib().tbt_apply_bt, xM, self.sizeM(), self.sizeA())
+
+    def applyC(self, xM):
+        """yM = C xM (linsolve.hpp:68, linsolve.cpp:336-349)."""
+        return self._apply(lib().tbt_apply_c, xM, self.sizeM(), self.sizeM())
 
     def diagonal(self) -> np.ndarray:
         d = np.empty(self.size(), dtype=np.complex128)

@@ -137,6 +137,41 @@ def test_gpu_margin_apply(gpu, nx, ny, m, e, k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,m,e", SHAPES[:4] + [(4, 3, 6, [5, 12, 6, 10, 6, 9, 5, 11, 4])])
+@pytest.mark.parametrize("k", [1, 2])
+def test_gpu_margin_blocks(gpu, nx, ny, m, e, k):
+    """applyB / applyBT / applyC (linsolve.hpp:66-68) against the oracle's
+    full operator on [xA; 0] and [0; xM]."""
+    from paper_2506_04710_b200 import ToeplitzMatvec
+    rep = rep_with_margin(nx, ny, m, e)
+    op = ToeplitzMatvec(rep, max_nrhs=k)
+    o = oracle.Oracle.from_rep(rep)
+    nA, nM = op.sizeA(), op.sizeM()
+    X = gen.rhs_normal(nA + nM, k, 17)
+    for c in range(k):
+        xa = np.concatenate([X[:nA, c], np.zeros(nM, complex)])
+        xm = np.concatenate([np.zeros(nA, complex), X[nA:, c]])
+        ya, ym = o.apply(xa), o.apply(xm)
+        got_b = op.applyB(X[:nA, c:c + 1])[:, 0] if k > 1 else op.applyB(X[:nA, c])
+        got_bt = op.applyBT(X[nA:, c:c + 1])[:, 0] if k > 1 else op.applyBT(X[nA:, c])
+        got_c = op.applyC(X[nA:, c:c + 1])[:, 0] if k > 1 else op.applyC(X[nA:, c])
+        for got, ref in ((got_b, ya[nA:]), (got_bt, ym[:nA]), (got_c, ym[nA:])):
+            assert np.linalg.norm(got - ref) <= 1e-11 * max(np.linalg.norm(ref), 1e-300)
+    Yb = op.applyB(X[:nA])  # all columns at once
+    assert Yb.shape == (nM, k)
+
+
+@pytest.mark.gpu
+def test_gpu_margin_blocks_need_margin(gpu):
+    from paper_2506_04710_b200 import ToeplitzMatvec, UserError
+    rep = rep_with_margin(4, 3, 6, SHAPES[0][3])
+    rep.margin = None
+    op = ToeplitzMatvec(rep)
+    with pytest.raises(UserError):
+        op.applyB(np.zeros(op.sizeA(), complex))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("k,orthog", [(1, 1), (3, 1), (2, 0)])
 def test_gpu_margin_gmres(gpu, k, orthog):
     from paper_2506_04710_b200 import ToeplitzMatvec
