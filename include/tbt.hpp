@@ -109,19 +109,24 @@ class ToeplitzMatvec {
   tbt_ctx* ctx_ = nullptr;
 };
 
-// iterativeSolve (linsolve.hpp:88-89): columns of V, throws NumericError if
-// any column did not converge (linsolve.cpp:591).
-inline SolveResult iterativeSolve(ToeplitzMatvec& op, const std::vector<Vector>& V, const SolverOptions& opt) {
+namespace detail {
+using SolveFn = tbt_status (*)(tbt_ctx*, const double*, double*, int, const tbt_gmres_opts*, tbt_gmres_stats*, int);
+inline SolveResult solveColumns(SolveFn fn, ToeplitzMatvec& op, const std::vector<Vector>& V,
+                                const SolverOptions& opt) {
   const int p = static_cast<int>(V.size());
   const long n = op.size();
   std::vector<Complex> b(static_cast<size_t>(n) * p), x(b.size());
-  for (int c = 0; c < p; ++c) std::copy(V[c].begin(), V[c].end(), b.begin() + static_cast<long>(c) * n);
+  for (int c = 0; c < p; ++c) {
+    if (static_cast<long>(V[c].size()) != n) throw UserError("solve: excitation length mismatch");
+    std::copy(V[c].begin(), V[c].end(), b.begin() + static_cast<long>(c) * n);
+  }
   tbt_gmres_opts o{opt.tol, opt.maxIter, opt.restart, opt.precondition ? 1 : 0, 0, 0, 1};
   std::vector<int> its(p), conv(p), hlen(p);
   std::vector<double> res(p);
   tbt_gmres_stats st{its.data(), res.data(), conv.data(), nullptr, hlen.data(), 0};
-  const tbt_status s = tbt_gmres(op.handle(), reinterpret_cast<const double*>(b.data()),
-                                 reinterpret_cast<double*>(x.data()), p, &o, &st, TBT_HOST);
+  const tbt_status s =
+      fn(op.handle(), reinterpret_cast<const double*>(b.data()), reinterpret_cast<double*>(x.data()), p, &o, &st,
+         TBT_HOST);
   SolveResult out;
   for (int c = 0; c < p; ++c)
     out.current.emplace_back(x.begin() + static_cast<long>(c) * n, x.begin() + static_cast<long>(c + 1) * n);
@@ -130,5 +135,21 @@ inline SolveResult iterativeSolve(ToeplitzMatvec& op, const std::vector<Vector>&
   check(s);
   return out;
 }
+}  // namespace detail
+
+// iterativeSolve (linsolve.hpp:88-89): columns of V, throws NumericError if
+// any column did not converge (linsolve.cpp:591).
+inline SolveResult iterativeSolve(ToeplitzMatvec& op, const std::vector<Vector>& V, const SolverOptions& opt) {
+  return detail::solveColumns(tbt_gmres, op, V, opt);
+}
+
+// schurSolve (linsolve.hpp:93-95, linsolve.cpp:595-682): V vanishes on the
+// margin rows; NumericError on an unconverged inner solve or a singular S.
+inline SolveResult schurSolve(ToeplitzMatvec& op, const std::vector<Vector>& V, const SolverOptions& opt) {
+  return detail::solveColumns(tbt_schur_solve, op, V, opt);
+}
+
+// toeplitzMatvec (linsolve.hpp:80-81): one-shot apply.
+inline Vector toeplitzMatvec(ToeplitzMatvec& op, const Vector& x) { return op.apply(x); }
 
 }  // namespace tbt

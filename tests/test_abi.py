@@ -64,7 +64,11 @@ def test_cpp_mirror_compiles(tmp_path):
                    '  std::vector<tbt::Complex> gen(1);\n'
                    '  try { tbt::ToeplitzMatvec op(1, 1, 1, gen); int e[9] = {0};\n'
                    '        e[4] = 1; op.setMargin(e, nullptr, nullptr, nullptr, nullptr);\n'
-                   '        op.precompute(); (void)op.apply(tbt::Vector(op.size())); }\n'
+                   '        op.precompute(); (void)op.apply(tbt::Vector(op.size()));\n'
+                   '        (void)op.applyB(tbt::Vector(op.sizeA())); (void)op.applyBT(tbt::Vector(op.sizeM()));\n'
+                   '        (void)op.applyC(tbt::Vector(op.sizeM())); (void)tbt::toeplitzMatvec(op, tbt::Vector(op.size()));\n'
+                   '        tbt::SolverOptions so; std::vector<tbt::Vector> V(1, tbt::Vector(op.size()));\n'
+                   '        (void)tbt::iterativeSolve(op, V, so); (void)tbt::schurSolve(op, V, so); }\n'
                    '  catch (const std::exception&) {}\n'
                    '  return 0;\n'
                    '}\n')
