@@ -8,6 +8,7 @@
 #include <cstring>
 #include <fstream>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -246,7 +247,22 @@ using namespace tbt;
 
 struct tbt_ctx {
   Ctx c;
+  // One call at a time per context: the reference's apply is re-entrant
+  // (per-call scratch, linsolve.cpp:263-265) and is called from parallelFor
+  // workers; here the device buffers, stream and graphs are per context, so
+  // concurrent callers on one context are serialised (use one context per
+  // thread for concurrency).
+  std::recursive_mutex mu;
 };
+
+namespace {
+template <typename Fn>
+tbt_status guardedCtx(tbt_ctx* h, Fn&& fn) {
+  if (!h) return guarded(fn);  // fn reports the null argument
+  std::lock_guard<std::recursive_mutex> lock(h->mu);
+  return guarded(fn);
+}
+}  // namespace
 
 extern "C" {
 
@@ -377,7 +393,7 @@ void tbt_destroy(tbt_ctx* h) {
 }
 
 tbt_status tbt_set_stream(tbt_ctx* h, void* stream) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_set_stream: null context");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -402,7 +418,7 @@ long long tbt_size_m(const tbt_ctx* h) { return h ? h->c.nM : 0; }
 
 tbt_status tbt_set_margin(tbt_ctx* h, const int* e, const double* bside, const double* brow, const double* bcorner,
                           const double* cmat) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && e, "tbt_set_margin: null argument");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
@@ -433,7 +449,7 @@ tbt_status tbt_set_margin(tbt_ctx* h, const int* e, const double* bside, const d
 }
 
 tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblocks) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && blocks, "tbt_set_generators: null argument");
     Ctx& c = h->c;
     const long long want = static_cast<long long>(c.nx) * c.ny + static_cast<long long>(c.nx - 1) * (c.ny - 1);
@@ -457,7 +473,7 @@ tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblock
 }
 
 tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const double* u, const double* v) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_set_correction: null context");
     Ctx& c = h->c;
     TBT_USER_CHECK(rank >= 0, "tbt_set_correction: rank must be >= 0");
@@ -574,7 +590,7 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
 }
 
 tbt_status tbt_precompute(tbt_ctx* h) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_precompute: null context");
     Ctx& c = h->c;
     TBT_USER_CHECK(c.haveGenerators && c.dGen, "tbt_precompute: call tbt_set_generators first");
@@ -591,7 +607,7 @@ tbt_status tbt_precompute(tbt_ctx* h) {
 }
 
 static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, int where, bool withCorr) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && x && y, "tbt_apply: null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -691,7 +707,7 @@ tbt_status tbt_apply_a(tbt_ctx* h, const double* x, double* y, int nrhs, int whe
 //   part 0: B (xA -> yM), 1: B^T (xM -> yA), 2: C (xM -> yM)
 static tbt_status applyMarginPart(tbt_ctx* h, const double* x, double* y, int nrhs, int where, int part) {
   static const char* names[3] = {"tbt_apply_b", "tbt_apply_bt", "tbt_apply_c"};
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && x && y, std::string(names[part]) + ": null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -730,7 +746,7 @@ tbt_status tbt_apply_c(tbt_ctx* h, const double* x, double* y, int nrhs, int whe
 }
 
 tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && d, "tbt_diagonal: null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -745,7 +761,7 @@ tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
 tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt_gmres_opts* opts,
                      tbt_gmres_stats* stats, int where) {
   std::string failure;
-  tbt_status st = guarded([&] {
+  tbt_status st = guardedCtx(h, [&] {
     TBT_USER_CHECK(h && b && x && opts, "tbt_gmres: null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -817,7 +833,7 @@ tbt_status tbt_gmres(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt
 
 tbt_status tbt_schur_solve(tbt_ctx* h, const double* b, double* x, int nrhs, const tbt_gmres_opts* opts,
                            tbt_gmres_stats* stats, int where) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && b && x && opts, "tbt_schur_solve: null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -920,7 +936,7 @@ tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside, double* 
 }
 
 tbt_status tbt_save_spectra(tbt_ctx* h, const char* path) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && path, "tbt_save_spectra: null argument");
     TBT_CUDA_CHECK(cudaSetDevice(h->c.device));
     saveSpectra(h->c, path);
@@ -928,7 +944,7 @@ tbt_status tbt_save_spectra(tbt_ctx* h, const char* path) {
 }
 
 tbt_status tbt_load_spectra(tbt_ctx* h, const char* path) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && path, "tbt_load_spectra: null argument");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
@@ -990,7 +1006,7 @@ struct Out {
 
 tbt_status tbt_port_network(tbt_ctx* h, const double* current, long long ld, int p, const long long* feed_rows,
                             double edge_len, const double* z0, double* y, double* z, double* s, int where) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && current && feed_rows && z0 && y && z && s, "tbt_port_network: null argument");
     Ctx& c = h->c;
     TBT_USER_CHECK(p >= 1 && ld >= 1, "tbt_port_network: bad sizes");
@@ -1041,7 +1057,7 @@ tbt_status tbt_array_farfield(tbt_ctx* h, const double* const* tensors_co, const
                               const int* e, int ndir, const double* dirs, double dx, double dy, double k, double eta,
                               const double* current, int p, const double* weights, int q, double* co, double* cx,
                               int where) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && tensors_co && tensors_cx && e && dirs && current && weights && co && cx,
                    "tbt_array_farfield: null argument");
     Ctx& c = h->c;
@@ -1099,7 +1115,7 @@ tbt_status tbt_get_info(const tbt_ctx* h, tbt_info* info) {
 }
 
 tbt_status tbt_get_spectrum_bin(tbt_ctx* h, long long f, double* out) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && out, "tbt_get_spectrum_bin: null argument");
     Ctx& c = h->c;
     requireReady(c);
@@ -1118,7 +1134,7 @@ tbt_status tbt_get_spectrum_bin(tbt_ctx* h, long long f, double* out) {
 }
 
 tbt_status tbt_set_timing(tbt_ctx* h, int on) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_set_timing: null context");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -1128,7 +1144,7 @@ tbt_status tbt_set_timing(tbt_ctx* h, int on) {
 }
 
 tbt_status tbt_timing_read(tbt_ctx* h, double* total, int* count) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && total && count, "tbt_timing_read: null argument");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -1168,7 +1184,7 @@ tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin, i
 }
 
 tbt_status tbt_dist_init(tbt_ctx* h, int nranks, int rank, const char* id) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && id, "tbt_dist_init: null argument");
     Ctx& c = h->c;
     TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
@@ -1217,7 +1233,7 @@ tbt_status tbt_dist_rows(const tbt_ctx* h, int* row_begin, int* row_end) {
 }
 
 tbt_status tbt_phase_times(tbt_ctx* h, int on, double* out_us) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_phase_times: null context");
     Ctx& c = h->c;
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
@@ -1243,7 +1259,7 @@ tbt_status tbt_phase_times(tbt_ctx* h, int on, double* out_us) {
 
 tbt_status tbt_bench_apply(tbt_ctx* h, const double* x_dev, double* y_dev, int nrhs, int iters, int use_graph,
                            double* out_ms, double* out_binprod_ms) {
-  return guarded([&] {
+  return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && x_dev && y_dev && iters >= 1, "tbt_bench_apply: bad argument");
     Ctx& c = h->c;
     requireReady(c);

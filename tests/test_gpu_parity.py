@@ -336,3 +336,31 @@ def test_zero_copy_pinned_apply(gpu, corr):
     o = oracle.Oracle.from_rep(rep, nthreads=0)
     ref = o.apply(x)
     assert rel(yh.numpy(), ref) < MATVEC_TOL
+
+
+@pytest.mark.gpu
+def test_concurrent_callers_one_context(gpu):
+    """The reference calls apply from parallelFor workers (linsolve.cpp:572);
+    concurrent callers on one context are serialised by the context lock and
+    every result matches a serial apply."""
+    import threading
+    rep = ToeplitzRep.synthetic(Config("thr", 6, 5, 8, 1, 2, 21, "normal", 20))
+    op = ToeplitzMatvec(rep)
+    xs = [gen.rhs_normal(op.size(), 1, 40 + t)[:, 0] for t in range(4)]
+    ref = [op.apply(x) for x in xs]
+    errors = []
+
+    def worker(t):
+        try:
+            for _ in range(25):
+                if not np.array_equal(op.apply(xs[t]), ref[t]):
+                    errors.append(t)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
