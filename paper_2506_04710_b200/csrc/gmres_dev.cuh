@@ -255,14 +255,15 @@ __device__ __forceinline__ void forwardSubstWarp(double2* cv, const double2* sL,
 // coefficients h_i = <v_i, (I - v_{i-1}v_{i-1}^H)...(I - v_0 v_0^H) w> are
 // obtained as h = (I + L)^{-1} c with c = V^H w and L the strictly lower
 // part of the basis Gram matrix V^H V (identical to the MGS sweep in exact
-// arithmetic; L accumulates one row per iteration). Three grid barriers per
+// arithmetic; L accumulates one row per iteration). Two grid barriers per
 // step instead of j + 2:
 //   pass 1  per-CTA partials of c_k = <v_k, w> and S_jk = <v_j, v_k>
-//           (one warp per k, the CTA's row chunk of w and v_j in smem)
-//   -- barrier --  CTA k reduces dot k over the grid
-//   -- barrier --  every CTA: forward substitution for h (warp 0)
+//           (a warp per two k, the CTA's row chunk of w and v_j in smem)
+//   -- barrier --  every CTA reduces every dot (fixed order, same bits),
+//                  forward substitution for h (warp 0)
 //   pass 2  w' = w - V h, ||w'||^2
 //   -- barrier --  v_{j+1} = w' / ||w'||, Givens (CTA 0)
+// (`dots` is unused since the totals stay in shared memory.)
 // shw: dynamic shared memory of arnoldiLSSmem(chunk) double2; scratch:
 // blockDim/32 entries; hcol: RMAX+2; sh: 3*RMAX+4.
 __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, double2* dotPart, double2* shw,
@@ -337,25 +338,52 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   }
   gridBarrier(bar);
   mark(1);
-  // Grid totals: CTA d reduces dot d (c_0..c_j, then S_j0..S_j,j-1).
-  const int ndots = 2 * j + 1;
-  for (int d = blockIdx.x; d < ndots; d += gridDim.x) {
-    const int slot = d <= j ? d : lds + (d - j - 1);
-    if (warp == 0) {
-      const double2 t = warpTotal(dotPart + static_cast<long long>(slot) * gridDim.x);
-      if (lane == 0) {
-        dots[slot] = t;
-        if (d > j) S[static_cast<long long>(j) * lds + (d - j - 1)] = t;
+  // Grid totals, reduced by EVERY CTA itself (no second grid barrier):
+  // 16 lanes per dot slot, 2 slots per warp; lane q of a group sums the
+  // partials q, q+16, ... in order, then a 4-step butterfly — the same bits
+  // in every CTA. Slots: c_0..c_j, then S_j0..S_j,j-1 (CTA 0 also records
+  // row j of S for the later iterations).
+  double2* sL = cv + RMAX + 1;  // lower triangle of L, packed rows: row i at i*(i-1)/2
+  {
+    const int ndots = 2 * j + 1;
+    const int grp = lane >> 4, gl = lane & 15;
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    const int G = static_cast<int>(gridDim.x);
+    for (int d0 = warp * 2; d0 < ndots; d0 += nw * 2) {
+      const int d = d0 + grp;
+      double2 t = make_double2(0.0, 0.0);
+      if (d < ndots) {
+        const double2* pp = dotPart + static_cast<long long>(d <= j ? d : lds + (d - j - 1)) * G;
+        double2 v[10];
+        for (int k0 = gl; k0 < G; k0 += 160) {
+#pragma unroll
+          for (int q = 0; q < 10; ++q) {
+            const int k = k0 + 16 * q;
+            v[q] = k < G ? __ldcg(pp + k) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int q = 0; q < 10; ++q) t = cadd(t, v[q]);
+        }
+      }
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) {
+        t.x += __shfl_xor_sync(0xffffffffu, t.x, off);
+        t.y += __shfl_xor_sync(0xffffffffu, t.y, off);
+      }
+      if (gl == 0 && d < ndots) {
+        if (d <= j) {
+          cv[d] = t;
+        } else {
+          sL[j * (j - 1) / 2 + (d - j - 1)] = t;
+          if (blockIdx.x == 0) S[static_cast<long long>(j) * lds + (d - j - 1)] = t;
+        }
       }
     }
   }
-  gridBarrier(bar);
   mark(2);
-  // Stage the lower triangle rows 1..j of L (shared memory after cv).
-  double2* sL = cv + RMAX + 1;  // packed rows: row i at i*(i-1)/2
-  for (int i = 1 + warp; i <= j; i += static_cast<int>(blockDim.x >> 5))  // row i: warp, lanes over k < i
+  // Rows 1..j-1 of L from the earlier iterations.
+  for (int i = 1 + warp; i < j; i += static_cast<int>(blockDim.x >> 5))  // row i: warp, lanes over k < i
     for (int k = lane; k < i; k += 32) sL[i * (i - 1) / 2 + k] = __ldcg(S + static_cast<long long>(i) * lds + k);
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) cv[i] = __ldcg(dots + i);
   __syncthreads();
   // h = (I + L)^{-1} c, column-oriented on warp 0 (rows in registers; the
   // register count follows the restart length).
