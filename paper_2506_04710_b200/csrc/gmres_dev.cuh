@@ -97,9 +97,15 @@ __device__ __forceinline__ void blockPartial(double2 v, double2* scratch, double
 // Grid total of the partials, computed by each warp independently in a
 // fixed order (bitwise identical in every warp and CTA).
 __device__ __forceinline__ double2 warpTotal(const double2* part) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, G = static_cast<int>(gridDim.x);
   double2 s = make_double2(0.0, 0.0);
-  for (int k = lane; k < static_cast<int>(gridDim.x); k += 32) s = cadd(s, __ldcg(part + k));
+  for (int k0 = lane; k0 < G; k0 += 256) {  // up to 8 loads in flight per lane, summed in k order
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = k0 + 32 * q < G ? __ldcg(part + k0 + 32 * q) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = cadd(s, v[q]);
+  }
   return warpSum(s);
 }
 
