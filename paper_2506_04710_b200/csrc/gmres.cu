@@ -381,7 +381,13 @@ __global__ void colReduce(GmresArgs A, ColsLS L, int nslots) {
   const int lane = threadIdx.x & 31;
   const double2* p = L.part + (static_cast<long long>(col) * 2 * (A.restart + 1) + slot) * L.nblk;
   double2 t = make_double2(0.0, 0.0);
-  for (int b = lane; b < L.nblk; b += 32) t = cadd(t, p[b]);
+  for (int b0 = lane; b0 < L.nblk; b0 += 256) {  // 8 loads in flight per lane, summed in block order
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = b0 + 32 * q < L.nblk ? p[b0 + 32 * q] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t = cadd(t, v[q]);
+  }
   t = warpSum(t);
   if (lane == 0) L.tot[static_cast<long long>(slot) * A.ncols + col] = t;
 }

@@ -281,7 +281,13 @@ __global__ void cornerReduce(CornerArgs ca, const double2* __restrict__ part, do
   while (i >= ca.em[c]) i -= ca.em[c++];
   const double2* p = part + (static_cast<long long>(gRow) * K + rhs) * nblk;
   double2 acc = make_double2(0.0, 0.0);
-  for (int b = lane; b < nblk; b += 32) acc = cadd(acc, p[b]);
+  for (int b0 = lane; b0 < nblk; b0 += 256) {  // 8 loads in flight per lane, summed in block order
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = b0 + 32 * q < nblk ? p[b0 + 32 * q] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = cadd(acc, v[q]);
+  }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
