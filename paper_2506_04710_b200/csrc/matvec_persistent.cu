@@ -309,7 +309,14 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   const int auxId = blockIdx.x * kAux + (warp - kConsumers / 32 - 1);  // valid when aux
   double2* slab = fftb + ((producer || aux) ? 0 : warp) * C::SLAB;
   const int nwarps = gridDim.x * (kConsumers / 32);
-  const int gw = blockIdx.x * (kConsumers / 32) + warp;  // global consumer warp id
+  // Global consumer warp id of a transform phase's first item: warp-major
+  // (consecutive items on different SMs) when the phase has at most one item
+  // per warp, so a short phase spreads over every SM (C2); CTA-major (a
+  // CTA's warps on neighbouring lines) when warps loop over several items.
+  auto firstItem = [&](int items) {
+    return items <= nwarps ? warp * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x)
+                           : static_cast<int>(blockIdx.x) * (kConsumers / 32) + warp;
+  };
 
   if (a.skip && *reinterpret_cast<const volatile int*>(a.skip)) return;  // uniform: set before launch
   stamp(a, 0);
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     const int chunks0 = M / W0::WB;
     const int rowItems = a.ny * chunks0;
     const int items = rowItems;
-    for (int it = gw; it < items; it += nwarps) {
+    for (int it = firstItem(items); it < items; it += nwarps) {
       if (it < rowItems) {
         const int r = it / chunks0, b0 = (it % chunks0) * W0::WB;
         warpLineFft<N0, false>(
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     const int chunks1 = M / W1::WB;
     const int colItems = a.L0 * chunks1;
     const int items = colItems;
-    for (int it = gw; it < items; it += nwarps) {
+    for (int it = firstItem(items); it < items; it += nwarps) {
       const int s0 = it / chunks1, b0 = (it % chunks1) * W1::WB;
       warpLineFft<N1, false>(
           slab, a.tw1,
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   } else if (!producer) {
     const int chunks1 = M / W1::WB;
     const int items = a.L0 * chunks1;
-    for (int it = gw; it < items; it += nwarps) {
+    for (int it = firstItem(items); it < items; it += nwarps) {
       const int s0 = it / chunks1, b0 = (it % chunks1) * W1::WB;
       warpLineFft<N1, true>(
           slab, a.tw1, [&](int s1, int b) { return a.yhat[(static_cast<long long>(s1) * a.L0 + s0) * M + b0 + b]; },
@@ -517,7 +524,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     const int chunks0 = M / W0::WB;
     const int items = a.ny * chunks0;
     const int bl = (threadIdx.x & 31) % W0::WB;
-    for (int it = gw; it < items; it += nwarps) {
+    for (int it = firstItem(items); it < items; it += nwarps) {
       const int r = it / chunks0, b0 = (it % chunks0) * W0::WB;
       double2 pre[RO];
 #pragma unroll
