@@ -21,6 +21,7 @@
 // only), so the transform phases need no CTA-wide synchronisation.
 // Restates applyA + apply (proj/src/linsolve.cpp:260-290,373-388).
 #include <algorithm>
+#include <cstdlib>
 
 #include "fft_reg.cuh"
 #include "gmres_dev.cuh"
@@ -74,7 +75,8 @@ struct PArgs {
   double2* tvec;          // [nPairs][M] pair vectors
   double2* ycorr;
   int prefetchAt;               // phase at which the spectrum ring is primed (0 = kernel start)
-  long long l2Chunks;           // spectrum chunks per CTA bulk-prefetched into L2 at kernel start
+  long long l2Chunks;           // spectrum chunks per CTA bulk-prefetched into L2 (zero-copy x only)
+  int l2At;                     // ... at kernel start (0) or after grid barrier 0 (1)
   const int* skip;              // optional: the whole launch is a no-op when *skip != 0
   int pdl;                      // launched with programmatic stream serialization
   int ctaMajor;                 // CTA-major transform items in every phase (zero-copy launches)
@@ -293,16 +295,31 @@ struct PCfg {
   static constexpr int SLAB0 = WarpFft<N0>::SLAB, SLAB1 = WarpFft<N1>::SLAB;
   static constexpr int SLAB = (SLAB0 > SLAB1 ? SLAB0 : SLAB1) > 1 ? (SLAB0 > SLAB1 ? SLAB0 : SLAB1) : 1;
   static constexpr uint32_t FFTB = (kConsumers / 32) * SLAB * 16;
-  static constexpr uint32_t SMEM = STAGES * STAGE + RED + FFTB + 2 * STAGES * 8;
+  // The transpose-product reduction buffer (phase B only) aliases the FFT
+  // slabs (phases A / C only): a grid barrier separates every phase.
+  static constexpr uint32_t WORK = RED > FFTB ? RED : FFTB;
+  static constexpr uint32_t SMEM = STAGES * STAGE + WORK + 2 * STAGES * 8;
 };
+
+// L2 bulk prefetch of the spectrum chunks after the ring's first `pre`.
+template <int M, int RCH>
+__device__ __forceinline__ void prefetchL2(const PArgs& a, long long pre, long long total) {
+  constexpr int NCH = M / RCH;
+  const long long pfEnd = pre + a.l2Chunks < total ? pre + a.l2Chunks : total;
+  for (long long it = pre; it < pfEnd; ++it) {
+    const long long p = blockIdx.x + (it / NCH) * gridDim.x;
+    const int ch = static_cast<int>(it % NCH);
+    bulkPrefetchL2(a.S + p * M * M + static_cast<long long>(ch) * RCH * M, RCH * M * 16);
+  }
+}
 
 template <int M, int TC, int RCH, int STAGES, int N0, int N1>
 __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
   extern __shared__ __align__(128) unsigned char smem[];
   double2* red = reinterpret_cast<double2*>(smem + STAGES * C::STAGE);
-  double2* fftb = reinterpret_cast<double2*>(smem + STAGES * C::STAGE + C::RED);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + C::RED + C::FFTB);
+  double2* fftb = red;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + C::WORK);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsumers / 32;
@@ -352,12 +369,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     // Zero-copy applies read x from host memory over PCIe in phase A1 while
     // HBM idles: stream the chunks after the ring's into L2 meanwhile, so
     // phase B starts on L2 hits (l2Chunks is 0 for device-resident x).
-    const long long pfEnd = pre + a.l2Chunks < total ? pre + a.l2Chunks : total;
-    for (long long it = pre; it < pfEnd; ++it) {
-      const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
-      const int ch = static_cast<int>(it % C::NCH);
-      bulkPrefetchL2(a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK);
-    }
+    if (a.l2At == 0) prefetchL2<M, RCH>(a, pre, total);
   }
   // Programmatic dependent launch: the CTA started while the previous apply
   // was finishing (its set-up and the spectrum prime above touch nothing the
@@ -392,6 +404,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   gridSync(a.barFlags, a, 0);
   stamp(a, 1);
   if (producer && lane == 0 && a.prefetchAt == 1) prefetch();
+  if (producer && lane == 0 && a.l2At == 1) prefetchL2<M, RCH>(a, pre, total);
   // ---- phase A2: column FFTs (level 1) -> xhat
   if (!producer && !aux) {
     const int chunks1 = M / W1::WB;
@@ -612,6 +625,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
   a.prefetchAt = c.prefetchAt;
   a.l2Chunks = c.zeroCopyL2Bytes / (static_cast<long long>(smCount(c.device)) * C::CHUNK);
+  a.l2At = 0;
   a.skip = c.skipFlag;
   a.pdl = (c.usePdl && !gm && !c.skipFlag) ? 1 : 0;
   a.ctaMajor = a.xStage ? 1 : 0;  // zero-copy: CTA-major keeps a CTA's host reads together (e2e +2-3 %)
@@ -662,7 +676,20 @@ bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, 
   if (!persistentSupported(c) || c.dist) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
-    case 64064064: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64064064: {
+      // Ring shape (rows per stage, stages); TBT_P64 selects a variant for tuning.
+      static const int v = [] {
+        const char* e = getenv("TBT_P64");
+        return e ? atoi(e) : 0;
+      }();
+      // Measured (C2 back-to-back): half blocks x 4 stages 37.6 us, whole
+      // blocks x 2 38.2, half x 5 40.6, quarter x 8 41.0, quarter x 11 47.1 —
+      // more bytes in flight per SM than 128 KB only slows the stream.
+      switch (v) {
+        case 1: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+        default: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+      }
+    }
     case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
