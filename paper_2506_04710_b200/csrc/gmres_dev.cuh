@@ -300,9 +300,10 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   }
   __syncthreads();
   // Pass 1: warp w owns dots k = w, w + nw, ...; it takes them two at a
-  // time with 8 rows per lane per vector in flight (16 loads), c_k in slot
-  // k, S_jk in slot lds + k.
+  // time with 16 rows per lane per vector in flight (32 loads: one trip for
+  // row chunks up to 512, i.e. C2), c_k in slot k, S_jk in slot lds + k.
   {
+    constexpr int U1 = 16;
     const int nw = static_cast<int>(blockDim.x >> 5);
     for (int k0 = warp; k0 <= j; k0 += 2 * nw) {
       const int k1 = k0 + nw;
@@ -310,16 +311,16 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
       const double2* V0 = A.V + static_cast<long long>(k0) * n + r0;
       const double2* V1 = A.V + static_cast<long long>(two ? k1 : k0) * n + r0;
       double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
-      for (int r = lane; r < cnt; r += 256) {
-        double2 v0[8], v1[8];
+      for (int r = lane; r < cnt; r += 32 * U1) {
+        double2 v0[U1], v1[U1];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < U1; ++u) {
           const int rr = r + 32 * u;
           v0[u] = rr < cnt ? V0[rr] : make_double2(0.0, 0.0);
           v1[u] = rr < cnt && two ? V1[rr] : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < U1; ++u) {
           const int rr = r + 32 * u;
           if (rr < cnt) {
             const double2 wv = ws[rr], vv = vj[rr];
@@ -402,21 +403,42 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   __syncthreads();
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = cv[i];
-  // Pass 2: w' = w - V h and ||w'||^2.
+  // Pass 2: w' = w - V h and ||w'||^2. Two rows per thread at a time
+  // (16 loads in flight); per row the update order over k is unchanged.
   double2 acc = make_double2(0.0, 0.0);
-  for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-    double2 wv = ws[r];
+  const int bd = static_cast<int>(blockDim.x);
+  for (int ra = threadIdx.x; ra < cnt; ra += 2 * bd) {
+    const int rb = ra + bd;
+    const bool hb = rb < cnt;
+    const int rbs = hb ? rb : ra;
+    double2 wa = ws[ra], wb = ws[rbs];
+    const double2* Va = A.V + r0 + ra;
+    const double2* Vb = A.V + r0 + rbs;
     int k = 0;
     for (; k + 8 <= j + 1; k += 8) {
-      double2 v[8];
+      double2 va[8], vb[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = A.V[static_cast<long long>(k + u) * n + r0 + r];
+      for (int u = 0; u < 8; ++u) {
+        va[u] = Va[static_cast<long long>(k + u) * n];
+        vb[u] = Vb[static_cast<long long>(k + u) * n];
+      }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) wv = csub(wv, cmul(cv[k + u], v[u]));
+      for (int u = 0; u < 8; ++u) {
+        wa = csub(wa, cmul(cv[k + u], va[u]));
+        wb = csub(wb, cmul(cv[k + u], vb[u]));
+      }
     }
-    for (; k <= j; ++k) wv = csub(wv, cmul(cv[k], A.V[static_cast<long long>(k) * n + r0 + r]));
-    ws[r] = wv;
-    acc.x += wv.x * wv.x + wv.y * wv.y;
+    for (; k <= j; ++k) {
+      const double2 va = Va[static_cast<long long>(k) * n], vb = Vb[static_cast<long long>(k) * n];
+      wa = csub(wa, cmul(cv[k], va));
+      wb = csub(wb, cmul(cv[k], vb));
+    }
+    ws[ra] = wa;
+    acc.x += wa.x * wa.x + wa.y * wa.y;
+    if (hb) {
+      ws[rb] = wb;
+      acc.x += wb.x * wb.x + wb.y * wb.y;
+    }
   }
   blockPartial(acc, scratch, partSlot(A, 0, 0));
   if (blockIdx.x == 0) givensStage(A, 0, j, hcol, sh);  // made visible by the barrier
