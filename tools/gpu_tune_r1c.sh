@@ -1,9 +1,8 @@
-# Software-pipelined column-phase FFT items: parity + phase timing (C2, C4, C5).
+# Dynamically scheduled persistent DMMA GEMM: parity + C3 timing.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "config_apply or c4_sampled or c5_full or apply_matches or gmres_c2" 2>&1 | tail -2
-for c in C2 C4; do
-  echo "== $c"
-  timeout 300 python tools/prof_phases.py --config $c --n 30 2>&1 | tail -6
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_margin.py -m gpu -q -x -k "multi_rhs or c3 or smooth or many_columns or schur" 2>&1 | tail -2
+for i in 1 2; do
+timeout 300 python tools/prof_apply.py --config C3 --embed smooth 2>&1 | tail -1
+timeout 300 python tools/prof_apply.py --config C3 2>&1 | tail -1
 done
-echo "== C5"
-timeout 600 python tools/prof_phases.py --config C5 --n 10 2>&1 | tail -6
+timeout 300 python tools/bench_gmres.py C3 50 smooth 2>&1 | tail -2
