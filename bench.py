@@ -17,6 +17,11 @@ reference's parallelFor does (proj/src/linsolve.cpp:572).
 N > 1 (torchrun): every rank runs an independent replica of the workload
 (a frequency-sweep point per GPU), so scaling is "weak"; the timed region
 is bracketed by barriers and the max over ranks is reported.
+
+"sharded" (every N, --no-sharded skips it): C4 through the multi-GPU
+operator — bins split over the job's GPUs, NCCL all-to-all transposes — as
+device ms per matvec and exposed NCCL ms per matvec (max over ranks; at
+N = 1 a one-rank communicator, i.e. the sharded path's own overhead).
 """
 from __future__ import annotations
 
@@ -194,6 +199,61 @@ def run_reference(args):
     return 0
 
 
+SHARDED_TIMEOUT_S = 240
+
+
+def sharded_c4(world, rank, local, dist, steps=30, warmup=3):
+    """C4 through the multi-GPU operator (csrc/dist.cu): frequency bins split
+    by level-0 column groups, element-row slabs, NCCL all-to-all transposes
+    around the column transforms. Device time per matvec (CUDA events on the
+    context stream, max over ranks) and the exposed NCCL time per matvec
+    (events around each exchange, tbt_set_timing on a distributed context)."""
+    import torch
+
+    from paper_2506_04710_b200 import CONFIGS, ToeplitzMatvec, ToeplitzRep, dist_unique_id, init_from_torch
+    cfg = CONFIGS["C4"]
+    d = init_from_torch() if dist is not None else (1, 0, dist_unique_id())
+    op = ToeplitzMatvec(ToeplitzRep.synthetic(cfg), max_nrhs=1, device=local, dist=d)
+    try:
+        st = torch.cuda.Stream()
+        op.set_stream(st.cuda_stream)
+        r0, r1 = op.rows()
+        dev = f"cuda:{local}"
+        g = torch.Generator(device=dev).manual_seed(77 + rank)
+        x = torch.randn((r1 - r0) * cfg.nx * cfg.m, dtype=torch.complex128, device=dev, generator=g)
+        y = torch.empty_like(x)
+        for _ in range(warmup):
+            op.apply_device(x.data_ptr(), y.data_ptr())
+        st.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            op.apply_device(x.data_ptr(), y.data_ptr())
+        e1.record(st)
+        st.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        op.set_timing(True)
+        for _ in range(steps):
+            op.apply_device(x.data_ptr(), y.data_ptr())
+        comm_total, cnt = op.timing_read()
+        op.set_timing(False)
+        comm = comm_total / steps
+        if dist is not None:
+            t = torch.tensor([ms, comm], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, comm = (float(v) for v in t.tolist())
+        info = op.info()
+        return {"config": "C4: 64x64, m=128, 1 RHS, pow2 128x128 embedding, sharded over the job's GPUs",
+                "n_gpus": world, "ms_per_matvec": ms, "matvec_per_s": 1e3 / ms,
+                "exposed_nccl_ms_per_matvec": comm, "nccl_sections_per_matvec": cnt / steps,
+                "element_rows_this_rank": [r0, r1], "spectrum_pairs_this_rank": info.pairs,
+                "timing": "CUDA events on the context stream, max over ranks"}
+    finally:
+        op.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +263,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--gmres-iters", type=int, default=200)
+    ap.add_argument("--no-sharded", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -409,8 +470,29 @@ def main():
         "gpu_launches": K * info.kernels_per_apply,
         "clocks": clocks.summary(),
         "gmres": gm,
+        "sharded": None,
         "cpu_baseline": cpu,
     }
+    # ---- the bin-sharded operator on C4 across the job's
+    # GPUs (a one-rank NCCL communicator at N=1): per-matvec time and the
+    # exposed NCCL exchange time. A watchdog prints the line without it if a
+    # collective gets stuck, so it cannot cost the main measurement.
+    if not args.no_sharded:
+        done = threading.Event()
+
+        def watchdog():
+            if not done.wait(SHARDED_TIMEOUT_S):
+                if rank == 0:
+                    line["sharded"] = {"error": f"timed out after {SHARDED_TIMEOUT_S} s"}
+                    print(json.dumps(line), flush=True)
+                os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            line["sharded"] = sharded_c4(world, rank, local, dist)
+        except Exception as exc:  # reported, not fatal for the main line
+            line["sharded"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+        done.set()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

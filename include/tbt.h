@@ -241,7 +241,10 @@ tbt_status tbt_get_spectrum_bin(tbt_ctx* ctx, long long f, double* out);
 /* Per-launch timing of the bin-product kernel (K3). While enabled, every
  * apply records CUDA events around K3 on the context stream (and is not
  * replayed from a CUDA graph); tbt_timing_read synchronises and returns the
- * summed K3 milliseconds and the number of timed launches since enabling. */
+ * summed K3 milliseconds and the number of timed launches since enabling.
+ * On a distributed context (tbt_dist_init) the timed sections are instead
+ * the NCCL exchanges of every apply (forward all-to-all, all-to-all back,
+ * and the x slab all-gather of the edge/corner correction). */
 tbt_status tbt_set_timing(tbt_ctx* ctx, int on);
 tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
 

@@ -120,6 +120,30 @@ void distFree(Ctx& c) {
   c.comm = nullptr;
 }
 
+namespace {
+// With tbt_set_timing on, a distributed context times its NCCL exchanges
+// (events on the context stream around each group; nothing overlaps them,
+// so this is the exposed communication time) instead of the bin product.
+template <class F>
+void commSection(Ctx& c, F&& f) {
+  if (!c.timeBinprod) {
+    f();
+    return;
+  }
+  if (c.tCount == static_cast<int>(c.tEvA.size())) {
+    cudaEvent_t a, b;
+    TBT_CUDA_CHECK(cudaEventCreate(&a));
+    TBT_CUDA_CHECK(cudaEventCreate(&b));
+    c.tEvA.push_back(a);
+    c.tEvB.push_back(b);
+  }
+  TBT_CUDA_CHECK(cudaEventRecord(c.tEvA[c.tCount], c.stream));
+  f();
+  TBT_CUDA_CHECK(cudaEventRecord(c.tEvB[c.tCount], c.stream));
+  ++c.tCount;
+}
+}  // namespace
+
 void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   const int P = c.nranks, me = c.myRank;
   const int B = nrhs * c.m;
@@ -159,14 +183,16 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
     recvOff[q + 1] = recvOff[q] + static_cast<long long>(c.rowStart[q + 1] - c.rowStart[q]) * myCols * B;
   }
   TBT_CUDA_CHECK(cudaGetLastError());
-  TBT_NCCL_CHECK(nccl().groupStart());
-  for (int q = 0; q < P; ++q) {
-    const size_t sc = static_cast<size_t>(sendOff[q + 1] - sendOff[q]) * 2;
-    const size_t rc = static_cast<size_t>(recvOff[q + 1] - recvOff[q]) * 2;
-    if (sc) TBT_NCCL_CHECK(nccl().send(c.dSend + sendOff[q], sc, ncclDouble, q, c.comm, s));
-    if (rc) TBT_NCCL_CHECK(nccl().recv(c.dRecv + recvOff[q], rc, ncclDouble, q, c.comm, s));
-  }
-  TBT_NCCL_CHECK(nccl().groupEnd());
+  commSection(c, [&] {
+    TBT_NCCL_CHECK(nccl().groupStart());
+    for (int q = 0; q < P; ++q) {
+      const size_t sc = static_cast<size_t>(sendOff[q + 1] - sendOff[q]) * 2;
+      const size_t rc = static_cast<size_t>(recvOff[q + 1] - recvOff[q]) * 2;
+      if (sc) TBT_NCCL_CHECK(nccl().send(c.dSend + sendOff[q], sc, ncclDouble, q, c.comm, s));
+      if (rc) TBT_NCCL_CHECK(nccl().recv(c.dRecv + recvOff[q], rc, ncclDouble, q, c.comm, s));
+    }
+    TBT_NCCL_CHECK(nccl().groupEnd());
+  });
   // Received blocks are [rows of q][my columns][b] in row order: exactly
   // dTcol[r][j][b] for r = 0..ny-1 (rank slabs are contiguous and ordered).
   const double2* tcol = c.dRecv;
@@ -209,17 +235,19 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
 
   // 6. All-to-all back: rows of rank q x my columns -> q; from q: my rows x
   //    columns of q.
-  TBT_NCCL_CHECK(nccl().groupStart());
-  for (int q = 0; q < P; ++q) {
-    const long long rows = c.rowStart[q + 1] - c.rowStart[q];
-    const size_t sc = static_cast<size_t>(rows) * myCols * B * 2;
-    const size_t rc = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * B * 2;
-    if (sc)
-      TBT_NCCL_CHECK(nccl().send(c.dTcol + static_cast<long long>(c.rowStart[q]) * myCols * B, sc, ncclDouble, q,
-                              c.comm, s));
-    if (rc) TBT_NCCL_CHECK(nccl().recv(c.dSend + sendOff[q], rc, ncclDouble, q, c.comm, s));
-  }
-  TBT_NCCL_CHECK(nccl().groupEnd());
+  commSection(c, [&] {
+    TBT_NCCL_CHECK(nccl().groupStart());
+    for (int q = 0; q < P; ++q) {
+      const long long rows = c.rowStart[q + 1] - c.rowStart[q];
+      const size_t sc = static_cast<size_t>(rows) * myCols * B * 2;
+      const size_t rc = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * B * 2;
+      if (sc)
+        TBT_NCCL_CHECK(nccl().send(c.dTcol + static_cast<long long>(c.rowStart[q]) * myCols * B, sc, ncclDouble, q,
+                                c.comm, s));
+      if (rc) TBT_NCCL_CHECK(nccl().recv(c.dSend + sendOff[q], rc, ncclDouble, q, c.comm, s));
+    }
+    TBT_NCCL_CHECK(nccl().groupEnd());
+  });
   for (int q = 0; q < P; ++q) {
     const int nq = static_cast<int>(c.colsOfRank[q].size());
     const long long cnt = static_cast<long long>(c.myRows) * nq * B;
@@ -252,16 +280,18 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   //    neighbouring rows: all-gather the slabs, then add my rows).
   launchAntisym(c, x, y, nrhs, c.myRows * c.nx);
   if (withCorr && c.haveCorr && c.nTerms > 0) {
-    TBT_NCCL_CHECK(nccl().groupStart());
-    const size_t mine = static_cast<size_t>(c.myRows) * c.nx * B * 2;
-    for (int q = 0; q < P; ++q) {
-      const size_t rc = static_cast<size_t>(c.rowStart[q + 1] - c.rowStart[q]) * c.nx * B * 2;
-      if (mine) TBT_NCCL_CHECK(nccl().send(x, mine, ncclDouble, q, c.comm, s));
-      if (rc)
-        TBT_NCCL_CHECK(nccl().recv(c.dXfull + static_cast<long long>(c.rowStart[q]) * c.nx * B, rc, ncclDouble, q,
-                                c.comm, s));
-    }
-    TBT_NCCL_CHECK(nccl().groupEnd());
+    commSection(c, [&] {
+      TBT_NCCL_CHECK(nccl().groupStart());
+      const size_t mine = static_cast<size_t>(c.myRows) * c.nx * B * 2;
+      for (int q = 0; q < P; ++q) {
+        const size_t rc = static_cast<size_t>(c.rowStart[q + 1] - c.rowStart[q]) * c.nx * B * 2;
+        if (mine) TBT_NCCL_CHECK(nccl().send(x, mine, ncclDouble, q, c.comm, s));
+        if (rc)
+          TBT_NCCL_CHECK(nccl().recv(c.dXfull + static_cast<long long>(c.rowStart[q]) * c.nx * B, rc, ncclDouble, q,
+                                  c.comm, s));
+      }
+      TBT_NCCL_CHECK(nccl().groupEnd());
+    });
     launchCorrVector(c, c.dXfull, c.dYcorr, nrhs, s);
     const long long cnt = static_cast<long long>(c.myRows) * c.nx * B;
     addRows<<<gridFor(cnt, sms), 256, 0, s>>>(y, c.dYcorr + static_cast<long long>(c.myRow0) * c.nx * B, cnt);

@@ -1,8 +1,4 @@
-# Dynamically scheduled persistent DMMA GEMM: parity + C3 timing.
+# New GPU property tests, dist tests, and the bench line with the sharded C4 block.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_margin.py -m gpu -q -x -k "multi_rhs or c3 or smooth or many_columns or schur" 2>&1 | tail -2
-for i in 1 2; do
-timeout 300 python tools/prof_apply.py --config C3 --embed smooth 2>&1 | tail -1
-timeout 300 python tools/prof_apply.py --config C3 2>&1 | tail -1
-done
-timeout 300 python tools/bench_gmres.py C3 50 smooth 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_properties.py tests/test_dist.py -m gpu -q -x 2>&1 | tail -3
+timeout 600 python bench.py --steps 1000 --warmup 5 --no-cpu > gpurun_out/b_sharded.json 2> gpurun_out/b_sharded.err; python -c "import json; d=json.load(open('gpurun_out/b_sharded.json')); print(d['value'], d['sharded'])" || tail -5 gpurun_out/b_sharded.err
