@@ -34,6 +34,56 @@ __global__ void dmma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Larger FP64 MMA shapes (sm_90+): m16n8k4 / m16n8k8 / m16n8k16.
+template <int K>
+__global__ void dmma16(double* out, int iters) {
+  double acc[4][4];
+  double af[K / 2], bf[K / 4];
+#pragma unroll
+  for (int k = 0; k < K / 2; ++k) af[k] = 1.0 + threadIdx.x * 1e-6 + k;
+#pragma unroll
+  for (int k = 0; k < K / 4; ++k) bf[k] = 0.5 + k;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (K == 4)
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                     : "+d"(acc[k][0]), "+d"(acc[k][1]), "+d"(acc[k][2]), "+d"(acc[k][3])
+                     : "d"(af[0]), "d"(af[1]), "d"(bf[0]));
+      else if constexpr (K == 8)
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+d"(acc[k][0]), "+d"(acc[k][1]), "+d"(acc[k][2]), "+d"(acc[k][3])
+                     : "d"(af[0]), "d"(af[1]), "d"(af[2]), "d"(af[3]), "d"(bf[0]), "d"(bf[1]));
+      else
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                     "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                     : "+d"(acc[k][0]), "+d"(acc[k][1]), "+d"(acc[k][2]), "+d"(acc[k][3])
+                     : "d"(af[0]), "d"(af[1]), "d"(af[2]), "d"(af[3]), "d"(af[4]), "d"(af[5]), "d"(af[6]),
+                       "d"(af[7]), "d"(bf[0]), "d"(bf[1]), "d"(bf[2]), "d"(bf[3]));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += acc[k][0] + acc[k][1] + acc[k][2] + acc[k][3];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int K>
+void runDmma16(double* out, int sms, int bpsm, int iters, cudaEvent_t a, cudaEvent_t b) {
+  dim3 g(sms * bpsm), t(256);
+  dmma16<K><<<g, t>>>(out, 100);
+  cudaEventRecord(a);
+  dmma16<K><<<g, t>>>(out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double flops = 2.0 * 16 * 8 * K * 4 * iters * (double)g.x * (t.x / 32);
+  printf("DMMA m16n8k%-2d %d CTA/SM: %.1f TFLOP/s\n", K, bpsm, flops / (ms * 1e-3) / 1e12);
+}
+
 int main() {
   double* out;
   cudaMalloc(&out, 8);
@@ -62,6 +112,9 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     flops = 2.0 * 256 * 4 * iters * (double)g.x * (t.x / 32);
     printf("DMMA  %d CTA/SM: %.1f TFLOP/s\n", bpsm, flops / (ms * 1e-3) / 1e12);
+    runDmma16<4>(out, sms, bpsm, iters / 2, a, b);
+    runDmma16<8>(out, sms, bpsm, iters / 4, a, b);
+    runDmma16<16>(out, sms, bpsm, iters / 8, a, b);
   }
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }

@@ -1,4 +1,11 @@
-# New GPU property tests, dist tests, and the bench line with the sharded C4 block.
+# DMMA GEMM: padded transposed A chunk (TBT_GEMM_TPAD) A/B on C3, + parity.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_properties.py tests/test_dist.py -m gpu -q -x 2>&1 | tail -3
-timeout 600 python bench.py --steps 1000 --warmup 5 --no-cpu > gpurun_out/b_sharded.json 2> gpurun_out/b_sharded.err; python -c "import json; d=json.load(open('gpurun_out/b_sharded.json')); print(d['value'], d['sharded'])" || tail -5 gpurun_out/b_sharded.err
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_margin.py -m gpu -q -x -k "multi_rhs or c3 or many_columns or schur" 2>&1 | tail -2
+for i in 1 2; do
+for t in 0 1; do
+  echo "== TPAD=$t"
+  TBT_GEMM_TPAD=$t timeout 300 python tools/prof_apply.py --config C3 --embed smooth 2>&1 | tail -1
+  TBT_GEMM_TPAD=$t timeout 300 python tools/prof_apply.py --config C3 2>&1 | tail -1
+done
+done
+./tools/fp64test 2>&1 | tail -8
