@@ -1,11 +1,6 @@
-# DMMA GEMM: padded transposed A chunk (TBT_GEMM_TPAD) A/B on C3, + parity.
+# Default bench run (with the sharded C4 block incl. distributed GMRES).
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_margin.py -m gpu -q -x -k "multi_rhs or c3 or many_columns or schur" 2>&1 | tail -2
-for i in 1 2; do
-for t in 0 1; do
-  echo "== TPAD=$t"
-  TBT_GEMM_TPAD=$t timeout 300 python tools/prof_apply.py --config C3 --embed smooth 2>&1 | tail -1
-  TBT_GEMM_TPAD=$t timeout 300 python tools/prof_apply.py --config C3 2>&1 | tail -1
-done
-done
-./tools/fp64test 2>&1 | tail -8
+start=$(date +%s)
+timeout 900 python bench.py > gpurun_out/b_full.json 2> gpurun_out/b_full.err
+echo "bench wall s: $(( $(date +%s) - start ))"
+python -c "import json; d=json.loads(open('gpurun_out/b_full.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['gmres']['ms_per_iteration']); print(d['sharded'])" || tail -5 gpurun_out/b_full.err
