@@ -1,6 +1,12 @@
-# Default bench run (with the sharded C4 block incl. distributed GMRES).
+# Warp-synchronous line groups in the cluster 2-D transforms: parity with
+# small batch chunks forced, and C3 timing per (CL, BC).
 mkdir -p gpurun_out
-start=$(date +%s)
-timeout 900 python bench.py > gpurun_out/b_full.json 2> gpurun_out/b_full.err
-echo "bench wall s: $(( $(date +%s) - start ))"
-python -c "import json; d=json.loads(open('gpurun_out/b_full.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['gmres']['ms_per_iteration']); print(d['sharded'])" || tail -5 gpurun_out/b_full.err
+TBT_FFT2D=4,4 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "c3 or smooth or multi_rhs" 2>&1 | tail -2
+for f in "" "4,4" "4,2" "2,4" "1,4"; do
+  echo "== smooth fft2d=$f"
+  TBT_FFT2D=$f timeout 300 python tools/prof_apply.py --config C3 --embed smooth 2>&1 | tail -1
+done
+for f in "" "8,4" "4,4"; do
+  echo "== pow2 fft2d=$f"
+  TBT_FFT2D=$f timeout 300 python tools/prof_apply.py --config C3 2>&1 | tail -1
+done
