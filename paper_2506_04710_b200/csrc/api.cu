@@ -231,11 +231,14 @@ bool poisonBuffers() {
 }
 
 int smCount(int device) {
-  static int cached[64] = {0};
-  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  static std::atomic<int> cached[64] = {};
+  if (device >= 0 && device < 64) {
+    const int c = cached[device].load(std::memory_order_relaxed);
+    if (c) return c;
+  }
   int v = 0;
   TBT_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
-  if (device >= 0 && device < 64) cached[device] = v;
+  if (device >= 0 && device < 64) cached[device].store(v, std::memory_order_relaxed);
   return v;
 }
 

@@ -313,12 +313,11 @@ binprodRing(const double2* __restrict__ S, const int* __restrict__ pairF, const 
 template <int M, int TC, int RCH, int STAGES>
 void launchRing(Ctx& c) {
   using C = RingCfg<M, TC, RCH, STAGES>;
-  static bool attrSet = false;
-  if (!attrSet) {
+  static std::atomic<unsigned long long> attrSet{0};
+  oncePerDevice(attrSet, [] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodRing<M, TC, RCH, STAGES>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attrSet = true;
-  }
+  });
   const int sms = smCount(c.device);
   const int grid = static_cast<int>(std::min<long long>(c.npairs, sms));
   binprodRing<M, TC, RCH, STAGES><<<grid, C::NT + 32, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,
@@ -364,11 +363,10 @@ void launchBinProduct(Ctx& c, int nrhs) {
       if (c.m <= 64) {
         const int ld = c.m | 1;
         const size_t smem = (static_cast<size_t>(c.m) * ld + 2 * kMultiRc * c.m) * sizeof(double2);
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        oncePerDevice(attr, [] {
           TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodMulti, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-          attr = true;
-        }
+        });
         const long long items = c.npairs * ((nrhs + kMultiRc - 1) / kMultiRc);
         const long long grid = std::min<long long>(items, 16LL * sms);
         binprodMulti<<<static_cast<int>(grid), 256, smem, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,

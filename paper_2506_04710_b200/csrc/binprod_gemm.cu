@@ -169,12 +169,11 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
 template <int M>
 void launchGemm(Ctx& c, int nrhs) {
   using C = GemmCfg<M>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(C::SMEM)));
-    attr = true;
-  }
+  });
   const int nTiles = (nrhs + NTILE - 1) / NTILE;
   const long long items = c.npairs * 2 * nTiles;
   const int grid = static_cast<int>(std::min<long long>(items, 16LL * smCount(c.device)));

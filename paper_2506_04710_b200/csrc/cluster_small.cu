@@ -692,11 +692,10 @@ void launchClusterApply(Ctx& c, const double2* x, double2* y, bool withCorr) {
   size_t smem = 0;
   buildArgs(c, a, smem);
   a.binMap = cs.dBinMap;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(clusterApplyKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  });
   clusterApplyKernel<<<CL, CT, smem, c.stream>>>(a, x, y, withCorr ? 1 : 0);
   TBT_CUDA_CHECK(cudaGetLastError());
 }
@@ -715,11 +714,10 @@ void launchClusterGmres(Ctx& c, const GmresArgs& A, bool withCorr) {
   a.oH = a.oS + (R + 1) * (R + 1);
   smem += sizeof(double2) * (static_cast<size_t>(R + 1) * a.nloc + static_cast<size_t>(R + 1) * (R + 1) +
                              static_cast<size_t>(R + 1) * R);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(clusterGmresKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  });
   clusterGmresKernel<<<CL, CT, smem, c.stream>>>(a, A, withCorr ? 1 : 0);
   TBT_CUDA_CHECK(cudaGetLastError());
   if (prof) {

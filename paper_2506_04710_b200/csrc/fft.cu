@@ -87,13 +87,12 @@ void launchT(const FftPass& p, cudaStream_t s) {
   const size_t sm = (R2 > 1) ? sizeof(double2) * R1 * R2 * BC : 0;
   dim3 grid(p.lines, (p.batch + BC - 1) / BC);
   if (sm > 48 * 1024) {  // opt in above the default dynamic shared-memory limit
-    static bool done[2] = {false, false};
-    if (!done[p.inverse ? 1 : 0]) {
+    static std::atomic<unsigned long long> done[2] = {{0}, {0}};
+    oncePerDevice(done[p.inverse ? 1 : 0], [&] {
       const void* fn = p.inverse ? reinterpret_cast<const void*>(fftPassKernel<R1, R2, BC, true>)
                                  : reinterpret_cast<const void*>(fftPassKernel<R1, R2, BC, false>);
       TBT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      done[p.inverse ? 1 : 0] = true;
-    }
+    });
   }
   if (p.inverse)
     fftPassKernel<R1, R2, BC, true><<<grid, NT, sm, s>>>(p);

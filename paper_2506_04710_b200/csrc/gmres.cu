@@ -17,6 +17,7 @@
 // The Givens sweep and the back substitution run on staged shared-memory /
 // register copies of H, cs, sn, g (one memory round trip, not one per entry).
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 
 #include <cstdio>
@@ -915,11 +916,19 @@ __global__ void __launch_bounds__(kThreads) gmresUpdate(GmresArgs A) {
 void coopLaunch(const void* fn, int grid, size_t smem, GmresArgs& args, cudaStream_t s) {
   // Same (maximal) shared-memory carveout as the persistent apply kernel, so
   // alternating launches do not reconfigure L1/shared memory on every SM.
-  static std::vector<const void*> configured;
-  if (std::find(configured.begin(), configured.end(), fn) == configured.end()) {
-    TBT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        cudaSharedmemCarveoutMaxShared));
-    configured.push_back(fn);
+  // Per (kernel, device), under a lock: contexts on other threads / GPUs.
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> configured;
+  {
+    int dev = 0;
+    TBT_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(fn, dev);
+    if (std::find(configured.begin(), configured.end(), key) == configured.end()) {
+      TBT_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+      configured.push_back(key);
+    }
   }
   void* params[] = {&args};
   TBT_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), params, smem, s));

@@ -580,11 +580,10 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
   auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [&] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+  });
   PArgs a{};
   a.S = c.dSpectra;
   a.pairF = c.dPairF;

@@ -1,6 +1,8 @@
 // Internal declarations of the B200 block-Toeplitz library (libtbt.so).
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -310,5 +312,19 @@ bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, 
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);
+
+// Runs f (a cudaFuncSetAttribute call) once per device for the kernel that
+// owns `mask`: function attributes are per device, so a process driving
+// contexts on several GPUs must set them on each. The bit is published only
+// after f returned, so no caller launches before its attribute is set.
+template <class F>
+inline void oncePerDevice(std::atomic<unsigned long long>& mask, F&& f) {
+  int dev = 0;
+  TBT_CUDA_CHECK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  f();
+  mask.fetch_or(bit, std::memory_order_release);
+}
 
 }  // namespace tbt
