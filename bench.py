@@ -195,7 +195,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference C++ cannot be built here (Eigen3 absent, SURVEY.md 8(c)); oracle port timed instead",
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -274,7 +274,33 @@ def sharded_c4(world, rank, local, dist, steps=30, warmup=3, gmres_iters=20):
         op.close()
 
 
+_JSON_FD = None
+
+
+def _quiet_stdout():
+    """Points fd 1 at stderr for the rest of the run and keeps the real
+    stdout for the one JSON line: native libraries print to stdout (NCCL's
+    version banner on communicator init), which must not precede the line."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    """Writes the bench's single JSON line to the real stdout."""
+    sys.stdout.flush()
+    try:
+        import ctypes
+        ctypes.CDLL(None).fflush(None)  # C stdio buffers of native libraries
+    except OSError:
+        pass
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    _quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=4000)
@@ -504,7 +530,7 @@ def main():
             if not done.wait(SHARDED_TIMEOUT_S):
                 if rank == 0:
                     line["sharded"] = {"error": f"timed out after {SHARDED_TIMEOUT_S} s"}
-                    print(json.dumps(line), flush=True)
+                    emit(line)
                 os._exit(0)
 
         threading.Thread(target=watchdog, daemon=True).start()
@@ -514,7 +540,7 @@ def main():
             line["sharded"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
         done.set()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.destroy_process_group()
     return 0
