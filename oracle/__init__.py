@@ -77,6 +77,22 @@ def ref_lib() -> C.CDLL | None:
     return _ref
 
 
+def bind_inputs() -> None:
+    """Routes paper_2506_04710_b200.gen (the seeded inputs of tbt_gen.h) to
+    liboracle.so's copy of csrc/gen.cpp, so a CPU-only process (bench.py
+    --impl reference) never maps the product library."""
+    from paper_2506_04710_b200 import gen
+    gen.bind(lib())
+
+
+def product_mapped() -> bool:
+    """True when libtbt.so is mapped into this process."""
+    try:
+        return "libtbt.so" in open("/proc/self/maps").read()
+    except OSError:
+        return False
+
+
 def _p(a: np.ndarray):
     return a.ctypes.data_as(dp)
 
@@ -276,3 +292,160 @@ def array_farfield(nx, ny, e, tensors, dirs, dx, dy, k, eta, current, weights):
     lib().orc_array_farfield(nx, ny, e.ctypes.data_as(ip), pco, pcx, ndir, _p(d), dx, dy, k, eta, _p(cur),
                              cur.shape[1], _p(W), q, _p(co), _p(cx))
     return co, cx
+
+
+# ---------------------------------------------------------------------------
+# The reference itself: oracle/_ref/libref_linsolve.so, the reference's own
+# linsolve.cpp / toeplitz.cpp / fft.cpp (+ mesh, array_model, partition)
+# compiled unchanged against the functional Eigen-subset shim
+# (oracle/eigen_shim, oracle/ref_pin/ref_capi.cpp). Pins this oracle.
+
+REF_LINSOLVE_SO = HERE / "_ref" / "libref_linsolve.so"
+_refls = None
+
+
+def ref_linsolve() -> C.CDLL | None:
+    """The reference's operator / solver library, or None when not built."""
+    global _refls
+    if _refls is None and REF_LINSOLVE_SO.exists():
+        L = C.CDLL(str(REF_LINSOLVE_SO))
+        vp = C.c_void_p
+        llp = C.POINTER(C.c_longlong)
+        L.refp_last_error.restype = C.c_char_p
+        L.refp_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.refp_save.argtypes = [vp, C.c_char_p]
+        L.refp_destroy.restype = None
+        L.refp_destroy.argtypes = [vp]
+        L.refp_sizes.argtypes = [vp, llp, llp, ip]
+        L.refp_edge_start.argtypes = [vp, llp]
+        L.refp_apply.argtypes = [vp, C.c_int, dp, dp]
+        L.refp_apply_a_cols.argtypes = [vp, dp, dp, C.c_int, C.c_int]
+        L.refp_diagonal.argtypes = [vp, dp]
+        L.refp_gmres.argtypes = [vp, dp, dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, ip, dp, ip, llp]
+        L.refp_solve.argtypes = [vp, C.c_int, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, dp, ip,
+                                 dp]
+        L.refp_reconstruct_full.argtypes = [vp, dp]
+        L.refp_excitation.argtypes = [vp, C.c_int, ip, C.c_int, llp]
+        _refls = L
+    return _refls
+
+
+class RefError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status  # 1 UserError, 2 NumericError, 3 other
+
+
+class RefOperator:
+    """The reference's ToeplitzMatvec over a ZTOE1 block cache (loaded by its
+    own loadBlockCache, toeplitz.cpp:754-815), with its own solvers."""
+
+    APPLY, APPLY_A, APPLY_B, APPLY_BT, APPLY_C = range(5)
+
+    def __init__(self, path):
+        self._L = ref_linsolve()
+        if self._L is None:
+            raise ImportError(f"{REF_LINSOLVE_SO} missing: run `make -C oracle ref` where the reference is mounted")
+        h = C.c_void_p()
+        self._check(self._L.refp_load(str(path).encode(), C.byref(h)))
+        self._h = h
+        nA, nM, mode = C.c_longlong(), C.c_longlong(), C.c_int()
+        self._L.refp_sizes(self._h, C.byref(nA), C.byref(nM), C.byref(mode))
+        self.nA, self.nM, self.mode = nA.value, nM.value, mode.value
+        self.n = self.nA + self.nM
+
+    def _check(self, st):
+        if st:
+            raise RefError(st, self._L.refp_last_error().decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.refp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def save(self, path):
+        self._check(self._L.refp_save(self._h, str(path).encode()))
+
+    def edge_start(self):
+        out = np.zeros(4 * (self.n + 8) + 64, np.int64)
+        k = self._L.refp_edge_start(self._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
+        return out[:k].copy()
+
+    def _apply(self, which, x, n_out):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.empty(n_out, np.complex128)
+        self._check(self._L.refp_apply(self._h, which, _p(x), _p(y)))
+        return y
+
+    def apply(self, x):
+        return self._apply(self.APPLY, x, self.n)
+
+    def applyA(self, x):
+        return self._apply(self.APPLY_A, x, self.nA)
+
+    def applyB(self, xA):
+        return self._apply(self.APPLY_B, xA, self.nM)
+
+    def applyBT(self, xM):
+        return self._apply(self.APPLY_BT, xM, self.nA)
+
+    def applyC(self, xM):
+        return self._apply(self.APPLY_C, xM, self.nM)
+
+    def apply_a_cols(self, X, threads=1):
+        X = np.asfortranarray(X, dtype=np.complex128)
+        Y = np.empty_like(X, order="F")
+        self._check(self._L.refp_apply_a_cols(self._h, _p(X), _p(Y), X.shape[1], threads))
+        return Y
+
+    def diagonal(self):
+        d = np.empty(self.n, np.complex128)
+        self._check(self._L.refp_diagonal(self._h, _p(d)))
+        return d
+
+    def gmres(self, b, tol=1e-8, max_iter=2000, restart=60, precondition=True, use_a_only=False):
+        """The reference's own gmres() (linsolve.cpp:425-515) on one column:
+        dict(x, iterations, residual, converged, matvecs), partial results
+        kept when it does not converge."""
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        x = np.empty_like(b)
+        it, conv = C.c_int(), C.c_int()
+        res = C.c_double()
+        mv = C.c_longlong()
+        self._check(self._L.refp_gmres(self._h, _p(b), _p(x), 1 if use_a_only else 0, 1 if precondition else 0, tol,
+                                       max_iter, restart, C.byref(it), C.byref(res), C.byref(conv), C.byref(mv)))
+        return dict(x=x, iterations=it.value, residual=res.value, converged=bool(conv.value), matvecs=mv.value)
+
+    def solve(self, kind, V, tol=1e-8, max_iter=2000, restart=60, precondition=True, threads=1):
+        """kind: 'iterative' | 'schur' | 'dense' (linsolve.cpp:532-682).
+        Raises RefError(status 1/2) as the reference throws."""
+        V = np.asfortranarray(V, dtype=np.complex128)
+        vec = V.ndim == 1
+        if vec:
+            V = V[:, None]
+        p = V.shape[1]
+        X = np.empty_like(V, order="F")
+        its = np.zeros(p, np.int32)
+        res = np.zeros(p, np.float64)
+        k = {"iterative": 0, "schur": 1, "dense": 2}[kind]
+        self._check(self._L.refp_solve(self._h, k, _p(V), p, tol, max_iter, restart, 1 if precondition else 0,
+                                       threads, _p(X), its.ctypes.data_as(ip), _p(res)))
+        return dict(x=X[:, 0] if vec else X, iterations=its.tolist(), residual=res.tolist())
+
+    def dense(self):
+        z = np.empty((self.n, self.n), np.complex128, order="F")
+        self._check(self._L.refp_reconstruct_full(self._h, _p(z)))
+        return z
+
+    def excitation_rows(self, feed_local_edge, ports):
+        pa = np.ascontiguousarray(ports, dtype=np.int32)
+        rows = np.zeros(len(pa), np.int64)
+        self._check(self._L.refp_excitation(self._h, feed_local_edge, pa.ctypes.data_as(ip), len(pa),
+                                            rows.ctypes.data_as(C.POINTER(C.c_longlong))))
+        return rows

@@ -8,7 +8,29 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import dp, lib, llp
+from ._lib import SIGNATURES, dp, llp
+from ._lib import lib as _product_lib
+
+_source = None
+
+
+def bind(library) -> None:
+    """Draws every input from `library` instead of libtbt.so: any shared
+    object exporting the tbt_gen.h symbols (oracle/liboracle.so compiles the
+    same csrc/gen.cpp, so the values are identical). The reference arm of
+    bench.py uses it to keep libtbt.so out of its process."""
+    global _source
+    if library is not None:
+        for name, (res, args) in SIGNATURES.items():
+            if name.startswith("tbtgen_"):
+                fn = getattr(library, name)
+                fn.restype = res
+                fn.argtypes = args
+    _source = library
+
+
+def lib():
+    return _source if _source is not None else _product_lib()
 
 
 def _ptr(a: np.ndarray):

@@ -87,9 +87,11 @@ def assemble_c(nx, ny, e, recs):
     return C
 
 
-def write_ztoe1(path, nx, ny, e, gen_raw, margin, recs, mode=2):
+def write_ztoe1(path, nx, ny, e, gen_raw, margin=None, recs=None, mode=2):
     """gen_raw: (nb, m, m) column-major blocks (gen.blocks_raw order);
-    margin: a Margin (bside / brow / bcorner in tbt_gen.h layout)."""
+    margin: a Margin (bside / brow / bcorner in tbt_gen.h layout), or None
+    for an A-only cache (margin components empty: the loader zero-fills
+    records that are absent, toeplitz.cpp:766)."""
     m = e[4]
     with open(path, "wb") as f:
         f.write(b"ZTOE1")
@@ -104,6 +106,9 @@ def write_ztoe1(path, nx, ny, e, gen_raw, margin, recs, mode=2):
             for j in range(2 * nx - 1):
                 _rec(f, 1, i, j, 0, gen_raw[t].T)
                 t += 1
+        if margin is None:
+            f.write(struct.pack("<B", 255))
+            return
         off = 0
         for r in range(2):
             em = e[EDGE[r] - 1]
@@ -134,4 +139,25 @@ def write_ztoe1(path, nx, ny, e, gen_raw, margin, recs, mode=2):
             _rec(f, 7, g, 0, 0, recs["c5x"][g])
         for (a, b), mat in recs["c55"].items():
             _rec(f, 8, a, b, 0, mat)
+        f.write(struct.pack("<B", 255))
+
+
+def write_ztoe1_dense(path, nx, ny, e, mode, a_level1=None, b_full=None, c_full=None, z_full=None):
+    """SemiSparse (mode 1: ny first-level A blocks, each (nx*m)^2, plus dense
+    B and C) or Full (mode 0: the whole matrix) caches, tags 9-12
+    (toeplitz.cpp:730-745)."""
+    with open(path, "wb") as f:
+        f.write(b"ZTOE1")
+        f.write(struct.pack("<B", mode))
+        f.write(struct.pack("<ii", nx, ny))
+        f.write(struct.pack("<9i", *e))
+        if mode == 1:
+            for i, blk in enumerate(a_level1):
+                _rec(f, 9, i, 0, 0, blk)
+            if b_full is not None and b_full.size:
+                _rec(f, 10, 0, 0, 0, b_full)
+            if c_full is not None and c_full.size:
+                _rec(f, 11, 0, 0, 0, c_full)
+        elif mode == 0:
+            _rec(f, 12, 0, 0, 0, z_full)
         f.write(struct.pack("<B", 255))
