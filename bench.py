@@ -4,15 +4,21 @@ BASELINE.json's config 2 (32x32 array, m = 64, complex128, 1 RHS).
 
 One step = one application of the operator (K2 forward FFT passes -> K3
 bin-pair product -> K4 inverse passes -> edge/corner correction) to a
-device-resident vector. L2 is flushed between steps (untimed 256 MiB
-write), each step is bracketed by CUDA events on the launching stream.
+device-resident vector. The headline `value` times K back-to-back steps
+between two CUDA events on the launching stream: the dominant input, the
+134 MB half spectrum, is larger than the 126 MB L2, so every step reads it
+from HBM; `cold_l2_ms_per_step` repeats the step with an untimed 256 MiB L2
+flush before each one.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
---impl reference times the reference's CPU algorithm (the oracle
-restatement in oracle/, the reference itself cannot be built here: Eigen3
-is absent) with every host thread, one column per thread as the
-reference's parallelFor does (proj/src/linsolve.cpp:572).
+--impl reference times the reference ITSELF on the host CPU: its own
+applyA (proj/src/linsolve.cpp:260-290) compiled unchanged into
+oracle/_ref/libref_linsolve.so (oracle/Makefile, against a functional
+Eigen-subset shim), every host thread, one column per thread as the
+reference's parallelFor does (linsolve.cpp:572). That process never maps
+libtbt.so: its inputs come from oracle/liboracle.so's copy of the seeded
+generator (csrc/gen.cpp), and it checks /proc/self/maps before timing.
 
 N > 1 (torchrun): every rank runs an independent replica of the workload
 (a frequency-sweep point per GPU), so scaling is "weak"; the timed region
@@ -136,67 +142,206 @@ def host_cpu():
     return {"model": model, "nproc": os.cpu_count()}
 
 
-def cpu_sample(rep, cfg, seconds=12.0, threads=1):
-    """Oracle port timed on host cores: returns (matvec/s, count, elapsed)."""
+def reference_operator(cfg, tmpdir):
+    """The reference's own ToeplitzMatvec (oracle/_ref/libref_linsolve.so)
+    on cfg's generator blocks, read from a ZTOE1 cache by its own
+    loadBlockCache (untimed, one-time). None when the library is absent."""
+    import oracle
+    if oracle.ref_linsolve() is None:
+        return None
+    from paper_2506_04710_b200 import gen
+    path = os.path.join(tmpdir, f"{cfg.name}.ztoe1")
+    oracle.write_ztoe1_a(path, cfg.nx, cfg.ny, cfg.m, gen.blocks_raw(cfg.nx, cfg.ny, cfg.m, cfg.seed))
+    op = oracle.RefOperator(path)
+    os.unlink(path)
+    return op
+
+
+def cpu_sample(rep, cfg, seconds=12.0, threads=1, prefer_reference=True):
+    """The reference's applyA timed on host cores (kind "reference"), or the
+    oracle port (kind "port") when oracle/_ref is absent or not preferred
+    (C4: the reference builds its 4.3 GB of spectra on one thread, ~1 min):
+    returns (matvec/s, count, elapsed, precompute s, kind, what)."""
+    import tempfile
+
     import numpy as np
 
     import oracle
-    t0 = time.perf_counter()
-    o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)  # spectra: one-time, untimed
-    t_pre = time.perf_counter() - t0
     from paper_2506_04710_b200 import gen
     X = np.asfortranarray(gen.rhs_normal(cfg.n, threads, 77))
-    o.apply_cols(X, nthreads=threads)  # warm
+    t0 = time.perf_counter()
+    ref = None
+    if prefer_reference:
+        with tempfile.TemporaryDirectory() as td:
+            ref = reference_operator(cfg, td)
+    if ref is not None:
+        fn = lambda: ref.apply_a_cols(X, threads=threads)  # noqa: E731
+        kind, what = "reference", "the reference's own applyA (oracle/_ref/libref_linsolve.so, linsolve.cpp:260-290)"
+    else:
+        o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)
+        fn = lambda: o.apply_cols(X, nthreads=threads)  # noqa: E731
+        kind, what = "port", "oracle/oracle.cpp restatement of applyA + correction"
+    t_pre = time.perf_counter() - t0  # spectra precompute: one-time, untimed
+    fn()  # warm
     count, t0 = 0, time.perf_counter()
     while True:
-        o.apply_cols(X, nthreads=threads)
+        fn()
         count += threads
         el = time.perf_counter() - t0
         if el >= seconds and count >= 3:
             break
-    return count / el, count, el, t_pre
+    return count / el, count, el, t_pre, kind, what
 
 
-def run_reference(args):
-    """--impl reference: the reference algorithm on the host CPU."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    from paper_2506_04710_b200 import CONFIGS, ToeplitzRep
+def cpu_sample_c5(seconds_cap=60.0):
+    """C5 on the host CPU: the reference algorithm's applyA does not fit
+    host memory there (38.65 GB of spectra + 19.2 GB of generators), so the
+    oracle times a bounded sample (orc_sampled_apply): all 192 forward 2-D
+    FFTs of x plus the per-row work (products over every bin and source
+    function, inverse 2-D FFT, crop) of 4 of the 192 output rows, one
+    thread; the matvec time is t_fwd + 192/4 * t_rows."""
     import numpy as np
 
     import oracle
-    from paper_2506_04710_b200 import gen
+    from paper_2506_04710_b200 import CONFIGS, gen
+    cfg = CONFIGS["C5"]
+    rows = [3, 61, 130, 191]
+    x = gen.rhs_normal(cfg.n, 1, 77)[:, 0]
+    t0 = time.perf_counter()
+    _, tf, tr = oracle.sampled_apply(cfg.nx, cfg.ny, cfg.m, cfg.seed, rows, x)
+    est = tf + cfg.m / len(rows) * tr
+    return {"value": 1.0 / est, "unit": "matvec/s", "cores": 1, "kind": "port",
+            "sample": f"C5 applyA restated (oracle/oracle.cpp orc_sampled_apply, linsolve.cpp:260-290): all "
+                      f"{cfg.m} forward 2-D FFTs ({tf:.2f} s) + {len(rows)} of {cfg.m} output rows "
+                      f"({tr:.3f} s), one thread; matvec = t_fwd + {cfg.m}/{len(rows)} t_rows = {est:.2f} s; "
+                      f"the reference itself needs ~58 GB host RAM at C5",
+            "wall_s": time.perf_counter() - t0}
+
+
+def run_reference(args):
+    """--impl reference: the reference itself on the host CPU."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import tempfile
+
+    import numpy as np
+
+    import oracle
+    oracle.bind_inputs()  # inputs from liboracle's copy of csrc/gen.cpp
+    from paper_2506_04710_b200 import CONFIGS, gen
     cfg = CONFIGS[CONFIG]
     cores = os.cpu_count() or 1
-    rep = ToeplitzRep.synthetic(cfg)
-    o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)
+    with tempfile.TemporaryDirectory() as td:
+        ref = reference_operator(cfg, td)
+    if ref is not None:
+        fn = lambda X: ref.apply_a_cols(X, threads=cores)  # noqa: E731
+        kind = "reference"
+        what = "the reference's own applyA (oracle/_ref/libref_linsolve.so: proj/src/linsolve.cpp compiled unchanged)"
+    else:
+        from paper_2506_04710_b200 import ToeplitzRep
+        o = oracle.Oracle.from_rep(ToeplitzRep.synthetic(cfg), precompute=True, nthreads=0)
+        fn = lambda X: o.apply_cols(X, nthreads=cores)  # noqa: E731
+        kind, what = "port", "oracle/oracle.cpp restatement of applyA + correction"
+    assert not oracle.product_mapped(), "reference arm must not map libtbt.so"
     X = np.asfortranarray(gen.rhs_normal(cfg.n, cores, 5))
     for _ in range(max(1, min(args.warmup, 3))):
-        o.apply_cols(X, nthreads=cores)
+        fn(X)
     # Each step: one batch of `cores` independent matvecs (one column per thread);
     # steps are bounded so the whole run stays within a few minutes.
-    steps = max(1, min(args.steps, 40))
+    steps = max(1, min(args.steps, 20))
     t0 = time.perf_counter()
     for _ in range(steps):
-        o.apply_cols(X, nthreads=cores)
+        fn(X)
     el = time.perf_counter() - t0
     value = steps * cores / el
-    sample = (f"{steps} steps x {cores} concurrent {cfg.name} matvecs (oracle/oracle.cpp restatement of "
-              f"applyA + correction, one column per thread as parallelFor, linsolve.cpp:572)")
+    sample = f"{steps} steps x {cores} concurrent {cfg.name} matvecs ({what}), one column per thread as parallelFor"
     line = {
         "impl": "reference", "metric": f"block-Toeplitz matvecs/s ({cfg.name}, complex128)", "value": value,
         "unit": "matvec/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * el / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded generator, include/tbt_gen.h)",
         "config": {"workload": workload_desc(cfg), "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "port", "sample": sample,
+        "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": kind, "sample": sample,
                          "host": host_cpu()},
         "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference C++ cannot be built here (Eigen3 absent, SURVEY.md 8(c)); oracle port timed instead",
+        "product_library_mapped": oracle.product_mapped(),
+        "note": "the reference has no GPU path; the BASELINE edge/corner correction is not a reference feature "
+                "and is not in this arm (<0.5% of the CPU work)",
     }
     emit(line)
     return 0
+
+
+def large_configs(local, with_cpu):
+    """C4 (64x64, m=128) and C5 (128x128, m=192) on this GPU, as extra keys
+    of the bench line so the driver observes them: device-resident applies
+    (back-to-back, CUDA events on the context stream; both spectra exceed
+    L2 by 34x / 160x), the roofline on the same algorithmic bytes as the
+    headline, GMRES(50) time per inner iteration over a fixed budget
+    (second solve: workspace and graphs cached), and a bounded CPU sample."""
+    import numpy as np
+    import torch
+
+    from paper_2506_04710_b200 import CONFIGS, SolverOptions, ToeplitzMatvec, ToeplitzRep, gen, rhs_for
+    from paper_2506_04710_b200._lib import TBT_DEVICE
+    peak, _ = measured_hbm()
+    dev = f"cuda:{local}"
+    out = {}
+    for name, n_apply, budget in (("C4", 200, 40), ("C5", 30, 8)):
+        cfg = CONFIGS[name]
+        t0 = time.perf_counter()
+        rep = ToeplitzRep.synthetic(cfg)
+        op = ToeplitzMatvec(rep, max_nrhs=1, device=local)
+        setup_s = time.perf_counter() - t0
+        try:
+            st = torch.cuda.Stream(device=dev)
+            op.set_stream(st.cuda_stream)
+            info = op.info()
+            x = torch.from_numpy(np.ascontiguousarray(gen.rhs_normal(cfg.n, 1, 3)[:, 0])).to(dev)
+            y = torch.empty_like(x)
+            for _ in range(3):
+                op.apply_device(x.data_ptr(), y.data_ptr())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(n_apply):
+                op.apply_device(x.data_ptr(), y.data_ptr())
+            e1.record(st)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / n_apply
+            kbytes = 16 * (info.pairs * cfg.m * cfg.m + 2 * info.bins * cfg.m + 2 * cfg.n)
+            b = torch.from_numpy(np.ascontiguousarray(np.asarray(rhs_for(cfg)).reshape(cfg.n))).to(dev)
+            xd = torch.empty_like(b)
+            opt = SolverOptions(tol=cfg.tol, maxIter=budget, restart=cfg.restart)
+            for _ in range(2):
+                e0.record(st)
+                g = op.gmres(None, opt, raise_on_fail=False, where=TBT_DEVICE, b_ptr=b.data_ptr(),
+                             x_ptr=xd.data_ptr(), nrhs=1, hist_cap=4 * budget + 8)
+                e1.record(st)
+                e1.synchronize()
+            gms = e0.elapsed_time(e1)
+            out[name] = {
+                "workload": workload_desc(cfg), "ms_per_apply": ms, "matvec_per_s": 1e3 / ms, "applies_timed": n_apply,
+                "roofline": {"bound": "hbm", "bytes_per_launch": kbytes, "achieved": kbytes / (ms * 1e-3) / 1e9,
+                             "peak": peak, "unit": "GB/s", "frac": kbytes / (ms * 1e-3) / 1e9 / peak},
+                "kernels_per_apply": info.kernels_per_apply, "apply_path": info.apply_path,
+                "gmres": {"restart": cfg.restart, "iteration_budget": budget, "iterations": g.iterations[0],
+                          "matvecs": g.matvecs, "ms_total": gms, "ms_per_iteration": gms / max(g.iterations[0], 1),
+                          "final_true_residual": g.residual[0]},
+                "setup_s": setup_s}
+        finally:
+            op.close()
+            del rep
+            torch.cuda.empty_cache()
+        if with_cpu and name == "C4":
+            v, cnt, el, t_pre, kind, what = cpu_sample(ToeplitzRep.synthetic(cfg), cfg, seconds=8.0, threads=1,
+                                                       prefer_reference=False)
+            out[name]["cpu_baseline"] = {"value": v, "unit": "matvec/s", "cores": 1, "kind": kind,
+                                         "sample": f"{cnt} single-thread matvecs in {el:.1f} s ({what}); spectra "
+                                                   f"precompute {t_pre:.1f} s excluded"}
+        if with_cpu and name == "C5":
+            out[name]["cpu_baseline"] = cpu_sample_c5()
+    return out
 
 
 SHARDED_TIMEOUT_S = 240
@@ -310,6 +455,7 @@ def main():
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--gmres-iters", type=int, default=200)
     ap.add_argument("--no-sharded", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the C4 / C5 extra keys")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -467,16 +613,17 @@ def main():
     spectrum = info.pairs * mm                       # half spectrum, read once
     vec_k3 = 2 * info.bins * cfg.m * c16             # xhat read + yhat write by the bin products
     step_mean = total_ms / K
+    # Algorithmic bytes per launch (with the half spectrum this
+    # design stores): the stored spectrum read once, xhat read + yhat written
+    # by the bin products, x read + y written once. Transform intermediates
+    # (the row-transformed grid T, xhat written by the forward pass, yhat read
+    # by the inverse) live in L2 and are NOT counted; ncu's DRAM bytes per
+    # launch are reported beside as `traffic`.
+    kbytes = spectrum + vec_k3 + 2 * cfg.n * c16
     if info.apply_path == 2:
-        tbuf = cfg.ny * info.L0 * cfg.m * c16
-        # x read, T write+read, xhat write (+ read in K3), yhat (write in K3) + read,
-        # T write+read, y write
-        fft_bytes = cfg.n * c16 + 2 * tbuf + info.bins * cfg.m * c16 + info.bins * cfg.m * c16 + 2 * tbuf + cfg.n * c16
-        kbytes = spectrum + vec_k3 + fft_bytes
         kms = step_mean
         kname = "matvec_persistent (K2+K3+K4 phases in one cooperative kernel, 1 launch per step)"
     else:
-        kbytes = spectrum + vec_k3
         kms = k3_ms
         kname = "binprod (K3, bin-pair product)"
     achieved = kbytes / (kms * 1e-3) / 1e9
@@ -484,19 +631,21 @@ def main():
     traffic = ncu_traffic(f"{cfg.name}_matvec_persistent") if info.apply_path == 2 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
-            "kernel": kname, "bytes_per_launch": kbytes, "ms_per_launch": kms,
-            "peak_source": peak_src}
+            "kernel": kname, "bytes_per_launch": kbytes,
+            "bytes_definition": "half spectrum (npairs*m^2*16) + xhat/yhat (2*L*m*16) + x/y (2*n*16)",
+            "ms_per_launch": kms, "peak_source": peak_src}
     if phase_us is not None:
         roof["phase_us"] = dict(zip(["rows+corr", "cols", "binprod", "inv_cols", "inv_rows"], phase_us))
-        roof["binprod_phase_gbs"] = (spectrum + vec_k3) / (phase_us[2] * 1e-6) / 1e9 if phase_us[2] > 0 else None
+        if phase_us[2] > 0:
+            roof["binprod_phase_gbs"] = (spectrum + vec_k3) / (phase_us[2] * 1e-6) / 1e9
+            roof["k3_phase_frac"] = roof["binprod_phase_gbs"] / peak
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cnt, el, t_pre = cpu_sample(rep, cfg, seconds=12.0, threads=1)
-        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port", "host": host_cpu(),
-               "sample": f"{cnt} single-thread {cfg.name} matvecs in {el:.1f} s (oracle/oracle.cpp, reference "
-                         f"flags -O3; applyA is serial in the reference, linsolve.cpp:260-290); one-time spectra "
-                         f"precompute {t_pre:.2f} s excluded"}
+        v, cnt, el, t_pre, kind, what = cpu_sample(rep, cfg, seconds=12.0, threads=1)
+        cpu = {"value": v, "unit": "matvec/s", "cores": 1, "kind": kind, "host": host_cpu(),
+               "sample": f"{cnt} single-thread {cfg.name} matvecs in {el:.1f} s ({what}; -O3, applyA is serial in "
+                         f"the reference); one-time spectra precompute {t_pre:.2f} s excluded"}
 
     line = {
         "metric": f"block-Toeplitz matvecs/s ({cfg.name}, complex128)",
@@ -518,7 +667,13 @@ def main():
         "gmres": gm,
         "sharded": None,
         "cpu_baseline": cpu,
+        "large_configs": None,
     }
+    if not args.no_large and world == 1:
+        try:
+            line["large_configs"] = large_configs(local, rank == 0 and not args.no_cpu)
+        except Exception as exc:  # reported, not fatal for the main line
+            line["large_configs"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
     # ---- the bin-sharded operator on C4 across the job's
     # GPUs (a one-rank NCCL communicator at N=1): per-matvec time and the
     # exposed NCCL exchange time. A watchdog prints the line without it if a

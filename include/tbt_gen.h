@@ -43,6 +43,13 @@ int tbtgen_block_shift(int nx, int ny, long long t, int* i, int* j);
 int tbtgen_blocks(int nx, int ny, int m, uint64_t seed, double* out,
                   int nthreads);
 
+/* Row a and column a of every canonical block (t-major, m entries each):
+ * rows[t*m + b] = Z_t(a, b), cols[t*m + b] = Z_t(b, a), the same values as
+ * tbtgen_blocks without materialising the blocks (the C5 CPU sample needs a
+ * few output rows of the 19 GB generator set). Returns 0 on success. */
+int tbtgen_block_lines(int nx, int ny, int m, uint64_t seed, int a, double* rows, double* cols,
+                       int nthreads);
+
 /* Nine-component edge/corner perturbations. For component c in
  * {1,2,3,4,6,7,8,9} (reference numbering, proj/include/arraymom/
  * array_model.hpp:26-29) and relation rel in {0 self, 1 +x, 2 -x, 3 +y, 4 -y}

@@ -57,6 +57,8 @@ def lib() -> C.CDLL:
         L.orc_apply_cols.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_int, C.c_int]
         L.orc_apply_rows.argtypes = [C.c_void_p, dp, C.POINTER(C.c_longlong), C.c_longlong, dp]
         L.orc_dense.argtypes = [C.c_void_p, dp]
+        L.orc_sampled_apply.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(dp), C.POINTER(dp), dp, dp, dp,
+                                        dp, C.c_int]
         L.orc_diagonal.argtypes = [C.c_void_p, dp]
         L.orc_gmres.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.c_int, ip, dp, ip, dp, C.c_int, ip]
@@ -252,6 +254,24 @@ class Oracle:
                     converged=conv.tolist(), history=hists)
 
 
+def sampled_apply(nx, ny, m, seed, rows, x, nthreads=0):
+    """Bounded sample of the reference's applyA (orc_sampled_apply): output
+    rows `rows` (basis indices) of every element, plus the timed forward
+    section and the timed per-row section (single thread). Needs only
+    row / column `a` of each canonical block (gen.block_lines), so it runs at
+    C5 where the spectra (38.65 GB) do not fit host memory."""
+    from paper_2506_04710_b200 import gen
+    lines = [gen.block_lines(nx, ny, m, seed, int(a), nthreads) for a in rows]
+    pr = (dp * len(rows))(*[_p(r) for r, _ in lines])
+    pc = (dp * len(rows))(*[_p(c) for _, c in lines])
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    y = np.empty((len(rows), nx * ny), np.complex128)
+    tf, tr = C.c_double(), C.c_double()
+    if lib().orc_sampled_apply(nx, ny, m, len(rows), pr, pc, _p(x), _p(y), C.byref(tf), C.byref(tr), nthreads):
+        raise ValueError("orc_sampled_apply failed")
+    return y, tf.value, tr.value
+
+
 def port_network(current, feed_rows, edge_len, z0):
     """portNetwork restated (postproc.cpp:186-230): dict(y, z, s)."""
     cur = np.asfortranarray(current, dtype=np.complex128)
@@ -328,6 +348,26 @@ def ref_linsolve() -> C.CDLL | None:
         L.refp_excitation.argtypes = [vp, C.c_int, ip, C.c_int, llp]
         _refls = L
     return _refls
+
+
+def write_ztoe1_a(path, nx, ny, m, gen_raw):
+    """A-only ZTOE1 block cache (saveBlockCache's format, toeplitz.cpp:
+    701-752: "ZTOE1", u8 mode 2 = Sparse, i32 nx, ny, e[9], AGen records
+    {u8 1, i32 i, j, 0, i64 rows, cols, column-major complex128}, u8 255)
+    from gen.blocks_raw-ordered blocks, for RefOperator."""
+    import struct
+    e = [0] * 9
+    e[4] = m
+    g = np.ascontiguousarray(gen_raw, dtype=np.complex128)
+    with open(path, "wb") as f:
+        f.write(b"ZTOE1" + struct.pack("<Bii9i", 2, nx, ny, *e))
+        t = 0
+        for i in range(ny):
+            for j in range(nx if i == 0 else 2 * nx - 1):
+                f.write(struct.pack("<Biiiqq", 1, i, j, 0, m, m))
+                f.write(g[t].tobytes())  # raw [t][b][a]: already column-major
+                t += 1
+        f.write(struct.pack("<B", 255))
 
 
 class RefError(RuntimeError):

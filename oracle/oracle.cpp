@@ -9,6 +9,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -1078,5 +1079,90 @@ extern "C" int orc_array_farfield(int nx, int ny, const int* e, const double* co
       CX[i + static_cast<long>(j) * ndir] = front * fcx;
     }
   }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Bounded CPU sample of applyA (linsolve.cpp:260-290) at sizes whose spectra
+// do not fit host memory (C5: 38.65 GB): the whole forward half (e5 padded
+// 2-D FFTs of x, :264-274) and, for `nrows` output rows m, the reference's
+// per-row work (accumulate sum_n ahat_{m,n} * xhat_n over all bins, inverse
+// 2-D FFT, crop and scale, :276-288). The spectra of those rows are built
+// first (untimed) from row m / column m of every canonical block
+// (tbtgen_block_lines), so aEntry's mirrored half (:219) is available.
+// Returns the two timed sections in seconds; y[r * ne + e] is the r-th
+// sampled output row (the row whose lines were passed) of element e, comparable with a full apply at those rows.
+extern "C" int orc_sampled_apply(int nx, int ny, int m, int nrows, const double* const* row_lines,
+                                 const double* const* col_lines, const double* xd, double* yd, double* t_fwd,
+                                 double* t_rows, int nthreads) {
+  if (nx < 1 || ny < 1 || m < 1 || nrows < 1) return 1;
+  const long L1 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * ny - 1)));
+  const long L0 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * nx - 1)));
+  const long L = L1 * L0;
+  const long ne = static_cast<long>(nx) * ny;
+  auto blockIndex = [&](int i, int j) -> long {
+    if (i == 0) return j;
+    return nx + static_cast<long>(i - 1) * (2 * nx - 1) + (j - (1 - nx));
+  };
+  auto fft2 = [&](cplx* g, bool inverse, cvec& col) {
+    for (long r = 0; r < L1; ++r) radix2(g + r * L0, static_cast<size_t>(L0), inverse);
+    for (long c = 0; c < L0; ++c) {
+      for (long r = 0; r < L1; ++r) col[r] = g[r * L0 + c];
+      radix2(col.data(), static_cast<size_t>(L1), inverse);
+      for (long r = 0; r < L1; ++r) g[r * L0 + c] = col[r];
+    }
+  };
+  // Spectra of the sampled rows: ahat[(r * m + n) * L + f].
+  std::vector<cplx> ahat(static_cast<size_t>(nrows) * m * L);
+  forkJoin(static_cast<long>(nrows) * m, nthreads, [&](long lo, long hi) {
+    cvec grid(static_cast<size_t>(L)), col(static_cast<size_t>(L1));
+    for (long rn = lo; rn < hi; ++rn) {
+      const int r = static_cast<int>(rn / m), n = static_cast<int>(rn % m);
+      const cplx* rl = reinterpret_cast<const cplx*>(row_lines[r]);
+      const cplx* cl = reinterpret_cast<const cplx*>(col_lines[r]);
+      std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+      for (int i = 1 - ny; i <= ny - 1; ++i)
+        for (int j = 1 - nx; j <= nx - 1; ++j) {
+          const long s1 = i >= 0 ? i : L1 + i;
+          const long s0 = j >= 0 ? j : L0 + j;
+          // aEntry(i, j, row, n) = Z_t(row, n); the mirrored half is
+          // aEntry(-i, -j, n, row) = Z_t'(n, row) = column `row` of t'.
+          const bool mirrored = i < 0 || (i == 0 && j < 0);
+          grid[s1 * L0 + s0] = mirrored ? cl[blockIndex(-i, -j) * m + n] : rl[blockIndex(i, j) * m + n];
+        }
+      fft2(grid.data(), false, col);
+      std::copy(grid.begin(), grid.end(), ahat.begin() + rn * L);
+    }
+  });
+  const cplx* x = reinterpret_cast<const cplx*>(xd);
+  cplx* y = reinterpret_cast<cplx*>(yd);
+  using clk = std::chrono::steady_clock;
+  // Timed, single thread, as the reference's applyA: the forward half.
+  auto t0 = clk::now();
+  cvec xhat(static_cast<size_t>(m) * L), grid(static_cast<size_t>(L)), col(static_cast<size_t>(L1));
+  for (int n = 0; n < m; ++n) {
+    std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+    for (int r = 0; r < ny; ++r)
+      for (int c = 0; c < nx; ++c) grid[static_cast<long>(r) * L0 + c] = x[(static_cast<long>(r) * nx + c) * m + n];
+    fft2(grid.data(), false, col);
+    std::copy(grid.begin(), grid.end(), xhat.begin() + static_cast<long>(n) * L);
+  }
+  auto t1 = clk::now();
+  const double scale = 1.0 / static_cast<double>(L);
+  for (int r = 0; r < nrows; ++r) {
+    std::fill(grid.begin(), grid.end(), cplx{0.0, 0.0});
+    for (int n = 0; n < m; ++n) {
+      const cplx* g = ahat.data() + (static_cast<size_t>(r) * m + n) * L;
+      const cplx* xr = xhat.data() + static_cast<size_t>(n) * L;
+      for (long f = 0; f < L; ++f) grid[f] += g[f] * xr[f];
+    }
+    fft2(grid.data(), true, col);
+    for (int rr = 0; rr < ny; ++rr)
+      for (int c = 0; c < nx; ++c)
+        y[r * ne + static_cast<long>(rr) * nx + c] = grid[static_cast<long>(rr) * L0 + c] * scale;
+  }
+  auto t2 = clk::now();
+  *t_fwd = std::chrono::duration<double>(t1 - t0).count();
+  *t_rows = std::chrono::duration<double>(t2 - t1).count();
   return 0;
 }

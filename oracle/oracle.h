@@ -71,6 +71,13 @@ int orc_apply_cols(const orc_op* op, const double* x, double* y, int ncols,
 int orc_apply_rows(const orc_op* op, const double* x, const long long* elems,
                    long long count, double* y);
 /* Dense Z (N x N column-major); only for small N. */
+/* Bounded CPU sample of applyA at sizes whose spectra do not fit host memory:
+ * the forward transforms of x and the per-row work of nrows output rows whose
+ * block row / column lines (tbtgen_block_lines) are given; timed sections in
+ * seconds (single thread), y[r * nx*ny + e]. */
+int orc_sampled_apply(int nx, int ny, int m, int nrows, const double* const* row_lines,
+                      const double* const* col_lines, const double* x, double* y, double* t_fwd, double* t_rows,
+                      int nthreads);
 int orc_dense(const orc_op* op, double* z);
 /* Diagonal of the operator (ToeplitzMatvec::diagonal, linsolve.cpp:390-408,
  * plus the correction's diagonal). */

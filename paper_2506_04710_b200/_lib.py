@@ -85,6 +85,7 @@ SIGNATURES = {
     "tbtgen_num_blocks": (C.c_longlong, [C.c_int, C.c_int]),
     "tbtgen_block_shift": (C.c_int, [C.c_int, C.c_int, C.c_longlong, ip, ip]),
     "tbtgen_blocks": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, dp, C.c_int]),
+    "tbtgen_block_lines": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, dp, dp, C.c_int]),
     "tbtgen_correction": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_double, dp, dp, dp]),
     "tbtgen_rhs_normal": (C.c_int, [C.c_longlong, C.c_int, C.c_uint64, dp]),
     "tbtgen_rhs_delta_steered": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]),

@@ -92,43 +92,64 @@ int tbtgen_block_shift(int nx, int ny, long long t, int* i, int* j) {
   return 0;
 }
 
+// Entry (a, b) of canonical block t (shift i, j): the definition in tbt_gen.h.
+static inline void blockEntry(int i, int j, int m, uint64_t key, int a, int b, double* re, double* im) {
+  const double R = std::sqrt(static_cast<double>(i) * i + static_cast<double>(j) * j);
+  const double amp = 1.0 / (1.0 + R);
+  const double wr = std::cos(M_PI * R) * amp;
+  const double wi = -std::sin(M_PI * R) * amp;
+  const double inv = 1.0 / std::sqrt(static_cast<double>(m));
+  const bool self = (i == 0 && j == 0);
+  // Column-major draw counter; the self block reuses the upper triangle's
+  // draw for (a, b) and (b, a).
+  long long k = static_cast<long long>(b) * m + a;
+  if (self && a > b) k = static_cast<long long>(a) * m + b;
+  double u, v;
+  normalPair(key, static_cast<uint64_t>(k), &u, &v);
+  u *= inv;
+  v *= inv;
+  *re = wr * u - wi * v;
+  *im = wr * v + wi * u;
+  if (self && a == b) {
+    *re += 2.0;
+    *im += 2.0;
+  }
+}
+
 int tbtgen_blocks(int nx, int ny, int m, uint64_t seed, double* out,
                   int nthreads) {
   if (nx < 1 || ny < 1 || m < 1 || out == nullptr) return 1;
   const long long nb = tbtgen_num_blocks(nx, ny);
   const long long bsz = static_cast<long long>(m) * m;
-  const double inv = 1.0 / std::sqrt(static_cast<double>(m));
   parallelRange(nb, nthreads, [&](long long lo, long long hi) {
     for (long long t = lo; t < hi; ++t) {
       int i = 0, j = 0;
       tbtgen_block_shift(nx, ny, t, &i, &j);
-      const double R = std::sqrt(static_cast<double>(i) * i +
-                                 static_cast<double>(j) * j);
-      const double amp = 1.0 / (1.0 + R);
-      const double wr = std::cos(M_PI * R) * amp;
-      const double wi = -std::sin(M_PI * R) * amp;
       const uint64_t key = streamKey(seed, kStreamBlock + static_cast<uint64_t>(t));
       double* blk = out + 2 * t * bsz;
-      const bool self = (i == 0 && j == 0);
       for (int b = 0; b < m; ++b)
         for (int a = 0; a < m; ++a) {
-          // Column-major draw counter; the self block reuses the upper
-          // triangle's draw for (a, b) and (b, a).
-          long long k = static_cast<long long>(b) * m + a;
-          if (self && a > b) k = static_cast<long long>(a) * m + b;
-          double u, v;
-          normalPair(key, static_cast<uint64_t>(k), &u, &v);
-          u *= inv;
-          v *= inv;
-          double re = wr * u - wi * v;
-          double im = wr * v + wi * u;
-          if (self && a == b) {
-            re += 2.0;
-            im += 2.0;
-          }
-          blk[2 * (static_cast<long long>(b) * m + a)] = re;
-          blk[2 * (static_cast<long long>(b) * m + a) + 1] = im;
+          const long long o = 2 * (static_cast<long long>(b) * m + a);
+          blockEntry(i, j, m, key, a, b, blk + o, blk + o + 1);
         }
+    }
+  });
+  return 0;
+}
+
+int tbtgen_block_lines(int nx, int ny, int m, uint64_t seed, int a, double* rows, double* cols, int nthreads) {
+  if (nx < 1 || ny < 1 || m < 1 || a < 0 || a >= m || rows == nullptr || cols == nullptr) return 1;
+  const long long nb = tbtgen_num_blocks(nx, ny);
+  parallelRange(nb, nthreads, [&](long long lo, long long hi) {
+    for (long long t = lo; t < hi; ++t) {
+      int i = 0, j = 0;
+      tbtgen_block_shift(nx, ny, t, &i, &j);
+      const uint64_t key = streamKey(seed, kStreamBlock + static_cast<uint64_t>(t));
+      for (int b = 0; b < m; ++b) {
+        const long long o = 2 * (t * m + b);
+        blockEntry(i, j, m, key, a, b, rows + o, rows + o + 1);
+        blockEntry(i, j, m, key, b, a, cols + o, cols + o + 1);
+      }
     }
   });
   return 0;

@@ -65,6 +65,16 @@ def blocks_raw(nx: int, ny: int, m: int, seed: int, nthreads: int = 0) -> np.nda
     return out
 
 
+def block_lines(nx: int, ny: int, m: int, seed: int, a: int, nthreads: int = 0):
+    """(rows, cols), each (nb, m): rows[t, b] = Z_t(a, b), cols[t, b] = Z_t(b, a)."""
+    nb = num_blocks(nx, ny)
+    rows = np.empty((nb, m), dtype=np.complex128)
+    cols = np.empty((nb, m), dtype=np.complex128)
+    if lib().tbtgen_block_lines(nx, ny, m, seed, a, _ptr(rows), _ptr(cols), nthreads):
+        raise ValueError("tbtgen_block_lines failed")
+    return rows, cols
+
+
 def correction(m: int, rank: int, seed: int, scale: float = 0.1):
     """(d[40, m], U[40, rank, m], V[40, rank, m]) in the C ABI layout."""
     d = np.empty((40, m), dtype=np.complex128)

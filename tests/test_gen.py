@@ -73,3 +73,23 @@ def test_components():
     assert [gen.component(4, 3, 0, c) for c in range(4)] == [1, 4, 4, 7]
     assert [gen.component(4, 3, 1, c) for c in range(4)] == [2, 5, 5, 8]
     assert [gen.component(4, 3, 2, c) for c in range(4)] == [3, 6, 6, 9]
+
+
+def test_block_lines_match_blocks():
+    """tbtgen_block_lines (row a / column a of every canonical block) draws
+    the same values as tbtgen_blocks; oracle.sampled_apply builds on it."""
+    nx, ny, m = 4, 3, 5
+    g = gen.blocks(nx, ny, m, 9)  # [t, a, b]
+    for a in range(m):
+        rows, cols = gen.block_lines(nx, ny, m, 9, a)
+        assert np.array_equal(rows, g[:, a, :]) and np.array_equal(cols, g[:, :, a])
+
+
+def test_sampled_apply_matches_full_apply():
+    import oracle
+    nx, ny, m = 5, 4, 6
+    o = oracle.Oracle(nx, ny, m, gen.blocks_raw(nx, ny, m, 3))
+    x = gen.rhs_normal(nx * ny * m, 1, 4)[:, 0]
+    y = o.applyA(x).reshape(nx * ny, m)
+    ys, tf, tr = oracle.sampled_apply(nx, ny, m, 3, [0, 4, 5], x)
+    assert np.array_equal(ys, y[:, [0, 4, 5]].T) and tf >= 0 and tr >= 0
