@@ -243,8 +243,8 @@ tbt_status tbt_get_spectrum_bin(tbt_ctx* ctx, long long f, double* out);
  * replayed from a CUDA graph); tbt_timing_read synchronises and returns the
  * summed K3 milliseconds and the number of timed launches since enabling.
  * On a distributed context (tbt_dist_init) the timed sections are instead
- * the NCCL exchanges of every apply (forward all-to-all, all-to-all back,
- * and the x slab all-gather of the edge/corner correction). */
+ * the exchanges of every apply (forward all-to-all, all-to-all back, and
+ * the one-row halo exchange of the edge/corner correction). */
 tbt_status tbt_set_timing(tbt_ctx* ctx, int on);
 tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
 
@@ -258,9 +258,21 @@ tbt_status tbt_timing_read(tbt_ctx* ctx, double* binprod_ms_total, int* count);
  * tbt_gmres then take and return this rank's row slab (tbt_dist_rows). The
  * distributed tbt_gmres runs the low-synchronisation Arnoldi (orthog = 1
  * whatever opts->orthog says) with two ncclAllReduce calls per iteration;
- * every rank returns the same stats. */
+ * every rank returns the same stats. Requires nranks <= min(ny, L0). */
 tbt_status tbt_dist_unique_id(char* id /* NCCL_UNIQUE_ID_BYTES = 128 */);
 tbt_status tbt_dist_init(tbt_ctx* ctx, int nranks, int rank, const char* id);
+/* The same sharded operator with an in-process transport: nranks contexts
+ * of ONE process (any device, normally all on one GPU) that share the same
+ * 128-byte id form a group; every rank's calls must be issued concurrently
+ * from its own host thread (as the ranks of a multi-process job would be).
+ * Exchanges synchronise the calling rank's stream, meet the other ranks at a
+ * host barrier and copy device to device; all-reduce sums run in fixed rank
+ * order. The pack / exchange / unpack code is the NCCL path's. Used to run
+ * and test the P > 1 partition on a single GPU. A failed call on one rank
+ * aborts the group (the others fail instead of waiting). */
+tbt_status tbt_dist_init_loopback(tbt_ctx* ctx, int nranks, int rank, const char* id);
+/* 0 not distributed, 1 NCCL, 2 loopback. */
+tbt_status tbt_dist_transport(const tbt_ctx* ctx, int* kind);
 tbt_status tbt_dist_rows(const tbt_ctx* ctx, int* row_begin, int* row_end);
 /* The partition itself (host only, no device needed). */
 tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin,

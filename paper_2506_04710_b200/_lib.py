@@ -78,6 +78,8 @@ SIGNATURES = {
     "tbt_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "tbt_dist_unique_id": (C.c_int, [C.c_char_p]),
     "tbt_dist_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
+    "tbt_dist_init_loopback": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
+    "tbt_dist_transport": (C.c_int, [C.c_void_p, ip]),
     "tbt_dist_rows": (C.c_int, [C.c_void_p, ip, ip]),
     "tbt_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, ip, ip, ip, ip]),
     "tbt_phase_times": (C.c_int, [C.c_void_p, C.c_int, dp]),

@@ -244,6 +244,30 @@ int smCount(int device) {
 
 void setError(const std::string& msg) { gLastError = msg; }
 
+// The nine-component correction as terms grouped by target (tbt_gen.h):
+// for every element e of a non-interior component and relation rel with an
+// in-array neighbour e', y_e += P x_e' and y_e' += P^T x_e.
+std::vector<std::vector<std::array<int, 4>>> corrTermsByTarget(int nx, int ny) {
+  static const int dr[5] = {0, 0, 0, 1, -1};
+  static const int dc[5] = {0, 1, -1, 0, 0};
+  std::vector<std::vector<std::array<int, 4>>> byTarget(static_cast<size_t>(nx) * ny);
+  for (int r = 0; r < ny; ++r)
+    for (int col = 0; col < nx; ++col) {
+      const int comp = componentOf(nx, ny, r, col);
+      if (comp == 5) continue;
+      const int e = r * nx + col;
+      for (int rel = 0; rel < 5; ++rel) {
+        const int r2 = r + dr[rel], c2 = col + dc[rel];
+        if (r2 < 0 || r2 >= ny || c2 < 0 || c2 >= nx) continue;
+        const int e2 = r2 * nx + c2;
+        const int slot = kSlotOfComp[comp] * 5 + rel;
+        byTarget[e].push_back({e, e2, slot, 0});   // y_e  += P   x_e'
+        byTarget[e2].push_back({e2, e, slot, 1});  // y_e' += P^T x_e
+      }
+    }
+  return byTarget;
+}
+
 }  // namespace tbt
 
 using namespace tbt;
@@ -263,7 +287,11 @@ template <typename Fn>
 tbt_status guardedCtx(tbt_ctx* h, Fn&& fn) {
   if (!h) return guarded(fn);  // fn reports the null argument
   std::lock_guard<std::recursive_mutex> lock(h->mu);
-  return guarded(fn);
+  const tbt_status st = guarded(fn);
+  // A failed call on one rank of a loopback group must not leave the other
+  // ranks waiting at its next exchange.
+  if (st != TBT_OK && h->c.comm) h->c.comm->abort();
+  return st;
 }
 }  // namespace
 
@@ -520,23 +548,7 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
       uploadSync(c.dCorrV, v, static_cast<size_t>(40) * rank * m * sizeof(double2), c.stream);
     }
     // Term list grouped by target element (CSR).
-    static const int dr[5] = {0, 0, 0, 1, -1};
-    static const int dc[5] = {0, 1, -1, 0, 0};
-    std::vector<std::vector<std::array<int, 4>>> byTarget(c.ne);
-    for (int r = 0; r < c.ny; ++r)
-      for (int col = 0; col < c.nx; ++col) {
-        const int comp = componentOf(c.nx, c.ny, r, col);
-        if (comp == 5) continue;
-        const int e = r * c.nx + col;
-        for (int rel = 0; rel < 5; ++rel) {
-          const int r2 = r + dr[rel], c2 = col + dc[rel];
-          if (r2 < 0 || r2 >= c.ny || c2 < 0 || c2 >= c.nx) continue;
-          const int e2 = r2 * c.nx + c2;
-          const int slot = kSlotOfComp[comp] * 5 + rel;
-          byTarget[e].push_back({e, e2, slot, 0});   // y_e  += P   x_e'
-          byTarget[e2].push_back({e2, e, slot, 1});  // y_e' += P^T x_e
-        }
-      }
+    const auto byTarget = corrTermsByTarget(c.nx, c.ny);
     std::vector<int> info, targets, ptr{0}, eptr{0};
     for (int e = 0; e < c.ne; ++e) {
       eptr.push_back(eptr.back() + static_cast<int>(byTarget[e].size()));
@@ -1176,6 +1188,7 @@ tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin, i
                          int* cols) {
   return guarded([&] {
     TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks && ny >= 1 && L0 >= 1, "tbt_dist_plan: bad arguments");
+    TBT_USER_CHECK(nranks <= ny && nranks <= L0, "tbt_dist_plan: more ranks than element rows or level-0 bins");
     std::vector<int> rs;
     std::vector<std::vector<int>> cl;
     distPlan(ny, L0, nranks, rs, cl);
@@ -1186,43 +1199,61 @@ tbt_status tbt_dist_plan(int ny, int L0, int nranks, int rank, int* row_begin, i
   });
 }
 
+namespace {
+// Shared by both transports: the partition (dist.cu distPlan), the
+// exchange buffers and the communicator of this rank.
+void distInit(tbt_ctx* h, int nranks, int rank, const char* id, bool loopback) {
+  TBT_USER_CHECK(h && id, "tbt_dist_init: null argument");
+  Ctx& c = h->c;
+  TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
+  TBT_USER_CHECK(!c.margin, "tbt_dist_init: margin parts are not supported on a distributed context");
+  TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "tbt_dist_init: bad rank");
+  TBT_USER_CHECK(nranks <= c.L0, "tbt_dist_init: more ranks than level-0 bins");
+  // Every rank owns at least one element row (its slab of the vectors, the
+  // halo rows of the correction, non-empty reduction grids).
+  TBT_USER_CHECK(nranks <= c.ny, "tbt_dist_init: more ranks than element rows (ny)");
+  TBT_CUDA_CHECK(cudaSetDevice(c.device));
+  distFree(c);
+  c.dropGraph();
+  c.nranks = nranks;
+  c.myRank = rank;
+  distPlan(c.ny, c.L0, nranks, c.rowStart, c.colsOfRank);
+  c.myRow0 = c.rowStart[rank];
+  c.myRows = c.rowStart[rank + 1] - c.rowStart[rank];
+  c.myColList = c.colsOfRank[rank];
+  c.colsOffset.assign(nranks + 1, 0);
+  std::vector<int> flat;
+  for (int q = 0; q < nranks; ++q) {
+    flat.insert(flat.end(), c.colsOfRank[q].begin(), c.colsOfRank[q].end());
+    c.colsOffset[q + 1] = static_cast<int>(flat.size());
+  }
+  const long long B = static_cast<long long>(c.maxNrhs) * c.m;
+  const long long myCols = static_cast<long long>(c.myColList.size());
+  TBT_CUDA_CHECK(cudaMalloc(&c.dColsOfRank, flat.size() * sizeof(int)));
+  uploadSync(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), c.stream);
+  TBT_CUDA_CHECK(cudaMalloc(&c.dTrow, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dSend, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dTcol, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dRecv, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dXhalo, (c.myRows + 2) * static_cast<long long>(c.nx) * B * sizeof(double2)));
+  memsetSync(c.dXhalo, 0, (c.myRows + 2) * static_cast<long long>(c.nx) * B * sizeof(double2), c.stream);
+  c.comm = loopback ? makeLoopbackComm(nranks, rank, id) : makeNcclComm(nranks, rank, id);
+  c.dist = true;
+}
+}  // namespace
+
 tbt_status tbt_dist_init(tbt_ctx* h, int nranks, int rank, const char* id) {
-  return guardedCtx(h, [&] {
-    TBT_USER_CHECK(h && id, "tbt_dist_init: null argument");
-    Ctx& c = h->c;
-    TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
-    TBT_USER_CHECK(!c.margin, "tbt_dist_init: margin parts are not supported on a distributed context");
-    TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "tbt_dist_init: bad rank");
-    TBT_USER_CHECK(nranks <= c.L0, "tbt_dist_init: more ranks than level-0 bins");
-    TBT_CUDA_CHECK(cudaSetDevice(c.device));
-    distFree(c);
-    c.dropGraph();
-    c.nranks = nranks;
-    c.myRank = rank;
-    distPlan(c.ny, c.L0, nranks, c.rowStart, c.colsOfRank);
-    c.myRow0 = c.rowStart[rank];
-    c.myRows = c.rowStart[rank + 1] - c.rowStart[rank];
-    c.myColList = c.colsOfRank[rank];
-    c.colsOffset.assign(nranks + 1, 0);
-    std::vector<int> flat;
-    for (int q = 0; q < nranks; ++q) {
-      flat.insert(flat.end(), c.colsOfRank[q].begin(), c.colsOfRank[q].end());
-      c.colsOffset[q + 1] = static_cast<int>(flat.size());
-    }
-    const long long B = static_cast<long long>(c.maxNrhs) * c.m;
-    const long long myCols = static_cast<long long>(c.myColList.size());
-    TBT_CUDA_CHECK(cudaMalloc(&c.dColsOfRank, flat.size() * sizeof(int)));
-    uploadSync(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), c.stream);
-    TBT_CUDA_CHECK(cudaMalloc(&c.dTrow, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMalloc(&c.dSend, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMalloc(&c.dTcol, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMalloc(&c.dRecv, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMalloc(&c.dXfull, c.ne * B * sizeof(double2)));
-    ncclUniqueId u;
-    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
-    const ncclResult_t r = nccl().commInitRank(&c.comm, nranks, u, rank);
-    if (r != ncclSuccess) throw Error{TBT_CUDA_ERROR, std::string("ncclCommInitRank: ") + nccl().errorString(r)};
-    c.dist = true;
+  return guardedCtx(h, [&] { distInit(h, nranks, rank, id, false); });
+}
+
+tbt_status tbt_dist_init_loopback(tbt_ctx* h, int nranks, int rank, const char* id) {
+  return guardedCtx(h, [&] { distInit(h, nranks, rank, id, true); });
+}
+
+tbt_status tbt_dist_transport(const tbt_ctx* h, int* kind) {
+  return guarded([&] {
+    TBT_USER_CHECK(h && kind, "tbt_dist_transport: null argument");
+    *kind = h->c.dist && h->c.comm ? h->c.comm->kind() : 0;
   });
 }
 

@@ -207,21 +207,27 @@ __global__ void antisymApply(const double2* __restrict__ K, const double2* __res
 
 }  // namespace
 
-void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
-  if (!c.haveCorr || c.nTerms == 0) return;
+void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
+  if (t.nTargets == 0) return;
   if (nrhs >= 8 && (c.rank == 4 || c.rank == 8) && (c.m == 64 || c.m == 128)) {
-    dim3 grid(c.nTargets, (nrhs + 31) / 32);
+    dim3 grid(t.nTargets, (nrhs + 31) / 32);
     auto k = c.m == 64 ? (c.rank == 4 ? corrMulti<2, 4> : corrMulti<2, 8>)
                        : (c.rank == 4 ? corrMulti<4, 4> : corrMulti<4, 8>);
-    k<<<grid, 256, 0, s>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs);
+    k<<<grid, 256, 0, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs);
     TBT_CUDA_CHECK(cudaGetLastError());
     return;
   }
-  dim3 grid(c.nTargets, nrhs);
-  const size_t smem = static_cast<size_t>(c.maxTermsPerTarget) * std::max(c.rank, 1) * sizeof(double2);
-  corrFused<<<grid, 256, smem, s>>>(c.dTermInfo, c.dTargetList, c.dTargetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr,
+  dim3 grid(t.nTargets, nrhs);
+  const size_t smem = static_cast<size_t>(t.maxTerms) * std::max(c.rank, 1) * sizeof(double2);
+  corrFused<<<grid, 256, smem, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr,
                                     c.m, c.rank, nrhs);
   TBT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
+  if (!c.haveCorr || c.nTerms == 0) return;
+  launchCorrVectorOn(c, CorrTables{c.dTermInfo, c.dTargetList, c.dTargetPtr, c.nTargets, c.maxTermsPerTarget}, x,
+                     ycorr, nrhs, s);
 }
 
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs) {

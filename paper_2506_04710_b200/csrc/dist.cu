@@ -12,13 +12,23 @@
 //    ncclRecv; NCCL has no all-to-all primitive) -> column FFTs of the local
 //    columns -> bin products of the local pairs (the K3 kernels) -> inverse
 //    column FFTs keeping ny rows -> all-to-all back -> inverse row FFTs.
-//    The edge/corner correction needs neighbour rows: x is all-gathered
-//    (P2P sends of each rank's slab) and each rank adds its rows of it.
+//    The edge/corner correction of an element reads x of its 4-neighbours
+//    only: one halo element row is exchanged with each slab neighbour and
+//    each rank evaluates the terms of its own target elements.
+//  * The exchanges go through a Comm (tbt_internal.cuh): NCCL across
+//    processes / GPUs, or the in-process loopback transport that runs P
+//    rank contexts on one device (tbt_dist_init_loopback).
 // Replaces applyA / apply (proj/src/linsolve.cpp:260-290,373-388), which has
 // no distributed counterpart ("Non-goals: distributed").
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 
@@ -53,6 +63,202 @@ const NcclApi& nccl() {
   if (!api.ok) throw Error{TBT_CUDA_ERROR, "NCCL (libnccl.so.2) could not be loaded"};
   return api;
 }
+
+// ---------------------------------------------------------------- NCCL
+namespace {
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(int nranks, int rank, const char* id) {
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    const ncclResult_t r = nccl().commInitRank(&comm_, nranks, u, rank);
+    if (r != ncclSuccess) throw Error{TBT_CUDA_ERROR, std::string("ncclCommInitRank: ") + nccl().errorString(r)};
+  }
+  ~NcclComm() override {
+    if (comm_) nccl().commDestroy(comm_);
+  }
+  void groupStart() override { TBT_NCCL_CHECK(nccl().groupStart()); }
+  void send(const void* buf, size_t n, int peer, cudaStream_t s) override {
+    TBT_NCCL_CHECK(nccl().send(buf, n, ncclDouble, peer, comm_, s));
+  }
+  void recv(void* buf, size_t n, int peer, cudaStream_t s) override {
+    TBT_NCCL_CHECK(nccl().recv(buf, n, ncclDouble, peer, comm_, s));
+  }
+  void groupEnd(cudaStream_t) override { TBT_NCCL_CHECK(nccl().groupEnd()); }
+  void allReduceSum(double* buf, size_t n, cudaStream_t s) override {
+    TBT_NCCL_CHECK(nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, comm_, s));
+  }
+  int kind() const override { return 1; }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+};
+
+// ---------------------------------------------------------------- loopback
+constexpr int kLoopMaxRanks = 64;
+constexpr auto kLoopTimeout = std::chrono::seconds(120);
+
+struct LoopSend {
+  int peer;
+  const void* buf;
+  size_t n;
+};
+
+// Shared state of the P contexts of one loopback group (same process).
+struct LoopGroup {
+  int P = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long generation = 0;
+  bool aborted = false;
+  std::vector<std::vector<LoopSend>> sends;  // [rank] this group's posted sends
+  std::vector<const double*> reduceIn;       // [rank] all-reduce inputs
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) throw Error{TBT_CUDA_ERROR, "loopback transport: another rank failed"};
+    const unsigned long long g = generation;
+    if (++arrived == P) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, kLoopTimeout, [&] { return generation != g || aborted; })) {
+      aborted = true;
+      cv.notify_all();
+      throw Error{TBT_CUDA_ERROR, "loopback transport: timed out waiting for the other ranks"};
+    }
+    if (aborted) throw Error{TBT_CUDA_ERROR, "loopback transport: another rank failed"};
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+std::mutex gLoopMu;
+std::map<std::string, std::weak_ptr<LoopGroup>> gLoopGroups;
+
+struct SumArgs {
+  const double* in[kLoopMaxRanks];
+};
+
+// out[k] = in[0][k] + in[1][k] + ... + in[P-1][k], in that order on every
+// rank, so all ranks hold bitwise identical totals.
+__global__ void loopSum(SumArgs a, int P, double* __restrict__ out, long long n) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double v = a.in[0][k];
+    for (int r = 1; r < P; ++r) v += a.in[r][k];
+    out[k] = v;
+  }
+}
+
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm(int nranks, int rank, const char* id) : rank_(rank) {
+    if (nranks > kLoopMaxRanks) throw Error{TBT_USER_ERROR, "tbt_dist_init_loopback: at most 64 ranks"};
+    const std::string key(id, NCCL_UNIQUE_ID_BYTES);
+    std::lock_guard<std::mutex> lk(gLoopMu);
+    for (auto it = gLoopGroups.begin(); it != gLoopGroups.end();)
+      it = it->second.expired() ? gLoopGroups.erase(it) : std::next(it);
+    auto& slot = gLoopGroups[key];
+    g_ = slot.lock();
+    if (!g_) {
+      g_ = std::make_shared<LoopGroup>();
+      g_->P = nranks;
+      g_->sends.assign(nranks, {});
+      g_->reduceIn.assign(nranks, nullptr);
+      slot = g_;
+    }
+    if (g_->P != nranks) throw Error{TBT_USER_ERROR, "tbt_dist_init_loopback: ranks disagree on the group size"};
+  }
+  ~LoopbackComm() override {
+    if (tmp_) cudaFree(tmp_);
+  }
+  void groupStart() override {
+    sends_.clear();
+    recvs_.clear();
+  }
+  void send(const void* buf, size_t n, int peer, cudaStream_t) override { sends_.push_back({peer, buf, n}); }
+  void recv(void* buf, size_t n, int peer, cudaStream_t) override { recvs_.push_back({peer, buf, n}); }
+  void groupEnd(cudaStream_t s) override {
+    guard([&] {
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));  // send buffers complete
+      g_->sends[rank_] = sends_;
+      g_->barrier();
+      // The k-th receive from q matches q's k-th send to this rank (NCCL's
+      // ordering rule for grouped point-to-point operations).
+      std::vector<int> used(g_->P, 0);
+      for (const LoopSend& r : recvs_) {
+        const std::vector<LoopSend>& theirs = g_->sends[r.peer];
+        int seen = 0;
+        const LoopSend* match = nullptr;
+        for (const LoopSend& t : theirs)
+          if (t.peer == rank_ && seen++ == used[r.peer]) {
+            match = &t;
+            break;
+          }
+        if (!match || match->n != r.n)
+          throw Error{TBT_CUDA_ERROR, "loopback transport: unmatched or mis-sized receive"};
+        ++used[r.peer];
+        if (r.n)
+          TBT_CUDA_CHECK(cudaMemcpyAsync(const_cast<void*>(r.buf), match->buf, r.n * sizeof(double),
+                                         cudaMemcpyDeviceToDevice, s));
+      }
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));  // received data landed
+      g_->barrier();                             // every peer finished reading my sends
+    });
+  }
+  void allReduceSum(double* buf, size_t n, cudaStream_t s) override {
+    guard([&] {
+      if (n > tmpN_) {
+        if (tmp_) cudaFree(tmp_);
+        tmp_ = nullptr;
+        TBT_CUDA_CHECK(cudaMalloc(&tmp_, n * sizeof(double)));
+        tmpN_ = n;
+      }
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+      g_->reduceIn[rank_] = buf;
+      g_->barrier();
+      SumArgs a{};
+      for (int r = 0; r < g_->P; ++r) a.in[r] = g_->reduceIn[r];
+      const int blocks = static_cast<int>(std::min<long long>((static_cast<long long>(n) + 255) / 256, 1024));
+      if (n) loopSum<<<std::max(blocks, 1), 256, 0, s>>>(a, g_->P, tmp_, static_cast<long long>(n));
+      TBT_CUDA_CHECK(cudaGetLastError());
+      TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+      g_->barrier();  // every rank read every input
+      if (n) TBT_CUDA_CHECK(cudaMemcpyAsync(buf, tmp_, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    });
+  }
+  void abort() override { g_->abort(); }
+  int kind() const override { return 2; }
+
+ private:
+  template <class F>
+  void guard(F&& f) {
+    try {
+      f();
+    } catch (...) {
+      g_->abort();
+      throw;
+    }
+  }
+  int rank_;
+  std::shared_ptr<LoopGroup> g_;
+  std::vector<LoopSend> sends_, recvs_;
+  double* tmp_ = nullptr;
+  size_t tmpN_ = 0;
+};
+
+}  // namespace
+
+Comm* makeNcclComm(int nranks, int rank, const char* id) { return new NcclComm(nranks, rank, id); }
+Comm* makeLoopbackComm(int nranks, int rank, const char* id) { return new LoopbackComm(nranks, rank, id); }
 
 // Row slabs and column groups (pure host logic; tested on the CPU).
 void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols) {
@@ -112,12 +318,56 @@ int gridFor(long long n, int sms) { return static_cast<int>(std::max<long long>(
 
 void distFree(Ctx& c) {
   for (void* p : {static_cast<void*>(c.dColsOfRank), static_cast<void*>(c.dTrow), static_cast<void*>(c.dTcol),
-                  static_cast<void*>(c.dSend), static_cast<void*>(c.dRecv), static_cast<void*>(c.dXfull)})
+                  static_cast<void*>(c.dSend), static_cast<void*>(c.dRecv), static_cast<void*>(c.dXhalo),
+                  static_cast<void*>(c.dTermInfoLoc), static_cast<void*>(c.dTargetListLoc),
+                  static_cast<void*>(c.dTargetPtrLoc), static_cast<void*>(c.dYcorrLoc)})
     if (p) cudaFree(p);
   c.dColsOfRank = nullptr;
-  c.dTrow = c.dTcol = c.dSend = c.dRecv = c.dXfull = nullptr;
-  if (c.comm) nccl().commDestroy(c.comm);
+  c.dTrow = c.dTcol = c.dSend = c.dRecv = c.dXhalo = c.dYcorrLoc = nullptr;
+  c.dTermInfoLoc = c.dTargetListLoc = c.dTargetPtrLoc = nullptr;
+  c.nTargetsLoc = c.maxTermsLoc = 0;
+  c.distCorrReady = false;
+  delete c.comm;
   c.comm = nullptr;
+}
+
+// The correction terms whose target is one of this rank's elements
+// (corrTermsByTarget, api.cu: the single-GPU term order per target), with
+// sources re-indexed into the halo buffer dXhalo = x rows
+// [myRow0 - 1, myRow0 + myRows] (rows outside the array unused) and
+// targets into the local slab. Built on the first distributed apply.
+void distCorrPrepare(Ctx& c) {
+  if (c.distCorrReady) return;
+  const auto byTarget = corrTermsByTarget(c.nx, c.ny);
+  const int r0 = c.myRow0, r1 = c.myRow0 + c.myRows;
+  std::vector<int> info, targets, ptr{0};
+  int maxTerms = 0;
+  for (int e = r0 * c.nx; e < r1 * c.nx; ++e) {
+    const auto& terms = byTarget[e];
+    if (terms.empty()) continue;
+    targets.push_back(e - r0 * c.nx);
+    for (const auto& t : terms) {
+      const int srow = t[1] / c.nx, scol = t[1] % c.nx;
+      if (srow < r0 - 1 || srow > r1) throw Error{TBT_CUDA_ERROR, "distributed correction: source outside the halo"};
+      info.insert(info.end(), {targets.back(), (srow - (r0 - 1)) * c.nx + scol, t[2], t[3]});
+    }
+    ptr.push_back(static_cast<int>(info.size() / 4));
+    maxTerms = std::max(maxTerms, static_cast<int>(terms.size()));
+  }
+  c.nTargetsLoc = static_cast<int>(targets.size());
+  c.maxTermsLoc = maxTerms;
+  const size_t slab = static_cast<size_t>(c.myRows) * c.nx * c.maxNrhs * c.m;
+  TBT_CUDA_CHECK(cudaMalloc(&c.dYcorrLoc, std::max<size_t>(1, slab) * sizeof(double2)));
+  memsetSync(c.dYcorrLoc, 0, std::max<size_t>(1, slab) * sizeof(double2), c.stream);
+  if (c.nTargetsLoc > 0) {
+    TBT_CUDA_CHECK(cudaMalloc(&c.dTermInfoLoc, info.size() * sizeof(int)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dTargetListLoc, targets.size() * sizeof(int)));
+    TBT_CUDA_CHECK(cudaMalloc(&c.dTargetPtrLoc, ptr.size() * sizeof(int)));
+    uploadSync(c.dTermInfoLoc, info.data(), info.size() * sizeof(int), c.stream);
+    uploadSync(c.dTargetListLoc, targets.data(), targets.size() * sizeof(int), c.stream);
+    uploadSync(c.dTargetPtrLoc, ptr.data(), ptr.size() * sizeof(int), c.stream);
+  }
+  c.distCorrReady = true;
 }
 
 namespace {
@@ -184,14 +434,14 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   }
   TBT_CUDA_CHECK(cudaGetLastError());
   commSection(c, [&] {
-    TBT_NCCL_CHECK(nccl().groupStart());
+    c.comm->groupStart();
     for (int q = 0; q < P; ++q) {
       const size_t sc = static_cast<size_t>(sendOff[q + 1] - sendOff[q]) * 2;
       const size_t rc = static_cast<size_t>(recvOff[q + 1] - recvOff[q]) * 2;
-      if (sc) TBT_NCCL_CHECK(nccl().send(c.dSend + sendOff[q], sc, ncclDouble, q, c.comm, s));
-      if (rc) TBT_NCCL_CHECK(nccl().recv(c.dRecv + recvOff[q], rc, ncclDouble, q, c.comm, s));
+      if (sc) c.comm->send(c.dSend + sendOff[q], sc, q, s);
+      if (rc) c.comm->recv(c.dRecv + recvOff[q], rc, q, s);
     }
-    TBT_NCCL_CHECK(nccl().groupEnd());
+    c.comm->groupEnd(s);
   });
   // Received blocks are [rows of q][my columns][b] in row order: exactly
   // dTcol[r][j][b] for r = 0..ny-1 (rank slabs are contiguous and ordered).
@@ -236,17 +486,15 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   // 6. All-to-all back: rows of rank q x my columns -> q; from q: my rows x
   //    columns of q.
   commSection(c, [&] {
-    TBT_NCCL_CHECK(nccl().groupStart());
+    c.comm->groupStart();
     for (int q = 0; q < P; ++q) {
       const long long rows = c.rowStart[q + 1] - c.rowStart[q];
       const size_t sc = static_cast<size_t>(rows) * myCols * B * 2;
       const size_t rc = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * B * 2;
-      if (sc)
-        TBT_NCCL_CHECK(nccl().send(c.dTcol + static_cast<long long>(c.rowStart[q]) * myCols * B, sc, ncclDouble, q,
-                                c.comm, s));
-      if (rc) TBT_NCCL_CHECK(nccl().recv(c.dSend + sendOff[q], rc, ncclDouble, q, c.comm, s));
+      if (sc) c.comm->send(c.dTcol + static_cast<long long>(c.rowStart[q]) * myCols * B, sc, q, s);
+      if (rc) c.comm->recv(c.dSend + sendOff[q], rc, q, s);
     }
-    TBT_NCCL_CHECK(nccl().groupEnd());
+    c.comm->groupEnd(s);
   });
   for (int q = 0; q < P; ++q) {
     const int nq = static_cast<int>(c.colsOfRank[q].size());
@@ -276,25 +524,36 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   ia.tw = c.dTw0;
   launchFftPass(ia, s);
 
-  // 8. Spatial terms: K (element-local) and the correction (needs x of the
-  //    neighbouring rows: all-gather the slabs, then add my rows).
+  // 8. Spatial terms: K (element-local) and the correction. A correction
+  //    term couples an element with its 4-neighbours only, so one halo row
+  //    from each slab neighbour suffices: dXhalo = [row r0-1][my rows][row
+  //    r1] (every rank owns >= 1 row, tbt_dist_init checks nranks <= ny).
   launchAntisym(c, x, y, nrhs, c.myRows * c.nx);
   if (withCorr && c.haveCorr && c.nTerms > 0) {
-    commSection(c, [&] {
-      TBT_NCCL_CHECK(nccl().groupStart());
-      const size_t mine = static_cast<size_t>(c.myRows) * c.nx * B * 2;
-      for (int q = 0; q < P; ++q) {
-        const size_t rc = static_cast<size_t>(c.rowStart[q + 1] - c.rowStart[q]) * c.nx * B * 2;
-        if (mine) TBT_NCCL_CHECK(nccl().send(x, mine, ncclDouble, q, c.comm, s));
-        if (rc)
-          TBT_NCCL_CHECK(nccl().recv(c.dXfull + static_cast<long long>(c.rowStart[q]) * c.nx * B, rc, ncclDouble, q,
-                                  c.comm, s));
-      }
-      TBT_NCCL_CHECK(nccl().groupEnd());
-    });
-    launchCorrVector(c, c.dXfull, c.dYcorr, nrhs, s);
-    const long long cnt = static_cast<long long>(c.myRows) * c.nx * B;
-    addRows<<<gridFor(cnt, sms), 256, 0, s>>>(y, c.dYcorr + static_cast<long long>(c.myRow0) * c.nx * B, cnt);
+    distCorrPrepare(c);
+    const long long rowLen = static_cast<long long>(c.nx) * B;
+    const long long mine = static_cast<long long>(c.myRows) * rowLen;
+    TBT_CUDA_CHECK(cudaMemcpyAsync(c.dXhalo + rowLen, x, mine * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    if (P > 1) {
+      commSection(c, [&] {
+        c.comm->groupStart();
+        const size_t n = static_cast<size_t>(rowLen) * 2;
+        if (me > 0) {
+          c.comm->send(x, n, me - 1, s);
+          c.comm->recv(c.dXhalo, n, me - 1, s);
+        }
+        if (me < P - 1) {
+          c.comm->send(x + mine - rowLen, n, me + 1, s);
+          c.comm->recv(c.dXhalo + rowLen + mine, n, me + 1, s);
+        }
+        c.comm->groupEnd(s);
+      });
+    }
+    if (c.nTargetsLoc > 0) {
+      CorrTables t{c.dTermInfoLoc, c.dTargetListLoc, c.dTargetPtrLoc, c.nTargetsLoc, c.maxTermsLoc};
+      launchCorrVectorOn(c, t, c.dXhalo, c.dYcorrLoc, nrhs, s);
+    }
+    addRows<<<gridFor(mine, sms), 256, 0, s>>>(y, c.dYcorrLoc, mine);
     TBT_CUDA_CHECK(cudaGetLastError());
   }
 }

@@ -723,9 +723,7 @@ struct ColsRunner {
   void reduce(int nslots) {
     colReduce<<<dim3((nslots + 7) / 8, A->ncols), 256, 0, s>>>(*A, L, nslots);
     TBT_CUDA_CHECK(cudaGetLastError());
-    if (c->dist)
-      TBT_NCCL_CHECK(nccl().allReduce(L.tot, L.tot, static_cast<size_t>(nslots) * A->ncols * 2, ncclDouble, ncclSum,
-                                      c->comm, s));
+    if (c->dist) c->comm->allReduceSum(reinterpret_cast<double*>(L.tot), static_cast<size_t>(nslots) * A->ncols * 2, s);
   }
   template <int K>
   void vecPass(int mode) {

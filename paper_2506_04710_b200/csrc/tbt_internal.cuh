@@ -1,6 +1,7 @@
 // Internal declarations of the B200 block-Toeplitz library (libtbt.so).
 #pragma once
 
+#include <array>
 #include <atomic>
 
 #include <cuda_runtime.h>
@@ -96,6 +97,29 @@ struct CorrTerm {  // y[target] += P x[source] (trans 0) or P^T x[source]
   int target, source, slot, trans;
 };
 
+// Transport of the sharded operator (dist.cu): grouped point-to-point
+// exchanges and a sum all-reduce, on the calling context's stream.
+//  * NCCL: one process per GPU (ncclSend / ncclRecv / ncclAllReduce over
+//    NVLink / NVSwitch), the production path;
+//  * loopback: P rank contexts of ONE process on one device, each driven by
+//    its own host thread; groupEnd / allReduceSum synchronise the caller's
+//    stream, meet the other ranks at a host barrier and move the data with
+//    device-to-device copies (sums in fixed rank order). No kernel ever
+//    waits on another rank, so it is safe on a single GPU, and it runs the
+//    exact pack / exchange / unpack code of the NCCL path at any P.
+struct Comm {
+  virtual ~Comm() = default;
+  virtual void groupStart() = 0;
+  virtual void send(const void* buf, size_t ndoubles, int peer, cudaStream_t s) = 0;
+  virtual void recv(void* buf, size_t ndoubles, int peer, cudaStream_t s) = 0;
+  virtual void groupEnd(cudaStream_t s) = 0;
+  virtual void allReduceSum(double* buf, size_t ndoubles, cudaStream_t s) = 0;  // in place
+  virtual void abort() {}  // a rank failed: release the others (loopback)
+  virtual int kind() const = 0;  // 1 NCCL, 2 loopback
+};
+Comm* makeNcclComm(int nranks, int rank, const char* id);
+Comm* makeLoopbackComm(int nranks, int rank, const char* id);
+
 struct Ctx {
   int nx = 0, ny = 0, m = 0, ne = 0, maxNrhs = 1, device = 0;
   long long n = 0;  // nx*ny*m
@@ -125,7 +149,7 @@ struct Ctx {
   // s0 -> L0 - s0, so both bins of every stored pair are local).
   bool dist = false;
   int nranks = 1, myRank = 0;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;
   std::vector<int> rowStart;                  // [nranks+1]
   std::vector<std::vector<int>> colsOfRank;   // [nranks]
   std::vector<int> myColList;
@@ -136,7 +160,15 @@ struct Ctx {
   double2* dTcol = nullptr;   // [ny][myCols][B]
   double2* dSend = nullptr;
   double2* dRecv = nullptr;
-  double2* dXfull = nullptr;  // [ne][B] all-gathered x for the correction
+  double2* dXhalo = nullptr;  // [myRows + 2 halo rows][nx][B]: x for the local correction
+  // Correction terms whose target is a local element, sources indexed into
+  // dXhalo (row - (myRow0 - 1)), targets into this rank's slab.
+  int* dTermInfoLoc = nullptr;
+  int* dTargetListLoc = nullptr;
+  int* dTargetPtrLoc = nullptr;
+  int nTargetsLoc = 0, maxTermsLoc = 0;
+  double2* dYcorrLoc = nullptr;  // [myRows*nx][B], zero outside the targets
+  bool distCorrReady = false;
 
   // Generators (host copy kept for diagonal / K) and spectra.
   std::vector<double2> genHost;   // only the self block Z(0,0) (m*m, column-major)
@@ -222,6 +254,17 @@ constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
+// A term table (CSR by target): termInfo[4t..] = (target, source, slot, trans).
+struct CorrTables {
+  const int* termInfo;
+  const int* targetList;
+  const int* targetPtr;
+  int nTargets, maxTerms;
+};
+void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);
+// Per target element, its correction terms {target, source, slot, trans} in
+// the order every apply path accumulates them (api.cu).
+std::vector<std::vector<std::array<int, 4>>> corrTermsByTarget(int nx, int ny);
 void launchAntisym(Ctx& c, const double2* x, double2* y, int nrhs, int nElems = -1);  // correction.cu
 void launchLayout(const double2* in, double2* out, long long n, int nrhs, bool toInternal, cudaStream_t s, int m);  // apply.cu
 // External n_user x nrhs column-major <-> internal [e][rhs][m] of n_int rows per column (zero padding).

@@ -133,6 +133,10 @@ class ToeplitzMatvec:
         dist: (nranks, rank, nccl_unique_id_bytes) to shard the operator over
         one process per GPU (see dist_unique_id / init_from_torch); apply /
         applyA / diagonal then work on this rank's element-row slab.
+        (nranks, rank, group_id, "loopback") runs rank `rank` of the same
+        sharded operator in this process (tbt_dist_init_loopback; see
+        loopback_group_id): every rank's calls must then be issued
+        concurrently, one host thread per rank.
         spectra_cache: a TBTS1 file; loaded instead of K1 when it exists,
         written after K1 otherwise (row f3)."""
         self.rep = rep
@@ -162,8 +166,12 @@ class ToeplitzMatvec:
             _check(lib().tbt_set_margin(self._h, e.ctypes.data_as(C.POINTER(C.c_int)),
                                         *[a.ctypes.data_as(dp) for a in arrs]))
         if dist is not None:
-            nranks, rank, uid = dist
-            _check(lib().tbt_dist_init(self._h, int(nranks), int(rank), bytes(uid)))
+            nranks, rank, uid = dist[:3]
+            transport = dist[3] if len(dist) > 3 else "nccl"
+            if transport not in ("nccl", "loopback"):
+                raise UserError(f"transport must be 'nccl' or 'loopback', got {transport!r}")
+            init = lib().tbt_dist_init_loopback if transport == "loopback" else lib().tbt_dist_init
+            _check(init(self._h, int(nranks), int(rank), bytes(uid)))
         if cached:
             _check(lib().tbt_load_spectra(self._h, spectra_cache.encode()))
         else:
@@ -421,6 +429,12 @@ def dist_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().tbt_dist_unique_id(buf))
     return buf.raw
+
+
+def loopback_group_id() -> bytes:
+    """A fresh 128-byte id naming one in-process loopback group."""
+    import os
+    return os.urandom(128)
 
 
 def dist_plan(ny: int, L0: int, nranks: int, rank: int):
