@@ -27,10 +27,11 @@
  * reference's unknown order, element-major / basis-minor:
  * index (r*nx + c)*m + k (src/array_model.cpp:219-220,230-235). Several
  * right-hand sides are stored column-major (n x nrhs), like Eigen's MatrixXc.
- * One context is bound to one CUDA device and one stream; calls on a context
- * are serialised by the caller (the reference's apply is const and
- * re-entrant per thread; the batched nrhs entry points replace its
- * per-column threads, linsolve.cpp:572).
+ * One context is bound to one CUDA device and one stream. Every entry point
+ * takes the context's lock, so concurrent calls on one context are
+ * serialised by the library (use one context per thread for concurrency;
+ * the reference's apply is const and re-entrant per thread, and the batched
+ * nrhs entry points replace its per-column threads, linsolve.cpp:572).
  *
  * There is no CPU fallback: without a usable sm_100 device every compute
  * entry point returns TBT_CUDA_ERROR.
@@ -190,7 +191,13 @@ tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside,
                           double* brow, double* bcorner, double* c);
 /* Persisted bin-major half spectrum (+ the self block): tbt_load_spectra
  * replaces tbt_set_generators + tbt_precompute on a context of the same
- * nx, ny, m and embedding (K1 skipped across runs). */
+ * nx, ny, m and embedding (K1 skipped across runs). tbt_set_cache_key
+ * (<= 32 bytes, e.g. a digest of the generator blocks) names the generator
+ * set: tbt_save_spectra stores it, and tbt_load_spectra into a context with
+ * a key rejects (user error) a file written under another key or none. A
+ * context without a key loads any cache of its shape (explicit opt-in for
+ * callers that no longer hold the generators). */
+tbt_status tbt_set_cache_key(tbt_ctx* ctx, const unsigned char* key, int len);
 tbt_status tbt_save_spectra(tbt_ctx* ctx, const char* path);
 tbt_status tbt_load_spectra(tbt_ctx* ctx, const char* path);
 

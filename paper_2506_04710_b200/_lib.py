@@ -67,6 +67,7 @@ SIGNATURES = {
     "tbt_load_ztoe1": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "tbt_ztoe1_dims": (C.c_int, [C.c_char_p, ip, ip, ip]),
     "tbt_ztoe1_read": (C.c_int, [C.c_char_p, dp, dp, dp, dp, dp]),
+    "tbt_set_cache_key": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     "tbt_save_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
     "tbt_load_spectra": (C.c_int, [C.c_void_p, C.c_char_p]),
     "tbt_port_network": (C.c_int, [C.c_void_p, dp, C.c_longlong, C.c_int, llp, C.c_double, dp, dp, dp, dp, C.c_int]),

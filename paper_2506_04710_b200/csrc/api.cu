@@ -110,7 +110,10 @@ void refreshDiagonal(Ctx& c, std::vector<double2>* dOut) {
       }
   }
   marginDiagonal(c, d);  // C's diagonal after the element part (linsolve.cpp:400-406)
-  if (dOut) *dOut = d;
+  if (dOut) {  // tbt_diagonal: read only, the device Jacobi buffers stay as they are
+    *dOut = d;
+    return;
+  }
   auto invert = [](const std::vector<double2>& dv) {
     std::vector<double2> inv(dv.size());
     for (size_t k = 0; k < dv.size(); ++k) {
@@ -427,6 +430,7 @@ tbt_status tbt_set_stream(tbt_ctx* h, void* stream) {
   return guardedCtx(h, [&] {
     TBT_USER_CHECK(h, "tbt_set_stream: null context");
     Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     if (c.ownStream) {
       TBT_CUDA_CHECK(cudaStreamDestroy(c.stream));
@@ -508,6 +512,8 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     TBT_USER_CHECK(h, "tbt_set_correction: null context");
     Ctx& c = h->c;
     TBT_USER_CHECK(rank >= 0, "tbt_set_correction: rank must be >= 0");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    c.distCorrReady = false;  // a distributed context rebuilds its local term tables
     freePtr(c.dCorrD);
     freePtr(c.dCorrU);
     freePtr(c.dCorrV);
@@ -765,6 +771,7 @@ tbt_status tbt_diagonal(tbt_ctx* h, double* d) {
     TBT_USER_CHECK(h && d, "tbt_diagonal: null argument");
     Ctx& c = h->c;
     requireReady(c);
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
     std::vector<double2> dd;
     refreshDiagonal(c, &dd);
     const size_t first = c.dist ? static_cast<size_t>(c.myRow0) * c.nx * c.m : 0;
@@ -947,6 +954,16 @@ tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside, double* 
     put(brow, z.brow);
     put(bcorner, z.bcorner);
     put(cm, z.c);
+  });
+}
+
+tbt_status tbt_set_cache_key(tbt_ctx* h, const unsigned char* key, int len) {
+  return guardedCtx(h, [&] {
+    TBT_USER_CHECK(h && (key || len == 0) && len >= 0 && len <= 32, "tbt_set_cache_key: bad arguments");
+    Ctx& c = h->c;
+    std::memset(c.cacheKey, 0, sizeof c.cacheKey);
+    if (len > 0) std::memcpy(c.cacheKey, key, static_cast<size_t>(len));
+    c.haveCacheKey = len > 0;
   });
 }
 

@@ -379,11 +379,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
     ++histLen;
   };
   const double bnorm = sqrt(norm2(bl));
-  int iterations = 0, histLen = 0, converged = bnorm == 0.0 ? 1 : 0, done = converged;
+  int iterations = 0, histLen = 0, converged = bnorm == 0.0 ? 1 : 0, done = converged, checks = 0;
   double residual = 0.0, beta0 = 0.0, beta = 0.0;
   while (!done) {
     // r = b - A x, residual (linsolve.cpp:446-452).
     clusterApply(c, xl, withCorr != 0);
+    ++checks;
     for (int t = threadIdx.x; t < nloc; t += blockDim.x) w[t] = csub(bl[t], y[t]);
     __syncthreads();
     const double res = sqrt(norm2(w)) / bnorm;
@@ -564,6 +565,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CT) clusterGmresKer
     st.converged = converged;
     st.cycleActive = 0;
     st.histLen = histLen;
+    st.checks = checks;
   }
   c.cl.sync();
 }

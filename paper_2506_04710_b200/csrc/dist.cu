@@ -338,6 +338,11 @@ void distFree(Ctx& c) {
 // targets into the local slab. Built on the first distributed apply.
 void distCorrPrepare(Ctx& c) {
   if (c.distCorrReady) return;
+  for (void* p : {static_cast<void*>(c.dTermInfoLoc), static_cast<void*>(c.dTargetListLoc),
+                  static_cast<void*>(c.dTargetPtrLoc), static_cast<void*>(c.dYcorrLoc)})
+    if (p) cudaFree(p);
+  c.dTermInfoLoc = c.dTargetListLoc = c.dTargetPtrLoc = nullptr;
+  c.dYcorrLoc = nullptr;
   const auto byTarget = corrTermsByTarget(c.nx, c.ny);
   const int r0 = c.myRow0, r1 = c.myRow0 + c.myRows;
   std::vector<int> info, targets, ptr{0};

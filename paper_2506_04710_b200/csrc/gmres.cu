@@ -1064,9 +1064,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
       if (A.histCap > 0)
         TBT_CUDA_CHECK(cudaMemcpyAsync(hist.data(), A.hist, sizeof(double) * 2 * A.histCap, cudaMemcpyDeviceToHost, s));
       TBT_CUDA_CHECK(cudaStreamSynchronize(s));
-      int restarts = 0;  // matvecs: one per restart (history kinds 0 / 2) + one per inner iteration
-      for (int k = 0; k < std::min(st[0].histLen, A.histCap); ++k) restarts += hist[2 * k] != 1.0;
-      matvecs = restarts + st[0].iterations;
+      // matvecs: one per true-residual check (each restart and the final
+      // one, counted by the kernel) + one per inner iteration.
+      matvecs = st[0].checks + st[0].iterations;
       out = st;
       return;
     }

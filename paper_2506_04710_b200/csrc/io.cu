@@ -219,9 +219,11 @@ void readZtoe1(const std::string& path, Ztoe1Data& out) {
 namespace {
 struct SpecHeader {
   char magic[5];
-  uint8_t version;
+  uint8_t version;  // 2: + the generator key
   int32_t nx, ny, m, L0, L1;
   int64_t npairs;
+  uint8_t hasKey;
+  uint8_t key[32];  // tbt_set_cache_key of the context that wrote the file
 };
 }  // namespace
 
@@ -236,13 +238,15 @@ void saveSpectra(Ctx& c, const std::string& path) {
   TBT_USER_CHECK(static_cast<bool>(out), "cannot write spectra cache: " + path);
   SpecHeader h{};
   std::memcpy(h.magic, "TBTS1", 5);
-  h.version = 1;
+  h.version = 2;
   h.nx = c.nx;
   h.ny = c.ny;
   h.m = c.m;
   h.L0 = c.L0;
   h.L1 = c.L1;
   h.npairs = c.npairs;
+  h.hasKey = c.haveCacheKey ? 1 : 0;
+  std::memcpy(h.key, c.cacheKey, sizeof h.key);
   out.write(reinterpret_cast<const char*>(&h), sizeof h);
   out.write(reinterpret_cast<const char*>(c.genHost.data()), static_cast<std::streamsize>(mm * sizeof(double2)));
   out.write(reinterpret_cast<const char*>(host.data()), static_cast<std::streamsize>(host.size() * sizeof(double2)));
@@ -255,9 +259,14 @@ void loadSpectra(Ctx& c, const std::string& path) {
   TBT_USER_CHECK(static_cast<bool>(in), "cannot open spectra cache: " + path);
   SpecHeader h{};
   in.read(reinterpret_cast<char*>(&h), sizeof h);
-  TBT_USER_CHECK(in && std::string(h.magic, 5) == "TBTS1" && h.version == 1, "not a TBTS1 spectra cache: " + path);
+  TBT_USER_CHECK(in && std::string(h.magic, 5) == "TBTS1" && h.version == 2, "not a TBTS1 spectra cache: " + path);
   TBT_USER_CHECK(h.nx == c.nx && h.ny == c.ny && h.m == c.m && h.L0 == c.L0 && h.L1 == c.L1,
                  "spectra cache: dimensions / embedding do not match the context");
+  // A cache of another generator set with the same shape (another frequency
+  // of a sweep, another seed) would silently give a wrong operator.
+  if (c.haveCacheKey)
+    TBT_USER_CHECK(h.hasKey && std::memcmp(h.key, c.cacheKey, sizeof h.key) == 0,
+                   "spectra cache: generator key does not match the context (written for other generators)");
   const long long mm = static_cast<long long>(c.m) * c.m;
   c.genHost.resize(static_cast<size_t>(mm));
   in.read(reinterpret_cast<char*>(c.genHost.data()), static_cast<std::streamsize>(mm * sizeof(double2)));

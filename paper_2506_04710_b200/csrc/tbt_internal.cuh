@@ -174,6 +174,11 @@ struct Ctx {
   std::vector<double2> genHost;   // only the self block Z(0,0) (m*m, column-major)
   double2* dGen = nullptr;        // all canonical blocks on the device until tbt_precompute
   bool haveGenerators = false, havePrecompute = false;
+  // Identity of the generator set for TBTS1 spectrum caches (tbt_set_cache_key):
+  // written with the cache, and a load into a context that has a key
+  // requires the same key.
+  unsigned char cacheKey[32] = {};
+  bool haveCacheKey = false;
   long long npairs = 0;
   double2* dSpectra = nullptr;    // [npairs][m][m] row-major
   int* dPairF = nullptr;          // representative bin of pair p
@@ -276,7 +281,8 @@ void applyOperator(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
 // GMRES (gmres.cu): per-column state mirrored to the host.
 struct GmresState {
   double bnorm, beta, residual, beta0;
-  int iterations, ncount, stopInner, done, converged, cycleActive, histLen, pad;
+  int iterations, ncount, stopInner, done, converged, cycleActive, histLen;
+  int checks;  // true-residual applies (restart checks + the final one), cluster solve
 };
 void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres_opts& o, bool useAOnly,
                 std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs);

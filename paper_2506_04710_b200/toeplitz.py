@@ -138,7 +138,10 @@ class ToeplitzMatvec:
         loopback_group_id): every rank's calls must then be issued
         concurrently, one host thread per rank.
         spectra_cache: a TBTS1 file; loaded instead of K1 when it exists,
-        written after K1 otherwise (row f3)."""
+        written after K1 otherwise (row f3). The cache is keyed by a BLAKE2b
+        digest of rep.generators (tbt_set_cache_key): a file written for
+        other generators of the same shape is rejected (UserError). A rep
+        without generators (shape only) loads any cache of its shape."""
         self.rep = rep
         self._h = C.c_void_p()
         if embed not in ("pow2", "smooth"):
@@ -147,6 +150,10 @@ class ToeplitzMatvec:
         _check(lib().tbt_create(C.byref(desc), C.byref(self._h)))
         import os
         cached = spectra_cache is not None and os.path.exists(spectra_cache)
+        if spectra_cache is not None and rep.generators.size:
+            import hashlib
+            key = hashlib.blake2b(np.ascontiguousarray(rep.generators).view(np.uint8), digest_size=32).digest()
+            _check(lib().tbt_set_cache_key(self._h, key, len(key)))
         if not cached:
             gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
             _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))

@@ -247,6 +247,10 @@ def test_gpu_matches_reference(gpu, tmp_path, name):
     res = op.gmres(b, SolverOptions(tol=cfg.tol, maxIter=budget, restart=cfg.restart), raise_on_fail=False)
     assert res.iterations[0] == r["iterations"]
     assert res.matvecs == r["matvecs"]
+    # operator applications are counted by the solver, not inferred from the history
+    res0 = op.gmres(b, SolverOptions(tol=cfg.tol, maxIter=budget, restart=cfg.restart), raise_on_fail=False,
+                    hist_cap=0)
+    assert res0.matvecs == r["matvecs"] and res0.iterations == res.iterations
     assert rel(res.current[:, 0] if res.current.ndim == 2 else res.current, r["x"]) <= 1e-8
 
 

@@ -99,3 +99,7 @@ def test_gpu_spectra_cache_roundtrip(gpu, tmp_path):
     other = ToeplitzRep.synthetic(Config("sc", 5, 5, 16, 1, 4, 2, "normal", 20))
     with pytest.raises(UserError):
         ToeplitzMatvec(other, spectra_cache=cache)
+    # same shape, other generators (another sweep frequency / seed): rejected by the key
+    reseeded = ToeplitzRep.synthetic(Config("sc", 6, 5, 16, 1, 4, 9, "normal", 20))
+    with pytest.raises(UserError, match="generator key"):
+        ToeplitzMatvec(reseeded, spectra_cache=cache)
