@@ -147,6 +147,12 @@ long long tbt_size_m(const tbt_ctx* ctx);
  * (array_model.cpp:218-228); tbt_apply_a and use_a_only solves keep n. */
 tbt_status tbt_set_margin(tbt_ctx* ctx, const int* e, const double* bside, const double* brow,
                           const double* bcorner, const double* cmat);
+/* SemiSparse representations (the reference's aLevel1 + bFull + cFull,
+ * toeplitz.hpp:90-93): A as generators through tbt_set_generators (read
+ * out of aLevel1 by aEntry's SemiSparse rule, linsolve.cpp:220-224), B as
+ * one dense nM x nA and C as one dense nM x nM matrix, both column-major;
+ * B, B^T and C are applied as dense products (linsolve.cpp:294,318,338). */
+tbt_status tbt_set_margin_dense(tbt_ctx* ctx, const int* e, const double* b_full, const double* c);
 /* The margin blocks alone (ToeplitzMatvec::applyB / applyBT / applyC,
  * linsolve.hpp:66-68; linsolve.cpp:292-314, 316-334, 336-349):
  *   tbt_apply_b   yM = B xA      x: n   x nrhs, y: n_m x nrhs
@@ -177,18 +183,25 @@ tbt_status tbt_schur_solve(tbt_ctx* ctx, const double* b, double* x, int nrhs,
                            int where);
 
 /* Row f3: a reference ZTOE1 block cache (saveBlockCache,
- * proj/src/toeplitz.cpp:700-743; Sparse mode) straight into a precomputed
- * context: AGen -> generators, BSide/BRow/BCorner -> margin B, the C records
- * assembled into the margin block by partBlock's rules (:506-573).
+ * proj/src/toeplitz.cpp:700-743) straight into a precomputed context.
+ * Sparse mode: AGen -> generators, BSide/BRow/BCorner -> margin B, the C
+ * records assembled into the margin block by partBlock's rules (:506-573).
+ * SemiSparse mode: generators read out of ALevel1, BFullM / CFullM ->
+ * tbt_set_margin_dense. Full-mode caches are rejected (user error).
  * tbt_ztoe1_dims reads only the header (e: 9 ints). */
 tbt_status tbt_load_ztoe1(const char* path, int max_nrhs, int device,
                           int flags, tbt_ctx** ctx);
 tbt_status tbt_ztoe1_dims(const char* path, int* nx, int* ny, int* e);
-/* Host-only parse of a ZTOE1 cache into the tbt_set_generators /
+/* Host-only parse of a Sparse ZTOE1 cache into the tbt_set_generators /
  * tbt_set_margin layouts (any pointer may be NULL; sizes from
  * tbt_ztoe1_dims and tbtgen_margin_lengths). */
 tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside,
                           double* brow, double* bcorner, double* c);
+/* Storage mode byte of a ZTOE1 file (0 Full, 1 SemiSparse, 2 Sparse), and
+ * the host parse of a SemiSparse cache: generators (Sparse order, read out
+ * of aLevel1), bFull (nM x nA) and cFull (nM x nM), column-major. */
+tbt_status tbt_ztoe1_mode(const char* path, int* mode);
+tbt_status tbt_ztoe1_read_dense(const char* path, double* gen, double* b_full, double* c);
 /* Persisted bin-major half spectrum (+ the self block): tbt_load_spectra
  * replaces tbt_set_generators + tbt_precompute on a context of the same
  * nx, ny, m and embedding (K1 skipped across runs). tbt_set_cache_key

@@ -44,6 +44,7 @@ def lib() -> C.CDLL:
         L.orc_bins.argtypes = [C.c_void_p]
         L.orc_set_correction.argtypes = [C.c_void_p, C.c_int, dp, dp, dp]
         L.orc_set_margin.argtypes = [C.c_void_p, ip, dp, dp, dp, dp]
+        L.orc_set_margin_dense.argtypes = [C.c_void_p, ip, dp, dp]
         L.orc_size.restype = C.c_longlong
         L.orc_size.argtypes = [C.c_void_p]
         L.orc_schur.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -130,7 +131,15 @@ class Oracle:
             u = np.ascontiguousarray(u) if rank > 0 else np.zeros(1, np.complex128)
             v = np.ascontiguousarray(v) if rank > 0 else np.zeros(1, np.complex128)
             lib().orc_set_correction(self._h, rank, _p(d), _p(u), _p(v))
-        if margin is not None:
+        if margin is not None and hasattr(margin, "b_full"):  # DenseMargin (SemiSparse)
+            e = np.ascontiguousarray(margin.e, dtype=np.int32)
+            arrs = [np.ascontiguousarray(a, dtype=np.complex128) for a in (margin.b_full, margin.c)]
+            arrs = [a if a.size else np.zeros(1, np.complex128) for a in arrs]
+            if lib().orc_set_margin_dense(self._h, e.ctypes.data_as(ip), *[_p(a) for a in arrs]):
+                raise ValueError("orc_set_margin_dense failed")
+            self._margin_keep = arrs
+            self.n = int(lib().orc_size(self._h))
+        elif margin is not None:
             e = np.ascontiguousarray(margin.e, dtype=np.int32)
             arrs = [np.ascontiguousarray(a, dtype=np.complex128) for a in
                     (margin.bside, margin.brow, margin.bcorner, margin.c)]

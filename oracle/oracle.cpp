@@ -224,6 +224,9 @@ struct orc_op {
   int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long nM = 0;
   cvec bSideRaw, bRowRaw, bCornerRaw, cDense;  // tbt_gen.h layouts
+  // SemiSparse (linsolve.cpp:294, :318): B is one dense nM x nA matrix.
+  bool denseB = false;
+  cvec bDense;  // nM x nA column-major
   Toe1D bSide[2];
   std::vector<Toe1D> bRow[2];
   long sideStart[2] = {0, 0}, rowStart[2] = {0, 0}, cornerStart[4] = {0, 0, 0, 0};
@@ -234,6 +237,11 @@ struct orc_op {
   // applyB (linsolve.cpp:292-314): yM = B xA.
   void applyB(const cplx* xA, cplx* yM) const {
     for (long k = 0; k < nM; ++k) yM[k] = 0.0;
+    if (denseB) {  // rep.bFull * xA
+      for (long q = 0; q < nA; ++q)
+        for (long k = 0; k < nM; ++k) yM[k] += bDense[q * nM + k] * xA[q];
+      return;
+    }
     for (int r = 0; r < 2; ++r) bSide[r].apply(xA, yM + sideStart[r]);
     for (int r = 0; r < 2; ++r)
       for (int j = 0; j < ny && !bRow[r].empty(); ++j)
@@ -252,6 +260,14 @@ struct orc_op {
 
   // applyBT (linsolve.cpp:316-334): yA += B^T xM.
   void applyBT(const cplx* xM, cplx* yA) const {
+    if (denseB) {  // rep.bFull.transpose() * xM
+      for (long q = 0; q < nA; ++q) {
+        cplx acc{0.0, 0.0};
+        for (long k = 0; k < nM; ++k) acc += bDense[q * nM + k] * xM[k];
+        yA[q] += acc;
+      }
+      return;
+    }
     for (int r = 0; r < 2; ++r) bSide[r].applyT(xM + sideStart[r], yA);
     for (int r = 0; r < 2; ++r)
       for (int j = 0; j < ny && !bRow[r].empty(); ++j)
@@ -525,6 +541,21 @@ int orc_set_margin(orc_op* op, const int* e, const double* bside, const double* 
     }
     off += static_cast<long>(ny) * (2 * nx - 1) * bsz;
   }
+  op->haveMargin = true;
+  return 0;
+}
+
+// SemiSparse margin coupling: dense B (nM x nA) and C (nM x nM), column-major.
+int orc_set_margin_dense(orc_op* op, const int* e, const double* bfull, const double* c) {
+  if (!op || !e || e[4] != op->e5) return 1;
+  const int nx = op->nx, ny = op->ny;
+  for (int q = 0; q < 9; ++q) op->e[q] = e[q];
+  op->nM = static_cast<long>(ny) * (e[1] + e[7]) + static_cast<long>(nx) * (e[5] + e[3]) + e[2] + e[8] + e[0] + e[6];
+  const cplx* bf = reinterpret_cast<const cplx*>(bfull);
+  const cplx* cc = reinterpret_cast<const cplx*>(c);
+  op->bDense.assign(bf, bf + op->nM * op->nA);
+  op->cDense.assign(cc, cc + op->nM * op->nM);
+  op->denseB = true;
   op->haveMargin = true;
   return 0;
 }

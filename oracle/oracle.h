@@ -54,6 +54,9 @@ int orc_set_correction(orc_op* op, int rank, const double* d, const double* u,
  * gmres then act on nA + nM unknowns (orc_size). */
 int orc_set_margin(orc_op* op, const int* e, const double* bside, const double* brow, const double* bcorner,
                    const double* c);
+/* SemiSparse margin coupling (linsolve.cpp:294,318,338): dense B (nM x nA)
+ * and C (nM x nM), column-major. */
+int orc_set_margin_dense(orc_op* op, const int* e, const double* bfull, const double* c);
 long long orc_size(const orc_op* op);
 
 int orc_apply_a(const orc_op* op, const double* x, double* y);

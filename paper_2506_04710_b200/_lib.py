@@ -60,6 +60,9 @@ SIGNATURES = {
     "tbt_size_a": (C.c_longlong, [C.c_void_p]),
     "tbt_size_m": (C.c_longlong, [C.c_void_p]),
     "tbt_set_margin": (C.c_int, [C.c_void_p, ip, dp, dp, dp, dp]),
+    "tbt_set_margin_dense": (C.c_int, [C.c_void_p, ip, dp, dp]),
+    "tbt_ztoe1_mode": (C.c_int, [C.c_char_p, ip]),
+    "tbt_ztoe1_read_dense": (C.c_int, [C.c_char_p, dp, dp, dp]),
     "tbt_gmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),
                             C.POINTER(TbtGmresStats), C.c_int]),
     "tbt_schur_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(TbtGmresOpts),

@@ -402,7 +402,7 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dAntisym), static_cast<void*>(c.dTw0), static_cast<void*>(c.dTw1),
                   static_cast<void*>(c.dCorrD), static_cast<void*>(c.dCorrU), static_cast<void*>(c.dCorrV),
                   static_cast<void*>(c.dTermInfo), static_cast<void*>(c.dTargetList),
-                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dElemPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dYcorr), static_cast<void*>(c.dTermVec),
+                  static_cast<void*>(c.dTargetPtr), static_cast<void*>(c.dElemPtr), static_cast<void*>(c.dProj), static_cast<void*>(c.dYcorr), static_cast<void*>(c.dYcorrP), static_cast<void*>(c.dTermVec),
                   static_cast<void*>(c.dPairInfo), static_cast<void*>(c.dPairTargetPtr),
                   static_cast<void*>(c.dT),
                   static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
@@ -451,6 +451,29 @@ void* tbt_get_stream(tbt_ctx* h) { return h ? static_cast<void*>(h->c.stream) : 
 long long tbt_size_a(const tbt_ctx* h) { return h ? h->c.n : 0; }
 long long tbt_size_m(const tbt_ctx* h) { return h ? h->c.nM : 0; }
 
+namespace {
+// After a margin operator was (re)built: staging vectors that hold the
+// padded pseudo-elements, and the Jacobi diagonal.
+void marginResized(Ctx& c) {
+  const size_t len = static_cast<size_t>(c.ne + c.neM) * c.maxNrhs * c.m;
+  freePtr(c.dXin);
+  freePtr(c.dYout);
+  c.dXin = c.dYout = nullptr;
+  TBT_CUDA_CHECK(cudaMalloc(&c.dXin, len * sizeof(double2)));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dYout, len * sizeof(double2)));
+  if (poisonBuffers()) {
+    memsetSync(c.dXin, 0xFF, len * sizeof(double2), c.stream);
+    memsetSync(c.dYout, 0xFF, len * sizeof(double2), c.stream);
+  }
+  if (c.havePrecompute) refreshDiagonal(c, nullptr);
+}
+
+long long marginCount(const Ctx& c, const int* e) {
+  return static_cast<long long>(c.ny) * (e[1] + e[7]) + static_cast<long long>(c.nx) * (e[5] + e[3]) + e[2] + e[8] +
+         e[0] + e[6];
+}
+}  // namespace
+
 tbt_status tbt_set_margin(tbt_ctx* h, const int* e, const double* bside, const double* brow, const double* bcorner,
                           const double* cmat) {
   return guardedCtx(h, [&] {
@@ -460,29 +483,31 @@ tbt_status tbt_set_margin(tbt_ctx* h, const int* e, const double* bside, const d
     TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     c.dropGraph();
     freeGmresWorkspace(c);
-    const long long nM = static_cast<long long>(c.ny) * (e[1] + e[7]) + static_cast<long long>(c.nx) * (e[5] + e[3]) +
-                         e[2] + e[8] + e[0] + e[6];
+    const long long nM = marginCount(c, e);
     TBT_USER_CHECK(nM == 0 || cmat, "tbt_set_margin: C is required when there are margin unknowns");
     TBT_USER_CHECK((e[1] + e[7] == 0 || bside) && (e[5] + e[3] == 0 || brow) &&
                        (e[2] + e[8] + e[0] + e[6] == 0 || bcorner),
                    "tbt_set_margin: missing generator array");
     marginSet(c, e, reinterpret_cast<const double2*>(bside), reinterpret_cast<const double2*>(brow),
               reinterpret_cast<const double2*>(bcorner), reinterpret_cast<const double2*>(cmat));
-    // Staging vectors hold the padded pseudo-elements too.
-    const size_t len = static_cast<size_t>(c.ne + c.neM) * c.maxNrhs * c.m;
-    freePtr(c.dXin);
-    freePtr(c.dYout);
-    c.dXin = c.dYout = nullptr;
-    TBT_CUDA_CHECK(cudaMalloc(&c.dXin, len * sizeof(double2)));
-    TBT_CUDA_CHECK(cudaMalloc(&c.dYout, len * sizeof(double2)));
-    if (poisonBuffers()) {
-      memsetSync(c.dXin, 0xFF, len * sizeof(double2), c.stream);
-      memsetSync(c.dYout, 0xFF, len * sizeof(double2), c.stream);
-    }
-    if (c.havePrecompute) refreshDiagonal(c, nullptr);
+    marginResized(c);
   });
 }
 
+tbt_status tbt_set_margin_dense(tbt_ctx* h, const int* e, const double* bfull, const double* cmat) {
+  return guardedCtx(h, [&] {
+    TBT_USER_CHECK(h && e, "tbt_set_margin_dense: null argument");
+    Ctx& c = h->c;
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.dropGraph();
+    freeGmresWorkspace(c);
+    const long long nM = marginCount(c, e);
+    TBT_USER_CHECK(nM == 0 || (bfull && cmat), "tbt_set_margin_dense: B and C are required when there are margin unknowns");
+    marginSetDense(c, e, reinterpret_cast<const double2*>(bfull), reinterpret_cast<const double2*>(cmat));
+    marginResized(c);
+  });
+}
 tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblocks) {
   return guardedCtx(h, [&] {
     TBT_USER_CHECK(h && blocks, "tbt_set_generators: null argument");
@@ -523,10 +548,12 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     freePtr(c.dProj);
     freePtr(c.dElemPtr);
     freePtr(c.dYcorr);
+    freePtr(c.dYcorrP);
     freePtr(c.dTermVec);
     freePtr(c.dPairInfo);
     freePtr(c.dPairTargetPtr);
     c.dYcorr = nullptr;
+    c.dYcorrP = nullptr;
     c.dTermVec = nullptr;
     c.dPairInfo = c.dPairTargetPtr = nullptr;
     c.nCorrPairs = 0;
@@ -580,6 +607,8 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
                                               sizeof(double2)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dYcorr, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2)));
       memsetSync(c.dYcorr, 0, static_cast<size_t>(c.ne) * c.maxNrhs * c.m * sizeof(double2), c.stream);
+      TBT_CUDA_CHECK(cudaMalloc(&c.dYcorrP, static_cast<size_t>(c.ne) * c.m * sizeof(double2)));
+      memsetSync(c.dYcorrP, 0, static_cast<size_t>(c.ne) * c.m * sizeof(double2), c.stream);
       // (target, source) pairs: terms of one target grouped by source.
       std::vector<int> pinfo, pptr{0};
       for (int e : targets) {
@@ -913,7 +942,10 @@ tbt_status tbt_load_ztoe1(const char* path, int max_nrhs, int device, int flags,
       };
       chk(tbt_set_generators(h, reinterpret_cast<const double*>(z.gen.data()),
                              static_cast<long long>(z.gen.size() / (static_cast<size_t>(z.e[4]) * z.e[4]))));
-      if (z.nM > 0)
+      if (z.nM > 0 && z.mode == 1)
+        chk(tbt_set_margin_dense(h, z.e, reinterpret_cast<const double*>(z.bfull.data()),
+                                 reinterpret_cast<const double*>(z.c.data())));
+      else if (z.nM > 0)
         chk(tbt_set_margin(h, z.e, reinterpret_cast<const double*>(z.bside.data()),
                            reinterpret_cast<const double*>(z.brow.data()),
                            reinterpret_cast<const double*>(z.bcorner.data()),
@@ -953,6 +985,33 @@ tbt_status tbt_ztoe1_read(const char* path, double* gen, double* bside, double* 
     put(bside, z.bside);
     put(brow, z.brow);
     put(bcorner, z.bcorner);
+    put(cm, z.c);
+  });
+}
+
+tbt_status tbt_ztoe1_mode(const char* path, int* mode) {
+  return guarded([&] {
+    TBT_USER_CHECK(path && mode, "tbt_ztoe1_mode: null argument");
+    std::ifstream in(path, std::ios::binary);
+    TBT_USER_CHECK(static_cast<bool>(in), std::string("cannot open block cache: ") + path);
+    char head[6];
+    in.read(head, 6);
+    TBT_USER_CHECK(in && std::string(head, 5) == "ZTOE1", std::string("not a ZTOE1 block cache: ") + path);
+    *mode = static_cast<unsigned char>(head[5]);
+  });
+}
+
+tbt_status tbt_ztoe1_read_dense(const char* path, double* gen, double* bfull, double* cm) {
+  return guarded([&] {
+    TBT_USER_CHECK(path, "tbt_ztoe1_read_dense: null path");
+    Ztoe1Data z;
+    readZtoe1(path, z);
+    TBT_USER_CHECK(z.mode == 1, "tbt_ztoe1_read_dense: not a SemiSparse cache");
+    auto put = [](double* dst, const std::vector<double2>& src) {
+      if (dst && !src.empty()) std::memcpy(dst, src.data(), src.size() * sizeof(double2));
+    };
+    put(gen, z.gen);
+    put(bfull, z.bfull);
     put(cm, z.c);
   });
 }

@@ -8,9 +8,14 @@
 //    the device operator: AGen -> generators, BSide / BRow / BCorner -> the
 //    margin B generators, and the C records (CToe, CFullRect, C5x, C55) are
 //    assembled into the dense margin block with partBlock's rules
-//    (:506-573).
+//    (:506-573). SemiSparse-mode caches (ALevel1 / BFullM / CFullM) map too:
+//    the reference's SemiSparse ToeplitzMatvec runs the same FFT applyA on
+//    generators read out of aLevel1 (aEntry, linsolve.cpp:220-224) and
+//    applies B, B^T, C as dense products (:294, :318, :338). Full-mode
+//    caches hold only the dense matrix and are rejected.
 //  * A persisted bin-major spectrum ("TBTS1"), so repeated runs on the same
 //    operator (frequency sweeps re-solving many excitations) skip K1.
+#include <algorithm>
 #include <array>
 #include <complex>
 #include <cstdint>
@@ -65,10 +70,11 @@ void readZtoe1(const std::string& path, Ztoe1Data& out) {
     out.e[c] = readVal<int32_t>(in);
     TBT_USER_CHECK(out.e[c] >= 0, "block cache: negative edge count");
   }
-  // StorageMode {Full, SemiSparse, Sparse} (toeplitz.hpp:27): the device
-  // operator is built from the Sparse generators.
-  TBT_USER_CHECK(mode == 2, "block cache: only Sparse-mode caches map onto the Toeplitz operator (mode " +
-                                std::to_string(mode) + ")");
+  // StorageMode {Full, SemiSparse, Sparse} (toeplitz.hpp:27).
+  TBT_USER_CHECK(mode == 2 || mode == 1,
+                 "block cache: Full-mode caches hold no block-Toeplitz generators (mode " + std::to_string(mode) +
+                     "); use a Sparse or SemiSparse cache");
+  out.mode = mode;
   const int nx = out.nx, ny = out.ny, m = out.e[4];
   std::map<std::tuple<int, int, int, int>, Mat> rec;
   for (;;) {
@@ -81,6 +87,12 @@ void readZtoe1(const std::string& path, Ztoe1Data& out) {
     TBT_USER_CHECK(mt.rows >= 0 && mt.cols >= 0 && mt.rows * mt.cols < (int64_t{1} << 36),
                    "block cache: bad record dimensions");
     TBT_USER_CHECK(tag >= kAGen && tag <= kZFullM, "block cache: unknown record tag");
+    // Records the mode's layout has no slot for (initLayout, :181-238): the
+    // reference's reader fails on them (index out of range / dimensions).
+    const bool sparseTag = tag <= kC55;
+    TBT_USER_CHECK(tag != kZFullM && (mode == 2 ? sparseTag : !sparseTag),
+                   "block cache: record does not belong to a " + std::string(mode == 2 ? "Sparse" : "SemiSparse") +
+                       "-mode layout");
     mt.v.resize(static_cast<size_t>(mt.rows * mt.cols));
     in.read(reinterpret_cast<char*>(mt.v.data()), static_cast<std::streamsize>(mt.v.size() * sizeof(cplx)));
     TBT_USER_CHECK(static_cast<bool>(in), "block cache: truncated file");
@@ -104,12 +116,45 @@ void readZtoe1(const std::string& path, Ztoe1Data& out) {
   auto append = [](std::vector<double2>& dst, const Mat& mt) {
     for (const cplx& z : mt.v) dst.push_back(make_double2(z.real(), z.imag()));
   };
+  const long long nA = static_cast<long long>(nx) * ny * m;
+  out.nM = static_cast<long long>(ny) * (out.e[1] + out.e[7]) + static_cast<long long>(nx) * (out.e[5] + out.e[3]) +
+           out.e[2] + out.e[8] + out.e[0] + out.e[6];
+  if (mode == 1) {
+    // aLevel1[i] is the (nx m)^2 block row of element row i against element
+    // row 0 (initLayout :193-196); generator (i, j) is its block
+    // (max(j, 0), max(-j, 0)) — aEntry's SemiSparse branch (linsolve.cpp:
+    // 220-224) — taken in the canonical Sparse order.
+    const int64_t w = static_cast<int64_t>(nx) * m;
+    out.gen.clear();
+    for (int i = 0; i < ny; ++i) {
+      const Mat a1 = get(kALevel1, i, 0, 0, w, w);
+      for (int j = (i == 0 ? 0 : 1 - nx); j <= nx - 1; ++j) {
+        const int64_t r0 = static_cast<int64_t>(std::max(j, 0)) * m, c0 = static_cast<int64_t>(std::max(-j, 0)) * m;
+        for (int b = 0; b < m; ++b)
+          for (int a = 0; a < m; ++a) {
+            const cplx z = a1.at(r0 + a, c0 + b);
+            out.gen.push_back(make_double2(z.real(), z.imag()));
+          }
+      }
+    }
+    out.bside.clear();
+    out.brow.clear();
+    out.bcorner.clear();
+    out.bfull.clear();
+    out.c.clear();
+    if (out.nM > 0) {
+      const Mat bf = get(kBFullM, 0, 0, 0, out.nM, nA);
+      const Mat cf = get(kCFullM, 0, 0, 0, out.nM, out.nM);
+      for (const cplx& z : bf.v) out.bfull.push_back(make_double2(z.real(), z.imag()));
+      for (const cplx& z : cf.v) out.c.push_back(make_double2(z.real(), z.imag()));
+    }
+    return;
+  }
   // A generators in canonical order: aGen[0][j], then aGen[i][j - (1-nx)].
   out.gen.clear();
   for (int j = 0; j < nx; ++j) append(out.gen, get(kAGen, 0, j, 0, m, m));
   for (int i = 1; i < ny; ++i)
     for (int j = 0; j < 2 * nx - 1; ++j) append(out.gen, get(kAGen, i, j, 0, m, m));
-  const long long nA = static_cast<long long>(nx) * ny * m;
   out.bside.clear();
   out.brow.clear();
   out.bcorner.clear();

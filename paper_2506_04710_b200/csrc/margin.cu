@@ -333,6 +333,38 @@ __global__ void addBT(double2* __restrict__ y, const double2* __restrict__ zA, c
 }
 
 
+// Dense B (SemiSparse representations, linsolve.cpp:294 / :318).
+// ys[k][rhs] += sum_q B[k][q] xA[q][rhs]; CTA per (k, rhs), B row-major,
+// xA in the internal layout [e][rhs][b] (q = e*m + b).
+__global__ void __launch_bounds__(128) denseBProd(const double2* __restrict__ Bd, const double2* __restrict__ x,
+                                                  double2* __restrict__ ys, long long nA, int m, int K) {
+  __shared__ double2 red[4];
+  const long long k = blockIdx.x / K;
+  const int rhs = static_cast<int>(blockIdx.x % K);
+  const double2* row = Bd + k * nA;
+  double2 acc = make_double2(0.0, 0.0);
+  for (long long q = threadIdx.x; q < nA; q += blockDim.x)
+    cfma(acc, __ldg(row + q), x[((q / m) * K + rhs) * m + q % m]);
+  acc = ctaSum128(acc, red);
+  if (threadIdx.x == 0) ys[k * K + rhs] = cadd(ys[k * K + rhs], acc);
+}
+
+// yA[q][rhs] += sum_k B[k][q] xs[k][rhs] (B^T xM): thread per (q, rhs), the
+// reads of one B row are coalesced across q.
+__global__ void denseBTProd(const double2* __restrict__ Bd, const double2* __restrict__ xs, double2* __restrict__ y,
+                            long long nA, long long nM, int m, int K) {
+  const long long total = nA * K;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long q = o % nA;
+    const int rhs = static_cast<int>(o / nA);
+    double2 acc = make_double2(0.0, 0.0);
+    for (long long k = 0; k < nM; ++k) cfma(acc, __ldg(Bd + k * nA + q), xs[k * K + rhs]);
+    double2& dst = y[((q / m) * K + rhs) * m + q % m];
+    dst = cadd(dst, acc);
+  }
+}
+
 // ---- single-column fused margin products: every generator spectrum and
 // corner block is read ONCE per apply and feeds both B (row dots) and B^T
 // (column sums at the reversed bin / transposed block). EM bounds the rows
@@ -762,6 +794,42 @@ void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, 
   // The raw uploads and sequences are no longer needed once the spectra exist.
 }
 
+// SemiSparse margin coupling: dense B (nM x nA) and C (nM x nM), both
+// column-major as the reference stores bFull / cFull (toeplitz.hpp:90-93).
+void marginSetDense(Ctx& c, const int* e, const double2* Bm, const double2* Cm) {
+  TBT_USER_CHECK(e[4] == c.m, "tbt_set_margin_dense: e[4] must equal the element basis size m");
+  for (int q = 0; q < 9; ++q) TBT_USER_CHECK(e[q] >= 0, "tbt_set_margin_dense: negative edge count");
+  TBT_USER_CHECK(!c.dist, "tbt_set_margin_dense: not supported on a distributed context");
+  marginFree(c);
+  auto* M = new MarginOp;
+  c.margin = M;
+  M->stream = c.stream;
+  const int nx = c.nx, ny = c.ny, m = c.m, K = c.maxNrhs;
+  const long long nA = c.n;
+  for (int q = 0; q < 9; ++q) M->e[q] = e[q];
+  M->nM = static_cast<long long>(ny) * (e[1] + e[7]) + static_cast<long long>(nx) * (e[5] + e[3]) + e[2] + e[8] +
+          e[0] + e[6];
+  c.nM = M->nM;
+  c.neM = static_cast<int>((M->nM + m - 1) / m);
+  cudaStream_t s = c.stream;
+  if (M->nM > 0) {
+    double2* raw = M->alloc(static_cast<size_t>(M->nM) * nA);
+    uploadSync(raw, Bm, static_cast<size_t>(M->nM) * nA * sizeof(double2), s);
+    M->bDense = M->alloc(static_cast<size_t>(M->nM) * nA);
+    transposeCM<<<gridFor(M->nM * nA), 256, 0, s>>>(raw, M->bDense, M->nM, nA);
+    double2* rawC = M->alloc(static_cast<size_t>(M->nM) * M->nM);
+    uploadSync(rawC, Cm, static_cast<size_t>(M->nM) * M->nM * sizeof(double2), s);
+    M->C = M->alloc(static_cast<size_t>(M->nM) * M->nM);
+    transposeCM<<<gridFor(M->nM * M->nM), 256, 0, s>>>(rawC, M->C, M->nM, M->nM);
+    TBT_CUDA_CHECK(cudaGetLastError());
+    M->diag.resize(M->nM);
+    for (long long k = 0; k < M->nM; ++k) M->diag[k] = Cm[k * M->nM + k];
+  }
+  M->xs = M->alloc(static_cast<size_t>(M->nM) * K);
+  M->ys = M->alloc(static_cast<size_t>(M->nM) * K);
+  TBT_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
 void marginDiagonal(const Ctx& c, std::vector<double2>& d) {
   if (!c.margin) return;
   d.insert(d.end(), c.margin->diag.begin(), c.margin->diag.end());
@@ -909,10 +977,20 @@ void marginApply(Ctx& c, const double2* x, double2* y, int K) {
   MarginOp* M = c.margin;
   if (!M || M->nM == 0) return;
   static const bool noFuse = getenv("TBT_MARGIN_UNFUSED") != nullptr;
-  if (K == 1 && !noFuse && marginApplyFused1(c, x, y)) return;
   cudaStream_t s = c.stream;
   const int nx = c.nx, ny = c.ny, m = c.m, ne = c.ne;
   const long long nA = c.n, B = static_cast<long long>(K) * m;
+  if (M->bDense) {
+    // SemiSparse: yM = B xA + C xM, yA += B^T xM (linsolve.cpp:294,318,338).
+    marginGather<<<gridFor(M->nM * K), 256, 0, s>>>(x, M->xs, M->nM, ne, m, K);
+    cProd<<<static_cast<unsigned>(M->nM * K), 128, 0, s>>>(M->C, M->xs, M->ys, M->nM, K, 1);
+    denseBProd<<<static_cast<unsigned>(M->nM * K), 128, 0, s>>>(M->bDense, x, M->ys, nA, m, K);
+    denseBTProd<<<gridFor(nA * K), 256, 0, s>>>(M->bDense, M->xs, y, nA, M->nM, m, K);
+    marginScatter<<<gridFor(static_cast<long long>(c.neM) * K * m), 256, 0, s>>>(M->ys, y, M->nM, ne, c.neM, m, K);
+    TBT_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
+  if (K == 1 && !noFuse && marginApplyFused1(c, x, y)) return;
   marginGather<<<gridFor(M->nM * K), 256, 0, s>>>(x, M->xs, M->nM, ne, m, K);
   CornerArgs ca{};
   for (int q = 0; q < 4; ++q) {

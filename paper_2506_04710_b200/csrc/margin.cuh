@@ -20,6 +20,10 @@ struct MarginOp {
   double2* rawRow[2] = {nullptr, nullptr};
   double2* corner[4] = {nullptr, nullptr, nullptr, nullptr};  // [em][nA] row-major
   double2* C = nullptr;                    // [nM][nM] row-major
+  // SemiSparse representations (reference bFull, toeplitz.hpp:90-93): B is
+  // one dense nM x nA matrix applied by dense products (linsolve.cpp:294,
+  // 318); no Toeplitz / corner regions then.
+  double2* bDense = nullptr;               // [nM][nA] row-major
   double2* twY = nullptr;
   double2* twX = nullptr;
   std::vector<double2> diag;               // C's diagonal (host)

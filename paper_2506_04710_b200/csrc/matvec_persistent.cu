@@ -620,7 +620,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.nPairs = c.nCorrPairs;
   a.pInfo = c.dPairInfo;
   a.pTargetPtr = c.dPairTargetPtr;
-  a.ycorr = c.dYcorr;
+  a.ycorr = c.dYcorrP;
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
   a.prefetchAt = c.prefetchAt;
   a.l2Chunks = c.zeroCopyL2Bytes / (static_cast<long long>(smCount(c.device)) * C::CHUNK);
@@ -675,20 +675,11 @@ bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, 
   if (!persistentSupported(c) || c.dist) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
-    case 64064064: {
-      // Ring shape (rows per stage, stages); TBT_P64 selects a variant for tuning.
-      static const int v = [] {
-        const char* e = getenv("TBT_P64");
-        return e ? atoi(e) : 0;
-      }();
-      // Measured (C2 back-to-back): half blocks x 4 stages 37.6 us, whole
-      // blocks x 2 38.2, half x 5 40.6, quarter x 8 41.0, quarter x 11 47.1 —
-      // more bytes in flight per SM than 128 KB only slows the stream.
-      switch (v) {
-        case 1: return launchP<64, 16, 64, 2, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-        default: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-      }
-    }
+    // Ring shape: half blocks (32 rows) x 4 stages. Measured (C2 back to
+    // back): 37.6 us; whole blocks x 2 38.2, half x 5 40.6, quarter x 8
+    // 41.0, quarter x 11 47.1 — more bytes in flight per SM than 128 KB only
+    // slows the stream.
+    case 64064064: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);

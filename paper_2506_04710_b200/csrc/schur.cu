@@ -32,6 +32,7 @@ struct BTArgs {
   const double2* rawSide[2];
   const double2* rawRow[2];
   const double2* corner[4];
+  const double2* dense;  // SemiSparse: B row-major [nM][nA] (margin.cuh bDense)
 };
 
 // bt[q + k*nA] = (B^T)_{q,k} = B_{k,q}: the margin unknown k's coupling to
@@ -42,6 +43,10 @@ __global__ void buildBT(BTArgs a, double2* __restrict__ bt) {
   for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long q = o % a.nA, k = o / a.nA;
+    if (a.dense) {  // bt[k*nA + q] = B[k][q]: the same index as the row-major B
+      bt[o] = a.dense[o];
+      continue;
+    }
     double2 v = make_double2(0.0, 0.0);
     bool done = false;
     for (int r = 0; r < 2 && !done; ++r) {
@@ -234,6 +239,7 @@ void schurSolve(Ctx& c, const double2* b, double2* x, int p, const tbt_gmres_opt
     a.m = c.m;
     a.nA = nA;
     a.nM = nM;
+    a.dense = M->bDense;
     for (int r = 0; r < 2; ++r) {
       a.emSide[r] = M->emSide[r];
       a.emRow[r] = M->emRow[r];

@@ -200,7 +200,11 @@ struct Ctx {
   double2* dCorrV = nullptr;
   std::vector<double2> corrDHost;
   int nTerms = 0, nTargets = 0, maxTermsPerTarget = 0;
-  double2* dYcorr = nullptr;    // [ne][maxNrhs*m] correction vector
+  double2* dYcorr = nullptr;    // [ne][maxNrhs*m] correction vector (multi-launch paths)
+  // The persistent kernel's own [ne][m] correction vector: it writes only
+  // the target elements and reads every element, so the entries off the
+  // targets must stay zero whatever column count the other paths used.
+  double2* dYcorrP = nullptr;
   double2* dTermVec = nullptr;  // [nCorrPairs][m] per-(target,source) vectors (persistent apply)
   int nCorrPairs = 0;
   int* dPairInfo = nullptr;       // [pair][4] {target, source, code0, code1}
@@ -311,10 +315,12 @@ const NcclApi& nccl();
   } while (0)
 // io.cu (row f3): reference ZTOE1 block caches, persisted spectra.
 struct Ztoe1Data {
+  int mode = 2;  // StorageMode: 1 SemiSparse, 2 Sparse
   int nx = 0, ny = 0;
   int e[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long nM = 0;
   std::vector<double2> gen, bside, brow, bcorner, c;  // tbt_gen.h layouts; c: nM x nM column-major
+  std::vector<double2> bfull;                         // SemiSparse: nM x nA column-major
 };
 void readZtoe1(const std::string& path, Ztoe1Data& out);
 void saveSpectra(Ctx& c, const std::string& path);
@@ -335,6 +341,7 @@ void arrayFarfield(Ctx& c, const double2* const* tco, const double2* const* tcx,
 // margin.cu
 void marginSet(Ctx& c, const int* e, const double2* bside, const double2* brow, const double2* bcorner,
                const double2* C);
+void marginSetDense(Ctx& c, const int* e, const double2* B, const double2* C);  // SemiSparse: dense B, C
 void marginFree(Ctx& c);
 void marginApply(Ctx& c, const double2* x, double2* y, int nrhs);  // y's element part already holds A x
 void marginDiagonal(const Ctx& c, std::vector<double2>& d);          // appends C's diagonal

@@ -95,6 +95,33 @@ class Margin:
 
 
 @dataclass
+class DenseMargin:
+    """Margin coupling of a SemiSparse representation (ToeplitzRep::bFull,
+    cFull, toeplitz.hpp:90-93): B (nM x nA) and C (nM x nM) as dense
+    matrices, flattened column-major. e as in Margin."""
+    e: list
+    b_full: np.ndarray
+    c: np.ndarray
+
+    def size(self, nx: int, ny: int) -> int:
+        e = self.e
+        return ny * (e[1] + e[7]) + nx * (e[5] + e[3]) + e[2] + e[8] + e[0] + e[6]
+
+
+def generators_from_level1(nx: int, ny: int, m: int, a_level1) -> np.ndarray:
+    """Canonical Sparse-order generator blocks (gen.blocks_raw layout) read
+    out of SemiSparse first-level blocks: shift (i, j) is block
+    (max(j, 0), max(-j, 0)) of aLevel1[i] (aEntry, linsolve.cpp:220-224)."""
+    blocks = []
+    for i in range(ny):
+        a1 = np.asarray(a_level1[i])
+        for j in range(0 if i == 0 else 1 - nx, nx):
+            r0, c0 = max(j, 0) * m, max(-j, 0) * m
+            blocks.append(a1[r0:r0 + m, c0:c0 + m].T)  # raw [b][a] = column-major (a, b)
+    return np.ascontiguousarray(np.stack(blocks), dtype=np.complex128)
+
+
+@dataclass
 class SolverOptions:  # linsolve.hpp:47-53
     tol: float = 1e-8
     maxIter: int = 2000
@@ -165,7 +192,16 @@ class ToeplitzMatvec:
             _check(lib().tbt_set_correction(self._h, c.rank, d.ctypes.data_as(dp),
                                             u.ctypes.data_as(dp) if u is not None else None,
                                             v.ctypes.data_as(dp) if v is not None else None))
-        if rep.margin is not None:
+        if isinstance(rep.margin, DenseMargin):
+            mg = rep.margin
+            e = np.ascontiguousarray(mg.e, dtype=np.int32)
+            b = np.ascontiguousarray(mg.b_full, dtype=np.complex128)
+            cm = np.ascontiguousarray(mg.c, dtype=np.complex128)
+            b = b if b.size else np.zeros(1, np.complex128)
+            cm = cm if cm.size else np.zeros(1, np.complex128)
+            _check(lib().tbt_set_margin_dense(self._h, e.ctypes.data_as(C.POINTER(C.c_int)), b.ctypes.data_as(dp),
+                                              cm.ctypes.data_as(dp)))
+        elif rep.margin is not None:
             mg = rep.margin
             e = np.ascontiguousarray(mg.e, dtype=np.int32)
             arrs = [np.ascontiguousarray(a, dtype=np.complex128) for a in (mg.bside, mg.brow, mg.bcorner, mg.c)]
@@ -409,8 +445,9 @@ def array_farfield(op: "ToeplitzMatvec", tensors, e, dirs, dx: float, dy: float,
 
 
 def read_ztoe1(path: str) -> ToeplitzRep:
-    """A reference ZTOE1 block cache (Sparse mode) as a ToeplitzRep with its
-    margin data (host-side parse, csrc/io.cu; row f3)."""
+    """A reference ZTOE1 block cache as a ToeplitzRep with its margin data
+    (host-side parse, csrc/io.cu; row f3): Sparse caches give a Margin,
+    SemiSparse caches a DenseMargin (generators read out of aLevel1)."""
     from . import gen as _gen
     nx, ny = C.c_int(), C.c_int()
     e = (C.c_int * 9)()
@@ -419,6 +456,18 @@ def read_ztoe1(path: str) -> ToeplitzRep:
     m = ev[4]
     nb = _gen.num_blocks(nx, ny)
     g = np.empty((nb, m, m), np.complex128)
+    mode = C.c_int()
+    _check(lib().tbt_ztoe1_mode(path.encode(), C.byref(mode)))
+    if mode.value == 1:
+        dm = DenseMargin(ev, np.empty(0, np.complex128), np.empty(0, np.complex128))
+        nA = nx * ny * m
+        nM = dm.size(nx, ny)
+        bf = np.empty(max(nM * nA, 1), np.complex128)
+        cf = np.empty(max(nM * nM, 1), np.complex128)
+        _check(lib().tbt_ztoe1_read_dense(path.encode(), g.ctypes.data_as(dp), bf.ctypes.data_as(dp),
+                                          cf.ctypes.data_as(dp)))
+        margin = DenseMargin(ev, bf[:nM * nA], cf[:nM * nM]) if nM else None
+        return ToeplitzRep(nx, ny, m, g, None, margin)
     ea = np.ascontiguousarray(ev, dtype=np.int32)
     ns, nr, nc = C.c_longlong(), C.c_longlong(), C.c_longlong()
     nM = int(lib().tbtgen_margin_lengths(nx, ny, ea.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ns), C.byref(nr),

@@ -1,0 +1,86 @@
+"""Parity of the non-default product paths selected by environment knobs
+(read once per process, so tests/test_env_paths.py runs this script in a
+fresh subprocess per setting). Prints "OK <check>" per passed check and
+exits non-zero on the first mismatch.
+
+    TBT_APPLY=multi python tests/env_paths_check.py apply gmres
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+import oracle  # noqa: E402
+from paper_2506_04710_b200 import CONFIGS, Config, SolverOptions, ToeplitzMatvec, ToeplitzRep, gen  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def check_apply():
+    """C2 apply (host buffers) and a 3-column apply against the oracle."""
+    cfg = CONFIGS["C2"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep, max_nrhs=3)
+    o = oracle.Oracle.from_rep(rep)
+    X = gen.rhs_normal(cfg.n, 3, 4)
+    Y = op.apply(X)
+    for c in range(3):
+        ref = o.apply(np.ascontiguousarray(X[:, c]))
+        assert rel(Y[:, c], ref) < 1e-11, ("apply", c, rel(Y[:, c], ref))
+        assert rel(op.apply(np.ascontiguousarray(X[:, c])), ref) < 1e-11
+
+
+def check_gmres():
+    """C1 to convergence and C2 over a 60-iteration budget (one restart)."""
+    for name, budget in (("C1", 2000), ("C2", 60)):
+        cfg = CONFIGS[name]
+        rep = ToeplitzRep.synthetic(cfg)
+        op = ToeplitzMatvec(rep)
+        o = oracle.Oracle.from_rep(rep)
+        b = gen.rhs_normal(cfg.n, 1, cfg.seed)[:, 0]
+        g = op.gmres(b, SolverOptions(tol=cfg.tol, maxIter=budget, restart=cfg.restart), raise_on_fail=False)
+        r = o.gmres(b, tol=cfg.tol, max_iter=budget, restart=cfg.restart)
+        assert g.iterations == r["iterations"], (name, g.iterations, r["iterations"])
+        assert rel(g.current, r["x"]) < 1e-8, (name, rel(g.current, r["x"]))
+        h, hr = g.history[0], r["history"][0]
+        assert h.shape == hr.shape and np.all(np.abs(h[:, 1] - hr[:, 1]) <= 1e-8 * np.abs(hr[:, 1]) + 1e-14)
+
+
+def check_smooth():
+    """C3 grid (18 x 9, smooth 36 x 18 embedding), 8 columns."""
+    cfg = Config("s", 18, 9, 64, 8, 8, 3, "normal", 50)
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep, max_nrhs=8, embed="smooth")
+    o = oracle.Oracle.from_rep(rep)
+    X = gen.rhs_normal(cfg.n, 8, 6)
+    Y = op.apply(X)
+    for c in range(8):
+        ref = o.apply(np.ascontiguousarray(X[:, c]))
+        assert rel(Y[:, c], ref) < 1e-11, ("smooth", c)
+
+
+def check_margin():
+    """Margin coupling (B / B^T / C) single- and multi-column."""
+    nx, ny, m, e = 4, 3, 6, [2, 3, 1, 4, 6, 2, 3, 5, 1]
+    rep = ToeplitzRep.synthetic(Config("mg", nx, ny, m, 1, 2, 3, "normal", 20))
+    rep.margin = gen.margin(nx, ny, e, 103)
+    op = ToeplitzMatvec(rep, max_nrhs=2)
+    o = oracle.Oracle.from_rep(rep)
+    X = gen.rhs_normal(o.n, 2, 5)
+    Y = op.apply(X)
+    for c in range(2):
+        ref = o.apply(np.ascontiguousarray(X[:, c]))
+        assert rel(Y[:, c], ref) < 1e-11 and rel(op.apply(np.ascontiguousarray(X[:, c])), ref) < 1e-11
+
+
+CHECKS = {"apply": check_apply, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin}
+
+if __name__ == "__main__":
+    for name in sys.argv[1:]:
+        CHECKS[name]()
+        print("OK", name, flush=True)

@@ -1,0 +1,45 @@
+"""Every non-default product path behind an environment knob is held to the
+same oracle parity as the default (tests/env_paths_check.py in a fresh
+process per setting; the knobs are read once per process):
+
+  TBT_APPLY=multi     multi-launch apply instead of the persistent kernel
+  TBT_GMRES=cols      column-blocked Arnoldi for a single column
+  TBT_GMRES=unfused   separate apply / Arnoldi launches (no fused epilogue)
+  TBT_BINPROD=1       K3 v1 (no TMA ring), with TBT_APPLY=multi
+  TBT_PDL=0           device-resident applies replayed from a CUDA graph
+  TBT_FFT=passes      line-pass transforms instead of the cluster 2-D kernels
+  TBT_FFT2D=2,4       cluster 2-D transform with a forced cluster / batch split
+  TBT_E2E=staged      host applies through explicit copies, not zero-copy
+  TBT_MARGIN_UNFUSED=1  separate margin B / B^T kernels for one column
+"""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+SCRIPT = Path(__file__).resolve().parent / "env_paths_check.py"
+
+CASES = [
+    ({}, ["apply", "gmres", "smooth", "margin"]),  # the defaults, same checks (single after multi-column applies)
+    ({"TBT_APPLY": "multi"}, ["apply", "gmres"]),
+    ({"TBT_GMRES": "cols"}, ["gmres"]),
+    ({"TBT_GMRES": "unfused"}, ["gmres"]),
+    ({"TBT_BINPROD": "1", "TBT_APPLY": "multi"}, ["apply"]),
+    ({"TBT_PDL": "0"}, ["apply", "gmres"]),
+    ({"TBT_FFT": "passes"}, ["smooth", "apply"]),
+    ({"TBT_FFT2D": "2,4"}, ["smooth"]),
+    ({"TBT_E2E": "staged"}, ["apply"]),
+    ({"TBT_MARGIN_UNFUSED": "1"}, ["margin"]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env,checks", CASES, ids=[",".join(f"{k}={v}" for k, v in e.items()) or "defaults" for e, _ in CASES])
+def test_env_path_parity(gpu, env, checks):
+    full = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, str(SCRIPT), *checks], env=full, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr[-3000:]
+    for c in checks:
+        assert f"OK {c}" in r.stdout
