@@ -292,7 +292,7 @@ def large_configs(local, with_cpu):
     peak, _ = measured_hbm()
     dev = f"cuda:{local}"
     out = {}
-    for name, n_apply, budget in (("C4", 200, 40), ("C5", 30, 8)):
+    for name, n_apply, budget in (("C4", 200, 50), ("C5", 30, 50)):
         cfg = CONFIGS[name]
         t0 = time.perf_counter()
         rep = ToeplitzRep.synthetic(cfg)

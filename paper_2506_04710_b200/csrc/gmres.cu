@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kThreads) gmresInit(GmresArgs A) {
 }
 
 // r = b - A x, residual test, z = M r, beta, v0 = z / beta (linsolve.cpp:446-461).
+constexpr int kCyU = 4;  // element-wise passes: slots in flight per thread
+
 __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
   __shared__ double2 scratch[kWarps];
   extern __shared__ int sFlag[];  // [ncols]: 1 = this cycle runs
@@ -78,11 +80,23 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
     if (threadIdx.x == 0) sFlag[col] = run ? 1 : 0;
     double2 acc = make_double2(0.0, 0.0);
     if (run)
-      for (long long s = s0; s < slots; s += stride) {
-        const long long q = slotIndex(s, col, A.ncols, A.m);
-        const double2 r = csub(A.b[q], A.ax[q]);
-        A.w[q] = r;
-        acc.x += r.x * r.x + r.y * r.y;
+      for (long long sb = s0; sb < slots; sb += kCyU * stride) {  // kCyU slots in flight per thread
+        double2 bv[kCyU], av[kCyU];
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          const long long q = slotIndex(s < slots ? s : sb, col, A.ncols, A.m);
+          bv[u] = A.b[q];
+          av[u] = A.ax[q];
+        }
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          if (s >= slots) continue;
+          const double2 r = csub(bv[u], av[u]);
+          A.w[slotIndex(s, col, A.ncols, A.m)] = r;
+          acc.x += r.x * r.x + r.y * r.y;
+        }
       }
     blockPartial(acc, scratch, partSlot(A, 0, col));
     __syncthreads();
@@ -113,12 +127,23 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
     __syncthreads();
     double2 acc = make_double2(0.0, 0.0);
     if (sFlag[col])
-      for (long long s = s0; s < slots; s += stride) {
-        const long long q = slotIndex(s, col, A.ncols, A.m);
-        double2 z = A.w[q];
-        if (A.dinv) z = cmul(z, A.dinv[s]);
-        A.V[q] = z;
-        acc.x += z.x * z.x + z.y * z.y;
+      for (long long sb = s0; sb < slots; sb += kCyU * stride) {
+        double2 wv[kCyU], dv[kCyU];
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          const long long sc = s < slots ? s : sb;
+          wv[u] = A.w[slotIndex(sc, col, A.ncols, A.m)];
+          dv[u] = A.dinv ? A.dinv[sc] : make_double2(1.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          if (s >= slots) continue;
+          const double2 z = A.dinv ? cmul(wv[u], dv[u]) : wv[u];
+          A.V[slotIndex(s, col, A.ncols, A.m)] = z;
+          acc.x += z.x * z.x + z.y * z.y;
+        }
       }
     blockPartial(acc, scratch, partSlot(A, 1, col));
     __syncthreads();
@@ -146,10 +171,18 @@ __global__ void __launch_bounds__(kThreads) gmresCycleStart(GmresArgs A) {
       }
     }
     if (beta != 0.0)
-      for (long long s = s0; s < slots; s += stride) {
-        const long long q = slotIndex(s, col, A.ncols, A.m);
-        const double2 z = A.V[q];
-        A.V[q] = make_double2(z.x / beta, z.y / beta);
+      for (long long sb = s0; sb < slots; sb += kCyU * stride) {
+        double2 zv[kCyU];
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          zv[u] = A.V[slotIndex(s < slots ? s : sb, col, A.ncols, A.m)];
+        }
+#pragma unroll
+        for (int u = 0; u < kCyU; ++u) {
+          const long long s = sb + u * stride;
+          if (s < slots) A.V[slotIndex(s, col, A.ncols, A.m)] = make_double2(zv[u].x / beta, zv[u].y / beta);
+        }
       }
   }
 }
@@ -226,6 +259,238 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiLS(GmresArgs A, double2*
   __shared__ double2 hcol[RMAX + 2];
   __shared__ double2 sh[3 * RMAX + 4];
   arnoldiLS(A, S, dots, dotPart, shw, scratch, hcol, sh, A.bar);
+}
+
+// One Arnoldi step j, single column, low-synchronisation MGS, for vectors
+// whose per-CTA row chunk does not fit shared memory (C4: 3.5 k rows, C5:
+// 21 k rows per SM): the same recurrence as arnoldiLS (h = (I + L)^{-1} c,
+// c = V^H M w, S_j = V^H v_j; two passes over the basis, two grid barriers)
+// with the chunk streamed in sub-chunks of kBigSub rows:
+//   pass 1  per sub-chunk: M w and v_j staged in shared memory; every warp
+//           owns a contiguous slice of the sub-chunk and sweeps ALL basis
+//           vectors over it, four at a time (8 rows per lane per vector:
+//           32 loads in flight per lane), so all warps stream at any j;
+//           per-(warp, vector) partials accumulate in shared memory in
+//           sub-chunk order and are summed over the warps in warp order
+//   -- barrier --  every CTA reduces every dot, forward substitution
+//   pass 2  w' = M w - V h written to v_{j+1} unnormalised, ||w'||^2
+//           (4 rows per thread, 8 vectors unrolled: 32 loads in flight)
+//   -- barrier --  v_{j+1} /= ||w'|| (the chunk rereads its own rows, L2),
+//                  Givens (CTA 0)
+// All sums are fixed-order: bitwise reproducible.
+constexpr int kBigSub = 2048;
+constexpr int kBigRowsPerLane = kBigSub / (kWarps * 32);  // 8
+constexpr int kBigVec = 4;                                 // basis vectors per sweep step
+
+size_t lsBigSmem(int restart) {  // dynamic: ws, vj sub-chunks + packed L + per-warp partials
+  return sizeof(double2) * (2 * kBigSub + static_cast<size_t>(restart) * (restart + 1) / 2 +
+                            2 * static_cast<size_t>(kWarps) * (restart + 1));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gmresArnoldiLSBig(GmresArgs A, double2* S, double2* dotPart) {
+  extern __shared__ double2 dyn[];
+  const int lds = A.restart + 1;
+  double2* ws = dyn;                                          // [kBigSub]
+  double2* vj = dyn + kBigSub;                                // [kBigSub]
+  double2* sL = vj + kBigSub;                                 // packed rows of L: row i at i*(i-1)/2
+  double2* wpart = sL + static_cast<long long>(A.restart) * (A.restart + 1) / 2;  // [2][kWarps][lds]
+  __shared__ double2 cv[RMAX + 1];
+  __shared__ double2 scratch[kWarps];
+  __shared__ double2 hcol[RMAX + 2];
+  __shared__ double2 sh[3 * RMAX + 4];
+  const int run = A.st[0].cycleActive && !A.st[0].stopInner;
+  if (!run) return;  // uniform over the grid
+  const int j = A.j;
+  const long long n = static_cast<long long>(A.ne) * A.m;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * chunk;
+  const long long cnt = r0 >= n ? 0 : (n - r0 < chunk ? n - r0 : chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nw = kWarps;
+  const double2* Vj = A.V + static_cast<long long>(j) * n + r0;
+  const double2* w = A.w + r0;
+  const double2* dinv = A.dinv ? A.dinv + r0 : nullptr;
+  for (int t = threadIdx.x; t < 2 * nw * lds; t += blockDim.x) wpart[t] = make_double2(0.0, 0.0);
+  // ---- pass 1
+  for (long long s0 = 0; s0 < cnt; s0 += kBigSub) {
+    const int sc = static_cast<int>(cnt - s0 < kBigSub ? cnt - s0 : kBigSub);
+    __syncthreads();  // previous sub-chunk's readers are done
+    {  // stage M w and v_j: all of a thread's loads issued before its stores
+      constexpr int PT = kBigSub / kThreads;
+      double2 lw[PT], ld[PT], lv[PT];
+#pragma unroll
+      for (int u = 0; u < PT; ++u) {
+        const int r = threadIdx.x + u * kThreads;
+        const bool ok = r < sc;
+        lw[u] = ok ? w[s0 + r] : make_double2(0.0, 0.0);
+        ld[u] = ok && dinv ? dinv[s0 + r] : make_double2(1.0, 0.0);
+        lv[u] = ok ? Vj[s0 + r] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < PT; ++u) {
+        const int r = threadIdx.x + u * kThreads;
+        ws[r] = dinv ? cmul(lw[u], ld[u]) : lw[u];
+        vj[r] = lv[u];
+      }
+    }
+    __syncthreads();
+    const int rw = warp * 32 * kBigRowsPerLane;  // this warp's slice of the sub-chunk
+    for (int k0 = 0; k0 <= j; k0 += kBigVec) {
+      double2 c[kBigVec], q[kBigVec];
+      double2 v[kBigVec][kBigRowsPerLane];
+#pragma unroll
+      for (int t = 0; t < kBigVec; ++t) {
+        c[t] = q[t] = make_double2(0.0, 0.0);
+        const int k = k0 + t <= j ? k0 + t : j;
+        const double2* Vk = A.V + static_cast<long long>(k) * n + r0 + s0 + rw;
+#pragma unroll
+        for (int u = 0; u < kBigRowsPerLane; ++u) {
+          const int rr = rw + lane + 32 * u;
+          v[t][u] = (rr < sc && k0 + t <= j) ? Vk[lane + 32 * u] : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBigRowsPerLane; ++u) {
+        const int rr = rw + lane + 32 * u;
+        const double2 wv = rr < sc ? ws[rr] : make_double2(0.0, 0.0);
+        const double2 vv = rr < sc ? vj[rr] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < kBigVec; ++t) {
+          cfma_conj(c[t], v[t][u], wv);
+          cfma_conj(q[t], vv, v[t][u]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kBigVec; ++t) {
+        const double2 ct = warpSum(c[t]), qt = warpSum(q[t]);
+        if (lane == 0 && k0 + t <= j) {  // the warp owns its slots: sub-chunks in order
+          double2& pc = wpart[static_cast<long long>(warp) * lds + k0 + t];
+          double2& pq = wpart[static_cast<long long>(nw + warp) * lds + k0 + t];
+          pc = cadd(pc, ct);
+          pq = cadd(pq, qt);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+    double2 tc = wpart[k], tq = wpart[static_cast<long long>(nw) * lds + k];
+    for (int w2 = 1; w2 < nw; ++w2) {
+      tc = cadd(tc, wpart[static_cast<long long>(w2) * lds + k]);
+      tq = cadd(tq, wpart[static_cast<long long>(nw + w2) * lds + k]);
+    }
+    dotPart[static_cast<long long>(k) * gridDim.x + blockIdx.x] = tc;
+    if (k < j) dotPart[static_cast<long long>(lds + k) * gridDim.x + blockIdx.x] = tq;
+  }
+  gridBarrier(A.bar);
+  // ---- grid totals, reduced by every CTA in the same fixed order
+  double2* sLrow = sL;
+  {
+    const int ndots = 2 * j + 1;
+    const int grp = lane >> 4, gl = lane & 15;
+    const int G = static_cast<int>(gridDim.x);
+    for (int d0 = warp * 2; d0 < ndots; d0 += nw * 2) {
+      const int d = d0 + grp;
+      double2 t = make_double2(0.0, 0.0);
+      if (d < ndots) {
+        const double2* pp = dotPart + static_cast<long long>(d <= j ? d : lds + (d - j - 1)) * G;
+        double2 v[10];
+        for (int k0 = gl; k0 < G; k0 += 160) {
+#pragma unroll
+          for (int q = 0; q < 10; ++q) {
+            const int k = k0 + 16 * q;
+            v[q] = k < G ? __ldcg(pp + k) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int q = 0; q < 10; ++q) t = cadd(t, v[q]);
+        }
+      }
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) {
+        t.x += __shfl_xor_sync(0xffffffffu, t.x, off);
+        t.y += __shfl_xor_sync(0xffffffffu, t.y, off);
+      }
+      if (gl == 0 && d < ndots) {
+        if (d <= j) {
+          cv[d] = t;
+        } else {
+          sLrow[j * (j - 1) / 2 + (d - j - 1)] = t;
+          if (blockIdx.x == 0) S[static_cast<long long>(j) * lds + (d - j - 1)] = t;
+        }
+      }
+    }
+  }
+  for (int i = 1 + warp; i < j; i += nw)
+    for (int k = lane; k < i; k += 32) sLrow[i * (i - 1) / 2 + k] = __ldcg(S + static_cast<long long>(i) * lds + k);
+  __syncthreads();
+  if (warp == 0) {
+    if (A.restart < 64)
+      forwardSubstWarp<2>(cv, sLrow, j, lane);
+    else
+      forwardSubstWarp<(RMAX + 31) / 32 + 1>(cv, sLrow, j, lane);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = cv[i];
+  // ---- pass 2: w' = M w - V h -> v_{j+1} (unnormalised), ||w'||^2; four
+  // rows per thread, the update order over k unchanged per row.
+  double2* vout = A.V + static_cast<long long>(j + 1) * n + r0;
+  double2 acc = make_double2(0.0, 0.0);
+  const int bd = static_cast<int>(blockDim.x);
+  constexpr int RT = 4;
+  for (long long ra = threadIdx.x; ra < cnt; ra += RT * bd) {
+    double2 wr[RT];
+    long long rs[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const long long r = ra + t * bd;
+      rs[t] = r < cnt ? r : ra;
+      wr[t] = w[rs[t]];
+      if (dinv) wr[t] = cmul(wr[t], dinv[rs[t]]);
+    }
+    int k = 0;
+    for (; k + 8 <= j + 1; k += 8) {
+      double2 vv[8][RT];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) vv[u][t] = A.V[static_cast<long long>(k + u) * n + r0 + rs[t]];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) wr[t] = csub(wr[t], cmul(cv[k + u], vv[u][t]));
+    }
+    for (; k <= j; ++k)
+#pragma unroll
+      for (int t = 0; t < RT; ++t) wr[t] = csub(wr[t], cmul(cv[k], A.V[static_cast<long long>(k) * n + r0 + rs[t]]));
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      if (ra + t * bd < cnt) {
+        vout[ra + t * bd] = wr[t];
+        acc.x += wr[t].x * wr[t].x + wr[t].y * wr[t].y;
+      }
+  }
+  blockPartial(acc, scratch, partSlot(A, 0, 0));
+  if (blockIdx.x == 0) givensStage(A, 0, j, hcol, sh);  // made visible by the barrier
+  gridBarrier(A.bar);
+  const double hn = sqrt(warpTotal(partSlot(A, 0, 0)).x);
+  if (hn > 0.0) {
+    constexpr int PT = 8;  // loads in flight per thread
+    for (long long rb = threadIdx.x; rb < cnt; rb += PT * static_cast<long long>(blockDim.x)) {
+      double2 v[PT];
+#pragma unroll
+      for (int u = 0; u < PT; ++u) {
+        const long long r = rb + u * static_cast<long long>(blockDim.x);
+        v[u] = r < cnt ? __ldcg(vout + r) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < PT; ++u) {
+        const long long r = rb + u * static_cast<long long>(blockDim.x);
+        if (r < cnt) vout[r] = make_double2(v[u].x / hn, v[u].y / hn);
+      }
+    }
+  }
+  if (blockIdx.x == 0) givensFinish(A, 0, j, hn, sh);
 }
 
 // One Arnoldi step j for many columns: one CTA per column runs the
@@ -892,6 +1157,46 @@ __global__ void __launch_bounds__(kThreads) gmresUpdate(GmresArgs A) {
   const long long slots = static_cast<long long>(A.ne) * A.m;
   const long long nall = slots * A.ncols;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  if (A.ncols == 1) {
+    // One column: y in shared memory, four slots per thread with eight basis
+    // loads each in flight (per slot the order over i is unchanged).
+    if (!A.st[0].cycleActive) return;
+    const int nc = A.st[0].ncount;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) shH[i] = __ldcg(A.ycoef + i);
+    __syncthreads();
+    constexpr int QT = 4;  // slots per thread per trip: 32 basis loads in flight
+    for (long long qa = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; qa < nall;
+         qa += QT * stride) {
+      long long qs[QT];
+      double2 xv[QT];
+#pragma unroll
+      for (int t = 0; t < QT; ++t) {
+        const long long q = qa + t * stride;
+        qs[t] = q < nall ? q : qa;
+        xv[t] = A.x[qs[t]];
+      }
+      int i = 0;
+      for (; i + 8 <= nc; i += 8) {
+        double2 v[8][QT];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int t = 0; t < QT; ++t) v[u][t] = A.V[static_cast<long long>(i + u) * nall + qs[t]];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int t = 0; t < QT; ++t) xv[t] = cadd(xv[t], cmul(shH[i + u], v[u][t]));
+      }
+      for (; i < nc; ++i)
+#pragma unroll
+        for (int t = 0; t < QT; ++t) xv[t] = cadd(xv[t], cmul(shH[i], A.V[static_cast<long long>(i) * nall + qs[t]]));
+#pragma unroll
+      for (int t = 0; t < QT; ++t)
+        if (qa + t * stride < nall) A.x[qa + t * stride] = xv[t];
+    }
+    return;
+  }
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < nall; q += stride) {
     const int col = static_cast<int>((q / A.m) % A.ncols);
     if (!A.st[col].cycleActive) continue;
@@ -958,12 +1263,15 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
   // from C4 up the column-blocked kernels are faster (measured: C4 0.553 vs
   // 0.573 ms per iteration, C5 4.6 vs 5.2).
   const long long lsChunk = (nloc + grid - 1) / grid;
-  const bool colsLS =
-      c.dist || withMargin || (o.orthog == 1 && c.m <= 256 && (ncols > 1 || lsChunk > 2048 || c.forceCols));
+  // One column, large vectors (row chunk beyond shared memory, C4 / C5):
+  // the streamed low-sync step, two launches per iteration (apply + LS).
+  const bool bigLS = !c.dist && !withMargin && o.orthog == 1 && ncols == 1 && lsChunk > 2048 && !c.forceCols;
+  const bool colsLS = !bigLS && (c.dist || withMargin ||
+                                 (o.orthog == 1 && c.m <= 256 && (ncols > 1 || lsChunk > 2048 || c.forceCols)));
   TBT_USER_CHECK(!withMargin || c.m <= 256, "tbt_gmres: margin solves support m <= 256");
   TBT_USER_CHECK(!c.dist || c.m <= 256, "tbt_gmres: distributed solve supports m <= 256");
   const bool fast = !colsLS && ncols == 1 && nloc <= static_cast<long long>(grid) * kThreads * FAST_K;
-  const bool lowSync = !colsLS && o.orthog == 1 && ncols == 1 && lsChunk <= 4096;
+  const bool lowSync = !colsLS && !bigLS && o.orthog == 1 && ncols == 1 && lsChunk <= 2048;
   const int colsKpl = c.m <= 32 ? 1 : c.m <= 64 ? 2 : c.m <= 128 ? 4 : 8;
   const size_t colsSolveSmem = lsColsSolveSmem(R);
   const size_t lsSmem = static_cast<size_t>(arnoldiLSSmem(lsChunk, R)) * sizeof(double2);
@@ -1038,6 +1346,9 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     if (colsLS && colsSolveSmem > 48 * 1024)
       TBT_CUDA_CHECK(cudaFuncSetAttribute(lsColsSolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(colsSolveSmem)));
+    if (bigLS)
+      TBT_CUDA_CHECK(cudaFuncSetAttribute(gmresArnoldiLSBig, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(lsBigSmem(R))));
     if (lowSync) {
       TBT_CUDA_CHECK(cudaFuncSetAttribute(gmresArnoldiLS, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(lsSmem)));
@@ -1081,7 +1392,11 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     };
     auto arnoldi = [&](int j) {
       A.j = j;
-      if (lowSync) {
+      if (bigLS) {
+        void* params[] = {&A, &lsS, &lsPart};
+        TBT_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gmresArnoldiLSBig), dim3(grid),
+                                                   dim3(kThreads), params, lsBigSmem(R), s));
+      } else if (lowSync) {
         void* params[] = {&A, &lsS, &lsDots, &lsPart};
         TBT_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gmresArnoldiLS), dim3(grid),
                                                    dim3(kThreads), params, lsSmem, s));
@@ -1116,7 +1431,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     keyA.b = nullptr;
     keyA.x = nullptr;
     keyA.j = 0;
-    const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0);
+    const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0) | (bigLS ? 16 : 0);
     if (useGraph && (!W.inner || std::memcmp(&keyA, &W.graphKey, sizeof(GmresArgs)) != 0 || W.graphFlags != flags)) {
       if (W.inner) cudaGraphExecDestroy(W.inner);
       W.inner = nullptr;
@@ -1151,7 +1466,10 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
         else
           coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
         if (useGraph) {
-          TBT_CUDA_CHECK(cudaGraphLaunch(inner, s));
+          // The cycle start may have ended the solve (budget or tolerance
+          // reached): then the 'restart' no-op nodes are not worth a launch.
+          pull();
+          if (st[0].cycleActive && !st[0].stopInner) TBT_CUDA_CHECK(cudaGraphLaunch(inner, s));
         } else {
           pull();
           bool anyRun = false;

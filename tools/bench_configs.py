@@ -6,8 +6,9 @@ budget (C1 to convergence), and the oracle's CPU time on a bounded sample.
     python tools/bench_configs.py [--configs C1,C2,C3,C4,C5] [--out file.json]
 
 Rooflines: single-RHS configs are HBM-bound; the bytes are what one apply
-must move (half spectrum once, x/xhat/yhat/y and the transform
-intermediates, as in bench.py) against MEASURED_PEAKS.json hbm_gbs. C3's
+must move (half spectrum once, xhat / yhat, x / y, as in bench.py) against
+MEASURED_PEAKS.json hbm_gbs. G48 / G40 are shapes outside the persistent
+kernel's instantiations (the multi-launch apply.cu chain). C3's
 162-column apply is FP64-bound: 8 m^2 nrhs bins flops against the DMMA peak
 measured by tools/fp64test.cu (37.1 TF/s)."""
 import argparse
@@ -23,7 +24,14 @@ sys.path.insert(0, str(REPO))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2506_04710_b200 import CONFIGS, SolverOptions, ToeplitzMatvec, ToeplitzRep, gen, rhs_for  # noqa: E402
+from paper_2506_04710_b200 import CONFIGS, Config, SolverOptions, ToeplitzMatvec, ToeplitzRep, gen, rhs_for  # noqa: E402
+
+# Shapes outside the persistent kernel's instantiations (matvec_persistent.cu):
+# the multi-launch apply.cu chain, measured on the same byte count.
+EXTRA = {
+    "G48": Config("G48", 48, 48, 96, 1, 8, 5, "normal", 50),   # 128x128 bins, m = 96
+    "G40": Config("G40", 40, 24, 64, 1, 8, 6, "normal", 50),   # 64x128 bins, m = 64
+}
 from paper_2506_04710_b200._lib import TBT_DEVICE  # noqa: E402
 
 DMMA_TFLOPS = 37.1  # tools/fp64test.cu, mma.sync.m8n8k4.f64 on this B200 pool
@@ -47,12 +55,13 @@ def timed(fn, n, stream):
 
 
 def apply_bytes(cfg, info):
+    """Algorithmic bytes of one apply (SURVEY.md 8(d) with the stored half
+    spectrum): spectrum once, xhat read + yhat written, x read + y written.
+    Transform intermediates are not counted (bench.py uses the same)."""
     c16 = 16
     spectrum = info.pairs * cfg.m * cfg.m * c16
     vec = 2 * info.bins * cfg.m * c16 * cfg.nrhs
-    tbuf = cfg.ny * info.L0 * cfg.m * c16 * cfg.nrhs
-    fft = 2 * cfg.n * c16 * cfg.nrhs + 4 * tbuf + 2 * info.bins * cfg.m * c16 * cfg.nrhs
-    return spectrum + vec + fft
+    return spectrum + vec + 2 * cfg.n * c16 * cfg.nrhs
 
 
 def cpu_apply(rep, cfg, seconds, cols=1):
@@ -74,7 +83,7 @@ def cpu_apply(rep, cfg, seconds, cols=1):
 
 
 def run(name, args, out):
-    cfg = CONFIGS[name]
+    cfg = CONFIGS[name] if name in CONFIGS else EXTRA[name]
     res = {"config": name, "shape": f"{cfg.nx}x{cfg.ny}, m={cfg.m}, nrhs={cfg.nrhs}"}
     rep = ToeplitzRep.synthetic(cfg)
     stream = torch.cuda.Stream()
@@ -106,7 +115,7 @@ def run(name, args, out):
         B = np.asarray(rhs_for(cfg)).reshape(cfg.n, -1)
         bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
         xd = torch.empty_like(bd)
-        budget = {"C1": cfg.max_iter, "C2": 200, "C3": 50, "C4": 100, "C5": 10}[name]
+        budget = {"C1": cfg.max_iter, "C2": 200, "C3": 50, "C4": 100, "C5": 10}.get(name, 50)
         opt = SolverOptions(tol=cfg.tol, maxIter=budget, restart=cfg.restart)
         for rep_i in range(2):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -123,7 +132,9 @@ def run(name, args, out):
         res[embed] = r
         del op
         torch.cuda.empty_cache()
-    if name != "C5" and not args.no_cpu:
+    if name in EXTRA:
+        pass
+    elif name != "C5" and not args.no_cpu:
         cols = min(os.cpu_count() or 1, cfg.nrhs)
         o, cpu = cpu_apply(rep, cfg, seconds={"C1": 3, "C2": 8, "C3": 10, "C4": 10}[name], cols=cols)
         if name in ("C1", "C2"):
