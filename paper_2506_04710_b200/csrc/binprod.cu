@@ -324,6 +324,171 @@ void launchRing(Ctx& c) {
                                                                           c.dXhat, c.dYhat);
 }
 
+// ---------------------------------------------------------------------------
+// K3 for one right-hand side and ANY m up to 256 (the tuned ring kernels
+// above are instantiated for m = 64, 128, 192): the same warp-specialised
+// cp.async.bulk ring and register tiling with m a run-time value. Chunks
+// are 16 contiguous rows of the block (the last one may be partial); warp w
+// owns rows w and w + 8 of a chunk, lane l columns l + 32 j (j < CPT, CPT =
+// ceil(m / 32) a template parameter; columns >= m are predicated off). A
+// warp loads its operands into registers and releases the slot before
+// computing; column products accumulate in registers across the pair's
+// chunks and meet across the warps in shared memory once per pair.
+constexpr uint32_t kAnyStages = 6;
+constexpr int kAnyRows = 16;
+
+template <int CPT>
+__global__ void __launch_bounds__(288, 1)
+binprodRingAny(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
+               long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int m,
+               uint32_t stageBytes, int nst) {
+  constexpr int NT = 256, RPT = kAnyRows / (NT / 32);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stageBytes);
+  uint64_t* empty = full + nst;
+  double2* red = reinterpret_cast<double2*>(smem + nst * stageBytes + 2 * nst * 8);  // [2][8][m]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbarInit(full + s, 1);
+      mbarInit(empty + s, NT / 32);
+    }
+    fenceBarrierInit();
+  }
+  __syncthreads();
+  if (blockIdx.x >= npairs) return;
+  const int nch = (m + kAnyRows - 1) / kAnyRows;
+  const long long mine = (npairs - 1 - blockIdx.x) / gridDim.x + 1;
+  const long long total = mine * nch;
+  const long long mm = static_cast<long long>(m) * m;
+  const uint32_t xfOff = static_cast<uint32_t>(kAnyRows) * m * 16;
+
+  if (warp == NT / 32) {  // producer
+    if (lane == 0) {
+      const uint64_t polS = policyEvictFirst();
+      const uint64_t polX = policyEvictLast();
+      for (long long it = 0; it < total; ++it) {
+        const int s = static_cast<int>(it % nst);
+        const uint32_t ph = static_cast<uint32_t>((it / nst) & 1);
+        const long long p = blockIdx.x + (it / nch) * gridDim.x;
+        const int ch = static_cast<int>(it % nch);
+        const int rr = min(kAnyRows, m - ch * kAnyRows);
+        const long long f = pairF[p], g = pairG[p];
+        const uint32_t chunk = static_cast<uint32_t>(rr) * m * 16, xf = static_cast<uint32_t>(m) * 16;
+        mbarWait(empty + s, ph ^ 1u);
+        unsigned char* st = smem + s * stageBytes;
+        mbarArriveExpectTx(full + s, chunk + xf + static_cast<uint32_t>(rr) * 16);
+        bulkG2S(st, S + p * mm + static_cast<long long>(ch) * kAnyRows * m, chunk, full + s, polS);
+        bulkG2S(st + xfOff, xhat + f * m, xf, full + s, polX);
+        bulkG2S(st + xfOff + xf, xhat + g * m + static_cast<long long>(ch) * kAnyRows, static_cast<uint32_t>(rr) * 16,
+                full + s, polX);
+      }
+    }
+    return;
+  }
+
+  double2 yga[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) yga[j] = make_double2(0.0, 0.0);
+  for (long long it = 0; it < total; ++it) {
+    const int s = static_cast<int>(it % nst);
+    const uint32_t ph = static_cast<uint32_t>((it / nst) & 1);
+    const long long pi = it / nch;
+    const long long p = blockIdx.x + pi * gridDim.x;
+    const int ch = static_cast<int>(it % nch);
+    const int rr = min(kAnyRows, m - ch * kAnyRows);
+    mbarWait(full + s, ph);
+    const double2* A = reinterpret_cast<const double2*>(smem + s * stageBytes);
+    const double2* xf = A + kAnyRows * m;
+    const double2* xg = xf + m;
+    double2 a[RPT][CPT], xfr[CPT], xgv[RPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = lane + 32 * j;
+      xfr[j] = c < m ? xf[c] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = warp + (NT / 32) * i;
+      const bool rok = r < rr;
+      xgv[i] = rok ? xg[r] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int c = lane + 32 * j;
+        a[i][j] = rok && c < m ? A[r * m + c] : make_double2(0.0, 0.0);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbarArrive(empty + s);  // slot free: operands are in registers
+
+    const long long f = pairF[p], g = pairG[p];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = warp + (NT / 32) * i;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) cfma(acc, a[i][j], xfr[j]);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) acc = cadd(acc, shflXor(acc, off));
+      if (lane == 0 && r < rr) yhat[f * m + static_cast<long long>(ch) * kAnyRows + r] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) cfma(yga[j], a[i][j], xgv[i]);
+
+    if (ch == nch - 1) {
+      double2* rb = red + (pi & 1) * (NT / 32) * m;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int c = lane + 32 * j;
+        if (c < m) rb[warp * m + c] = yga[j];
+        yga[j] = make_double2(0.0, 0.0);
+      }
+      namedBarrier(1, NT);
+      if (f != g)
+        for (int q = threadIdx.x; q < m; q += NT) {
+          double2 acc = rb[q];
+#pragma unroll
+          for (int w = 1; w < NT / 32; ++w) acc = cadd(acc, rb[w * m + q]);
+          yhat[g * m + q] = acc;
+        }
+    }
+  }
+}
+
+template <int CPT>
+void launchRingAny(Ctx& c) {
+  const int m = c.m;
+  const uint32_t stage =
+      static_cast<uint32_t>((static_cast<size_t>(kAnyRows) * m * 16 + m * 16 + kAnyRows * 16 + 127) / 128 * 128);
+  // ~150 KB of chunks in flight per SM (2..6 stages; C2 / C4 measured best
+  // around 128 KB for this stream).
+  const int nst = static_cast<int>(std::max<uint32_t>(2, std::min<uint32_t>(kAnyStages, 150u * 1024 / stage)));
+  const size_t smem = nst * static_cast<size_t>(stage) + 2 * nst * 8 + 2 * 8 * static_cast<size_t>(m) * sizeof(double2);
+  static std::atomic<unsigned long long> attrSet{0};
+  oncePerDevice(attrSet, [] {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodRingAny<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024));
+  });
+  const int grid = static_cast<int>(std::min<long long>(c.npairs, smCount(c.device)));
+  binprodRingAny<CPT><<<grid, 288, smem, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, m,
+                                                     stage, nst);
+}
+
+void launchStream(Ctx& c) {
+  switch ((c.m + 31) / 32) {
+    case 1: launchRingAny<1>(c); break;
+    case 2: launchRingAny<2>(c); break;
+    case 3: launchRingAny<3>(c); break;
+    case 4: launchRingAny<4>(c); break;
+    case 5: launchRingAny<5>(c); break;
+    case 6: launchRingAny<6>(c); break;
+    case 7: launchRingAny<7>(c); break;
+    default: launchRingAny<8>(c); break;
+  }
+}
+
 template <int M, int TC, int RCH>
 void launchTile(Ctx& c, int nrhs) {
   const int sms = smCount(c.device);
@@ -351,6 +516,11 @@ void launchBinProduct(Ctx& c, int nrhs) {
       case 12: launchRing<128, 32, 16, 4>(c); break;
       case 13: launchRing<192, 32, 16, 3>(c); break;
     }
+    TBT_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
+  if (nrhs == 1 && binprodVariant(c.m) == 0 && c.m <= 256) {
+    launchStream(c);
     TBT_CUDA_CHECK(cudaGetLastError());
     return;
   }

@@ -141,6 +141,35 @@ __device__ __forceinline__ void bar6(unsigned long long* c) {
   __syncthreads();
 }
 
+// V8: cluster-assisted. The cluster's CTAs meet at the hardware cluster
+// barrier (release / acquire at cluster scope), its rank-0 CTA alone
+// arrives on the global counter (grid / cluster-size arrivals instead of
+// one per CTA) and polls, then the cluster meets again.
+__device__ __forceinline__ void clusterSync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned clusterRank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned clusterSize() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void bar8(unsigned long long* c) {
+  clusterSync();
+  if (clusterRank() == 0 && threadIdx.x == 0) {
+    const unsigned long long g = gridDim.x / clusterSize();
+    const unsigned long long old = atomAddRelease(c, 1ULL);
+    const unsigned long long target = (old / g + 1) * g;
+    while (ldAcquire(c) < target) {
+    }
+  }
+  clusterSync();
+}
+
 __global__ void __launch_bounds__(352, 1) kern(int variant, int iters, int stores, unsigned long long* c,
                                                unsigned long long* flags, unsigned long long* rel, double* buf,
                                                long long* out) {
@@ -162,6 +191,8 @@ __global__ void __launch_bounds__(352, 1) kern(int variant, int iters, int store
       bar5(c);
     else if (variant == 7)
       bar6(c);
+    else if (variant == 8)
+      bar8(c);
     else
       bar3(flags, rel + 16, variant - 2);
   }
@@ -202,6 +233,38 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       printf("variant %2d stores/thread %2d: %.3f us per barrier (%s)\n", v, stores, 1e3 * ms / iters,
              cudaGetErrorString(err));
+    }
+  }
+  for (int cs : {2, 4}) {
+    for (int stores : {0, 8}) {
+      int v = 8;
+      cudaMemset(c, 0, 8);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(sms);
+      cfg.blockDim = dim3(352);
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      at[1].id = cudaLaunchAttributeClusterDimension;
+      at[1].val.clusterDim.x = cs;
+      at[1].val.clusterDim.y = 1;
+      at[1].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      int ncl = 0;
+      cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaError_t el = cudaLaunchKernelEx(&cfg, kern, v, iters, stores, c, flags, rel, buf, out);
+      cudaEventRecord(e0);
+      cudaLaunchKernelEx(&cfg, kern, v, iters, stores, c, flags, rel, buf, out);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("variant  8 cluster %d (max active clusters %d) stores/thread %2d: %.3f us per barrier (%s / %s)\n", cs,
+             ncl, stores, 1e3 * ms / iters, cudaGetErrorString(el), cudaGetErrorString(err));
     }
   }
   return 0;

@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2506_04710_b200 import CONFIGS, ToeplitzMatvec, ToeplitzRep, gen  # noqa: E402
+from paper_2506_04710_b200 import CONFIGS, Config, ToeplitzMatvec, ToeplitzRep, gen  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
@@ -20,7 +20,8 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--nocorr", action="store_true")
 ap.add_argument("--embed", default="pow2")
 args = ap.parse_args()
-cfg = CONFIGS[args.config]
+EXTRA = {"G48": Config("G48", 48, 48, 96, 1, 8, 5, "normal", 50), "G40": Config("G40", 40, 24, 64, 1, 8, 6, "normal", 50)}
+cfg = CONFIGS[args.config] if args.config in CONFIGS else EXTRA[args.config]
 rep = ToeplitzRep.synthetic(cfg)
 if args.nocorr:
     rep.correction = None
