@@ -109,6 +109,16 @@ void* tbt_get_stream(tbt_ctx* ctx);
  * column-major complex, ToeplitzRep Sparse order (see above). Host memory. */
 tbt_status tbt_set_generators(tbt_ctx* ctx, const double* blocks,
                               long long nblocks);
+/* FULL generator layout (non-reciprocal operators, which the reference's
+ * Sparse ToeplitzRep cannot hold, toeplitz.hpp:72-74): the block of EVERY
+ * shift, (2ny-1)(2nx-1) of them, shift i = 1-ny..ny-1 (level 1, outer) by
+ * j = 1-nx..nx-1 (level 0, inner), each m x m column-major; block (i, j)
+ * couples source element (r, c) to target (r+i, c+j). Internally split into
+ * a reciprocal part (the usual half spectrum) and an anti-reciprocal part
+ * (a second half spectrum with the partner product negated); when the
+ * input is reciprocal the second part is empty. Such contexts take the
+ * multi-launch apply path and cannot be distributed or spectrum-cached. */
+tbt_status tbt_set_generators_full(tbt_ctx* ctx, const double* blocks, long long nblocks);
 
 /* 40 diag + rank-r terms (8 edge/corner components x 5 relations, layout of
  * tbtgen_correction in tbt_gen.h). rank 0 with d = NULL clears. Host memory. */

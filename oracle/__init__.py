@@ -36,6 +36,8 @@ def lib() -> C.CDLL:
         L.orc_fft.argtypes = [dp, C.c_size_t, C.c_int]
         L.orc_create.restype = C.c_void_p
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, dp]
+        L.orc_create_full.restype = C.c_void_p
+        L.orc_create_full.argtypes = [C.c_int, C.c_int, C.c_int, dp]
         L.orc_destroy.restype = None
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_precompute.argtypes = [C.c_void_p, C.c_int]
@@ -118,11 +120,12 @@ class Oracle:
     """Restated ToeplitzMatvec + gmres over canonical Sparse generators."""
 
     def __init__(self, nx, ny, m, generators_raw: np.ndarray, correction=None, precompute=True,
-                 nthreads: int = 0, margin=None):
+                 nthreads: int = 0, margin=None, layout: str = "sparse"):
         self.nx, self.ny, self.m = nx, ny, m
         self.nA = self.n = nx * ny * m
         g = np.ascontiguousarray(generators_raw, dtype=np.complex128)
-        self._h = lib().orc_create(nx, ny, m, _p(g))
+        create = lib().orc_create_full if layout == "full" else lib().orc_create
+        self._h = create(nx, ny, m, _p(g))
         if not self._h:
             raise ValueError("orc_create failed")
         if correction is not None:
@@ -158,7 +161,7 @@ class Oracle:
             c = rep.correction
             corr = (c.rank, c.d, c.u, c.v)
         return cls(rep.nx, rep.ny, rep.m, rep.generators, corr, precompute, nthreads,
-                   getattr(rep, "margin", None))
+                   getattr(rep, "margin", None), getattr(rep, "layout", "sparse"))
 
     def precompute(self, nthreads: int = 0):
         lib().orc_precompute(self._h, nthreads)

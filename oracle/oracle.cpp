@@ -209,6 +209,7 @@ struct orc_op {
   int nx = 0, ny = 0, e5 = 0;
   long nA = 0;
   std::vector<cplx> gen;  // canonical blocks, column-major each
+  std::vector<cplx> genFull;  // FULL layout (tbt_set_generators_full): every shift
   long L0 = 1, L1 = 1, L = 1;
   std::vector<cplx> ahat;  // [(m*e5+n)*L + f], f = s1*L0 + s0
   bool haveSpectra = false;
@@ -303,6 +304,9 @@ struct orc_op {
   // aEntry (linsolve.cpp:218-227), Sparse branch: negative half through the
   // block symmetry A(-i,-j) = A(i,j)^T.
   cplx aEntry(int i, int j, int m, int n) const {
+    if (!genFull.empty())  // FULL layout: every shift stored (non-reciprocal operators)
+      return genFull[(static_cast<size_t>(i + ny - 1) * (2 * nx - 1) + static_cast<size_t>(j + nx - 1)) * e5 * e5 +
+                     static_cast<size_t>(n) * e5 + m];
     if (i < 0 || (i == 0 && j < 0)) return aEntry(-i, -j, n, m);
     const long t = blockIndex(i, j);
     return gen[static_cast<size_t>(t) * e5 * e5 + static_cast<size_t>(n) * e5 + m];
@@ -441,6 +445,24 @@ orc_op* orc_create(int nx, int ny, int m, const double* blocks) {
   const size_t nb = static_cast<size_t>(nx) * ny + static_cast<size_t>(nx - 1) * (ny - 1);
   op->gen.resize(nb * m * m);
   std::memcpy(static_cast<void*>(op->gen.data()), blocks, nb * m * m * sizeof(cplx));
+  op->L1 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * ny - 1)));
+  op->L0 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * nx - 1)));
+  op->L = op->L1 * op->L0;
+  return op;
+}
+
+// FULL layout: (2ny-1)(2nx-1) blocks, shift i = 1-ny..ny-1 outer, j inner.
+// aEntry reads every shift directly (no A(-s) = A(s)^T mirror).
+orc_op* orc_create_full(int nx, int ny, int m, const double* blocks) {
+  if (nx < 1 || ny < 1 || m < 1 || blocks == nullptr) return nullptr;
+  auto* op = new orc_op;
+  op->nx = nx;
+  op->ny = ny;
+  op->e5 = m;
+  op->nA = static_cast<long>(nx) * ny * m;
+  const size_t nb = static_cast<size_t>(2 * nx - 1) * (2 * ny - 1);
+  op->genFull.resize(nb * m * m);
+  std::memcpy(static_cast<void*>(op->genFull.data()), blocks, nb * m * m * sizeof(cplx));
   op->L1 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * ny - 1)));
   op->L0 = static_cast<long>(pow2AtLeast(static_cast<size_t>(2 * nx - 1)));
   op->L = op->L1 * op->L0;

@@ -36,6 +36,9 @@ int orc_fft(double* a, size_t n, int inverse);
  * order toeplitz.cpp:305-312), m x m column-major complex each. The blocks
  * are copied. */
 orc_op* orc_create(int nx, int ny, int m, const double* blocks);
+/* FULL generator layout (every shift, non-reciprocal): (2ny-1)(2nx-1)
+ * blocks, i = 1-ny..ny-1 outer, j = 1-nx..nx-1 inner, m x m column-major. */
+orc_op* orc_create_full(int nx, int ny, int m, const double* blocks);
 void orc_destroy(orc_op* op);
 
 /* buildASpectra (proj/src/linsolve.cpp:239-258), optionally threaded over

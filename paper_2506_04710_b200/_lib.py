@@ -49,6 +49,7 @@ SIGNATURES = {
     "tbt_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tbt_get_stream": (C.c_void_p, [C.c_void_p]),
     "tbt_set_generators": (C.c_int, [C.c_void_p, dp, C.c_longlong]),
+    "tbt_set_generators_full": (C.c_int, [C.c_void_p, dp, C.c_longlong]),
     "tbt_set_correction": (C.c_int, [C.c_void_p, C.c_int, dp, dp, dp]),
     "tbt_precompute": (C.c_int, [C.c_void_p]),
     "tbt_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),

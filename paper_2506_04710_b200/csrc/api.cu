@@ -398,7 +398,8 @@ void tbt_destroy(tbt_ctx* h) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
-  for (void* p : {static_cast<void*>(c.dSpectra), static_cast<void*>(c.dPairF), static_cast<void*>(c.dPairG),
+  for (void* p : {static_cast<void*>(c.dSpectra), static_cast<void*>(c.dSpectraAnti), static_cast<void*>(c.dGenAnti),
+                  static_cast<void*>(c.dPairF), static_cast<void*>(c.dPairG),
                   static_cast<void*>(c.dAntisym), static_cast<void*>(c.dTw0), static_cast<void*>(c.dTw1),
                   static_cast<void*>(c.dCorrD), static_cast<void*>(c.dCorrU), static_cast<void*>(c.dCorrV),
                   static_cast<void*>(c.dTermInfo), static_cast<void*>(c.dTargetList),
@@ -527,6 +528,72 @@ tbt_status tbt_set_generators(tbt_ctx* h, const double* blocks, long long nblock
     TBT_CUDA_CHECK(cudaSetDevice(c.device));
     TBT_CUDA_CHECK(cudaMalloc(&c.dGen, cnt * sizeof(double2)));
     uploadSync(c.dGen, blocks, cnt * sizeof(double2), c.stream);
+    if (c.dGenAnti) cudaFree(c.dGenAnti);
+    c.dGenAnti = nullptr;
+    c.fullMode = false;
+    c.haveGenerators = true;
+    c.havePrecompute = false;
+  });
+}
+
+// FULL generator layout: every shift's block, also for
+// non-reciprocal operators the reference's Sparse ToeplitzRep cannot hold
+// (toeplitz.hpp:72-74). Split into a reciprocal part, stored and applied
+// exactly like tbt_set_generators' (Z_s(s) = (Z(s) + Z(-s)^T)/2, and the
+// whole self block Z(0,0), whose antisymmetric part goes to K as usual), and
+// an anti-reciprocal part Z_a(s) = (Z(s) - Z(-s)^T)/2 for s != 0, whose
+// spectrum obeys Ahat_a(-f) = -Ahat_a(f)^T (second half spectrum, second K3
+// pass). Blocks: i = 1-ny .. ny-1 (outer), j = 1-nx .. nx-1, m x m
+// column-major.
+tbt_status tbt_set_generators_full(tbt_ctx* h, const double* blocks, long long nblocks) {
+  return guardedCtx(h, [&] {
+    TBT_USER_CHECK(h && blocks, "tbt_set_generators_full: null argument");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(!c.dist, "tbt_set_generators_full: not supported on a distributed context");
+    const int nx = c.nx, ny = c.ny, m = c.m;
+    const long long want = static_cast<long long>(2 * nx - 1) * (2 * ny - 1);
+    TBT_USER_CHECK(nblocks == want, "tbt_set_generators_full: expected " + std::to_string(want) +
+                                        " blocks ((2ny-1)*(2nx-1)), got " + std::to_string(nblocks));
+    const size_t mm = static_cast<size_t>(m) * m;
+    const double2* z = reinterpret_cast<const double2*>(blocks);
+    auto full = [&](int i, int j) {  // block of shift (i, j)
+      return z + (static_cast<size_t>(i + ny - 1) * (2 * nx - 1) + static_cast<size_t>(j + nx - 1)) * mm;
+    };
+    const long long ncan = static_cast<long long>(nx) * ny + static_cast<long long>(nx - 1) * (ny - 1);
+    std::vector<double2> gs(static_cast<size_t>(ncan) * mm), ga(static_cast<size_t>(ncan) * mm);
+    bool anti = false;
+    long long t = 0;
+    for (int i = 0; i < ny; ++i)
+      for (int j = (i == 0 ? 0 : 1 - nx); j <= nx - 1; ++j, ++t) {
+        const double2* zp = full(i, j);
+        const double2* zn = full(-i, -j);
+        for (int b = 0; b < m; ++b)
+          for (int a = 0; a < m; ++a) {
+            const double2 v = zp[static_cast<size_t>(b) * m + a];   // Z(s)(a, b)
+            const double2 w = zn[static_cast<size_t>(a) * m + b];   // Z(-s)(b, a) = Z(-s)^T(a, b)
+            const size_t o = static_cast<size_t>(t) * mm + static_cast<size_t>(b) * m + a;
+            if (i == 0 && j == 0) {
+              gs[o] = v;
+              ga[o] = make_double2(0.0, 0.0);
+            } else {
+              gs[o] = make_double2(0.5 * (v.x + w.x), 0.5 * (v.y + w.y));
+              ga[o] = make_double2(0.5 * (v.x - w.x), 0.5 * (v.y - w.y));
+              if (ga[o].x != 0.0 || ga[o].y != 0.0) anti = true;
+            }
+          }
+      }
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    c.genHost.assign(gs.begin(), gs.begin() + static_cast<long long>(mm));
+    if (c.dGen) cudaFree(c.dGen);
+    if (c.dGenAnti) cudaFree(c.dGenAnti);
+    c.dGen = c.dGenAnti = nullptr;
+    TBT_CUDA_CHECK(cudaMalloc(&c.dGen, gs.size() * sizeof(double2)));
+    uploadSync(c.dGen, gs.data(), gs.size() * sizeof(double2), c.stream);
+    c.fullMode = anti;
+    if (anti) {
+      TBT_CUDA_CHECK(cudaMalloc(&c.dGenAnti, ga.size() * sizeof(double2)));
+      uploadSync(c.dGenAnti, ga.data(), ga.size() * sizeof(double2), c.stream);
+    }
     c.haveGenerators = true;
     c.havePrecompute = false;
   });
@@ -651,6 +718,8 @@ tbt_status tbt_precompute(tbt_ctx* h) {
     refreshDiagonal(c, nullptr);
     cudaFree(c.dGen);
     c.dGen = nullptr;
+    if (c.dGenAnti) cudaFree(c.dGenAnti);
+    c.dGenAnti = nullptr;
     c.haveGenerators = false;  // a new precompute needs the blocks again
     c.havePrecompute = true;
   });
@@ -1283,6 +1352,7 @@ void distInit(tbt_ctx* h, int nranks, int rank, const char* id, bool loopback) {
   Ctx& c = h->c;
   TBT_USER_CHECK(!c.havePrecompute, "tbt_dist_init: call before tbt_precompute");
   TBT_USER_CHECK(!c.margin, "tbt_dist_init: margin parts are not supported on a distributed context");
+  TBT_USER_CHECK(!c.fullMode, "tbt_dist_init: FULL (non-reciprocal) generators are not supported on a distributed context");
   TBT_USER_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "tbt_dist_init: bad rank");
   TBT_USER_CHECK(nranks <= c.L0, "tbt_dist_init: more ranks than level-0 bins");
   // Every rank owns at least one element row (its slab of the vectors, the

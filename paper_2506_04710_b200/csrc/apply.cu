@@ -67,10 +67,12 @@ void binProductTimed(Ctx& c, int nrhs) {
     }
     TBT_CUDA_CHECK(cudaEventRecord(c.tEvA[c.tCount], s));
     launchBinProduct(c, nrhs);
+    launchBinProductAnti(c, nrhs);
     TBT_CUDA_CHECK(cudaEventRecord(c.tEvB[c.tCount], s));
     ++c.tCount;
   } else {
     launchBinProduct(c, nrhs);
+    launchBinProductAnti(c, nrhs);
   }
 }
 

@@ -112,7 +112,7 @@ binprodTile(const double2* __restrict__ S, const int* __restrict__ pairF, const 
 __global__ void __launch_bounds__(128)
 binprodGeneric(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
                long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int m,
-               int nrhs) {
+               int nrhs, int acc = 0, double sg = 1.0) {
   const long long B = static_cast<long long>(nrhs) * m;
   for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
     const int f = pairF[p], g = pairG[p];
@@ -123,13 +123,16 @@ binprodGeneric(const double2* __restrict__ S, const int* __restrict__ pairF, con
       for (int a = threadIdx.x; a < m; a += blockDim.x) {
         double2 s = make_double2(0.0, 0.0);
         for (int b = 0; b < m; ++b) cfma(s, A[static_cast<long long>(a) * m + b], xf[b]);
-        yhat[f * B + rhs * m + a] = s;
+        double2& yo = yhat[f * B + rhs * m + a];
+        yo = acc ? cadd(yo, s) : s;
       }
       if (f != g)
         for (int b = threadIdx.x; b < m; b += blockDim.x) {
           double2 s = make_double2(0.0, 0.0);
           for (int a = 0; a < m; ++a) cfma(s, A[static_cast<long long>(a) * m + b], xg[a]);
-          yhat[g * B + rhs * m + b] = s;
+          double2& yo = yhat[g * B + rhs * m + b];
+          const double2 v = make_double2(sg * s.x, sg * s.y);
+          yo = acc ? cadd(yo, v) : v;
         }
     }
   }
@@ -341,7 +344,7 @@ template <int CPT>
 __global__ void __launch_bounds__(288, 1)
 binprodRingAny(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
                long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int m,
-               uint32_t stageBytes, int nst) {
+               uint32_t stageBytes, int nst, int accum, double sg) {
   constexpr int NT = 256, RPT = kAnyRows / (NT / 32);
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stageBytes);
@@ -430,7 +433,10 @@ binprodRingAny(const double2* __restrict__ S, const int* __restrict__ pairF, con
       for (int j = 0; j < CPT; ++j) cfma(acc, a[i][j], xfr[j]);
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) acc = cadd(acc, shflXor(acc, off));
-      if (lane == 0 && r < rr) yhat[f * m + static_cast<long long>(ch) * kAnyRows + r] = acc;
+      if (lane == 0 && r < rr) {
+        double2& yo = yhat[f * m + static_cast<long long>(ch) * kAnyRows + r];
+        yo = accum ? cadd(yo, acc) : acc;
+      }
     }
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
@@ -451,14 +457,15 @@ binprodRingAny(const double2* __restrict__ S, const int* __restrict__ pairF, con
           double2 acc = rb[q];
 #pragma unroll
           for (int w = 1; w < NT / 32; ++w) acc = cadd(acc, rb[w * m + q]);
-          yhat[g * m + q] = acc;
+          const double2 v = make_double2(sg * acc.x, sg * acc.y);
+          yhat[g * m + q] = accum ? cadd(yhat[g * m + q], v) : v;
         }
     }
   }
 }
 
 template <int CPT>
-void launchRingAny(Ctx& c) {
+void launchRingAny(Ctx& c, const double2* S, int accum, double sg) {
   const int m = c.m;
   const uint32_t stage =
       static_cast<uint32_t>((static_cast<size_t>(kAnyRows) * m * 16 + m * 16 + kAnyRows * 16 + 127) / 128 * 128);
@@ -472,20 +479,20 @@ void launchRingAny(Ctx& c) {
                                         227 * 1024));
   });
   const int grid = static_cast<int>(std::min<long long>(c.npairs, smCount(c.device)));
-  binprodRingAny<CPT><<<grid, 288, smem, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, m,
-                                                     stage, nst);
+  binprodRingAny<CPT><<<grid, 288, smem, c.stream>>>(S, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, m, stage,
+                                                     nst, accum, sg);
 }
 
-void launchStream(Ctx& c) {
+void launchStream(Ctx& c, const double2* S, int accum = 0, double sg = 1.0) {
   switch ((c.m + 31) / 32) {
-    case 1: launchRingAny<1>(c); break;
-    case 2: launchRingAny<2>(c); break;
-    case 3: launchRingAny<3>(c); break;
-    case 4: launchRingAny<4>(c); break;
-    case 5: launchRingAny<5>(c); break;
-    case 6: launchRingAny<6>(c); break;
-    case 7: launchRingAny<7>(c); break;
-    default: launchRingAny<8>(c); break;
+    case 1: launchRingAny<1>(c, S, accum, sg); break;
+    case 2: launchRingAny<2>(c, S, accum, sg); break;
+    case 3: launchRingAny<3>(c, S, accum, sg); break;
+    case 4: launchRingAny<4>(c, S, accum, sg); break;
+    case 5: launchRingAny<5>(c, S, accum, sg); break;
+    case 6: launchRingAny<6>(c, S, accum, sg); break;
+    case 7: launchRingAny<7>(c, S, accum, sg); break;
+    default: launchRingAny<8>(c, S, accum, sg); break;
   }
 }
 
@@ -520,7 +527,7 @@ void launchBinProduct(Ctx& c, int nrhs) {
     return;
   }
   if (nrhs == 1 && binprodVariant(c.m) == 0 && c.m <= 256) {
-    launchStream(c);
+    launchStream(c, c.dSpectra);
     TBT_CUDA_CHECK(cudaGetLastError());
     return;
   }
@@ -547,6 +554,20 @@ void launchBinProduct(Ctx& c, int nrhs) {
       binprodGeneric<<<static_cast<int>(grid), 128, 0, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs,
                                                                   c.dXhat, c.dYhat, c.m, nrhs);
     }
+  }
+  TBT_CUDA_CHECK(cudaGetLastError());
+}
+
+// FULL generators: yhat += A_a xhat with the anti-reciprocal part's half
+// spectrum (the partner product negated: Ahat_a(-f) = -Ahat_a(f)^T).
+void launchBinProductAnti(Ctx& c, int nrhs) {
+  if (!c.fullMode || !c.dSpectraAnti) return;
+  if (nrhs == 1 && c.m <= 256) {
+    launchStream(c, c.dSpectraAnti, 1, -1.0);
+  } else {
+    const long long grid = std::min<long long>(c.npairs, 4LL * smCount(c.device));
+    binprodGeneric<<<static_cast<int>(std::max<long long>(grid, 1)), 128, 0, c.stream>>>(
+        c.dSpectraAnti, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, c.m, nrhs, 1, -1.0);
   }
   TBT_CUDA_CHECK(cudaGetLastError());
 }

@@ -645,7 +645,7 @@ bool buildArgs(Ctx& c, CsArgs& a, size_t& smemBytes) {
 
 // Whether the one-cluster path serves this context (tiny operators only).
 bool clusterSmallSupported(const Ctx& c, int restart) {
-  if (c.dist || c.margin || c.forceMultiPass || c.timeBinprod) return false;
+  if (c.dist || c.margin || c.forceMultiPass || c.timeBinprod || c.fullMode) return false;
   if (c.L > 256 || c.m > 64 || c.ne > 256 || c.npairs < 1 || c.rank > 8) return false;
   CsArgs a{};
   size_t base = 0;

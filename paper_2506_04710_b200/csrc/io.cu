@@ -274,6 +274,7 @@ struct SpecHeader {
 
 void saveSpectra(Ctx& c, const std::string& path) {
   TBT_USER_CHECK(c.havePrecompute && !c.dist, "tbt_save_spectra: needs a precomputed single-GPU context");
+  TBT_USER_CHECK(!c.fullMode, "tbt_save_spectra: FULL (non-reciprocal) generators are not cached");
   const long long mm = static_cast<long long>(c.m) * c.m;
   std::vector<double2> host(static_cast<size_t>(c.npairs * mm));
   TBT_CUDA_CHECK(cudaMemcpyAsync(host.data(), c.dSpectra, host.size() * sizeof(double2), cudaMemcpyDeviceToHost,

@@ -660,7 +660,7 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
 }  // namespace
 
 bool persistentSupported(const Ctx& c) {
-  if (c.hasAntisym) return false;
+  if (c.hasAntisym || c.fullMode) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
     case 64064064: case 128128128: case 192256256: case 64032032: case 128032016: case 64016032:

@@ -30,10 +30,12 @@ __device__ __forceinline__ int shiftOf(int s, int L, int n) {
   return INT_MIN;                // zero padding
 }
 
-// G[s1][s0][ab] = Z(shift)(a, b) for rows a in [a0, a0 + rows).
+// G[s1][s0][ab] = Z(shift)(a, b) for rows a in [a0, a0 + rows); the
+// mirrored half is mir * Z(-shift)^T (mir = 1: reciprocal generators; -1:
+// the anti-reciprocal part of a FULL generator set, tbt_set_generators_full).
 __global__ void gatherShiftGrid(const double2* __restrict__ gen, const double2* __restrict__ s0blk,
                                 double2* __restrict__ G, int nx, int ny, int m, int L0, int L1,
-                                int a0, int rows) {
+                                int a0, int rows, double mir) {
   const long long B = static_cast<long long>(rows) * m;
   const long long total = static_cast<long long>(L0) * L1 * B;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
@@ -55,6 +57,7 @@ __global__ void gatherShiftGrid(const double2* __restrict__ gen, const double2* 
         const int ii = -i, jj = -j;
         const long long t = (ii == 0) ? jj : nx + static_cast<long long>(ii - 1) * (2 * nx - 1) + (jj - (1 - nx));
         v = gen[t * mm + static_cast<long long>(a) * m + b];
+        v = make_double2(mir * v.x, mir * v.y);
       }
     }
     G[q] = v;
@@ -151,34 +154,26 @@ void planPairs(Ctx& c, std::vector<int>& pairFGlobal) {
   uploadSync(c.dPairG, c.pairG.data(), c.npairs * sizeof(int), c.stream);
 }
 
-void buildSpectra(Ctx& c) {
+namespace {
+// K1 for one generator set (canonical Sparse order on the device, self
+// block S0 column-major) into spectra [pair][a][b] (bin-pair-major).
+void transformGenerators(Ctx& c, const double2* dGen, const std::vector<double2>& s0, double mir, double2* spectra,
+                         const int* dPairFGlobal) {
   const int m = c.m, nx = c.nx, ny = c.ny;
   const long long mm = static_cast<long long>(m) * m;
-  // canonical generator blocks: c.dGen (tbt_set_generators)
   cudaStream_t s = c.stream;
-  const std::vector<double2> s0 = splitSelfBlock(c);
-  std::vector<int> pairFGlobal;
-  planPairs(c, pairFGlobal);
-  int* dPairFGlobal = nullptr;
-  TBT_CUDA_CHECK(cudaMalloc(&dPairFGlobal, std::max<long long>(c.npairs, 1) * sizeof(int)));
-  uploadSync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), s);
-
-  // Generators and S0 on the device for the gather.
-  const double2* dGen = c.dGen;
   double2 *dS0 = nullptr, *dG = nullptr;
   TBT_CUDA_CHECK(cudaMalloc(&dS0, mm * sizeof(double2)));
   uploadSync(dS0, s0.data(), mm * sizeof(double2), s);
-
   // Row chunks bounded to ~4 GiB of transform workspace.
   const long long budget = 4LL << 30;
   int rows = static_cast<int>(std::max<long long>(1, std::min<long long>(m, budget / (c.L * m * 16))));
   TBT_CUDA_CHECK(cudaMalloc(&dG, c.L * rows * m * sizeof(double2)));
-
   const int sms = smCount(c.device);
   for (int a0 = 0; a0 < m; a0 += rows) {
     const int r = std::min(rows, m - a0);
     const long long B = static_cast<long long>(r) * m;
-    gatherShiftGrid<<<sms * 8, 256, 0, s>>>(dGen, dS0, dG, nx, ny, m, c.L0, c.L1, a0, r);
+    gatherShiftGrid<<<sms * 8, 256, 0, s>>>(dGen, dS0, dG, nx, ny, m, c.L0, c.L1, a0, r, mir);
     TBT_CUDA_CHECK(cudaGetLastError());
     FftPass pa;  // along s0 (level 0), one line per s1 row, in place
     pa.in = dG;
@@ -200,12 +195,34 @@ void buildSpectra(Ctx& c) {
     pb.batch = static_cast<int>(B);
     pb.tw = c.dTw1;
     launchFftPass(pb, s);
-    if (c.npairs > 0) scatterPairs<<<sms * 8, 256, 0, s>>>(dG, dPairFGlobal, c.dSpectra, c.npairs, m, a0, r);
+    if (c.npairs > 0) scatterPairs<<<sms * 8, 256, 0, s>>>(dG, dPairFGlobal, spectra, c.npairs, m, a0, r);
     TBT_CUDA_CHECK(cudaGetLastError());
   }
   TBT_CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(dG);
   cudaFree(dS0);
+}
+}  // namespace
+
+void buildSpectra(Ctx& c) {
+  const long long mm = static_cast<long long>(c.m) * c.m;
+  cudaStream_t s = c.stream;
+  const std::vector<double2> s0 = splitSelfBlock(c);
+  std::vector<int> pairFGlobal;
+  planPairs(c, pairFGlobal);
+  int* dPairFGlobal = nullptr;
+  TBT_CUDA_CHECK(cudaMalloc(&dPairFGlobal, std::max<long long>(c.npairs, 1) * sizeof(int)));
+  uploadSync(dPairFGlobal, pairFGlobal.data(), c.npairs * sizeof(int), s);
+  transformGenerators(c, c.dGen, s0, 1.0, c.dSpectra, dPairFGlobal);
+  if (c.dSpectraAnti) cudaFree(c.dSpectraAnti);
+  c.dSpectraAnti = nullptr;
+  if (c.fullMode) {
+    // The anti-reciprocal part (FULL generators): Ahat_a(-f) = -Ahat_a(f)^T,
+    // the same half storage with the partner's product negated by K3.
+    TBT_CUDA_CHECK(cudaMalloc(&c.dSpectraAnti, std::max<long long>(c.npairs, 1) * mm * sizeof(double2)));
+    const std::vector<double2> zero(static_cast<size_t>(mm), make_double2(0.0, 0.0));
+    transformGenerators(c, c.dGenAnti, zero, -1.0, c.dSpectraAnti, dPairFGlobal);
+  }
   cudaFree(dPairFGlobal);
 }
 

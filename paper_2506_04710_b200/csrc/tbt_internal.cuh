@@ -181,6 +181,14 @@ struct Ctx {
   bool haveCacheKey = false;
   long long npairs = 0;
   double2* dSpectra = nullptr;    // [npairs][m][m] row-major
+  // FULL (non-reciprocal) generators, tbt_set_generators_full: A = A_s + A_a
+  // with A_s reciprocal (the usual half spectrum, dGen / dSpectra) and A_a
+  // anti-reciprocal, A_a(-s) = -A_a(s)^T (canonical half in dGenAnti until
+  // tbt_precompute, its half spectrum in dSpectraAnti, applied by a second
+  // K3 pass that negates the partner product). Multi-launch apply path only.
+  bool fullMode = false;
+  double2* dGenAnti = nullptr;
+  double2* dSpectraAnti = nullptr;
   int* dPairF = nullptr;          // representative bin of pair p
   int* dPairG = nullptr;          // partner bin (== F for self-paired)
   std::vector<int> pairF, pairG;  // host copies
@@ -258,6 +266,7 @@ std::vector<double2> splitSelfBlock(Ctx& c);                   // spectra.cu: K 
 void planPairs(Ctx& c, std::vector<int>& pairFGlobal);         // spectra.cu: pair tables + spectrum allocation
 void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
+void launchBinProductAnti(Ctx& c, int nrhs);                  // binprod.cu: FULL generators, yhat += A_a xhat
 int binprodVariant(int m);                                    // binprod.cu
 constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEMM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu

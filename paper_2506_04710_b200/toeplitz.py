@@ -63,6 +63,10 @@ class ToeplitzRep:
     generators: np.ndarray  # (nb, m, m) column-major blocks, raw layout of gen.blocks_raw
     correction: Correction | None = None
     margin: "Margin | None" = None
+    # "sparse": the reference's canonical half (nx*ny + (nx-1)*(ny-1) blocks,
+    # A(-s) = A(s)^T); "full": every shift, (2ny-1)*(2nx-1) blocks, i = 1-ny
+    # .. ny-1 outer, j = 1-nx .. nx-1 inner (non-reciprocal operators).
+    layout: str = "sparse"
 
     @classmethod
     def synthetic(cls, cfg) -> "ToeplitzRep":
@@ -183,7 +187,8 @@ class ToeplitzMatvec:
             _check(lib().tbt_set_cache_key(self._h, key, len(key)))
         if not cached:
             gen = np.ascontiguousarray(rep.generators, dtype=np.complex128)
-            _check(lib().tbt_set_generators(self._h, gen.ctypes.data_as(dp), gen.shape[0]))
+            setg = lib().tbt_set_generators_full if rep.layout == "full" else lib().tbt_set_generators
+            _check(setg(self._h, gen.ctypes.data_as(dp), gen.shape[0]))
         if rep.correction is not None:
             c = rep.correction
             d = np.ascontiguousarray(c.d)
