@@ -75,3 +75,51 @@ def test_cpp_mirror_compiles(tmp_path):
     r = subprocess.run([gxx, "-std=c++17", "-fsyntax-only", "-I", str(REPO / "include"), str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def _build_mirror_demo(tmp_path):
+    import shutil
+    import subprocess
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    repo = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "mirror_demo"
+    lib_dir = repo / "paper_2506_04710_b200"
+    subprocess.run([gxx, "-std=c++17", "-O2", f"-I{repo / 'include'}", str(repo / "tests" / "cpp" / "mirror_demo.cpp"),
+                    f"-L{lib_dir}", "-ltbt", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_mirror_links_and_runs(tmp_path):
+    """The C++ mirror linked against libtbt.so and run (on a CPU-only host
+    the constructor must report the missing device, not fall back)."""
+    import subprocess
+    import torch
+    exe = _build_mirror_demo(tmp_path)
+    r = subprocess.run([str(exe), str(tmp_path / "out.bin")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    if not torch.cuda.is_available():
+        assert r.stdout.startswith("no device")
+
+
+@pytest.mark.gpu
+def test_gpu_cpp_mirror_matches_oracle(gpu, tmp_path):
+    import subprocess
+
+    import numpy as np
+
+    import oracle
+    from paper_2506_04710_b200 import CONFIGS, ToeplitzRep
+    exe = _build_mirror_demo(tmp_path)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+    v = np.fromfile(out, dtype=np.complex128).reshape(3, -1)
+    x, y, sol = v
+    cfg = CONFIGS["C1"]
+    rep = ToeplitzRep.synthetic(cfg)
+    o = oracle.Oracle(cfg.nx, cfg.ny, cfg.m, rep.generators)  # no correction in the demo
+    assert np.linalg.norm(y - o.applyA(x)) / np.linalg.norm(y) < 1e-11
+    ref = o.gmres(x, tol=1e-8, max_iter=2000, restart=30)
+    assert np.linalg.norm(sol - ref["x"]) / np.linalg.norm(ref["x"]) < 1e-8
