@@ -664,6 +664,8 @@ bool persistentSupported(const Ctx& c) {
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
     case 64064064: case 128128128: case 192256256: case 64032032: case 128032016: case 64016032:
+    // beyond the BASELINE shapes: other array sizes and basis counts
+    case 96128128: case 64128064: case 64064128: case 64128128: case 128064064: case 128256256: case 192128128:
       return true;
     default:
       return false;
@@ -685,6 +687,13 @@ bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, 
     case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 96128128: return launchP<96, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64128064: return launchP<64, 16, 64, 2, 128, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64064128: return launchP<64, 16, 64, 2, 64, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64128128: return launchP<64, 16, 64, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128064064: return launchP<128, 32, 16, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128256256: return launchP<128, 32, 16, 4, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 192128128: return launchP<192, 32, 16, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     default: return false;
   }
 }

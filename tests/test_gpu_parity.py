@@ -364,3 +364,31 @@ def test_concurrent_callers_one_context(gpu):
     for t in th:
         t.join()
     assert not errors
+
+
+# Persistent single-kernel apply instantiated beyond the BASELINE shapes
+# (matvec_persistent.cu): (m, L0, L1) -> a grid that selects it.
+PERSISTENT_EXTRA = [(33, 33, 96), (40, 24, 64), (24, 40, 64), (40, 40, 64), (20, 17, 128), (65, 70, 128), (40, 36, 192)]
+
+
+@pytest.mark.parametrize("nx,ny,m", PERSISTENT_EXTRA)
+def test_persistent_extra_shapes(gpu, nx, ny, m):
+    rep = ToeplitzRep.synthetic(Config("pe", nx, ny, m, 1, 8, 4, "normal", 50))
+    op = ToeplitzMatvec(rep)
+    assert op.info().apply_path == 2, "expected the persistent kernel"
+    x = gen.rhs_normal(nx * ny * m, 1, 3)[:, 0]
+    y = op.apply(x).reshape(nx * ny, m)
+    o = oracle.Oracle.from_rep(rep, precompute=False)
+    el = [0, nx - 1, (ny // 2) * nx + nx // 3, nx * ny - nx, nx * ny - 1]
+    yr = o.apply_rows(x, el)
+    assert np.linalg.norm(y[el] - yr) / np.linalg.norm(yr) < MATVEC_TOL
+    # single-column GMRES through the persistent kernel (fused LS step where
+    # the row chunk fits shared memory, the streamed one otherwise)
+    g = op.gmres(x, SolverOptions(tol=1e-8, maxIter=12, restart=10), raise_on_fail=False)
+    assert g.iterations[0] == 12 and np.isfinite(g.residual[0])
+    if nx * ny * m <= 70000:  # the oracle's spectra are cheap here: full GMRES parity
+        o.precompute()
+        r = o.gmres(x, tol=1e-8, max_iter=12, restart=10)
+        assert g.iterations == r["iterations"] and rel(g.current, r["x"]) < 1e-8
+        h, hr = g.history[0], r["history"][0]
+        assert h.shape == hr.shape and np.all(np.abs(h[:, 1] - hr[:, 1]) <= 1e-8 * np.abs(hr[:, 1]) + 1e-14)
