@@ -69,13 +69,18 @@ def measured_hbm():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
 
 
+TRAFFIC_FILES = ("r2_traffic.json", "r1_traffic.json")  # newest capture first
+
+
 def ncu_traffic(key):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r1_traffic.json), or None."""
-    try:
-        return json.loads((REPO / "profiles" / "r1_traffic.json").read_text())[key]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+    capture (profiles/r2_traffic.json, else r1), and the file it came from."""
+    for name in TRAFFIC_FILES:
+        try:
+            return json.loads((REPO / "profiles" / name).read_text())[key]["dram_bytes_per_launch"], name
+        except Exception:
+            continue
+    return None, None
 
 
 def workload_desc(cfg):
@@ -657,9 +662,9 @@ def main():
         kname = "binprod (K3, bin-pair product)"
     achieved = kbytes / (kms * 1e-3) / 1e9
     b_alg_full = 16 * (info.bins * cfg.m * cfg.m + (2 * cfg.m * info.bins + 2 * cfg.n))
-    traffic = ncu_traffic(f"{cfg.name}_matvec_persistent") if info.apply_path == 2 else None
+    traffic, tsrc = ncu_traffic(f"{cfg.name}_matvec_persistent") if info.apply_path == 2 else (None, None)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
+            "traffic": traffic, "traffic_source": f"profiles/{tsrc} (ncu --set full, one launch)" if tsrc else None,
             "kernel": kname, "bytes_per_launch": kbytes,
             "bytes_definition": "half spectrum (npairs*m^2*16) + xhat/yhat (2*L*m*16) + x/y (2*n*16)",
             "ms_per_launch": kms, "peak_source": peak_src}

@@ -65,21 +65,33 @@ def apply_bytes(cfg, info):
 
 
 def cpu_apply(rep, cfg, seconds, cols=1):
+    """CPU matvecs/s on `cols` host threads (one column each): the reference's
+    own applyA (oracle/_ref/libref_linsolve.so, kind "reference") up to C3,
+    the oracle port beyond (the reference builds its spectra on one thread).
+    Returns the oracle too (for the GMRES timing)."""
+    import tempfile
+
     import oracle
+    import bench
     t0 = time.perf_counter()
     o = oracle.Oracle.from_rep(rep, precompute=True, nthreads=0)
+    ref = None
+    if cfg.n * cfg.m <= 4_000_000:
+        with tempfile.TemporaryDirectory() as td:
+            ref = bench.reference_operator(cfg, td)
     pre = time.perf_counter() - t0
     X = np.asfortranarray(gen.rhs_normal(cfg.n, cols, 77))
-    o.apply_cols(X, nthreads=cols)
+    fn = (lambda: ref.apply_a_cols(X, threads=cols)) if ref is not None else (lambda: o.apply_cols(X, nthreads=cols))
+    fn()
     cnt, t0 = 0, time.perf_counter()
     while True:
-        o.apply_cols(X, nthreads=cols)
+        fn()
         cnt += cols
         el = time.perf_counter() - t0
         if el >= seconds and cnt >= 2 * cols:
             break
     return o, {"matvecs_per_s": cnt / el, "threads": cols, "sample": f"{cnt} matvecs in {el:.1f} s",
-               "spectra_precompute_s": pre}
+               "kind": "reference" if ref is not None else "port", "spectra_precompute_s": pre}
 
 
 def run(name, args, out):
