@@ -168,14 +168,19 @@ void requireReady(const Ctx& c) {
 // One single-column apply, replayed from the cached CUDA graph unless K3
 // timing is on.
 void runApply1(Ctx& c, const double2* x, double2* y, bool withCorr) {
-  if (c.timeBinprod || c.dist) {
+  // The loopback transport meets the other ranks on the host: no capture.
+  if (c.timeBinprod || (c.dist && c.comm->kind() != 1)) {
     applyInternal(c, x, y, 1, withCorr);
     return;
   }
-  if (c.usePdl && !c.zeroCopyStage) {  // direct launch: consecutive applies overlap launch and tail (PDL)
+  if (c.usePdl && !c.zeroCopyStage && !c.dist) {  // direct launch: consecutive applies overlap launch and tail (PDL)
     applyInternal(c, x, y, 1, withCorr);
     return;
   }
+  // Sharded over NCCL: the ~12 kernels and three grouped send / receive
+  // exchanges of an apply replay as one CUDA graph (NCCL operations are
+  // capturable), so small operators are not bound by launch overhead.
+  if (c.dist && withCorr && c.haveCorr && c.nTerms > 0) distCorrPrepare(c);
   if (!c.graphExec || c.graphX != x || c.graphY != y || c.graphCorr != withCorr) {
     c.dropGraph();
     cudaGraph_t graph;
@@ -1377,6 +1382,12 @@ void distInit(tbt_ctx* h, int nranks, int rank, const char* id, bool loopback) {
   const long long myCols = static_cast<long long>(c.myColList.size());
   TBT_CUDA_CHECK(cudaMalloc(&c.dColsOfRank, flat.size() * sizeof(int)));
   uploadSync(c.dColsOfRank, flat.data(), flat.size() * sizeof(int), c.stream);
+  std::vector<int4> tab;
+  for (int q = 0; q < nranks; ++q)
+    for (int j = 0; j < static_cast<int>(c.colsOfRank[q].size()); ++j)
+      tab.push_back(make_int4(c.colsOfRank[q][j], j, static_cast<int>(c.colsOfRank[q].size()), c.colsOffset[q]));
+  TBT_CUDA_CHECK(cudaMalloc(&c.dColTab, tab.size() * sizeof(int4)));
+  uploadSync(c.dColTab, tab.data(), tab.size() * sizeof(int4), c.stream);
   TBT_CUDA_CHECK(cudaMalloc(&c.dTrow, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
   TBT_CUDA_CHECK(cudaMalloc(&c.dSend, std::max<long long>(1, c.myRows * c.L0 * B) * sizeof(double2)));
   TBT_CUDA_CHECK(cudaMalloc(&c.dTcol, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));

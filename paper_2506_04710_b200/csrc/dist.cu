@@ -280,29 +280,28 @@ void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std
 
 namespace {
 
-// dst[(row * nsel + j) * B + b] = src[row * srcRow + col[j] * B + b]
-__global__ void gatherColumns(const double2* __restrict__ src, double2* __restrict__ dst, int rows, int nsel,
-                              const int* __restrict__ col, int B, long long srcRow) {
-  const long long total = static_cast<long long>(rows) * nsel * B;
+// All peers at once: t runs over the concatenated column lists (peer q's
+// columns at t in [colsOffset[q], colsOffset[q+1])); tab[t] = {column s0,
+// position j in q's list, q's column count, colsOffset[q]}. Peer q's block
+// starts at rows * colsOffset[q] * B (the send offsets of the all-to-all).
+//   gather:  dst[rows*base*B + (row*nq + j)*B + b] = src[row*srcRow + col*B + b]
+//   scatter: the inverse map.
+template <bool GATHER>
+__global__ void permuteColumns(const double2* __restrict__ src, double2* __restrict__ dst, int rows, int L0,
+                               const int4* __restrict__ tab, int B, long long rowLen) {
+  const long long total = static_cast<long long>(rows) * L0 * B;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int b = static_cast<int>(q % B);
-    const long long rj = q / B;
-    const int j = static_cast<int>(rj % nsel), row = static_cast<int>(rj / nsel);
-    dst[q] = src[row * srcRow + static_cast<long long>(col[j]) * B + b];
-  }
-}
-
-// dst[row * dstRow + col[j] * B + b] = src[(row * nsel + j) * B + b]
-__global__ void scatterColumns(const double2* __restrict__ src, double2* __restrict__ dst, int rows, int nsel,
-                               const int* __restrict__ col, int B, long long dstRow) {
-  const long long total = static_cast<long long>(rows) * nsel * B;
-  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
-       q += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int b = static_cast<int>(q % B);
-    const long long rj = q / B;
-    const int j = static_cast<int>(rj % nsel), row = static_cast<int>(rj / nsel);
-    dst[row * dstRow + static_cast<long long>(col[j]) * B + b] = src[q];
+    const long long rt = q / B;
+    const int t = static_cast<int>(rt % L0), row = static_cast<int>(rt / L0);
+    const int4 e = tab[t];
+    const long long packed = static_cast<long long>(rows) * e.w * B + (static_cast<long long>(row) * e.z + e.y) * B + b;
+    const long long grid = row * rowLen + static_cast<long long>(e.x) * B + b;
+    if (GATHER)
+      dst[packed] = src[grid];
+    else
+      dst[grid] = src[packed];
   }
 }
 
@@ -317,12 +316,14 @@ int gridFor(long long n, int sms) { return static_cast<int>(std::max<long long>(
 }  // namespace
 
 void distFree(Ctx& c) {
-  for (void* p : {static_cast<void*>(c.dColsOfRank), static_cast<void*>(c.dTrow), static_cast<void*>(c.dTcol),
+  for (void* p : {static_cast<void*>(c.dColsOfRank), static_cast<void*>(c.dColTab), static_cast<void*>(c.dTrow),
+                  static_cast<void*>(c.dTcol),
                   static_cast<void*>(c.dSend), static_cast<void*>(c.dRecv), static_cast<void*>(c.dXhalo),
                   static_cast<void*>(c.dTermInfoLoc), static_cast<void*>(c.dTargetListLoc),
                   static_cast<void*>(c.dTargetPtrLoc), static_cast<void*>(c.dYcorrLoc)})
     if (p) cudaFree(p);
   c.dColsOfRank = nullptr;
+  c.dColTab = nullptr;
   c.dTrow = c.dTcol = c.dSend = c.dRecv = c.dXhalo = c.dYcorrLoc = nullptr;
   c.dTermInfoLoc = c.dTargetListLoc = c.dTargetPtrLoc = nullptr;
   c.nTargetsLoc = c.maxTermsLoc = 0;
@@ -405,7 +406,6 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   const int myCols = static_cast<int>(c.myColList.size());
   const int sms = smCount(c.device);
   cudaStream_t s = c.stream;
-  const int* myColDev = c.dColsOfRank + c.colsOffset[me];
 
   // 1. Row FFTs (level 0) of the local rows -> dTrow[r][s0][b].
   FftPass fa;
@@ -424,20 +424,18 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   launchFftPass(fa, s);
 
   // 2. All-to-all: my rows x columns of q  ->  rank q.
-  long long off = 0;
   std::vector<long long> sendOff(P + 1, 0), recvOff(P + 1, 0);
   for (int q = 0; q < P; ++q) {
-    const int nq = static_cast<int>(c.colsOfRank[q].size());
-    const long long cnt = static_cast<long long>(c.myRows) * nq * B;
-    if (cnt > 0)
-      gatherColumns<<<gridFor(cnt, sms), 256, 0, s>>>(c.dTrow, c.dSend + off, c.myRows, nq,
-                                                        c.dColsOfRank + c.colsOffset[q], B,
-                                                        static_cast<long long>(c.L0) * B);
-    off += cnt;
-    sendOff[q + 1] = off;
+    sendOff[q + 1] = static_cast<long long>(c.myRows) * c.colsOffset[q + 1] * B;
     recvOff[q + 1] = recvOff[q] + static_cast<long long>(c.rowStart[q + 1] - c.rowStart[q]) * myCols * B;
   }
-  TBT_CUDA_CHECK(cudaGetLastError());
+  {  // one launch packs the blocks of every peer
+    const long long cnt = static_cast<long long>(c.myRows) * c.L0 * B;
+    if (cnt > 0)
+      permuteColumns<true><<<gridFor(cnt, sms), 256, 0, s>>>(c.dTrow, c.dSend, c.myRows, c.L0, c.dColTab, B,
+                                                             static_cast<long long>(c.L0) * B);
+    TBT_CUDA_CHECK(cudaGetLastError());
+  }
   commSection(c, [&] {
     c.comm->groupStart();
     for (int q = 0; q < P; ++q) {
@@ -501,15 +499,13 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
     }
     c.comm->groupEnd(s);
   });
-  for (int q = 0; q < P; ++q) {
-    const int nq = static_cast<int>(c.colsOfRank[q].size());
-    const long long cnt = static_cast<long long>(c.myRows) * nq * B;
+  {
+    const long long cnt = static_cast<long long>(c.myRows) * c.L0 * B;
     if (cnt > 0)
-      scatterColumns<<<gridFor(cnt, sms), 256, 0, s>>>(c.dSend + sendOff[q], c.dTrow, c.myRows, nq,
-                                                         c.dColsOfRank + c.colsOffset[q], B,
-                                                         static_cast<long long>(c.L0) * B);
+      permuteColumns<false><<<gridFor(cnt, sms), 256, 0, s>>>(c.dSend, c.dTrow, c.myRows, c.L0, c.dColTab, B,
+                                                              static_cast<long long>(c.L0) * B);
+    TBT_CUDA_CHECK(cudaGetLastError());
   }
-  TBT_CUDA_CHECK(cudaGetLastError());
 
   // 7. Inverse row FFTs of my rows, keep nx points, 1/L -> y (local slab).
   FftPass ia;

@@ -155,6 +155,7 @@ struct Ctx {
   std::vector<int> myColList;
   int myRow0 = 0, myRows = 0;
   int* dColsOfRank = nullptr;                 // concatenated column lists
+  int4* dColTab = nullptr;                    // [L0] {column, j, peer's column count, peer's colsOffset}
   std::vector<int> colsOffset;                // [nranks+1] offsets into dColsOfRank
   double2* dTrow = nullptr;   // [myRows][L0][B]
   double2* dTcol = nullptr;   // [ny][myCols][B]
@@ -365,6 +366,7 @@ void memsetSync(void* dst, int value, size_t bytes, cudaStream_t s);        // a
 
 void distPlan(int ny, int L0, int P, std::vector<int>& rowStart, std::vector<std::vector<int>>& cols);
 void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);
+void distCorrPrepare(Ctx& c);  // local correction tables (allocates: call outside stream capture)
 void distFree(Ctx& c);
 
 // Persistent single-kernel apply (matvec_persistent.cu).
