@@ -379,6 +379,7 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       if (penv) c.prefetchAt = std::max(0, std::min(2, atoi(penv)));
       const char* fenv = getenv("TBT_FFT");
       c.forceMultiPass = fenv && std::string(fenv) == "passes";
+      c.forceFused2d = fenv && std::string(fenv) == "fused";
       const char* genv = getenv("TBT_GMRES");
       c.forceUnfused = genv && std::string(genv) == "unfused";
       c.forceCols = genv && std::string(genv) == "cols";
@@ -787,6 +788,14 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
       c.zeroCopyL2Bytes = 0;
       c.zeroCopyStage = false;
       TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    } else if (where == TBT_HOST && nrhs > 1 && !c.timeBinprod && [&] {
+                 TBT_CUDA_CHECK(cudaMemcpyAsync(c.dYout, xin, bytes, cudaMemcpyHostToDevice, c.stream));
+                 return applyUserLayout(c, c.dYout, c.dXin, nrhs, withCorr);
+               }()) {
+      // Many columns without the layout kernels (transform passes read and
+      // write the column-major layout themselves).
+      TBT_CUDA_CHECK(cudaMemcpyAsync(yout, c.dXin, bytes, cudaMemcpyDeviceToHost, c.stream));
+      TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     } else if (where == TBT_HOST) {
       if (nrhs == 1) {
         TBT_CUDA_CHECK(cudaMemcpyAsync(c.dXin, xin, bytes, cudaMemcpyHostToDevice, c.stream));
@@ -808,7 +817,7 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
     } else {
       if (nrhs == 1) {
         runApply1(c, xin, yout, withCorr);
-      } else {
+      } else if (c.timeBinprod || !applyUserLayout(c, xin, yout, nrhs, withCorr)) {
         launchLayout(xin, c.dXin, nloc, nrhs, true, c.stream, c.m);
         applyInternal(c, c.dXin, c.dYout, nrhs, withCorr);
         launchLayout(c.dYout, yout, nloc, nrhs, false, c.stream, c.m);

@@ -123,20 +123,32 @@ bool applyFused(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
 
 }  // namespace
 
-void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
-  if (c.dist) {
-    applyDist(c, x, y, nrhs, withCorr);
-    return;
-  }
-  if (nrhs == 1 && clusterSmallSupported(c, 1)) {  // tiny operators: one cluster, one launch
-    launchClusterApply(c, x, y, withCorr);
-    return;
-  }
-  if (nrhs == 1 && c.persistent && !c.timeBinprod && launchPersistentApply(c, x, y, withCorr)) return;
-  if (c.fused2d && !c.forceMultiPass && applyFused(c, x, y, nrhs, withCorr)) return;
+namespace {
+
+bool regPassesServe(const Ctx& c, int nrhs) {
+  return static_cast<long long>(nrhs) * c.m >= 1024 && c.L0 <= 64 && c.L1 <= 64 && !c.forceFused2d;
+}
+
+// The four 1-D passes around K3 (user = x / y in the caller's column-major
+// layout, register passes only).
+void applyPasses(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr, bool regPasses, bool user) {
   const long long B = static_cast<long long>(nrhs) * c.m;
   cudaStream_t s = c.stream;
-
+  // The correction's term vectors depend on x only: a parallel branch joined
+  // before the last pass, which adds them in its store epilogue.
+  const bool corrBranch = regPasses && withCorr && c.haveCorr && c.nTerms > 0;
+  if (corrBranch) {
+    TBT_CUDA_CHECK(cudaEventRecord(c.evFork, s));
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(c.side, c.evFork, 0));
+    launchCorrVector(c, x, c.dYcorr, nrhs, c.side, user ? c.n : 0);
+    TBT_CUDA_CHECK(cudaEventRecord(c.evJoin, c.side));
+  }
+  auto pass = [&](const FftPass& p) {
+    if (!(regPasses && launchFftPassReg(p, s))) {
+      if (p.inUser || p.outUser) throw Error{TBT_CUDA_ERROR, "user-layout transform pass without the register kernel"};
+      launchFftPass(p, s);
+    }
+  };
   FftPass fa;  // forward, level 0 (x): one line per element row r < ny
   fa.in = x;
   fa.out = c.dT;
@@ -150,7 +162,13 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
   fa.n_out = c.L0;
   fa.batch = static_cast<int>(B);
   fa.tw = c.dTw0;
-  launchFftPass(fa, s);
+  if (user) {
+    fa.inUser = 1;
+    fa.userNx = c.nx;
+    fa.userM = c.m;
+    fa.userN = c.n;
+  }
+  pass(fa);
 
   FftPass fb;  // forward, level 1 (y): one line per column s0
   fb.in = c.dT;
@@ -165,7 +183,7 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
   fb.n_out = c.L1;
   fb.batch = static_cast<int>(B);
   fb.tw = c.dTw1;
-  launchFftPass(fb, s);
+  pass(fb);
 
   binProductTimed(c, nrhs);
 
@@ -183,7 +201,7 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
   ib.batch = static_cast<int>(B);
   ib.inverse = 1;
   ib.tw = c.dTw1;
-  launchFftPass(ib, s);
+  pass(ib);
 
   FftPass ia;  // inverse, level 0: keep the nx element columns, scale 1/L
   ia.in = c.dT;
@@ -200,10 +218,51 @@ void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr
   ia.inverse = 1;
   ia.scale = 1.0 / static_cast<double>(c.L);
   ia.tw = c.dTw0;
-  launchFftPass(ia, s);
+  if (corrBranch) {
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(s, c.evJoin, 0));
+    ia.tPtr = c.dElemPtr;
+    ia.ycorr = c.dYcorr;
+    ia.corrNx = c.nx;
+  }
+  if (user) {
+    ia.outUser = 1;
+    ia.userNx = c.nx;
+    ia.userM = c.m;
+    ia.userN = c.n;
+  }
+  pass(ia);
 
-  launchAntisym(c, x, y, nrhs);
-  if (withCorr) launchCorrection(c, x, y, nrhs);
+  if (!user) {
+    launchAntisym(c, x, y, nrhs);
+    if (withCorr && !corrBranch) launchCorrection(c, x, y, nrhs);
+  }
+}
+
+
+}  // namespace
+
+void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
+  if (c.dist) {
+    applyDist(c, x, y, nrhs, withCorr);
+    return;
+  }
+  if (nrhs == 1 && clusterSmallSupported(c, 1)) {  // tiny operators: one cluster, one launch
+    launchClusterApply(c, x, y, withCorr);
+    return;
+  }
+  if (nrhs == 1 && c.persistent && !c.timeBinprod && launchPersistentApply(c, x, y, withCorr)) return;
+  // Wide batches (many right-hand sides) with short lines: register line
+  // passes (one thread per line and batch entry, fft.cu) beat the cluster
+  // 2-D kernels (C3: see DESIGN.md section 4.2); TBT_FFT=fused keeps those.
+  const bool regPasses = regPassesServe(c, nrhs);
+  if (!regPasses && c.fused2d && !c.forceMultiPass && applyFused(c, x, y, nrhs, withCorr)) return;
+  applyPasses(c, x, y, nrhs, withCorr, regPasses, false);
+}
+
+bool applyUserLayout(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
+  if (nrhs < 2 || c.dist || c.margin || c.hasAntisym || !regPassesServe(c, nrhs)) return false;
+  applyPasses(c, x, y, nrhs, withCorr, true, true);
+  return true;
 }
 
 }  // namespace tbt

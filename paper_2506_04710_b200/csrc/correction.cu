@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInf
                                                  const int* __restrict__ targetPtr, const double2* __restrict__ D,
                                                  const double2* __restrict__ U, const double2* __restrict__ V,
                                                  const double2* __restrict__ x, double2* __restrict__ ycorr, int m,
-                                                 int rank, int nrhs) {
+                                                 int rank, int nrhs, long long xE, long long xR) {
   extern __shared__ double2 sproj[];  // [terms of this target][rank]
   const int ti = blockIdx.x, rhs = blockIdx.y;
   const int e = targetList[ti];
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInf
   for (int t = t0 + warp; t < t1; t += blockDim.x / 32) {
     const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
     const double2* W = (trans ? U : V) + static_cast<long long>(slot) * rank * m;
-    const double2* xs = x + (static_cast<long long>(src) * nrhs + rhs) * m;
+    const double2* xs = x + src * xE + rhs * xR;
     for (int q = 0; q < rank; ++q) {
       double2 s = make_double2(0.0, 0.0);
       for (int a = lane; a < m; a += 32) cfma(s, __ldg(W + static_cast<long long>(q) * m + a), __ldg(xs + a));
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInf
     double2 acc = make_double2(0.0, 0.0);
     for (int t = t0; t < t1; ++t) {
       const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
-      cfma(acc, __ldg(D + static_cast<long long>(slot) * m + a), __ldg(x + (static_cast<long long>(src) * nrhs + rhs) * m + a));
+      cfma(acc, __ldg(D + static_cast<long long>(slot) * m + a), __ldg(x + src * xE + rhs * xR + a));
       const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * rank * m + a;
       for (int q = 0; q < rank; ++q) cfma(acc, __ldg(W2 + static_cast<long long>(q) * m), sproj[(t - t0) * rank + q]);
     }
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInf
                                                  const int* __restrict__ targetPtr, const double2* __restrict__ D,
                                                  const double2* __restrict__ U, const double2* __restrict__ V,
                                                  const double2* __restrict__ x, double2* __restrict__ ycorr,
-                                                 int nrhs) {
+                                                 int nrhs, long long xE, long long xR) {
   constexpr int M = 32 * KPL;
   constexpr int RPW = 4;  // columns per warp
   constexpr int RC = 8 * RPW;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInf
 #pragma unroll
     for (int j = 0; j < RPW; ++j) {
       const int r = r0 + warp * RPW + j;
-      const double2* xs = x + (static_cast<long long>(src) * nrhs + r) * M;
+      const double2* xs = x + src * xE + static_cast<long long>(r) * xR;
 #pragma unroll
       for (int k = 0; k < KPL; ++k) xv[j][k] = r < nrhs ? __ldg(xs + lane + 32 * k) : make_double2(0.0, 0.0);
     }
@@ -207,27 +207,32 @@ __global__ void antisymApply(const double2* __restrict__ K, const double2* __res
 
 }  // namespace
 
-void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
+void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                        long long xUserN) {
   if (t.nTargets == 0) return;
+  // x's element / column strides: internal [e][rhs][a], or the user's
+  // column-major n x nrhs (xUserN = n > 0).
+  const long long xE = xUserN > 0 ? c.m : static_cast<long long>(nrhs) * c.m;
+  const long long xR = xUserN > 0 ? xUserN : c.m;
   if (nrhs >= 8 && (c.rank == 4 || c.rank == 8) && (c.m == 64 || c.m == 128)) {
     dim3 grid(t.nTargets, (nrhs + 31) / 32);
     auto k = c.m == 64 ? (c.rank == 4 ? corrMulti<2, 4> : corrMulti<2, 8>)
                        : (c.rank == 4 ? corrMulti<4, 4> : corrMulti<4, 8>);
-    k<<<grid, 256, 0, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs);
+    k<<<grid, 256, 0, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs, xE, xR);
     TBT_CUDA_CHECK(cudaGetLastError());
     return;
   }
   dim3 grid(t.nTargets, nrhs);
   const size_t smem = static_cast<size_t>(t.maxTerms) * std::max(c.rank, 1) * sizeof(double2);
   corrFused<<<grid, 256, smem, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr,
-                                    c.m, c.rank, nrhs);
+                                    c.m, c.rank, nrhs, xE, xR);
   TBT_CUDA_CHECK(cudaGetLastError());
 }
 
-void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s) {
+void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s, long long xUserN) {
   if (!c.haveCorr || c.nTerms == 0) return;
   launchCorrVectorOn(c, CorrTables{c.dTermInfo, c.dTargetList, c.dTargetPtr, c.nTargets, c.maxTermsPerTarget}, x,
-                     ycorr, nrhs, s);
+                     ycorr, nrhs, s, xUserN);
 }
 
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs) {

@@ -81,6 +81,85 @@ fftPassKernel(FftPass p) {
   (void)N;
 }
 
+// One thread per (line, batch entry): consecutive threads take consecutive
+// batch entries, so every point's load / store is one contiguous 16-byte-
+// per-lane run (512 B per warp), and a thread keeps all n_in loads of its
+// line in flight. The N = R1 * R2 transform runs in registers: R2 radix-R1
+// DFTs over the decimated inputs, the twiddles w_N^(n2 k1) (table), then R1
+// radix-R2 DFTs; natural order in and out. No shared memory, no barriers.
+template <int N, bool INV>
+__global__ void __launch_bounds__(128) regLineKernel(FftPass p) {
+  using S = fftreg::Split<N>;
+  constexpr int R1 = S::R1, R2 = S::R2;
+  const int bg = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bg >= p.batch) return;
+  const int line = blockIdx.y;
+  const long long userBase = p.userM ? static_cast<long long>(bg / p.userM) * p.userN + bg % p.userM : 0;
+  const double2* in = p.inUser ? p.in + userBase + static_cast<long long>(line) * p.userNx * p.userM
+                               : p.in + line * p.in_line_stride + bg;
+  const long long inStride = p.inUser ? p.userM : p.in_point_stride;
+  double2 t[R2][R1];  // t[n2][n1] = x[R2 * n1 + n2]
+#pragma unroll
+  for (int n1 = 0; n1 < R1; ++n1)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const int pt = R2 * n1 + n2;
+      t[n2][n1] = pt < p.n_in ? ldg2(in + static_cast<long long>(pt) * inStride) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+  for (int n2 = 0; n2 < R2; ++n2) dftReg<R1, INV>(t[n2]);  // -> t[n2][k1]
+#pragma unroll
+  for (int n2 = 1; n2 < R2; ++n2)
+#pragma unroll
+    for (int k1 = 1; k1 < R1; ++k1) {
+      double2 w = __ldg(p.tw + n2 * k1);  // n2 * k1 < N
+      if (INV) w.y = -w.y;
+      t[n2][k1] = cmul(t[n2][k1], w);
+    }
+  double2* out = p.outUser ? p.out + userBase + static_cast<long long>(line) * p.userNx * p.userM
+                           : p.out + line * p.out_line_stride + bg;
+  const long long outStride = p.outUser ? p.userM : p.out_point_stride;
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    double2 v[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) v[n2] = t[n2][k1];
+    if constexpr (R2 > 1) dftReg<R2, INV>(v);
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) t[n2][k1] = v[n2];  // t[k2][k1] = X[k1 + R1 k2]
+  }
+  // Which output points carry correction terms (a mask for this line, read
+  // once), then every correction load of the thread in flight together.
+  unsigned long long targets = 0;
+  if (p.ycorr)
+    for (int pt = 0; pt < p.n_out && pt < 64; ++pt) {
+      const int e = line * p.corrNx + pt;
+      if (__ldg(p.tPtr + e) != __ldg(p.tPtr + e + 1)) targets |= 1ull << pt;
+    }
+#pragma unroll
+  for (int k2 = 0; k2 < R2; ++k2)
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int pt = k1 + R1 * k2;
+      if (pt < p.n_out) {
+        double2 o = cscale(t[k2][k1], p.scale);
+        // ycorr is internal [e][B]: e * B + bg = line * out_line_stride + pt * out_point_stride + bg
+        if ((targets >> pt) & 1ull)
+          o = cadd(o, p.ycorr[line * p.out_line_stride + static_cast<long long>(pt) * p.out_point_stride + bg]);
+        out[static_cast<long long>(pt) * outStride] = o;
+      }
+    }
+}
+
+template <int N>
+void launchReg(const FftPass& p, cudaStream_t s) {
+  dim3 grid((p.batch + 127) / 128, p.lines);
+  if (p.inverse)
+    regLineKernel<N, true><<<grid, 128, 0, s>>>(p);
+  else
+    regLineKernel<N, false><<<grid, 128, 0, s>>>(p);
+}
+
 template <int R1, int R2, int BC>
 void launchT(const FftPass& p, cudaStream_t s) {
   constexpr int NT = BC * (R1 > R2 ? R1 : R2);
@@ -115,6 +194,26 @@ void launchN(const FftPass& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool launchFftPassReg(const FftPass& p, cudaStream_t s) {
+  if (p.lines == 0 || p.batch == 0) return true;
+  if (p.batch < 512 || p.lines > 65535) return false;
+  switch (p.n) {
+    case 8: launchReg<8>(p, s); break;
+    case 9: launchReg<9>(p, s); break;
+    case 12: launchReg<12>(p, s); break;
+    case 16: launchReg<16>(p, s); break;
+    case 18: launchReg<18>(p, s); break;
+    case 24: launchReg<24>(p, s); break;
+    case 32: launchReg<32>(p, s); break;
+    case 36: launchReg<36>(p, s); break;
+    case 48: launchReg<48>(p, s); break;
+    case 64: launchReg<64>(p, s); break;
+    default: return false;
+  }
+  TBT_CUDA_CHECK(cudaGetLastError());
+  return true;
+}
 
 void launchFftPass(const FftPass& p, cudaStream_t s) {
   if (p.lines == 0 || p.batch == 0) return;

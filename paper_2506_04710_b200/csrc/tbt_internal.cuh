@@ -72,8 +72,23 @@ struct FftPass {
   int inverse = 0;
   double scale = 1.0;
   const double2* tw = nullptr;  // exp(-2 pi i t / n), t < n
+  // Optional store epilogue (the last inverse pass of a multi-RHS apply):
+  // out += ycorr at the same index for elements e = line * corrNx + point
+  // with correction terms (tPtr[e] != tPtr[e + 1]).
+  const int* tPtr = nullptr;
+  const double2* ycorr = nullptr;
+  int corrNx = 0;
+  // Register passes only: read `in` / write `out` in the user's column-major
+  // n x nrhs layout (element e = line * userNx + point, batch entry
+  // bg = rhs * userM + a -> rhs * userN + e * userM + a) instead of the
+  // strided internal one.
+  int inUser = 0, outUser = 0, userNx = 0, userM = 0;
+  long long userN = 0;
 };
 void launchFftPass(const FftPass& p, cudaStream_t s);
+// Register line pass (fft.cu): one thread per (line, batch entry), the whole
+// line in registers; for n <= 64 and wide batches. Returns false otherwise.
+bool launchFftPassReg(const FftPass& p, cudaStream_t s);
 
 // Cluster-fused 2-D transform (fft2d.cu).
 struct Fft2dArgs {
@@ -141,6 +156,7 @@ struct Ctx {
   const int* skipFlag = nullptr;  // device flag: persistent applies become no-ops when set
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
   bool forceMultiPass = false;             // TBT_FFT=passes
+  bool forceFused2d = false;               // TBT_FFT=fused: cluster 2-D kernels also for wide batches
   bool forceUnfused = false;               // TBT_GMRES=unfused: separate apply / Arnoldi launches
   bool forceCols = false;                  // TBT_GMRES=cols: column-blocked Arnoldi for one column too
 
@@ -266,13 +282,18 @@ void buildSpectra(Ctx& c);                                    // spectra.cu
 std::vector<double2> splitSelfBlock(Ctx& c);                   // spectra.cu: K on device, returns S0
 void planPairs(Ctx& c, std::vector<int>& pairFGlobal);         // spectra.cu: pair tables + spectrum allocation
 void applyInternal(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
+// Many columns straight from / to the user's column-major layout (no layout
+// kernels) when the register-pass path serves the context; false otherwise.
+bool applyUserLayout(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr);  // apply.cu
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 void launchBinProductAnti(Ctx& c, int nrhs);                  // binprod.cu: FULL generators, yhat += A_a xhat
 int binprodVariant(int m);                                    // binprod.cu
 constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEMM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
-void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);  // correction.cu
+// xUserN > 0: x in the user's column-major n x nrhs layout instead of [e][rhs][a].
+void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                      long long xUserN = 0);  // correction.cu
 // A term table (CSR by target): termInfo[4t..] = (target, source, slot, trans).
 struct CorrTables {
   const int* termInfo;
@@ -280,7 +301,8 @@ struct CorrTables {
   const int* targetPtr;
   int nTargets, maxTerms;
 };
-void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s);
+void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                        long long xUserN = 0);
 // Per target element, its correction terms {target, source, slot, trans} in
 // the order every apply path accumulates them (api.cu).
 std::vector<std::vector<std::array<int, 4>>> corrTermsByTarget(int nx, int ny);

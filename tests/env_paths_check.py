@@ -64,6 +64,22 @@ def check_smooth():
         assert rel(Y[:, c], ref) < 1e-11, ("smooth", c)
 
 
+def check_wide():
+    """Wide batches (C3 grid, m = 128, 16 columns: B = 2048), both
+    embeddings: register line passes by default, cluster 2-D kernels under
+    TBT_FFT=fused."""
+    for embed in ("smooth", "pow2"):
+        cfg = Config("w", 18, 9, 128, 16, 8, 3, "normal", 50)
+        rep = ToeplitzRep.synthetic(cfg)
+        op = ToeplitzMatvec(rep, max_nrhs=16, embed=embed)
+        o = oracle.Oracle.from_rep(rep)
+        X = gen.rhs_normal(cfg.n, 16, 7)
+        Y = op.apply(X)
+        for c in (0, 5, 15):
+            ref = o.apply(np.ascontiguousarray(X[:, c]))
+            assert rel(Y[:, c], ref) < 1e-11, ("wide", embed, c)
+
+
 def check_margin():
     """Margin coupling (B / B^T / C) single- and multi-column."""
     nx, ny, m, e = 4, 3, 6, [2, 3, 1, 4, 6, 2, 3, 5, 1]
@@ -78,7 +94,8 @@ def check_margin():
         assert rel(Y[:, c], ref) < 1e-11 and rel(op.apply(np.ascontiguousarray(X[:, c])), ref) < 1e-11
 
 
-CHECKS = {"apply": check_apply, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin}
+CHECKS = {"apply": check_apply, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin,
+          "wide": check_wide}
 
 if __name__ == "__main__":
     for name in sys.argv[1:]:

@@ -8,6 +8,8 @@ process per setting; the knobs are read once per process):
   TBT_BINPROD=1       K3 v1 (no TMA ring), with TBT_APPLY=multi
   TBT_PDL=0           device-resident applies replayed from a CUDA graph
   TBT_FFT=passes      line-pass transforms instead of the cluster 2-D kernels
+  TBT_FFT=fused       cluster 2-D kernels also for wide batches (default there:
+                      register line passes)
   TBT_FFT2D=2,4       cluster 2-D transform with a forced cluster / batch split
   TBT_E2E=staged      host applies through explicit copies, not zero-copy
   TBT_MARGIN_UNFUSED=1  separate margin B / B^T kernels for one column
@@ -22,7 +24,8 @@ import pytest
 SCRIPT = Path(__file__).resolve().parent / "env_paths_check.py"
 
 CASES = [
-    ({}, ["apply", "gmres", "smooth", "margin"]),  # the defaults, same checks (single after multi-column applies)
+    ({}, ["apply", "gmres", "smooth", "margin", "wide"]),  # the defaults (single after multi-column applies)
+    ({"TBT_FFT": "fused"}, ["wide"]),
     ({"TBT_APPLY": "multi"}, ["apply", "gmres"]),
     ({"TBT_GMRES": "cols"}, ["gmres"]),
     ({"TBT_GMRES": "unfused"}, ["gmres"]),
