@@ -88,7 +88,7 @@ fftPassKernel(FftPass p) {
 // DFTs over the decimated inputs, the twiddles w_N^(n2 k1) (table), then R1
 // radix-R2 DFTs; natural order in and out. No shared memory, no barriers.
 template <int N, bool INV>
-__global__ void __launch_bounds__(128) regLineKernel(FftPass p) {
+__global__ void __launch_bounds__(128, (N >= 48 ? 1 : N >= 24 ? 3 : 4)) regLineKernel(FftPass p) {
   using S = fftreg::Split<N>;
   constexpr int R1 = S::R1, R2 = S::R2;
   const int bg = blockIdx.x * blockDim.x + threadIdx.x;
