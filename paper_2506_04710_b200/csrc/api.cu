@@ -1403,6 +1403,8 @@ void distInit(tbt_ctx* h, int nranks, int rank, const char* id, bool loopback) {
   TBT_CUDA_CHECK(cudaMalloc(&c.dRecv, std::max<long long>(1, c.ny * myCols * B) * sizeof(double2)));
   TBT_CUDA_CHECK(cudaMalloc(&c.dXhalo, (c.myRows + 2) * static_cast<long long>(c.nx) * B * sizeof(double2)));
   memsetSync(c.dXhalo, 0, (c.myRows + 2) * static_cast<long long>(c.nx) * B * sizeof(double2), c.stream);
+  TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.commStream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : c.distEv) TBT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   c.comm = loopback ? makeLoopbackComm(nranks, rank, id) : makeNcclComm(nranks, rank, id);
   c.dist = true;
 }

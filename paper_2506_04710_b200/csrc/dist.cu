@@ -26,6 +26,7 @@
 #include <array>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -284,11 +285,12 @@ namespace {
 // columns at t in [colsOffset[q], colsOffset[q+1])); tab[t] = {column s0,
 // position j in q's list, q's column count, colsOffset[q]}. Peer q's block
 // starts at rows * colsOffset[q] * B (the send offsets of the all-to-all).
-//   gather:  dst[rows*base*B + (row*nq + j)*B + b] = src[row*srcRow + col*B + b]
-//   scatter: the inverse map.
+//   gather:  dst[rows*base*B + (row*nq + j)*B + b] = src[row*rowLen + col*colStride + b]
+//   scatter: the inverse map. (B = the chunk's batch entries, colStride =
+//   the full batch of the grid layout.)
 template <bool GATHER>
 __global__ void permuteColumns(const double2* __restrict__ src, double2* __restrict__ dst, int rows, int L0,
-                               const int4* __restrict__ tab, int B, long long rowLen) {
+                               const int4* __restrict__ tab, int B, long long rowLen, long long colStride) {
   const long long total = static_cast<long long>(rows) * L0 * B;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -297,7 +299,7 @@ __global__ void permuteColumns(const double2* __restrict__ src, double2* __restr
     const int t = static_cast<int>(rt % L0), row = static_cast<int>(rt / L0);
     const int4 e = tab[t];
     const long long packed = static_cast<long long>(rows) * e.w * B + (static_cast<long long>(row) * e.z + e.y) * B + b;
-    const long long grid = row * rowLen + static_cast<long long>(e.x) * B + b;
+    const long long grid = row * rowLen + static_cast<long long>(e.x) * colStride + b;
     if (GATHER)
       dst[packed] = src[grid];
     else
@@ -330,6 +332,13 @@ void distFree(Ctx& c) {
   c.distCorrReady = false;
   delete c.comm;
   c.comm = nullptr;
+  for (cudaEvent_t& e : c.distEv)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
+  if (c.commStream) cudaStreamDestroy(c.commStream);
+  c.commStream = nullptr;
 }
 
 // The correction terms whose target is one of this rank's elements
@@ -406,124 +415,172 @@ void applyDist(Ctx& c, const double2* x, double2* y, int nrhs, bool withCorr) {
   const int myCols = static_cast<int>(c.myColList.size());
   const int sms = smCount(c.device);
   cudaStream_t s = c.stream;
+  // Exchanges overlap the transforms: the batch (basis x RHS) is cut into
+  // nch chunks; chunk k's all-to-all runs on the comm stream while chunk
+  // k+1 is row-transformed and packed (forward), and chunk k's inverse rows
+  // run while chunk k+1 comes back. K3 needs every basis index of a bin, so
+  // the chunks meet before it. Timed runs (tbt_set_timing) keep one chunk
+  // on the compute stream so the exchange time is the exposed one.
+  // TBT_DIST_CHUNKS=k forces k chunks (also with one rank; tests).
+  static const int forced = [] {
+    const char* e = getenv("TBT_DIST_CHUNKS");
+    return e ? std::max(1, std::min(4, atoi(e))) : 0;
+  }();
+  // Default: two chunks only when this rank's exchange is large enough for
+  // its transfer to outweigh the extra NCCL launch latency (>= 8 MB; one
+  // rank measured +30% on C2, +4.5% on C4, +1.2% on C5 from the chunking
+  // alone).
+  const double xbytes = static_cast<double>(c.myRows) * c.L0 * B * sizeof(double2);
+  int nch = (P > 1 && B >= 32 && xbytes >= 8.0 * (1 << 20)) ? 2 : 1;
+  if (forced) nch = forced;
+  if (c.timeBinprod || B % nch != 0) nch = 1;
+  const int Bc = B / nch;
+  cudaStream_t sc = nch > 1 ? c.commStream : s;
 
-  // 1. Row FFTs (level 0) of the local rows -> dTrow[r][s0][b].
-  FftPass fa;
-  fa.in = x;
-  fa.out = c.dTrow;
-  fa.lines = c.myRows;
-  fa.in_line_stride = static_cast<long long>(c.nx) * B;
-  fa.in_point_stride = B;
-  fa.out_line_stride = static_cast<long long>(c.L0) * B;
-  fa.out_point_stride = B;
-  fa.n = c.L0;
-  fa.n_in = c.nx;
-  fa.n_out = c.L0;
-  fa.batch = B;
-  fa.tw = c.dTw0;
-  launchFftPass(fa, s);
-
-  // 2. All-to-all: my rows x columns of q  ->  rank q.
-  std::vector<long long> sendOff(P + 1, 0), recvOff(P + 1, 0);
-  for (int q = 0; q < P; ++q) {
-    sendOff[q + 1] = static_cast<long long>(c.myRows) * c.colsOffset[q + 1] * B;
-    recvOff[q + 1] = recvOff[q] + static_cast<long long>(c.rowStart[q + 1] - c.rowStart[q]) * myCols * B;
-  }
-  {  // one launch packs the blocks of every peer
-    const long long cnt = static_cast<long long>(c.myRows) * c.L0 * B;
-    if (cnt > 0)
-      permuteColumns<true><<<gridFor(cnt, sms), 256, 0, s>>>(c.dTrow, c.dSend, c.myRows, c.L0, c.dColTab, B,
-                                                             static_cast<long long>(c.L0) * B);
+  auto rowFft = [&](int k) {  // 1. row FFTs (level 0) of the local rows -> dTrow[r][s0][b]
+    FftPass fa;
+    fa.in = x + static_cast<long long>(k) * Bc;
+    fa.out = c.dTrow + static_cast<long long>(k) * Bc;
+    fa.lines = c.myRows;
+    fa.in_line_stride = static_cast<long long>(c.nx) * B;
+    fa.in_point_stride = B;
+    fa.out_line_stride = static_cast<long long>(c.L0) * B;
+    fa.out_point_stride = B;
+    fa.n = c.L0;
+    fa.n_in = c.nx;
+    fa.n_out = c.L0;
+    fa.batch = Bc;
+    fa.tw = c.dTw0;
+    launchFftPass(fa, s);
+  };
+  // Chunk k's packed regions: send [q][row][j][b] at k * myRows*L0*Bc,
+  // receive / dTcol [r][j][b] at k * ny*myCols*Bc.
+  const long long sendChunk = static_cast<long long>(c.myRows) * c.L0 * Bc;
+  const long long recvChunk = static_cast<long long>(c.ny) * myCols * Bc;
+  auto sendOff = [&](int k, int q) { return k * sendChunk + static_cast<long long>(c.myRows) * c.colsOffset[q] * Bc; };
+  auto recvOff = [&](int k, int q) {
+    return k * recvChunk + static_cast<long long>(c.rowStart[q]) * myCols * Bc;
+  };
+  auto permute = [&](int k, bool gather) {
+    const long long cnt = static_cast<long long>(c.myRows) * c.L0 * Bc;
+    if (cnt == 0) return;
+    double2* grid = c.dTrow + static_cast<long long>(k) * Bc;
+    double2* packed = c.dSend + k * sendChunk;
+    if (gather)
+      permuteColumns<true><<<gridFor(cnt, sms), 256, 0, s>>>(grid, packed, c.myRows, c.L0, c.dColTab, Bc,
+                                                             static_cast<long long>(c.L0) * B, B);
+    else
+      permuteColumns<false><<<gridFor(cnt, sms), 256, 0, s>>>(packed, grid, c.myRows, c.L0, c.dColTab, Bc,
+                                                              static_cast<long long>(c.L0) * B, B);
     TBT_CUDA_CHECK(cudaGetLastError());
-  }
-  commSection(c, [&] {
-    c.comm->groupStart();
-    for (int q = 0; q < P; ++q) {
-      const size_t sc = static_cast<size_t>(sendOff[q + 1] - sendOff[q]) * 2;
-      const size_t rc = static_cast<size_t>(recvOff[q + 1] - recvOff[q]) * 2;
-      if (sc) c.comm->send(c.dSend + sendOff[q], sc, q, s);
-      if (rc) c.comm->recv(c.dRecv + recvOff[q], rc, q, s);
+  };
+  // 2. all-to-all of chunk k: my rows x columns of q -> rank q.
+  auto exchangeFwd = [&](int k) {
+    commSection(c, [&] {
+      c.comm->groupStart();
+      for (int q = 0; q < P; ++q) {
+        const size_t scount = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * Bc * 2;
+        const size_t rcount = static_cast<size_t>(c.rowStart[q + 1] - c.rowStart[q]) * myCols * Bc * 2;
+        if (scount) c.comm->send(c.dSend + sendOff(k, q), scount, q, sc);
+        if (rcount) c.comm->recv(c.dRecv + recvOff(k, q), rcount, q, sc);
+      }
+      c.comm->groupEnd(sc);
+    });
+  };
+  // 6. all-to-all back of chunk k: rows of rank q x my columns -> q.
+  auto exchangeBack = [&](int k) {
+    commSection(c, [&] {
+      c.comm->groupStart();
+      for (int q = 0; q < P; ++q) {
+        const size_t scount = static_cast<size_t>(c.rowStart[q + 1] - c.rowStart[q]) * myCols * Bc * 2;
+        const size_t rcount = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * Bc * 2;
+        if (scount) c.comm->send(c.dTcol + recvOff(k, q), scount, q, sc);
+        if (rcount) c.comm->recv(c.dSend + sendOff(k, q), rcount, q, sc);
+      }
+      c.comm->groupEnd(sc);
+    });
+  };
+  auto colFft = [&](int k, bool inverse) {  // 3. / 5. column FFTs of my columns
+    FftPass f;
+    const long long packed = k * recvChunk;
+    if (!inverse) {  // received [r][j][bc] -> xhat[s1][j][b]
+      f.in = c.dRecv + packed;
+      f.out = c.dXhat + static_cast<long long>(k) * Bc;
+      f.in_line_stride = Bc;
+      f.in_point_stride = static_cast<long long>(myCols) * Bc;
+      f.out_line_stride = B;
+      f.out_point_stride = static_cast<long long>(myCols) * B;
+      f.n_in = c.ny;
+      f.n_out = c.L1;
+      f.tw = c.dTw1;
+    } else {  // yhat[s1][j][b] -> dTcol [r][j][bc], keep the ny element rows
+      f.in = c.dYhat + static_cast<long long>(k) * Bc;
+      f.out = c.dTcol + packed;
+      f.in_line_stride = B;
+      f.in_point_stride = static_cast<long long>(myCols) * B;
+      f.out_line_stride = Bc;
+      f.out_point_stride = static_cast<long long>(myCols) * Bc;
+      f.n_in = c.L1;
+      f.n_out = c.ny;
+      f.inverse = 1;
+      f.tw = c.dTw1;
     }
-    c.comm->groupEnd(s);
-  });
-  // Received blocks are [rows of q][my columns][b] in row order: exactly
-  // dTcol[r][j][b] for r = 0..ny-1 (rank slabs are contiguous and ordered).
-  const double2* tcol = c.dRecv;
+    f.lines = myCols;
+    f.n = c.L1;
+    f.batch = Bc;
+    launchFftPass(f, s);
+  };
+  auto rowFftInv = [&](int k) {  // 7. inverse row FFTs, keep nx points, 1/L -> y slab
+    FftPass ia;
+    ia.in = c.dTrow + static_cast<long long>(k) * Bc;
+    ia.out = y + static_cast<long long>(k) * Bc;
+    ia.lines = c.myRows;
+    ia.in_line_stride = static_cast<long long>(c.L0) * B;
+    ia.in_point_stride = B;
+    ia.out_line_stride = static_cast<long long>(c.nx) * B;
+    ia.out_point_stride = B;
+    ia.n = c.L0;
+    ia.n_in = c.L0;
+    ia.n_out = c.nx;
+    ia.batch = Bc;
+    ia.inverse = 1;
+    ia.scale = 1.0 / static_cast<double>(c.L);
+    ia.tw = c.dTw0;
+    launchFftPass(ia, s);
+  };
+  auto handOff = [&](cudaStream_t from, cudaStream_t to, int ev) {
+    if (from == to) return;
+    TBT_CUDA_CHECK(cudaEventRecord(c.distEv[ev], from));
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(to, c.distEv[ev], 0));
+  };
 
-  // 3. Column FFTs (level 1) of my columns -> xhat_local[s1][j][b].
-  FftPass fb;
-  fb.in = tcol;
-  fb.out = c.dXhat;
-  fb.lines = myCols;
-  fb.in_line_stride = B;
-  fb.in_point_stride = static_cast<long long>(myCols) * B;
-  fb.out_line_stride = B;
-  fb.out_point_stride = static_cast<long long>(myCols) * B;
-  fb.n = c.L1;
-  fb.n_in = c.ny;
-  fb.n_out = c.L1;
-  fb.batch = B;
-  fb.tw = c.dTw1;
-  launchFftPass(fb, s);
-
-  // 4. Bin-pair products on the local pairs.
+  // Events: 0-3 pack done (k), 4-7 received (k); reused for the inverse
+  // (same stream order, so a reused event is never waited on stale).
+  // Forward: rows + pack of chunk k+1 overlap the exchange of chunk k.
+  for (int k = 0; k < nch; ++k) {
+    rowFft(k);
+    permute(k, true);
+    handOff(s, sc, k);
+    exchangeFwd(k);
+  }
+  for (int k = 0; k < nch; ++k) {
+    handOff(sc, s, 4 + k);
+    colFft(k, false);
+  }
+  // 4. Bin-pair products on the local pairs (every basis index of a bin).
   if (c.npairs > 0) launchBinProduct(c, nrhs);
-
-  // 5. Inverse column FFTs, keep the ny element rows -> dTcol[r][j][b].
-  FftPass ib;
-  ib.in = c.dYhat;
-  ib.out = c.dTcol;
-  ib.lines = myCols;
-  ib.in_line_stride = B;
-  ib.in_point_stride = static_cast<long long>(myCols) * B;
-  ib.out_line_stride = B;
-  ib.out_point_stride = static_cast<long long>(myCols) * B;
-  ib.n = c.L1;
-  ib.n_in = c.L1;
-  ib.n_out = c.ny;
-  ib.batch = B;
-  ib.inverse = 1;
-  ib.tw = c.dTw1;
-  launchFftPass(ib, s);
-
-  // 6. All-to-all back: rows of rank q x my columns -> q; from q: my rows x
-  //    columns of q.
-  commSection(c, [&] {
-    c.comm->groupStart();
-    for (int q = 0; q < P; ++q) {
-      const long long rows = c.rowStart[q + 1] - c.rowStart[q];
-      const size_t sc = static_cast<size_t>(rows) * myCols * B * 2;
-      const size_t rc = static_cast<size_t>(c.myRows) * c.colsOfRank[q].size() * B * 2;
-      if (sc) c.comm->send(c.dTcol + static_cast<long long>(c.rowStart[q]) * myCols * B, sc, q, s);
-      if (rc) c.comm->recv(c.dSend + sendOff[q], rc, q, s);
-    }
-    c.comm->groupEnd(s);
-  });
-  {
-    const long long cnt = static_cast<long long>(c.myRows) * c.L0 * B;
-    if (cnt > 0)
-      permuteColumns<false><<<gridFor(cnt, sms), 256, 0, s>>>(c.dSend, c.dTrow, c.myRows, c.L0, c.dColTab, B,
-                                                              static_cast<long long>(c.L0) * B);
-    TBT_CUDA_CHECK(cudaGetLastError());
+  // Inverse: the exchange back of chunk k overlaps the inverse columns of
+  // chunk k+1, then the inverse rows of chunk k the exchange of chunk k+1.
+  for (int k = 0; k < nch; ++k) {
+    colFft(k, true);
+    handOff(s, sc, k);
+    exchangeBack(k);
   }
-
-  // 7. Inverse row FFTs of my rows, keep nx points, 1/L -> y (local slab).
-  FftPass ia;
-  ia.in = c.dTrow;
-  ia.out = y;
-  ia.lines = c.myRows;
-  ia.in_line_stride = static_cast<long long>(c.L0) * B;
-  ia.in_point_stride = B;
-  ia.out_line_stride = static_cast<long long>(c.nx) * B;
-  ia.out_point_stride = B;
-  ia.n = c.L0;
-  ia.n_in = c.L0;
-  ia.n_out = c.nx;
-  ia.batch = B;
-  ia.inverse = 1;
-  ia.scale = 1.0 / static_cast<double>(c.L);
-  ia.tw = c.dTw0;
-  launchFftPass(ia, s);
+  for (int k = 0; k < nch; ++k) {
+    handOff(sc, s, 4 + k);
+    permute(k, false);
+    rowFftInv(k);
+  }
 
   // 8. Spatial terms: K (element-local) and the correction. A correction
   //    term couples an element with its 4-neighbours only, so one halo row

@@ -166,6 +166,8 @@ struct Ctx {
   bool dist = false;
   int nranks = 1, myRank = 0;
   Comm* comm = nullptr;
+  cudaStream_t commStream = nullptr;  // exchanges of the chunked (overlapped) sharded apply
+  cudaEvent_t distEv[8] = {};         // fork / join events between the compute and comm streams
   std::vector<int> rowStart;                  // [nranks+1]
   std::vector<std::vector<int>> colsOfRank;   // [nranks]
   std::vector<int> myColList;

@@ -94,8 +94,44 @@ def check_margin():
         assert rel(Y[:, c], ref) < 1e-11 and rel(op.apply(np.ascontiguousarray(X[:, c])), ref) < 1e-11
 
 
+def check_dist():
+    """Sharded apply + GMRES: one NCCL rank (exchanges to itself, captured in
+    a CUDA graph) and three loopback ranks, with the chunk count of the
+    overlapped exchanges forced by TBT_DIST_CHUNKS."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2506_04710_b200 import dist_unique_id, loopback_group_id
+    for (nx, ny, m), k in (((32, 32, 64), 1), ((6, 5, 64), 3), ((4, 4, 24), 1)):
+        rep = ToeplitzRep.synthetic(Config("d", nx, ny, m, 1, 4, 3, "normal", 20))
+        o = oracle.Oracle.from_rep(rep)
+        X = gen.rhs_normal(o.n, k, 5)
+        op = ToeplitzMatvec(rep, max_nrhs=k, dist=(1, 0, dist_unique_id()))
+        for _ in range(2):
+            Y = op.apply(X if k > 1 else X[:, 0]).reshape(o.n, k)
+            for c in range(k):
+                assert rel(Y[:, c], o.apply(np.ascontiguousarray(X[:, c]))) < 1e-11, ("nccl", nx, c)
+        opt = SolverOptions(tol=1e-8, maxIter=60, restart=15)
+        g = op.gmres(X, opt, raise_on_fail=False)
+        r = o.gmres(X, tol=1e-8, max_iter=60, restart=15)
+        assert g.iterations == r["iterations"], ("nccl gmres", g.iterations, r["iterations"])
+        op.close()
+        P = 3
+        gid = loopback_group_id()
+        ops = [ToeplitzMatvec(rep, max_nrhs=k, dist=(P, q, gid, "loopback")) for q in range(P)]
+        parts = []
+        for q in ops:
+            r0, r1 = q.rows()
+            parts.append(np.ascontiguousarray(X[r0 * nx * m:r1 * nx * m]))
+        with ThreadPoolExecutor(P) as ex:
+            Ys = list(ex.map(lambda q: ops[q].apply(parts[q] if k > 1 else parts[q][:, 0]), range(P)))
+        Y = np.concatenate([y.reshape(-1, k) for y in Ys], axis=0)
+        for c in range(k):
+            assert rel(Y[:, c], o.apply(np.ascontiguousarray(X[:, c]))) < 1e-11, ("loopback", nx, c)
+        for q in ops:
+            q.close()
+
+
 CHECKS = {"apply": check_apply, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin,
-          "wide": check_wide}
+          "wide": check_wide, "dist": check_dist}
 
 if __name__ == "__main__":
     for name in sys.argv[1:]:

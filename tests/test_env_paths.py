@@ -13,6 +13,8 @@ process per setting; the knobs are read once per process):
   TBT_FFT2D=2,4       cluster 2-D transform with a forced cluster / batch split
   TBT_E2E=staged      host applies through explicit copies, not zero-copy
   TBT_MARGIN_UNFUSED=1  separate margin B / B^T kernels for one column
+  TBT_DIST_CHUNKS=k   sharded apply with k overlapped exchange chunks
+                      (default 2 at P > 1, 1 at P = 1)
 """
 import os
 import subprocess
@@ -35,6 +37,9 @@ CASES = [
     ({"TBT_FFT2D": "2,4"}, ["smooth"]),
     ({"TBT_E2E": "staged"}, ["apply"]),
     ({"TBT_MARGIN_UNFUSED": "1"}, ["margin"]),
+    ({}, ["dist"]),
+    ({"TBT_DIST_CHUNKS": "2"}, ["dist"]),
+    ({"TBT_DIST_CHUNKS": "4"}, ["dist"]),
 ]
 
 
