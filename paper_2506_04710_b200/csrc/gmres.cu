@@ -274,10 +274,15 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiLS(GmresArgs A, double2*
 //           sub-chunk order and are summed over the warps in warp order
 //   -- barrier --  every CTA reduces every dot, forward substitution
 //   pass 2  w' = M w - V h written to v_{j+1} unnormalised, ||w'||^2
-//           (4 rows per thread, 8 vectors unrolled: 32 loads in flight)
+//           (4 rows per thread, 8 vectors unrolled: 32 loads in flight),
+//           row blocks in reverse order so the first ones hit what pass 1
+//           left in L2 (C5: 4.20 -> 4.18 ms per iteration)
 //   -- barrier --  v_{j+1} /= ||w'|| (the chunk rereads its own rows, L2),
 //                  Givens (CTA 0)
-// All sums are fixed-order: bitwise reproducible.
+// All sums are fixed-order: bitwise reproducible. Measured alternatives
+// (C4, same box): a bulk-copy ring for pass 1 (tiles w, v_j, v_k through
+// shared memory, warp-owned row slices) 0.533 vs 0.520 ms per iteration;
+// (vector, segment) work items with register accumulators 0.545.
 constexpr int kBigSub = 2048;
 constexpr int kBigRowsPerLane = kBigSub / (kWarps * 32);  // 8
 constexpr int kBigVec = 4;                                 // basis vectors per sweep step
@@ -438,7 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) gmresArnoldiLSBig(GmresArgs A, do
   double2 acc = make_double2(0.0, 0.0);
   const int bd = static_cast<int>(blockDim.x);
   constexpr int RT = 4;
-  for (long long ra = threadIdx.x; ra < cnt; ra += RT * bd) {
+  const long long nblk = (cnt + RT * bd - 1) / (RT * bd);
+  for (long long bi = nblk - 1; bi >= 0; --bi) {  // reverse: pass 1's last rows are still in L2
+    const long long ra = bi * RT * bd + threadIdx.x;
     double2 wr[RT];
     long long rs[RT];
 #pragma unroll
