@@ -7,6 +7,8 @@
 // S3 += (Ar + Ai)(Br + Bi); Re = S1 - S2, Im = S3 - S1 - S2 at the end. The
 // kernel is DMMA-bound, so this removes a quarter of its work; the extra
 // rounding is a few ulps of |A||X| (the matvec parity bound is 1e-11).
+// TBT_GEMM=4m selects the 4M form (Re += Ar Br + (-Ai) Bi, Im += Ar Bi +
+// Ai Br: four DMMAs, two accumulator sets) for comparison.
 // The reference re-streams every block once per column
 // (linsolve.cpp:276-282, 572).
 //
@@ -15,6 +17,8 @@
 // of 32 through a cp.async double buffer: the A chunk (M x 32 for A, or the
 // 32 contiguous rows of A for A^T) and the X chunk (32 x NTILE).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "tbt_internal.cuh"
 
@@ -56,7 +60,7 @@ struct GemmCfg {
 };
 
 // item = ((p * 2 + t) * nTiles + tile); t = 1 is the transposed product.
-template <int M>
+template <int M, bool FOURM>
 __global__ void __launch_bounds__(NT, 1)
 binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
             long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int nrhs) {
@@ -80,13 +84,14 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
     double2* Y = yhat + static_cast<long long>(bin) * B;
     const int n0 = tile * NTILE;
 
-    double acc[C::MB][NB][3][2];  // [mblock][nblock][S1/S2/S3][c0/c1]
+    constexpr int NACC = FOURM ? 2 : 3;
+    double acc[C::MB][NB][NACC][2];  // [mblock][nblock][S1/S2/S3 or Re/Im][c0/c1]
 #pragma unroll
     for (int a = 0; a < C::MB; ++a)
 #pragma unroll
       for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) acc[a][b][q][0] = acc[a][b][q][1] = 0.0;
+        for (int q = 0; q < NACC; ++q) acc[a][b][q][0] = acc[a][b][q][1] = 0.0;
 
     auto load = [&](int kc, int stage) {
       double2* sA = gsm + stage * C::STAGE;
@@ -129,22 +134,29 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
           const double2 v = t == 0 ? sA[i * (KC + PADC) + kk + tig] : sA[(kk + tig) * M + i];
           ar[a] = v.x;
           ai[a] = v.y;
-          as[a] = v.x + v.y;
+          as[a] = FOURM ? -v.y : v.x + v.y;  // 4M: the negated imaginary part
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           const double2 v = sB[(b * 8 + gid) * (KC + PADC) + kk + tig];
           br[b] = v.x;
           bi[b] = v.y;
-          bs[b] = v.x + v.y;
+          if (!FOURM) bs[b] = v.x + v.y;
         }
 #pragma unroll
         for (int a = 0; a < C::MB; ++a) {
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
-            dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
-            dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
+            if (FOURM) {
+              dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+              dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+              dmma(acc[a][b][0][0], acc[a][b][0][1], as[a], bi[b]);
+              dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+            } else {
+              dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+              dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+              dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
+            }
           }
         }
       }
@@ -159,33 +171,48 @@ binprodGemm(const double2* __restrict__ S, const int* __restrict__ pairF, const 
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int n = n0 + b * 8 + 2 * tig + h;
-          const double s1 = acc[a][b][0][h], s2 = acc[a][b][1][h], s3 = acc[a][b][2][h];
-          if (n < nrhs) Y[static_cast<long long>(n) * M + i] = make_double2(s1 - s2, s3 - s1 - s2);
+          if (n >= nrhs) continue;
+          if (FOURM) {
+            Y[static_cast<long long>(n) * M + i] = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+          } else {
+            const double s1 = acc[a][b][0][h], s2 = acc[a][b][1][h], s3 = acc[a][b][NACC - 1][h];
+            Y[static_cast<long long>(n) * M + i] = make_double2(s1 - s2, s3 - s1 - s2);
+          }
         }
     }
   }
 }
 
-template <int M>
+template <int M, bool FOURM>
 void launchGemm(Ctx& c, int nrhs) {
   using C = GemmCfg<M>;
   static std::atomic<unsigned long long> attr{0};
   oncePerDevice(attr, [] {
-    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm<M, FOURM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(C::SMEM)));
   });
   const int nTiles = (nrhs + NTILE - 1) / NTILE;
   const long long items = c.npairs * 2 * nTiles;
   const int grid = static_cast<int>(std::min<long long>(items, 16LL * smCount(c.device)));
-  binprodGemm<M><<<grid, NT, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, nrhs);
+  binprodGemm<M, FOURM>
+      <<<grid, NT, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG, c.npairs, c.dXhat, c.dYhat, nrhs);
+}
+
+bool gemm4m() {
+  static const bool on = [] {
+    const char* e = getenv("TBT_GEMM");
+    return e && strcmp(e, "4m") == 0;
+  }();
+  return on;
 }
 
 }  // namespace
 
 bool launchBinProductGemm(Ctx& c, int nrhs) {
+  const bool four = gemm4m();
   switch (c.m) {
-    case 64: launchGemm<64>(c, nrhs); break;
-    case 128: launchGemm<128>(c, nrhs); break;
+    case 64: four ? launchGemm<64, true>(c, nrhs) : launchGemm<64, false>(c, nrhs); break;
+    case 128: four ? launchGemm<128, true>(c, nrhs) : launchGemm<128, false>(c, nrhs); break;
     default: return false;
   }
   TBT_CUDA_CHECK(cudaGetLastError());
