@@ -607,12 +607,28 @@ def main():
         for _ in range(ke):
             st = lib().tbt_apply(op._h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()), 1, TBT_HOST)
             assert st == 0
+        e2e_single_s = time.perf_counter() - t0
+        # Streamed: tbt_apply_many over batches of distinct pinned host
+        # vectors; every vector's H2D copy, apply and D2H copy is inside the
+        # timed region, consecutive vectors overlap on the copy engines.
+        nb = 64
+        xs_many = torch.from_numpy(np.ascontiguousarray(gen.rhs_normal(cfg.n, nb, 77).T)).pin_memory()
+        ys_many = torch.empty_like(xs_many).pin_memory()
+        op.apply_many_ptr(xs_many.data_ptr(), ys_many.data_ptr(), nb)  # warm-up (slot allocation)
+        ref_y = ys_many[3].numpy().copy()
+        barrier()
+        calls = max(1, ke // nb)
+        t0 = time.perf_counter()
+        for _ in range(calls):
+            op.apply_many_ptr(xs_many.data_ptr(), ys_many.data_ptr(), nb)
         e2e_s = time.perf_counter() - t0
+        assert np.array_equal(ys_many[3].numpy(), ref_y)  # same vector, same bits every call
         if dist is not None:
-            t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+            t = torch.tensor([e2e_s, e2e_single_s], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = world * ke / e2e_s
+            e2e_s, e2e_single_s = (float(v) for v in t.tolist())
+        e2e = world * calls * nb / e2e_s
+        e2e_single = world * ke / e2e_single_s
 
         # ---- GMRES: fixed budget (C2 stalls under GMRES(50)+Jacobi)
         gm = None
@@ -695,7 +711,11 @@ def main():
         "roofline": roof,
         "equivalent_full_spectrum_gbs": b_alg_full / (step_mean * 1e-3) / 1e9,
         "cold_l2_ms_per_step": cold_ms,
-        "e2e": {"value": e2e, "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16, "d2h_bytes_per_step": cfg.n * 16},
+        "e2e": {"value": e2e, "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16, "d2h_bytes_per_step": cfg.n * 16,
+                "mode": "tbt_apply_many: batches of 64 distinct pinned host vectors; per vector H2D copy, apply, "
+                        "D2H copy, overlapped across vectors on the copy engines; host wall clock",
+                "single_call_value": e2e_single,
+                "single_call_mode": "tbt_apply(TBT_HOST) per vector: zero-copy persistent kernel + stream sync"},
         "gpu_launches": K * info.kernels_per_apply,
         "clocks": clocks.summary(),
         "gmres": gm,

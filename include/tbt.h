@@ -134,6 +134,16 @@ tbt_status tbt_precompute(tbt_ctx* ctx);
  * (x, y) pointer pair. */
 tbt_status tbt_apply(tbt_ctx* ctx, const double* x, double* y, int nrhs,
                      int where);
+/* y_i = Z x_i for `count` independent single-column vectors in HOST
+ * memory (x: count consecutive length-n vectors, y likewise), e.g. a batch
+ * of excitations or a stream of requests. The host-to-device copy of
+ * x_{i+1}, the apply of x_i and the device-to-host copy of y_{i-1} overlap
+ * (two device slots, copy streams next to the context stream); returns
+ * when every y_i is in host memory. Same results as count calls of
+ * tbt_apply(ctx, x_i, y_i, 1, TBT_HOST); overlap needs pinned host memory
+ * (pageable memory works but serialises). Single-GPU contexts without
+ * margin parts. */
+tbt_status tbt_apply_many(tbt_ctx* ctx, const double* x, double* y, long long count);
 /* y = A x (pure two-level block-Toeplitz part). */
 tbt_status tbt_apply_a(tbt_ctx* ctx, const double* x, double* y, int nrhs,
                        int where);

@@ -53,6 +53,7 @@ SIGNATURES = {
     "tbt_set_correction": (C.c_int, [C.c_void_p, C.c_int, dp, dp, dp]),
     "tbt_precompute": (C.c_int, [C.c_void_p]),
     "tbt_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "tbt_apply_many": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong]),
     "tbt_apply_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "tbt_apply_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "tbt_apply_bt": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),

@@ -422,6 +422,14 @@ void tbt_destroy(tbt_ctx* h) {
   marginFree(c);
   clusterSmallFree(c);
   freeGmresWorkspace(c);
+  for (int k = 0; k < 2; ++k) {
+    freePtr(c.dManyX[k]);
+    freePtr(c.dManyY[k]);
+  }
+  for (cudaEvent_t e : c.manyEv)
+    if (e) cudaEventDestroy(e);
+  if (c.manyIn) cudaStreamDestroy(c.manyIn);
+  if (c.manyOut) cudaStreamDestroy(c.manyOut);
   for (auto e : c.tEvA) cudaEventDestroy(e);
   for (auto e : c.tEvB) cudaEventDestroy(e);
   if (c.evBinA) cudaEventDestroy(c.evBinA);
@@ -828,6 +836,52 @@ static tbt_status applyCommon(tbt_ctx* h, const double* x, double* y, int nrhs, 
 
 tbt_status tbt_apply(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {
   return applyCommon(h, x, y, nrhs, where, true);
+}
+
+tbt_status tbt_apply_many(tbt_ctx* h, const double* x, double* y, long long count) {
+  return guardedCtx(h, [&] {
+    TBT_USER_CHECK(h && (count == 0 || (x && y)) && count >= 0, "tbt_apply_many: bad argument");
+    Ctx& c = h->c;
+    requireReady(c);
+    TBT_USER_CHECK(!c.dist && !c.margin, "tbt_apply_many: single-GPU operator without margin parts only");
+    TBT_CUDA_CHECK(cudaSetDevice(c.device));
+    if (count == 0) return;
+    const size_t bytes = static_cast<size_t>(c.n) * sizeof(double2);
+    if (!c.manyIn) {
+      for (int k = 0; k < 2; ++k) {
+        TBT_CUDA_CHECK(cudaMalloc(&c.dManyX[k], bytes));
+        TBT_CUDA_CHECK(cudaMalloc(&c.dManyY[k], bytes));
+      }
+      for (cudaEvent_t& e : c.manyEv) TBT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.manyIn, cudaStreamNonBlocking));
+      TBT_CUDA_CHECK(cudaStreamCreateWithFlags(&c.manyOut, cudaStreamNonBlocking));
+    }
+    // Everything earlier on the context stream (previous applies that may
+    // still read a slot) precedes the first copy.
+    TBT_CUDA_CHECK(cudaEventRecord(c.manyEv[2], c.stream));
+    TBT_CUDA_CHECK(cudaEventRecord(c.manyEv[3], c.stream));
+    TBT_CUDA_CHECK(cudaStreamWaitEvent(c.manyIn, c.manyEv[2], 0));
+    const char* xh = reinterpret_cast<const char*>(x);
+    char* yh = reinterpret_cast<char*>(y);
+    for (long long i = 0; i < count; ++i) {
+      const int k = static_cast<int>(i & 1);
+      // x_i -> slot k once the apply of i-2 has finished reading it
+      if (i >= 2) TBT_CUDA_CHECK(cudaStreamWaitEvent(c.manyIn, c.manyEv[2 + k], 0));
+      TBT_CUDA_CHECK(cudaMemcpyAsync(c.dManyX[k], xh + i * bytes, bytes, cudaMemcpyHostToDevice, c.manyIn));
+      TBT_CUDA_CHECK(cudaEventRecord(c.manyEv[k], c.manyIn));
+      // apply i once x_i landed and y slot k was read back (i-2)
+      TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.manyEv[k], 0));
+      if (i >= 2) TBT_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.manyEv[4 + k], 0));
+      runApply1(c, c.dManyX[k], c.dManyY[k], true);
+      TBT_CUDA_CHECK(cudaEventRecord(c.manyEv[2 + k], c.stream));
+      // y_i back to the host on the outbound copy engine
+      TBT_CUDA_CHECK(cudaStreamWaitEvent(c.manyOut, c.manyEv[2 + k], 0));
+      TBT_CUDA_CHECK(cudaMemcpyAsync(yh + i * bytes, c.dManyY[k], bytes, cudaMemcpyDeviceToHost, c.manyOut));
+      TBT_CUDA_CHECK(cudaEventRecord(c.manyEv[4 + k], c.manyOut));
+    }
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.manyOut));
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
 }
 
 tbt_status tbt_apply_a(tbt_ctx* h, const double* x, double* y, int nrhs, int where) {

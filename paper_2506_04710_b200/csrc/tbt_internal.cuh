@@ -165,6 +165,12 @@ struct Ctx {
   // s0 -> L0 - s0, so both bins of every stored pair are local).
   bool dist = false;
   int nranks = 1, myRank = 0;
+  // tbt_apply_many: two device slots per direction, copy streams and the
+  // events that order H2D -> apply -> D2H per slot (allocated on first use).
+  double2* dManyX[2] = {nullptr, nullptr};
+  double2* dManyY[2] = {nullptr, nullptr};
+  cudaStream_t manyIn = nullptr, manyOut = nullptr;
+  cudaEvent_t manyEv[6] = {};  // [0..1] x landed, [2..3] apply done, [4..5] y read back
   Comm* comm = nullptr;
   cudaStream_t commStream = nullptr;  // exchanges of the chunked (overlapped) sharded apply
   cudaEvent_t distEv[8] = {};         // fork / join events between the compute and comm streams

@@ -288,6 +288,22 @@ class ToeplitzMatvec:
     def applyA(self, x):
         return self._apply(lib().tbt_apply_a, x, self.sizeA())
 
+    def apply_many(self, X) -> np.ndarray:
+        """Z x_i for a batch of independent vectors, X of shape (count, n)
+        (one vector per row); host copies overlap the applies
+        (tbt_apply_many). Pageable numpy memory serialises the copies: pass
+        pinned buffers to apply_many_ptr for the overlapped stream."""
+        X = np.ascontiguousarray(X, dtype=np.complex128)
+        if X.ndim != 2 or X.shape[1] != self.size():
+            raise ValueError(f"apply_many: X must have shape (count, {self.size()})")
+        Y = np.empty_like(X)
+        _check(lib().tbt_apply_many(self._h, X.ctypes.data, Y.ctypes.data, X.shape[0]))
+        return Y
+
+    def apply_many_ptr(self, x_ptr: int, y_ptr: int, count: int) -> None:
+        """tbt_apply_many on host pointers (e.g. pinned torch tensors)."""
+        _check(lib().tbt_apply_many(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), count))
+
     def applyB(self, xA):
         """yM = B xA (linsolve.hpp:66, linsolve.cpp:292-314)."""
         return self._apply(lib().tbt_apply_b, xA, self.sizeA(), self.sizeM())

@@ -13,6 +13,7 @@ process per setting; the knobs are read once per process):
   TBT_FFT2D=2,4       cluster 2-D transform with a forced cluster / batch split
   TBT_E2E=staged      host applies through explicit copies, not zero-copy
   TBT_MARGIN_UNFUSED=1  separate margin B / B^T kernels for one column
+  TBT_GEMM=4m         4M complex DMMA GEMM for many right-hand sides
   TBT_DIST_CHUNKS=k   sharded apply with k overlapped exchange chunks
                       (default 2 at P > 1, 1 at P = 1)
 """
@@ -37,6 +38,7 @@ CASES = [
     ({"TBT_FFT2D": "2,4"}, ["smooth"]),
     ({"TBT_E2E": "staged"}, ["apply"]),
     ({"TBT_MARGIN_UNFUSED": "1"}, ["margin"]),
+    ({"TBT_GEMM": "4m"}, ["wide", "smooth"]),
     ({}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "2"}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "4"}, ["dist"]),
