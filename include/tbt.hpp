@@ -88,6 +88,23 @@ class ToeplitzMatvec {
   Vector applyB(const Vector& xA) const { return run(tbt_apply_b, xA, sizeA(), sizeM()); }   // linsolve.hpp:66
   Vector applyBT(const Vector& xM) const { return run(tbt_apply_bt, xM, sizeM(), sizeA()); } // linsolve.hpp:67
   Vector applyC(const Vector& xM) const { return run(tbt_apply_c, xM, sizeM(), sizeM()); }   // linsolve.hpp:68
+  // Many independent applies on host vectors, copies overlapped with the
+  // applies (tbt_apply_many; the reference runs them one column per thread,
+  // linsolve.cpp:572). Each vector must have length size().
+  std::vector<Vector> applyMany(const std::vector<Vector>& xs) const {
+    const long n = sizeA();
+    std::vector<Complex> xb(static_cast<size_t>(n) * xs.size()), yb(xb.size());
+    for (size_t i = 0; i < xs.size(); ++i) {
+      if (static_cast<long>(xs[i].size()) != n) throw UserError("applyMany: vector length mismatch");
+      std::copy(xs[i].begin(), xs[i].end(), xb.begin() + static_cast<long>(i) * n);
+    }
+    check(tbt_apply_many(ctx_, reinterpret_cast<const double*>(xb.data()), reinterpret_cast<double*>(yb.data()),
+                         static_cast<long long>(xs.size())));
+    std::vector<Vector> ys;
+    for (size_t i = 0; i < xs.size(); ++i)
+      ys.emplace_back(yb.begin() + static_cast<long>(i) * n, yb.begin() + static_cast<long>(i + 1) * n);
+    return ys;
+  }
   Vector diagonal() const {                                                      // linsolve.hpp:69
     Vector d(static_cast<size_t>(size()));
     check(tbt_diagonal(ctx_, reinterpret_cast<double*>(d.data())));

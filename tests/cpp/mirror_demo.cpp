@@ -1,7 +1,7 @@
 // Drives the C++ mirror include/tbt.hpp the way a reference caller would
 // (tbt::ToeplitzMatvec / tbt::iterativeSolve in place of arraymom's),
 // linked against the product library: config C1 generators from tbt_gen.h,
-// one apply and one GMRES(30) solve. Writes x, A x and the solution as raw
+// one apply (also through applyMany) and one GMRES(30) solve. Writes x, A x and the solution as raw
 // complex128 to argv[1] for tests/test_abi.py to check against the oracle.
 // Without a usable device the constructor throws tbt::DeviceError: the demo
 // prints "no device" and exits 0 (there is no CPU fallback).
@@ -22,6 +22,11 @@ int main(int argc, char** argv) {
     tbt::Vector x(static_cast<size_t>(op.size()));
     tbtgen_rhs_normal(op.size(), 1, 42, reinterpret_cast<double*>(x.data()));
     const tbt::Vector y = op.apply(x);
+    const std::vector<tbt::Vector> ys = op.applyMany({x, y, x});
+    if (ys.size() != 3 || ys[0] != y || ys[2] != y) {
+      std::printf("applyMany mismatch\n");
+      return 1;
+    }
     tbt::SolverOptions opt;
     opt.restart = 30;
     const tbt::SolveResult r = tbt::iterativeSolve(op, {x}, opt);
