@@ -89,6 +89,7 @@ SIGNATURES = {
     "tbt_dist_rows": (C.c_int, [C.c_void_p, ip, ip]),
     "tbt_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, ip, ip, ip, ip]),
     "tbt_phase_times": (C.c_int, [C.c_void_p, C.c_int, dp]),
+    "tbt_cta_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_longlong, llp]),
     "tbt_timing_read": (C.c_int, [C.c_void_p, dp, ip]),
     "tbtgen_num_blocks": (C.c_longlong, [C.c_int, C.c_int]),
     "tbtgen_block_shift": (C.c_int, [C.c_int, C.c_int, C.c_longlong, ip, ip]),

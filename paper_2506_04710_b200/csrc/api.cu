@@ -373,6 +373,11 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       }
       TBT_CUDA_CHECK(cudaMalloc(&c.dPhaseNs, 32 * sizeof(unsigned long long)));
       memsetSync(c.dPhaseNs, 0, 32 * sizeof(unsigned long long), c.stream);
+      if (const char* tenv = getenv("TBT_CTATRACE"); tenv && tenv[0] == '1') {
+        const size_t nb = static_cast<size_t>(kCtaTraceSlots) * kCtaTraceEvents * kCtaTraceMaxGrid * 8;
+        TBT_CUDA_CHECK(cudaMalloc(&c.dCtaTrace, nb));
+        memsetSync(c.dCtaTrace, 0, nb, c.stream);
+      }
       const char* aenv = getenv("TBT_APPLY");
       c.persistent = !(aenv && std::string(aenv) == "multi");
       const char* penv = getenv("TBT_PREFETCH");
@@ -415,6 +420,7 @@ void tbt_destroy(tbt_ctx* h) {
                   static_cast<void*>(c.dXhat), static_cast<void*>(c.dYhat), static_cast<void*>(c.dXin),
                   static_cast<void*>(c.dYout), static_cast<void*>(c.dDiagInv), static_cast<void*>(c.dDiagInvA),
                   static_cast<void*>(c.dGridBar), static_cast<void*>(c.dPhaseNs), static_cast<void*>(c.dBarFlags),
+                  static_cast<void*>(c.dCtaTrace),
                   static_cast<void*>(c.dGen)})
     freePtr(p);
   c.dropGraph();
@@ -1510,6 +1516,19 @@ tbt_status tbt_phase_times(tbt_ctx* h, int on, double* out_us) {
     for (int k = 16; k < 24; ++k) init[k] = ~0ULL;
     uploadSync(c.dPhaseNs, init.data(), 32 * sizeof(unsigned long long), c.stream);
     c.phaseTiming = on != 0;
+  });
+}
+
+tbt_status tbt_cta_trace(tbt_ctx* h, unsigned long long* out, long long cap, long long* launches) {
+  return guardedCtx(h, [&] {
+    TBT_USER_CHECK(h && out && launches, "tbt_cta_trace: bad argument");
+    Ctx& c = h->c;
+    TBT_USER_CHECK(c.dCtaTrace, "tbt_cta_trace: tracing is off (set TBT_CTATRACE=1 before tbt_create)");
+    const long long n = static_cast<long long>(kCtaTraceSlots) * kCtaTraceEvents * kCtaTraceMaxGrid;
+    TBT_USER_CHECK(cap >= n, "tbt_cta_trace: buffer too small");
+    TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    TBT_CUDA_CHECK(cudaMemcpy(out, c.dCtaTrace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    *launches = c.ctaTraceLaunches;
   });
 }
 

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) gmresArnoldiLS(GmresArgs A, double2*
   __shared__ double2 scratch[kWarps];
   __shared__ double2 hcol[RMAX + 2];
   __shared__ double2 sh[3 * RMAX + 4];
-  arnoldiLS(A, S, dots, dotPart, shw, scratch, hcol, sh, A.bar);
+  arnoldiLS(A, A.j, S, dots, dotPart, shw, scratch, hcol, sh, A.bar);
 }
 
 // One Arnoldi step j, single column, low-synchronisation MGS, for vectors
@@ -1433,7 +1433,14 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     // (restart x [apply, Arnoldi]); every node turns into a no-op once the
     // column's inner loop stopped (device flag), so the host synchronises
     // once per restart cycle.
-    const bool useGraph = ncols == 1 && !c.timeBinprod && !c.dist && !withMargin;
+    // Fused single column: the whole inner loop of a cycle is ONE persistent
+    // launch (matvec_persistent.cu, apply + Arnoldi per column, the Givens
+    // stop decision read back on the device), unless the shape is not
+    // instantiated or TBT_GMRES=graph asks for the captured graph of per-column
+    // launches.
+    static const bool graphEnv = getenv("TBT_GMRES") && std::string(getenv("TBT_GMRES")) == "graph";
+    bool cycleKernel = fuse && ncols == 1 && !withMargin && !graphEnv && persistentSupported(c);
+    const bool useGraph = !cycleKernel && ncols == 1 && !c.timeBinprod && !c.dist && !withMargin;
     GmresArgs keyA = A;  // what the captured nodes bake in (b, x unused by them)
     keyA.b = nullptr;
     keyA.x = nullptr;
@@ -1472,7 +1479,18 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
           cols.cycleStart();
         else
           coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
-        if (useGraph) {
+        bool cycleDone = false;
+        if (cycleKernel) {
+          pull();
+          cycleDone = true;
+          if (st[0].cycleActive && !st[0].stopInner) {
+            A.j = 0;
+            cycleDone = launchPersistentApply(c, A.V, A.w, !useAOnly, &A, lsS, lsDots, lsPart, true);
+            cycleKernel = cycleDone;  // LS scratch does not fit next to the ring: per-column launches
+          }
+        }
+        if (cycleDone) {
+        } else if (useGraph) {
           // The cycle start may have ended the solve (budget or tolerance
           // reached): then the 'restart' no-op nodes are not worth a launch.
           pull();

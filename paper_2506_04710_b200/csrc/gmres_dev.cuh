@@ -161,17 +161,16 @@ __device__ inline void givensStage(const GmresArgs& A, int col, int j, const dou
   }
 }
 
-// Needs givensStage's shared-memory staging visible (a __syncthreads after it).
-__device__ inline void givensFinish(const GmresArgs& A, int col, int j, double hn, double2* sh) {
-  const int ldh = A.restart + 1;
-  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+// The sequential part of the Givens step (one thread): rotations 0..j-1 on
+// the staged column, the new rotation, g, the state and the stop decision.
+__device__ inline void givensCore(const GmresArgs& A, int col, int j, double hn, double2* sh) {
   double2* cs = A.cs + static_cast<long long>(col) * A.restart;
   double2* sn = A.sn + static_cast<long long>(col) * A.restart;
   double2* g = A.g + static_cast<long long>(col) * (A.restart + 1);
   double2* hc = sh;
   double2* scs = sh + RMAX + 2;
   double2* ssn = scs + RMAX;
-  if (threadIdx.x == 0) {
+  {
     GmresState& st = A.st[col];
     // Global state the tail needs, loaded before the sequential sweep so
     // the loads overlap it.
@@ -210,9 +209,39 @@ __device__ inline void givensFinish(const GmresArgs& A, int col, int j, double h
     pushHist(A, col, 1.0, cabs2(gj1) / beta0);
     if (rel < 0.1 * A.tol || !(hn > 0.0) || j + 1 >= A.restart || iters + 1 >= A.maxIter) st.stopInner = 1;
   }
+}
+
+// Needs givensStage's shared-memory staging visible (a __syncthreads after it).
+__device__ inline void givensFinish(const GmresArgs& A, int col, int j, double hn, double2* sh) {
+  const int ldh = A.restart + 1;
+  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+  if (threadIdx.x == 0) givensCore(A, col, j, hn, sh);
   __syncthreads();
-  for (int t = threadIdx.x; t <= j + 1; t += blockDim.x) H[t + j * ldh] = hc[t];
+  for (int t = threadIdx.x; t <= j + 1; t += blockDim.x) H[t + j * ldh] = sh[t];
   __syncthreads();
+}
+
+// The whole Givens step of column j on ONE warp (the restart-cycle kernel's
+// auxiliary warp), the unrotated column read from H (written by the LS step
+// of column j), sh: 3*RMAX+4 entries of this warp's shared memory.
+__device__ inline void givensWarp(const GmresArgs& A, int col, int j, double hn, double2* sh) {
+  const int lane = threadIdx.x & 31;
+  const int ldh = A.restart + 1;
+  double2* H = A.H + static_cast<long long>(col) * ldh * A.restart;
+  const double2* cs = A.cs + static_cast<long long>(col) * A.restart;
+  const double2* sn = A.sn + static_cast<long long>(col) * A.restart;
+  double2* scs = sh + RMAX + 2;
+  double2* ssn = scs + RMAX;
+  for (int t = lane; t <= j; t += 32) sh[t] = __ldcg(H + t + j * ldh);
+  for (int t = lane; t < j; t += 32) {
+    scs[t] = __ldcg(cs + t);
+    ssn[t] = __ldcg(sn + t);
+  }
+  __syncwarp();
+  if (lane == 0) givensCore(A, col, j, hn, sh);
+  __syncwarp();
+  for (int t = lane; t <= j + 1; t += 32) H[t + j * ldh] = sh[t];
+  __syncwarp();
 }
 
 __device__ inline void givensStep(const GmresArgs& A, int col, int j, double hn, const double2* hcolIn,
@@ -272,16 +301,28 @@ __device__ __forceinline__ void forwardSubstWarp(double2* cv, const double2* sL,
 // (`dots` is unused since the totals stay in shared memory.)
 // shw: dynamic shared memory of arnoldiLSSmem(chunk) double2; scratch:
 // blockDim/32 entries; hcol: RMAX+2; sh: 3*RMAX+4.
-__device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, double2* dotPart, double2* shw,
-                          double2* scratch, double2* hcol, double2* sh, unsigned long long* bar) {
-  const int run = A.st[0].cycleActive && !A.st[0].stopInner;
+//
+// Lagged normalisation (lagged = true, the restart-cycle kernel): v_j arrives
+// unnormalised (w' of the previous step) with its norm hnPrev known since the
+// step's first grid barrier; the staging divides it by hnPrev and writes the
+// normalised rows back, pass 2 stores w' unnormalised straight into v_{j+1}
+// and publishes the CTA's ||w'||^2 partial; the w' norm, v_{j+1}'s
+// normalisation and the Givens step of column j move into the next step (no
+// third grid barrier, no normalisation pass). The unrotated column h is left
+// in H(:, j) for that Givens step.
+__device__ inline void arnoldiLS(const GmresArgs& A, int j, double2* S, double2* dots, double2* dotPart, double2* shw,
+                          double2* scratch, double2* hcol, double2* sh, unsigned long long* bar,
+                          bool lagged = false, double hnPrev = 1.0) {
+  // Written by CTA 0 before a grid barrier (or before this launch): read
+  // through L1 (the persistent restart-cycle loop re-reads it per column).
+  const volatile GmresState* stv = A.st;
+  const int run = stv->cycleActive && !stv->stopInner;
   if (!run) return;  // uniform over the grid
   unsigned long long pt[5] = {0, 0, 0, 0, 0};
   auto mark = [&](int k) {
     if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt[k]));
   };
   mark(0);
-  const int j = A.j;
   const int lds = A.restart + 1;
   const long long n = static_cast<long long>(A.ne) * A.m;
   const long long chunk = (n + gridDim.x - 1) / gridDim.x;
@@ -292,11 +333,17 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   double2* cv = vj + chunk;  // [j+1] totals of c, later h
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double2* Vj = A.V + static_cast<long long>(j) * n;
+  const bool rescale = lagged && hnPrev != 1.0;
   for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
     double2 wv = A.w[r0 + r];
     if (A.dinv) wv = cmul(wv, A.dinv[r0 + r]);
     ws[r] = wv;
-    vj[r] = Vj[r0 + r];
+    double2 vv = __ldcg(Vj + r0 + r);
+    if (rescale) {
+      vv = make_double2(vv.x / hnPrev, vv.y / hnPrev);
+      A.V[static_cast<long long>(j) * n + r0 + r] = vv;
+    }
+    vj[r] = vv;
   }
   __syncthreads();
   // Pass 1: warp w owns dots k = w, w + nw, ...; it takes them two at a
@@ -310,14 +357,16 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
       const bool two = k1 <= j;
       const double2* V0 = A.V + static_cast<long long>(k0) * n + r0;
       const double2* V1 = A.V + static_cast<long long>(two ? k1 : k0) * n + r0;
+      // Lagged: v_j's rows were just rewritten (normalised) by this CTA: read them from vj.
+      const bool sm0 = lagged && k0 == j, sm1 = lagged && two && k1 == j;
       double2 c0 = make_double2(0.0, 0.0), c1 = c0, s0 = c0, s1 = c0;
       for (int r = lane; r < cnt; r += 32 * U1) {
         double2 v0[U1], v1[U1];
 #pragma unroll
         for (int u = 0; u < U1; ++u) {
           const int rr = r + 32 * u;
-          v0[u] = rr < cnt ? V0[rr] : make_double2(0.0, 0.0);
-          v1[u] = rr < cnt && two ? V1[rr] : make_double2(0.0, 0.0);
+          v0[u] = rr < cnt ? (sm0 ? vj[rr] : __ldcg(V0 + rr)) : make_double2(0.0, 0.0);
+          v1[u] = rr < cnt && two ? (sm1 ? vj[rr] : __ldcg(V1 + rr)) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < U1; ++u) {
@@ -402,7 +451,10 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
   }
   __syncthreads();
   if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) hcol[i] = cv[i];
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+      hcol[i] = cv[i];
+      if (lagged) A.H[i + static_cast<long long>(j) * (A.restart + 1)] = cv[i];
+    }
   // Pass 2: w' = w - V h and ||w'||^2. Two rows per thread at a time
   // (16 loads in flight); per row the update order over k is unchanged.
   double2 acc = make_double2(0.0, 0.0);
@@ -415,12 +467,13 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
     const double2* Va = A.V + r0 + ra;
     const double2* Vb = A.V + r0 + rbs;
     int k = 0;
-    for (; k + 8 <= j + 1; k += 8) {
+    const int kEnd = lagged ? j : j + 1;  // lagged: the k = j term from vj below (same order)
+    for (; k + 8 <= kEnd; k += 8) {
       double2 va[8], vb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        va[u] = Va[static_cast<long long>(k + u) * n];
-        vb[u] = Vb[static_cast<long long>(k + u) * n];
+        va[u] = __ldcg(Va + static_cast<long long>(k + u) * n);
+        vb[u] = __ldcg(Vb + static_cast<long long>(k + u) * n);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -428,19 +481,36 @@ __device__ inline void arnoldiLS(const GmresArgs& A, double2* S, double2* dots, 
         wb = csub(wb, cmul(cv[k + u], vb[u]));
       }
     }
-    for (; k <= j; ++k) {
-      const double2 va = Va[static_cast<long long>(k) * n], vb = Vb[static_cast<long long>(k) * n];
+    for (; k < kEnd; ++k) {
+      const double2 va = __ldcg(Va + static_cast<long long>(k) * n), vb = __ldcg(Vb + static_cast<long long>(k) * n);
       wa = csub(wa, cmul(cv[k], va));
       wb = csub(wb, cmul(cv[k], vb));
     }
+    if (lagged) {
+      wa = csub(wa, cmul(cv[j], vj[ra]));
+      wb = csub(wb, cmul(cv[j], vj[rbs]));
+    }
     ws[ra] = wa;
     acc.x += wa.x * wa.x + wa.y * wa.y;
+    if (lagged) A.V[static_cast<long long>(j + 1) * n + r0 + ra] = wa;
     if (hb) {
       ws[rb] = wb;
       acc.x += wb.x * wb.x + wb.y * wb.y;
+      if (lagged) A.V[static_cast<long long>(j + 1) * n + r0 + rb] = wb;
     }
   }
   blockPartial(acc, scratch, partSlot(A, 0, 0));
+  if (lagged) {
+    if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t3;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+      A.prof[0] += pt[1] - pt[0];
+      A.prof[1] += pt[2] - pt[1];
+      A.prof[2] += t3 - pt[2];
+      A.prof[4] += 1;
+    }
+    return;
+  }
   if (blockIdx.x == 0) givensStage(A, 0, j, hcol, sh);  // made visible by the barrier
   gridBarrier(bar);
   mark(3);

@@ -83,12 +83,30 @@ struct PArgs {
   // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
   // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
   int arnoldi;
+  int cycle;  // with arnoldi: the whole restart cycle (columns 0, 1, ...) in this launch
   GmresArgs gm;
   double2* lsS;
   double2* lsDots;
   double2* lsPart;
   unsigned long long* phaseNs;  // optional: globaltimer at phase boundaries (CTA 0)
+  unsigned long long* cta;      // optional (TBT_CTATRACE): per-CTA event times [12][gridDim.x] of this launch
 };
+
+// Per-CTA trace (TBT_CTATRACE=1): 0 start, 1 after the PDL wait, 2+k / 6+k
+// arrival at / release from grid barrier k, 10 end, 11 = %smid.
+__device__ __forceinline__ void trace(const PArgs& a, int ev) {
+  if (a.cta && threadIdx.x == 0) {
+    unsigned long long t;
+    if (ev == 11) {
+      unsigned s;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+      t = s;
+    } else {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    }
+    a.cta[ev * kCtaTraceMaxGrid + blockIdx.x] = t;
+  }
+}
 
 __device__ __forceinline__ void stamp(const PArgs& a, int k) {
   if (a.phaseNs && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -102,6 +120,7 @@ __device__ __forceinline__ void stamp(const PArgs& a, int k) {
 // earliest / latest CTA arrival of barrier k (ns) at phaseNs[16+k] / phaseNs[8+k].
 __device__ __forceinline__ void gridSync(unsigned long long* counter, const PArgs& a, int k) {
   __syncthreads();
+  if (k < 4) trace(a, 2 + k);
   if (threadIdx.x == 0) {
     if (a.phaseNs) {
       unsigned long long t;
@@ -111,6 +130,7 @@ __device__ __forceinline__ void gridSync(unsigned long long* counter, const PArg
     }
     gridArriveWait(counter);
   }
+  if (k < 4) trace(a, 6 + k);
   __syncthreads();
 }
 
@@ -206,17 +226,17 @@ __device__ __forceinline__ bool outActive() {
 // self relation), tvec[pair] = sum_terms diag(d) x_src + W2 (W^T x_src).
 // Runs on the auxiliary warp during phase B, off the critical path.
 template <int M>
-__device__ void termItem(const PArgs& a, int p) {
+__device__ void termItem(const PArgs& a, const double2* xc, int p) {
   constexpr int KPL = (M + 31) / 32;
   constexpr int QB = 8;  // projections loaded / reduced per batch
   const int lane = threadIdx.x & 31;
   const int4 info = *reinterpret_cast<const int4*>(a.pInfo + 4 * p);
-  const double2* xs = a.xc + static_cast<long long>(info.y) * M;
+  const double2* xs = xc + static_cast<long long>(info.y) * M;
   double2 xv[KPL], acc[KPL];
 #pragma unroll
   for (int k = 0; k < KPL; ++k) {
     const int kk = lane + 32 * k;
-    xv[k] = kk < M ? __ldg(xs + kk) : make_double2(0.0, 0.0);
+    xv[k] = kk < M ? __ldcg(xs + kk) : make_double2(0.0, 0.0);  // x may be written in-kernel (restart-cycle launch)
     acc[k] = make_double2(0.0, 0.0);
   }
   for (int ent = 0; ent < 2; ++ent) {
@@ -298,7 +318,11 @@ struct PCfg {
   // The transpose-product reduction buffer (phase B only) aliases the FFT
   // slabs (phases A / C only): a grid barrier separates every phase.
   static constexpr uint32_t WORK = RED > FFTB ? RED : FFTB;
-  static constexpr uint32_t SMEM = STAGES * STAGE + WORK + 2 * STAGES * 8;
+  // Restart-cycle launches: the lagged Givens step's staging + the previous
+  // column's norm, kept apart from the ring (primed while it runs).
+  static constexpr uint32_t GVOFF = STAGES * STAGE + WORK + 2 * STAGES * 8;
+  static constexpr uint32_t GVB = (3 * gmresdev::RMAX + 4 + 1) * 16;
+  static constexpr uint32_t SMEM = GVOFF + GVB;
 };
 
 // L2 bulk prefetch of the spectrum chunks after the ring's first `pre`.
@@ -321,6 +345,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   double2* fftb = red;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + C::WORK);
   uint64_t* empty = full + STAGES;
+  double2* gvSh = reinterpret_cast<double2*>(smem + C::GVOFF);
+  double* hnS = reinterpret_cast<double*>(gvSh + 3 * gmresdev::RMAX + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == kConsumers / 32;
   const bool aux = warp > kConsumers / 32;
@@ -337,6 +363,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
                            : static_cast<int>(blockIdx.x) * (kConsumers / 32) + warp;
   };
 
+  trace(a, 0);
+  trace(a, 11);
   if (a.skip && *reinterpret_cast<const volatile int*>(a.skip)) return;  // uniform: set before launch
   stamp(a, 0);
   if (threadIdx.x == 0) {
@@ -352,13 +380,19 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   const long long total = mine * C::NCH;
   const long long pre = total < STAGES ? total : STAGES;
   uint64_t polS = 0, polX = 0;
+  // Ring position: stage and phase parity of chunk `it` of iteration `iter`
+  // (a restart-cycle launch runs several applies through the same ring).
+  long long ringBase = 0;
   auto prefetch = [&]() {
     // Spectrum chunks of the first STAGES items: independent of x.
     for (long long it = 0; it < pre; ++it) {
+      const long long gi = ringBase + it;
+      const int s = static_cast<int>(gi % STAGES);
       const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
       const int ch = static_cast<int>(it % C::NCH);
-      mbarArriveExpectTx(full + it, C::STAGE);
-      bulkG2S(smem + it * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + it,
+      if (gi >= STAGES) mbarWait(empty + s, static_cast<uint32_t>(((gi / STAGES) & 1) ^ 1));
+      mbarArriveExpectTx(full + s, C::STAGE);
+      bulkG2S(smem + s * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + s,
               polS);
     }
   };
@@ -375,10 +409,32 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   // was finishing (its set-up and the spectrum prime above touch nothing the
   // previous grid writes); wait for it before x / T / xhat / y are used.
   if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  trace(a, 1);
 
   using W0 = WarpFft<N0>;
   using W1 = WarpFft<N1>;
   const double2 zero = make_double2(0.0, 0.0);
+  // One apply per iteration; a restart-cycle launch (a.cycle) runs the
+  // apply + Arnoldi step for columns j = 0, 1, ... until CTA 0's Givens step
+  // stops the cycle, x = v_j each time.
+  const long long nvec = static_cast<long long>(a.gm.ne) * a.gm.m;
+  for (int iter = 0;; ++iter) {
+  const int jcol = a.cycle ? iter : a.gm.j;
+  const double2* __restrict__ xin = a.cycle ? a.gm.V + static_cast<long long>(jcol) * nvec : a.x;
+  ringBase = static_cast<long long>(iter) * total;
+  // Lagged normalisation (restart-cycle launch, column j >= 1): x = v_j is
+  // the previous step's w' (unnormalised); its norm is reduced from the
+  // previous step's partials by one auxiliary warp per CTA during phase A1
+  // (every CTA gets the same bits), and CTA 0's auxiliary warp runs the
+  // Givens step of column j-1 meanwhile (its stop decision is read after
+  // grid barrier 0). y is scaled by 1/||w'|| in phase C2, v_j's rows are
+  // normalised by the LS step.
+  const bool lagStep = a.cycle && iter > 0;
+  if (lagStep && aux && warp == kConsumers / 32 + 1) {
+    const double hn = sqrt(gmresdev::warpTotal(gmresdev::partSlot(a.gm, 0, 0)).x);
+    if (lane == 0) *hnS = hn;
+    if (blockIdx.x == 0) gmresdev::givensWarp(a.gm, 0, jcol - 1, hn, gvSh);
+  }
 
   // ---- phase A1: row FFTs (level 0)
   if (!producer && !aux) {
@@ -393,7 +449,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
             [&](int c, int b) {
               if (c >= a.nx) return zero;
               const long long q = (static_cast<long long>(r) * a.nx + c) * M + b0 + b;
-              const double2 v = a.x[q];
+              const double2 v = xin[q];
               if (a.xStage) a.xStage[q] = v;  // zero-copy: later readers use the HBM copy
               return v;
             },
@@ -403,6 +459,14 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   }
   gridSync(a.barFlags, a, 0);
   stamp(a, 1);
+  if (lagStep) {
+    const volatile GmresState* st = a.gm.st;
+    if (!st->cycleActive || st->stopInner) break;  // uniform: CTA 0's Givens finished before barrier 0
+    if (producer && lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring held the LS scratch
+      prefetch();
+    }
+  }
   if (producer && lane == 0 && a.prefetchAt == 1) prefetch();
   if (producer && lane == 0 && a.l2At == 1) prefetchL2<M, RCH>(a, pre, total);
   // ---- phase A2: column FFTs (level 1) -> xhat
@@ -426,13 +490,13 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   // ---- phase B: bin-pair products (+ correction term vectors on the aux warp)
   if (aux) {
     if (a.corr)
-      for (int p = auxId; p < a.nPairs; p += gridDim.x * kAux) termItem<M>(a, p);
+      for (int p = auxId; p < a.nPairs; p += gridDim.x * kAux) termItem<M>(a, a.cycle ? xin : a.xc, p);
   } else if (producer) {
     if (lane == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       for (long long it = 0; it < total; ++it) {
-        const int s = static_cast<int>(it % STAGES);
-        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+        const int s = static_cast<int>((ringBase + it) % STAGES);
+        const uint32_t ph = static_cast<uint32_t>(((ringBase + it) / STAGES) & 1);
         const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
         const int ch = static_cast<int>(it % C::NCH);
         const long long f = a.pairF[p], g = a.pairG[p];
@@ -450,8 +514,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     const int tc = threadIdx.x % TC, tr = threadIdx.x / TC;
     double2 yga[C::CPT];
     for (long long it = 0; it < total; ++it) {
-      const int s = static_cast<int>(it % STAGES);
-      const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
+      const int s = static_cast<int>((ringBase + it) % STAGES);
+      const uint32_t ph = static_cast<uint32_t>(((ringBase + it) / STAGES) & 1);
       const long long pi = it / C::NCH;
       const int ch = static_cast<int>(it % C::NCH);
       const long long p = blockIdx.x + pi * gridDim.x;
@@ -534,6 +598,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   // Past the last grid barrier: the next apply may launch its CTAs now.
   if (a.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- phase C2: inverse row FFTs, keep nx points, scale, correction -> y
+  const double hnPrev = lagStep ? *hnS : 1.0;
   if (!producer && !aux) {
     constexpr int RO = Split<N0>::R2 == 1 ? Split<N0>::R1 : Split<N0>::R2;  // outputs per lane
     const int chunks0 = M / W0::WB;
@@ -554,12 +619,18 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
           [&](int c, int b, double2 v, int q) {
             if (c < a.nx) {
               const long long e = static_cast<long long>(r) * a.nx + c;
-              a.y[e * M + b0 + b] = cadd(cscale(v, a.scale), pre[q]);
+              double2 out = cadd(cscale(v, a.scale), pre[q]);
+              if (lagStep) out = make_double2(out.x / hnPrev, out.y / hnPrev);
+              a.y[e * M + b0 + b] = out;
             }
           });
     }
   }
   stamp(a, 5);
+  if (a.cta) {
+    __syncthreads();
+    trace(a, 10);
+  }
   if (a.arnoldi) {
     gridSync(a.barFlags, a, 4);  // y (= w) complete grid-wide
     // Shared memory is free again: LS scratch, then hcol / Givens staging.
@@ -570,13 +641,27 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     double2* sh = hcol + gmresdev::RMAX + 2;
     double2* scratch = sh + 3 * gmresdev::RMAX + 4;
     __syncthreads();
-    gmresdev::arnoldiLS(a.gm, a.lsS, a.lsDots, a.lsPart, shw, scratch, hcol, sh, a.barFlags);
+    gmresdev::arnoldiLS(a.gm, jcol, a.lsS, a.lsDots, a.lsPart, shw, scratch, hcol, sh, a.barFlags, a.cycle != 0,
+                        hnPrev);
   }
+  if (!a.cycle) break;
+  // w' = v_{j+1} unnormalised (every CTA's rows) and the norm partials
+  // visible grid-wide before the next column's phase A1 reads them.
+  gridSync(a.barFlags, a, 5);
+  if (jcol + 1 >= a.gm.restart) {
+    // Last column of the cycle: its Givens step here (v_{j+1} is not used).
+    if (blockIdx.x == 0 && warp == 0) {
+      const double hn = sqrt(gmresdev::warpTotal(gmresdev::partSlot(a.gm, 0, 0)).x);
+      gmresdev::givensWarp(a.gm, 0, jcol, hn, gvSh);
+    }
+    break;
+  }
+  }  // iteration loop
 }
 
 template <int M, int TC, int RCH, int STAGES, int N0, int N1>
 bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
-             double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr) {
+             double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr, bool cycle = false) {
   using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
   auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1>;
@@ -622,6 +707,11 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.pTargetPtr = c.dPairTargetPtr;
   a.ycorr = c.dYcorrP;
   a.phaseNs = c.phaseTiming ? c.dPhaseNs : nullptr;
+  a.cta = nullptr;
+  if (c.dCtaTrace) {
+    a.cta = c.dCtaTrace + (c.ctaTraceLaunches % kCtaTraceSlots) * kCtaTraceEvents * kCtaTraceMaxGrid;
+    ++c.ctaTraceLaunches;
+  }
   a.prefetchAt = c.prefetchAt;
   a.l2Chunks = c.zeroCopyL2Bytes / (static_cast<long long>(smCount(c.device)) * C::CHUNK);
   a.l2At = 0;
@@ -634,8 +724,11 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
     const long long need =
         (gmresdev::arnoldiLSSmem(chunk, gm->restart) + gmresdev::RMAX + 2 + 3 * gmresdev::RMAX + 4 + 32) *
         static_cast<long long>(sizeof(double2));
-    if (need > static_cast<long long>(C::SMEM)) return false;
+    // The LS scratch reuses the ring and reduction space, never the mbarriers.
+    if (need > static_cast<long long>(STAGES * C::STAGE + C::WORK)) return false;
     a.arnoldi = 1;
+    a.cycle = cycle ? 1 : 0;
+    if (cycle) a.prefetchAt = 0;  // the loop re-primes the ring at the end of every column
     a.gm = *gm;
     a.lsS = lsS;
     a.lsDots = lsDots;
@@ -646,14 +739,32 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   cfg.blockDim = dim3(kThreadsP);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = c.stream;
+  // Launch mode. The grid barriers need all CTAs co-resident (one per SM).
+  // A cooperative launch guarantees it (or fails), but a cooperative grid is
+  // only dispatched once the previous grid has fully drained: measured C2
+  // back to back 37.1 us vs 35.7 us for a plain launch with programmatic
+  // dependent launch, whose CTAs are placed the moment the previous apply's
+  // CTAs exit (its griddepcontrol.wait then covers the rest). So the first
+  // apply of a context is launched cooperatively — it fails rather than
+  // hangs if this process cannot have one CTA on every SM (e.g. an MPS SM
+  // limit) — and later PDL applies launch plainly with the same grid.
+  // TBT_COOP=1 keeps every launch cooperative.
+  static const bool forceCoop = getenv("TBT_COOP") && getenv("TBT_COOP")[0] == '1';
+  const bool coop = forceCoop || !a.pdl || !c.coopChecked;
   cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
+  int na = 0;
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na++].val.cooperative = 1;
+  }
+  if (a.pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = a.pdl ? 2 : 1;
+  cfg.numAttrs = na;
   TBT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+  if (coop) c.coopChecked = true;
   return true;
 }
 
@@ -673,7 +784,7 @@ bool persistentSupported(const Ctx& c) {
 }
 
 bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm,
-                           double2* lsS, double2* lsDots, double2* lsPart) {
+                           double2* lsS, double2* lsDots, double2* lsPart, bool cycle) {
   if (!persistentSupported(c) || c.dist) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
@@ -681,19 +792,19 @@ bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, 
     // back): 37.6 us; whole blocks x 2 38.2, half x 5 40.6, quarter x 8
     // 41.0, quarter x 11 47.1 — more bytes in flight per SM than 128 KB only
     // slows the stream.
-    case 64064064: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 96128128: return launchP<96, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 64128064: return launchP<64, 16, 64, 2, 128, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 64064128: return launchP<64, 16, 64, 2, 64, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 64128128: return launchP<64, 16, 64, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 128064064: return launchP<128, 32, 16, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 128256256: return launchP<128, 32, 16, 4, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
-    case 192128128: return launchP<192, 32, 16, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64064064: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 96128128: return launchP<96, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 64128064: return launchP<64, 16, 64, 2, 128, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 64064128: return launchP<64, 16, 64, 2, 64, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 64128128: return launchP<64, 16, 64, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 128064064: return launchP<128, 32, 16, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 128256256: return launchP<128, 32, 16, 4, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    case 192128128: return launchP<192, 32, 16, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
     default: return false;
   }
 }

@@ -152,9 +152,12 @@ struct Ctx {
   int prefetchAt = 0;                      // TBT_PREFETCH: 0 kernel start, 1 after rows, 2 after columns
   long long zeroCopyL2Bytes = 0;  // set around zero-copy launches: spectrum bytes to prefetch into L2
   bool zeroCopyStage = false;     // set around zero-copy launches: stage x in dXin for the correction reads
+  bool coopChecked = false;      // a cooperative persistent launch succeeded on this context (co-residency)
   bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)
   const int* skipFlag = nullptr;  // device flag: persistent applies become no-ops when set
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
+  unsigned long long* dCtaTrace = nullptr; // TBT_CTATRACE=1: per-CTA event times of the persistent apply
+  long long ctaTraceLaunches = 0;          // launches traced so far (slot = count % kCtaTraceSlots)
   bool forceMultiPass = false;             // TBT_FFT=passes
   bool forceFused2d = false;               // TBT_FFT=fused: cluster 2-D kernels also for wide batches
   bool forceUnfused = false;               // TBT_GMRES=unfused: separate apply / Arnoldi launches
@@ -296,6 +299,7 @@ bool applyUserLayout(Ctx& c, const double2* x, double2* y, int nrhs, bool withCo
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 void launchBinProductAnti(Ctx& c, int nrhs);                  // binprod.cu: FULL generators, yhat += A_a xhat
 int binprodVariant(int m);                                    // binprod.cu
+constexpr int kCtaTraceSlots = 8, kCtaTraceEvents = 12, kCtaTraceMaxGrid = 256;  // TBT_CTATRACE buffer shape
 constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEMM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
@@ -405,7 +409,8 @@ struct GmresArgs;
 struct GmresWs;
 void freeGmresWorkspace(Ctx& c);  // gmres.cu
 bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
-                           double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr);
+                           double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr,
+                           bool cycle = false);
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);

@@ -170,6 +170,59 @@ __device__ __forceinline__ void bar8(unsigned long long* c) {
   clusterSync();
 }
 
+// V9: one arrival counter (acq_rel atomics, nobody polls it); the last
+// arriver (thread 0) broadcasts the generation to per-CTA flag lines
+// (128 B apart); every CTA polls only its own line.
+// V10: as V9 with warp 0: lane 0 arrives, the last arriver's 32 lanes write
+// the flags (grid/32 stores each).
+// V11: V0 with a 32 ns back-off between polls.
+__device__ __forceinline__ unsigned long long atomAddAcqRelU(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void bar9(unsigned long long* c, unsigned long long* flags, unsigned long long gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long g = gridDim.x;
+    const unsigned long long old = atomAddAcqRelU(c, 1ULL);
+    if (old % g == g - 1)
+      for (unsigned k = 0; k < gridDim.x; ++k) stRelease(flags + 16 * k, gen);
+    while (ldAcquire(flags + 16 * blockIdx.x) < gen) {
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void bar10(unsigned long long* c, unsigned long long* flags, unsigned long long gen) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned long long g = gridDim.x;
+    unsigned long long old = 0;
+    if (threadIdx.x == 0) old = atomAddAcqRelU(c, 1ULL);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old % g == g - 1) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (unsigned k = threadIdx.x; k < gridDim.x; k += 32)
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(flags + 16 * k), "l"(gen) : "memory");
+    }
+    if (threadIdx.x == 0)
+      while (ldAcquire(flags + 16 * blockIdx.x) < gen) {
+      }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void bar11(unsigned long long* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long g = gridDim.x;
+    const unsigned long long old = atomAddRelease(c, 1ULL);
+    const unsigned long long target = (old / g + 1) * g;
+    while (ldAcquire(c) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(352, 1) kern(int variant, int iters, int stores, unsigned long long* c,
                                                unsigned long long* flags, unsigned long long* rel, double* buf,
                                                long long* out) {
@@ -193,6 +246,12 @@ __global__ void __launch_bounds__(352, 1) kern(int variant, int iters, int store
       bar6(c);
     else if (variant == 8)
       bar8(c);
+    else if (variant == 9)
+      bar9(c, flags, ++gen);
+    else if (variant == 10)
+      bar10(c, flags, ++gen);
+    else if (variant == 11)
+      bar11(c);
     else
       bar3(flags, rel + 16, variant - 2);
   }
@@ -217,7 +276,8 @@ int main() {
   cudaMemset(rel, 0, 8 * 64);
   const int iters = 2000;
   for (int stores : {0, 8, 32}) {
-    for (int v : {0, 1, 4, 5, 7}) {
+    for (int v : {0, 1, 4, 5, 7, 9, 10, 11}) {
+      cudaMemset(c, 0, 8);
       cudaMemset(flags, 0, 8 * 16 * sms);
       cudaMemset(rel, 0, 8 * 64);
       void* args[] = {&v, const_cast<int*>(&iters), &stores, &c, &flags, &rel, &buf, &out};
@@ -225,6 +285,8 @@ int main() {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaLaunchCooperativeKernel((void*)kern, sms, 352, args, 0, 0);  // warm-up
+      cudaMemset(c, 0, 8);
+      cudaMemset(flags, 0, 8 * 16 * sms);
       cudaEventRecord(e0);
       cudaLaunchCooperativeKernel((void*)kern, sms, 352, args, 0, 0);
       cudaEventRecord(e1);
