@@ -69,12 +69,12 @@ def measured_hbm():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
 
 
-TRAFFIC_FILES = ("r2_traffic.json", "r1_traffic.json")  # newest capture first
+TRAFFIC_FILES = ("r2b_traffic.json", "r2_traffic.json", "r1_traffic.json")  # newest capture first
 
 
 def ncu_traffic(key):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r2_traffic.json, else r1), and the file it came from."""
+    capture (the newest of profiles/r2b, r2, r1 _traffic.json), and the file it came from."""
     for name in TRAFFIC_FILES:
         try:
             return json.loads((REPO / "profiles" / name).read_text())[key]["dram_bytes_per_launch"], name
@@ -672,7 +672,7 @@ def main():
     kbytes = spectrum + vec_k3 + 2 * cfg.n * c16
     if info.apply_path == 2:
         kms = step_mean
-        kname = "matvec_persistent (K2+K3+K4 phases in one cooperative kernel, 1 launch per step)"
+        kname = "matvec_persistent (K2+K3+K4 phases in one persistent kernel, 1 launch per step)"
     else:
         kms = k3_ms
         kname = "binprod (K3, bin-pair product)"

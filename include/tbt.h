@@ -329,10 +329,12 @@ tbt_status tbt_phase_times(tbt_ctx* ctx, int on, double* out_us);
 
 /* Per-CTA trace of the persistent apply (diagnostics; needs TBT_CTATRACE=1
  * in the environment when the context is created): the last 8 launches,
- * slot = launch index mod 8, each [12 events][256 CTAs] of u64:
+ * slot = launch index mod 8, each [16 events][256 CTAs] of u64:
  * %globaltimer ns at 0 CTA start, 1 after the programmatic-launch wait,
  * 2..5 arrival at / 6..9 release from grid barriers 0..3, 10 end of the
- * inverse row phase; event 11 holds %smid. cap >= 8*12*256. */
+ * inverse row phase, and for a fused GMRES step 12 after its y barrier,
+ * 13 after its dot barrier, 14 at its end; event 11 holds %smid.
+ * cap >= 8*16*256. */
 tbt_status tbt_cta_trace(tbt_ctx* ctx, unsigned long long* out, long long cap, long long* launches);
 
 /* Times `iters` back-to-back device-resident applies (nrhs columns) with

@@ -31,6 +31,16 @@ namespace {
 
 using namespace gmresdev;
 
+// Last column of a lagged restart cycle (matvec_persistent.cu LAGGED): its
+// w' norm from the G per-CTA partials of the last node, and its Givens step.
+__global__ void gmresLaggedFinish(GmresArgs A, int j, int G) {
+  __shared__ double2 sh[3 * RMAX + 4];
+  const volatile GmresState* st = A.st;
+  if (!st->cycleActive || st->stopInner) return;  // a node already ended the cycle
+  const double hn = sqrt(warpTotalN(partSlotN(A, 0, 0, G), G).x);
+  givensWarp(A, 0, j, hn, sh);
+}
+
 __global__ void __launch_bounds__(kThreads) gmresInit(GmresArgs A) {
   __shared__ double2 scratch[kWarps];
   const long long slots = static_cast<long long>(A.ne) * A.m;
@@ -1421,39 +1431,47 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     // One inner iteration: the apply and the Arnoldi step, fused into the
     // persistent apply kernel when possible (one cooperative launch).
     const bool fuse = lowSync && !c.timeBinprod && !c.dist && !c.forceUnfused;
-    auto iteration = [&](int j) {
-      A.j = j;
-      if (fuse && launchPersistentApply(c, A.V + static_cast<long long>(j) * nall, A.w, !useAOnly, &A, lsS, lsDots,
-                                        lsPart))
-        return;
-      applyOperator(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
-      arnoldi(j);
-    };
     // Single column: the whole inner loop of a cycle is one CUDA graph
     // (restart x [apply, Arnoldi]); every node turns into a no-op once the
     // column's inner loop stopped (device flag), so the host synchronises
     // once per restart cycle.
-    // Fused single column: the whole inner loop of a cycle is ONE persistent
-    // launch (matvec_persistent.cu, apply + Arnoldi per column, the Givens
-    // stop decision read back on the device), unless the shape is not
-    // instantiated or TBT_GMRES=graph asks for the captured graph of per-column
-    // launches.
-    static const bool graphEnv = getenv("TBT_GMRES") && std::string(getenv("TBT_GMRES")) == "graph";
-    bool cycleKernel = fuse && ncols == 1 && !withMargin && !graphEnv && persistentSupported(c);
-    const bool useGraph = !cycleKernel && ncols == 1 && !c.timeBinprod && !c.dist && !withMargin;
+    const bool useGraph = ncols == 1 && !c.timeBinprod && !c.dist && !withMargin;
+    // Fused nodes with lagged normalisation (matvec_persistent.cu LAGGED):
+    // node j finishes column j-1 (norm, Givens step, stop decision) under
+    // its own phase A1 and the nodes are serialised programmatically (PDL),
+    // so a node's CTAs are placed as the previous node's exit; a last node
+    // finishes column restart-1. TBT_GMRES=nolag keeps the unlagged nodes.
+    static const bool noLagEnv = getenv("TBT_GMRES") && std::string(getenv("TBT_GMRES")) == "nolag";
+    const bool lagged = useGraph && fuse && !noLagEnv && persistentLaggedFits(c, A);
+    auto iteration = [&](int j) {
+      A.j = j;
+      if (fuse && launchPersistentApply(c, A.V + static_cast<long long>(j) * nall, A.w, !useAOnly, &A, lsS, lsDots,
+                                        lsPart, lagged))
+        return;
+      applyOperator(c, A.V + static_cast<long long>(j) * nall, A.w, ncols, !useAOnly);
+      arnoldi(j);
+    };
     GmresArgs keyA = A;  // what the captured nodes bake in (b, x unused by them)
     keyA.b = nullptr;
     keyA.x = nullptr;
     keyA.j = 0;
-    const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0) | (bigLS ? 16 : 0);
+    const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0) | (bigLS ? 16 : 0) |
+                      (lagged ? 32 : 0);
     if (useGraph && (!W.inner || std::memcmp(&keyA, &W.graphKey, sizeof(GmresArgs)) != 0 || W.graphFlags != flags)) {
       if (W.inner) cudaGraphExecDestroy(W.inner);
       W.inner = nullptr;
       c.skipFlag = &A.st[0].stopInner;
+      // Plain (programmatically serialised) nodes need this context's
+      // co-residency check: one cooperative apply of scratch first.
+      if (lagged && !c.coopChecked) launchPersistentApply(c, A.V, A.w, false);
       cudaGraph_t gph;
       TBT_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
         for (int j = 0; j < R; ++j) iteration(j);
+        if (lagged) {
+          gmresLaggedFinish<<<1, 32, 0, s>>>(A, R - 1, smCount(c.device));
+          TBT_CUDA_CHECK(cudaGetLastError());
+        }
       } catch (...) {
         cudaStreamEndCapture(s, &gph);
         c.skipFlag = nullptr;
@@ -1479,18 +1497,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
           cols.cycleStart();
         else
           coopLaunch(reinterpret_cast<const void*>(gmresCycleStart), grid, smem, A, s);
-        bool cycleDone = false;
-        if (cycleKernel) {
-          pull();
-          cycleDone = true;
-          if (st[0].cycleActive && !st[0].stopInner) {
-            A.j = 0;
-            cycleDone = launchPersistentApply(c, A.V, A.w, !useAOnly, &A, lsS, lsDots, lsPart, true);
-            cycleKernel = cycleDone;  // LS scratch does not fit next to the ring: per-column launches
-          }
-        }
-        if (cycleDone) {
-        } else if (useGraph) {
+        if (useGraph) {
           // The cycle start may have ended the solve (budget or tolerance
           // reached): then the 'restart' no-op nodes are not worth a launch.
           pull();

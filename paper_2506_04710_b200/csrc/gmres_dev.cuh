@@ -96,8 +96,8 @@ __device__ __forceinline__ void blockPartial(double2 v, double2* scratch, double
 
 // Grid total of the partials, computed by each warp independently in a
 // fixed order (bitwise identical in every warp and CTA).
-__device__ __forceinline__ double2 warpTotal(const double2* part) {
-  const int lane = threadIdx.x & 31, G = static_cast<int>(gridDim.x);
+__device__ __forceinline__ double2 warpTotalN(const double2* part, int G) {
+  const int lane = threadIdx.x & 31;
   double2 s = make_double2(0.0, 0.0);
   for (int k0 = lane; k0 < G; k0 += 256) {  // up to 8 loads in flight per lane, summed in k order
     double2 v[8];
@@ -108,9 +108,16 @@ __device__ __forceinline__ double2 warpTotal(const double2* part) {
   }
   return warpSum(s);
 }
+__device__ __forceinline__ double2 warpTotal(const double2* part) {
+  return warpTotalN(part, static_cast<int>(gridDim.x));
+}
 
+// Partials of a launch with G CTAs (gridDim.x by default).
+__device__ __forceinline__ double2* partSlotN(const GmresArgs& A, int phase, int col, int G) {
+  return A.partial + (static_cast<long long>(phase & 1) * A.ncols + col) * G;
+}
 __device__ __forceinline__ double2* partSlot(const GmresArgs& A, int phase, int col) {
-  return A.partial + (static_cast<long long>(phase & 1) * A.ncols + col) * gridDim.x;
+  return partSlotN(A, phase, col, static_cast<int>(gridDim.x));
 }
 
 __device__ __forceinline__ long long slotIndex(long long s, int col, int ncols, int m) {
@@ -312,7 +319,7 @@ __device__ __forceinline__ void forwardSubstWarp(double2* cv, const double2* sL,
 // in H(:, j) for that Givens step.
 __device__ inline void arnoldiLS(const GmresArgs& A, int j, double2* S, double2* dots, double2* dotPart, double2* shw,
                           double2* scratch, double2* hcol, double2* sh, unsigned long long* bar,
-                          bool lagged = false, double hnPrev = 1.0) {
+                          bool lagged = false, double hnPrev = 1.0, unsigned long long* traceDots = nullptr) {
   // Written by CTA 0 before a grid barrier (or before this launch): read
   // through L1 (the persistent restart-cycle loop re-reads it per column).
   const volatile GmresState* stv = A.st;
@@ -394,6 +401,11 @@ __device__ inline void arnoldiLS(const GmresArgs& A, int j, double2* S, double2*
   }
   gridBarrier(bar);
   mark(1);
+  if (traceDots && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    traceDots[blockIdx.x] = t;
+  }
   // Grid totals, reduced by EVERY CTA itself (no second grid barrier):
   // 16 lanes per dot slot, 2 slots per warp; lane q of a group sums the
   // partials q, q+16, ... in order, then a 4-step butterfly — the same bits

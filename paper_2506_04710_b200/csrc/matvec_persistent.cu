@@ -83,7 +83,6 @@ struct PArgs {
   // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
   // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
   int arnoldi;
-  int cycle;  // with arnoldi: the whole restart cycle (columns 0, 1, ...) in this launch
   GmresArgs gm;
   double2* lsS;
   double2* lsDots;
@@ -93,7 +92,9 @@ struct PArgs {
 };
 
 // Per-CTA trace (TBT_CTATRACE=1): 0 start, 1 after the PDL wait, 2+k / 6+k
-// arrival at / release from grid barrier k, 10 end, 11 = %smid.
+// arrival at / release from grid barrier k, 10 end of C2, 11 = %smid,
+// fused GMRES step: 12 after the y barrier, 13 after the LS dot barrier
+// (CTA-local time at which the reduce starts), 14 end of the step.
 __device__ __forceinline__ void trace(const PArgs& a, int ev) {
   if (a.cta && threadIdx.x == 0) {
     unsigned long long t;
@@ -236,7 +237,7 @@ __device__ void termItem(const PArgs& a, const double2* xc, int p) {
 #pragma unroll
   for (int k = 0; k < KPL; ++k) {
     const int kk = lane + 32 * k;
-    xv[k] = kk < M ? __ldcg(xs + kk) : make_double2(0.0, 0.0);  // x may be written in-kernel (restart-cycle launch)
+    xv[k] = kk < M ? __ldcg(xs + kk) : make_double2(0.0, 0.0);  // L2: x may be this GMRES step's v_j
     acc[k] = make_double2(0.0, 0.0);
   }
   for (int ent = 0; ent < 2; ++ent) {
@@ -301,7 +302,7 @@ __device__ void sumTermsItem(const PArgs& a, int ti) {
   }
 }
 
-template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+template <int M, int TC, int RCH, int STAGES, int N0, int N1, bool LAGGED = false>
 struct PCfg {
   static constexpr int TRN = kConsumers / TC;
   static constexpr int CPT = M / TC;
@@ -318,10 +319,10 @@ struct PCfg {
   // The transpose-product reduction buffer (phase B only) aliases the FFT
   // slabs (phases A / C only): a grid barrier separates every phase.
   static constexpr uint32_t WORK = RED > FFTB ? RED : FFTB;
-  // Restart-cycle launches: the lagged Givens step's staging + the previous
+  // LAGGED launches: the lagged Givens step's staging + the previous
   // column's norm, kept apart from the ring (primed while it runs).
   static constexpr uint32_t GVOFF = STAGES * STAGE + WORK + 2 * STAGES * 8;
-  static constexpr uint32_t GVB = (3 * gmresdev::RMAX + 4 + 1) * 16;
+  static constexpr uint32_t GVB = LAGGED ? (3 * gmresdev::RMAX + 4 + 1) * 16 : 0;
   static constexpr uint32_t SMEM = GVOFF + GVB;
 };
 
@@ -337,9 +338,13 @@ __device__ __forceinline__ void prefetchL2(const PArgs& a, long long pre, long l
   }
 }
 
-template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+// LAGGED: the GMRES-step variant with lagged normalisation, a separate
+// instantiation so that its extra state costs the plain apply no registers
+// (a first version that looped over a whole restart cycle inside one launch
+// spilled in phase B: C2 apply 35.7 -> 40.4 us, GMRES 66 -> 72 us/iteration).
+template <int M, int TC, int RCH, int STAGES, int N0, int N1, bool LAGGED>
 __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
-  using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
+  using C = PCfg<M, TC, RCH, STAGES, N0, N1, LAGGED>;
   extern __shared__ __align__(128) unsigned char smem[];
   double2* red = reinterpret_cast<double2*>(smem + STAGES * C::STAGE);
   double2* fftb = red;
@@ -365,7 +370,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
 
   trace(a, 0);
   trace(a, 11);
-  if (a.skip && *reinterpret_cast<const volatile int*>(a.skip)) return;  // uniform: set before launch
+  if (!LAGGED && a.skip && *reinterpret_cast<const volatile int*>(a.skip)) return;  // uniform: set before launch
   stamp(a, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -380,19 +385,13 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   const long long total = mine * C::NCH;
   const long long pre = total < STAGES ? total : STAGES;
   uint64_t polS = 0, polX = 0;
-  // Ring position: stage and phase parity of chunk `it` of iteration `iter`
-  // (a restart-cycle launch runs several applies through the same ring).
-  long long ringBase = 0;
   auto prefetch = [&]() {
     // Spectrum chunks of the first STAGES items: independent of x.
     for (long long it = 0; it < pre; ++it) {
-      const long long gi = ringBase + it;
-      const int s = static_cast<int>(gi % STAGES);
       const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
       const int ch = static_cast<int>(it % C::NCH);
-      if (gi >= STAGES) mbarWait(empty + s, static_cast<uint32_t>(((gi / STAGES) & 1) ^ 1));
-      mbarArriveExpectTx(full + s, C::STAGE);
-      bulkG2S(smem + s * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + s,
+      mbarArriveExpectTx(full + it, C::STAGE);
+      bulkG2S(smem + it * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + it,
               polS);
     }
   };
@@ -414,26 +413,35 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   using W0 = WarpFft<N0>;
   using W1 = WarpFft<N1>;
   const double2 zero = make_double2(0.0, 0.0);
-  // One apply per iteration; a restart-cycle launch (a.cycle) runs the
-  // apply + Arnoldi step for columns j = 0, 1, ... until CTA 0's Givens step
-  // stops the cycle, x = v_j each time.
-  const long long nvec = static_cast<long long>(a.gm.ne) * a.gm.m;
-  for (int iter = 0;; ++iter) {
-  const int jcol = a.cycle ? iter : a.gm.j;
-  const double2* __restrict__ xin = a.cycle ? a.gm.V + static_cast<long long>(jcol) * nvec : a.x;
-  ringBase = static_cast<long long>(iter) * total;
-  // Lagged normalisation (restart-cycle launch, column j >= 1): x = v_j is
-  // the previous step's w' (unnormalised); its norm is reduced from the
-  // previous step's partials by one auxiliary warp per CTA during phase A1
-  // (every CTA gets the same bits), and CTA 0's auxiliary warp runs the
-  // Givens step of column j-1 meanwhile (its stop decision is read after
-  // grid barrier 0). y is scaled by 1/||w'|| in phase C2, v_j's rows are
-  // normalised by the LS step.
-  const bool lagStep = a.cycle && iter > 0;
-  if (lagStep && aux && warp == kConsumers / 32 + 1) {
-    const double hn = sqrt(gmresdev::warpTotal(gmresdev::partSlot(a.gm, 0, 0)).x);
-    if (lane == 0) *hnS = hn;
-    if (blockIdx.x == 0) gmresdev::givensWarp(a.gm, 0, jcol - 1, hn, gvSh);
+  // Completes the primed ring stages with (unused) x-hat parts and waits
+  // for them, so that a CTA leaving before phase B has no copies in flight.
+  auto drainPrimed = [&]() {
+    if (producer && lane == 0)
+      for (long long it = 0; it < pre; ++it) {
+        bulkG2S(smem + it * C::STAGE + C::CHUNK, a.xhat, C::XF, full + it, polX);
+        bulkG2S(smem + it * C::STAGE + C::CHUNK + C::XF, a.xhat, C::XG, full + it, polX);
+      }
+    if (threadIdx.x == 0)
+      for (long long it = 0; it < pre; ++it) mbarWait(full + it, 0);
+    __syncthreads();
+  };
+  // LAGGED (GMRES column j of a captured restart cycle, the launches
+  // serialised programmatically): a node after the cycle's last column
+  // returns (its stop flag is final once the previous node has completed).
+  // For j >= 1, x = v_j is the previous step's w' (unnormalised): in phase
+  // B one auxiliary warp per CTA reduces its norm from the previous step's
+  // partials (every CTA gets the same bits) and CTA 0's runs the Givens step
+  // of column j-1; if that ended the cycle, the LS step of this node is
+  // skipped (its apply ran for nothing, once per cycle). y is scaled by
+  // 1/||w'|| in phase C2 and v_j's rows are normalised by the LS step.
+  const int jcol = a.gm.j;
+  const bool lagStep = LAGGED && jcol > 0;
+  if constexpr (LAGGED) {
+    const volatile GmresState* st = a.gm.st;
+    if (!st->cycleActive || st->stopInner) {  // uniform: the previous node completed
+      drainPrimed();
+      return;
+    }
   }
 
   // ---- phase A1: row FFTs (level 0)
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
             [&](int c, int b) {
               if (c >= a.nx) return zero;
               const long long q = (static_cast<long long>(r) * a.nx + c) * M + b0 + b;
-              const double2 v = xin[q];
+              const double2 v = a.x[q];
               if (a.xStage) a.xStage[q] = v;  // zero-copy: later readers use the HBM copy
               return v;
             },
@@ -459,14 +467,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   }
   gridSync(a.barFlags, a, 0);
   stamp(a, 1);
-  if (lagStep) {
-    const volatile GmresState* st = a.gm.st;
-    if (!st->cycleActive || st->stopInner) break;  // uniform: CTA 0's Givens finished before barrier 0
-    if (producer && lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring held the LS scratch
-      prefetch();
-    }
-  }
+
   if (producer && lane == 0 && a.prefetchAt == 1) prefetch();
   if (producer && lane == 0 && a.l2At == 1) prefetchL2<M, RCH>(a, pre, total);
   // ---- phase A2: column FFTs (level 1) -> xhat
@@ -489,14 +490,21 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
 
   // ---- phase B: bin-pair products (+ correction term vectors on the aux warp)
   if (aux) {
+    // Lagged: the previous column's norm (every CTA) and Givens step (CTA 0)
+    // under the spectrum stream, ahead of this warp's correction terms.
+    if (lagStep && warp == kConsumers / 32 + 1) {
+      const double hn = sqrt(gmresdev::warpTotal(gmresdev::partSlot(a.gm, 0, 0)).x);
+      if (lane == 0) *hnS = hn;
+      if (blockIdx.x == 0) gmresdev::givensWarp(a.gm, 0, jcol - 1, hn, gvSh);
+    }
     if (a.corr)
-      for (int p = auxId; p < a.nPairs; p += gridDim.x * kAux) termItem<M>(a, a.cycle ? xin : a.xc, p);
+      for (int p = auxId; p < a.nPairs; p += gridDim.x * kAux) termItem<M>(a, a.xc, p);
   } else if (producer) {
     if (lane == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       for (long long it = 0; it < total; ++it) {
-        const int s = static_cast<int>((ringBase + it) % STAGES);
-        const uint32_t ph = static_cast<uint32_t>(((ringBase + it) / STAGES) & 1);
+        const int s = static_cast<int>(it % STAGES);
+        const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
         const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
         const int ch = static_cast<int>(it % C::NCH);
         const long long f = a.pairF[p], g = a.pairG[p];
@@ -514,8 +522,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     const int tc = threadIdx.x % TC, tr = threadIdx.x / TC;
     double2 yga[C::CPT];
     for (long long it = 0; it < total; ++it) {
-      const int s = static_cast<int>((ringBase + it) % STAGES);
-      const uint32_t ph = static_cast<uint32_t>(((ringBase + it) / STAGES) & 1);
+      const int s = static_cast<int>(it % STAGES);
+      const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
       const long long pi = it / C::NCH;
       const int ch = static_cast<int>(it % C::NCH);
       const long long p = blockIdx.x + pi * gridDim.x;
@@ -577,6 +585,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   gridSync(a.barFlags, a, 2);
   stamp(a, 3);
 
+
   // ---- phase C1: inverse column FFTs, keep ny rows -> T (+ correction sums on the aux warp)
   if (aux) {
     if (a.corr)
@@ -599,6 +608,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   if (a.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- phase C2: inverse row FFTs, keep nx points, scale, correction -> y
   const double hnPrev = lagStep ? *hnS : 1.0;
+  const double hnInv = 1.0 / hnPrev;
   if (!producer && !aux) {
     constexpr int RO = Split<N0>::R2 == 1 ? Split<N0>::R1 : Split<N0>::R2;  // outputs per lane
     const int chunks0 = M / W0::WB;
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
             if (c < a.nx) {
               const long long e = static_cast<long long>(r) * a.nx + c;
               double2 out = cadd(cscale(v, a.scale), pre[q]);
-              if (lagStep) out = make_double2(out.x / hnPrev, out.y / hnPrev);
+              if (lagStep) out = cscale(out, hnInv);
               a.y[e * M + b0 + b] = out;
             }
           });
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   }
   if (a.arnoldi) {
     gridSync(a.barFlags, a, 4);  // y (= w) complete grid-wide
+    trace(a, 12);
     // Shared memory is free again: LS scratch, then hcol / Givens staging.
     const long long chunk = (static_cast<long long>(a.gm.ne) * a.gm.m + gridDim.x - 1) / gridDim.x;
     double2* shw = reinterpret_cast<double2*>(smem);
@@ -641,30 +652,18 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
     double2* sh = hcol + gmresdev::RMAX + 2;
     double2* scratch = sh + 3 * gmresdev::RMAX + 4;
     __syncthreads();
-    gmresdev::arnoldiLS(a.gm, jcol, a.lsS, a.lsDots, a.lsPart, shw, scratch, hcol, sh, a.barFlags, a.cycle != 0,
-                        hnPrev);
+    gmresdev::arnoldiLS(a.gm, jcol, a.lsS, a.lsDots, a.lsPart, shw, scratch, hcol, sh, a.barFlags, LAGGED,
+                        hnPrev, a.cta ? a.cta + 13 * kCtaTraceMaxGrid : nullptr);
+    trace(a, 14);
   }
-  if (!a.cycle) break;
-  // w' = v_{j+1} unnormalised (every CTA's rows) and the norm partials
-  // visible grid-wide before the next column's phase A1 reads them.
-  gridSync(a.barFlags, a, 5);
-  if (jcol + 1 >= a.gm.restart) {
-    // Last column of the cycle: its Givens step here (v_{j+1} is not used).
-    if (blockIdx.x == 0 && warp == 0) {
-      const double hn = sqrt(gmresdev::warpTotal(gmresdev::partSlot(a.gm, 0, 0)).x);
-      gmresdev::givensWarp(a.gm, 0, jcol, hn, gvSh);
-    }
-    break;
-  }
-  }  // iteration loop
 }
 
-template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+template <int M, int TC, int RCH, int STAGES, int N0, int N1, bool LAGGED = false>
 bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
-             double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr, bool cycle = false) {
-  using C = PCfg<M, TC, RCH, STAGES, N0, N1>;
+             double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr) {
+  using C = PCfg<M, TC, RCH, STAGES, N0, N1, LAGGED>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
-  auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1>;
+  auto kern = matvecPersistent<M, TC, RCH, STAGES, N0, N1, LAGGED>;
   static std::atomic<unsigned long long> attr{0};
   oncePerDevice(attr, [&] {
     TBT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -727,8 +726,13 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
     // The LS scratch reuses the ring and reduction space, never the mbarriers.
     if (need > static_cast<long long>(STAGES * C::STAGE + C::WORK)) return false;
     a.arnoldi = 1;
-    a.cycle = cycle ? 1 : 0;
-    if (cycle) a.prefetchAt = 0;  // the loop re-primes the ring at the end of every column
+    if (LAGGED) {
+      // Captured restart-cycle nodes, serialised programmatically (the
+      // stop flag is read after the programmatic wait).
+      a.pdl = c.usePdl ? 1 : 0;
+      a.skip = nullptr;
+      a.prefetchAt = 0;  // a skipped node drains the primed stages
+    }
     a.gm = *gm;
     a.lsS = lsS;
     a.lsDots = lsDots;
@@ -783,28 +787,62 @@ bool persistentSupported(const Ctx& c) {
   }
 }
 
+template <int M, int TC, int RCH, int STAGES, int N0, int N1>
+bool laggedFits(const Ctx& c, const GmresArgs& gm) {
+  using C = PCfg<M, TC, RCH, STAGES, N0, N1, true>;
+  const long long chunk = (static_cast<long long>(gm.ne) * gm.m + smCount(c.device) - 1) / smCount(c.device);
+  const long long need =
+      (gmresdev::arnoldiLSSmem(chunk, gm.restart) + gmresdev::RMAX + 2 + 3 * gmresdev::RMAX + 4 + 32) *
+      static_cast<long long>(sizeof(double2));
+  return need <= static_cast<long long>(STAGES * C::STAGE + C::WORK);
+}
+
+bool persistentLaggedFits(const Ctx& c, const GmresArgs& gm) {
+  if (!persistentSupported(c) || c.dist || gm.ncols != 1) return false;
+  switch (c.m * 1000000 + c.L0 * 1000 + c.L1) {
+    case 64064064: return laggedFits<64, 16, 32, 4, 64, 64>(c, gm);
+    case 64032032: return laggedFits<64, 16, 64, 2, 32, 32>(c, gm);
+    case 64016032: return laggedFits<64, 16, 64, 2, 16, 32>(c, gm);
+    case 128032016: return laggedFits<128, 32, 16, 4, 32, 16>(c, gm);
+    case 64128064: return laggedFits<64, 16, 64, 2, 128, 64>(c, gm);
+    case 64064128: return laggedFits<64, 16, 64, 2, 64, 128>(c, gm);
+    case 64128128: return laggedFits<64, 16, 64, 2, 128, 128>(c, gm);
+    case 128064064: return laggedFits<128, 32, 16, 4, 64, 64>(c, gm);
+    default: return false;
+  }
+}
+
 bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm,
-                           double2* lsS, double2* lsDots, double2* lsPart, bool cycle) {
+                           double2* lsS, double2* lsDots, double2* lsPart, bool lagged) {
   if (!persistentSupported(c) || c.dist) return false;
   const int key = c.m * 1000000 + c.L0 * 1000 + c.L1;
   switch (key) {
     // Ring shape: half blocks (32 rows) x 4 stages. Measured (C2 back to
     // back): 37.6 us; whole blocks x 2 38.2, half x 5 40.6, quarter x 8
     // 41.0, quarter x 11 47.1 — more bytes in flight per SM than 128 KB only
-    // slows the stream.
-    case 64064064: return launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 64032032: return launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 64016032: return launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 128128128: return launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 128032016: return launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 192256256: return launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 96128128: return launchP<96, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 64128064: return launchP<64, 16, 64, 2, 128, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 64064128: return launchP<64, 16, 64, 2, 64, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 64128128: return launchP<64, 16, 64, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 128064064: return launchP<128, 32, 16, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 128256256: return launchP<128, 32, 16, 4, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
-    case 192128128: return launchP<192, 32, 16, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart, cycle);
+    // slows the stream. LAGGED GMRES-step variants exist for the shapes whose
+    // LS row chunk can fit next to the ring (<= 2048 rows per CTA).
+    case 64064064: return lagged ? launchP<64, 16, 32, 4, 64, 64, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 32, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64032032: return lagged ? launchP<64, 16, 64, 2, 32, 32, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 64, 2, 32, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64016032: return lagged ? launchP<64, 16, 64, 2, 16, 32, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 64, 2, 16, 32>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128128128: return !lagged && launchP<128, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128032016: return lagged ? launchP<128, 32, 16, 4, 32, 16, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<128, 32, 16, 4, 32, 16>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 192256256: return !lagged && launchP<192, 32, 16, 2, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 96128128: return !lagged && launchP<96, 32, 16, 4, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64128064: return lagged ? launchP<64, 16, 64, 2, 128, 64, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 64, 2, 128, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64064128: return lagged ? launchP<64, 16, 64, 2, 64, 128, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 64, 2, 64, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 64128128: return lagged ? launchP<64, 16, 64, 2, 128, 128, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<64, 16, 64, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128064064: return lagged ? launchP<128, 32, 16, 4, 64, 64, true>(c, x, y, withCorr, gm, lsS, lsDots, lsPart)
+                         : launchP<128, 32, 16, 4, 64, 64>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 128256256: return !lagged && launchP<128, 32, 16, 4, 256, 256>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
+    case 192128128: return !lagged && launchP<192, 32, 16, 2, 128, 128>(c, x, y, withCorr, gm, lsS, lsDots, lsPart);
     default: return false;
   }
 }

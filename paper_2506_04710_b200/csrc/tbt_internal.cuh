@@ -299,7 +299,7 @@ bool applyUserLayout(Ctx& c, const double2* x, double2* y, int nrhs, bool withCo
 void launchBinProduct(Ctx& c, int nrhs);                      // binprod.cu
 void launchBinProductAnti(Ctx& c, int nrhs);                  // binprod.cu: FULL generators, yhat += A_a xhat
 int binprodVariant(int m);                                    // binprod.cu
-constexpr int kCtaTraceSlots = 8, kCtaTraceEvents = 12, kCtaTraceMaxGrid = 256;  // TBT_CTATRACE buffer shape
+constexpr int kCtaTraceSlots = 8, kCtaTraceEvents = 16, kCtaTraceMaxGrid = 256;  // TBT_CTATRACE buffer shape
 constexpr int kGemmMinRhs = 8;  // from this many columns on, K3 is the DMMA GEMM
 bool launchBinProductGemm(Ctx& c, int nrhs);                 // binprod_gemm.cu
 void launchCorrection(Ctx& c, const double2* x, double2* y, int nrhs);  // correction.cu
@@ -410,7 +410,10 @@ struct GmresWs;
 void freeGmresWorkspace(Ctx& c);  // gmres.cu
 bool launchPersistentApply(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArgs* gm = nullptr,
                            double2* lsS = nullptr, double2* lsDots = nullptr, double2* lsPart = nullptr,
-                           bool cycle = false);
+                           bool lagged = false);
+// A LAGGED (lagged-normalisation) GMRES-step instantiation exists for this
+// shape and its LS scratch fits next to the ring.
+bool persistentLaggedFits(const Ctx& c, const GmresArgs& gm);
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);

@@ -357,13 +357,13 @@ class ToeplitzMatvec:
 
     def cta_trace(self):
         """Per-CTA event times of the last 8 persistent applies (TBT_CTATRACE=1):
-        (launches, array [8 slots][12 events][256 CTAs] of uint64)."""
+        (launches, array [8 slots][16 events][256 CTAs] of uint64)."""
         import numpy as np
-        n = 8 * 12 * 256
+        n = 8 * 16 * 256
         buf = (C.c_ulonglong * n)()
         cnt = C.c_longlong()
         _check(lib().tbt_cta_trace(self._h, buf, n, C.byref(cnt)))
-        return cnt.value, np.frombuffer(buf, dtype=np.uint64).reshape(8, 12, 256).copy()
+        return cnt.value, np.frombuffer(buf, dtype=np.uint64).reshape(8, 16, 256).copy()
 
     def bench_apply(self, x_ptr: int, y_ptr: int, iters: int, use_graph: bool = True):
         ms, bms = C.c_double(), C.c_double()

@@ -5,8 +5,8 @@ process per setting; the knobs are read once per process):
   TBT_APPLY=multi     multi-launch apply instead of the persistent kernel
   TBT_GMRES=cols      column-blocked Arnoldi for a single column
   TBT_GMRES=unfused   separate apply / Arnoldi launches (no fused epilogue)
-  TBT_GMRES=graph     fused apply + Arnoldi per column, one captured graph per
-                      restart cycle (default: one persistent launch per cycle)
+  TBT_GMRES=nolag     fused apply + Arnoldi nodes without the lagged
+                      normalisation (normalise + Givens inside each node)
   TBT_COOP=1          every persistent apply launched cooperatively
   TBT_BINPROD=1       K3 v1 (no TMA ring), with TBT_APPLY=multi
   TBT_PDL=0           device-resident applies replayed from a CUDA graph
@@ -35,7 +35,7 @@ CASES = [
     ({"TBT_APPLY": "multi"}, ["apply", "gmres"]),
     ({"TBT_GMRES": "cols"}, ["gmres"]),
     ({"TBT_GMRES": "unfused"}, ["gmres"]),
-    ({"TBT_GMRES": "graph"}, ["gmres"]),
+    ({"TBT_GMRES": "nolag"}, ["gmres"]),
     ({"TBT_COOP": "1"}, ["apply", "gmres"]),
     ({"TBT_BINPROD": "1", "TBT_APPLY": "multi"}, ["apply"]),
     ({"TBT_PDL": "0"}, ["apply", "gmres"]),

@@ -1,0 +1,18 @@
+# Round-2 (second session) measurement: GPU suite, smoke, both bench arms,
+# every config, launch list of the bench command and --set full captures of
+# the top kernels (each command ran clean before its ncu pass).
+mkdir -p gpurun_out/r2b
+nproc; lscpu | grep "Model name"; nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv,noheader
+start=$(date +%s); timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -4; echo "gpu suite $(( $(date +%s) - start )) s"
+timeout 300 python __graft_entry__.py --smoke 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r2b/bench.json 2> gpurun_out/r2b/bench.err; echo "bench rc $?"
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r2b/bench_reference.json 2> gpurun_out/r2b/bench_reference.err; echo "ref rc $?"
+timeout 1500 python tools/bench_configs.py --configs C1,C2,C3,C4,C5,G48,G40 --out gpurun_out/r2b/configs.json > gpurun_out/r2b/configs.log 2>&1; echo "configs rc $?"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv --log-file gpurun_out/r2b/bench_launches.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-gmres --no-sharded --no-large > /dev/null 2>&1; echo "launches rc $?"
+NCU="ncu --set full --clock-control none --import-source on -f"
+$NCU -k regex:matvecPersistent -s 5 -c 1 -o gpurun_out/r2b/c2_persistent python tools/prof_apply.py --config C2 --iters 8 > /dev/null 2>&1; echo "c2 rc $?"
+$NCU -k regex:matvecPersistent -s 5 -c 1 -o gpurun_out/r2b/c4_persistent python tools/prof_apply.py --config C4 --iters 8 > /dev/null 2>&1; echo "c4 rc $?"
+$NCU -k regex:binprodGemm -s 2 -c 1 -o gpurun_out/r2b/c3_gemm python tools/prof_apply.py --config C3 --embed smooth --iters 4 > /dev/null 2>&1; echo "gemm rc $?"
+$NCU -k regex:regLineKernel -s 8 -c 4 -o gpurun_out/r2b/c3_reglines python tools/prof_apply.py --config C3 --embed smooth --iters 4 > /dev/null 2>&1; echo "reglines rc $?"
+$NCU -k regex:matvecPersistent -s 1 -c 1 -o gpurun_out/r2b/c2_gmres_cycle python tools/prof_gmres.py C2 50 > /dev/null 2>&1; echo "cycle rc $?"
+ls -la gpurun_out/r2b
