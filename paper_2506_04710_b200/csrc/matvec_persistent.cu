@@ -88,7 +88,7 @@ struct PArgs {
   double2* lsDots;
   double2* lsPart;
   unsigned long long* phaseNs;  // optional: globaltimer at phase boundaries (CTA 0)
-  unsigned long long* cta;      // optional (TBT_CTATRACE): per-CTA event times [12][gridDim.x] of this launch
+  unsigned long long* cta;      // optional (TBT_CTATRACE): per-CTA event times [16][256] of this launch
 };
 
 // Per-CTA trace (TBT_CTATRACE=1): 0 start, 1 after the PDL wait, 2+k / 6+k

@@ -130,7 +130,26 @@ def check_dist():
             q.close()
 
 
-CHECKS = {"apply": check_apply, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin,
+def check_many():
+    """tbt_apply_many over pinned and pageable C2 batches: bit-identical to
+    single applies, oracle parity on the first and last vector."""
+    import torch
+    cfg = CONFIGS["C2"]
+    rep = ToeplitzRep.synthetic(cfg)
+    op = ToeplitzMatvec(rep)
+    o = oracle.Oracle.from_rep(rep)
+    X = np.ascontiguousarray(gen.rhs_normal(cfg.n, 5, 9).T)
+    xt = torch.from_numpy(X.copy()).pin_memory()
+    yt = torch.empty_like(xt).pin_memory()
+    op.apply_many_ptr(xt.data_ptr(), yt.data_ptr(), 5)
+    for Y in (yt.numpy(), op.apply_many(X)):
+        for i in range(5):
+            assert np.array_equal(Y[i], op.apply(X[i])), ("many", i)
+        for i in (0, 4):
+            assert rel(Y[i], o.apply(X[i])) < 1e-11, ("many oracle", i)
+
+
+CHECKS = {"apply": check_apply, "many": check_many, "gmres": check_gmres, "smooth": check_smooth, "margin": check_margin,
           "wide": check_wide, "dist": check_dist}
 
 if __name__ == "__main__":

@@ -46,6 +46,23 @@ def test_apply_many_pinned(gpu):
             assert np.array_equal(Y[i], op.apply(X[i]))
 
 
+@pytest.mark.parametrize("count", [1, 2, 3, 16])
+def test_apply_many_pinned_every_vector(gpu, count):
+    """Pinned batches (two device slots per direction, copies on both copy
+    engines): every vector, first and last included, is bit-identical to a
+    single device-resident apply."""
+    import torch
+    cfg = CONFIGS["C2"]
+    op = ToeplitzMatvec(ToeplitzRep.synthetic(cfg))
+    X = np.ascontiguousarray(gen.rhs_normal(cfg.n, count, 40 + count).T)
+    xt = torch.from_numpy(X.copy()).pin_memory()
+    yt = torch.full_like(xt, complex("nan")).pin_memory()
+    op.apply_many_ptr(xt.data_ptr(), yt.data_ptr(), count)
+    Y = yt.numpy()
+    for i in range(count):
+        assert np.array_equal(Y[i], op.apply(X[i])), i
+
+
 def test_apply_many_full_layout_and_edges(gpu):
     from test_full_layout import _rep
     rep = _rep(5, 3, 24, 4)

@@ -30,7 +30,7 @@ import pytest
 SCRIPT = Path(__file__).resolve().parent / "env_paths_check.py"
 
 CASES = [
-    ({}, ["apply", "gmres", "smooth", "margin", "wide"]),  # the defaults (single after multi-column applies)
+    ({}, ["apply", "gmres", "smooth", "margin", "wide", "many"]),  # the defaults (single after multi-column applies)
     ({"TBT_FFT": "fused"}, ["wide"]),
     ({"TBT_APPLY": "multi"}, ["apply", "gmres"]),
     ({"TBT_GMRES": "cols"}, ["gmres"]),

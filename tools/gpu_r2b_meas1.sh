@@ -1,7 +1,12 @@
-# Round-2 (second session) measurement, part 1 (the GPU suite and smoke ran
-# green on the same code in tools/gpu_r2b_final.sh: 208 passed).
+# Round-2 (second session) measurement, part 1: GPU suite, smoke, both bench
+# arms, every config, the bench launch list and --set full captures of the
+# C2 / C4 persistent applies and the C3 DMMA GEMM (every ncu pass after the
+# same command ran clean). Part 2: tools/gpu_r2b_meas2.sh (the gpurun_out
+# limit is 64 MiB per call).
 mkdir -p gpurun_out/r2b
 nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv,noheader
+start=$(date +%s); timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -3; echo "gpu suite $(( $(date +%s) - start )) s"
+timeout 300 python __graft_entry__.py --smoke 2>&1 | tail -1
 timeout 900 python bench.py > gpurun_out/r2b/bench.json 2> gpurun_out/r2b/bench.err; echo "bench rc $?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r2b/bench_reference.json 2> gpurun_out/r2b/bench_reference.err; echo "ref rc $?"
 timeout 1500 python tools/bench_configs.py --configs C1,C2,C3,C4,C5,G48,G40 --out gpurun_out/r2b/configs.json > gpurun_out/r2b/configs.log 2>&1; echo "configs rc $?"
