@@ -276,6 +276,25 @@ std::vector<std::vector<std::array<int, 4>>> corrTermsByTarget(int nx, int ny) {
   return byTarget;
 }
 
+namespace {
+std::atomic<int> gLiveContexts[64];
+}
+void liveContextAdd(Ctx& c) {
+  if (c.device >= 0 && c.device < 64 && !c.countedLive) {
+    gLiveContexts[c.device].fetch_add(1);
+    c.countedLive = true;
+  }
+}
+void liveContextRemove(Ctx& c) {
+  if (c.countedLive) {
+    gLiveContexts[c.device].fetch_sub(1);
+    c.countedLive = false;
+  }
+}
+bool plainLaunchOk(const Ctx& c) {
+  return c.device >= 0 && c.device < 64 && gLiveContexts[c.device].load() == 1;
+}
+
 }  // namespace tbt
 
 using namespace tbt;
@@ -400,6 +419,7 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
       tbt_destroy(h);
       throw;
     }
+    liveContextAdd(h->c);
     *out = h;
   });
 }
@@ -407,6 +427,7 @@ tbt_status tbt_create(const tbt_desc* desc, tbt_ctx** out) {
 void tbt_destroy(tbt_ctx* h) {
   if (!h) return;
   Ctx& c = h->c;
+  liveContextRemove(c);
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
   for (void* p : {static_cast<void*>(c.dSpectra), static_cast<void*>(c.dSpectraAnti), static_cast<void*>(c.dGenAnti),

@@ -1456,7 +1456,7 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
     keyA.x = nullptr;
     keyA.j = 0;
     const int flags = (fuse ? 1 : 0) | (lowSync ? 2 : 0) | (fast ? 4 : 0) | (useAOnly ? 8 : 0) | (bigLS ? 16 : 0) |
-                      (lagged ? 32 : 0);
+                      (lagged ? 32 : 0) | (plainLaunchOk(c) ? 64 : 0);  // plain vs cooperative nodes
     if (useGraph && (!W.inner || std::memcmp(&keyA, &W.graphKey, sizeof(GmresArgs)) != 0 || W.graphFlags != flags)) {
       if (W.inner) cudaGraphExecDestroy(W.inner);
       W.inner = nullptr;

@@ -751,10 +751,11 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   // CTAs exit (its griddepcontrol.wait then covers the rest). So the first
   // apply of a context is launched cooperatively — it fails rather than
   // hangs if this process cannot have one CTA on every SM (e.g. an MPS SM
-  // limit) — and later PDL applies launch plainly with the same grid.
+  // limit) — and later PDL applies launch plainly with the same grid, as
+  // long as this is the only live context on the device (plainLaunchOk).
   // TBT_COOP=1 keeps every launch cooperative.
   static const bool forceCoop = getenv("TBT_COOP") && getenv("TBT_COOP")[0] == '1';
-  const bool coop = forceCoop || !a.pdl || !c.coopChecked;
+  const bool coop = forceCoop || !a.pdl || !c.coopChecked || !plainLaunchOk(c);
   cudaLaunchAttribute at[2];
   int na = 0;
   if (coop) {

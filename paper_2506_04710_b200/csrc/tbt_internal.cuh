@@ -153,6 +153,7 @@ struct Ctx {
   long long zeroCopyL2Bytes = 0;  // set around zero-copy launches: spectrum bytes to prefetch into L2
   bool zeroCopyStage = false;     // set around zero-copy launches: stage x in dXin for the correction reads
   bool coopChecked = false;      // a cooperative persistent launch succeeded on this context (co-residency)
+  bool countedLive = false;      // included in the live-context count of its device (plainLaunchOk)
   bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)
   const int* skipFlag = nullptr;  // device flag: persistent applies become no-ops when set
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply
@@ -417,6 +418,14 @@ bool persistentLaggedFits(const Ctx& c, const GmresArgs& gm);
 
 // Launch configuration helper: SM count of the context's device.
 int smCount(int device);
+// Context lifetime bookkeeping per device. Persistent kernels launch plainly
+// (not cooperatively) only while ONE context lives on the device: two
+// plain grid-barrier grids issued from different contexts' streams could
+// each end up partly resident and wait on each other forever, which a
+// cooperative launch rules out.
+void liveContextAdd(Ctx& c);
+void liveContextRemove(Ctx& c);
+bool plainLaunchOk(const Ctx& c);
 
 // Runs f (a cudaFuncSetAttribute call) once per device for the kernel that
 // owns `mask`: function attributes are per device, so a process driving
