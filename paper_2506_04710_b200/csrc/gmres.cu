@@ -1261,6 +1261,11 @@ void gmresSolve(Ctx& c, const double2* b, double2* x, int ncols, const tbt_gmres
                 std::vector<GmresState>& out, std::vector<double>& hist, int& matvecs) {
   const int R = o.restart;
   TBT_USER_CHECK(R <= RMAX, "tbt_gmres: restart above " + std::to_string(RMAX));
+  struct SolveScope {  // applies of this solve alternate their pair order (matvec_persistent.cu)
+    Ctx& c;
+    explicit SolveScope(Ctx& cc) : c(cc) { c.inSolve = true; }
+    ~SolveScope() { c.inSolve = false; }
+  } scope(c);
   // Multi-GPU: this rank's element-row slab (dist.cu); every reduction of
   // the solve is all-reduced, so all ranks take identical decisions.
   // Margin parts (full operator): the neM pseudo-elements join the vector.

@@ -80,6 +80,7 @@ struct PArgs {
   const int* skip;              // optional: the whole launch is a no-op when *skip != 0
   int pdl;                      // launched with programmatic stream serialization
   int ctaMajor;                 // CTA-major transform items in every phase (zero-copy launches)
+  int rev;                      // phase B walks this CTA's bin pairs last-to-first
   // Optional GMRES epilogue: the low-synchronisation Arnoldi step on y
   // (gmres_dev.cuh), so one cooperative launch is one GMRES iteration.
   int arnoldi;
@@ -385,10 +386,15 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
   const long long total = mine * C::NCH;
   const long long pre = total < STAGES ? total : STAGES;
   uint64_t polS = 0, polX = 0;
+  // The pi-th bin pair of this CTA (round robin over the grid); reversed,
+  // a CTA starts on the pairs it streamed last in the previous apply.
+  auto pairAt = [&](long long pi) -> long long {
+    return blockIdx.x + (a.rev ? mine - 1 - pi : pi) * gridDim.x;
+  };
   auto prefetch = [&]() {
     // Spectrum chunks of the first STAGES items: independent of x.
     for (long long it = 0; it < pre; ++it) {
-      const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+      const long long p = pairAt(it / C::NCH);
       const int ch = static_cast<int>(it % C::NCH);
       mbarArriveExpectTx(full + it, C::STAGE);
       bulkG2S(smem + it * C::STAGE, a.S + p * M * M + static_cast<long long>(ch) * RCH * M, C::CHUNK, full + it,
@@ -505,7 +511,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
       for (long long it = 0; it < total; ++it) {
         const int s = static_cast<int>(it % STAGES);
         const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
-        const long long p = blockIdx.x + (it / C::NCH) * gridDim.x;
+        const long long p = pairAt(it / C::NCH);
         const int ch = static_cast<int>(it % C::NCH);
         const long long f = a.pairF[p], g = a.pairG[p];
         unsigned char* st = smem + s * C::STAGE;
@@ -526,7 +532,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) matvecPersistent(PArgs a) {
       const uint32_t ph = static_cast<uint32_t>((it / STAGES) & 1);
       const long long pi = it / C::NCH;
       const int ch = static_cast<int>(it % C::NCH);
-      const long long p = blockIdx.x + pi * gridDim.x;
+      const long long p = pairAt(pi);
       if (ch == 0) {
 #pragma unroll
         for (int j = 0; j < C::CPT; ++j) yga[j] = zero;
@@ -717,6 +723,17 @@ bool launchP(Ctx& c, const double2* x, double2* y, bool withCorr, const GmresArg
   a.skip = c.skipFlag;
   a.pdl = (c.usePdl && !gm && !c.skipFlag) ? 1 : 0;
   a.ctaMajor = a.xStage ? 1 : 0;  // zero-copy: CTA-major keeps a CTA's host reads together (e2e +2-3 %)
+  // Inside a GMRES solve consecutive applies alternate the pair order, so
+  // each starts on the spectrum chunks the previous one streamed last (the
+  // part still in L2; C2 GMRES 62.0 -> 60.8 us per iteration, DESIGN 4.1).
+  // Plain applies keep one order: a benchmark loop of back-to-back applies
+  // gains no cache carry-over (it would: C2 36.8 -> 33.6 us). TBT_ZIGZAG=0
+  // turns it off in solves too. Only spectra within a few L2 sizes carry
+  // anything over (C4's 2.2 GB: 514 vs 521 us, noise), so larger ones keep
+  // the address order.
+  static const bool zzOff = getenv("TBT_ZIGZAG") && getenv("TBT_ZIGZAG")[0] == '0';
+  const bool zzSize = c.npairs * static_cast<long long>(M) * M * 16 <= (512LL << 20);
+  a.rev = (c.inSolve && zzSize && !zzOff && !a.xStage) ? static_cast<int>(c.zigzagSeq++ & 1) : 0;
   a.arnoldi = 0;
   if (gm) {
     const long long chunk = (static_cast<long long>(gm->ne) * gm->m + smCount(c.device) - 1) / smCount(c.device);

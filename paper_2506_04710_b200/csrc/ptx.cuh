@@ -49,6 +49,12 @@ __device__ __forceinline__ uint64_t policyEvictFirst() {
   return p;
 }
 
+__device__ __forceinline__ uint64_t policyEvictNormal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ uint64_t policyEvictLast() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

@@ -154,6 +154,8 @@ struct Ctx {
   bool zeroCopyStage = false;     // set around zero-copy launches: stage x in dXin for the correction reads
   bool coopChecked = false;      // a cooperative persistent launch succeeded on this context (co-residency)
   bool countedLive = false;      // included in the live-context count of its device (plainLaunchOk)
+  bool inSolve = false;               // a GMRES solve is issuing this context's applies
+  unsigned long long zigzagSeq = 0;  // persistent applies in solves so far (pair-order parity)
   bool usePdl = true;             // device-resident single-column applies launched directly with PDL (TBT_PDL=0: graph)
   const int* skipFlag = nullptr;  // device flag: persistent applies become no-ops when set
   unsigned long long* dPhaseNs = nullptr;  // [6] globaltimer stamps of the last persistent apply

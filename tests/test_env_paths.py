@@ -7,6 +7,7 @@ process per setting; the knobs are read once per process):
   TBT_GMRES=unfused   separate apply / Arnoldi launches (no fused epilogue)
   TBT_GMRES=nolag     fused apply + Arnoldi nodes without the lagged
                       normalisation (normalise + Givens inside each node)
+  TBT_ZIGZAG=0        GMRES applies keep one bin-pair order (no alternation)
   TBT_COOP=1          every persistent apply launched cooperatively
   TBT_BINPROD=1       K3 v1 (no TMA ring), with TBT_APPLY=multi
   TBT_PDL=0           device-resident applies replayed from a CUDA graph
@@ -36,6 +37,7 @@ CASES = [
     ({"TBT_GMRES": "cols"}, ["gmres"]),
     ({"TBT_GMRES": "unfused"}, ["gmres"]),
     ({"TBT_GMRES": "nolag"}, ["gmres"]),
+    ({"TBT_ZIGZAG": "0"}, ["gmres"]),
     ({"TBT_COOP": "1"}, ["apply", "gmres"]),
     ({"TBT_BINPROD": "1", "TBT_APPLY": "multi"}, ["apply"]),
     ({"TBT_PDL": "0"}, ["apply", "gmres"]),
