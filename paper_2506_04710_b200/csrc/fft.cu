@@ -87,7 +87,10 @@ fftPassKernel(FftPass p) {
 // line in flight. The N = R1 * R2 transform runs in registers: R2 radix-R1
 // DFTs over the decimated inputs, the twiddles w_N^(n2 k1) (table), then R1
 // radix-R2 DFTs; natural order in and out. No shared memory, no barriers.
-template <int N, bool INV>
+// CROP (inverse passes that keep n_out <= ceil(N/2) points, i.e. every
+// embedding's crop): the unused outputs and their arithmetic drop out at
+// compile time, and the registers they held carry the correction values.
+template <int N, bool INV, bool CROP>
 __global__ void __launch_bounds__(128, (N >= 48 ? 1 : N >= 24 ? 3 : 4)) regLineKernel(FftPass p) {
   using S = fftreg::Split<N>;
   constexpr int R1 = S::R1, R2 = S::R2;
@@ -105,6 +108,14 @@ __global__ void __launch_bounds__(128, (N >= 48 ? 1 : N >= 24 ? 3 : 4)) regLineK
     for (int n2 = 0; n2 < R2; ++n2) {
       const int pt = R2 * n1 + n2;
       t[n2][n1] = pt < p.n_in ? ldg2(in + static_cast<long long>(pt) * inStride) : make_double2(0.0, 0.0);
+    }
+  // Which output points carry correction terms (a mask for this line), read
+  // while the line's own loads are in flight.
+  unsigned long long targets = 0;
+  if (p.ycorr)
+    for (int pt = 0; pt < p.n_out && pt < 64; ++pt) {
+      const int e = line * p.corrNx + pt;
+      if (__ldg(p.tPtr + e) != __ldg(p.tPtr + e + 1)) targets |= 1ull << pt;
     }
 #pragma unroll
   for (int n2 = 0; n2 < R2; ++n2) dftReg<R1, INV>(t[n2]);  // -> t[n2][k1]
@@ -128,36 +139,49 @@ __global__ void __launch_bounds__(128, (N >= 48 ? 1 : N >= 24 ? 3 : 4)) regLineK
 #pragma unroll
     for (int n2 = 0; n2 < R2; ++n2) t[n2][k1] = v[n2];  // t[k2][k1] = X[k1 + R1 k2]
   }
-  // Which output points carry correction terms (a mask for this line, read
-  // once), then every correction load of the thread in flight together.
-  unsigned long long targets = 0;
-  if (p.ycorr)
-    for (int pt = 0; pt < p.n_out && pt < 64; ++pt) {
-      const int e = line * p.corrNx + pt;
-      if (__ldg(p.tPtr + e) != __ldg(p.tPtr + e + 1)) targets |= 1ull << pt;
-    }
+  // ycorr is internal [e][B]: e * B + bg = line * out_line_stride + pt * out_point_stride + bg
+  constexpr int NC = (N + 1) / 2;
+  const double2* yc = p.ycorr + line * p.out_line_stride + bg;
+  if constexpr (CROP) {
+    // Every correction load of the thread goes out before the first store
+    // (read-only loads, so the stores do not order them; one at a time they
+    // were 18 serial latencies per thread, half of the last pass's time in
+    // ncu's stall samples).
+    double2 cv[NC];
 #pragma unroll
-  for (int k2 = 0; k2 < R2; ++k2)
+    for (int pt = 0; pt < NC; ++pt)
+      cv[pt] = (targets >> pt) & 1ull ? ldg2(yc + static_cast<long long>(pt) * p.out_point_stride) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      const int pt = k1 + R1 * k2;
-      if (pt < p.n_out) {
-        double2 o = cscale(t[k2][k1], p.scale);
-        // ycorr is internal [e][B]: e * B + bg = line * out_line_stride + pt * out_point_stride + bg
-        if ((targets >> pt) & 1ull)
-          o = cadd(o, p.ycorr[line * p.out_line_stride + static_cast<long long>(pt) * p.out_point_stride + bg]);
-        out[static_cast<long long>(pt) * outStride] = o;
+    for (int k2 = 0; k2 < R2; ++k2)
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int pt = k1 + R1 * k2;
+        if (pt < NC && pt < p.n_out) out[static_cast<long long>(pt) * outStride] = cadd(cscale(t[k2][k1], p.scale), cv[pt]);
       }
-    }
+  } else {
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2)
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int pt = k1 + R1 * k2;
+        if (pt < p.n_out) {
+          double2 o = cscale(t[k2][k1], p.scale);
+          if ((targets >> pt) & 1ull) o = cadd(o, ldg2(yc + static_cast<long long>(pt) * p.out_point_stride));
+          out[static_cast<long long>(pt) * outStride] = o;
+        }
+      }
+  }
 }
 
 template <int N>
 void launchReg(const FftPass& p, cudaStream_t s) {
   dim3 grid((p.batch + 127) / 128, p.lines);
-  if (p.inverse)
-    regLineKernel<N, true><<<grid, 128, 0, s>>>(p);
+  if (!p.inverse)
+    regLineKernel<N, false, false><<<grid, 128, 0, s>>>(p);
+  else if (p.n_out <= (N + 1) / 2)
+    regLineKernel<N, true, true><<<grid, 128, 0, s>>>(p);
   else
-    regLineKernel<N, false><<<grid, 128, 0, s>>>(p);
+    regLineKernel<N, true, false><<<grid, 128, 0, s>>>(p);
 }
 
 template <int R1, int R2, int BC>
