@@ -221,7 +221,7 @@ struct Gemm2Cfg {
 };
 
 // item = (((p * 2 + t) * nTiles + tile) * (M / RC2) + h); h selects the 64-row part.
-template <int M, int NST>
+template <int M, int NST, bool LATE>
 __global__ void __launch_bounds__(NT2, 2)
 binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const int* __restrict__ pairG,
              long long npairs, const double2* __restrict__ xhat, double2* __restrict__ yhat, int nrhs) {
@@ -257,9 +257,8 @@ binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const
 #pragma unroll
       for (int q = 0; q < 3; ++q) acc[a][b][q][0] = acc[a][b][q][1] = 0.0;
 
-  auto load = [&](int kc) {
+  auto loadA = [&](int kc) {
     double2* sA = gsm + (kc % NST) * C::STAGE;
-    double2* sB = sA + C::A_ELEMS;
     const int k0 = kc * KC2;
     if (t == 0) {  // sA[i][k] = A[i0 + i][k0 + k]
 #pragma unroll
@@ -274,6 +273,10 @@ binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const
         cpAsync16(sA + k * (RC2 + PADT) + i, A + static_cast<long long>(k0 + k) * M + i0 + i, true);
       }
     }
+  };
+  auto loadB = [&](int kc) {
+    double2* sB = gsm + (kc % NST) * C::STAGE + C::A_ELEMS;
+    const int k0 = kc * KC2;
 #pragma unroll
     for (int q = threadIdx.x; q < NTILE * KC2; q += NT2) {  // sB[n][k] = X[n0+n][k0+k]
       const int n = q / KC2, k = q % KC2;
@@ -285,14 +288,26 @@ binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const
   constexpr int NKC = M / KC2;
 #pragma unroll
   for (int q = 0; q < NST - 1; ++q) {
-    load(q);
+    loadA(q);
+    loadB(q);
     cpCommit();
   }
   for (int kc = 0; kc < NKC; ++kc) {
     cpWait<NST - 2>();  // this thread's pieces of chunk kc have landed
     __syncthreads();    // everyone's have, and everyone is done with chunk kc - 1
-    if (kc + NST - 1 < NKC) load(kc + NST - 1);  // into chunk kc - 1's buffer
-    cpCommit();                                  // (an empty group keeps the wait count uniform)
+    // Chunk kc + NST - 1 goes into chunk kc - 1's buffer. LATE: its cp.async
+    // pieces and their address arithmetic are issued between this chunk's
+    // DMMA groups (A after the first k step, X after the second) instead of
+    // ahead of them, where every warp of the CTA did that work with the pipe
+    // idle right after the barrier.
+    const bool more = kc + NST - 1 < NKC;
+    if (!LATE) {
+      if (more) {
+        loadA(kc + NST - 1);
+        loadB(kc + NST - 1);
+      }
+      cpCommit();  // (an empty group keeps the wait count uniform)
+    }
     const double2* sA = gsm + (kc % NST) * C::STAGE;
     const double2* sB = sA + C::A_ELEMS;
 #pragma unroll
@@ -322,6 +337,11 @@ binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const
           dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
         }
       }
+      if (LATE && kk == 0 && more) loadA(kc + NST - 1);
+      if (LATE && kk == 4) {
+        if (more) loadB(kc + NST - 1);
+        cpCommit();
+      }
     }
   }
   // D fragment: row gid, columns 2*tig + {0,1}; Y[n][i] (column n contiguous).
@@ -340,30 +360,33 @@ binprodGemm2(const double2* __restrict__ S, const int* __restrict__ pairF, const
   }
 }
 
-template <int M, int NST>
+template <int M, int NST, bool LATE>
 void launchGemm2(Ctx& c, int nrhs) {
   using C = Gemm2Cfg<NST>;
   static std::atomic<unsigned long long> attr{0};
   oncePerDevice(attr, [] {
-    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm2<M, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm2<M, NST, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(C::SMEM)));
-    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm2<M, NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(binprodGemm2<M, NST, LATE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         cudaSharedmemCarveoutMaxShared));
   });
   const int nTiles = (nrhs + NTILE - 1) / NTILE;
   const long long items = c.npairs * 2 * nTiles * (M / RC2);
-  binprodGemm2<M, NST><<<static_cast<unsigned>(items), NT2, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG,
+  binprodGemm2<M, NST, LATE><<<static_cast<unsigned>(items), NT2, C::SMEM, c.stream>>>(c.dSpectra, c.dPairF, c.dPairG,
                                                                                 c.npairs, c.dXhat, c.dYhat, nrhs);
 }
 
 // TBT_GEMM: "4m" the 4M form; "wide" the one-CTA-per-SM 3M kernel; default
-// for m = 128 (and "pair3" with a 3-stage ring) the two-CTAs-per-SM kernel.
+// for m = 128 the two-CTAs-per-SM kernel, 2-stage ring, late cp.async issue
+// ("late3": 3-stage ring; "pair2" / "pair3": loads issued ahead of the chunk).
 int gemmShape() {
   static const int v = [] {
     const char* e = getenv("TBT_GEMM");
     if (e && strcmp(e, "wide") == 0) return 0;
+    if (e && strcmp(e, "pair2") == 0) return 2;
     if (e && strcmp(e, "pair3") == 0) return 3;
-    return 2;
+    if (e && strcmp(e, "late3") == 0) return 13;
+    return 12;
   }();
   return v;
 }
@@ -381,7 +404,12 @@ int gemm4m() {
 bool launchBinProductGemm(Ctx& c, int nrhs) {
   const int four = gemm4m();
   if (c.m == 128 && !four && gemmShape()) {
-    gemmShape() == 3 ? launchGemm2<128, 3>(c, nrhs) : launchGemm2<128, 2>(c, nrhs);
+    switch (gemmShape()) {
+      case 2: launchGemm2<128, 2, false>(c, nrhs); break;
+      case 3: launchGemm2<128, 3, false>(c, nrhs); break;
+      case 13: launchGemm2<128, 3, true>(c, nrhs); break;
+      default: launchGemm2<128, 2, true>(c, nrhs);
+    }
     TBT_CUDA_CHECK(cudaGetLastError());
     return true;
   }

@@ -18,9 +18,11 @@ process per setting; the knobs are read once per process):
   TBT_E2E=staged      host applies through explicit copies, not zero-copy
   TBT_MARGIN_UNFUSED=1  separate margin B / B^T kernels for one column
   TBT_GEMM=4m         4M complex DMMA GEMM for many right-hand sides
-  TBT_GEMM=wide|pair3  3M GEMM at m = 128 as one 8-warp CTA per SM / as two
-                      4-warp CTAs per SM with a 3-stage ring (default: two
-                      4-warp CTAs, 64-row tiles, 2-stage cp.async ring)
+  TBT_GEMM=wide|pair2|pair3|late3  3M GEMM at m = 128 as one 8-warp CTA per
+                      SM / as two 4-warp CTAs per SM with the chunk loads
+                      issued ahead of the chunk (2- / 3-stage ring) or
+                      between its DMMA groups with a 3-stage ring (default:
+                      two 4-warp CTAs, 2-stage ring, loads between the groups)
   TBT_DIST_CHUNKS=k   sharded apply with k overlapped exchange chunks
                       (default 2 at P > 1, 1 at P = 1)
 """
@@ -50,7 +52,9 @@ CASES = [
     ({"TBT_MARGIN_UNFUSED": "1"}, ["margin"]),
     ({"TBT_GEMM": "4m"}, ["wide", "smooth"]),
     ({"TBT_GEMM": "wide"}, ["wide"]),
+    ({"TBT_GEMM": "pair2"}, ["wide"]),
     ({"TBT_GEMM": "pair3"}, ["wide"]),
+    ({"TBT_GEMM": "late3"}, ["wide"]),
     ({}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "2"}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "4"}, ["dist"]),
