@@ -9,6 +9,8 @@
 //  * the antisymmetric part K of Z(0,0) (see spectra.cu): y_e += K x_e.
 // Internal vector layout is [element][rhs][basis].
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 
 #include "tbt_internal.cuh"
 
@@ -104,20 +106,30 @@ __global__ void __launch_bounds__(256) corrFused(const int* __restrict__ termInf
   }
 }
 
-// Many right-hand sides: one CTA per (target, chunk of 32 columns). Each
+// Many right-hand sides: one CTA per (target, chunk of 8*RPW columns). Each
 // term's d, U, V (rank RANK, m = 32*KPL) are staged once in shared memory and
-// reused by all 32 columns of the chunk (instead of once per column); every
-// warp owns 4 columns whose sums stay in registers across the term list.
-template <int KPL, int RANK>
-__global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInfo, const int* __restrict__ targetList,
-                                                 const int* __restrict__ targetPtr, const double2* __restrict__ D,
-                                                 const double2* __restrict__ U, const double2* __restrict__ V,
-                                                 const double2* __restrict__ x, double2* __restrict__ ycorr,
-                                                 int nrhs, long long xE, long long xR) {
+// reused by all columns of the chunk (instead of once per column); every
+// warp owns RPW columns whose sums stay in registers across the term list.
+// The term list is a latency chain (stage, barrier, x loads, rank loop with
+// warp reductions): the next term's d, U, V arrive through a second cp.async
+// stage and its x values are loaded before the current term's arithmetic,
+// and RPW = 2 keeps two CTAs (16 warps) on an SM. With RPW = 4, one stage and
+// one CTA per SM the kernel took 136 us at C3 and, although on a side stream,
+// cost 108 us of the 663 us apply.
+__device__ __forceinline__ void corrCpAsync16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int KPL, int RANK, int RPW>
+__global__ void __launch_bounds__(256, RPW <= 2 ? 2 : 1)
+corrMulti(const int* __restrict__ termInfo, const int* __restrict__ targetList, const int* __restrict__ targetPtr,
+          const double2* __restrict__ D, const double2* __restrict__ U, const double2* __restrict__ V,
+          const double2* __restrict__ x, double2* __restrict__ ycorr, int nrhs, long long xE, long long xR) {
   constexpr int M = 32 * KPL;
-  constexpr int RPW = 4;  // columns per warp
   constexpr int RC = 8 * RPW;
-  __shared__ double2 sW[RANK][M], sW2[RANK][M], sD[M];
+  constexpr int STG = (2 * RANK + 1) * M;  // W, W2, d
+  extern __shared__ __align__(16) double2 csm[];  // [2][STG]
   const int ti = blockIdx.x;
   const int r0 = blockIdx.y * RC;
   const int e = targetList[ti];
@@ -128,21 +140,21 @@ __global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInf
   for (int j = 0; j < RPW; ++j)
 #pragma unroll
     for (int k = 0; k < KPL; ++k) acc[j][k] = make_double2(0.0, 0.0);
-  for (int t = t0; t < t1; ++t) {
-    const int src = termInfo[4 * t + 1], slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+
+  auto stage = [&](int t, int st) {
+    const int slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
     const double2* W = (trans ? U : V) + static_cast<long long>(slot) * RANK * M;
     const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * RANK * M;
-    __syncthreads();
-    for (int q = threadIdx.x; q < RANK * M; q += blockDim.x) {
-      (&sW[0][0])[q] = __ldg(W + q);
-      (&sW2[0][0])[q] = __ldg(W2 + q);
+    double2* sW = csm + st * STG;
+    for (int q = threadIdx.x; q < RANK * M; q += 256) {
+      corrCpAsync16(sW + q, W + q);
+      corrCpAsync16(sW + RANK * M + q, W2 + q);
     }
-    for (int q = threadIdx.x; q < M; q += blockDim.x) sD[q] = __ldg(D + static_cast<long long>(slot) * M + q);
-    __syncthreads();
-    // All RPW columns advance together through the rank loop: one shared
-    // memory read of U/V row q serves RPW columns, and the RPW butterfly
-    // reductions interleave.
-    double2 xv[RPW][KPL];
+    for (int q = threadIdx.x; q < M; q += 256) corrCpAsync16(sW + 2 * RANK * M + q, D + static_cast<long long>(slot) * M + q);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto loadX = [&](int t, double2 (&xv)[RPW][KPL]) {
+    const int src = termInfo[4 * t + 1];
 #pragma unroll
     for (int j = 0; j < RPW; ++j) {
       const int r = r0 + warp * RPW + j;
@@ -150,36 +162,93 @@ __global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInf
 #pragma unroll
       for (int k = 0; k < KPL; ++k) xv[j][k] = r < nrhs ? __ldg(xs + lane + 32 * k) : make_double2(0.0, 0.0);
     }
+  };
+
+  double2 xv[RPW][KPL], xn[RPW][KPL];
+  if (t0 < t1) {
+    stage(t0, 0);
+    loadX(t0, xv);
+  }
+  for (int t = t0; t < t1; ++t) {
+    const int st = (t - t0) & 1;
+    if (t + 1 < t1) {
+      stage(t + 1, st ^ 1);  // read last in iteration t - 1, which ended with a barrier
+      loadX(t + 1, xn);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double2* sW = csm + st * STG;
+    const double2* sW2 = sW + RANK * M;
+    const double2* sD = sW2 + RANK * M;
+    // All RPW columns advance together through the rank loop: one shared
+    // memory read of U/V row q serves RPW columns.
 #pragma unroll
     for (int k = 0; k < KPL; ++k) {
       const double2 d = sD[lane + 32 * k];
 #pragma unroll
       for (int j = 0; j < RPW; ++j) cfma(acc[j][k], d, xv[j][k]);
     }
+    // Rank rows in groups of four: the four projections of a column are
+    // reduced together (lanes trade two values at offset 16, one at offset
+    // 8, then a 3-level butterfly on the single remaining value; the totals
+    // come back by indexed shuffles): 10 shuffles and 6 additions per value
+    // pair and group instead of 20 and 20 with one butterfly per row.
 #pragma unroll 1
-    for (int q = 0; q < RANK; ++q) {
-      double2 p[RPW];
+    for (int q0 = 0; q0 < RANK; q0 += 4) {
+      double2 p[4][RPW];
 #pragma unroll
-      for (int j = 0; j < RPW; ++j) p[j] = make_double2(0.0, 0.0);
+      for (int i = 0; i < 4; ++i) {
 #pragma unroll
-      for (int k = 0; k < KPL; ++k) {
-        const double2 w = sW[q][lane + 32 * k];
+        for (int j = 0; j < RPW; ++j) p[i][j] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < RPW; ++j) cfma(p[j], w, xv[j][k]);
-      }
+        for (int k = 0; k < KPL; ++k) {
+          const double2 w = sW[(q0 + i) * M + lane + 32 * k];
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-        for (int j = 0; j < RPW; ++j) {
-          p[j].x += __shfl_xor_sync(0xffffffffu, p[j].x, off);
-          p[j].y += __shfl_xor_sync(0xffffffffu, p[j].y, off);
+          for (int j = 0; j < RPW; ++j) cfma(p[i][j], w, xv[j][k]);
         }
-#pragma unroll
-      for (int k = 0; k < KPL; ++k) {
-        const double2 w2 = sW2[q][lane + 32 * k];
-#pragma unroll
-        for (int j = 0; j < RPW; ++j) cfma(acc[j][k], w2, p[j]);
       }
+      const bool b4 = lane & 16, b3 = lane & 8;
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const double2 s0 = b4 ? p[0][j] : p[2][j], s1 = b4 ? p[1][j] : p[3][j];
+        double2 r0 = b4 ? p[2][j] : p[0][j], r1 = b4 ? p[3][j] : p[1][j];
+        r0.x += __shfl_xor_sync(0xffffffffu, s0.x, 16);
+        r0.y += __shfl_xor_sync(0xffffffffu, s0.y, 16);
+        r1.x += __shfl_xor_sync(0xffffffffu, s1.x, 16);
+        r1.y += __shfl_xor_sync(0xffffffffu, s1.y, 16);
+        const double2 s = b3 ? r0 : r1;
+        double2 v = b3 ? r1 : r0;
+        v.x += __shfl_xor_sync(0xffffffffu, s.x, 8);
+        v.y += __shfl_xor_sync(0xffffffffu, s.y, 8);
+#pragma unroll
+        for (int off = 4; off >= 1; off >>= 1) {
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+        }
+        // lane l now holds the total of row q0 + (l >> 3)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          p[i][j].x = __shfl_sync(0xffffffffu, v.x, 8 * i);
+          p[i][j].y = __shfl_sync(0xffffffffu, v.y, 8 * i);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+          const double2 w2 = sW2[(q0 + i) * M + lane + 32 * k];
+#pragma unroll
+          for (int j = 0; j < RPW; ++j) cfma(acc[j][k], w2, p[i][j]);
+        }
+    }
+    __syncthreads();  // stage st is refilled in the next iteration
+    if (t + 1 < t1) {
+#pragma unroll
+      for (int j = 0; j < RPW; ++j)
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) xv[j][k] = xn[j][k];
     }
   }
 #pragma unroll
@@ -188,6 +257,40 @@ __global__ void __launch_bounds__(256) corrMulti(const int* __restrict__ termInf
     if (r >= nrhs) break;
 #pragma unroll
     for (int k = 0; k < KPL; ++k) ycorr[(static_cast<long long>(e) * nrhs + r) * M + lane + 32 * k] = acc[j][k];
+  }
+}
+
+template <int KPL, int RANK, int RPW>
+void launchCorrMulti(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                     long long xE, long long xR) {
+  constexpr size_t SMEM = 2 * (2 * RANK + 1) * 32 * KPL * sizeof(double2);
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [] {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(corrMulti<KPL, RANK, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(SMEM)));
+  });
+  dim3 grid(t.nTargets, (nrhs + 8 * RPW - 1) / (8 * RPW));
+  corrMulti<KPL, RANK, RPW><<<grid, 256, SMEM, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU,
+                                                    c.dCorrV, x, ycorr, nrhs, xE, xR);
+}
+
+// Columns per warp of corrMulti (TBT_CORR_RPW = 1 | 2 | 4; default 2).
+int corrRpw() {
+  static const int v = [] {
+    const char* e = getenv("TBT_CORR_RPW");
+    const int r = e ? atoi(e) : 2;
+    return r == 1 || r == 4 ? r : 2;
+  }();
+  return v;
+}
+
+template <int KPL, int RANK>
+void launchCorrMultiRpw(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                        long long xE, long long xR) {
+  switch (corrRpw()) {
+    case 1: launchCorrMulti<KPL, RANK, 1>(c, t, x, ycorr, nrhs, s, xE, xR); break;
+    case 4: launchCorrMulti<KPL, RANK, 4>(c, t, x, ycorr, nrhs, s, xE, xR); break;
+    default: launchCorrMulti<KPL, RANK, 2>(c, t, x, ycorr, nrhs, s, xE, xR);
   }
 }
 
@@ -215,10 +318,12 @@ void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* 
   const long long xE = xUserN > 0 ? c.m : static_cast<long long>(nrhs) * c.m;
   const long long xR = xUserN > 0 ? xUserN : c.m;
   if (nrhs >= 8 && (c.rank == 4 || c.rank == 8) && (c.m == 64 || c.m == 128)) {
-    dim3 grid(t.nTargets, (nrhs + 31) / 32);
-    auto k = c.m == 64 ? (c.rank == 4 ? corrMulti<2, 4> : corrMulti<2, 8>)
-                       : (c.rank == 4 ? corrMulti<4, 4> : corrMulti<4, 8>);
-    k<<<grid, 256, 0, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU, c.dCorrV, x, ycorr, nrhs, xE, xR);
+    if (c.m == 64)
+      c.rank == 4 ? launchCorrMultiRpw<2, 4>(c, t, x, ycorr, nrhs, s, xE, xR)
+                  : launchCorrMultiRpw<2, 8>(c, t, x, ycorr, nrhs, s, xE, xR);
+    else
+      c.rank == 4 ? launchCorrMultiRpw<4, 4>(c, t, x, ycorr, nrhs, s, xE, xR)
+                  : launchCorrMultiRpw<4, 8>(c, t, x, ycorr, nrhs, s, xE, xR);
     TBT_CUDA_CHECK(cudaGetLastError());
     return;
   }
