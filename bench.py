@@ -69,12 +69,12 @@ def measured_hbm():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
 
 
-TRAFFIC_FILES = ("r2c_traffic.json", "r2b_traffic.json", "r2_traffic.json", "r1_traffic.json")  # newest capture first
+TRAFFIC_FILES = ("r2d_traffic.json", "r2c_traffic.json", "r2b_traffic.json", "r2_traffic.json", "r1_traffic.json")  # newest capture first
 
 
 def ncu_traffic(key):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (the newest of profiles/r2c, r2b, r2, r1 _traffic.json), and the file it came from."""
+    capture (the newest of profiles/r2d, r2c, r2b, r2, r1 _traffic.json), and the file it came from."""
     for name in TRAFFIC_FILES:
         try:
             return json.loads((REPO / "profiles" / name).read_text())[key]["dram_bytes_per_launch"], name
