@@ -704,6 +704,13 @@ tbt_status tbt_set_correction(tbt_ctx* h, int rank, const double* d, const doubl
     for (size_t k = 0; k + 1 < ptr.size(); ++k) c.maxTermsPerTarget = std::max(c.maxTermsPerTarget, ptr[k + 1] - ptr[k]);
     if (c.nTerms > 0) {
       TBT_CUDA_CHECK(cudaMalloc(&c.dTermInfo, info.size() * sizeof(int)));
+      // [nTargets] target elements, then [nTargets] target indices by descending
+      // term count (the many-column kernels launch their longest CTAs first)
+      std::vector<int> order(targets.size());
+      for (size_t k = 0; k < order.size(); ++k) order[k] = static_cast<int>(k);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b]; });
+      targets.insert(targets.end(), order.begin(), order.end());
       TBT_CUDA_CHECK(cudaMalloc(&c.dTargetList, targets.size() * sizeof(int)));
       TBT_CUDA_CHECK(cudaMalloc(&c.dTargetPtr, ptr.size() * sizeof(int)));
       uploadSync(c.dTermInfo, info.data(), info.size() * sizeof(int), c.stream);

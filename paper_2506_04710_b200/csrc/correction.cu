@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <string>
 
 #include "tbt_internal.cuh"
 
@@ -124,14 +125,14 @@ __device__ __forceinline__ void corrCpAsync16(void* dst, const void* src) {
 template <int KPL, int RANK, int RPW>
 __global__ void __launch_bounds__(256, RPW <= 2 ? 2 : 1)
 corrMulti(const int* __restrict__ termInfo, const int* __restrict__ targetList, const int* __restrict__ targetPtr,
-          const double2* __restrict__ D, const double2* __restrict__ U, const double2* __restrict__ V,
+          const int* __restrict__ order, const double2* __restrict__ D, const double2* __restrict__ U, const double2* __restrict__ V,
           const double2* __restrict__ x, double2* __restrict__ ycorr, int nrhs, long long xE, long long xR) {
   constexpr int M = 32 * KPL;
   constexpr int RC = 8 * RPW;
   constexpr int STG = (2 * RANK + 1) * M;  // W, W2, d
   extern __shared__ __align__(16) double2 csm[];  // [2][STG]
-  const int ti = blockIdx.x;
-  const int r0 = blockIdx.y * RC;
+  const int ti = order ? order[blockIdx.y] : blockIdx.y;  // grid (column chunks, targets): a target's chunks adjacent
+  const int r0 = blockIdx.x * RC;
   const int e = targetList[ti];
   const int t0 = targetPtr[ti], t1 = targetPtr[ti + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -269,9 +270,175 @@ void launchCorrMulti(Ctx& c, const CorrTables& t, const double2* x, double2* yco
     TBT_CUDA_CHECK(cudaFuncSetAttribute(corrMulti<KPL, RANK, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(SMEM)));
   });
-  dim3 grid(t.nTargets, (nrhs + 8 * RPW - 1) / (8 * RPW));
-  corrMulti<KPL, RANK, RPW><<<grid, 256, SMEM, s>>>(t.termInfo, t.targetList, t.targetPtr, c.dCorrD, c.dCorrU,
-                                                    c.dCorrV, x, ycorr, nrhs, xE, xR);
+  dim3 grid((nrhs + 8 * RPW - 1) / (8 * RPW), t.nTargets);
+  corrMulti<KPL, RANK, RPW><<<grid, 256, SMEM, s>>>(t.termInfo, t.targetList, t.targetPtr, t.order, c.dCorrD,
+                                                    c.dCorrU, c.dCorrV, x, ycorr, nrhs, xE, xR);
+}
+
+// Rank-8 terms on the FP64 tensor path (the default; TBT_CORR=vec selects
+// corrMulti): a warp owns 8
+// columns; per term P(8 x 8 cols) = W(8 x m) X(m x 8 cols) and
+// Y(m x 8 cols) += W2^T(m x 8) P as mma.sync.m8n8k4.f64 tiles (4M complex
+// form: four real DMMAs per complex tile), X fragments straight from global
+// memory (each value is used once per warp), P turned from the accumulator
+// layout into the B-operand layout through 1 KB of warp-private shared
+// memory; the diagonal term stays on DFMA. No cross-lane reductions.
+__device__ __forceinline__ void corrDmmaOp(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int KPL>
+__global__ void __launch_bounds__(128, 2)
+corrDmma(const int* __restrict__ termInfo, const int* __restrict__ targetList, const int* __restrict__ targetPtr,
+         const int* __restrict__ order, const double2* __restrict__ D, const double2* __restrict__ U, const double2* __restrict__ V,
+         const double2* __restrict__ x, double2* __restrict__ ycorr, int nrhs, long long xE, long long xR) {
+  constexpr int M = 32 * KPL, RANK = 8, MBLK = M / 8;
+  constexpr int LDW = M + 4, LDW2 = M + 2;  // row pitches: conflict-free A fragments of W (rows = q) and W2 (k = q)
+  constexpr int STG = RANK * LDW + RANK * LDW2 + M;
+  constexpr int NBAT = M / 16;  // batches of 4 k steps = 16 basis rows = 2 m-blocks
+  extern __shared__ __align__(16) double2 csm[];  // [2][STG], then per warp: P [64], X batch [16][8]
+  const int ti = order ? order[blockIdx.y] : blockIdx.y;
+  const int e = targetList[ti];
+  const int t0 = targetPtr[ti], t1 = targetPtr[ti + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  double2* sP = csm + 2 * STG + warp * 192;
+  double2* sX = sP + 64;
+  const int c0 = blockIdx.x * 32 + warp * 8;
+  const bool active = c0 < nrhs;
+  const int cb = c0 + gid;  // the column of this lane's B fragments
+  const bool cbok = cb < nrhs;
+  const long long xcol = static_cast<long long>(cbok ? cb : 0) * xR + tig;
+  double yr[MBLK][2], yi[MBLK][2];
+#pragma unroll
+  for (int mb = 0; mb < MBLK; ++mb) yr[mb][0] = yr[mb][1] = yi[mb][0] = yi[mb][1] = 0.0;
+
+  auto stage = [&](int t, int st) {
+    const int slot = termInfo[4 * t + 2], trans = termInfo[4 * t + 3];
+    const double2* W = (trans ? U : V) + static_cast<long long>(slot) * RANK * M;
+    const double2* W2 = (trans ? V : U) + static_cast<long long>(slot) * RANK * M;
+    double2* sW = csm + st * STG;
+    double2* sW2 = sW + RANK * LDW;
+    for (int q = threadIdx.x; q < RANK * M; q += 128) {
+      const int r = q / M, a = q % M;
+      corrCpAsync16(sW + r * LDW + a, W + q);
+      corrCpAsync16(sW2 + r * LDW2 + a, W2 + q);
+    }
+    for (int q = threadIdx.x; q < M; q += 128) corrCpAsync16(sW2 + RANK * LDW2 + q, D + static_cast<long long>(slot) * M + q);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // X fragments of one batch: rows 16 bt + 4 u + tig of column cb.
+  auto loadX = [&](const double2* xs, int bt, double2 (&xq)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xq[u] = cbok ? __ldg(xs + bt * 16 + u * 4) : make_double2(0.0, 0.0);
+  };
+
+  double2 xq[2][4];
+  if (t0 < t1) {
+    stage(t0, 0);
+    if (active) loadX(x + termInfo[4 * t0 + 1] * xE + xcol, 0, xq[0]);
+  }
+  for (int t = t0; t < t1; ++t) {
+    const int st = (t - t0) & 1;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // term t's stage has landed everywhere; everyone is done with term t - 1's
+    if (t + 1 < t1) stage(t + 1, st ^ 1);
+    if (!active) continue;
+    const double2* sW = csm + st * STG;
+    const double2* sW2 = sW + RANK * LDW;
+    const double2* sD = sW2 + RANK * LDW2;
+    const double2* xs = x + termInfo[4 * t + 1] * xE + xcol;
+    double pr[2] = {0.0, 0.0}, pi[2] = {0.0, 0.0};
+#pragma unroll
+    for (int bt = 0; bt < NBAT; ++bt) {
+      if (bt + 1 < NBAT) loadX(xs, bt + 1, xq[(bt + 1) & 1]);
+      double2(&xb)[4] = xq[bt & 1];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 w = sW[gid * LDW + bt * 16 + u * 4 + tig];
+        corrDmmaOp(pr, w.x, xb[u].x);
+        corrDmmaOp(pr, -w.y, xb[u].y);
+        corrDmmaOp(pi, w.x, xb[u].y);
+        corrDmmaOp(pi, w.y, xb[u].x);
+      }
+      // Diagonal term: the batch's X values go from the B layout (row 4u +
+      // tig, column gid) to the accumulator layout (row gid of m-block 2 bt +
+      // mbl, columns 2 tig + {0,1}) through warp-private shared memory
+      // (column index XOR row: conflict-free reads, 2-way writes).
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = u * 4 + tig;
+        sX[r * 8 + (gid ^ (r & 7))] = xb[u];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mbl = 0; mbl < 2; ++mbl) {
+        const int mb = 2 * bt + mbl;
+        const double2 d = sD[mb * 8 + gid];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 xv = sX[(mbl * 8 + gid) * 8 + ((2 * tig + h) ^ gid)];
+          yr[mb][h] = fma(d.x, xv.x, fma(-d.y, xv.y, yr[mb][h]));
+          yi[mb][h] = fma(d.x, xv.y, fma(d.y, xv.x, yi[mb][h]));
+        }
+      }
+      __syncwarp();
+    }
+    // accumulator layout (row q = gid, columns 2 tig + {0,1}) -> B layout (k = q = tig (+4), column gid)
+    sP[gid * 8 + 2 * tig] = make_double2(pr[0], pi[0]);
+    sP[gid * 8 + 2 * tig + 1] = make_double2(pr[1], pi[1]);
+    __syncwarp();
+    const double2 pb0 = sP[tig * 8 + gid], pb1 = sP[(4 + tig) * 8 + gid];
+    __syncwarp();
+    // the next term's first X batch arrives under this term's second product
+    if (t + 1 < t1) loadX(x + termInfo[4 * (t + 1) + 1] * xE + xcol, 0, xq[0]);
+#pragma unroll
+    for (int mb = 0; mb < MBLK; ++mb) {
+      const double2 w0 = sW2[tig * LDW2 + mb * 8 + gid], w1 = sW2[(4 + tig) * LDW2 + mb * 8 + gid];
+      corrDmmaOp(yr[mb], w0.x, pb0.x);
+      corrDmmaOp(yr[mb], -w0.y, pb0.y);
+      corrDmmaOp(yi[mb], w0.x, pb0.y);
+      corrDmmaOp(yi[mb], w0.y, pb0.x);
+      corrDmmaOp(yr[mb], w1.x, pb1.x);
+      corrDmmaOp(yr[mb], -w1.y, pb1.y);
+      corrDmmaOp(yi[mb], w1.x, pb1.y);
+      corrDmmaOp(yi[mb], w1.y, pb1.x);
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = c0 + 2 * tig + h;
+    if (c >= nrhs) continue;
+#pragma unroll
+    for (int mb = 0; mb < MBLK; ++mb)
+      ycorr[(static_cast<long long>(e) * nrhs + c) * M + mb * 8 + gid] = make_double2(yr[mb][h], yi[mb][h]);
+  }
+}
+
+template <int KPL>
+void launchCorrDmma(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
+                    long long xE, long long xR) {
+  constexpr int M = 32 * KPL;
+  constexpr size_t SMEM = (2 * (8 * (M + 4) + 8 * (M + 2) + M) + 4 * 192) * sizeof(double2);
+  static std::atomic<unsigned long long> attr{0};
+  oncePerDevice(attr, [] {
+    TBT_CUDA_CHECK(cudaFuncSetAttribute(corrDmma<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(SMEM)));
+  });
+  dim3 grid((nrhs + 31) / 32, t.nTargets);
+  corrDmma<KPL><<<grid, 128, SMEM, s>>>(t.termInfo, t.targetList, t.targetPtr, t.order, c.dCorrD, c.dCorrU, c.dCorrV, x,
+                                        ycorr, nrhs, xE, xR);
+}
+
+bool corrUseDmma() {
+  static const bool on = [] {
+    const char* e = getenv("TBT_CORR");
+    return !(e && std::string(e) == "vec");  // TBT_CORR=vec: the DFMA / shuffle kernel (corrMulti) for rank 8 too
+  }();
+  return on;
 }
 
 // Columns per warp of corrMulti (TBT_CORR_RPW = 1 | 2 | 4; default 2).
@@ -318,7 +485,9 @@ void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* 
   const long long xE = xUserN > 0 ? c.m : static_cast<long long>(nrhs) * c.m;
   const long long xR = xUserN > 0 ? xUserN : c.m;
   if (nrhs >= 8 && (c.rank == 4 || c.rank == 8) && (c.m == 64 || c.m == 128)) {
-    if (c.m == 64)
+    if (c.rank == 8 && corrUseDmma())
+      c.m == 64 ? launchCorrDmma<2>(c, t, x, ycorr, nrhs, s, xE, xR) : launchCorrDmma<4>(c, t, x, ycorr, nrhs, s, xE, xR);
+    else if (c.m == 64)
       c.rank == 4 ? launchCorrMultiRpw<2, 4>(c, t, x, ycorr, nrhs, s, xE, xR)
                   : launchCorrMultiRpw<2, 8>(c, t, x, ycorr, nrhs, s, xE, xR);
     else
@@ -336,7 +505,9 @@ void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* 
 
 void launchCorrVector(Ctx& c, const double2* x, double2* ycorr, int nrhs, cudaStream_t s, long long xUserN) {
   if (!c.haveCorr || c.nTerms == 0) return;
-  launchCorrVectorOn(c, CorrTables{c.dTermInfo, c.dTargetList, c.dTargetPtr, c.nTargets, c.maxTermsPerTarget}, x,
+  launchCorrVectorOn(c, CorrTables{c.dTermInfo, c.dTargetList, c.dTargetPtr, c.nTargets, c.maxTermsPerTarget,
+                                   c.dTargetList + c.nTargets},
+                     x,
                      ycorr, nrhs, s, xUserN);
 }
 

@@ -315,6 +315,7 @@ struct CorrTables {
   const int* targetList;
   const int* targetPtr;
   int nTargets, maxTerms;
+  const int* order = nullptr;  // [nTargets] launch order of the targets (longest term lists first), or identity
 };
 void launchCorrVectorOn(Ctx& c, const CorrTables& t, const double2* x, double2* ycorr, int nrhs, cudaStream_t s,
                         long long xUserN = 0);

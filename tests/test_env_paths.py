@@ -23,6 +23,9 @@ process per setting; the knobs are read once per process):
                       issued ahead of the chunk (2- / 3-stage ring) or
                       between its DMMA groups with a 3-stage ring (default:
                       two 4-warp CTAs, 2-stage ring, loads between the groups)
+  TBT_CORR=vec        rank-8 many-column correction on DFMA + warp shuffles
+                      (corrMulti) instead of the FP64 tensor path (corrDmma)
+  TBT_CORR_RPW=1|4    columns per warp of corrMulti
   TBT_DIST_CHUNKS=k   sharded apply with k overlapped exchange chunks
                       (default 2 at P > 1, 1 at P = 1)
 """
@@ -55,6 +58,9 @@ CASES = [
     ({"TBT_GEMM": "pair2"}, ["wide"]),
     ({"TBT_GEMM": "pair3"}, ["wide"]),
     ({"TBT_GEMM": "late3"}, ["wide"]),
+    ({"TBT_CORR": "vec"}, ["wide"]),
+    ({"TBT_CORR": "vec", "TBT_CORR_RPW": "4"}, ["wide"]),
+    ({"TBT_CORR": "vec", "TBT_CORR_RPW": "1"}, ["wide"]),
     ({}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "2"}, ["dist"]),
     ({"TBT_DIST_CHUNKS": "4"}, ["dist"]),
