@@ -321,10 +321,40 @@ void loadSpectra(Ctx& c, const std::string& path) {
   std::vector<int> pairFGlobal;
   planPairs(c, pairFGlobal);
   TBT_USER_CHECK(c.npairs == h.npairs, "spectra cache: pair count mismatch");
-  std::vector<double2> host(static_cast<size_t>(c.npairs * mm));
-  in.read(reinterpret_cast<char*>(host.data()), static_cast<std::streamsize>(host.size() * sizeof(double2)));
-  TBT_USER_CHECK(static_cast<bool>(in), "spectra cache: truncated file");
-  uploadSync(c.dSpectra, host.data(), host.size() * sizeof(double2), c.stream);
+  // The spectrum goes file -> pinned chunk -> device, the copy of one chunk
+  // under the read of the next (one pageable multi-GB vector, zero-filled,
+  // read and then staged by the driver, took 3.7 s at C4 against 0.22 s for
+  // generators + K1).
+  struct Pinned {
+    char* p[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Pinned() {
+      for (int b = 0; b < 2; ++b) {
+        if (ev[b]) cudaEventDestroy(ev[b]);
+        if (p[b]) cudaFreeHost(p[b]);
+      }
+    }
+  } pin;
+  const size_t total = static_cast<size_t>(c.npairs * mm) * sizeof(double2);
+  const size_t chunk = std::min<size_t>(total, 64u << 20);
+  for (int b = 0; b < 2 && chunk > 0; ++b) {
+    TBT_CUDA_CHECK(cudaMallocHost(&pin.p[b], chunk));
+    TBT_CUDA_CHECK(cudaEventCreateWithFlags(&pin.ev[b], cudaEventDisableTiming));
+  }
+  int b = 0;
+  for (size_t off = 0; off < total; off += chunk, b ^= 1) {
+    const size_t n = std::min(chunk, total - off);
+    TBT_CUDA_CHECK(cudaEventSynchronize(pin.ev[b]));  // the copy that last used this buffer
+    in.read(pin.p[b], static_cast<std::streamsize>(n));
+    if (!in) {
+      cudaStreamSynchronize(c.stream);
+      TBT_USER_CHECK(false, "spectra cache: truncated file");
+    }
+    TBT_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(c.dSpectra) + off, pin.p[b], n, cudaMemcpyHostToDevice,
+                                   c.stream));
+    TBT_CUDA_CHECK(cudaEventRecord(pin.ev[b], c.stream));
+  }
+  TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 }  // namespace tbt
