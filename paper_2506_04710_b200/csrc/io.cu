@@ -270,16 +270,30 @@ struct SpecHeader {
   uint8_t hasKey;
   uint8_t key[32];  // tbt_set_cache_key of the context that wrote the file
 };
+
+// Two pinned staging buffers with an event each.
+struct PinnedPair {
+  char* p[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  void alloc(size_t bytes) {
+    for (int b = 0; b < 2; ++b) {
+      TBT_CUDA_CHECK(cudaMallocHost(&p[b], bytes));
+      TBT_CUDA_CHECK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+  }
+  ~PinnedPair() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev[b]) cudaEventDestroy(ev[b]);
+      if (p[b]) cudaFreeHost(p[b]);
+    }
+  }
+};
 }  // namespace
 
 void saveSpectra(Ctx& c, const std::string& path) {
   TBT_USER_CHECK(c.havePrecompute && !c.dist, "tbt_save_spectra: needs a precomputed single-GPU context");
   TBT_USER_CHECK(!c.fullMode, "tbt_save_spectra: FULL (non-reciprocal) generators are not cached");
   const long long mm = static_cast<long long>(c.m) * c.m;
-  std::vector<double2> host(static_cast<size_t>(c.npairs * mm));
-  TBT_CUDA_CHECK(cudaMemcpyAsync(host.data(), c.dSpectra, host.size() * sizeof(double2), cudaMemcpyDeviceToHost,
-                                 c.stream));
-  TBT_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   std::ofstream out(path, std::ios::binary);
   TBT_USER_CHECK(static_cast<bool>(out), "cannot write spectra cache: " + path);
   SpecHeader h{};
@@ -295,7 +309,23 @@ void saveSpectra(Ctx& c, const std::string& path) {
   std::memcpy(h.key, c.cacheKey, sizeof h.key);
   out.write(reinterpret_cast<const char*>(&h), sizeof h);
   out.write(reinterpret_cast<const char*>(c.genHost.data()), static_cast<std::streamsize>(mm * sizeof(double2)));
-  out.write(reinterpret_cast<const char*>(host.data()), static_cast<std::streamsize>(host.size() * sizeof(double2)));
+  // device -> pinned chunk -> file, the copy of the next chunk under the write of this one
+  PinnedPair pin;
+  const size_t total = static_cast<size_t>(c.npairs * mm) * sizeof(double2);
+  const size_t chunk = std::min<size_t>(total, 64u << 20);
+  if (chunk > 0) pin.alloc(chunk);
+  auto fetch = [&](size_t off, int b) {
+    TBT_CUDA_CHECK(cudaMemcpyAsync(pin.p[b], reinterpret_cast<const char*>(c.dSpectra) + off, std::min(chunk, total - off),
+                                   cudaMemcpyDeviceToHost, c.stream));
+    TBT_CUDA_CHECK(cudaEventRecord(pin.ev[b], c.stream));
+  };
+  if (total > 0) fetch(0, 0);
+  int b = 0;
+  for (size_t off = 0; off < total; off += chunk, b ^= 1) {
+    if (off + chunk < total) fetch(off + chunk, b ^ 1);
+    TBT_CUDA_CHECK(cudaEventSynchronize(pin.ev[b]));
+    out.write(pin.p[b], static_cast<std::streamsize>(std::min(chunk, total - off)));
+  }
   TBT_USER_CHECK(static_cast<bool>(out), "failed writing spectra cache: " + path);
 }
 
@@ -325,22 +355,10 @@ void loadSpectra(Ctx& c, const std::string& path) {
   // under the read of the next (one pageable multi-GB vector, zero-filled,
   // read and then staged by the driver, took 3.7 s at C4 against 0.22 s for
   // generators + K1).
-  struct Pinned {
-    char* p[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    ~Pinned() {
-      for (int b = 0; b < 2; ++b) {
-        if (ev[b]) cudaEventDestroy(ev[b]);
-        if (p[b]) cudaFreeHost(p[b]);
-      }
-    }
-  } pin;
+  PinnedPair pin;
   const size_t total = static_cast<size_t>(c.npairs * mm) * sizeof(double2);
   const size_t chunk = std::min<size_t>(total, 64u << 20);
-  for (int b = 0; b < 2 && chunk > 0; ++b) {
-    TBT_CUDA_CHECK(cudaMallocHost(&pin.p[b], chunk));
-    TBT_CUDA_CHECK(cudaEventCreateWithFlags(&pin.ev[b], cudaEventDisableTiming));
-  }
+  if (chunk > 0) pin.alloc(chunk);
   int b = 0;
   for (size_t off = 0; off < total; off += chunk, b ^= 1) {
     const size_t n = std::min(chunk, total - off);
