@@ -12,10 +12,12 @@
 // The reference re-streams every block once per column
 // (linsolve.cpp:276-282, 572).
 //
-// CTA tile: all M rows x NTILE right-hand sides of one (pair, transpose)
-// item; 8 warps, warp w owns rows [w*M/8, (w+1)*M/8). K advances in chunks
-// of 32 through a cp.async double buffer: the A chunk (M x 32 for A, or the
-// 32 contiguous rows of A for A^T) and the X chunk (32 x NTILE).
+// Two CTA shapes. binprodGemm (m = 64, and m = 128 under TBT_GEMM=wide|4m):
+// all M rows x NTILE right-hand sides of one (pair, transpose) item; 8 warps,
+// warp w owns rows [w*M/8, (w+1)*M/8). K advances in chunks of 32 through a
+// cp.async double buffer: the A chunk (M x 32 for A, or the 32 contiguous
+// rows of A for A^T) and the X chunk (32 x NTILE). binprodGemm2 (the m = 128
+// default, below): 64-row tiles on 4-warp CTAs, two per SM.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
