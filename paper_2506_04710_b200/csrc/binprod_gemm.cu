@@ -405,6 +405,11 @@ int gemm4m() {
 
 bool launchBinProductGemm(Ctx& c, int nrhs) {
   const int four = gemm4m();
+  if (c.m == 64 && !four && gemmShape()) {
+    launchGemm2<64, 2, true>(c, nrhs);
+    TBT_CUDA_CHECK(cudaGetLastError());
+    return true;
+  }
   if (c.m == 128 && !four && gemmShape()) {
     switch (gemmShape()) {
       case 2: launchGemm2<128, 2, false>(c, nrhs); break;
