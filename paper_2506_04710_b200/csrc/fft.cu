@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(128, (N >= 48 ? 1 : N >= 24 ? 3 : 4)) regLineK
   }
   // ycorr is internal [e][B]: e * B + bg = line * out_line_stride + pt * out_point_stride + bg
   constexpr int NC = (N + 1) / 2;
-  const double2* yc = p.ycorr + line * p.out_line_stride + bg;
+  const double2* yc = p.ycorr ? p.ycorr + line * p.out_line_stride + bg : nullptr;  // read only where targets != 0
   if constexpr (CROP) {
     // Every correction load of the thread goes out before the first store
     // (read-only loads, so the stores do not order them; one at a time they
